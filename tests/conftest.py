@@ -1,0 +1,48 @@
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA (B200) device and the built libnvc.so")
+
+
+def golden(name):
+    return np.load(os.path.join(GOLDEN, name + ".npz"), allow_pickle=False)
+
+
+@pytest.fixture(scope="session")
+def g_rng():
+    return golden("rng")
+
+
+@pytest.fixture(scope="session")
+def g_scenes():
+    return golden("scenes")
+
+
+@pytest.fixture(scope="session")
+def g_hash():
+    return golden("hashgrid")
+
+
+@pytest.fixture(scope="session")
+def g_mlp():
+    return golden("mlp")
+
+
+@pytest.fixture(scope="session")
+def g_samp():
+    return golden("sampling")
+
+
+@pytest.fixture(scope="session")
+def g_train():
+    return golden("training")
