@@ -1,0 +1,207 @@
+/* nvc.h -- C ABI of the B200-native neural visibility cache (libnvc.so).
+ *
+ * The reference (`viscache` 0.1.0, /root/reference/pkg/src/viscache) is a pure
+ * Python package; its "plugin" interface for this path is the duck-typed
+ * cache object (`mode`, `output_dim`, `infer`, `train_step`) plus the sampling
+ * functions that consume it.  Each entry point below replaces one reference
+ * routine; the citation names the routine it stands in for.  A Python
+ * (ctypes) host layer, `paper_2506_05930_b200`, mirrors the reference API on
+ * top of these calls.
+ *
+ * Conventions
+ *  - Every pointer argument is a DEVICE pointer unless named `host_*`.
+ *  - Every call is asynchronous on the given CUDA stream (NULL = legacy).
+ *  - Return 0 on success, a negative nvc_status on error; nvc_last_error()
+ *    returns a thread-local message describing the last failure.
+ *  - The caller owns all memory (model state included); nvc_model only
+ *    carries pointers and shapes.  No torch types cross this boundary.
+ *  - Doubles are IEEE binary64, integers little-endian, arrays row-major.
+ */
+#ifndef NVC_H_
+#define NVC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NVC_MAX_LEVELS 32
+#define NVC_MAX_LAYERS 8
+#define NVC_ABI_VERSION 1
+
+typedef enum {
+    NVC_OK = 0,
+    NVC_ERR_ARG = -1,          /* invalid argument (bad shape, null pointer, unsupported config) */
+    NVC_ERR_CUDA = -2,         /* a CUDA runtime call or kernel launch failed */
+    NVC_ERR_UNSUPPORTED = -3   /* valid config the requested kernel does not handle */
+} nvc_status;
+
+/* Fixed-point scale of the hash-grid / MLP gradient accumulators (int64):
+ * value = fx * 2^-48.  Integer accumulation makes the scatter deterministic
+ * and makes the data-parallel allreduce order-independent. */
+#define NVC_GRAD_FX_BITS 48
+
+/* Hash grid + MLP: the reference VisibilityCache state (cache.py:25-45,
+ * hashgrid.py:32-65, mlp.py:24-60).  Parameter order in `params` is the
+ * reference `_param_dict` / snapshot order: grid (L,T,F), w0 (out,in), b0, w1, ... */
+typedef struct {
+    int32_t levels;                       /* L */
+    int32_t features;                     /* F */
+    int64_t table_size;                   /* T (power of two) */
+    int32_t resolution[NVC_MAX_LEVELS];   /* floor(base * scale^l), computed by the host */
+    int32_t dense[NVC_MAX_LEVELS];        /* (res+1)^3 <= T */
+    double aabb_min[3];
+    double span[3];                       /* max(aabb_max - aabb_min, 1e-12) */
+    int32_t n_layers;                     /* number of weight matrices */
+    int32_t dims[NVC_MAX_LAYERS + 1];     /* input (= L*F), hidden..., output (= K) */
+    float alpha;                          /* leaky-ReLU slope (0.01) */
+    int32_t out_sigmoid;                  /* 1: sigmoid + clip output, 0: leaky output */
+    /* device state, caller-allocated */
+    float *params;                        /* f32 master parameters, param_count */
+    float *adam_m, *adam_v;               /* f32 Adam moments, param_count */
+    int64_t *grad_fx;                     /* fixed-point gradient accumulator, param_count */
+    uint16_t *touched;                    /* per-table-entry epoch map, L*T */
+    uint16_t *table_h;                    /* fp16 shadow of the table (bit patterns), L*T*F */
+    uint16_t *wpack;                      /* fp16 weights in the tcgen05 K-major core-matrix layout */
+    int64_t param_count;
+    int64_t wpack_count;                  /* halfs in wpack (nvc_wpack_count) */
+} nvc_model;
+
+/* Scene tables (scene.py:158-215, geometry.py:97-158).  BVH arrays are in the
+ * reference's build order; tri_* arrays are in original triangle order. */
+typedef struct {
+    const double *node_min, *node_max;    /* (n_nodes, 3) */
+    const int32_t *node_left, *node_right, *node_start, *node_count;
+    const double *bv0, *bv1, *bv2;        /* (n_tris, 3), BVH leaf order */
+    const int64_t *perm;                  /* BVH index -> original triangle index */
+    const double *tv0, *tv1, *tv2;        /* (n_tris, 3), original order */
+    const int32_t *tri_material, *tri_light;
+    const double *mat_albedo;             /* (n_materials, 3) */
+    const uint8_t *lt_kind;               /* 0 rect, 1 point */
+    const double *lt_verts;               /* (K, 4, 3) */
+    const double *lt_normal;              /* (K, 3) */
+    const double *lt_radiance;            /* (K, 3) */
+    const double *lt_lumaw;               /* (K, 3) LUMA * radiance, precomputed by the host */
+    int64_t n_nodes, n_tris;
+    int32_t n_lights, n_materials;
+    double shadow_eps;                    /* geometry.py:221-223 */
+    double aabb_min[3], aabb_max[3];
+} nvc_scene;
+
+/* Pinhole camera with the basis precomputed by the host (scene.py:109-139). */
+typedef struct {
+    double pos[3], fwd[3], right[3], up[3];
+    double tan_half, aspect;
+    int32_t width, height;
+} nvc_camera;
+
+/* ---- library ---------------------------------------------------------- */
+const char *nvc_last_error(void);
+int32_t nvc_abi_version(void);
+/* halfs of packed fp16 weights the tcgen05 path needs for this topology */
+int64_t nvc_wpack_count(const nvc_model *m);
+/* bytes of scratch nvc_train_grads needs for b rows */
+int64_t nvc_train_workspace_bytes(const nvc_model *m, int64_t b);
+
+/* ---- state ------------------------------------------------------------ */
+/* Rebuild table_h and wpack from params (after loading / setting params). */
+int nvc_refresh_shadow(const nvc_model *m, void *stream);
+
+/* ---- encoder: hashgrid.py:94-131 (encode_batch, _level_lookup, spatial_hash) */
+/* feats (n, L*F) f32 from the f32 master table (exact reference op order);
+ * idx_out (n, L, 8) int32 and w_out (n, L, 8) f64 are optional (may be NULL). */
+int nvc_encode(const nvc_model *m, const double *pos, int64_t n, float *feats,
+               int32_t *idx_out, double *w_out, void *stream);
+
+/* ---- inference: cache.py:54-58 (VisibilityCache.infer) ---------------- */
+/* precision 0: f32 SIMT (parity: f32 table + f32 weights);
+ * precision 1: fused fp16 table + tcgen05/TMEM MLP (fp32 accumulate). */
+int nvc_infer(const nvc_model *m, const double *pos, int64_t n, int32_t precision,
+              float *out, void *stream);
+
+/* ---- training: cache.py:60-73 (train_step) split at the allreduce point --- */
+/* Accumulates the gradient of the loss into grad_fx and marks touched table
+ * entries with `epoch`.  The batch has b global rows (b = *b_dev when b_dev
+ * is non-NULL, else b_max); this call handles the shard rows
+ * [b*shard/n_shards, b*(shard+1)/n_shards): pos is indexed by global row,
+ * targets/mask (may be NULL) by shard-local row.  d_out is scaled by the
+ * global b*K (mlp.py:162) so data-parallel shards sum to the full-batch
+ * gradient.  loss_sum_out (device double) receives sum_rows(sum_k d^2)/K
+ * over the shard's rows (mean over b is the caller's division). */
+int nvc_train_grads(const nvc_model *m, const double *pos, const float *targets,
+                    const float *mask, int64_t b_max, const int64_t *b_dev,
+                    int32_t shard, int32_t n_shards, uint16_t epoch,
+                    void *workspace, double *loss_sum_out, void *stream);
+/* One bias-corrected Adam step over every parameter (mlp.py:203-218, dense
+ * like the reference), consuming and zeroing grad_fx; refreshes table_h and
+ * wpack.  t is the post-increment Adam step (>= 1), lr from lr_at (mlp.py:76).
+ * dense_grad=1 reads every grid gradient (needed after a data-parallel
+ * allreduce of grad_fx); 0 uses the touched map. */
+int nvc_adam_step(const nvc_model *m, int64_t t, double lr, uint16_t epoch,
+                  int32_t dense_grad, void *stream);
+
+/* ---- light selection: sampling.py:74-85, 184-218 ---------------------- */
+/* wrs_select_batch: weights (p, k) f64; draw for (row r, light j) is
+ * offset + r*k + j of Philox stream `key` (rng.py:54-56). */
+int nvc_wrs_select(const double *w, int64_t p, int32_t k, uint64_t key, uint64_t offset,
+                   int64_t *idx, double *w_sel, double *w_sum, void *stream);
+/* nls_sample_batch given visibility (p, k) f32 and luminance weights in
+ * light-major layout lum[j*p_stride + r] (f32 if lum_f64 == 0 else f64).
+ * Rows are pixels p_first.. of a p_total-pixel frame (screen-tile shards
+ * reproduce the whole-frame draws).  floor <= 0 selects the biased mode. */
+int nvc_nls_from_vis(const nvc_scene *sc, const float *vis, const void *lum, int32_t lum_f64,
+                     int64_t p_stride, int64_t p, int32_t k, int64_t p_first, int64_t p_total,
+                     uint64_t key, uint64_t offset, double floor,
+                     int64_t *ids, double *pts, double *big_w, void *stream);
+/* Fused encode -> tcgen05 MLP -> clamp * lum -> WRS -> light point, one
+ * pass per 128-pixel tile (the hot path). pos (p, 3) f64. */
+int nvc_nls_sample(const nvc_model *m, const nvc_scene *sc, const double *pos,
+                   const void *lum, int32_t lum_f64, int64_t p_stride, int64_t p,
+                   int64_t p_first, int64_t p_total, uint64_t key, uint64_t offset,
+                   double floor, int64_t *ids, double *pts, double *big_w, void *stream);
+/* Fused Neural DI (sampling.py:215-218): rgb (p,3) f64 = sum_k v_k f_k L_k * albedo/pi,
+ * factor in light-major layout (f32 or f64). */
+int nvc_neural_di(const nvc_model *m, const nvc_scene *sc, const double *pos,
+                  const double *albedo, const void *factor, int32_t factor_f64,
+                  int64_t p_stride, int64_t p, double *rgb, void *stream);
+
+/* ---- geometry + training data: geometry.py, render.py, training.py ----- */
+/* make_gbuffer (render.py:103-117) for pixels [p_first, p_first+p). */
+int nvc_gbuffer(const nvc_scene *sc, const nvc_camera *cam, uint64_t jitter_key,
+                int64_t p_first, int64_t p, double *pos, double *nrm, double *alb,
+                uint8_t *hit, int32_t *light_id, void *stream);
+/* light_factors_all (kernels.py:299-316) -> light-major f32/f64 factor and,
+ * optionally, lum = factor * (albedo . LUMA*L)/pi (sampling.py:134-139). */
+int nvc_light_factors(const nvc_scene *sc, const double *pos, const double *nrm,
+                      const double *alb, int64_t p, int64_t p_stride, int32_t out_f64,
+                      void *factor_out, void *lum_out, void *stream);
+/* visibility_batch (geometry.py:233-247): vis (n) f32 in {0,1}. */
+int nvc_visibility(const nvc_scene *sc, const double *x, const double *y, int64_t n,
+                   float *vis, void *stream);
+/* intersect_scene_batch (geometry.py:191-207): t, original tri index (-1 miss). */
+int nvc_closest_hit(const nvc_scene *sc, const double *orig, const double *dir,
+                    const double *t_min, const double *t_max, int64_t n,
+                    double *t_out, int64_t *tri_out, void *stream);
+/* One training batch (training.py:44-129, 176-195): world samples, screen
+ * samples (<= 9 rounds, order-preserving compaction) and targets.  Every
+ * shard generates all b = n_world + screen-hits global positions (cheap,
+ * keeps the in-order compaction global) and the targets of its rows
+ * [b*shard/n_shards, b*(shard+1)/n_shards) only (tgt may be NULL: no targets).  pos capacity:
+ * n_world+n_screen rows; tgt capacity: same rows x K (shard-local rows);
+ * n_rows (device int64) receives b. */
+int64_t nvc_batch_workspace_bytes(int32_t n_screen);
+/* compute_visibility_targets (training.py:103-120, light mode) for given
+ * positions (b,3): tgt (b,K) f32, light j / row i use draws j*2b+2i, +1. */
+int nvc_targets(const nvc_scene *sc, uint64_t key, const double *pos, int64_t b, float *tgt,
+                void *stream);
+int nvc_gen_train_batch(const nvc_scene *sc, const nvc_camera *cam, uint64_t key_world,
+                        uint64_t key_screen, uint64_t key_targets, int32_t n_world,
+                        int32_t n_screen, int32_t shard, int32_t n_shards,
+                        double *pos, float *tgt, int64_t *n_rows, void *workspace,
+                        void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NVC_H_ */

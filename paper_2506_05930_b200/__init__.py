@@ -1,0 +1,36 @@
+"""paper_2506_05930_b200 -- B200-native neural visibility cache (arXiv 2506.05930).
+
+A drop-in for the hot path of the reference ``viscache`` package: the cache
+object (``VisibilityCache``/``make_cache`` with ``infer``/``train_step``),
+the training-frame driver and WRS light sampling / Neural DI.  All compute
+runs in ``libnvc.so`` (hand-written sm_100a CUDA: FP64 geometry, hash-grid
+encoder, tcgen05/TMEM fused MLP, WRS with numpy-compatible Philox); this
+package is the host layer that keeps the reference's API.
+"""
+
+from . import rng
+from .cache import (MODE_CLUSTERS, MODE_LIGHTS, MODE_RADIANCE, PRECISION_FP16, PRECISION_FP32,
+                    VisibilityCache, make_cache)
+from .hashgrid import HashGridConfig, clustered_config
+from .mlp import MLPConfig, MLPParams, TrainStepConfig, lr_at
+from .render import GBuffer, gbuffer_and_ctx, make_gbuffer
+from .sampling import (CLAMP_FLOOR, PixelCtx, Reservoir, ShadingPoint, clamp_visibility,
+                       neural_di_batch, neural_di_shade, nls_sample, nls_sample_batch,
+                       nls_weights_batch, wrs_select, wrs_select_batch)
+from .scene import Camera, Light, Material, Scene, SceneError, load_scene, scene_from_dict
+from .scenes import boxes_point_scene, boxes_scene, rooms_scene
+from .training import (TrainFrameConfig, compute_visibility_targets, gen_screen_samples,
+                       gen_world_samples, train_frame)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "rng", "VisibilityCache", "make_cache", "MODE_LIGHTS", "MODE_CLUSTERS", "MODE_RADIANCE",
+    "PRECISION_FP16", "PRECISION_FP32", "HashGridConfig", "clustered_config", "MLPConfig",
+    "MLPParams", "TrainStepConfig", "lr_at", "GBuffer", "gbuffer_and_ctx", "make_gbuffer",
+    "CLAMP_FLOOR", "PixelCtx", "Reservoir", "ShadingPoint", "clamp_visibility", "neural_di_batch",
+    "neural_di_shade", "nls_sample", "nls_sample_batch", "nls_weights_batch", "wrs_select",
+    "wrs_select_batch", "Camera", "Light", "Material", "Scene", "SceneError", "load_scene",
+    "scene_from_dict", "boxes_scene", "boxes_point_scene", "rooms_scene", "TrainFrameConfig",
+    "compute_visibility_targets", "gen_screen_samples", "gen_world_samples", "train_frame",
+]

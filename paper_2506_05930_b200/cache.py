@@ -1,0 +1,337 @@
+"""The neural visibility cache: drop-in for ``viscache.cache`` (cache.py:25-139).
+
+State lives in HBM as one flat f32 parameter vector in the reference's
+``_param_dict`` order (grid, w0, b0, w1, b1, ...) plus Adam moments, an int64
+fixed-point gradient accumulator, a per-entry "touched" epoch map, the fp16
+shadow table the query kernel gathers from, and the fp16 weights packed in
+the tcgen05 core-matrix layout.  ``infer`` and ``train_step`` keep the
+reference's numpy-in / numpy-out signatures; ``*_device`` variants take and
+return CUDA tensors without host round trips.
+
+Extension over the reference: ``hidden_dims`` (the reference hardcodes
+(32, 32), cache.py:37-38).  Initialisation follows cache.py:41-43 for any
+width: one (seed, "init-params") stream, table first, then He weights.
+"""
+
+from __future__ import annotations
+
+import json
+import struct
+from dataclasses import asdict
+
+import numpy as np
+
+from . import _lib
+from . import rng as rngmod
+from .hashgrid import HashGridConfig, clustered_config, init_table
+from .mlp import LEAKY, SIGMOID, MLPConfig, MLPParams, TrainStepConfig, he_init, lr_at
+
+MODE_LIGHTS = "lights"
+MODE_CLUSTERS = "clusters"
+MODE_RADIANCE = "radiance"
+SNAP_MAGIC = b"VCSNAP1\n"
+
+PRECISION_FP32 = 0     # f32 table + f32 SIMT MLP (parity path)
+PRECISION_FP16 = 1     # fp16 shadow table + tcgen05/TMEM MLP (perf path)
+
+
+class VisibilityCache:
+    """Online-trained cache: position -> one sigmoid output per light/cluster."""
+
+    def __init__(self, mode: str, output_dim: int, grid: HashGridConfig,
+                 train: TrainStepConfig | None = None, seed: int = 0, dtype=np.float32,
+                 hidden_dims=(32, 32), device=None, precision: int = PRECISION_FP16):
+        if mode not in (MODE_LIGHTS, MODE_CLUSTERS, MODE_RADIANCE):
+            raise ValueError(f"unknown cache mode {mode!r}")
+        if np.dtype(dtype) != np.float32:
+            raise ValueError("the CUDA cache keeps float32 master parameters (dtype=np.float32)")
+        torch = _lib.require_cuda()
+        self.mode = mode
+        self.output_dim = int(output_dim)
+        self.grid_cfg = grid
+        self.net_cfg = MLPConfig(input_dim=grid.output_dim, output_dim=self.output_dim,
+                                 hidden_dims=tuple(hidden_dims),
+                                 output_activation=LEAKY if mode == MODE_RADIANCE else SIGMOID)
+        self.train_cfg = train or TrainStepConfig()
+        self.dtype = np.dtype(np.float32)
+        self.precision = precision
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.step = 0          # train_step count (drives lr_at)
+        self.adam_t = 0        # Adam bias-correction step
+        self._epoch = 0
+        gen = rngmod.stream(seed, rngmod.INIT_PARAMS)
+        table = init_table(grid, gen)
+        net = he_init(self.net_cfg, gen)
+        self._alloc()
+        self._upload(table, net)
+
+    # ---- state ----------------------------------------------------------
+    def _offsets(self):
+        offs, o = [], self.grid_cfg.param_count
+        for fo, fi in self.net_cfg.layer_dims:
+            offs.append((o, o + fo * fi))
+            o += fo * fi + fo
+        return offs, o
+
+    def _alloc(self) -> None:
+        import torch
+        offs, total = self._offsets()
+        self._layer_offs = offs
+        self.param_count_ = total
+        dev = self.device
+        g = self.grid_cfg
+        self.params = torch.zeros(total, dtype=torch.float32, device=dev)
+        self.adam_m = torch.zeros_like(self.params)
+        self.adam_v = torch.zeros_like(self.params)
+        self.grad_fx = torch.zeros(total, dtype=torch.int64, device=dev)
+        self.touched = torch.zeros(g.levels * g.table_size, dtype=torch.int16, device=dev)
+        self.table_h = torch.zeros(g.param_count, dtype=torch.float16, device=dev)
+        m = _lib.NvcModel()
+        m.levels, m.features, m.table_size = g.levels, g.features_per_level, g.table_size
+        for level in range(g.levels):
+            m.resolution[level] = g.resolution(level)
+            m.dense[level] = int(g.dense(level))
+        span = g.span()
+        for a in range(3):
+            m.aabb_min[a] = float(g.aabb_min[a])
+            m.span[a] = float(span[a])
+        dims = self.net_cfg.dims
+        if len(dims) - 1 > _lib.MAX_LAYERS:
+            raise ValueError(f"at most {_lib.MAX_LAYERS} layers are supported")
+        m.n_layers = len(dims) - 1
+        for i, d in enumerate(dims):
+            m.dims[i] = d
+        m.alpha = self.net_cfg.alpha
+        m.out_sigmoid = int(self.net_cfg.output_activation == SIGMOID)
+        m.param_count = total
+        wc = _lib.load().nvc_wpack_count(m)
+        self.wpack = torch.zeros(wc, dtype=torch.int16, device=dev)
+        m.wpack_count = wc
+        m.params, m.adam_m, m.adam_v = (t.data_ptr() for t in (self.params, self.adam_m, self.adam_v))
+        m.grad_fx, m.touched = self.grad_fx.data_ptr(), self.touched.data_ptr()
+        m.table_h, m.wpack = self.table_h.data_ptr(), self.wpack.data_ptr()
+        self.model = m
+        self._ws = None
+
+    def _upload(self, table: np.ndarray, net: MLPParams) -> None:
+        import torch
+        flat = np.concatenate([np.asarray(table, np.float32).reshape(-1)]
+                              + [x for w, b in zip(net.weights, net.biases)
+                                 for x in (np.asarray(w, np.float32).reshape(-1), np.asarray(b, np.float32))])
+        self.params.copy_(torch.from_numpy(flat))
+        self.refresh_shadow()
+
+    def refresh_shadow(self, stream=None) -> None:
+        _lib.call("nvc_refresh_shadow", self.model, _lib.stream_ptr(stream))
+
+    @property
+    def param_count(self) -> int:
+        return self.param_count_
+
+    def _host_params(self) -> np.ndarray:
+        return self.params.detach().cpu().numpy()
+
+    @property
+    def grid_params(self) -> np.ndarray:
+        g = self.grid_cfg
+        return self._host_params()[:g.param_count].reshape(g.levels, g.table_size, g.features_per_level)
+
+    @grid_params.setter
+    def grid_params(self, value) -> None:
+        self._upload(value, self.net_params)
+
+    @property
+    def net_params(self) -> MLPParams:
+        flat = self._host_params()
+        ws, bs = [], []
+        for (wo, bo), (fo, fi) in zip(self._layer_offs, self.net_cfg.layer_dims):
+            ws.append(flat[wo:wo + fo * fi].reshape(fo, fi).copy())
+            bs.append(flat[bo:bo + fo].copy())
+        return MLPParams(ws, bs)
+
+    @net_params.setter
+    def net_params(self, value: MLPParams) -> None:
+        self._upload(self.grid_params, value)
+
+    def _param_dict(self) -> dict:
+        return {"grid": self.grid_params, **self.net_params.as_dict()}
+
+    def adam_state(self) -> dict:
+        """Adam moments and step (the reference snapshot omits these)."""
+        return {"m": self.adam_m.cpu().numpy(), "v": self.adam_v.cpu().numpy(), "t": self.adam_t}
+
+    # ---- encoder / inference --------------------------------------------
+    def _pos_device(self, positions):
+        import torch
+        if isinstance(positions, torch.Tensor):
+            if positions.device != self.device or positions.dtype != torch.float64:
+                positions = positions.to(self.device, torch.float64)
+            return positions.contiguous(), True
+        pos = np.atleast_2d(np.asarray(positions, dtype=np.float64))
+        if pos.shape[1] != 3:
+            raise ValueError(f"positions must be (B, 3), got {pos.shape}")
+        if not np.all(np.isfinite(pos)):
+            raise ValueError("non-finite input features")
+        return torch.from_numpy(np.ascontiguousarray(pos)).to(self.device), False
+
+    def encode(self, positions, with_ctx: bool = False):
+        import torch
+        pos, is_dev = self._pos_device(positions)
+        n = pos.shape[0]
+        g = self.grid_cfg
+        feats = torch.empty((n, g.output_dim), dtype=torch.float32, device=self.device)
+        idx = torch.empty((n, g.levels, 8), dtype=torch.int32, device=self.device) if with_ctx else None
+        w = torch.empty((n, g.levels, 8), dtype=torch.float64, device=self.device) if with_ctx else None
+        _lib.call("nvc_encode", self.model, pos.data_ptr(), n, feats.data_ptr(), _lib.ptr(idx), _lib.ptr(w),
+                  _lib.stream_ptr())
+        if is_dev:
+            return (feats, idx, w) if with_ctx else feats
+        out = feats.cpu().numpy()
+        return (out, idx.cpu().numpy(), w.cpu().numpy()) if with_ctx else out
+
+    def infer_device(self, pos, precision: int | None = None, out=None):
+        import torch
+        n = pos.shape[0]
+        if out is None:
+            out = torch.empty((n, self.output_dim), dtype=torch.float32, device=self.device)
+        prec = self.precision if precision is None else precision
+        try:
+            _lib.call("nvc_infer", self.model, pos.data_ptr(), n, prec, out.data_ptr(), _lib.stream_ptr())
+        except _lib.NvcError:
+            if prec != PRECISION_FP16:
+                raise
+            # topology the tcgen05 kernel does not cover: use the fp32 CUDA path
+            _lib.call("nvc_infer", self.model, pos.data_ptr(), n, PRECISION_FP32, out.data_ptr(),
+                      _lib.stream_ptr())
+        return out
+
+    def infer(self, positions, precision: int | None = None):
+        """Predictions for (B,3) positions, shape (B, output_dim) float32."""
+        pos, is_dev = self._pos_device(positions)
+        out = self.infer_device(pos, precision)
+        return out if is_dev else out.cpu().numpy()
+
+    # ---- training -------------------------------------------------------
+    def _workspace(self, b: int):
+        import torch
+        need = _lib.load().nvc_train_workspace_bytes(self.model, b)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def next_epoch(self) -> int:
+        self._epoch = self._epoch % 65535 + 1
+        return self._epoch
+
+    def accumulate_grads(self, pos, targets, mask=None, b_max=None, b_dev=None, shard=0, n_shards=1,
+                         loss_out=None, epoch=None):
+        """Device gradient accumulation (the allreduce point for data parallelism)."""
+        import torch
+        b_max = int(pos.shape[0] if b_max is None else b_max)
+        if loss_out is None:
+            loss_out = torch.zeros(1, dtype=torch.float64, device=self.device)
+        ws = self._workspace(b_max)
+        ep = self._epoch if epoch is None else epoch
+        _lib.call("nvc_train_grads", self.model, pos.data_ptr(), targets.data_ptr(), _lib.ptr(mask), b_max,
+                  _lib.ptr(b_dev), shard, n_shards, ep, ws.data_ptr(), loss_out.data_ptr(), _lib.stream_ptr())
+        return loss_out
+
+    def apply_adam(self, dense_grad: bool = False) -> None:
+        lr = lr_at(self.step, self.train_cfg)
+        self.adam_t += 1
+        _lib.call("nvc_adam_step", self.model, self.adam_t, lr, self._epoch, int(dense_grad), _lib.stream_ptr())
+        self.step += 1
+
+    def train_step_device(self, pos, targets, mask=None, b_dev=None, b_max=None, comm=None):
+        """One fused step on device tensors; returns the loss as a 0-d CUDA tensor
+        (sum of per-row losses / b) without synchronising.  ``comm`` is an
+        optional callable(grad_fx, loss) run at the allreduce point."""
+        self.next_epoch()
+        loss = self.accumulate_grads(pos, targets, mask, b_max=b_max, b_dev=b_dev)
+        dense = False
+        if comm is not None:
+            comm(self.grad_fx, loss)
+            dense = True
+        self.apply_adam(dense_grad=dense)
+        b = b_dev.to(torch_f64()) if b_dev is not None else float(pos.shape[0])
+        return loss[0] / b
+
+    def train_step(self, positions, targets, mask=None) -> float:
+        """One fused encode/forward/backward/Adam update. Returns batch loss."""
+        import torch
+        pos, _ = self._pos_device(positions)
+        tg = torch.as_tensor(np.ascontiguousarray(np.atleast_2d(targets), dtype=np.float32)
+                             if not isinstance(targets, torch.Tensor) else targets).to(self.device, torch.float32)
+        if tg.shape != (pos.shape[0], self.output_dim):
+            raise ValueError(f"targets must be ({pos.shape[0]}, {self.output_dim}), got {tuple(tg.shape)}")
+        mk = None
+        if mask is not None:
+            mk = torch.as_tensor(np.broadcast_to(np.asarray(mask, np.float32), tg.shape).copy()
+                                 if not isinstance(mask, torch.Tensor) else mask).to(self.device, torch.float32)
+        loss = self.train_step_device(pos, tg.contiguous(), None if mk is None else mk.contiguous())
+        return float(loss.item())
+
+    # ---- snapshots (VCSNAP1, cache.py:77-117) ---------------------------
+    def save(self, path) -> None:
+        arrays = self._param_dict()
+        g = self.grid_cfg
+        header = {
+            "mode": self.mode, "output_dim": self.output_dim, "step": self.step,
+            "grid": {**{k: v for k, v in asdict(g).items() if k not in ("aabb_min", "aabb_max")},
+                     "aabb_min": g.aabb_min.tolist(), "aabb_max": g.aabb_max.tolist()},
+            "train": asdict(self.train_cfg),
+            "arrays": [{"name": k, "shape": list(v.shape)} for k, v in arrays.items()],
+            "hidden_dims": list(self.net_cfg.hidden_dims),
+        }
+        blob = json.dumps(header).encode("utf-8")
+        with open(path, "wb") as fh:
+            fh.write(SNAP_MAGIC)
+            fh.write(struct.pack("<I", len(blob)))
+            fh.write(blob)
+            for v in arrays.values():
+                fh.write(np.ascontiguousarray(v, dtype="<f4").tobytes())
+
+    @classmethod
+    def load(cls, path, **kw) -> "VisibilityCache":
+        with open(path, "rb") as fh:
+            if fh.read(len(SNAP_MAGIC)) != SNAP_MAGIC:
+                raise ValueError(f"{path}: not a cache snapshot")
+            (hlen,) = struct.unpack("<I", fh.read(4))
+            header = json.loads(fh.read(hlen).decode("utf-8"))
+            hidden = tuple(header.get("hidden_dims", (32, 32)))
+            obj = cls(mode=header["mode"], output_dim=header["output_dim"],
+                      grid=HashGridConfig(**header["grid"]), train=TrainStepConfig(**header["train"]),
+                      hidden_dims=hidden, **kw)
+            obj.step = header["step"]
+            arrays = obj._param_dict()
+            for spec in header["arrays"]:
+                shape = tuple(spec["shape"])
+                arrays[spec["name"]][...] = np.frombuffer(fh.read(4 * int(np.prod(shape))),
+                                                          dtype="<f4").reshape(shape)
+        ws = [arrays[f"w{i}"] for i in range(len(obj.net_cfg.layer_dims))]
+        bs = [arrays[f"b{i}"] for i in range(len(obj.net_cfg.layer_dims))]
+        obj._upload(arrays["grid"], MLPParams(ws, bs))
+        return obj
+
+
+def torch_f64():
+    import torch
+    return torch.float64
+
+
+def make_cache(scene, mode: str, seed: int = 0, clusters: int | None = None,
+               grid: HashGridConfig | None = None, train: TrainStepConfig | None = None,
+               dtype=np.float32, **kw) -> VisibilityCache:
+    """Cache sized to the scene: K lights, K clusters, or 3 RGB outputs (cache.py:120-139)."""
+    box = {"aabb_min": scene.aabb_min, "aabb_max": scene.aabb_max}
+    if mode == MODE_LIGHTS:
+        out, grid = scene.n_lights, grid or HashGridConfig(**box)
+    elif mode == MODE_CLUSTERS:
+        if clusters is None:
+            raise ValueError("cluster mode needs a cluster count")
+        out, grid = clusters, grid or clustered_config(**box)
+    elif mode == MODE_RADIANCE:
+        out, grid = 3, grid or HashGridConfig(**box)
+    else:
+        raise ValueError(f"unknown cache mode {mode!r}")
+    return VisibilityCache(mode, out, grid, train=train, seed=seed, dtype=dtype, **kw)

@@ -1,0 +1,194 @@
+// common.cuh -- shared device code for libnvc (sm_100a).
+//
+// Everything that has to reproduce the reference bit-for-bit uses explicit
+// round-to-nearest intrinsics (__dmul_rn, __dadd_rn, ...) so no FMA
+// contraction can creep in, whatever the TU's -fmad setting.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/nvc.h"
+
+namespace nvc {
+
+// ---------------------------------------------------------------------------
+// error plumbing (host)
+// ---------------------------------------------------------------------------
+void set_error(const char* fmt, ...);
+int check_launch(const char* what);
+
+#define NVC_REQUIRE(cond, ...)              \
+    do {                                    \
+        if (!(cond)) {                      \
+            ::nvc::set_error(__VA_ARGS__);  \
+            return NVC_ERR_ARG;             \
+        }                                   \
+    } while (0)
+
+constexpr int kNumSMs = 148;
+
+// fp32 SIMT inference (model.cu), used by nvc_infer(precision=0)
+int nvc_infer_f32(const nvc_model* m, const double* pos, int64_t n, float* out, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// Philox4x64-10, numpy-compatible random access (numpy Philox + rng.py:54-56).
+// Draw n of a stream = lane n%4 of the block at counter n/4 + 1 (numpy
+// increments the counter before producing its first buffer).
+// ---------------------------------------------------------------------------
+struct U4 {
+    uint64_t x[4];
+};
+
+__device__ __forceinline__ U4 philox_block(uint64_t counter, uint64_t key) {
+    uint64_t c0 = counter, c1 = 0, c2 = 0, c3 = 0, k0 = key, k1 = 0;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k0 += 0x9E3779B97F4A7C15ull;
+            k1 += 0xBB67AE8584CAA73Bull;
+        }
+        const uint64_t hi0 = __umul64hi(0xD2E7470EE14C6C93ull, c0);
+        const uint64_t lo0 = 0xD2E7470EE14C6C93ull * c0;
+        const uint64_t hi1 = __umul64hi(0xCA5A826395121157ull, c2);
+        const uint64_t lo1 = 0xCA5A826395121157ull * c2;
+        c0 = hi1 ^ c1 ^ k0;
+        c1 = lo1;
+        c2 = hi0 ^ c3 ^ k1;
+        c3 = lo0;
+    }
+    U4 o;
+    o.x[0] = c0;
+    o.x[1] = c1;
+    o.x[2] = c2;
+    o.x[3] = c3;
+    return o;
+}
+
+// numpy Generator.random(): (x >> 11) * 2^-53 (exact in binary64)
+__device__ __forceinline__ double u01(uint64_t x) { return (double)(x >> 11) * 0x1.0p-53; }
+
+__device__ __forceinline__ double draw(uint64_t key, uint64_t n) {
+    U4 b = philox_block(n / 4 + 1, key);
+    return u01(b.x[n & 3]);
+}
+
+// two consecutive draws n, n+1 (n even): always inside one Philox block
+__device__ __forceinline__ void draw2(uint64_t key, uint64_t n, double& a, double& b) {
+    U4 blk = philox_block(n / 4 + 1, key);
+    const int l = (int)(n & 3);
+    a = u01(blk.x[l]);
+    b = u01(blk.x[l + 1]);
+}
+
+// ---------------------------------------------------------------------------
+// fixed-point gradients
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ long long to_fx(double v) {
+    return __double2ll_rn(v * 0x1.0p48);
+}
+__device__ __forceinline__ float from_fx(long long q) {
+    return (float)((double)q * 0x1.0p-48);
+}
+__device__ __forceinline__ void red_add_fx(int64_t* p, long long v) {
+    if (v != 0)
+        asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"((unsigned long long)v) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// hash-grid addressing: hashgrid.py:94-114 (exact FP64 index math)
+// ---------------------------------------------------------------------------
+struct GridDev {
+    int L, F;
+    uint32_t tmask;
+    int64_t T;
+    int res[NVC_MAX_LEVELS];
+    int dense[NVC_MAX_LEVELS];
+    double lo[3], span[3];
+};
+
+inline GridDev grid_of(const nvc_model* m) {
+    GridDev g;
+    g.L = m->levels;
+    g.F = m->features;
+    g.T = m->table_size;
+    g.tmask = (uint32_t)(m->table_size - 1);
+    for (int l = 0; l < NVC_MAX_LEVELS; ++l) {
+        g.res[l] = m->resolution[l];
+        g.dense[l] = m->dense[l];
+    }
+    for (int a = 0; a < 3; ++a) {
+        g.lo[a] = m->aabb_min[a];
+        g.span[a] = m->span[a];
+    }
+    return g;
+}
+
+// q = clip((p - lo) / span, 0, 1)      (hashgrid.py:94-97)
+__device__ __forceinline__ void normalize(const GridDev& g, const double* p, double q[3]) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double v = __ddiv_rn(__dsub_rn(p[a], g.lo[a]), g.span[a]);
+        q[a] = fmin(fmax(v, 0.0), 1.0);
+    }
+}
+
+// per-level cell origin (int) and fractional offset (f64)  (hashgrid.py:100-103)
+__device__ __forceinline__ void cell(int n, const double q[3], int c0[3], double f[3]) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double x = __dmul_rn(q[a], (double)n);
+        int c = (int)x;  // trunc == floor for x >= 0
+        c = min(c, n - 1);
+        c0[a] = c;
+        f[a] = __dsub_rn(x, (double)c);
+    }
+}
+
+// vertex address of corner (bx,by,bz)   (hashgrid.py:104-114, 82-87)
+__device__ __forceinline__ uint32_t corner_index(const GridDev& g, int l, const int c0[3], int bx,
+                                                 int by, int bz) {
+    const uint32_t x = (uint32_t)(c0[0] + bx), y = (uint32_t)(c0[1] + by), z = (uint32_t)(c0[2] + bz);
+    if (g.dense[l]) {
+        const uint32_t m = (uint32_t)g.res[l] + 1u;
+        return x + m * (y + m * z);
+    }
+    return (x + y * 2654435761u + z * 805459861u) & g.tmask;
+}
+
+// trilinear weight of corner c = 4bx+2by+bz: (wx*wy)*wz in FP64 (hashgrid.py:105-107)
+__device__ __forceinline__ double corner_weight(const double f[3], int c) {
+    const double wx = (c & 4) ? f[0] : __dsub_rn(1.0, f[0]);
+    const double wy = (c & 2) ? f[1] : __dsub_rn(1.0, f[1]);
+    const double wz = (c & 1) ? f[2] : __dsub_rn(1.0, f[2]);
+    return __dmul_rn(__dmul_rn(wx, wy), wz);
+}
+
+// ---------------------------------------------------------------------------
+// scene helpers
+// ---------------------------------------------------------------------------
+// Scene.light_points (scene.py:204-215): id < 0 -> light 0; edges from vertices
+__device__ __forceinline__ void light_point(const nvc_scene& sc, int64_t id, double u0, double u1,
+                                            double out[3]) {
+    const int j = id < 0 ? 0 : (int)id;
+    const double* v = sc.lt_verts + 12 * j;
+    if (sc.lt_kind[j] == 1) {
+        out[0] = v[0];
+        out[1] = v[1];
+        out[2] = v[2];
+        return;
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double eu = __dsub_rn(v[3 + a], v[a]);
+        const double ev = __dsub_rn(v[9 + a], v[a]);
+        out[a] = __dadd_rn(__dadd_rn(v[a], __dmul_rn(u0, eu)), __dmul_rn(u1, ev));
+    }
+}
+
+__device__ __forceinline__ double norm3(double x, double y, double z) {
+    return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+}
+
+}  // namespace nvc

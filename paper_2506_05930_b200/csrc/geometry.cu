@@ -1,0 +1,524 @@
+// geometry.cu -- FP64 ray queries, G-buffer, unshadowed light factors and the
+// training-batch generator (SURVEY table K: K5, K6).
+//
+// This TU is compiled with -fmad=false: every expression below rounds like
+// the reference's serial numba/numpy code (no FMA contraction), which is what
+// makes G-buffers, screen samples and shadow-ray labels bit-exact.
+//
+// Reference routines (under /root/reference/pkg/src/viscache):
+//   ray_tri kernels.py:20-56, _aabb_hit :59-83, _inv_dir :86-90,
+//   closest_hit :93-137, any_hit :140-174, _rect_factor :220-281,
+//   _point_factor :284-296, light_factors_all :299-316,
+//   visibility_batch geometry.py:233-247, trace_rays render.py:49-75,
+//   make_gbuffer render.py:103-117, camera_rays_batch scene.py:129-139,
+//   gen_world_samples training.py:44-48, gen_screen_hits :67-94,
+//   compute_visibility_targets :103-120.
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace nvc {
+
+namespace {
+
+constexpr int kStack = 64;
+
+__device__ __forceinline__ double ray_tri(const double o[3], const double d[3], const double* a,
+                                          const double* b, const double* c, double t_min,
+                                          double t_max) {
+    const double e1x = b[0] - a[0], e1y = b[1] - a[1], e1z = b[2] - a[2];
+    const double e2x = c[0] - a[0], e2y = c[1] - a[1], e2z = c[2] - a[2];
+    const double px = d[1] * e2z - d[2] * e2y;
+    const double py = d[2] * e2x - d[0] * e2z;
+    const double pz = d[0] * e2y - d[1] * e2x;
+    const double det = e1x * px + e1y * py + e1z * pz;
+    if (fabs(det) < 1e-14) return -1.0;
+    const double inv = 1.0 / det;
+    const double tx = o[0] - a[0], ty = o[1] - a[1], tz = o[2] - a[2];
+    const double u = (tx * px + ty * py + tz * pz) * inv;
+    if (u < 0.0 || u > 1.0) return -1.0;
+    const double qx = ty * e1z - tz * e1y;
+    const double qy = tz * e1x - tx * e1z;
+    const double qz = tx * e1y - ty * e1x;
+    const double v = (d[0] * qx + d[1] * qy + d[2] * qz) * inv;
+    if (v < 0.0 || u + v > 1.0) return -1.0;
+    const double t = (e2x * qx + e2y * qy + e2z * qz) * inv;
+    if (t < t_min || t > t_max) return -1.0;
+    return t;
+}
+
+__device__ __forceinline__ bool aabb_hit(const double o[3], const double inv[3], const double* bmin,
+                                         const double* bmax, double t_max) {
+    double lo, hi;
+    {
+        double t0 = (bmin[0] - o[0]) * inv[0], t1 = (bmax[0] - o[0]) * inv[0];
+        if (t0 > t1) { const double s = t0; t0 = t1; t1 = s; }
+        lo = t0;
+        hi = t1;
+    }
+#pragma unroll
+    for (int a = 1; a < 3; ++a) {
+        double t0 = (bmin[a] - o[a]) * inv[a], t1 = (bmax[a] - o[a]) * inv[a];
+        if (t0 > t1) { const double s = t0; t0 = t1; t1 = s; }
+        if (t0 > lo) lo = t0;
+        if (t1 < hi) hi = t1;
+    }
+    return hi >= lo && lo <= t_max && hi >= 0.0;
+}
+
+__device__ __forceinline__ double inv_dir(double d) {
+    if (fabs(d) < 1e-300) return d >= 0.0 ? 1e300 : -1e300;
+    return 1.0 / d;
+}
+
+// nearest hit; returns BVH-order triangle index or -1, t in *t_out
+__device__ int64_t closest_hit(const nvc_scene& sc, const double o[3], const double d[3],
+                               double t_min, double t_max, double* t_out) {
+    *t_out = -1.0;
+    if (sc.n_tris == 0) return -1;
+    const double inv[3] = {inv_dir(d[0]), inv_dir(d[1]), inv_dir(d[2])};
+    double best_t = t_max;
+    int64_t best = -1;
+    int32_t stack[kStack];
+    int top = 0;
+    stack[top++] = 0;
+    while (top > 0) {
+        const int32_t n = stack[--top];
+        if (!aabb_hit(o, inv, sc.node_min + 3 * n, sc.node_max + 3 * n, best_t)) continue;
+        const int32_t cnt = __ldg(sc.node_count + n);
+        if (cnt > 0) {
+            const int32_t s = __ldg(sc.node_start + n);
+            for (int32_t k = s; k < s + cnt; ++k) {
+                const double t = ray_tri(o, d, sc.bv0 + 3 * k, sc.bv1 + 3 * k, sc.bv2 + 3 * k, t_min, best_t);
+                if (t >= 0.0) {
+                    best_t = t;
+                    best = k;
+                }
+            }
+        } else {
+            stack[top++] = __ldg(sc.node_left + n);
+            stack[top++] = __ldg(sc.node_right + n);
+        }
+    }
+    if (best >= 0) *t_out = best_t;
+    return best;
+}
+
+__device__ bool any_hit(const nvc_scene& sc, const double o[3], const double d[3], double t_min,
+                        double t_max) {
+    if (sc.n_tris == 0) return false;
+    const double inv[3] = {inv_dir(d[0]), inv_dir(d[1]), inv_dir(d[2])};
+    int32_t stack[kStack];
+    int top = 0;
+    stack[top++] = 0;
+    while (top > 0) {
+        const int32_t n = stack[--top];
+        if (!aabb_hit(o, inv, sc.node_min + 3 * n, sc.node_max + 3 * n, t_max)) continue;
+        const int32_t cnt = __ldg(sc.node_count + n);
+        if (cnt > 0) {
+            const int32_t s = __ldg(sc.node_start + n);
+            for (int32_t k = s; k < s + cnt; ++k)
+                if (ray_tri(o, d, sc.bv0 + 3 * k, sc.bv1 + 3 * k, sc.bv2 + 3 * k, t_min, t_max) >= 0.0)
+                    return true;
+        } else {
+            stack[top++] = __ldg(sc.node_left + n);
+            stack[top++] = __ldg(sc.node_right + n);
+        }
+    }
+    return false;
+}
+
+// visibility_batch for one segment (geometry.py:233-247)
+__device__ float segment_visible(const nvc_scene& sc, const double x[3], const double y[3]) {
+    const double eps = sc.shadow_eps;
+    const double d[3] = {y[0] - x[0], y[1] - x[1], y[2] - x[2]};
+    const double dist = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+    const double safe = fmax(dist, 1e-300);
+    const double dir[3] = {d[0] / safe, d[1] / safe, d[2] / safe};
+    double t_max = dist - eps;
+    if (t_max <= eps) return 1.0f;  // degenerate: endpoints closer than the epsilons
+    t_max = fmax(t_max, eps + 1e-12);
+    return any_hit(sc, x, dir, eps, t_max) ? 0.0f : 1.0f;
+}
+
+// camera_rays_batch (scene.py:129-139) for continuous image coords (sx, sy)
+__device__ void camera_ray(const nvc_camera& c, double sx, double sy, double d[3]) {
+    const double nx = ((2.0 * sx) / (double)c.width - 1.0) * c.tan_half * c.aspect;
+    const double ny = (1.0 - (2.0 * sy) / (double)c.height) * c.tan_half;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) d[a] = (c.fwd[a] + nx * c.right[a]) + ny * c.up[a];
+    const double n = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) d[a] = d[a] / n;
+}
+
+// _rect_factor (kernels.py:220-281)
+__device__ double rect_factor(const double p[3], const double n[3], const double* verts,
+                              const double* ln) {
+    const double side = (p[0] - verts[0]) * ln[0] + (p[1] - verts[1]) * ln[1] + (p[2] - verts[2]) * ln[2];
+    if (side <= 0.0) return 0.0;
+    double vx[4], vy[4], vz[4], cx[8], cy[8], cz[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        vx[i] = verts[3 * i + 0] - p[0];
+        vy[i] = verts[3 * i + 1] - p[1];
+        vz[i] = verts[3 * i + 2] - p[2];
+    }
+    int nc = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int j = (i + 1) & 3;
+        const double di = vx[i] * n[0] + vy[i] * n[1] + vz[i] * n[2];
+        const double dj = vx[j] * n[0] + vy[j] * n[1] + vz[j] * n[2];
+        if (di >= 0.0) {
+            cx[nc] = vx[i];
+            cy[nc] = vy[i];
+            cz[nc] = vz[i];
+            ++nc;
+        }
+        if ((di > 0.0 && dj < 0.0) || (di < 0.0 && dj > 0.0)) {
+            const double s = di / (di - dj);
+            cx[nc] = vx[i] + s * (vx[j] - vx[i]);
+            cy[nc] = vy[i] + s * (vy[j] - vy[i]);
+            cz[nc] = vz[i] + s * (vz[j] - vz[i]);
+            ++nc;
+        }
+    }
+    if (nc < 3) return 0.0;
+    for (int i = 0; i < nc; ++i) {
+        const double l = sqrt(cx[i] * cx[i] + cy[i] * cy[i] + cz[i] * cz[i]);
+        if (l < 1e-12) return 0.0;
+        cx[i] /= l;
+        cy[i] /= l;
+        cz[i] /= l;
+    }
+    double acc = 0.0;
+    for (int i = 0; i < nc; ++i) {
+        const int j = (i + 1) % nc;
+        double d = cx[i] * cx[j] + cy[i] * cy[j] + cz[i] * cz[j];
+        d = d > 1.0 ? 1.0 : (d < -1.0 ? -1.0 : d);
+        const double st0 = 1.0 - d * d;
+        const double st = sqrt(st0 > 0.0 ? st0 : 0.0);
+        const double ratio = st < 1e-9 ? 1.0 : acos(d) / st;
+        const double gx = cy[i] * cz[j] - cz[i] * cy[j];
+        const double gy = cz[i] * cx[j] - cx[i] * cz[j];
+        const double gz = cx[i] * cy[j] - cy[i] * cx[j];
+        acc += ratio * (gx * n[0] + gy * n[1] + gz * n[2]);
+    }
+    return 0.5 * fabs(acc);
+}
+
+// _point_factor (kernels.py:284-296)
+__device__ double point_factor(const double p[3], const double n[3], const double* l) {
+    const double wx = l[0] - p[0], wy = l[1] - p[1], wz = l[2] - p[2];
+    const double d2 = wx * wx + wy * wy + wz * wz;
+    if (d2 < 1e-24) return 0.0;
+    const double inv = 1.0 / sqrt(d2);
+    const double c = (wx * n[0] + wy * n[1] + wz * n[2]) * inv;
+    if (c <= 0.0) return 0.0;
+    return c / d2;
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+
+// trace_rays + make_gbuffer: jitter draws (2p, 2p+1) of the PRIMARY stream
+__global__ void k_gbuffer(nvc_scene sc, nvc_camera cam, uint64_t key, int64_t p_first, int64_t np,
+                          double* __restrict__ pos, double* __restrict__ nrm, double* __restrict__ alb,
+                          uint8_t* __restrict__ hit, int32_t* __restrict__ light_id) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= np) return;
+    const int64_t gp = p_first + i;
+    double j0, j1;
+    draw2(key, 2ull * (uint64_t)gp, j0, j1);
+    const int64_t ys = gp / cam.width, xs = gp - ys * cam.width;
+    double d[3];
+    camera_ray(cam, (double)xs + j0, (double)ys + j1, d);
+    double t;
+    const int64_t bt = closest_hit(sc, cam.pos, d, 0.0, __longlong_as_double(0x7ff0000000000000ll), &t);
+    const bool h = bt >= 0;
+    double P[3] = {0, 0, 0}, N[3] = {0, 0, 0}, A[3] = {0, 0, 0};
+    int32_t lid = -1;
+    if (h) {
+        const int64_t tri = __ldg(sc.perm + bt);
+        for (int a = 0; a < 3; ++a) P[a] = cam.pos[a] + t * d[a];
+        const double* v0 = sc.tv0 + 3 * tri;
+        const double* v1 = sc.tv1 + 3 * tri;
+        const double* v2 = sc.tv2 + 3 * tri;
+        const double e1[3] = {v1[0] - v0[0], v1[1] - v0[1], v1[2] - v0[2]};
+        const double e2[3] = {v2[0] - v0[0], v2[1] - v0[1], v2[2] - v0[2]};
+        N[0] = e1[1] * e2[2] - e1[2] * e2[1];
+        N[1] = e1[2] * e2[0] - e1[0] * e2[2];
+        N[2] = e1[0] * e2[1] - e1[1] * e2[0];
+        const double nn = fmax(sqrt((N[0] * N[0] + N[1] * N[1]) + N[2] * N[2]), 1e-300);
+        for (int a = 0; a < 3; ++a) N[a] = N[a] / nn;
+        const double facing = (N[0] * d[0] + N[1] * d[1]) + N[2] * d[2];
+        if (facing > 0.0)
+            for (int a = 0; a < 3; ++a) N[a] = N[a] * -1.0;
+        const int32_t mat = __ldg(sc.tri_material + tri);
+        if (mat >= 0)
+            for (int a = 0; a < 3; ++a) A[a] = __ldg(sc.mat_albedo + 3 * mat + a);
+        lid = __ldg(sc.tri_light + tri);
+    }
+    for (int a = 0; a < 3; ++a) {
+        pos[3 * i + a] = P[a];
+        nrm[3 * i + a] = N[a];
+        alb[3 * i + a] = A[a];
+    }
+    if (hit) hit[i] = h;
+    if (light_id) light_id[i] = lid;
+}
+
+// light_factors_all -> light-major factor[j*stride + p] (+ lum)
+template <typename T>
+__global__ void k_factors(nvc_scene sc, const double* __restrict__ pos, const double* __restrict__ nrm,
+                          const double* __restrict__ alb, int64_t np, int64_t stride,
+                          T* __restrict__ factor, T* __restrict__ lum) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y;
+    if (i >= np) return;
+    const double p[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+    const double n[3] = {nrm[3 * i], nrm[3 * i + 1], nrm[3 * i + 2]};
+    const double f = sc.lt_kind[j] == 0 ? rect_factor(p, n, sc.lt_verts + 12 * j, sc.lt_normal + 3 * j)
+                                        : point_factor(p, n, sc.lt_verts + 12 * j);
+    if (factor) factor[(int64_t)j * stride + i] = (T)f;
+    if (lum) {
+        const double* w = sc.lt_lumaw + 3 * j;
+        const double s = ((alb[3 * i] * w[0] + alb[3 * i + 1] * w[1]) + alb[3 * i + 2] * w[2]) / 3.141592653589793;
+        lum[(int64_t)j * stride + i] = (T)(f * s);
+    }
+}
+
+__global__ void k_visibility(nvc_scene sc, const double* __restrict__ x, const double* __restrict__ y,
+                             int64_t n, float* __restrict__ vis) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double a[3] = {x[3 * i], x[3 * i + 1], x[3 * i + 2]};
+    const double b[3] = {y[3 * i], y[3 * i + 1], y[3 * i + 2]};
+    vis[i] = segment_visible(sc, a, b);
+}
+
+__global__ void k_closest(nvc_scene sc, const double* __restrict__ o, const double* __restrict__ d,
+                          const double* __restrict__ t_min, const double* __restrict__ t_max, int64_t n,
+                          double* __restrict__ t_out, int64_t* __restrict__ tri_out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double oo[3] = {o[3 * i], o[3 * i + 1], o[3 * i + 2]};
+    const double dd[3] = {d[3 * i], d[3 * i + 1], d[3 * i + 2]};
+    double t;
+    const int64_t bt = closest_hit(sc, oo, dd, t_min[i], t_max[i], &t);
+    t_out[i] = t;
+    tri_out[i] = bt >= 0 ? __ldg(sc.perm + bt) : -1;
+}
+
+// ---- training batch --------------------------------------------------------
+struct BatchWs {
+    int64_t* counters;   // [0]=hits appended, [1]=want, [2]=draw offset
+    uint8_t* flag;       // n_screen
+    double* hp;          // n_screen * 3
+};
+
+__device__ __forceinline__ BatchWs batch_ws(void* ws, int n_screen) {
+    BatchWs w;
+    char* p = (char*)ws;
+    w.counters = (int64_t*)p;
+    w.hp = (double*)(p + 64);
+    w.flag = (uint8_t*)(p + 64 + 24 * (int64_t)n_screen);
+    return w;
+}
+
+// gen_world_samples: pos[i][c] = lo_c + (hi_c - lo_c) * u(3i + c)
+__global__ void k_world(nvc_scene sc, uint64_t key, int n, double* __restrict__ pos) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * n) return;
+    const int c = i % 3;
+    pos[i] = sc.aabb_min[c] + (sc.aabb_max[c] - sc.aabb_min[c]) * draw(key, (uint64_t)i);
+}
+
+// screen round with `want` rays starting at draw offset `off`
+__device__ __forceinline__ void screen_ray(const nvc_scene& sc, const nvc_camera& cam, uint64_t key,
+                                           int64_t off, int64_t want, int64_t i, uint8_t* flag,
+                                           double* hp) {
+    const double sx = draw(key, (uint64_t)(off + i)) * (double)cam.width;
+    const double sy = draw(key, (uint64_t)(off + want + i)) * (double)cam.height;
+    double d[3], t;
+    camera_ray(cam, sx, sy, d);
+    const int64_t bt = closest_hit(sc, cam.pos, d, 0.0, __longlong_as_double(0x7ff0000000000000ll), &t);
+    flag[i] = bt >= 0;
+    if (bt >= 0)
+        for (int a = 0; a < 3; ++a) hp[3 * i + a] = cam.pos[a] + t * d[a];
+}
+
+__global__ void k_screen_round0(nvc_scene sc, nvc_camera cam, uint64_t key, int n, void* ws) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    BatchWs w = batch_ws(ws, n);
+    screen_ray(sc, cam, key, 0, n, i, w.flag, w.hp);
+}
+
+// block-wide exclusive scan of 0/1 flags (1024 threads)
+__device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned bal = __ballot_sync(0xffffffffu, v);
+    const int in_warp = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) s_warp[wid] = __popc(bal);
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        int x = lane < nw ? s_warp[lane] : 0;
+        int incl = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane < nw) s_warp[lane] = incl - x;
+        if (lane == 31) *total = incl;
+    }
+    __syncthreads();
+    const int r = s_warp[wid] + in_warp;
+    __syncthreads();
+    return r;
+}
+
+// one block: order-preserving compaction of round 0, then rounds 1..8 in-block
+__global__ void __launch_bounds__(1024) k_screen_finish(nvc_scene sc, nvc_camera cam, uint64_t key,
+                                                        int n_world, int n, double* __restrict__ pos,
+                                                        int64_t* __restrict__ n_rows, void* ws) {
+    __shared__ int s_warp[32];
+    __shared__ int s_total;
+    BatchWs w = batch_ws(ws, n);
+    double* out = pos + 3 * (int64_t)n_world;
+    int64_t count = 0, want = n, off = 0;
+    for (int round = 0; round < 9 && want > 0; ++round) {
+        if (round > 0) {
+            for (int64_t i = threadIdx.x; i < want; i += blockDim.x) screen_ray(sc, cam, key, off, want, i, w.flag, w.hp);
+            __syncthreads();
+        }
+        int64_t hits = 0;
+        for (int64_t base = 0; base < want; base += blockDim.x) {
+            const int64_t i = base + threadIdx.x;
+            const int f = (i < want) ? (int)w.flag[i] : 0;
+            const int r = block_excl_scan(f, s_warp, &s_total);
+            if (f) {
+                const int64_t o = count + hits + r;
+                for (int a = 0; a < 3; ++a) out[3 * o + a] = w.hp[3 * i + a];
+            }
+            hits += s_total;
+            __syncthreads();
+        }
+        count += hits;
+        off += 2 * want;
+        want -= hits;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *n_rows = n_world + count;
+}
+
+// compute_visibility_targets (light mode): row i, light j uses draws j*2b + 2i, +1
+__global__ void k_targets(nvc_scene sc, uint64_t key, const double* __restrict__ pos,
+                          const int64_t* __restrict__ n_rows, int64_t b_host, int shard, int n_shards,
+                          int64_t cap, float* __restrict__ tgt) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y;
+    const int64_t b = n_rows ? *n_rows : b_host;
+    const int64_t lo = b * shard / n_shards, hi = b * (shard + 1) / n_shards;
+    const int64_t i = lo + r;
+    if (r >= cap || i >= hi) return;
+    double u0, u1, y[3];
+    draw2(key, (uint64_t)(2 * b * j + 2 * i), u0, u1);
+    light_point(sc, j, u0, u1, y);
+    const double x[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+    tgt[r * sc.n_lights + j] = segment_visible(sc, x, y);
+}
+
+__global__ void k_set_rows(int64_t* n_rows, int64_t v) { *n_rows = v; }
+
+inline int grid1(int64_t n, int bs) { return (int)((n + bs - 1) / bs); }
+
+}  // namespace
+
+}  // namespace nvc
+
+using namespace nvc;
+
+extern "C" {
+
+int nvc_gbuffer(const nvc_scene* sc, const nvc_camera* cam, uint64_t key, int64_t p_first, int64_t p,
+                double* pos, double* nrm, double* alb, uint8_t* hit, int32_t* light_id, void* stream) {
+    NVC_REQUIRE(sc && cam && pos && nrm && alb, "nvc_gbuffer: null argument");
+    if (p <= 0) return NVC_OK;
+    k_gbuffer<<<grid1(p, 128), 128, 0, (cudaStream_t)stream>>>(*sc, *cam, key, p_first, p, pos, nrm, alb, hit,
+                                                                light_id);
+    return check_launch("k_gbuffer");
+}
+
+int nvc_light_factors(const nvc_scene* sc, const double* pos, const double* nrm, const double* alb,
+                      int64_t p, int64_t stride, int32_t out_f64, void* factor, void* lum, void* stream) {
+    NVC_REQUIRE(sc && pos && nrm, "nvc_light_factors: null argument");
+    NVC_REQUIRE(!lum || alb, "nvc_light_factors: lum needs albedo");
+    NVC_REQUIRE(stride >= p, "nvc_light_factors: stride < p");
+    if (p <= 0) return NVC_OK;
+    dim3 g(grid1(p, 128), sc->n_lights);
+    if (out_f64)
+        k_factors<double><<<g, 128, 0, (cudaStream_t)stream>>>(*sc, pos, nrm, alb, p, stride, (double*)factor,
+                                                               (double*)lum);
+    else
+        k_factors<float><<<g, 128, 0, (cudaStream_t)stream>>>(*sc, pos, nrm, alb, p, stride, (float*)factor,
+                                                              (float*)lum);
+    return check_launch("k_factors");
+}
+
+int nvc_visibility(const nvc_scene* sc, const double* x, const double* y, int64_t n, float* vis,
+                   void* stream) {
+    NVC_REQUIRE(sc && x && y && vis, "nvc_visibility: null argument");
+    if (n <= 0) return NVC_OK;
+    k_visibility<<<grid1(n, 128), 128, 0, (cudaStream_t)stream>>>(*sc, x, y, n, vis);
+    return check_launch("k_visibility");
+}
+
+int nvc_closest_hit(const nvc_scene* sc, const double* o, const double* d, const double* t_min,
+                    const double* t_max, int64_t n, double* t_out, int64_t* tri_out, void* stream) {
+    NVC_REQUIRE(sc && o && d && t_min && t_max && t_out && tri_out, "nvc_closest_hit: null argument");
+    if (n <= 0) return NVC_OK;
+    k_closest<<<grid1(n, 128), 128, 0, (cudaStream_t)stream>>>(*sc, o, d, t_min, t_max, n, t_out, tri_out);
+    return check_launch("k_closest");
+}
+
+int64_t nvc_batch_workspace_bytes(int32_t n_screen) { return 64 + 25 * (int64_t)n_screen + 64; }
+
+int nvc_gen_train_batch(const nvc_scene* sc, const nvc_camera* cam, uint64_t key_world, uint64_t key_screen,
+                        uint64_t key_targets, int32_t n_world, int32_t n_screen, int32_t shard,
+                        int32_t n_shards, double* pos, float* tgt, int64_t* n_rows, void* ws, void* stream) {
+    NVC_REQUIRE(sc && cam && pos && n_rows && ws, "nvc_gen_train_batch: null argument");
+    NVC_REQUIRE(n_world >= 0 && n_screen >= 0 && n_shards >= 1 && shard >= 0 && shard < n_shards,
+                "nvc_gen_train_batch: bad counts/shard");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n_world > 0) k_world<<<grid1(3 * (int64_t)n_world, 256), 256, 0, s>>>(*sc, key_world, n_world, pos);
+    if (n_screen > 0) {
+        k_screen_round0<<<grid1(n_screen, 64), 64, 0, s>>>(*sc, *cam, key_screen, n_screen, ws);
+        k_screen_finish<<<1, 1024, 0, s>>>(*sc, *cam, key_screen, n_world, n_screen, pos, n_rows, ws);
+    } else {
+        k_set_rows<<<1, 1, 0, s>>>(n_rows, n_world);
+    }
+    int rc = check_launch("k_screen");
+    if (rc) return rc;
+    const int64_t total = (int64_t)n_world + n_screen;
+    const int64_t cap = total / n_shards + 1;
+    if (tgt && total > 0) {
+        dim3 g(grid1(cap, 64), sc->n_lights);
+        k_targets<<<g, 64, 0, s>>>(*sc, key_targets, pos, n_rows, 0, shard, n_shards, cap, tgt);
+    }
+    return check_launch("k_targets");
+}
+
+int nvc_targets(const nvc_scene* sc, uint64_t key, const double* pos, int64_t b, float* tgt, void* stream) {
+    NVC_REQUIRE(sc && pos && tgt, "nvc_targets: null argument");
+    if (b <= 0) return NVC_OK;
+    dim3 g(grid1(b, 64), sc->n_lights);
+    k_targets<<<g, 64, 0, (cudaStream_t)stream>>>(*sc, key, pos, nullptr, b, 0, 1, b, tgt);
+    return check_launch("k_targets");
+}
+
+}  // extern "C"

@@ -1,0 +1,602 @@
+// query.cu -- the hot path: fused hash-grid encode -> tcgen05/TMEM MLP ->
+// {visibility out | clamp * lum -> WRS -> light point | Neural DI}, one pass
+// per 128-pixel tile (SURVEY table K: K1 perf mode, K2, K7, K8), plus the
+// standalone WRS kernels used for parity on given weights.
+//
+// Reference routines (under /root/reference/pkg/src/viscache):
+//   VisibilityCache.infer cache.py:54-58, encode_batch hashgrid.py:117-131,
+//   forward mlp.py:110-140, clamp_visibility sampling.py:27-30,
+//   wrs_select_batch :74-85, nls_weights_batch :184-191,
+//   nls_sample_batch :194-205, neural_di_batch :215-218,
+//   PixelCtx.unshadowed_rgb :157-160, Scene.light_points scene.py:204-215.
+//
+// Tile pipeline (one CTA = 4 warps = 128 threads = 128 pixels = M of one
+// tcgen05.mma; thread t owns pixel row t, which is TMEM lane t):
+//   1. every thread encodes its pixel: FP64 cell/hash (bit-exact indices),
+//      half2 gathers from the fp16 shadow table (L2-resident), FP32 blend,
+//      fp16 features stored into the A tile in the UMMA K-major
+//      no-swizzle core-matrix layout;
+//   2. per layer one elected thread issues K/16 tcgen05.mma (M=128, N=width,
+//      A and B from smem descriptors, D in TMEM) and commits to an mbarrier;
+//   3. the 4 warps drain TMEM with tcgen05.ld 32x32b.x16 (16 columns per
+//      thread), add bias, activate, and write the next A tile (fp16);
+//   4. after the last layer each thread holds its pixel's K visibilities and
+//      runs the sequential FP64 reservoir (exactly the reference cumsum/
+//      compare order) with numpy-Philox uniforms, or the Neural-DI sum.
+// Several CTAs per SM overlap their gather phase with each other's MMA chain.
+#include <cstring>
+
+#include "common.cuh"
+
+namespace nvc {
+namespace {
+
+constexpr int kTile = 128;
+
+// ---------------------------------------------------------------------------
+// tcgen05 / mbarrier helpers (inline PTX, sm_100a)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// UMMA shared-memory descriptor, K-major, no swizzle (canonical
+// ((8,m),(T,2k)):((1T,SBO),(1,LBO)) with T = 8 halfs = 16 bytes)
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr & 0x3FFFFu) >> 4);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;   // descriptor version (sm_100)
+    return d;                 // base offset 0, lbo mode 0, swizzle none (0)
+}
+
+// instruction descriptor: kind::f16, A/B = f16, D = f32, both K-major, M=128
+__host__ __device__ constexpr uint32_t idesc_f16(int n) {
+    return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kTile >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float v[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---------------------------------------------------------------------------
+// kernel parameters
+// ---------------------------------------------------------------------------
+struct QNet {
+    int n_layers;
+    int dims[NVC_MAX_LAYERS + 1];
+    int np[NVC_MAX_LAYERS];          // padded N (multiple of 16)
+    int kp[NVC_MAX_LAYERS];          // padded K (multiple of 16)
+    int wofs[NVC_MAX_LAYERS];        // halfs offset of layer i in wpack
+    int64_t boff[NVC_MAX_LAYERS];    // bias offset in params
+    int wpack_halfs;
+    int hidden_kp;                   // max padded hidden width (A1 tile K)
+    int tmem_cols;
+    float alpha;
+    int out_sigmoid;
+    // smem carve-up (bytes)
+    int sm_wpack, sm_a0, sm_a1, sm_bias, sm_total;
+};
+
+enum Mode { kModeVis = 0, kModeNls = 1, kModeNdi = 2 };
+
+struct QOut {
+    int mode;
+    float* vis;                       // kModeVis: (P, K)
+    const void* lum;                  // kModeNls: light-major lum, kModeNdi: factor
+    int lum_f64;
+    int64_t stride;                   // light-major stride
+    int64_t p_first, p_total;
+    uint64_t key, offset;
+    double floor;
+    int64_t* ids;
+    double* pts;
+    double* big_w;
+    const double* albedo;             // kModeNdi
+    double* rgb;                      // kModeNdi
+};
+
+// streaming reservoir state of one pixel (wrs_select_batch, sequential FP64)
+struct Reservoir {
+    double s, wsel;
+    int sel;
+    uint64_t blk;       // cached Philox block index (n/4+1), 0 = none
+    U4 u;
+};
+
+__device__ __forceinline__ double draw_cached(Reservoir& r, uint64_t key, uint64_t n) {
+    const uint64_t b = n / 4 + 1;
+    if (b != r.blk) {
+        r.u = philox_block(b, key);
+        r.blk = b;
+    }
+    return u01(r.u.x[n & 3]);
+}
+
+__device__ __forceinline__ void reservoir_push(Reservoir& r, double w, int k, uint64_t key, uint64_t n) {
+    r.s = __dadd_rn(r.s, w);
+    if (w > 0.0) {   // u*s < 0 is impossible: zero-weight lights never need a uniform
+        const double u = draw_cached(r, key, n);
+        if (__dmul_rn(u, r.s) < w) {
+            r.sel = k;
+            r.wsel = w;
+        }
+    }
+}
+
+__device__ __forceinline__ void draw_pair(uint64_t key, uint64_t n, double& a, double& b) {
+    const U4 blk = philox_block(n / 4 + 1, key);
+    a = u01(blk.x[n & 3]);
+    if ((n & 3) != 3) {
+        b = u01(blk.x[(n & 3) + 1]);
+    } else {
+        const U4 nb = philox_block(n / 4 + 2, key);
+        b = u01(nb.x[0]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// encode one pixel into the A0 tile (fp16 shadow table, FP32 blend)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t a_off(int row, int k, int kp) {   // bytes
+    return (uint32_t)((row >> 3) * (kp * 16) + (k >> 3) * 128 + (row & 7) * 16 + (k & 7) * 2);
+}
+
+__device__ __forceinline__ void encode_row(const GridDev& g, const __half* __restrict__ table, const double* pos,
+                                           uint8_t* a0, int row, int kp0) {
+    double q[3];
+    normalize(g, pos, q);
+    for (int l = 0; l < g.L; ++l) {
+        int c0[3];
+        double f[3];
+        cell(g.res[l], q, c0, f);
+        const float fx = (float)f[0], fy = (float)f[1], fz = (float)f[2];
+        const float wxs[2] = {1.0f - fx, fx}, wys[2] = {1.0f - fy, fy}, wzs[2] = {1.0f - fz, fz};
+        const __half* tl = table + (int64_t)l * g.T * g.F;
+        if (g.F == 2) {
+            __half2 v[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const uint32_t idx = corner_index(g, l, c0, (c >> 2) & 1, (c >> 1) & 1, c & 1);
+                v[c] = __ldg(reinterpret_cast<const __half2*>(tl) + idx);
+            }
+            float a = 0.0f, b = 0.0f;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const float w = wxs[(c >> 2) & 1] * wys[(c >> 1) & 1] * wzs[c & 1];
+                const float2 fv = __half22float2(v[c]);
+                a = fmaf(w, fv.x, a);
+                b = fmaf(w, fv.y, b);
+            }
+            *reinterpret_cast<__half2*>(a0 + a_off(row, 2 * l, kp0)) = __floats2half2_rn(a, b);
+        } else {
+            float acc[8];
+            for (int k = 0; k < g.F; ++k) acc[k] = 0.0f;
+            for (int c = 0; c < 8; ++c) {
+                const uint32_t idx = corner_index(g, l, c0, (c >> 2) & 1, (c >> 1) & 1, c & 1);
+                const float w = wxs[(c >> 2) & 1] * wys[(c >> 1) & 1] * wzs[c & 1];
+                for (int k = 0; k < g.F; ++k) acc[k] = fmaf(w, __half2float(__ldg(tl + (int64_t)idx * g.F + k)), acc[k]);
+            }
+            for (int k = 0; k < g.F; ++k)
+                *reinterpret_cast<__half*>(a0 + a_off(row, l * g.F + k, kp0)) = __float2half_rn(acc[k]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// the fused kernel
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kTile) k_query(GridDev g, QNet net, const float* __restrict__ params,
+                                                 const __half* __restrict__ table,
+                                                 const uint16_t* __restrict__ wpack, const double* __restrict__ pos,
+                                                 int64_t P, nvc_scene sc, QOut o) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t mbar;
+    __shared__ uint32_t tmem_base_s;
+    uint8_t* s_w = smem + net.sm_wpack;
+    uint8_t* s_a0 = smem + net.sm_a0;
+    uint8_t* s_a1 = smem + net.sm_a1;
+    float* s_bias = reinterpret_cast<float*>(smem + net.sm_bias);
+    const int tid = threadIdx.x, warp = tid >> 5;
+
+    // ---- one-time setup: weights + biases -> smem, zero A0 padding, TMEM, mbarrier
+    {
+        const int n16 = net.wpack_halfs / 8;
+        const uint4* src = reinterpret_cast<const uint4*>(wpack);
+        uint4* dst = reinterpret_cast<uint4*>(s_w);
+        for (int i = tid; i < n16; i += kTile) dst[i] = __ldg(src + i);
+        int bo = 0;
+        for (int l = 0; l < net.n_layers; ++l) {
+            for (int n = tid; n < net.np[l]; n += kTile)
+                s_bias[bo + n] = n < net.dims[l + 1] ? __ldg(params + net.boff[l] + n) : 0.0f;
+            bo += net.np[l];
+        }
+        uint4 z = make_uint4(0, 0, 0, 0);
+        for (int i = tid; i < kTile * net.kp[0] / 8; i += kTile) reinterpret_cast<uint4*>(s_a0)[i] = z;
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                     "r"(net.tmem_cols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        mbar_init(&mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_s;
+    const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
+    uint32_t phase = 0;
+    const int K = net.dims[net.n_layers];
+    const uint32_t a0_addr = smem_u32(s_a0), a1_addr = smem_u32(s_a1), w_addr = smem_u32(s_w);
+
+    const int64_t ntiles = (P + kTile - 1) / kTile;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t p = tile * kTile + tid;
+        const bool valid = p < P;
+        // ---- 1. encode ----
+        if (valid) {
+            const double pp[3] = {pos[3 * p], pos[3 * p + 1], pos[3 * p + 2]};
+            encode_row(g, table, pp, s_a0, tid, net.kp[0]);
+        } else {
+            for (int k = 0; k < net.dims[0]; ++k)
+                *reinterpret_cast<__half*>(s_a0 + a_off(tid, k, net.kp[0])) = __float2half_rn(0.0f);
+        }
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+
+        Reservoir res;
+        res.s = 0.0;
+        res.wsel = 0.0;
+        res.sel = -1;
+        res.blk = 0;
+        double rgb[3] = {0.0, 0.0, 0.0};
+        const int64_t gp = o.p_first + p;
+
+        int bias_off = 0;
+        for (int l = 0; l < net.n_layers; ++l) {
+            // ---- 2. MMA (one elected thread) ----
+            if (tid == 0) {
+                tc_fence_after();
+                const uint32_t a_base = l == 0 ? a0_addr : a1_addr;
+                const uint32_t a_kp = l == 0 ? net.kp[0] : net.hidden_kp;
+                const uint32_t b_base = w_addr + 2u * net.wofs[l];
+                const uint32_t idesc = idesc_f16(net.np[l]);
+                for (int kk = 0; kk < net.kp[l] / 16; ++kk) {
+                    const uint64_t ad = smem_desc(a_base + kk * 256u, 128u, a_kp * 16u);
+                    const uint64_t bd = smem_desc(b_base + kk * 256u, 128u, (uint32_t)net.kp[l] * 16u);
+                    mma_f16(tmem, ad, bd, idesc, kk > 0 ? 1u : 0u);
+                }
+                mma_commit(&mbar);
+            }
+            mbar_wait(&mbar, phase);
+            phase ^= 1;
+            tc_fence_after();
+
+            // ---- 3. epilogue ----
+            const bool last = l == net.n_layers - 1;
+            for (int c = 0; c < net.np[l] / 16; ++c) {
+                float v[16];
+                tmem_ld16(t_row + (uint32_t)(c * 16), v);
+                if (!last) {
+                    __align__(16) __half h[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        float z = v[j] + s_bias[bias_off + c * 16 + j];
+                        z = z >= 0.0f ? z : net.alpha * z;
+                        h[j] = __float2half_rn(z);
+                    }
+                    uint8_t* dst = s_a1 + a_off(tid, c * 16, net.hidden_kp);
+                    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(h);
+                    *reinterpret_cast<uint4*>(dst + 128) = *reinterpret_cast<const uint4*>(h + 8);
+                } else if (valid) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int k = c * 16 + j;
+                        if (k >= K) break;
+                        const float z = v[j] + s_bias[bias_off + k];
+                        float a;
+                        if (net.out_sigmoid) {
+                            a = z >= 0.0f ? 1.0f / (1.0f + __expf(-z)) : __expf(z) / (1.0f + __expf(z));
+                            a = fminf(fmaxf(a, 1e-6f), 0.999999f);
+                        } else {
+                            a = z >= 0.0f ? z : net.alpha * z;
+                        }
+                        if (o.mode == kModeVis) {
+                            o.vis[p * K + k] = a;
+                        } else if (o.mode == kModeNls) {
+                            double vv = (double)a;
+                            vv = o.floor > 0.0 ? fmax(vv, o.floor) : fmax(vv, 0.0);
+                            const int64_t li = (int64_t)k * o.stride + p;
+                            const double lum = o.lum_f64 ? __ldg(reinterpret_cast<const double*>(o.lum) + li)
+                                                         : (double)__ldg(reinterpret_cast<const float*>(o.lum) + li);
+                            reservoir_push(res, __dmul_rn(vv, lum), k, o.key,
+                                           o.offset + (uint64_t)gp * (uint64_t)K + (uint64_t)k);
+                        } else {
+                            const int64_t li = (int64_t)k * o.stride + p;
+                            const double fct = o.lum_f64 ? __ldg(reinterpret_cast<const double*>(o.lum) + li)
+                                                         : (double)__ldg(reinterpret_cast<const float*>(o.lum) + li);
+                            const double wk = __dmul_rn((double)a, fct);
+#pragma unroll
+                            for (int ch = 0; ch < 3; ++ch)
+                                rgb[ch] = __dadd_rn(rgb[ch], __dmul_rn(wk, __ldg(sc.lt_radiance + 3 * k + ch)));
+                        }
+                    }
+                }
+            }
+            bias_off += net.np[l];
+            fence_async_smem();
+            tc_fence_before();
+            __syncthreads();
+        }
+
+        // ---- 4. per-pixel outputs ----
+        if (valid && o.mode == kModeNls) {
+            const double big_w = res.sel >= 0 ? __ddiv_rn(res.s, res.wsel > 0.0 ? res.wsel : 1.0) : 0.0;
+            double u0, u1, y[3];
+            draw_pair(o.key, o.offset + (uint64_t)o.p_total * (uint64_t)K + 2ull * (uint64_t)gp, u0, u1);
+            light_point(sc, res.sel, u0, u1, y);
+            o.ids[p] = res.sel;
+            o.big_w[p] = big_w;
+            o.pts[3 * p] = y[0];
+            o.pts[3 * p + 1] = y[1];
+            o.pts[3 * p + 2] = y[2];
+        } else if (valid && o.mode == kModeNdi) {
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch)
+                o.rgb[3 * p + ch] = __ddiv_rn(__dmul_rn(rgb[ch], o.albedo[3 * p + ch]), 3.141592653589793);
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(net.tmem_cols) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// standalone WRS on given weights (parity entry points)
+// ---------------------------------------------------------------------------
+__global__ void k_wrs_select(const double* __restrict__ w, int64_t P, int K, uint64_t key, uint64_t offset,
+                             int64_t* __restrict__ idx, double* __restrict__ wsel, double* __restrict__ wsum) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    Reservoir r;
+    r.s = 0.0;
+    r.wsel = 0.0;
+    r.sel = -1;
+    r.blk = 0;
+    for (int k = 0; k < K; ++k) reservoir_push(r, w[p * K + k], k, key, offset + (uint64_t)p * K + k);
+    idx[p] = r.sel;
+    wsel[p] = r.sel >= 0 ? r.wsel : 0.0;
+    wsum[p] = r.s;
+}
+
+template <typename T>
+__global__ void k_nls_from_vis(nvc_scene sc, const float* __restrict__ vis, const T* __restrict__ lum, int64_t stride,
+                               int64_t P, int K, int64_t p_first, int64_t p_total, uint64_t key, uint64_t offset,
+                               double floor, int64_t* __restrict__ ids, double* __restrict__ pts,
+                               double* __restrict__ big_w) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    const int64_t gp = p_first + p;
+    Reservoir r;
+    r.s = 0.0;
+    r.wsel = 0.0;
+    r.sel = -1;
+    r.blk = 0;
+    for (int k = 0; k < K; ++k) {
+        double v = (double)vis[p * K + k];
+        v = floor > 0.0 ? fmax(v, floor) : fmax(v, 0.0);
+        reservoir_push(r, __dmul_rn(v, (double)lum[(int64_t)k * stride + p]), k, key,
+                       offset + (uint64_t)gp * K + k);
+    }
+    double u0, u1, y[3];
+    draw_pair(key, offset + (uint64_t)p_total * K + 2ull * gp, u0, u1);
+    light_point(sc, r.sel, u0, u1, y);
+    ids[p] = r.sel;
+    big_w[p] = r.sel >= 0 ? __ddiv_rn(r.s, r.wsel > 0.0 ? r.wsel : 1.0) : 0.0;
+    pts[3 * p] = y[0];
+    pts[3 * p + 1] = y[1];
+    pts[3 * p + 2] = y[2];
+}
+
+inline int grid1(int64_t n, int bs) { return (int)((n + bs - 1) / bs); }
+
+int make_qnet(const nvc_model* m, QNet& q) {
+    NVC_REQUIRE(m && m->params && m->table_h && m->wpack, "tcgen05 path: model state not bound");
+    NVC_REQUIRE(m->n_layers >= 1 && m->n_layers <= NVC_MAX_LAYERS, "n_layers out of range");
+    NVC_REQUIRE(m->dims[0] == m->levels * m->features, "dims[0] must equal levels*features");
+    q.n_layers = m->n_layers;
+    int64_t wo = 0, bo = (int64_t)m->levels * m->table_size * m->features;
+    int hid = 16, maxnp = 16;
+    for (int i = 0; i <= m->n_layers; ++i) q.dims[i] = m->dims[i];
+    for (int i = 0; i < m->n_layers; ++i) {
+        if (m->dims[i] > 256 || m->dims[i + 1] > 256) {
+            set_error("tcgen05 path: layer widths must be <= 256");
+            return NVC_ERR_UNSUPPORTED;
+        }
+        q.np[i] = (m->dims[i + 1] + 15) / 16 * 16;
+        q.kp[i] = (m->dims[i] + 15) / 16 * 16;
+        q.wofs[i] = (int)wo;
+        wo += (int64_t)q.np[i] * q.kp[i];
+        bo += (int64_t)m->dims[i + 1] * m->dims[i];
+        q.boff[i] = bo;
+        bo += m->dims[i + 1];
+        if (i < m->n_layers - 1 && q.np[i] > hid) hid = q.np[i];
+        if (q.np[i] > maxnp) maxnp = q.np[i];
+    }
+    q.wpack_halfs = (int)wo;
+    q.hidden_kp = hid;
+    int cols = 32;
+    while (cols < maxnp) cols <<= 1;
+    q.tmem_cols = cols;
+    q.alpha = m->alpha;
+    q.out_sigmoid = m->out_sigmoid;
+    int nb = 0;
+    for (int i = 0; i < m->n_layers; ++i) nb += q.np[i];
+    q.sm_wpack = 0;
+    q.sm_a0 = (q.wpack_halfs * 2 + 1023) / 1024 * 1024;
+    q.sm_a1 = q.sm_a0 + (kTile * q.kp[0] * 2 + 1023) / 1024 * 1024;
+    q.sm_bias = q.sm_a1 + (kTile * q.hidden_kp * 2 + 1023) / 1024 * 1024;
+    q.sm_total = q.sm_bias + nb * 4 + 1024;   // +1024: dynamic-smem base alignment slack
+    if (q.sm_total > 220 * 1024) {
+        set_error("tcgen05 path: %d bytes of shared memory needed", q.sm_total);
+        return NVC_ERR_UNSUPPORTED;
+    }
+    return NVC_OK;
+}
+
+int launch_query(const nvc_model* m, const double* pos, int64_t P, const nvc_scene* sc, const QOut& o,
+                 cudaStream_t s) {
+    QNet q;
+    int rc = make_qnet(m, q);
+    if (rc) return rc;
+    if (P <= 0) return NVC_OK;
+    GridDev g = grid_of(m);
+    cudaFuncSetAttribute(k_query, cudaFuncAttributeMaxDynamicSharedMemorySize, q.sm_total);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query, kTile, q.sm_total);
+    per_sm = max(1, min(per_sm, 512 / q.tmem_cols));
+    int dev = 0, sms = kNumSMs;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t ntiles = (P + kTile - 1) / kTile;
+    const int64_t cap = (int64_t)sms * per_sm;
+    const int grid = (int)(ntiles < cap ? ntiles : cap);
+    nvc_scene scv;
+    if (sc) scv = *sc;
+    else memset(&scv, 0, sizeof scv);
+    k_query<<<grid, kTile, q.sm_total, s>>>(g, q, m->params, reinterpret_cast<const __half*>(m->table_h), m->wpack,
+                                            pos, P, scv, o);
+    return check_launch("k_query");
+}
+
+}  // namespace
+
+}  // namespace nvc
+
+using namespace nvc;
+
+extern "C" {
+
+int nvc_infer(const nvc_model* m, const double* pos, int64_t n, int32_t precision, float* out, void* stream) {
+    NVC_REQUIRE(m && pos && out, "nvc_infer: null argument");
+    if (n <= 0) return NVC_OK;
+    if (precision == 0) return nvc_infer_f32(m, pos, n, out, (cudaStream_t)stream);
+    QOut o;
+    memset(&o, 0, sizeof o);
+    o.mode = kModeVis;
+    o.vis = out;
+    return launch_query(m, pos, n, nullptr, o, (cudaStream_t)stream);
+}
+
+int nvc_nls_sample(const nvc_model* m, const nvc_scene* sc, const double* pos, const void* lum, int32_t lum_f64,
+                   int64_t stride, int64_t p, int64_t p_first, int64_t p_total, uint64_t key, uint64_t offset,
+                   double floor, int64_t* ids, double* pts, double* big_w, void* stream) {
+    NVC_REQUIRE(m && sc && pos && lum && ids && pts && big_w, "nvc_nls_sample: null argument");
+    NVC_REQUIRE(sc->n_lights == m->dims[m->n_layers], "nvc_nls_sample: output_dim != scene lights");
+    NVC_REQUIRE(stride >= p && p_total >= p_first + p, "nvc_nls_sample: bad stride / frame size");
+    QOut o;
+    memset(&o, 0, sizeof o);
+    o.mode = kModeNls;
+    o.lum = lum;
+    o.lum_f64 = lum_f64;
+    o.stride = stride;
+    o.p_first = p_first;
+    o.p_total = p_total;
+    o.key = key;
+    o.offset = offset;
+    o.floor = floor;
+    o.ids = ids;
+    o.pts = pts;
+    o.big_w = big_w;
+    return launch_query(m, pos, p, sc, o, (cudaStream_t)stream);
+}
+
+int nvc_neural_di(const nvc_model* m, const nvc_scene* sc, const double* pos, const double* albedo,
+                  const void* factor, int32_t factor_f64, int64_t stride, int64_t p, double* rgb, void* stream) {
+    NVC_REQUIRE(m && sc && pos && albedo && factor && rgb, "nvc_neural_di: null argument");
+    NVC_REQUIRE(sc->n_lights == m->dims[m->n_layers], "nvc_neural_di: output_dim != scene lights");
+    QOut o;
+    memset(&o, 0, sizeof o);
+    o.mode = kModeNdi;
+    o.lum = factor;
+    o.lum_f64 = factor_f64;
+    o.stride = stride;
+    o.albedo = albedo;
+    o.rgb = rgb;
+    return launch_query(m, pos, p, sc, o, (cudaStream_t)stream);
+}
+
+int nvc_wrs_select(const double* w, int64_t p, int32_t k, uint64_t key, uint64_t offset, int64_t* idx,
+                   double* w_sel, double* w_sum, void* stream) {
+    NVC_REQUIRE(w && idx && w_sel && w_sum && k >= 1, "nvc_wrs_select: bad argument");
+    if (p <= 0) return NVC_OK;
+    k_wrs_select<<<grid1(p, 128), 128, 0, (cudaStream_t)stream>>>(w, p, k, key, offset, idx, w_sel, w_sum);
+    return check_launch("k_wrs_select");
+}
+
+int nvc_nls_from_vis(const nvc_scene* sc, const float* vis, const void* lum, int32_t lum_f64, int64_t stride,
+                     int64_t p, int32_t k, int64_t p_first, int64_t p_total, uint64_t key, uint64_t offset,
+                     double floor, int64_t* ids, double* pts, double* big_w, void* stream) {
+    NVC_REQUIRE(sc && vis && lum && ids && pts && big_w && k >= 1, "nvc_nls_from_vis: bad argument");
+    NVC_REQUIRE(stride >= p && p_total >= p_first + p, "nvc_nls_from_vis: bad stride / frame size");
+    if (p <= 0) return NVC_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (lum_f64)
+        k_nls_from_vis<double><<<grid1(p, 128), 128, 0, s>>>(*sc, vis, (const double*)lum, stride, p, k, p_first,
+                                                             p_total, key, offset, floor, ids, pts, big_w);
+    else
+        k_nls_from_vis<float><<<grid1(p, 128), 128, 0, s>>>(*sc, vis, (const float*)lum, stride, p, k, p_first,
+                                                            p_total, key, offset, floor, ids, pts, big_w);
+    return check_launch("k_nls_from_vis");
+}
+
+}  // extern "C"

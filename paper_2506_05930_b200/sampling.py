@@ -1,0 +1,278 @@
+"""Light selection driven by the cache: drop-in for ``viscache.sampling``
+(sampling.py:19-222: WRS, unshadowed weights, NLS, Neural DI).
+
+Every function keeps the reference signature and numpy outputs.  The work
+runs on the GPU: the fused ``nvc_nls_sample`` / ``nvc_neural_di`` kernels when
+the cache is this package's :class:`VisibilityCache`, otherwise (any
+duck-typed cache exposing ``infer``, e.g. the reference tests' FixedCache)
+``cache.infer`` supplies the visibilities and ``nvc_nls_from_vis`` does the
+selection.  Uniforms come from the caller's Philox stream by global draw
+index, so results are bit-identical to the reference given the same weights,
+and screen-tile shards (``p_first``/``p_total``) reproduce the whole frame.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from . import rng as rngmod
+from .scene import LUMA, device_scene
+
+CLAMP_FLOOR = 0.001
+
+
+def clamp_visibility(v, floor: float = CLAMP_FLOOR):
+    return np.maximum(v, floor)
+
+
+@dataclass
+class ShadingPoint:
+    position: np.ndarray
+    normal: np.ndarray
+    albedo: np.ndarray
+    omega_o: np.ndarray | None = None
+
+    def __post_init__(self):
+        self.position = np.asarray(self.position, dtype=np.float64)
+        self.normal = np.asarray(self.normal, dtype=np.float64)
+        self.albedo = np.asarray(self.albedo, dtype=np.float64)
+
+
+@dataclass
+class Reservoir:
+    """Invariant (nonempty): W == w_sum / (M * w_y)  (sampling.py:46-62)."""
+
+    y: int = -1
+    point: np.ndarray | None = None
+    w_y: float = 0.0
+    w_sum: float = 0.0
+    M: float = 0.0
+    W: float = 0.0
+
+    @property
+    def empty(self) -> bool:
+        return self.y < 0 or self.W <= 0.0
+
+
+def _dev(a, torch, device, dtype):
+    if isinstance(a, torch.Tensor):
+        return a.to(device, dtype).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64 if dtype == torch.float64 else np.float32)).to(device)
+
+
+def wrs_select_batch(weights, rng):
+    """Row-wise streaming WRS on the GPU; (index, w_selected, w_sum), index -1 for all-zero rows."""
+    torch = _lib.require_cuda()
+    w = np.atleast_2d(np.asarray(weights, dtype=np.float64))
+    p, k = w.shape
+    key, off = rngmod.position(rng)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    wd = _dev(w, torch, dev, torch.float64)
+    idx = torch.empty(p, dtype=torch.int64, device=dev)
+    wsel = torch.empty(p, dtype=torch.float64, device=dev)
+    wsum = torch.empty(p, dtype=torch.float64, device=dev)
+    _lib.call("nvc_wrs_select", wd.data_ptr(), p, k, key, off, idx.data_ptr(), wsel.data_ptr(),
+              wsum.data_ptr(), _lib.stream_ptr())
+    rngmod.advance(rng, p * k)
+    return idx.cpu().numpy(), wsel.cpu().numpy(), wsum.cpu().numpy()
+
+
+def wrs_select(weights, rng) -> Reservoir:
+    w = np.asarray(weights, dtype=np.float64)
+    if w.ndim != 1 or w.size < 1:
+        raise ValueError("weight stream must be a nonempty 1-d sequence")
+    if np.any(w < 0):
+        raise ValueError("weights must be nonnegative")
+    idx, w_sel, w_sum = wrs_select_batch(w[None, :], rng)
+    if idx[0] < 0:
+        return Reservoir(M=w.size)
+    return Reservoir(y=int(idx[0]), w_y=float(w_sel[0]), w_sum=float(w_sum[0]), M=w.size,
+                     W=float(w_sum[0] / (w.size * w_sel[0])))
+
+
+class PixelCtx:
+    """Per-pixel shading data resident on the GPU, with lazily built
+    light-major (K, P) factor / luminance tables (sampling.py:109-160).
+
+    ``table_dtype`` float32 (default, half the HBM traffic of the hot loop)
+    or float64 (bit-faithful to the reference's FP64 tables)."""
+
+    def __init__(self, scene, positions, normals, albedos, factors=None, table_dtype=np.float32,
+                 device=None):
+        torch = _lib.require_cuda()
+        self.scene = scene
+        self.dscene = device_scene(scene, device)
+        dev = self.dscene.device
+        self.device = dev
+        self.pos = _dev(np.atleast_2d(positions) if not isinstance(positions, torch.Tensor) else positions,
+                        torch, dev, torch.float64).reshape(-1, 3)
+        self.nrm = _dev(np.atleast_2d(normals) if not isinstance(normals, torch.Tensor) else normals,
+                        torch, dev, torch.float64).reshape(-1, 3)
+        self.alb = _dev(np.atleast_2d(albedos) if not isinstance(albedos, torch.Tensor) else albedos,
+                        torch, dev, torch.float64).reshape(-1, 3)
+        self._host_pos = None if isinstance(positions, torch.Tensor) else np.ascontiguousarray(
+            np.atleast_2d(positions), dtype=np.float64)
+        self.table_dtype = np.dtype(table_dtype)
+        self._tdt = torch.float64 if self.table_dtype == np.float64 else torch.float32
+        self._factor = None
+        self._lum = None
+        if factors is not None:
+            self._factor = _dev(np.asarray(factors).T, torch, dev, self._tdt).contiguous()
+
+    @property
+    def n(self) -> int:
+        return self.pos.shape[0]
+
+    @property
+    def positions(self) -> np.ndarray:
+        if self._host_pos is None:
+            self._host_pos = self.pos.cpu().numpy()
+        return self._host_pos
+
+    def _build(self, want_lum: bool) -> None:
+        import torch
+        k, p = self.dscene.n_lights, self.n
+        fac = None if self._factor is not None else torch.empty((k, p), dtype=self._tdt, device=self.device)
+        lum = torch.empty((k, p), dtype=self._tdt, device=self.device) if want_lum else None
+        if fac is None and lum is None:
+            return
+        if fac is None:
+            # factors supplied by the caller: lum = factor * (albedo . LUMA*L)/pi on device
+            scale = (self.alb @ (torch.as_tensor(LUMA, device=self.device)[:, None]
+                                 * self.dscene.lt_radiance.T)) / np.pi
+            self._lum = (self._factor.to(torch.float64) * scale.T).to(self._tdt).contiguous()
+            return
+        _lib.call("nvc_light_factors", self.dscene.struct, self.pos.data_ptr(), self.nrm.data_ptr(),
+                  self.alb.data_ptr(), p, p, int(self._tdt == torch.float64), fac.data_ptr(), _lib.ptr(lum),
+                  _lib.stream_ptr())
+        self._factor = fac
+        if want_lum:
+            self._lum = lum
+
+    def factor_device(self):
+        if self._factor is None:
+            self._build(want_lum=self._lum is None)
+        return self._factor
+
+    def lum_device(self):
+        if self._lum is None:
+            self._build(want_lum=True)
+        return self._lum
+
+    def factor_matrix(self) -> np.ndarray:
+        return self.factor_device().T.to(dtype=__import__("torch").float64).cpu().numpy()
+
+    def lum_matrix(self) -> np.ndarray:
+        return self.lum_device().T.to(dtype=__import__("torch").float64).cpu().numpy()
+
+    def phat_ids(self, ids) -> np.ndarray:
+        ids = np.asarray(ids)
+        lum = self.lum_matrix()
+        return np.where(ids >= 0, np.take_along_axis(lum, np.maximum(ids, 0)[:, None], 1)[:, 0], 0.0)
+
+    def unshadowed_rgb(self, vis) -> np.ndarray:
+        import torch
+        v = _dev(np.asarray(vis, np.float64), torch, self.device, torch.float64)
+        f = self.factor_device().to(torch.float64).T
+        rgb = ((v * f) @ self.dscene.lt_radiance) * self.alb / np.pi
+        return rgb.cpu().numpy()
+
+
+def _ctx_for(sp: ShadingPoint, scene) -> PixelCtx:
+    return PixelCtx(scene, sp.position[None, :], sp.normal[None, :], sp.albedo[None, :],
+                    table_dtype=np.float64)
+
+
+def unshadowed_weight(sp: ShadingPoint, light_id: int, scene) -> float:
+    return float(_ctx_for(sp, scene).phat_ids(np.array([light_id]))[0])
+
+
+def unshadowed_rgb_one(sp: ShadingPoint, light_id: int, scene) -> np.ndarray:
+    f = _ctx_for(sp, scene).factor_matrix()[0, light_id]
+    return sp.albedo / np.pi * scene.lt_radiance[light_id] * f
+
+
+def _is_native(cache) -> bool:
+    from .cache import VisibilityCache
+    return isinstance(cache, VisibilityCache)
+
+
+def nls_weights_batch(ctx: PixelCtx, cache, clamp_floor: float | None = CLAMP_FLOOR) -> np.ndarray:
+    vis = np.asarray(cache.infer(ctx.positions), dtype=np.float64)
+    vis = clamp_visibility(vis, clamp_floor) if clamp_floor and clamp_floor > 0.0 else np.maximum(vis, 0.0)
+    return vis * ctx.lum_matrix()
+
+
+def nls_sample_device(ctx: PixelCtx, cache, key: int, offset: int = 0, clamp_floor=CLAMP_FLOOR,
+                      p_first: int = 0, p_total: int | None = None, out=None):
+    """Device-resident NLS: returns (ids int64, pts (P,3) f64, W f64) CUDA tensors.
+
+    Pixels of ctx are rows p_first.. of a p_total-pixel frame (screen-tile shard)."""
+    import torch
+    p = ctx.n
+    k = ctx.dscene.n_lights
+    total = p if p_total is None else p_total
+    if out is None:
+        out = (torch.empty(p, dtype=torch.int64, device=ctx.device),
+               torch.empty((p, 3), dtype=torch.float64, device=ctx.device),
+               torch.empty(p, dtype=torch.float64, device=ctx.device))
+    ids, pts, big_w = out
+    floor = float(clamp_floor) if clamp_floor and clamp_floor > 0.0 else 0.0
+    lum = ctx.lum_device()
+    lum64 = int(lum.dtype == torch.float64)
+    if _is_native(cache):
+        if cache.output_dim != k:
+            raise ValueError(f"cache has {cache.output_dim} outputs, scene has {k} lights")
+        _lib.call("nvc_nls_sample", cache.model, ctx.dscene.struct, ctx.pos.data_ptr(), lum.data_ptr(), lum64,
+                  lum.shape[1], p, p_first, total, key, offset, floor, ids.data_ptr(), pts.data_ptr(),
+                  big_w.data_ptr(), _lib.stream_ptr())
+    else:
+        vis = cache.infer(ctx.positions)
+        vis = vis if isinstance(vis, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(vis, np.float32))
+        vis = vis.to(ctx.device, torch.float32).contiguous()
+        _lib.call("nvc_nls_from_vis", ctx.dscene.struct, vis.data_ptr(), lum.data_ptr(), lum64, lum.shape[1], p,
+                  k, p_first, total, key, offset, floor, ids.data_ptr(), pts.data_ptr(), big_w.data_ptr(),
+                  _lib.stream_ptr())
+    return ids, pts, big_w
+
+
+def nls_sample_batch(ctx: PixelCtx, cache, rng, clamp_floor: float | None = CLAMP_FLOOR):
+    """Exhaustive-stream WRS over all lights: (light ids, emitter points, W = w_sum/w_sel)."""
+    key, off = rngmod.position(rng)
+    ids, pts, big_w = nls_sample_device(ctx, cache, key, off, clamp_floor)
+    k = ctx.dscene.n_lights
+    rngmod.advance(rng, ctx.n * k + 2 * ctx.n)
+    return ids.cpu().numpy(), pts.cpu().numpy(), big_w.cpu().numpy()
+
+
+def nls_sample(sp: ShadingPoint, cache, scene, rng, clamp_floor: float | None = CLAMP_FLOOR):
+    ids, pts, ws = nls_sample_batch(_ctx_for(sp, scene), cache, rng, clamp_floor)
+    return int(ids[0]), pts[0], float(ws[0])
+
+
+def neural_di_device(ctx: PixelCtx, cache, out=None):
+    import torch
+    p = ctx.n
+    if out is None:
+        out = torch.empty((p, 3), dtype=torch.float64, device=ctx.device)
+    if _is_native(cache):
+        fac = ctx.factor_device()
+        _lib.call("nvc_neural_di", cache.model, ctx.dscene.struct, ctx.pos.data_ptr(), ctx.alb.data_ptr(),
+                  fac.data_ptr(), int(fac.dtype == torch.float64), fac.shape[1], p, out.data_ptr(),
+                  _lib.stream_ptr())
+        return out
+    vis = cache.infer(ctx.positions)
+    out.copy_(torch.from_numpy(ctx.unshadowed_rgb(np.asarray(vis, np.float64))))
+    return out
+
+
+def neural_di_batch(ctx: PixelCtx, cache) -> np.ndarray:
+    """Biased shading: predicted visibility times analytic radiance (sampling.py:215-218)."""
+    return neural_di_device(ctx, cache).cpu().numpy()
+
+
+def neural_di_shade(sp: ShadingPoint, cache, scene) -> np.ndarray:
+    return neural_di_batch(_ctx_for(sp, scene), cache)[0]
