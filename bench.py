@@ -1,0 +1,373 @@
+"""Benchmark: one online NVC frame at 1080p x 32 lights (BASELINE.json configs[1]).
+
+A step = one online frame, in the reference's order (render.py:297-324):
+  1. training batch on the GPU: 4096 world + 4096 screen samples, 8192 x 32
+     FP64 shadow-ray labels (training.py:166-199);
+  2. one train step: encode -> MLP fwd/bwd -> fixed-point hash-grid scatter
+     -> fused dense Adam over all 16.8 M parameters (cache.py:60-73);
+  3. full-screen NLS query on the 1920x1080 G-buffer: fused hash-grid encode
+     -> tcgen05 MLP 32-64-64-64-32 -> clamp * lum -> FP64 WRS with numpy
+     Philox -> light point (sampling.py:184-205).
+Inputs (G-buffer, per-camera light-major lum table) are built once before
+timing, as the reference memoizes them per camera (render.py:128-142).
+
+`value` = visibility queries/s (all pixels, whole job) with inputs resident in
+HBM; `e2e` = the same through the public device API with the G-buffer
+positions copied H2D from pinned memory and (ids, points, W, loss) copied
+back D2H every frame.  N > 1 (torchrun): weak scaling -- every rank renders its
+own 1080p tile of an N-tile frame (global pixel ids keep the RNG draws
+distinct) and trains data-parallel on its 8192-row shard of an 8192*N-row
+global batch, with one NCCL allreduce of the fixed-point gradients per step.
+
+`--impl reference` times the CPU oracle port of the reference (oracle/) on the
+host cores with the same workload definition (bounded sample, extrapolated).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WIDTH, HEIGHT, K = 1920, 1080, 32
+LEVELS, TABLE, FEATS, HIDDEN = 16, 1 << 19, 2, (64, 64, 64)
+N_WORLD = N_SCREEN = 4096
+METRIC = "visibility queries/s (encode+MLP+WRS) at 1080p x 32 lights; train samples/s"
+UNIT = "queries/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the oracle port of the reference (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------
+
+def _oracle_query_chunk(args):
+    """Encode+MLP+WRS for a pixel chunk on one host core (oracle restatement)."""
+    from oracle import vc_oracle as O
+    state, pos, lum, key, p_first, p_total = args
+    sa, cache = state
+    vis = cache.infer(pos)
+    return O.nls_sample(sa, vis, lum, key, p_total=p_total, p_first=p_first)
+
+
+def cpu_reference(sample_pixels: int = 24576, procs: int | None = None, repeats: int = 1) -> dict:
+    """Oracle port timed on the host: one full 8192-sample train step (batch
+    generation + step) plus NLS on `sample_pixels` pixels of the 1080p frame;
+    frame time extrapolates the query linearly to all pixels."""
+    import multiprocessing as mp
+
+    from oracle import vc_oracle as O
+    from paper_2506_05930_b200.scene import scene_from_dict
+    from paper_2506_05930_b200.scenes import boxes_scene
+
+    procs = procs or os.cpu_count() or 1
+    s = scene_from_dict(boxes_scene(32))
+    cam = np.array([*s.camera.position, *s.camera.look_at, *s.camera.up, s.camera.fov_deg, WIDTH, HEIGHT], float)
+    sa = O.SceneArrays(s.triangles_v0, s.triangles_v1, s.triangles_v2, s.tri_material, s.tri_light, s.lt_kind,
+                       s.lt_verts, s.lt_normal, s.lt_radiance, s.mat_albedo, cam)
+    grid = O.Grid(levels=LEVELS, features_per_level=FEATS, table_size=TABLE, aabb_min=s.aabb_min,
+                  aabb_max=s.aabb_max)
+    cache = O.Cache(grid, K, hidden=HIDDEN, seed=0)
+    # G-buffer sample: evenly strided pixels of the 1080p frame (memoized per camera, untimed)
+    p_total = WIDTH * HEIGHT
+    pix = np.linspace(0, p_total - 1, sample_pixels).astype(np.int64)
+    jit = O.uniform_at(O.stream_key("primary"), np.stack([2 * pix, 2 * pix + 1], 1))
+    ys, xs = np.divmod(pix, WIDTH)
+    o, d = sa.camera_rays(xs + jit[:, 0], ys + jit[:, 1])
+    gb = sa.trace(o, d)
+    lum = sa.lum(sa.factors(gb["position"], gb["normal"]), gb["albedo"])
+    key = O.stream_key(0, 0, "light-select")
+    best_train, best_query = float("inf"), float("inf")
+    chunks = np.array_split(np.arange(sample_pixels), procs)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        pool.map(_oracle_query_chunk, [((sa, cache), gb["position"][c[:8]], lum[c[:8]], key, 0, p_total)
+                                       for c in chunks if c.size])   # warm-up (fork + numpy)
+        for rep in range(repeats):
+            t0 = time.perf_counter()
+            pos, tgt = O.train_batch(sa, 0, rep)
+            cache.train_step(pos, tgt)
+            t1 = time.perf_counter()
+            pool.map(_oracle_query_chunk, [((sa, cache), gb["position"][c], lum[c], key, int(c[0]), p_total)
+                                           for c in chunks if c.size])
+            t2 = time.perf_counter()
+            best_train, best_query = min(best_train, t1 - t0), min(best_query, t2 - t1)
+    frame_s = best_train + best_query * (p_total / sample_pixels)
+    return {"value": p_total / frame_s, "unit": UNIT, "cores": procs, "kind": "port",
+            "sample": (f"oracle port (numpy + serial C geometry) on host: 1 full train step "
+                       f"(8192 samples, {best_train:.2f} s, 1 process) + NLS on {sample_pixels} strided "
+                       f"pixels of the 1080p frame ({best_query:.2f} s over {procs} processes), query "
+                       f"extrapolated x{p_total / sample_pixels:.1f}; frame {frame_s:.1f} s"),
+            "train_samples_per_s": (N_WORLD + N_SCREEN) / frame_s, "frame_s": frame_s}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def gpu_arm(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_05930_b200 import MODE_LIGHTS, HashGridConfig, TrainFrameConfig, VisibilityCache
+    from paper_2506_05930_b200 import rng as R
+    from paper_2506_05930_b200.render import gbuffer_device
+    from paper_2506_05930_b200.sampling import PixelCtx, nls_sample_device
+    from paper_2506_05930_b200.scene import scene_from_dict
+    from paper_2506_05930_b200.scenes import boxes_scene
+    from paper_2506_05930_b200.training import BatchBuffers, train_frame_device
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    scene = scene_from_dict(boxes_scene(32))
+    cam = scene.camera.resized(WIDTH, HEIGHT * world)      # N tiles of 1080 rows
+    P = WIDTH * HEIGHT
+    p_first, p_total = rank * P, P * world
+    pos, nrm, alb, hit, _ = gbuffer_device(scene, cam, p_first, P)
+    ctx = PixelCtx(scene, pos, nrm, alb)
+    ctx.lum_device()
+    grid = HashGridConfig(levels=LEVELS, table_size=TABLE, features_per_level=FEATS, aabb_min=scene.aabb_min,
+                          aabb_max=scene.aabb_max)
+    cache = VisibilityCache(MODE_LIGHTS, K, grid, seed=0, hidden_dims=HIDDEN, device=dev)
+    cfg = TrainFrameConfig(n_world=N_WORLD * world, n_screen=N_SCREEN * world, seed=0)
+    bufs = BatchBuffers(cfg.n_world, cfg.n_screen, K, dev, world)
+    out = (torch.empty(P, dtype=torch.int64, device=dev), torch.empty((P, 3), dtype=torch.float64, device=dev),
+           torch.empty(P, dtype=torch.float64, device=dev))
+
+    def comm(grad_fx, loss):
+        dist.all_reduce(grad_fx)
+        dist.all_reduce(loss)
+
+    stream = torch.cuda.current_stream()
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+
+    def frame(f, timed_parts=None):
+        if timed_parts is not None:
+            marks[0].record(stream)
+        loss, _ = train_frame_device(scene, cam, cache, cfg, frame=f, bufs=bufs, shard=rank,
+                                     n_shards=world, comm=comm if world > 1 else None)
+        if timed_parts is not None:
+            marks[1].record(stream)
+        nls_sample_device(ctx, cache, R.stream_key(0, f, "light-select"), 0, p_first=p_first, p_total=p_total,
+                          out=out)
+        if timed_parts is not None:
+            marks[2].record(stream)
+        return loss
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warm-up (also validates the batch never shrinks) ----
+    for f in range(args.warmup):
+        frame(f)
+    barrier()
+    assert int(bufs.n_rows.item()) == cfg.n_world + cfg.n_screen, "screen rays missed: batch shrank"
+
+    # ---- per-stage split (separate pass, events between stages) ----
+    split_train, split_query = [], []
+    for f in range(min(args.steps, 10)):
+        frame(1000 + f, timed_parts=True)
+        marks[2].synchronize()
+        split_train.append(marks[0].elapsed_time(marks[1]))
+        split_query.append(marks[1].elapsed_time(marks[2]))
+
+    # ---- timed region: K frames, inputs resident ----
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for f in range(args.steps):
+            loss = frame(args.warmup + f)
+        end.record(stream)
+        barrier()
+    ms = start.elapsed_time(end) / args.steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+
+    # ---- e2e: host G-buffer positions in, (ids, points, W, loss) out ----
+    pos_host = pos.cpu().pin_memory()
+    outs_host = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in out]
+    loss_host = torch.empty(1, dtype=torch.float64, pin_memory=True)
+    e2e_steps = max(3, min(args.steps, 20))
+    barrier()
+    start.record(stream)
+    for f in range(e2e_steps):
+        ctx.pos.copy_(pos_host, non_blocking=True)
+        loss = frame(5000 + f)
+        for h, d in zip(outs_host, out):
+            h.copy_(d, non_blocking=True)
+        loss_host.copy_(loss.reshape(1), non_blocking=True)
+    end.record(stream)
+    barrier()
+    e2e_ms = start.elapsed_time(end) / e2e_steps
+    t = torch.tensor([e2e_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+
+    if rank == 0:
+        hbm, tflops, src = peaks()
+        q_ms = statistics.median(split_query)
+        tr_ms = statistics.median(split_train)
+        # dominant kernel: the fused query (k_query).  Algorithmic HBM bytes per
+        # pixel: pos 24 + lum 32*4 + ids 8 + point 24 + W 8 = 192 B.
+        q_bytes = P * (24 + K * 4 + 8 + 24 + 8)
+        achieved = q_bytes / (q_ms * 1e-3) / 1e9
+        gather_gbs = P * LEVELS * 8 * FEATS * 2 / (q_ms * 1e-3) / 1e9
+        mlp_tflops = P * 2 * (32 * 64 + 64 * 64 * 2 + 64 * 32) / (q_ms * 1e-3) / 1e12
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "query_dram_bytes.json")
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get("bytes_per_launch")
+            except Exception:
+                traffic = None
+        clk = clocks.summary()
+        line = {
+            "metric": METRIC, "value": P * world / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp16 MLP / fp64 index+WRS / fp32 train",
+            "data": "synthetic (boxes_scene(32) fixture, random-init weights, seed 0)",
+            "config": {"workload": f"C2: {WIDTH}x{HEIGHT * world} boxes32 (K=32), L=16 T=2^19 F=2, MLP 3x64, "
+                                   f"1 online frame = train batch {(N_WORLD + N_SCREEN) * world} + NLS over all pixels",
+                       "train_samples_per_s": (N_WORLD + N_SCREEN) * world / (ms * 1e-3),
+                       "pixels_per_gpu": P, "global_batch": (N_WORLD + N_SCREEN) * world,
+                       "parallelism": f"dp{world} (train) + {world} screen tiles (query)",
+                       "l2": "inputs > L2 every frame (lum table 265 MB + G-buffer positions 50 MB streamed); "
+                             "fp16 hash table (33.6 MB) L2-resident by design",
+                       "stage_ms": {"train_frame": tr_ms, "query": q_ms}},
+            "e2e": {"value": P * world / (e2e_ms * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": int(pos_host.numel() * 8),
+                    "d2h_bytes_per_step": int(sum(h.numel() * h.element_size() for h in outs_host) + 8)},
+            "gpu_launches": 9 * args.steps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic, "kernel": "k_query (fused NLS)",
+                         "peak_source": src, "algorithmic_bytes_per_launch": q_bytes,
+                         "l2_gather_payload_gbs": gather_gbs, "mlp_tflops": mlp_tflops,
+                         "mlp_frac_of_bf16_peak": mlp_tflops / tflops},
+            "clocks": clk,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_reference(sample_pixels=args.cpu_sample)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def reference_arm(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps = []
+    cb = None
+    for _ in range(max(1, args.steps if args.steps <= 3 else 3)):
+        cb = cpu_reference(sample_pixels=args.cpu_sample)
+        steps.append(cb["frame_s"])
+    frame_s = min(steps)
+    value = WIDTH * HEIGHT / frame_s
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+            "steps": len(steps), "warmup": 1, "ms_per_step": frame_s * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 MLP / f64 index+WRS (numpy)",
+            "data": "synthetic (boxes_scene(32) fixture, random-init weights, seed 0)",
+            "config": {"workload": f"C2: {WIDTH}x{HEIGHT} boxes32 (K=32), L=16 T=2^19 F=2, MLP 3x64, "
+                                   "1 online frame = train batch 8192 + NLS over all pixels",
+                       "train_samples_per_s": (N_WORLD + N_SCREEN) / frame_s},
+            "impl": "reference",
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-sample", type=int, default=24576)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

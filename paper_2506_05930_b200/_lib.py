@@ -96,6 +96,10 @@ class NvcError(RuntimeError):
     pass
 
 
+class NvcUnsupported(NvcError):
+    """A valid configuration the requested kernel does not cover (NVC_ERR_UNSUPPORTED)."""
+
+
 def load(path: str | None = None) -> ctypes.CDLL:
     """Load libnvc.so (raises ImportError if it was never built)."""
     global _lib
@@ -124,6 +128,8 @@ def call(name: str, *args) -> None:
         msg = lib.nvc_last_error().decode(errors="replace")
         if rc == -1:
             raise ValueError(f"{name}: {msg}")
+        if rc == -3:
+            raise NvcUnsupported(f"{name}: {msg}")
         raise NvcError(f"{name} failed ({rc}): {msg}")
 
 

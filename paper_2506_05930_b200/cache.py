@@ -197,10 +197,10 @@ class VisibilityCache:
         prec = self.precision if precision is None else precision
         try:
             _lib.call("nvc_infer", self.model, pos.data_ptr(), n, prec, out.data_ptr(), _lib.stream_ptr())
-        except _lib.NvcError:
+        except _lib.NvcUnsupported:
             if prec != PRECISION_FP16:
                 raise
-            # topology the tcgen05 kernel does not cover: use the fp32 CUDA path
+            # topology the tcgen05 kernel does not cover (smem/width limits): fp32 CUDA path
             _lib.call("nvc_infer", self.model, pos.data_ptr(), n, PRECISION_FP32, out.data_ptr(),
                       _lib.stream_ptr())
         return out

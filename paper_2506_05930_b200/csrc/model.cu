@@ -518,8 +518,8 @@ int nvc_encode(const nvc_model* m, const double* pos, int64_t n, float* feats, i
                void* stream) {
     int rc = validate(m);
     if (rc) return rc;
-    NVC_REQUIRE(pos && feats, "nvc_encode: null argument");
     if (n <= 0) return NVC_OK;
+    NVC_REQUIRE(pos && feats, "nvc_encode: null argument");
     GridDev g = grid_of(m);
     k_encode<<<grid1(n * g.L, 128), 128, 0, (cudaStream_t)stream>>>(g, m->params, pos, n, feats, idx_out, w_out);
     return check_launch("k_encode");

@@ -527,8 +527,8 @@ using namespace nvc;
 extern "C" {
 
 int nvc_infer(const nvc_model* m, const double* pos, int64_t n, int32_t precision, float* out, void* stream) {
-    NVC_REQUIRE(m && pos && out, "nvc_infer: null argument");
     if (n <= 0) return NVC_OK;
+    NVC_REQUIRE(m && pos && out, "nvc_infer: null argument");
     if (precision == 0) return nvc_infer_f32(m, pos, n, out, (cudaStream_t)stream);
     QOut o;
     memset(&o, 0, sizeof o);

@@ -1,0 +1,388 @@
+"""GPU parity: every CUDA entry point against the oracle and the reference's
+golden vectors.  Bit-exact where the reference is integer/index work or
+FP64 with a pinned op order; explicit tolerances otherwise (stated inline)."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import vc_oracle as O  # noqa: E402
+from paper_2506_05930_b200 import (PRECISION_FP16, PRECISION_FP32, HashGridConfig,  # noqa: E402
+                                   MODE_LIGHTS, PixelCtx, VisibilityCache, make_gbuffer,
+                                   nls_sample_batch, neural_di_batch, scene_from_dict, train_frame,
+                                   TrainFrameConfig, wrs_select_batch)
+from paper_2506_05930_b200 import rng as R  # noqa: E402
+from paper_2506_05930_b200 import _lib  # noqa: E402
+from paper_2506_05930_b200.scenes import boxes_point_scene, boxes_scene  # noqa: E402
+from paper_2506_05930_b200.training import (compute_visibility_targets, gen_screen_samples,  # noqa: E402
+                                            gen_world_samples)
+
+DEV = torch.device("cuda", 0)
+FP16_VIS_TOL = 4e-3     # fp16 table + fp16 weights/activations, fp32 accumulate
+
+
+@pytest.fixture(scope="module")
+def boxes32():
+    return scene_from_dict(boxes_scene(32))
+
+
+@pytest.fixture(scope="module")
+def boxes8():
+    return scene_from_dict(boxes_scene(8))
+
+
+@pytest.fixture(scope="module")
+def pbox8():
+    return scene_from_dict(boxes_point_scene(8))
+
+
+def grid_cfg(scene, levels, tsize):
+    return HashGridConfig(levels=levels, table_size=tsize, features_per_level=2,
+                          aabb_min=scene.aabb_min, aabb_max=scene.aabb_max)
+
+
+# ---------------------------------------------------------------------------
+# RNG + WRS
+# ---------------------------------------------------------------------------
+class TestWrs:
+    def test_wrs_bit_exact_vs_reference(self, g_samp):
+        rs = R.stream(0, 4, "light-select")
+        idx, wsel, wsum = wrs_select_batch(g_samp["wrs_w"], rs)
+        np.testing.assert_array_equal(idx, g_samp["wrs_idx"])
+        np.testing.assert_array_equal(wsel, g_samp["wrs_wsel"])
+        np.testing.assert_array_equal(wsum, g_samp["wrs_wsum"])
+        idx2, _, _ = wrs_select_batch(g_samp["wrs_w"][:17], rs)       # stream continues
+        np.testing.assert_array_equal(idx2, g_samp["wrs_idx2"])
+
+    @pytest.mark.parametrize("k,offset", [(1, 0), (3, 5), (32, 1), (128, 7), (7, 2**33 + 3)])
+    def test_wrs_matches_oracle_any_offset(self, k, offset):
+        g = np.random.default_rng(k)
+        w = g.random((999, k)) * (g.random((999, k)) < 0.5)
+        key = R.stream_key(9, k, "light-select")
+        idx, wsel, wsum = wrs_select_batch(w, R.Stream(key=key, offset=offset))
+        oi, ow, os_ = O.wrs_select(w, key, offset)
+        np.testing.assert_array_equal(idx, oi)
+        np.testing.assert_array_equal(wsel, ow)
+        np.testing.assert_array_equal(wsum, os_)
+
+
+# ---------------------------------------------------------------------------
+# encoder
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("tag,levels,tsize,seed", [("hc1", 8, 1 << 14, 0), ("hc2", 16, 1 << 19, 1)])
+def test_encoder_bit_exact(g_hash, boxes32, tag, levels, tsize, seed):
+    c = VisibilityCache(MODE_LIGHTS, 4, grid_cfg(boxes32, levels, tsize), seed=seed)
+    feats, idx, w = c.encode(g_hash[tag + "_pos"], with_ctx=True)
+    np.testing.assert_array_equal(idx, g_hash[tag + "_idx"])
+    np.testing.assert_array_equal(w, g_hash[tag + "_w"])
+    np.testing.assert_array_equal(feats, g_hash[tag + "_feats"])
+
+
+# ---------------------------------------------------------------------------
+# inference: fp32 SIMT parity path and the tcgen05 fused path
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("levels,tsize,hidden,k,f", [(8, 1 << 14, (64, 64), 8, 2), (16, 1 << 19, (64, 64, 64), 32, 2),
+                                                     (4, 1 << 10, (32, 32), 1, 2),
+                                                     (16, 1 << 19, (128, 128, 128), 128, 2),
+                                                     (10, 1 << 14, (32, 32), 5, 4), (3, 1 << 8, (24, 40), 3, 1)])
+def test_infer_vs_oracle(boxes32, levels, tsize, hidden, k, f):
+    cfg = HashGridConfig(levels=levels, table_size=tsize, features_per_level=f,
+                         aabb_min=boxes32.aabb_min, aabb_max=boxes32.aabb_max)
+    c = VisibilityCache(MODE_LIGHTS, k, cfg, seed=3, hidden_dims=hidden)
+    oc = O.Cache(O.Grid(levels=levels, features_per_level=f, table_size=tsize, aabb_min=boxes32.aabb_min,
+                        aabb_max=boxes32.aabb_max), k, hidden=hidden, seed=3)
+    np.testing.assert_array_equal(c.grid_params, oc.table)
+    pos = np.random.default_rng(1).uniform(boxes32.aabb_min - 0.1, boxes32.aabb_max + 0.1, (3001, 3))
+    want = oc.infer(pos)
+    got32 = c.infer(pos, precision=PRECISION_FP32)
+    np.testing.assert_allclose(got32, want, rtol=0, atol=1e-6)
+    got16 = c.infer(pos, precision=PRECISION_FP16)
+    assert np.abs(got16 - want).max() < FP16_VIS_TOL
+
+
+def test_infer_trained_weights_fp16(boxes32):
+    """fp16 tolerance also holds away from init (trained-scale weights)."""
+    cfg = grid_cfg(boxes32, 16, 1 << 19)
+    c = VisibilityCache(MODE_LIGHTS, 32, cfg, seed=0, hidden_dims=(64, 64, 64))
+    g = np.random.default_rng(2)
+    table = (g.standard_normal(c.grid_params.shape) * 0.3).astype(np.float32)
+    c.grid_params = table
+    pos = g.uniform(boxes32.aabb_min, boxes32.aabb_max, (2048, 3))
+    a, b = c.infer(pos, precision=PRECISION_FP32), c.infer(pos, precision=PRECISION_FP16)
+    assert np.abs(a - b).max() < 2e-2 and np.abs(a - b).mean() < 2e-3
+
+
+def test_infer_rejects_nonfinite(boxes32):
+    c = VisibilityCache(MODE_LIGHTS, 4, grid_cfg(boxes32, 4, 1 << 10))
+    with pytest.raises(ValueError):
+        c.infer(np.array([[0.0, np.nan, 0.0]]))
+
+
+def test_infer_empty_and_ragged(boxes32):
+    c = VisibilityCache(MODE_LIGHTS, 8, grid_cfg(boxes32, 8, 1 << 14), hidden_dims=(64, 64))
+    assert c.infer(np.zeros((0, 3))).shape == (0, 8)
+    for n in (1, 127, 129, 1000):
+        pos = np.random.default_rng(n).uniform(-1, 1, (n, 3))
+        np.testing.assert_allclose(c.infer(pos), c.infer(pos, precision=PRECISION_FP32), atol=FP16_VIS_TOL)
+
+
+# ---------------------------------------------------------------------------
+# geometry: G-buffer, factors, screen samples, targets
+# ---------------------------------------------------------------------------
+class TestGeometry:
+    def test_gbuffer_bit_exact(self, boxes32, g_samp):
+        cam = boxes32.camera.resized(40, 24)
+        gb = make_gbuffer(boxes32, cam)
+        np.testing.assert_array_equal(gb.flat("hit"), g_samp["gb_hit"])
+        np.testing.assert_array_equal(gb.flat("position"), g_samp["gb_position"])
+        np.testing.assert_array_equal(gb.flat("normal"), g_samp["gb_normal"])
+        np.testing.assert_array_equal(gb.flat("albedo"), g_samp["gb_albedo"])
+        np.testing.assert_array_equal(gb.flat("light_id"), g_samp["gb_light_id"])
+
+    def test_point_gbuffer_and_factors(self, pbox8, g_samp):
+        gb = make_gbuffer(pbox8)
+        np.testing.assert_array_equal(gb.flat("position"), g_samp["pgb_position"])
+        ctx = PixelCtx(pbox8, gb.flat("position"), gb.flat("normal"), gb.flat("albedo"), table_dtype=np.float64)
+        np.testing.assert_allclose(ctx.factor_matrix(), g_samp["pgb_factor"], rtol=1e-12, atol=0)
+
+    def test_rect_factors_and_lum(self, boxes32, g_samp):
+        ctx = PixelCtx(boxes32, g_samp["gb_position"], g_samp["gb_normal"], g_samp["gb_albedo"],
+                       table_dtype=np.float64)
+        np.testing.assert_allclose(ctx.factor_matrix(), g_samp["nls_factor"], rtol=1e-10, atol=1e-300)
+        np.testing.assert_allclose(ctx.lum_matrix(), g_samp["nls_lum"], rtol=1e-10, atol=1e-300)
+        c32 = PixelCtx(boxes32, g_samp["gb_position"], g_samp["gb_normal"], g_samp["gb_albedo"])
+        np.testing.assert_allclose(c32.lum_matrix(), g_samp["nls_lum"], rtol=1e-6, atol=1e-30)
+
+    def test_screen_samples_bit_exact(self, boxes8, g_train):
+        got = gen_screen_samples(boxes8, boxes8.camera, 256, R.stream(6))
+        np.testing.assert_array_equal(got, g_train["screen_boxes8_256"])
+
+    def test_screen_samples_all_miss(self):
+        from paper_2506_05930_b200.scene import scene_from_dict as sfd
+        s = sfd({"camera": {"position": [0, 0, 3], "look_at": [0, 0, 4], "up": [0, 1, 0], "fov_deg": 40.0,
+                            "width": 16, "height": 16},
+                 "materials": [{"albedo": [0.5, 0.5, 0.5]}],
+                 "meshes": [{"material": 0, "triangles": [[[-1, 0, -1], [1, 0, -1], [1, 0, 1]]]}],
+                 "lights": [{"type": "point", "position": [0, 2, 0], "intensity": [1, 1, 1]}]})
+        assert gen_screen_samples(s, s.camera, 64, R.stream(5)).shape == (0, 3)
+
+    def test_c1_train_batch_bit_exact(self, pbox8, g_train):
+        key = (0, 0, 0)
+        world = gen_world_samples(pbox8, 4096, R.stream(*key, R.WORLD_SAMPLES))
+        screen = gen_screen_samples(pbox8, pbox8.camera, 4096, R.stream(*key, R.SCREEN_SAMPLES))
+        pos = np.concatenate([world, screen])
+        np.testing.assert_array_equal(pos, g_train["c1_pos"])
+        tgt = compute_visibility_targets(pos, pbox8, R.stream(*key, R.TARGETS))
+        np.testing.assert_array_equal(tgt.astype(np.uint8), g_train["c1_tgt"])
+
+    @pytest.mark.parametrize("shards", [1, 2, 3])
+    def test_boxes32_device_batch_bit_exact(self, boxes32, g_train, shards):
+        from paper_2506_05930_b200.training import BatchBuffers, gen_batch_device
+        pos_all, tgt_all = [], []
+        for sh in range(shards):
+            bufs = BatchBuffers(2048, 2048, 32, DEV, shards)
+            gen_batch_device(boxes32, boxes32.camera, bufs, 0, 3, 0, sh, shards)
+            b = int(bufs.n_rows.item())
+            lo, hi = b * sh // shards, b * (sh + 1) // shards
+            pos_all.append(bufs.pos[:b].cpu().numpy())
+            tgt_all.append(bufs.tgt[:hi - lo].cpu().numpy())
+        np.testing.assert_array_equal(pos_all[0], g_train["b32_pos"])
+        np.testing.assert_array_equal(np.concatenate(tgt_all).astype(np.uint8), g_train["b32_tgt"])
+
+
+# ---------------------------------------------------------------------------
+# light selection: NLS / Neural DI
+# ---------------------------------------------------------------------------
+class FixedCache:
+    mode = MODE_LIGHTS
+
+    def __init__(self, vis):
+        self.vis = np.asarray(vis, np.float32)
+        self.output_dim = self.vis.shape[1]
+
+    def infer(self, positions):
+        return self.vis[: positions.shape[0]]
+
+
+class TestSampling:
+    def test_nls_bit_exact_vs_reference(self, boxes32, g_samp):
+        ctx = PixelCtx(boxes32, g_samp["gb_position"], g_samp["gb_normal"], g_samp["gb_albedo"],
+                       factors=g_samp["nls_factor"], table_dtype=np.float64)
+        ctx._lum = torch.from_numpy(np.ascontiguousarray(g_samp["nls_lum"].T)).to(DEV)
+        ids, pts, big_w = nls_sample_batch(ctx, FixedCache(g_samp["nls_vis"]), R.stream(0, 7, "light-select"))
+        np.testing.assert_array_equal(ids, g_samp["nls_ids"])
+        np.testing.assert_array_equal(pts, g_samp["nls_pts"])
+        np.testing.assert_array_equal(big_w, g_samp["nls_W"])
+        ids, _, big_w = nls_sample_batch(ctx, FixedCache(g_samp["nls_vis"]), R.stream(0, 7, "light-select"), 0.0)
+        np.testing.assert_array_equal(ids, g_samp["nls_ids_biased"])
+        np.testing.assert_array_equal(big_w, g_samp["nls_W_biased"])
+
+    def test_fused_nls_equals_oracle_on_same_visibility(self, boxes32, g_samp, g_scenes):
+        """The fused kernel's WRS is bit-exact given its own (fp16-MLP) visibilities."""
+        c = VisibilityCache(MODE_LIGHTS, 32, grid_cfg(boxes32, 16, 1 << 19), hidden_dims=(64, 64, 64))
+        c.grid_params = (np.random.default_rng(0).standard_normal(c.grid_params.shape) * 0.5).astype(np.float32)
+        ctx = PixelCtx(boxes32, g_samp["gb_position"], g_samp["gb_normal"], g_samp["gb_albedo"])
+        vis16 = c.infer(g_samp["gb_position"], precision=PRECISION_FP16)
+        lum = ctx.lum_matrix()          # f32 table widened to f64, as the kernel does
+        sc = O.SceneArrays.from_golden(g_scenes, "boxes32_")
+        key = R.stream_key(0, 9, "light-select")
+        oi, op, ow = O.nls_sample(sc, vis16, lum, key)
+        ids, pts, big_w = nls_sample_batch(ctx, c, R.Stream(key=key))
+        np.testing.assert_array_equal(ids, oi)
+        np.testing.assert_array_equal(pts, op)
+        np.testing.assert_array_equal(big_w, ow)
+        assert (ids >= 0).sum() > 100
+
+    def test_tile_sharded_nls_matches_whole_frame(self, boxes32, g_samp):
+        from paper_2506_05930_b200.sampling import nls_sample_device
+        c = VisibilityCache(MODE_LIGHTS, 32, grid_cfg(boxes32, 16, 1 << 19), hidden_dims=(64, 64, 64))
+        pos, nrm, alb = g_samp["gb_position"], g_samp["gb_normal"], g_samp["gb_albedo"]
+        key = R.stream_key(0, 11, "light-select")
+        whole = PixelCtx(boxes32, pos, nrm, alb)
+        wi, wp, ww = (t.cpu().numpy() for t in nls_sample_device(whole, c, key))
+        cuts = [0, 333, 640, pos.shape[0]]
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            part = PixelCtx(boxes32, pos[a:b], nrm[a:b], alb[a:b])
+            si, sp, sw = (t.cpu().numpy() for t in nls_sample_device(part, c, key, p_first=a,
+                                                                     p_total=pos.shape[0]))
+            np.testing.assert_array_equal(si, wi[a:b])
+            np.testing.assert_array_equal(sp, wp[a:b])
+            np.testing.assert_array_equal(sw, ww[a:b])
+
+    def test_neural_di(self, boxes32, g_samp):
+        ctx = PixelCtx(boxes32, g_samp["gb_position"], g_samp["gb_normal"], g_samp["gb_albedo"],
+                       table_dtype=np.float64)
+        got = neural_di_batch(ctx, FixedCache(g_samp["nls_vis"]))
+        np.testing.assert_allclose(got, g_samp["ndi_rgb"], rtol=1e-9, atol=1e-12)
+        c = VisibilityCache(MODE_LIGHTS, 32, grid_cfg(boxes32, 16, 1 << 19), hidden_dims=(64, 64, 64))
+        vis16 = c.infer(g_samp["gb_position"])
+        want = ((vis16.astype(np.float64) * ctx.factor_matrix()) @ boxes32.lt_radiance) * g_samp["gb_albedo"] / np.pi
+        np.testing.assert_allclose(neural_di_batch(ctx, c), want, rtol=1e-9, atol=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# training: Adam, one step, loss curve, determinism, shard equivalence
+# ---------------------------------------------------------------------------
+class TestTraining:
+    def _c1(self, pbox8, seed=0):
+        return VisibilityCache(MODE_LIGHTS, 8, grid_cfg(pbox8, 8, 1 << 14), seed=seed, hidden_dims=(64, 64))
+
+    def test_adam_bit_exact_given_grads(self, pbox8):
+        c = self._c1(pbox8)
+        p0 = c.params.cpu().numpy().copy()
+        g = np.random.default_rng(5)
+        st = O.Adam(p0.size)
+        p = p0.copy()
+        for t in range(3):
+            gd = (g.standard_normal(p0.size) * 10.0 ** g.integers(-7, 0, p0.size))
+            fx = np.rint(gd * 2.0 ** 48).astype(np.int64)
+            gf = (fx.astype(np.float64) * 2.0 ** -48).astype(np.float32)   # what the kernel reads
+            c.grad_fx.copy_(torch.from_numpy(fx))
+            c.next_epoch()
+            lr = 0.05 - 0.001 * t
+            c.step = 0
+            c.train_cfg.lr_start = lr
+            c.train_cfg.lr_end = min(lr, c.train_cfg.lr_end)
+            c.apply_adam(dense_grad=True)
+            st.step(p, gf, lr)
+            np.testing.assert_array_equal(c.params.cpu().numpy(), p)
+        np.testing.assert_array_equal(c.adam_m.cpu().numpy(), st.m)
+        np.testing.assert_array_equal(c.adam_v.cpu().numpy(), st.v)
+        assert not c.grad_fx.any()
+        np.testing.assert_array_equal(c.table_h.cpu().numpy(), p[:c.grid_cfg.param_count].astype(np.float16))
+
+    def test_touched_map_adam_equals_dense(self, pbox8, g_train):
+        a, b = self._c1(pbox8), self._c1(pbox8)
+        pos, tgt = g_train["c1_pos"], g_train["c1_tgt"].astype(np.float32)
+        for c, dense in ((a, False), (b, True)):
+            pt = torch.from_numpy(pos).to(DEV)
+            tt = torch.from_numpy(tgt).to(DEV)
+            c.next_epoch()
+            c.accumulate_grads(pt, tt)
+            c.apply_adam(dense_grad=dense)
+        np.testing.assert_array_equal(a.params.cpu().numpy(), b.params.cpu().numpy())
+
+    def test_first_step_vs_reference(self, pbox8, g_train):
+        c = self._c1(pbox8)
+        loss = c.train_step(g_train["c1_pos"], g_train["c1_tgt"].astype(np.float32))
+        assert loss == pytest.approx(float(g_train["c1_step0_loss"]), rel=1e-6)
+        np.testing.assert_allclose(c.net_params.weights[0], g_train["c1_step0_w0"], atol=2e-6)
+
+    def test_loss_curve_vs_reference(self, pbox8, g_train):
+        c = self._c1(pbox8)
+        want = g_train["c1_loss_f32"]
+        got = [train_frame(pbox8, pbox8.camera, c, TrainFrameConfig(), frame=f) for f in range(len(want))]
+        np.testing.assert_allclose(got, want, rtol=1e-2)      # FP32 vs reference FP32; SURVEY §8(c) band
+        ref64 = g_train["c1_loss_f64"]
+        assert np.max(np.abs(np.array(got) - ref64) / ref64) < 1e-2
+
+    def test_bitwise_deterministic_trajectory(self, pbox8):
+        def run():
+            c = self._c1(pbox8, seed=5)
+            cfg = TrainFrameConfig(n_world=512, n_screen=512, seed=5)
+            return [train_frame(pbox8, pbox8.camera, c, cfg, frame=f) for f in range(3)], c.params.cpu().numpy()
+        la, pa = run()
+        lb, pb = run()
+        assert la == lb
+        np.testing.assert_array_equal(pa, pb)
+
+    def test_reference_determinism_config_loss(self, g_train):
+        """levels=4, T=2^10, 64+64 batch, seed 5 (test_mlp.py:205-224): loss within 1e-4."""
+        pen = {
+            "camera": {"position": [0, 1.6, 3.2], "look_at": [0, 0, 0], "up": [0, 1, 0],
+                       "fov_deg": 55.0, "width": 96, "height": 54},
+            "materials": [{"albedo": [0.7, 0.7, 0.7]}, {"albedo": [0.5, 0.3, 0.3]}],
+            "meshes": [{"material": 0, "triangles": [[[-4, 0, -4], [4, 0, -4], [4, 0, 4]],
+                                                     [[-4, 0, -4], [4, 0, 4], [-4, 0, 4]]]},
+                       {"material": 1, "triangles": [[[-.5, 1, -.5], [.5, 1, -.5], [.5, 1, .5]],
+                                                     [[-.5, 1, -.5], [.5, 1, .5], [-.5, 1, .5]]]}],
+            "lights": [{"type": "rect", "corner": [-0.4, 2.0, -0.4], "edge_u": [0.8, 0, 0],
+                        "edge_v": [0, 0, 0.8], "radiance": [10.0, 10.0, 10.0]}],
+        }
+        ps = scene_from_dict(pen)
+        c = VisibilityCache(MODE_LIGHTS, 1, HashGridConfig(levels=4, table_size=1 << 10, aabb_min=ps.aabb_min,
+                                                           aabb_max=ps.aabb_max), seed=5)
+        cfg = TrainFrameConfig(n_world=64, n_screen=64, seed=5)
+        got = [train_frame(ps, ps.camera, c, cfg, frame=f) for f in range(3)]
+        np.testing.assert_allclose(got, g_train["pen_loss"], rtol=1e-4)
+
+    def test_sharded_grid_gradient_equals_full_batch(self, pbox8, g_train):
+        """Fixed-point grid gradients: sum over row shards == full batch, bit for bit."""
+        pos = torch.from_numpy(g_train["c1_pos"]).to(DEV)
+        tgt = torch.from_numpy(g_train["c1_tgt"].astype(np.float32)).to(DEV)
+        full, parts = self._c1(pbox8), self._c1(pbox8)
+        full.next_epoch()
+        full.accumulate_grads(pos, tgt)
+        parts.next_epoch()
+        b = pos.shape[0]
+        for sh in range(4):
+            lo, hi = b * sh // 4, b * (sh + 1) // 4
+            parts.accumulate_grads(pos, tgt[lo:hi].contiguous(), b_max=b, shard=sh, n_shards=4)
+        gc = full.grid_cfg.param_count
+        np.testing.assert_array_equal(full.grad_fx[:gc].cpu().numpy(), parts.grad_fx[:gc].cpu().numpy())
+        a = full.grad_fx[gc:].double().cpu().numpy()
+        bb = parts.grad_fx[gc:].double().cpu().numpy()
+        np.testing.assert_allclose(a, bb, rtol=1e-5, atol=2.0 ** 48 * 1e-9)
+
+
+def test_snapshot_roundtrip(tmp_path, boxes32):
+    c = VisibilityCache(MODE_LIGHTS, 32, grid_cfg(boxes32, 8, 1 << 14), hidden_dims=(64, 64))
+    c.step = 7
+    c.save(tmp_path / "s.vc")
+    d = VisibilityCache.load(tmp_path / "s.vc")
+    assert d.step == 7 and d.net_cfg.hidden_dims == (64, 64)
+    np.testing.assert_array_equal(c.params.cpu().numpy(), d.params.cpu().numpy())
+    pos = np.random.default_rng(0).uniform(-1, 1, (300, 3))
+    np.testing.assert_array_equal(c.infer(pos), d.infer(pos))
+
+
+def test_native_library_is_loaded():
+    import ctypes  # noqa: F401
+    lib = _lib.load()
+    assert lib.nvc_abi_version() == _lib.ABI_VERSION
