@@ -116,7 +116,7 @@ struct QNet {
     float alpha;
     int out_sigmoid;
     // smem carve-up (bytes)
-    int sm_wpack, sm_a0, sm_a1, sm_bias, sm_total;
+    int sm_wpack, sm_a0, sm_a1, sm_bias, sm_lum, sm_total;
 };
 
 enum Mode { kModeVis = 0, kModeNls = 1, kModeNdi = 2 };
@@ -183,220 +183,386 @@ __device__ __forceinline__ uint32_t a_off(int row, int k, int kp) {   // bytes
     return (uint32_t)((row >> 3) * (kp * 16) + (k >> 3) * 128 + (row & 7) * 16 + (k & 7) * 2);
 }
 
-__device__ __forceinline__ void encode_row(const GridDev& g, const __half* __restrict__ table, const double* pos,
-                                           uint8_t* a0, int row, int kp0) {
-    double q[3];
-    normalize(g, pos, q);
-    for (int l = 0; l < g.L; ++l) {
-        int c0[3];
-        double f[3];
-        cell(g.res[l], q, c0, f);
-        const float fx = (float)f[0], fy = (float)f[1], fz = (float)f[2];
-        const float wxs[2] = {1.0f - fx, fx}, wys[2] = {1.0f - fy, fy}, wzs[2] = {1.0f - fz, fz};
-        const __half* tl = table + (int64_t)l * g.T * g.F;
-        if (g.F == 2) {
-            __half2 v[8];
+// cell origin and fraction without int<->double conversions: adding 2^52
+// with round-down leaves floor(x) in the low mantissa bits.  Bit-identical to
+// c0 = min(int(x), n-1); f = x - c0 (hashgrid.py:100-103).
+__device__ __forceinline__ void cell_fast(int n, const double q[3], uint32_t c0[3], float f[3]) {
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const uint32_t idx = corner_index(g, l, c0, (c >> 2) & 1, (c >> 1) & 1, c & 1);
-                v[c] = __ldg(reinterpret_cast<const __half2*>(tl) + idx);
-            }
-            float a = 0.0f, b = 0.0f;
+    for (int a = 0; a < 3; ++a) {
+        const double x = __dmul_rn(q[a], (double)n);
+        const double t = __dadd_rd(x, 0x1p52);
+        uint32_t c = (uint32_t)__double2loint(t);
+        double fr = __dsub_rn(x, __dsub_rn(t, 0x1p52));
+        if (c > (uint32_t)(n - 1)) {   // x == n exactly (q == 1): reference clamps, f = 1
+            c = (uint32_t)(n - 1);
+            fr = 1.0;
+        }
+        c0[a] = c;
+        f[a] = (float)fr;
+    }
+}
+
+struct LevelAddr {
+    uint32_t base, sy, sz, mask;
+};
+
+__device__ __forceinline__ LevelAddr level_addr(const GridDev& g, int l, const uint32_t c0[3]) {
+    LevelAddr a;
+    if (g.dense[l]) {
+        const uint32_t m = (uint32_t)g.res[l] + 1u;
+        a.sy = m;
+        a.sz = m * m;
+        a.mask = 0xffffffffu;
+    } else {
+        a.sy = 2654435761u;
+        a.sz = 805459861u;
+        a.mask = g.tmask;
+    }
+    a.base = c0[0] + c0[1] * a.sy + c0[2] * a.sz;
+    return a;
+}
+
+// F == 2: gather two levels at once (16 half2 loads in flight), FP32 blend
+__device__ __forceinline__ void encode_row2(const GridDev& g, const __half2* __restrict__ table, const double q[3],
+                                            uint8_t* a0, int row, int kp0) {
+    for (int l = 0; l < g.L; l += 2) {
+        const int nl = (l + 1 < g.L) ? 2 : 1;
+        __half2 v[2][8];
+        float w[2][3];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const float w = wxs[(c >> 2) & 1] * wys[(c >> 1) & 1] * wzs[c & 1];
-                const float2 fv = __half22float2(v[c]);
-                a = fmaf(w, fv.x, a);
-                b = fmaf(w, fv.y, b);
+        for (int j = 0; j < 2; ++j) {
+            if (j < nl) {
+                uint32_t c0[3];
+                cell_fast(g.res[l + j], q, c0, w[j]);
+                const LevelAddr ad = level_addr(g, l + j, c0);
+                const __half2* tl = table + (size_t)(l + j) * (size_t)g.T;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const uint32_t idx = (ad.base + ((c >> 2) & 1) + ((c >> 1) & 1) * ad.sy + (c & 1) * ad.sz) & ad.mask;
+                    v[j][c] = __ldg(tl + idx);
+                }
             }
-            *reinterpret_cast<__half2*>(a0 + a_off(row, 2 * l, kp0)) = __floats2half2_rn(a, b);
-        } else {
-            float acc[8];
-            for (int k = 0; k < g.F; ++k) acc[k] = 0.0f;
-            for (int c = 0; c < 8; ++c) {
-                const uint32_t idx = corner_index(g, l, c0, (c >> 2) & 1, (c >> 1) & 1, c & 1);
-                const float w = wxs[(c >> 2) & 1] * wys[(c >> 1) & 1] * wzs[c & 1];
-                for (int k = 0; k < g.F; ++k) acc[k] = fmaf(w, __half2float(__ldg(tl + (int64_t)idx * g.F + k)), acc[k]);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            if (j < nl) {
+                const float fx = w[j][0], fy = w[j][1], fz = w[j][2];
+                const float wx[2] = {1.0f - fx, fx}, wy[2] = {1.0f - fy, fy}, wz[2] = {1.0f - fz, fz};
+                float a = 0.0f, b = 0.0f;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const float wc = (wx[(c >> 2) & 1] * wy[(c >> 1) & 1]) * wz[c & 1];
+                    const float2 fv = __half22float2(v[j][c]);
+                    a = fmaf(wc, fv.x, a);
+                    b = fmaf(wc, fv.y, b);
+                }
+                *reinterpret_cast<__half2*>(a0 + a_off(row, 2 * (l + j), kp0)) = __floats2half2_rn(a, b);
             }
-            for (int k = 0; k < g.F; ++k)
-                *reinterpret_cast<__half*>(a0 + a_off(row, l * g.F + k, kp0)) = __float2half_rn(acc[k]);
         }
     }
 }
 
+__device__ __forceinline__ void encode_rowF(const GridDev& g, const __half* __restrict__ table, const double q[3],
+                                            uint8_t* a0, int row, int kp0) {
+    for (int l = 0; l < g.L; ++l) {
+        uint32_t c0[3];
+        float f[3];
+        cell_fast(g.res[l], q, c0, f);
+        const LevelAddr ad = level_addr(g, l, c0);
+        const float wx[2] = {1.0f - f[0], f[0]}, wy[2] = {1.0f - f[1], f[1]}, wz[2] = {1.0f - f[2], f[2]};
+        const __half* tl = table + (size_t)l * (size_t)g.T * g.F;
+        float acc[8];
+        for (int k = 0; k < g.F; ++k) acc[k] = 0.0f;
+        for (int c = 0; c < 8; ++c) {
+            const uint32_t idx = (ad.base + ((c >> 2) & 1) + ((c >> 1) & 1) * ad.sy + (c & 1) * ad.sz) & ad.mask;
+            const float wc = (wx[(c >> 2) & 1] * wy[(c >> 1) & 1]) * wz[c & 1];
+            for (int k = 0; k < g.F; ++k) acc[k] = fmaf(wc, __half2float(__ldg(tl + (size_t)idx * g.F + k)), acc[k]);
+        }
+        for (int k = 0; k < g.F; ++k)
+            *reinterpret_cast<__half*>(a0 + a_off(row, l * g.F + k, kp0)) = __float2half_rn(acc[k]);
+    }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 // ---------------------------------------------------------------------------
-// the fused kernel
+// the fused kernel: warp-specialised, two tiles in flight per CTA
+//   warps 0-3  epilogue (TMEM lane quarter = warp): bias/act -> A1, final layer
+//              -> visibility / WRS / Neural DI
+//   warps 4-7  encode: pixel rows of the next tile -> A0[stage]
+//   warp  8    control: TMEM alloc, tcgen05.mma issue, bulk prefetch of the
+//              tile's light-major lum/factor rows into smem
+// TMEM holds two accumulators (tile i uses buffer i%2), so layer 0 of tile
+// i+1 runs while the epilogue walks the hidden layers of tile i.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kTile) k_query(GridDev g, QNet net, const float* __restrict__ params,
-                                                 const __half* __restrict__ table,
-                                                 const uint16_t* __restrict__ wpack, const double* __restrict__ pos,
-                                                 int64_t P, nvc_scene sc, QOut o) {
+constexpr int kEpiWarps = 4, kEncWarps = 4, kCtlWarp = 8;
+constexpr int kQThreads = 32 * (kEpiWarps + kEncWarps + 1);
+
+struct QBars {
+    uint64_t a0_full[2], a0_empty[2], acc_full[2], acc_empty[2], a1_full, lum_full[2], lum_empty[2];
+};
+
+__device__ __forceinline__ bool bulk_ok(const QOut& o, int64_t tile, int64_t P) {
+    return o.mode != kModeVis && !o.lum_f64 && (o.stride & 3) == 0 && ((uintptr_t)o.lum & 15) == 0 &&
+           (tile + 1) * kTile <= P;
+}
+
+__global__ void __launch_bounds__(kQThreads, 2) k_query(GridDev g, QNet net, const float* __restrict__ params,
+                                                        const __half* __restrict__ table,
+                                                        const uint16_t* __restrict__ wpack,
+                                                        const double* __restrict__ pos, int64_t P, nvc_scene sc,
+                                                        QOut o) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t mbar;
+    __shared__ QBars bars;
     __shared__ uint32_t tmem_base_s;
     uint8_t* s_w = smem + net.sm_wpack;
-    uint8_t* s_a0 = smem + net.sm_a0;
+    uint8_t* s_a0 = smem + net.sm_a0;            // 2 stages
     uint8_t* s_a1 = smem + net.sm_a1;
     float* s_bias = reinterpret_cast<float*>(smem + net.sm_bias);
-    const int tid = threadIdx.x, warp = tid >> 5;
+    float* s_lum = reinterpret_cast<float*>(smem + net.sm_lum);   // 2 stages of K x 128
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int K = net.dims[net.n_layers];
+    const int a0_stage = kTile * net.kp[0] * 2;
+    const int lum_stage = K * kTile;
 
-    // ---- one-time setup: weights + biases -> smem, zero A0 padding, TMEM, mbarrier
+    // ---- setup ----
     {
         const int n16 = net.wpack_halfs / 8;
         const uint4* src = reinterpret_cast<const uint4*>(wpack);
         uint4* dst = reinterpret_cast<uint4*>(s_w);
-        for (int i = tid; i < n16; i += kTile) dst[i] = __ldg(src + i);
+        for (int i = tid; i < n16; i += kQThreads) dst[i] = __ldg(src + i);
         int bo = 0;
         for (int l = 0; l < net.n_layers; ++l) {
-            for (int n = tid; n < net.np[l]; n += kTile)
+            for (int n = tid; n < net.np[l]; n += kQThreads)
                 s_bias[bo + n] = n < net.dims[l + 1] ? __ldg(params + net.boff[l] + n) : 0.0f;
             bo += net.np[l];
         }
-        uint4 z = make_uint4(0, 0, 0, 0);
-        for (int i = tid; i < kTile * net.kp[0] / 8; i += kTile) reinterpret_cast<uint4*>(s_a0)[i] = z;
+        const uint4 z = make_uint4(0, 0, 0, 0);
+        for (int i = tid; i < 2 * a0_stage / 16; i += kQThreads) reinterpret_cast<uint4*>(s_a0)[i] = z;
     }
-    if (warp == 0) {
+    if (warp == kCtlWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
                      "r"(net.tmem_cols)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     if (tid == 0) {
-        mbar_init(&mbar, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bars.a0_full[s], 32 * kEncWarps);
+            mbar_init(&bars.a0_empty[s], 1);
+            mbar_init(&bars.acc_full[s], 1);
+            mbar_init(&bars.acc_empty[s], 32 * kEpiWarps);
+            mbar_init(&bars.lum_full[s], 1);
+            mbar_init(&bars.lum_empty[s], 32 * kEpiWarps);
+        }
+        mbar_init(&bars.a1_full, 32 * kEpiWarps);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
-    const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
-    uint32_t phase = 0;
-    const int K = net.dims[net.n_layers];
-    const uint32_t a0_addr = smem_u32(s_a0), a1_addr = smem_u32(s_a1), w_addr = smem_u32(s_w);
-
+    const uint32_t acc_cols = (uint32_t)net.tmem_cols / 2;
     const int64_t ntiles = (P + kTile - 1) / kTile;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t p = tile * kTile + tid;
-        const bool valid = p < P;
-        // ---- 1. encode ----
-        if (valid) {
-            const double pp[3] = {pos[3 * p], pos[3 * p + 1], pos[3 * p + 2]};
-            encode_row(g, table, pp, s_a0, tid, net.kp[0]);
-        } else {
-            for (int k = 0; k < net.dims[0]; ++k)
-                *reinterpret_cast<__half*>(s_a0 + a_off(tid, k, net.kp[0])) = __float2half_rn(0.0f);
-        }
-        fence_async_smem();
-        tc_fence_before();
-        __syncthreads();
+    const int n_local = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
 
-        Reservoir res;
-        res.s = 0.0;
-        res.wsel = 0.0;
-        res.sel = -1;
-        res.blk = 0;
-        double rgb[3] = {0.0, 0.0, 0.0};
-        const int64_t gp = o.p_first + p;
-
-        int bias_off = 0;
-        for (int l = 0; l < net.n_layers; ++l) {
-            // ---- 2. MMA (one elected thread) ----
-            if (tid == 0) {
-                tc_fence_after();
-                const uint32_t a_base = l == 0 ? a0_addr : a1_addr;
+    if (warp == kCtlWarp) {
+        // ======================= control =======================
+        if (lane == 0) {
+            const uint32_t a0_addr = smem_u32(s_a0), a1_addr = smem_u32(s_a1), w_addr = smem_u32(s_w);
+            uint32_t a1_cnt = 0;
+            auto issue_layer = [&](int l, int i) {
+                const uint32_t a_base = l == 0 ? a0_addr + (uint32_t)((i & 1) * a0_stage) : a1_addr;
                 const uint32_t a_kp = l == 0 ? net.kp[0] : net.hidden_kp;
                 const uint32_t b_base = w_addr + 2u * net.wofs[l];
                 const uint32_t idesc = idesc_f16(net.np[l]);
+                const uint32_t d = tmem + (uint32_t)(i & 1) * acc_cols;
+                tc_fence_after();
                 for (int kk = 0; kk < net.kp[l] / 16; ++kk) {
                     const uint64_t ad = smem_desc(a_base + kk * 256u, 128u, a_kp * 16u);
                     const uint64_t bd = smem_desc(b_base + kk * 256u, 128u, (uint32_t)net.kp[l] * 16u);
-                    mma_f16(tmem, ad, bd, idesc, kk > 0 ? 1u : 0u);
+                    mma_f16(d, ad, bd, idesc, kk > 0 ? 1u : 0u);
                 }
-                mma_commit(&mbar);
-            }
-            mbar_wait(&mbar, phase);
-            phase ^= 1;
-            tc_fence_after();
-
-            // ---- 3. epilogue ----
-            const bool last = l == net.n_layers - 1;
-            for (int c = 0; c < net.np[l] / 16; ++c) {
-                float v[16];
-                tmem_ld16(t_row + (uint32_t)(c * 16), v);
-                if (!last) {
-                    __align__(16) __half h[16];
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        float z = v[j] + s_bias[bias_off + c * 16 + j];
-                        z = z >= 0.0f ? z : net.alpha * z;
-                        h[j] = __float2half_rn(z);
+            };
+            for (int i = 0; i <= n_local; ++i) {
+                if (i < n_local) {
+                    const int s = i & 1;
+                    const int64_t tile = blockIdx.x + (int64_t)i * gridDim.x;
+                    if (bulk_ok(o, tile, P)) {     // prefetch the tile's K rows of lum/factor
+                        if (i >= 2) mbar_wait(&bars.lum_empty[s], ((i >> 1) - 1) & 1);
+                        mbar_expect_tx(&bars.lum_full[s], (uint32_t)(K * kTile * 4));
+                        const float* src = reinterpret_cast<const float*>(o.lum) + tile * kTile;
+                        for (int k = 0; k < K; ++k)
+                            bulk_g2s(s_lum + s * lum_stage + k * kTile, src + (int64_t)k * o.stride, kTile * 4,
+                                     &bars.lum_full[s]);
                     }
-                    uint8_t* dst = s_a1 + a_off(tid, c * 16, net.hidden_kp);
-                    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(h);
-                    *reinterpret_cast<uint4*>(dst + 128) = *reinterpret_cast<const uint4*>(h + 8);
-                } else if (valid) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int k = c * 16 + j;
-                        if (k >= K) break;
-                        const float z = v[j] + s_bias[bias_off + k];
-                        float a;
-                        if (net.out_sigmoid) {
-                            a = z >= 0.0f ? 1.0f / (1.0f + __expf(-z)) : __expf(z) / (1.0f + __expf(z));
-                            a = fminf(fmaxf(a, 1e-6f), 0.999999f);
-                        } else {
-                            a = z >= 0.0f ? z : net.alpha * z;
-                        }
-                        if (o.mode == kModeVis) {
-                            o.vis[p * K + k] = a;
-                        } else if (o.mode == kModeNls) {
-                            double vv = (double)a;
-                            vv = o.floor > 0.0 ? fmax(vv, o.floor) : fmax(vv, 0.0);
-                            const int64_t li = (int64_t)k * o.stride + p;
-                            const double lum = o.lum_f64 ? __ldg(reinterpret_cast<const double*>(o.lum) + li)
-                                                         : (double)__ldg(reinterpret_cast<const float*>(o.lum) + li);
-                            reservoir_push(res, __dmul_rn(vv, lum), k, o.key,
-                                           o.offset + (uint64_t)gp * (uint64_t)K + (uint64_t)k);
-                        } else {
-                            const int64_t li = (int64_t)k * o.stride + p;
-                            const double fct = o.lum_f64 ? __ldg(reinterpret_cast<const double*>(o.lum) + li)
-                                                         : (double)__ldg(reinterpret_cast<const float*>(o.lum) + li);
-                            const double wk = __dmul_rn((double)a, fct);
-#pragma unroll
-                            for (int ch = 0; ch < 3; ++ch)
-                                rgb[ch] = __dadd_rn(rgb[ch], __dmul_rn(wk, __ldg(sc.lt_radiance + 3 * k + ch)));
-                        }
+                    // layer 0 of tile i
+                    mbar_wait(&bars.a0_full[s], (i >> 1) & 1);
+                    if (i >= 2) mbar_wait(&bars.acc_empty[s], ((i >> 1) - 1) & 1);
+                    issue_layer(0, i);
+                    mma_commit(&bars.a0_empty[s]);
+                    mma_commit(&bars.acc_full[s]);
+                }
+                if (i >= 1) {          // hidden layers of tile i-1
+                    for (int l = 1; l < net.n_layers; ++l) {
+                        mbar_wait(&bars.a1_full, a1_cnt & 1);
+                        ++a1_cnt;
+                        issue_layer(l, i - 1);
+                        mma_commit(&bars.acc_full[(i - 1) & 1]);
                     }
                 }
             }
-            bias_off += net.np[l];
-            fence_async_smem();
-            tc_fence_before();
-            __syncthreads();
         }
-
-        // ---- 4. per-pixel outputs ----
-        if (valid && o.mode == kModeNls) {
-            const double big_w = res.sel >= 0 ? __ddiv_rn(res.s, res.wsel > 0.0 ? res.wsel : 1.0) : 0.0;
-            double u0, u1, y[3];
-            draw_pair(o.key, o.offset + (uint64_t)o.p_total * (uint64_t)K + 2ull * (uint64_t)gp, u0, u1);
-            light_point(sc, res.sel, u0, u1, y);
-            o.ids[p] = res.sel;
-            o.big_w[p] = big_w;
-            o.pts[3 * p] = y[0];
-            o.pts[3 * p + 1] = y[1];
-            o.pts[3 * p + 2] = y[2];
-        } else if (valid && o.mode == kModeNdi) {
+        __syncwarp();
+    } else if (warp >= kEpiWarps) {
+        // ======================= encode =======================
+        const int row = tid - 32 * kEpiWarps;
+        for (int i = 0; i < n_local; ++i) {
+            const int s = i & 1;
+            const int64_t p = (blockIdx.x + (int64_t)i * gridDim.x) * kTile + row;
+            if (i >= 2) mbar_wait(&bars.a0_empty[s], ((i >> 1) - 1) & 1);
+            uint8_t* a0 = s_a0 + s * a0_stage;
+            if (p < P) {
+                const double pp[3] = {__ldg(pos + 3 * p), __ldg(pos + 3 * p + 1), __ldg(pos + 3 * p + 2)};
+                double q[3];
+                normalize(g, pp, q);
+                if (g.F == 2)
+                    encode_row2(g, reinterpret_cast<const __half2*>(table), q, a0, row, net.kp[0]);
+                else
+                    encode_rowF(g, table, q, a0, row, net.kp[0]);
+            } else {
+                for (int k = 0; k < net.dims[0]; ++k)
+                    *reinterpret_cast<__half*>(a0 + a_off(row, k, net.kp[0])) = __float2half_rn(0.0f);
+            }
+            fence_async_smem();
+            mbar_arrive(&bars.a0_full[s]);
+        }
+    } else {
+        // ======================= epilogue =======================
+        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+        uint32_t acc_cnt[2] = {0, 0};
+        for (int i = 0; i < n_local; ++i) {
+            const int s = i & 1;
+            const int64_t tile = blockIdx.x + (int64_t)i * gridDim.x;
+            const int64_t p = tile * kTile + tid;
+            const bool valid = p < P;
+            const int64_t gp = o.p_first + p;
+            const bool bulk = bulk_ok(o, tile, P);
+            const uint32_t t_acc = tmem + lane_base + (uint32_t)s * acc_cols;
+            Reservoir res;
+            res.s = 0.0;
+            res.wsel = 0.0;
+            res.sel = -1;
+            res.blk = 0;
+            double rgb[3] = {0.0, 0.0, 0.0};
+            int bias_off = 0;
+            for (int l = 0; l < net.n_layers; ++l) {
+                mbar_wait(&bars.acc_full[s], acc_cnt[s] & 1);
+                ++acc_cnt[s];
+                tc_fence_after();
+                const bool last = l == net.n_layers - 1;
+                if (!last) {
+                    for (int c = 0; c < net.np[l] / 16; ++c) {
+                        float v[16];
+                        tmem_ld16(t_acc + (uint32_t)(c * 16), v);
+                        __align__(16) __half h[16];
 #pragma unroll
-            for (int ch = 0; ch < 3; ++ch)
-                o.rgb[3 * p + ch] = __ddiv_rn(__dmul_rn(rgb[ch], o.albedo[3 * p + ch]), 3.141592653589793);
+                        for (int j = 0; j < 16; ++j) {
+                            float z = v[j] + s_bias[bias_off + c * 16 + j];
+                            z = z >= 0.0f ? z : net.alpha * z;
+                            h[j] = __float2half_rn(z);
+                        }
+                        uint8_t* dst = s_a1 + a_off(tid, c * 16, net.hidden_kp);
+                        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(h);
+                        *reinterpret_cast<uint4*>(dst + 128) = *reinterpret_cast<const uint4*>(h + 8);
+                    }
+                    fence_async_smem();
+                    tc_fence_before();
+                    mbar_arrive(&bars.a1_full);
+                } else {
+                    if (bulk) mbar_wait(&bars.lum_full[s], (i >> 1) & 1);
+                    const float* lrow = s_lum + s * lum_stage + tid;
+                    for (int c = 0; c < net.np[l] / 16; ++c) {
+                        float v[16];
+                        tmem_ld16(t_acc + (uint32_t)(c * 16), v);
+                        if (!valid) continue;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const int k = c * 16 + j;
+                            if (k >= K) break;
+                            const float z = v[j] + s_bias[bias_off + k];
+                            float a;
+                            if (net.out_sigmoid) {
+                                const float e = __expf(-fabsf(z));
+                                const float r = __fdividef(1.0f, 1.0f + e);
+                                a = z >= 0.0f ? r : e * r;
+                                a = fminf(fmaxf(a, 1e-6f), 0.999999f);
+                            } else {
+                                a = z >= 0.0f ? z : net.alpha * z;
+                            }
+                            if (o.mode == kModeVis) {
+                                o.vis[p * K + k] = a;
+                                continue;
+                            }
+                            double t;
+                            if (bulk)
+                                t = (double)lrow[k * kTile];
+                            else if (o.lum_f64)
+                                t = __ldg(reinterpret_cast<const double*>(o.lum) + (int64_t)k * o.stride + p);
+                            else
+                                t = (double)__ldg(reinterpret_cast<const float*>(o.lum) + (int64_t)k * o.stride + p);
+                            if (o.mode == kModeNls) {
+                                double vv = (double)a;
+                                vv = o.floor > 0.0 ? fmax(vv, o.floor) : fmax(vv, 0.0);
+                                reservoir_push(res, __dmul_rn(vv, t), k, o.key,
+                                               o.offset + (uint64_t)gp * (uint64_t)K + (uint64_t)k);
+                            } else {
+                                const double wk = __dmul_rn((double)a, t);
+#pragma unroll
+                                for (int ch = 0; ch < 3; ++ch)
+                                    rgb[ch] = __dadd_rn(rgb[ch], __dmul_rn(wk, __ldg(sc.lt_radiance + 3 * k + ch)));
+                            }
+                        }
+                    }
+                    tc_fence_before();
+                    mbar_arrive(&bars.acc_empty[s]);
+                    if (bulk) mbar_arrive(&bars.lum_empty[s]);
+                }
+                bias_off += net.np[l];
+            }
+            if (valid && o.mode == kModeNls) {
+                const double big_w = res.sel >= 0 ? __ddiv_rn(res.s, res.wsel > 0.0 ? res.wsel : 1.0) : 0.0;
+                double u0, u1, y[3];
+                draw_pair(o.key, o.offset + (uint64_t)o.p_total * (uint64_t)K + 2ull * (uint64_t)gp, u0, u1);
+                light_point(sc, res.sel, u0, u1, y);
+                o.ids[p] = res.sel;
+                o.big_w[p] = big_w;
+                o.pts[3 * p] = y[0];
+                o.pts[3 * p + 1] = y[1];
+                o.pts[3 * p + 2] = y[2];
+            } else if (valid && o.mode == kModeNdi) {
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch)
+                    o.rgb[3 * p + ch] = __ddiv_rn(__dmul_rn(rgb[ch], o.albedo[3 * p + ch]), 3.141592653589793);
+            }
         }
     }
 
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 0)
+    if (warp == kCtlWarp)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(net.tmem_cols) : "memory");
 }
 
@@ -449,7 +615,7 @@ __global__ void k_nls_from_vis(nvc_scene sc, const float* __restrict__ vis, cons
 
 inline int grid1(int64_t n, int bs) { return (int)((n + bs - 1) / bs); }
 
-int make_qnet(const nvc_model* m, QNet& q) {
+int make_qnet(const nvc_model* m, QNet& q, bool with_lum) {
     NVC_REQUIRE(m && m->params && m->table_h && m->wpack, "tcgen05 path: model state not bound");
     NVC_REQUIRE(m->n_layers >= 1 && m->n_layers <= NVC_MAX_LAYERS, "n_layers out of range");
     NVC_REQUIRE(m->dims[0] == m->levels * m->features, "dims[0] must equal levels*features");
@@ -475,18 +641,24 @@ int make_qnet(const nvc_model* m, QNet& q) {
     q.wpack_halfs = (int)wo;
     q.hidden_kp = hid;
     int cols = 32;
-    while (cols < maxnp) cols <<= 1;
+    while (cols < 2 * maxnp) cols <<= 1;      // two accumulators (tiles i, i+1)
+    if (cols > 512) {
+        set_error("tcgen05 path: %d TMEM columns needed", cols);
+        return NVC_ERR_UNSUPPORTED;
+    }
     q.tmem_cols = cols;
     q.alpha = m->alpha;
     q.out_sigmoid = m->out_sigmoid;
     int nb = 0;
     for (int i = 0; i < m->n_layers; ++i) nb += q.np[i];
+    const int K = m->dims[m->n_layers];
     q.sm_wpack = 0;
     q.sm_a0 = (q.wpack_halfs * 2 + 1023) / 1024 * 1024;
-    q.sm_a1 = q.sm_a0 + (kTile * q.kp[0] * 2 + 1023) / 1024 * 1024;
+    q.sm_a1 = q.sm_a0 + 2 * ((kTile * q.kp[0] * 2 + 1023) / 1024 * 1024);
     q.sm_bias = q.sm_a1 + (kTile * q.hidden_kp * 2 + 1023) / 1024 * 1024;
-    q.sm_total = q.sm_bias + nb * 4 + 1024;   // +1024: dynamic-smem base alignment slack
-    if (q.sm_total > 220 * 1024) {
+    q.sm_lum = q.sm_bias + (nb * 4 + 127) / 128 * 128;
+    q.sm_total = q.sm_lum + (with_lum ? 2 * K * kTile * 4 : 0) + 1024;
+    if (q.sm_total > 226 * 1024) {
         set_error("tcgen05 path: %d bytes of shared memory needed", q.sm_total);
         return NVC_ERR_UNSUPPORTED;
     }
@@ -496,13 +668,18 @@ int make_qnet(const nvc_model* m, QNet& q) {
 int launch_query(const nvc_model* m, const double* pos, int64_t P, const nvc_scene* sc, const QOut& o,
                  cudaStream_t s) {
     QNet q;
-    int rc = make_qnet(m, q);
+    int rc = make_qnet(m, q, o.mode != kModeVis);
     if (rc) return rc;
     if (P <= 0) return NVC_OK;
     GridDev g = grid_of(m);
     cudaFuncSetAttribute(k_query, cudaFuncAttributeMaxDynamicSharedMemorySize, q.sm_total);
+    cudaFuncSetAttribute(k_query, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query, kTile, q.sm_total);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query, kQThreads, q.sm_total) != cudaSuccess ||
+        per_sm < 1) {
+        cudaGetLastError();
+        per_sm = (227 * 1024) / (q.sm_total + 2048);
+    }
     per_sm = max(1, min(per_sm, 512 / q.tmem_cols));
     int dev = 0, sms = kNumSMs;
     cudaGetDevice(&dev);
@@ -513,7 +690,7 @@ int launch_query(const nvc_model* m, const double* pos, int64_t P, const nvc_sce
     nvc_scene scv;
     if (sc) scv = *sc;
     else memset(&scv, 0, sizeof scv);
-    k_query<<<grid, kTile, q.sm_total, s>>>(g, q, m->params, reinterpret_cast<const __half*>(m->table_h), m->wpack,
+    k_query<<<grid, kQThreads, q.sm_total, s>>>(g, q, m->params, reinterpret_cast<const __half*>(m->table_h), m->wpack,
                                             pos, P, scv, o);
     return check_launch("k_query");
 }
