@@ -324,6 +324,243 @@ __global__ void __launch_bounds__(kThreads) k_mlp(GridDev g, Net net, const floa
     }
 }
 
+// ---------------------------------------------------------------------------
+// Register-tiled SIMT training step (all widths multiples of 4, weights in
+// smem as W and W^T).  Same maths and row partition as k_mlp<true>, ~10x less
+// time: forward 2x4 tiles over Wt, grad-W 4x4 tiles over (dz, act), grad-act
+// 2x4 tiles over W, all operands in shared memory.
+// ---------------------------------------------------------------------------
+struct T2Layout {
+    int w[NVC_MAX_LAYERS], wt[NVC_MAX_LAYERS];   // float offsets of W_l [N][K] and W_l^T [K][N]
+    int act[NVC_MAX_LAYERS + 1];                 // act_l [kRows][D_l]
+    int dz0, dz1;                                // two [kRows][Dmax] buffers
+    int total;
+};
+
+__host__ __device__ inline T2Layout t2_layout(const Net& net) {
+    T2Layout t;
+    int o = 0, dmax = 0;
+    for (int l = 0; l < net.n_layers; ++l) {
+        const int sz = net.dims[l] * net.dims[l + 1];
+        t.w[l] = o;
+        o += sz;
+        t.wt[l] = o;
+        o += sz;
+    }
+    for (int l = 0; l <= net.n_layers; ++l) {
+        t.act[l] = o;
+        o += kRows * net.dims[l];
+        if (net.dims[l] > dmax) dmax = net.dims[l];
+    }
+    t.dz0 = o;
+    o += kRows * dmax;
+    t.dz1 = o;
+    o += kRows * dmax;
+    t.total = o;
+    return t;
+}
+
+__global__ void __launch_bounds__(kThreads) k_train2(GridDev g, Net net, const float* __restrict__ params,
+                                                    const double* __restrict__ pos, int64_t b_max,
+                                                    const int64_t* __restrict__ b_dev, int shard, int n_shards,
+                                                    const float* __restrict__ tgt, const float* __restrict__ mask,
+                                                    int64_t* __restrict__ grad_fx, uint16_t* __restrict__ touched,
+                                                    uint16_t epoch, float* __restrict__ part_w,
+                                                    double* __restrict__ part_loss) {
+    extern __shared__ float sm[];
+    const T2Layout tl = t2_layout(net);
+    const int tid = threadIdx.x;
+    const int64_t b = b_dev ? *b_dev : b_max;
+    const int64_t lo = b * shard / n_shards, hi = b * (shard + 1) / n_shards;
+    const int64_t row0 = lo + (int64_t)blockIdx.x * kRows;
+    const int nr = (int)max((int64_t)0, min((int64_t)kRows, hi - row0));
+    const int D0 = net.dims[0];
+    const int K = net.dims[net.n_layers];
+
+    // ---- weights -> smem (W and W^T), encode rows -> act0 ----
+    for (int l = 0; l < net.n_layers; ++l) {
+        const int N = net.dims[l + 1], Ki = net.dims[l];
+        const float* W = params + net.woff[l];
+        for (int e = tid; e < N * Ki; e += blockDim.x) {
+            const float w = __ldg(W + e);
+            const int n = e / Ki, k = e - n * Ki;
+            sm[tl.w[l] + e] = w;
+            sm[tl.wt[l] + k * N + n] = w;
+        }
+    }
+    for (int e = tid; e < kRows * g.L; e += blockDim.x) {
+        const int r = e / g.L, l = e - r * g.L;
+        float* dst = sm + tl.act[0] + r * D0 + l * g.F;
+        if (r < nr) {
+            const int64_t i = row0 + r;
+            const double pp[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+            double q[3];
+            normalize(g, pp, q);
+            encode_level_f32(g, params, q, l, dst, nullptr, nullptr);
+        } else {
+            for (int k = 0; k < g.F; ++k) dst[k] = 0.0f;
+        }
+    }
+    __syncthreads();
+
+    // ---- forward: z = act W^T + b, 2x4 register tiles ----
+    for (int l = 0; l < net.n_layers; ++l) {
+        const int Ki = net.dims[l], N = net.dims[l + 1];
+        const float* A = sm + tl.act[l];
+        const float* Wt = sm + tl.wt[l];
+        float* out = sm + tl.act[l + 1];
+        const bool last = l == net.n_layers - 1;
+        const int ng = N / 4;
+        for (int t = tid; t < (kRows / 2) * ng; t += blockDim.x) {
+            const int r0 = (t / ng) * 2, n0 = (t % ng) * 4;
+            float acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+            for (int k = 0; k < Ki; ++k) {
+                const float4 w = *reinterpret_cast<const float4*>(Wt + k * N + n0);
+                const float a0 = A[r0 * Ki + k], a1 = A[(r0 + 1) * Ki + k];
+                acc[0][0] = fmaf(a0, w.x, acc[0][0]);
+                acc[0][1] = fmaf(a0, w.y, acc[0][1]);
+                acc[0][2] = fmaf(a0, w.z, acc[0][2]);
+                acc[0][3] = fmaf(a0, w.w, acc[0][3]);
+                acc[1][0] = fmaf(a1, w.x, acc[1][0]);
+                acc[1][1] = fmaf(a1, w.y, acc[1][1]);
+                acc[1][2] = fmaf(a1, w.z, acc[1][2]);
+                acc[1][3] = fmaf(a1, w.w, acc[1][3]);
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float z = acc[i][j] + __ldg(params + net.boff[l] + n0 + j);
+                    out[(r0 + i) * N + n0 + j] = (last && net.out_sigmoid) ? sigmoid_ref(z) : leaky(z, net.alpha);
+                }
+        }
+        __syncthreads();
+    }
+
+    // ---- loss + output delta (mlp.py:143-149, 160-168) ----
+    float* dz = sm + tl.dz0;
+    float* dzn = sm + tl.dz1;
+    const float bk = (float)(b * K);
+    double lsum = 0.0;
+    for (int e = tid; e < kRows * K; e += blockDim.x) {
+        const int r = e / K;
+        float d = 0.0f;
+        if (r < nr) {
+            const int64_t li = (row0 - lo) * K + e;
+            const float sgm = sm[tl.act[net.n_layers] + e];
+            const float outc = net.out_sigmoid ? fminf(fmaxf(sgm, 1e-6f), 0.999999f) : sgm;
+            const float t = tgt[li];
+            const float mk = mask ? mask[li] : 1.0f;
+            float dd = __fsub_rn(outc, t);
+            if (mask) dd = __fmul_rn(dd, mk);
+            lsum += (double)__fmul_rn(dd, dd);
+            float dout = __fdiv_rn(__fmul_rn(2.0f, __fsub_rn(sgm, t)), bk);
+            if (mask) dout = __fmul_rn(dout, mk);
+            d = net.out_sigmoid ? __fmul_rn(__fmul_rn(dout, sgm), __fsub_rn(1.0f, sgm))
+                                : (sgm >= 0.0f ? dout : __fmul_rn(dout, net.alpha));
+        }
+        dz[e] = d;
+    }
+    {
+        __shared__ double s_l[kThreads / 32];
+        for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+        if ((tid & 31) == 0) s_l[tid >> 5] = lsum;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < kThreads / 32; ++w) t += s_l[w];
+            part_loss[blockIdx.x] = t / (double)K;
+        }
+    }
+    __syncthreads();
+
+    // ---- backward (mlp.py:170-183) ----
+    float* part = part_w + (int64_t)blockIdx.x * net.mlp_count;
+    for (int l = net.n_layers - 1; l >= 0; --l) {
+        const int Ki = net.dims[l], N = net.dims[l + 1];
+        const float* A = sm + tl.act[l];
+        // grad W[n][k] = sum_r dz[r][n] A[r][k]   (4x4 tiles)
+        float* gw = part + (net.woff[l] - net.grid_count);
+        const int kg = Ki / 4;
+        for (int t = tid; t < (N / 4) * kg; t += blockDim.x) {
+            const int n0 = (t / kg) * 4, k0 = (t % kg) * 4;
+            float acc[4][4] = {};
+            for (int r = 0; r < kRows; ++r) {
+                const float4 d4 = *reinterpret_cast<const float4*>(dz + r * N + n0);
+                const float4 a4 = *reinterpret_cast<const float4*>(A + r * Ki + k0);
+                const float dv[4] = {d4.x, d4.y, d4.z, d4.w}, av[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(dv[i], av[j], acc[i][j]);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                *reinterpret_cast<float4*>(gw + (n0 + i) * Ki + k0) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        }
+        float* gb = part + (net.boff[l] - net.grid_count);
+        for (int n = tid; n < N; n += blockDim.x) {
+            float acc = 0.0f;
+            for (int r = 0; r < kRows; ++r) acc += dz[r * N + n];
+            gb[n] = acc;
+        }
+        // grad act[r][k] = sum_n dz[r][n] W[n][k], through leaky'(z_{l-1}) (2x4 tiles)
+        const float* W = sm + tl.w[l];
+        for (int t = tid; t < (kRows / 2) * kg; t += blockDim.x) {
+            const int r0 = (t / kg) * 2, k0 = (t % kg) * 4;
+            float acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+            for (int n = 0; n < N; ++n) {
+                const float4 w = *reinterpret_cast<const float4*>(W + n * Ki + k0);
+                const float d0 = dz[r0 * N + n], d1 = dz[(r0 + 1) * N + n];
+                acc[0][0] = fmaf(d0, w.x, acc[0][0]);
+                acc[0][1] = fmaf(d0, w.y, acc[0][1]);
+                acc[0][2] = fmaf(d0, w.z, acc[0][2]);
+                acc[0][3] = fmaf(d0, w.w, acc[0][3]);
+                acc[1][0] = fmaf(d1, w.x, acc[1][0]);
+                acc[1][1] = fmaf(d1, w.y, acc[1][1]);
+                acc[1][2] = fmaf(d1, w.z, acc[1][2]);
+                acc[1][3] = fmaf(d1, w.w, acc[1][3]);
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    float v = acc[i][j];
+                    if (l > 0 && !(A[(r0 + i) * Ki + k0 + j] >= 0.0f)) v = __fmul_rn(v, net.alpha);
+                    dzn[(r0 + i) * Ki + k0 + j] = v;
+                }
+        }
+        __syncthreads();
+        float* t = dz;
+        dz = dzn;
+        dzn = t;
+    }
+
+    // ---- hash-grid scatter (hashgrid.py:140-151), fixed point ----
+    for (int e = tid; e < nr * g.L; e += blockDim.x) {
+        const int r = e / g.L, l = e - r * g.L;
+        const int64_t i = row0 + r;
+        const double pp[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+        double q[3];
+        normalize(g, pp, q);
+        int c0[3];
+        double f[3];
+        cell(g.res[l], q, c0, f);
+        const float* up = dz + r * D0 + l * g.F;
+        int64_t* gl = grad_fx + (int64_t)l * g.T * g.F;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const uint32_t idx = corner_index(g, l, c0, (c >> 2) & 1, (c >> 1) & 1, c & 1);
+            const double w = corner_weight(f, c);
+            for (int k = 0; k < g.F; ++k) {
+                const float contrib = (float)__dmul_rn(w, (double)up[k]);
+                red_add_fx(gl + (int64_t)idx * g.F + k, to_fx((double)contrib));
+            }
+            touched[(int64_t)l * g.T + idx] = epoch;
+        }
+    }
+}
+
 // fixed-order reduction of the per-block MLP partials and loss partials
 __global__ void k_reduce_parts(const float* __restrict__ part_w, const double* __restrict__ part_loss, int nblk,
                                int64_t mlp_count, int64_t grid_count, int64_t* __restrict__ grad_fx,
@@ -543,9 +780,18 @@ int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, con
     float* part_w = (float*)ws;
     double* part_loss = (double*)((char*)ws + ((int64_t)nblk * net.mlp_count * 4 + 255) / 256 * 256);
     cudaStream_t s = (cudaStream_t)stream;
-    cudaFuncSetAttribute(k_mlp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_mlp<true><<<nblk, kThreads, smem, s>>>(g, net, m->params, pos, b_max, b_dev, shard, n_shards, tgt, mask,
-                                              nullptr, m->grad_fx, m->touched, epoch, part_w, part_loss);
+    bool tiled = true;
+    for (int i = 0; i <= net.n_layers; ++i) tiled = tiled && (net.dims[i] % 4 == 0);
+    const int smem2 = t2_layout(net).total * 4 + 64;
+    if (tiled && smem2 <= 200 * 1024) {
+        cudaFuncSetAttribute(k_train2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+        k_train2<<<nblk, kThreads, smem2, s>>>(g, net, m->params, pos, b_max, b_dev, shard, n_shards, tgt, mask,
+                                               m->grad_fx, m->touched, epoch, part_w, part_loss);
+    } else {
+        cudaFuncSetAttribute(k_mlp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        k_mlp<true><<<nblk, kThreads, smem, s>>>(g, net, m->params, pos, b_max, b_dev, shard, n_shards, tgt, mask,
+                                                  nullptr, m->grad_fx, m->touched, epoch, part_w, part_loss);
+    }
     rc = check_launch("k_mlp<train>");
     if (rc) return rc;
     k_reduce_parts<<<grid1(net.mlp_count, 256), 256, 0, s>>>(part_w, part_loss, nblk, net.mlp_count,

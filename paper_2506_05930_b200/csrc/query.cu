@@ -24,6 +24,7 @@
 //      runs the sequential FP64 reservoir (exactly the reference cumsum/
 //      compare order) with numpy-Philox uniforms, or the Neural-DI sum.
 // Several CTAs per SM overlap their gather phase with each other's MMA chain.
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -52,6 +53,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
         "r"(phase)
         : "memory");
+}
+
+// wait with a short sleep between polls: for roles that are usually ahead
+// (encode, prefetch) so their spinning does not steal issue slots
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (true) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.b32 %0, 1, 0, P1;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+        if (done) return;
+        __nanosleep(64);
+    }
 }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -400,7 +418,7 @@ __global__ void __launch_bounds__(kQThreads, 2) k_query(GridDev g, QNet net, con
                     const int s = i & 1;
                     const int64_t tile = blockIdx.x + (int64_t)i * gridDim.x;
                     if (bulk_ok(o, tile, P)) {     // prefetch the tile's K rows of lum/factor
-                        if (i >= 2) mbar_wait(&bars.lum_empty[s], ((i >> 1) - 1) & 1);
+                        if (i >= 2) mbar_wait_sleep(&bars.lum_empty[s], ((i >> 1) - 1) & 1);
                         mbar_expect_tx(&bars.lum_full[s], (uint32_t)(K * kTile * 4));
                         const float* src = reinterpret_cast<const float*>(o.lum) + tile * kTile;
                         for (int k = 0; k < K; ++k)
@@ -431,7 +449,7 @@ __global__ void __launch_bounds__(kQThreads, 2) k_query(GridDev g, QNet net, con
         for (int i = 0; i < n_local; ++i) {
             const int s = i & 1;
             const int64_t p = (blockIdx.x + (int64_t)i * gridDim.x) * kTile + row;
-            if (i >= 2) mbar_wait(&bars.a0_empty[s], ((i >> 1) - 1) & 1);
+            if (i >= 2) mbar_wait_sleep(&bars.a0_empty[s], ((i >> 1) - 1) & 1);
             uint8_t* a0 = s_a0 + s * a0_stage;
             if (p < P) {
                 const double pp[3] = {__ldg(pos + 3 * p), __ldg(pos + 3 * p + 1), __ldg(pos + 3 * p + 2)};
@@ -476,16 +494,19 @@ __global__ void __launch_bounds__(kQThreads, 2) k_query(GridDev g, QNet net, con
                     for (int c = 0; c < net.np[l] / 16; ++c) {
                         float v[16];
                         tmem_ld16(t_acc + (uint32_t)(c * 16), v);
-                        __align__(16) __half h[16];
+                        // bias add in fp32, then leaky = max(z, alpha z) on packed half2
+                        __align__(16) __half2 h[8];
+                        const float2* bb = reinterpret_cast<const float2*>(s_bias + bias_off + c * 16);
+                        const __half2 al = __float2half2_rn(net.alpha);
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            float z = v[j] + s_bias[bias_off + c * 16 + j];
-                            z = z >= 0.0f ? z : net.alpha * z;
-                            h[j] = __float2half_rn(z);
+                        for (int j = 0; j < 8; ++j) {
+                            const float2 bj = bb[j];
+                            const __half2 z = __floats2half2_rn(v[2 * j] + bj.x, v[2 * j + 1] + bj.y);
+                            h[j] = __hmax2(z, __hmul2(z, al));
                         }
                         uint8_t* dst = s_a1 + a_off(tid, c * 16, net.hidden_kp);
                         *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(h);
-                        *reinterpret_cast<uint4*>(dst + 128) = *reinterpret_cast<const uint4*>(h + 8);
+                        *reinterpret_cast<uint4*>(dst + 128) = *reinterpret_cast<const uint4*>(h + 4);
                     }
                     fence_async_smem();
                     tc_fence_before();
@@ -674,13 +695,14 @@ int launch_query(const nvc_model* m, const double* pos, int64_t P, const nvc_sce
     GridDev g = grid_of(m);
     cudaFuncSetAttribute(k_query, cudaFuncAttributeMaxDynamicSharedMemorySize, q.sm_total);
     cudaFuncSetAttribute(k_query, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query, kQThreads, q.sm_total) != cudaSuccess ||
-        per_sm < 1) {
-        cudaGetLastError();
-        per_sm = (227 * 1024) / (q.sm_total + 2048);
-    }
-    per_sm = max(1, min(per_sm, 512 / q.tmem_cols));
+    cudaFuncAttributes fa;
+    int regs = 128;
+    if (cudaFuncGetAttributes(&fa, k_query) == cudaSuccess) regs = fa.numRegs;
+    cudaGetLastError();
+    const int by_smem = (228 * 1024) / (q.sm_total + 1024 + 1024);
+    const int by_regs = 65536 / (((regs + 7) / 8 * 8) * kQThreads);
+    int per_sm = max(1, min(min(by_smem, by_regs), 512 / q.tmem_cols));
+    if (const char* e = getenv("NVC_QUERY_CTAS_PER_SM")) per_sm = max(1, atoi(e));
     int dev = 0, sms = kNumSMs;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
