@@ -23,6 +23,13 @@ namespace {
 
 constexpr int kStack = 64;
 
+// Moller-Trumbore exactly as kernels.py:21-56.  The three barycentric /
+// distance numerators are formed before the (expensive, FP64) division; a
+// test whose outcome is already decided by the numerator's sign or magnitude
+// returns early.  Every early exit is one the reference also takes: with
+// |num| >= 2^-900 and |det| < 2^100 the quotient num*(1/det) cannot
+// underflow, so an opposite sign means a strictly negative u/v/t, and
+// |num| > 2|det| means |u| (or |v|, u+v) > 1 after any rounding.
 __device__ __forceinline__ double ray_tri(const double o[3], const double d[3], const double* a,
                                           const double* b, const double* c, double t_min,
                                           double t_max) {
@@ -33,16 +40,29 @@ __device__ __forceinline__ double ray_tri(const double o[3], const double d[3], 
     const double pz = d[0] * e2y - d[1] * e2x;
     const double det = e1x * px + e1y * py + e1z * pz;
     if (fabs(det) < 1e-14) return -1.0;
-    const double inv = 1.0 / det;
     const double tx = o[0] - a[0], ty = o[1] - a[1], tz = o[2] - a[2];
-    const double u = (tx * px + ty * py + tz * pz) * inv;
-    if (u < 0.0 || u > 1.0) return -1.0;
+    const double un = tx * px + ty * py + tz * pz;
     const double qx = ty * e1z - tz * e1y;
     const double qy = tz * e1x - tx * e1z;
     const double qz = tx * e1y - ty * e1x;
-    const double v = (d[0] * qx + d[1] * qy + d[2] * qz) * inv;
+    const double vn = d[0] * qx + d[1] * qy + d[2] * qz;
+    const double tn = e2x * qx + e2y * qy + e2z * qz;
+    const double ad = fabs(det);
+    if (ad < 0x1p100) {
+        const bool neg = det < 0.0;
+        const double lim = 2.0 * ad;
+        if (fabs(un) >= 0x1p-900 && ((un < 0.0) != neg || fabs(un) > lim)) return -1.0;   // u < 0 or u > 1
+        if (fabs(vn) >= 0x1p-900 && ((vn < 0.0) != neg || fabs(vn) > lim)) return -1.0;   // v < 0 or v > 1
+        if (fabs(un) >= 0x1p-900 && fabs(vn) >= 0x1p-900 && fabs(un) + fabs(vn) > 2.0 * lim)
+            return -1.0;                                                                  // u + v > 1
+        if (t_min >= 0.0 && fabs(tn) >= 0x1p-900 && (tn < 0.0) != neg) return -1.0;       // t < 0 <= t_min
+    }
+    const double inv = 1.0 / det;
+    const double u = un * inv;
+    if (u < 0.0 || u > 1.0) return -1.0;
+    const double v = vn * inv;
     if (v < 0.0 || u + v > 1.0) return -1.0;
-    const double t = (e2x * qx + e2y * qy + e2z * qz) * inv;
+    const double t = tn * inv;
     if (t < t_min || t > t_max) return -1.0;
     return t;
 }
@@ -416,21 +436,25 @@ __global__ void __launch_bounds__(1024) k_screen_finish(nvc_scene sc, nvc_camera
     if (threadIdx.x == 0) *n_rows = n_world + count;
 }
 
-// compute_visibility_targets (light mode): row i, light j uses draws j*2b + 2i, +1
-__global__ void k_targets(nvc_scene sc, uint64_t key, const double* __restrict__ pos,
-                          const int64_t* __restrict__ n_rows, int64_t b_host, int shard, int n_shards,
-                          int64_t cap, float* __restrict__ tgt) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y;
+// compute_visibility_targets (light mode): row i, light j uses draws j*2b + 2i, +1.
+// One warp per row, lanes over lights: the 32 shadow rays of a warp share an
+// origin and fan out to neighbouring emitters, so the BVH walk stays coherent.
+__global__ void __launch_bounds__(128) k_targets(nvc_scene sc, uint64_t key, const double* __restrict__ pos,
+                                                 const int64_t* __restrict__ n_rows, int64_t b_host, int shard,
+                                                 int n_shards, int64_t cap, float* __restrict__ tgt) {
+    const int64_t r = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
     const int64_t b = n_rows ? *n_rows : b_host;
     const int64_t lo = b * shard / n_shards, hi = b * (shard + 1) / n_shards;
     const int64_t i = lo + r;
     if (r >= cap || i >= hi) return;
-    double u0, u1, y[3];
-    draw2(key, (uint64_t)(2 * b * j + 2 * i), u0, u1);
-    light_point(sc, j, u0, u1, y);
     const double x[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
-    tgt[r * sc.n_lights + j] = segment_visible(sc, x, y);
+    for (int j = lane; j < sc.n_lights; j += 32) {
+        double u0, u1, y[3];
+        draw2(key, (uint64_t)(2 * b * j + 2 * i), u0, u1);
+        light_point(sc, j, u0, u1, y);
+        tgt[r * sc.n_lights + j] = segment_visible(sc, x, y);
+    }
 }
 
 __global__ void k_set_rows(int64_t* n_rows, int64_t v) { *n_rows = v; }
@@ -507,8 +531,7 @@ int nvc_gen_train_batch(const nvc_scene* sc, const nvc_camera* cam, uint64_t key
     const int64_t total = (int64_t)n_world + n_screen;
     const int64_t cap = total / n_shards + 1;
     if (tgt && total > 0) {
-        dim3 g(grid1(cap, 64), sc->n_lights);
-        k_targets<<<g, 64, 0, s>>>(*sc, key_targets, pos, n_rows, 0, shard, n_shards, cap, tgt);
+        k_targets<<<grid1(cap, 4), 128, 0, s>>>(*sc, key_targets, pos, n_rows, 0, shard, n_shards, cap, tgt);
     }
     return check_launch("k_targets");
 }
@@ -516,8 +539,7 @@ int nvc_gen_train_batch(const nvc_scene* sc, const nvc_camera* cam, uint64_t key
 int nvc_targets(const nvc_scene* sc, uint64_t key, const double* pos, int64_t b, float* tgt, void* stream) {
     NVC_REQUIRE(sc && pos && tgt, "nvc_targets: null argument");
     if (b <= 0) return NVC_OK;
-    dim3 g(grid1(b, 64), sc->n_lights);
-    k_targets<<<g, 64, 0, (cudaStream_t)stream>>>(*sc, key, pos, nullptr, b, 0, 1, b, tgt);
+    k_targets<<<grid1(b, 4), 128, 0, (cudaStream_t)stream>>>(*sc, key, pos, nullptr, b, 0, 1, b, tgt);
     return check_launch("k_targets");
 }
 

@@ -561,20 +561,31 @@ __global__ void __launch_bounds__(kThreads) k_train2(GridDev g, Net net, const f
     }
 }
 
-// fixed-order reduction of the per-block MLP partials and loss partials
-__global__ void k_reduce_parts(const float* __restrict__ part_w, const double* __restrict__ part_loss, int nblk,
-                               int64_t mlp_count, int64_t grid_count, int64_t* __restrict__ grad_fx,
-                               double* __restrict__ loss_out) {
-    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < mlp_count) {
-        double acc = 0.0;
-        for (int b = 0; b < nblk; ++b) acc += (double)part_w[(int64_t)b * mlp_count + j];
-        grad_fx[grid_count + j] += to_fx(acc);
-    }
-    if (j == 0 && loss_out) {
+// fixed-order reduction of the per-block MLP partials and loss partials:
+// block = 32 parameters x 8 warps; warp w sums partial blocks w, w+8, ...
+// in order, then the 8 warp sums are combined in warp order (deterministic).
+__global__ void __launch_bounds__(256) k_reduce_parts(const float* __restrict__ part_w,
+                                                      const double* __restrict__ part_loss, int nblk,
+                                                      int64_t mlp_count, int64_t grid_count,
+                                                      int64_t* __restrict__ grad_fx, double* __restrict__ loss_out) {
+    __shared__ double s_acc[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t j = (int64_t)blockIdx.x * 32 + lane;
+    double acc = 0.0;
+    if (j < mlp_count)
+        for (int b = w; b < nblk; b += 8) acc += (double)__ldg(part_w + (int64_t)b * mlp_count + j);
+    s_acc[w][lane] = acc;
+    __syncthreads();
+    if (w == 0 && j < mlp_count) {
         double t = 0.0;
-        for (int b = 0; b < nblk; ++b) t += part_loss[b];
-        *loss_out = t;
+        for (int i = 0; i < 8; ++i) t += s_acc[i][lane];
+        grad_fx[grid_count + j] += to_fx(t);
+    }
+    if (blockIdx.x == 0 && w == 1 && loss_out) {
+        double t = 0.0;
+        for (int b = lane; b < nblk; b += 32) t += part_loss[b];
+        for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) *loss_out = t;
     }
 }
 
@@ -601,43 +612,76 @@ __host__ __device__ inline int64_t wpack_index(const Net& net, int i, int n, int
     return o + (int64_t)(n >> 3) * (Kp * 8) + (k >> 3) * 64 + (n & 7) * 8 + (k & 7);
 }
 
-// grid part: 4 params per thread (F | 4 or handled scalar)
-__global__ void k_adam_grid(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
-                            int64_t* __restrict__ fx, const uint16_t* __restrict__ touched,
-                            uint16_t* __restrict__ table_h, int64_t n, int F, uint16_t epoch, int dense, AdamK a) {
-    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+// grid part: 8 params per thread, all loads issued before any math; the
+// gradient of an entry is read (and zeroed) only when its epoch matches.
+__device__ __forceinline__ float4 ld_stream(const float* p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_stream(float* p, float4 v) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(256) k_adam_grid(float* __restrict__ p, float* __restrict__ m,
+                                                   float* __restrict__ v, int64_t* __restrict__ fx,
+                                                   const uint16_t* __restrict__ touched,
+                                                   uint16_t* __restrict__ table_h, int64_t n, int F,
+                                                   uint16_t epoch, int dense, AdamK a) {
+    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
     if (i0 >= n) return;
-    if (i0 + 4 <= n) {
-        float4 P = *reinterpret_cast<const float4*>(p + i0);
-        float4 M = *reinterpret_cast<const float4*>(m + i0);
-        float4 V = *reinterpret_cast<const float4*>(v + i0);
-        float G[4];
-        float* Pp = &P.x;
-        float* Mp = &M.x;
-        float* Vp = &V.x;
-        __half h[4];
+    if (i0 + 8 <= n) {
+        float4 P[2], M[2], V[2];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int64_t i = i0 + j;
-            const bool hot = dense || __ldg(touched + i / F) == epoch;
+        for (int h = 0; h < 2; ++h) {
+            P[h] = ld_stream(p + i0 + 4 * h);
+            M[h] = ld_stream(m + i0 + 4 * h);
+            V[h] = ld_stream(v + i0 + 4 * h);
+        }
+        uint16_t tv[8];
+        if (!dense) {
+            if (F == 2) {
+                const uint2 t4 = __ldg(reinterpret_cast<const uint2*>(touched + i0 / 2));
+                tv[0] = tv[1] = (uint16_t)(t4.x & 0xffff);
+                tv[2] = tv[3] = (uint16_t)(t4.x >> 16);
+                tv[4] = tv[5] = (uint16_t)(t4.y & 0xffff);
+                tv[6] = tv[7] = (uint16_t)(t4.y >> 16);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) tv[j] = __ldg(touched + (i0 + j) / F);
+            }
+        }
+        float G[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
             G[j] = 0.0f;
-            if (hot) {
-                const long long q = fx[i];
+            if (dense || tv[j] == epoch) {
+                const long long q = fx[i0 + j];
                 if (q) {
                     G[j] = from_fx(q);
-                    fx[i] = 0;
+                    fx[i0 + j] = 0;
                 }
             }
-            Pp[j] = adam1(Pp[j], G[j], Mp[j], Vp[j], a);
-            h[j] = __float2half_rn(Pp[j]);
         }
-        *reinterpret_cast<float4*>(p + i0) = P;
-        *reinterpret_cast<float4*>(m + i0) = M;
-        *reinterpret_cast<float4*>(v + i0) = V;
-        uint2 hv;
-        hv.x = (uint32_t)__half_as_ushort(h[0]) | ((uint32_t)__half_as_ushort(h[1]) << 16);
-        hv.y = (uint32_t)__half_as_ushort(h[2]) | ((uint32_t)__half_as_ushort(h[3]) << 16);
-        *reinterpret_cast<uint2*>(table_h + i0) = hv;
+        __align__(16) __half hv[8];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            float* Pp = &P[h].x;
+            float* Mp = &M[h].x;
+            float* Vp = &V[h].x;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                Pp[j] = adam1(Pp[j], G[4 * h + j], Mp[j], Vp[j], a);
+                hv[4 * h + j] = __float2half_rn(Pp[j]);
+            }
+            st_stream(p + i0 + 4 * h, P[h]);
+            st_stream(m + i0 + 4 * h, M[h]);
+            st_stream(v + i0 + 4 * h, V[h]);
+        }
+        *reinterpret_cast<uint4*>(table_h + i0) = *reinterpret_cast<const uint4*>(hv);
     } else {
         for (int64_t i = i0; i < n; ++i) {
             const bool hot = dense || touched[i / F] == epoch;
@@ -794,7 +838,7 @@ int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, con
     }
     rc = check_launch("k_mlp<train>");
     if (rc) return rc;
-    k_reduce_parts<<<grid1(net.mlp_count, 256), 256, 0, s>>>(part_w, part_loss, nblk, net.mlp_count,
+    k_reduce_parts<<<grid1(net.mlp_count, 32), 256, 0, s>>>(part_w, part_loss, nblk, net.mlp_count,
                                                              net.grid_count, m->grad_fx, loss_out);
     return check_launch("k_reduce_parts");
 }
@@ -816,7 +860,7 @@ int nvc_adam_step(const nvc_model* m, int64_t t, double lr, uint16_t epoch, int3
     a.lr = (float)lr;
     a.eps = (float)1e-8;
     cudaStream_t s = (cudaStream_t)stream;
-    k_adam_grid<<<grid1((net.grid_count + 3) / 4, 256), 256, 0, s>>>(m->params, m->adam_m, m->adam_v, m->grad_fx,
+    k_adam_grid<<<grid1((net.grid_count + 7) / 8, 256), 256, 0, s>>>(m->params, m->adam_m, m->adam_v, m->grad_fx,
                                                                      m->touched, m->table_h, net.grid_count,
                                                                      m->features, epoch, dense, a);
     rc = check_launch("k_adam_grid");

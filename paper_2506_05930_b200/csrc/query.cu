@@ -324,7 +324,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // TMEM holds two accumulators (tile i uses buffer i%2), so layer 0 of tile
 // i+1 runs while the epilogue walks the hidden layers of tile i.
 // ---------------------------------------------------------------------------
-constexpr int kEpiWarps = 4, kEncWarps = 4, kCtlWarp = 8;
+constexpr int kEpiWarps = 4, kEncWarps = 2, kCtlWarp = kEpiWarps + kEncWarps;
 constexpr int kQThreads = 32 * (kEpiWarps + kEncWarps + 1);
 
 struct QBars {
@@ -336,7 +336,7 @@ __device__ __forceinline__ bool bulk_ok(const QOut& o, int64_t tile, int64_t P) 
            (tile + 1) * kTile <= P;
 }
 
-__global__ void __launch_bounds__(kQThreads, 2) k_query(GridDev g, QNet net, const float* __restrict__ params,
+__global__ void __launch_bounds__(kQThreads, 3) k_query(GridDev g, QNet net, const float* __restrict__ params,
                                                         const __half* __restrict__ table,
                                                         const uint16_t* __restrict__ wpack,
                                                         const double* __restrict__ pos, int64_t P, nvc_scene sc,
@@ -352,7 +352,6 @@ __global__ void __launch_bounds__(kQThreads, 2) k_query(GridDev g, QNet net, con
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int K = net.dims[net.n_layers];
     const int a0_stage = kTile * net.kp[0] * 2;
-    const int lum_stage = K * kTile;
 
     // ---- setup ----
     {
@@ -399,7 +398,7 @@ __global__ void __launch_bounds__(kQThreads, 2) k_query(GridDev g, QNet net, con
         // ======================= control =======================
         if (lane == 0) {
             const uint32_t a0_addr = smem_u32(s_a0), a1_addr = smem_u32(s_a1), w_addr = smem_u32(s_w);
-            uint32_t a1_cnt = 0;
+            uint32_t a1_cnt = 0, lum_uses = 0;
             auto issue_layer = [&](int l, int i) {
                 const uint32_t a_base = l == 0 ? a0_addr + (uint32_t)((i & 1) * a0_stage) : a1_addr;
                 const uint32_t a_kp = l == 0 ? net.kp[0] : net.hidden_kp;
@@ -413,19 +412,22 @@ __global__ void __launch_bounds__(kQThreads, 2) k_query(GridDev g, QNet net, con
                     mma_f16(d, ad, bd, idesc, kk > 0 ? 1u : 0u);
                 }
             };
+            // order per step i: L0(i), hidden layers of tile i-1, then the lum
+            // prefetch of tile i (its single smem stage frees only when the
+            // epilogue finished tile i-1, which needs those hidden layers)
+            auto prefetch_lum = [&](int i) {
+                const int64_t tile = blockIdx.x + (int64_t)i * gridDim.x;
+                if (!bulk_ok(o, tile, P)) return;
+                if (lum_uses > 0) mbar_wait_sleep(&bars.lum_empty[0], (lum_uses - 1) & 1);
+                mbar_expect_tx(&bars.lum_full[0], (uint32_t)(K * kTile * 4));
+                const float* src = reinterpret_cast<const float*>(o.lum) + tile * kTile;
+                for (int k = 0; k < K; ++k)
+                    bulk_g2s(s_lum + k * kTile, src + (int64_t)k * o.stride, kTile * 4, &bars.lum_full[0]);
+                ++lum_uses;
+            };
             for (int i = 0; i <= n_local; ++i) {
                 if (i < n_local) {
                     const int s = i & 1;
-                    const int64_t tile = blockIdx.x + (int64_t)i * gridDim.x;
-                    if (bulk_ok(o, tile, P)) {     // prefetch the tile's K rows of lum/factor
-                        if (i >= 2) mbar_wait_sleep(&bars.lum_empty[s], ((i >> 1) - 1) & 1);
-                        mbar_expect_tx(&bars.lum_full[s], (uint32_t)(K * kTile * 4));
-                        const float* src = reinterpret_cast<const float*>(o.lum) + tile * kTile;
-                        for (int k = 0; k < K; ++k)
-                            bulk_g2s(s_lum + s * lum_stage + k * kTile, src + (int64_t)k * o.stride, kTile * 4,
-                                     &bars.lum_full[s]);
-                    }
-                    // layer 0 of tile i
                     mbar_wait(&bars.a0_full[s], (i >> 1) & 1);
                     if (i >= 2) mbar_wait(&bars.acc_empty[s], ((i >> 1) - 1) & 1);
                     issue_layer(0, i);
@@ -440,28 +442,33 @@ __global__ void __launch_bounds__(kQThreads, 2) k_query(GridDev g, QNet net, con
                         mma_commit(&bars.acc_full[(i - 1) & 1]);
                     }
                 }
+                if (i < n_local) prefetch_lum(i);
             }
         }
         __syncwarp();
     } else if (warp >= kEpiWarps) {
         // ======================= encode =======================
-        const int row = tid - 32 * kEpiWarps;
+        const int et = tid - 32 * kEpiWarps;
+        constexpr int kRowsPerThread = kTile / (32 * kEncWarps);
         for (int i = 0; i < n_local; ++i) {
             const int s = i & 1;
-            const int64_t p = (blockIdx.x + (int64_t)i * gridDim.x) * kTile + row;
             if (i >= 2) mbar_wait_sleep(&bars.a0_empty[s], ((i >> 1) - 1) & 1);
             uint8_t* a0 = s_a0 + s * a0_stage;
-            if (p < P) {
-                const double pp[3] = {__ldg(pos + 3 * p), __ldg(pos + 3 * p + 1), __ldg(pos + 3 * p + 2)};
-                double q[3];
-                normalize(g, pp, q);
-                if (g.F == 2)
-                    encode_row2(g, reinterpret_cast<const __half2*>(table), q, a0, row, net.kp[0]);
-                else
-                    encode_rowF(g, table, q, a0, row, net.kp[0]);
-            } else {
-                for (int k = 0; k < net.dims[0]; ++k)
-                    *reinterpret_cast<__half*>(a0 + a_off(row, k, net.kp[0])) = __float2half_rn(0.0f);
+            for (int rr = 0; rr < kRowsPerThread; ++rr) {
+                const int row = et + rr * 32 * kEncWarps;
+                const int64_t p = (blockIdx.x + (int64_t)i * gridDim.x) * kTile + row;
+                if (p < P) {
+                    const double pp[3] = {__ldg(pos + 3 * p), __ldg(pos + 3 * p + 1), __ldg(pos + 3 * p + 2)};
+                    double q[3];
+                    normalize(g, pp, q);
+                    if (g.F == 2)
+                        encode_row2(g, reinterpret_cast<const __half2*>(table), q, a0, row, net.kp[0]);
+                    else
+                        encode_rowF(g, table, q, a0, row, net.kp[0]);
+                } else {
+                    for (int k = 0; k < net.dims[0]; ++k)
+                        *reinterpret_cast<__half*>(a0 + a_off(row, k, net.kp[0])) = __float2half_rn(0.0f);
+                }
             }
             fence_async_smem();
             mbar_arrive(&bars.a0_full[s]);
@@ -469,7 +476,7 @@ __global__ void __launch_bounds__(kQThreads, 2) k_query(GridDev g, QNet net, con
     } else {
         // ======================= epilogue =======================
         const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-        uint32_t acc_cnt[2] = {0, 0};
+        uint32_t acc_cnt[2] = {0, 0}, lum_uses = 0;
         for (int i = 0; i < n_local; ++i) {
             const int s = i & 1;
             const int64_t tile = blockIdx.x + (int64_t)i * gridDim.x;
@@ -512,8 +519,8 @@ __global__ void __launch_bounds__(kQThreads, 2) k_query(GridDev g, QNet net, con
                     tc_fence_before();
                     mbar_arrive(&bars.a1_full);
                 } else {
-                    if (bulk) mbar_wait(&bars.lum_full[s], (i >> 1) & 1);
-                    const float* lrow = s_lum + s * lum_stage + tid;
+                    if (bulk) mbar_wait(&bars.lum_full[0], lum_uses & 1);
+                    const float* lrow = s_lum + tid;
                     for (int c = 0; c < net.np[l] / 16; ++c) {
                         float v[16];
                         tmem_ld16(t_acc + (uint32_t)(c * 16), v);
@@ -558,7 +565,10 @@ __global__ void __launch_bounds__(kQThreads, 2) k_query(GridDev g, QNet net, con
                     }
                     tc_fence_before();
                     mbar_arrive(&bars.acc_empty[s]);
-                    if (bulk) mbar_arrive(&bars.lum_empty[s]);
+                    if (bulk) {
+                        mbar_arrive(&bars.lum_empty[0]);
+                        ++lum_uses;
+                    }
                 }
                 bias_off += net.np[l];
             }
@@ -678,7 +688,7 @@ int make_qnet(const nvc_model* m, QNet& q, bool with_lum) {
     q.sm_a1 = q.sm_a0 + 2 * ((kTile * q.kp[0] * 2 + 1023) / 1024 * 1024);
     q.sm_bias = q.sm_a1 + (kTile * q.hidden_kp * 2 + 1023) / 1024 * 1024;
     q.sm_lum = q.sm_bias + (nb * 4 + 127) / 128 * 128;
-    q.sm_total = q.sm_lum + (with_lum ? 2 * K * kTile * 4 : 0) + 1024;
+    q.sm_total = q.sm_lum + (with_lum ? K * kTile * 4 : 0) + 1024;
     if (q.sm_total > 226 * 1024) {
         set_error("tcgen05 path: %d bytes of shared memory needed", q.sm_total);
         return NVC_ERR_UNSUPPORTED;
@@ -708,7 +718,8 @@ int launch_query(const nvc_model* m, const double* pos, int64_t P, const nvc_sce
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t ntiles = (P + kTile - 1) / kTile;
     const int64_t cap = (int64_t)sms * per_sm;
-    const int grid = (int)(ntiles < cap ? ntiles : cap);
+    int grid = (int)(ntiles < cap ? ntiles : cap);
+    if (const char* e = getenv("NVC_QUERY_GRID")) grid = max(1, min(grid, atoi(e)));   // tests: many tiles per CTA
     nvc_scene scv;
     if (sc) scv = *sc;
     else memset(&scv, 0, sizeof scv);

@@ -239,6 +239,30 @@ class TestSampling:
         np.testing.assert_array_equal(big_w, ow)
         assert (ids >= 0).sum() > 100
 
+    @pytest.mark.parametrize("grid", ["3", "7"])
+    def test_fused_pipeline_many_tiles_per_cta(self, boxes32, g_scenes, monkeypatch, grid):
+        """Few CTAs -> every CTA cycles its A0 / TMEM / lum stages many times."""
+        from paper_2506_05930_b200.render import gbuffer_device
+        cam = boxes32.camera.resized(96, 54)
+        pos, nrm, alb, _, _ = gbuffer_device(boxes32, cam)
+        ctx = PixelCtx(boxes32, pos, nrm, alb)
+        c = VisibilityCache(MODE_LIGHTS, 32, grid_cfg(boxes32, 16, 1 << 19), hidden_dims=(64, 64, 64))
+        c.grid_params = (np.random.default_rng(1).standard_normal(c.grid_params.shape) * 0.5).astype(np.float32)
+        vis16 = c.infer(pos.cpu().numpy(), precision=PRECISION_FP16)
+        sc = O.SceneArrays.from_golden(g_scenes, "boxes32_")
+        key = R.stream_key(0, 12, "light-select")
+        oi, op, ow = O.nls_sample(sc, vis16, ctx.lum_matrix(), key)
+        monkeypatch.setenv("NVC_QUERY_GRID", grid)
+        np.testing.assert_array_equal(c.infer(pos.cpu().numpy(), precision=PRECISION_FP16), vis16)
+        ids, pts, big_w = nls_sample_batch(ctx, c, R.Stream(key=key))
+        np.testing.assert_array_equal(ids, oi)
+        np.testing.assert_array_equal(pts, op)
+        np.testing.assert_array_equal(big_w, ow)
+        rgb = neural_di_batch(ctx, c)
+        f = ctx.factor_matrix()
+        want = ((vis16.astype(np.float64) * f) @ boxes32.lt_radiance) * alb.cpu().numpy() / np.pi
+        np.testing.assert_allclose(rgb, want, rtol=1e-9, atol=1e-12)
+
     def test_tile_sharded_nls_matches_whole_frame(self, boxes32, g_samp):
         from paper_2506_05930_b200.sampling import nls_sample_device
         c = VisibilityCache(MODE_LIGHTS, 32, grid_cfg(boxes32, 16, 1 << 19), hidden_dims=(64, 64, 64))
