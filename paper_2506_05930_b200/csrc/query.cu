@@ -43,34 +43,21 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 
+// try_wait with a suspend-time hint: the waiting thread sleeps in hardware
+// until the phase completes (or 1 ms passes) instead of spinning on issue slots
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@P1 bra DONE_%=;\n\t"
         "bra WAIT_%=;\n"
         "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
-        "r"(phase)
+        "r"(phase), "r"(1000000u)
         : "memory");
 }
 
-// wait with a short sleep between polls: for roles that are usually ahead
-// (encode, prefetch) so their spinning does not steal issue slots
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
-    uint32_t done = 0;
-    while (true) {
-        asm volatile(
-            "{\n\t.reg .pred P1;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-            "selp.b32 %0, 1, 0, P1;\n\t}"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(phase)
-            : "memory");
-        if (done) return;
-        __nanosleep(64);
-    }
-}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) { mbar_wait(bar, phase); }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -163,10 +150,14 @@ struct Reservoir {
     U4 u;
 };
 
+// one out-of-line copy of the 10-round Philox keeps the fused kernel's
+// instruction footprint inside the SM instruction cache
+__device__ __noinline__ U4 philox_call(uint64_t counter, uint64_t key) { return philox_block(counter, key); }
+
 __device__ __forceinline__ double draw_cached(Reservoir& r, uint64_t key, uint64_t n) {
     const uint64_t b = n / 4 + 1;
     if (b != r.blk) {
-        r.u = philox_block(b, key);
+        r.u = philox_call(b, key);
         r.blk = b;
     }
     return u01(r.u.x[n & 3]);
@@ -184,12 +175,12 @@ __device__ __forceinline__ void reservoir_push(Reservoir& r, double w, int k, ui
 }
 
 __device__ __forceinline__ void draw_pair(uint64_t key, uint64_t n, double& a, double& b) {
-    const U4 blk = philox_block(n / 4 + 1, key);
+    const U4 blk = philox_call(n / 4 + 1, key);
     a = u01(blk.x[n & 3]);
     if ((n & 3) != 3) {
         b = u01(blk.x[(n & 3) + 1]);
     } else {
-        const U4 nb = philox_block(n / 4 + 2, key);
+        const U4 nb = philox_call(n / 4 + 2, key);
         b = u01(nb.x[0]);
     }
 }
@@ -336,6 +327,7 @@ __device__ __forceinline__ bool bulk_ok(const QOut& o, int64_t tile, int64_t P) 
            (tile + 1) * kTile <= P;
 }
 
+template <int kMode, bool kF2>
 __global__ void __launch_bounds__(kQThreads, 3) k_query(GridDev g, QNet net, const float* __restrict__ params,
                                                         const __half* __restrict__ table,
                                                         const uint16_t* __restrict__ wpack,
@@ -461,7 +453,7 @@ __global__ void __launch_bounds__(kQThreads, 3) k_query(GridDev g, QNet net, con
                     const double pp[3] = {__ldg(pos + 3 * p), __ldg(pos + 3 * p + 1), __ldg(pos + 3 * p + 2)};
                     double q[3];
                     normalize(g, pp, q);
-                    if (g.F == 2)
+                    if constexpr (kF2)
                         encode_row2(g, reinterpret_cast<const __half2*>(table), q, a0, row, net.kp[0]);
                     else
                         encode_rowF(g, table, q, a0, row, net.kp[0]);
@@ -539,7 +531,7 @@ __global__ void __launch_bounds__(kQThreads, 3) k_query(GridDev g, QNet net, con
                             } else {
                                 a = z >= 0.0f ? z : net.alpha * z;
                             }
-                            if (o.mode == kModeVis) {
+                            if (kMode == kModeVis) {
                                 o.vis[p * K + k] = a;
                                 continue;
                             }
@@ -550,7 +542,7 @@ __global__ void __launch_bounds__(kQThreads, 3) k_query(GridDev g, QNet net, con
                                 t = __ldg(reinterpret_cast<const double*>(o.lum) + (int64_t)k * o.stride + p);
                             else
                                 t = (double)__ldg(reinterpret_cast<const float*>(o.lum) + (int64_t)k * o.stride + p);
-                            if (o.mode == kModeNls) {
+                            if (kMode == kModeNls) {
                                 double vv = (double)a;
                                 vv = o.floor > 0.0 ? fmax(vv, o.floor) : fmax(vv, 0.0);
                                 reservoir_push(res, __dmul_rn(vv, t), k, o.key,
@@ -572,7 +564,7 @@ __global__ void __launch_bounds__(kQThreads, 3) k_query(GridDev g, QNet net, con
                 }
                 bias_off += net.np[l];
             }
-            if (valid && o.mode == kModeNls) {
+            if (valid && kMode == kModeNls) {
                 const double big_w = res.sel >= 0 ? __ddiv_rn(res.s, res.wsel > 0.0 ? res.wsel : 1.0) : 0.0;
                 double u0, u1, y[3];
                 draw_pair(o.key, o.offset + (uint64_t)o.p_total * (uint64_t)K + 2ull * (uint64_t)gp, u0, u1);
@@ -582,7 +574,7 @@ __global__ void __launch_bounds__(kQThreads, 3) k_query(GridDev g, QNet net, con
                 o.pts[3 * p] = y[0];
                 o.pts[3 * p + 1] = y[1];
                 o.pts[3 * p + 2] = y[2];
-            } else if (valid && o.mode == kModeNdi) {
+            } else if (valid && kMode == kModeNdi) {
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch)
                     o.rgb[3 * p + ch] = __ddiv_rn(__dmul_rn(rgb[ch], o.albedo[3 * p + ch]), 3.141592653589793);
@@ -703,11 +695,16 @@ int launch_query(const nvc_model* m, const double* pos, int64_t P, const nvc_sce
     if (rc) return rc;
     if (P <= 0) return NVC_OK;
     GridDev g = grid_of(m);
-    cudaFuncSetAttribute(k_query, cudaFuncAttributeMaxDynamicSharedMemorySize, q.sm_total);
-    cudaFuncSetAttribute(k_query, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    auto kern = k_query<kModeVis, true>;
+    const bool f2 = g.F == 2;
+    if (o.mode == kModeVis) kern = f2 ? k_query<kModeVis, true> : k_query<kModeVis, false>;
+    else if (o.mode == kModeNls) kern = f2 ? k_query<kModeNls, true> : k_query<kModeNls, false>;
+    else kern = f2 ? k_query<kModeNdi, true> : k_query<kModeNdi, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, q.sm_total);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncAttributes fa;
     int regs = 128;
-    if (cudaFuncGetAttributes(&fa, k_query) == cudaSuccess) regs = fa.numRegs;
+    if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess) regs = fa.numRegs;
     cudaGetLastError();
     const int by_smem = (228 * 1024) / (q.sm_total + 1024 + 1024);
     const int by_regs = 65536 / (((regs + 7) / 8 * 8) * kQThreads);
@@ -723,8 +720,8 @@ int launch_query(const nvc_model* m, const double* pos, int64_t P, const nvc_sce
     nvc_scene scv;
     if (sc) scv = *sc;
     else memset(&scv, 0, sizeof scv);
-    k_query<<<grid, kQThreads, q.sm_total, s>>>(g, q, m->params, reinterpret_cast<const __half*>(m->table_h), m->wpack,
-                                            pos, P, scv, o);
+    kern<<<grid, kQThreads, q.sm_total, s>>>(g, q, m->params, reinterpret_cast<const __half*>(m->table_h), m->wpack,
+                                             pos, P, scv, o);
     return check_launch("k_query");
 }
 
