@@ -197,6 +197,8 @@ def gpu_arm(args) -> None:
     grid = HashGridConfig(levels=LEVELS, table_size=TABLE, features_per_level=FEATS, aabb_min=scene.aabb_min,
                           aabb_max=scene.aabb_max)
     cache = VisibilityCache(MODE_LIGHTS, K, grid, seed=0, hidden_dims=HIDDEN, device=dev)
+    if not os.environ.get("NVC_NO_L2_PIN"):
+        cache.pin_table_in_l2()
     cfg = TrainFrameConfig(n_world=N_WORLD * world, n_screen=N_SCREEN * world, seed=0)
     bufs = BatchBuffers(cfg.n_world, cfg.n_screen, K, dev, world)
     out = (torch.empty(P, dtype=torch.int64, device=dev), torch.empty((P, 3), dtype=torch.float64, device=dev),

@@ -104,6 +104,12 @@ int64_t nvc_wpack_count(const nvc_model *m);
 /* bytes of scratch nvc_train_grads needs for b rows */
 int64_t nvc_train_workspace_bytes(const nvc_model *m, int64_t b);
 
+/* Pin [ptr, ptr+bytes) (the fp16 hash table) in the persisting L2 carve-out
+ * for kernels launched on `stream` (best effort; no-op if unsupported). */
+int nvc_l2_persist(const void *ptr, int64_t bytes, void *stream);
+/* Profiling aid: copy out / reset the query kernel's event trace. */
+int nvc_debug_trace(uint64_t *host_out, int32_t n, int32_t reset);
+
 /* ---- state ------------------------------------------------------------ */
 /* Rebuild table_h and wpack from params (after loading / setting params). */
 int nvc_refresh_shadow(const nvc_model *m, void *stream);
@@ -155,16 +161,22 @@ int nvc_nls_from_vis(const nvc_scene *sc, const float *vis, const void *lum, int
                      uint64_t key, uint64_t offset, double floor,
                      int64_t *ids, double *pts, double *big_w, void *stream);
 /* Fused encode -> tcgen05 MLP -> clamp * lum -> WRS -> light point, one
- * pass per 128-pixel tile (the hot path). pos (p, 3) f64. */
+ * pass per 128-pixel tile (the hot path). pos (p, 3) f64; nz_mask may be NULL. */
 int nvc_nls_sample(const nvc_model *m, const nvc_scene *sc, const double *pos,
-                   const void *lum, int32_t lum_f64, int64_t p_stride, int64_t p,
-                   int64_t p_first, int64_t p_total, uint64_t key, uint64_t offset,
+                   const void *lum, int32_t lum_f64, const uint32_t *nz_mask, int64_t p_stride,
+                   int64_t p, int64_t p_first, int64_t p_total, uint64_t key, uint64_t offset,
                    double floor, int64_t *ids, double *pts, double *big_w, void *stream);
 /* Fused Neural DI (sampling.py:215-218): rgb (p,3) f64 = sum_k v_k f_k L_k * albedo/pi,
  * factor in light-major layout (f32 or f64). */
 int nvc_neural_di(const nvc_model *m, const nvc_scene *sc, const double *pos,
                   const double *albedo, const void *factor, int32_t factor_f64,
-                  int64_t p_stride, int64_t p, double *rgb, void *stream);
+                  const uint32_t *nz_mask, int64_t p_stride, int64_t p, double *rgb, void *stream);
+/* Nonzero mask of a light-major table (K <= 32 uses one word per pixel):
+ * bit j of mask[w*p_stride + r] is set iff table[(32w+j)*p_stride + r] != 0.
+ * Passed as nz_mask above, it lets the fused kernels skip zero-weight lights
+ * (exact: they add 0 to the reservoir sum and are never selected). */
+int nvc_table_mask(const void *table, int32_t f64, int64_t p_stride, int64_t p, int32_t k,
+                   uint32_t *mask, void *stream);
 
 /* ---- geometry + training data: geometry.py, render.py, training.py ----- */
 /* make_gbuffer (render.py:103-117) for pixels [p_first, p_first+p). */

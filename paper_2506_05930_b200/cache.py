@@ -124,6 +124,10 @@ class VisibilityCache:
     def refresh_shadow(self, stream=None) -> None:
         _lib.call("nvc_refresh_shadow", self.model, _lib.stream_ptr(stream))
 
+    def pin_table_in_l2(self, stream=None) -> None:
+        """Keep the fp16 query table in the persisting L2 carve-out (best effort)."""
+        _lib.call("nvc_l2_persist", self.table_h.data_ptr(), self.table_h.numel() * 2, _lib.stream_ptr(stream))
+
     @property
     def param_count(self) -> int:
         return self.param_count_

@@ -166,6 +166,40 @@ __device__ __forceinline__ double corner_weight(const double f[3], int c) {
 }
 
 // ---------------------------------------------------------------------------
+// tcgen05 operand layout: fp16, K-major, 8-row core groups, swizzled by the
+// row within the group (SWIZZLE_32B/64B/128B chosen by the row width), the
+// canonical layout UMMA descriptors describe.  Shared by the packed weights
+// (written by the Adam / shadow kernels) and the A tiles of the query kernel.
+// ---------------------------------------------------------------------------
+__host__ __device__ inline int umma_kpad(int k) { return k <= 16 ? 16 : (k <= 32 ? 32 : (k + 63) / 64 * 64); }
+__host__ __device__ inline int umma_sw_bytes(int kp) { return kp * 2 >= 128 ? 128 : kp * 2; }
+
+// log2 of the swizzle row width in bytes for a padded K (kp in {16, 32, 64k})
+__host__ __device__ __forceinline__ int umma_sw_log2(int kp) { return kp >= 64 ? 7 : (kp == 32 ? 6 : 5); }
+
+// byte offset of element (r, k) in a [rows x kp] tile (rows % 8 == 0)
+__host__ __device__ __forceinline__ uint32_t umma_off(int r, int k, int rows, int kp) {
+    const int lg = umma_sw_log2(kp);
+    const uint32_t kb = (uint32_t)k * 2u;
+    const uint32_t atom = kb >> lg, within = kb & ((1u << lg) - 1u);
+    const uint32_t cs = (within >> 4) ^ ((uint32_t)(r & 7) >> (7 - lg));
+    return (atom * (uint32_t)rows << lg) + ((uint32_t)r << lg) + (cs << 4) + (within & 15u);
+}
+
+// per-layer padded N (rows of W) and K: hidden widths are padded like the next
+// layer's K so the A1 tile never carries stale columns
+__host__ __device__ inline void umma_pads(const int* dims, int n_layers, int* np, int* kp) {
+    for (int l = 0; l < n_layers; ++l) {
+        np[l] = (l < n_layers - 1) ? umma_kpad(dims[l + 1]) : (dims[l + 1] + 15) / 16 * 16;
+        kp[l] = l == 0 ? umma_kpad(dims[0]) : np[l - 1];
+    }
+}
+
+// halfs of one packed weight block, rounded to 1024 B so every block starts
+// on a swizzle-atom boundary
+__host__ __device__ inline int64_t umma_block_halfs(int np, int kp) { return ((int64_t)np * kp + 511) / 512 * 512; }
+
+// ---------------------------------------------------------------------------
 // scene helpers
 // ---------------------------------------------------------------------------
 // Scene.light_points (scene.py:204-215): id < 0 -> light 0; edges from vertices

@@ -604,12 +604,13 @@ __device__ __forceinline__ float adam1(float p, float g, float& m, float& v, con
     return __fsub_rn(p, __fdiv_rn(num, den));
 }
 
-// wpack offset (halfs) of W_i[n][k] in the tcgen05 K-major core-matrix layout
+// wpack offset (halfs) of W_i[n][k] in the tcgen05 swizzled K-major layout
 __host__ __device__ inline int64_t wpack_index(const Net& net, int i, int n, int k) {
+    int np[NVC_MAX_LAYERS], kp[NVC_MAX_LAYERS];
+    umma_pads(net.dims, net.n_layers, np, kp);
     int64_t o = 0;
-    for (int j = 0; j < i; ++j) o += (int64_t)((net.dims[j + 1] + 15) / 16 * 16) * ((net.dims[j] + 15) / 16 * 16);
-    const int Kp = (net.dims[i] + 15) / 16 * 16;
-    return o + (int64_t)(n >> 3) * (Kp * 8) + (k >> 3) * 64 + (n & 7) * 8 + (k & 7);
+    for (int j = 0; j < i; ++j) o += umma_block_halfs(np[j], kp[j]);
+    return o + umma_off(n, k, np[i], kp[i]) / 2;
 }
 
 // grid part: 8 params per thread, all loads issued before any math; the
@@ -728,13 +729,14 @@ __global__ void k_shadow_grid(const float* __restrict__ p, uint16_t* __restrict_
 __global__ void k_shadow_wpack(Net net, const float* __restrict__ p, uint16_t* __restrict__ wpack, int64_t total) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= total) return;
+    int np[NVC_MAX_LAYERS], kp[NVC_MAX_LAYERS];
+    umma_pads(net.dims, net.n_layers, np, kp);
     // walk layers to find (layer, n, k) of padded slot t in row-major padded order
     int64_t o = t;
     for (int l = 0; l < net.n_layers; ++l) {
-        const int Np = (net.dims[l + 1] + 15) / 16 * 16, Kp = (net.dims[l] + 15) / 16 * 16;
-        const int64_t sz = (int64_t)Np * Kp;
+        const int64_t sz = (int64_t)np[l] * kp[l];
         if (o < sz) {
-            const int n = (int)(o / Kp), k = (int)(o % Kp);
+            const int n = (int)(o / kp[l]), k = (int)(o % kp[l]);
             float w = 0.0f;
             if (n < net.dims[l + 1] && k < net.dims[l]) w = p[net.woff[l] + (int64_t)n * net.dims[l] + k];
             wpack[wpack_index(net, l, n, k)] = __half_as_ushort(__float2half_rn(w));
@@ -747,8 +749,10 @@ __global__ void k_shadow_wpack(Net net, const float* __restrict__ p, uint16_t* _
 }  // namespace
 
 int64_t wpack_count_of(const nvc_model* m) {
+    int np[NVC_MAX_LAYERS], kp[NVC_MAX_LAYERS];
+    umma_pads(m->dims, m->n_layers, np, kp);
     int64_t c = 0;
-    for (int i = 0; i < m->n_layers; ++i) c += (int64_t)((m->dims[i + 1] + 15) / 16 * 16) * ((m->dims[i] + 15) / 16 * 16);
+    for (int i = 0; i < m->n_layers; ++i) c += umma_block_halfs(np[i], kp[i]);
     return c;
 }
 

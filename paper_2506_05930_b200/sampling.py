@@ -119,6 +119,7 @@ class PixelCtx:
         self._tdt = torch.float64 if self.table_dtype == np.float64 else torch.float32
         self._factor = None
         self._lum = None
+        self._masks = {}
         if factors is not None:
             self._factor = _dev(np.asarray(factors).T, torch, dev, self._tdt).contiguous()
 
@@ -161,6 +162,19 @@ class PixelCtx:
         if self._lum is None:
             self._build(want_lum=True)
         return self._lum
+
+    def mask_device(self, which: str = "lum"):
+        """Per-pixel nonzero bitmask of the lum/factor table (None when K > 32)."""
+        import torch
+        if self.dscene.n_lights > 32:
+            return None
+        if which not in self._masks:
+            t = self.lum_device() if which == "lum" else self.factor_device()
+            m = torch.empty(t.shape[1], dtype=torch.int32, device=self.device)
+            _lib.call("nvc_table_mask", t.data_ptr(), int(t.dtype == torch.float64), t.shape[1], self.n,
+                      self.dscene.n_lights, m.data_ptr(), _lib.stream_ptr())
+            self._masks[which] = m
+        return self._masks[which]
 
     def factor_matrix(self) -> np.ndarray:
         return self.factor_device().T.to(dtype=__import__("torch").float64).cpu().numpy()
@@ -227,8 +241,8 @@ def nls_sample_device(ctx: PixelCtx, cache, key: int, offset: int = 0, clamp_flo
         if cache.output_dim != k:
             raise ValueError(f"cache has {cache.output_dim} outputs, scene has {k} lights")
         _lib.call("nvc_nls_sample", cache.model, ctx.dscene.struct, ctx.pos.data_ptr(), lum.data_ptr(), lum64,
-                  lum.shape[1], p, p_first, total, key, offset, floor, ids.data_ptr(), pts.data_ptr(),
-                  big_w.data_ptr(), _lib.stream_ptr())
+                  _lib.ptr(ctx.mask_device("lum")), lum.shape[1], p, p_first, total, key, offset, floor,
+                  ids.data_ptr(), pts.data_ptr(), big_w.data_ptr(), _lib.stream_ptr())
     else:
         vis = cache.infer(ctx.positions)
         vis = vis if isinstance(vis, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(vis, np.float32))
@@ -261,8 +275,8 @@ def neural_di_device(ctx: PixelCtx, cache, out=None):
     if _is_native(cache):
         fac = ctx.factor_device()
         _lib.call("nvc_neural_di", cache.model, ctx.dscene.struct, ctx.pos.data_ptr(), ctx.alb.data_ptr(),
-                  fac.data_ptr(), int(fac.dtype == torch.float64), fac.shape[1], p, out.data_ptr(),
-                  _lib.stream_ptr())
+                  fac.data_ptr(), int(fac.dtype == torch.float64), _lib.ptr(ctx.mask_device("factor")),
+                  fac.shape[1], p, out.data_ptr(), _lib.stream_ptr())
         return out
     vis = cache.infer(ctx.positions)
     out.copy_(torch.from_numpy(ctx.unshadowed_rgb(np.asarray(vis, np.float64))))
