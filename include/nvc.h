@@ -62,7 +62,7 @@ typedef struct {
     float *adam_m, *adam_v;               /* f32 Adam moments, param_count */
     int64_t *grad_fx;                     /* fixed-point gradient accumulator, param_count */
     uint16_t *touched;                    /* per-table-entry epoch map, L*T */
-    uint16_t *table_h;                    /* fp16 shadow of the table (bit patterns), L*T*F */
+    uint16_t *table_h;                    /* fp16 query table, x-pair layout: slot e = (f[e], f[next(e)]), 2*L*T*F */
     uint16_t *wpack;                      /* fp16 weights in the tcgen05 K-major core-matrix layout */
     int64_t param_count;
     int64_t wpack_count;                  /* halfs in wpack (nvc_wpack_count) */

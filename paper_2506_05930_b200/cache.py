@@ -85,7 +85,8 @@ class VisibilityCache:
         self.adam_v = torch.zeros_like(self.params)
         self.grad_fx = torch.zeros(total, dtype=torch.int64, device=dev)
         self.touched = torch.zeros(g.levels * g.table_size, dtype=torch.int16, device=dev)
-        self.table_h = torch.zeros(g.param_count, dtype=torch.float16, device=dev)
+        # fp16 query table in x-pair layout (common.cuh): 2 x the grid parameters
+        self.table_h = torch.zeros(2 * g.param_count, dtype=torch.float16, device=dev)
         m = _lib.NvcModel()
         m.levels, m.features, m.table_size = g.levels, g.features_per_level, g.table_size
         for level in range(g.levels):

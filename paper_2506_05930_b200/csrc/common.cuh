@@ -200,6 +200,16 @@ __host__ __device__ inline void umma_pads(const int* dims, int n_layers, int* np
 __host__ __device__ inline int64_t umma_block_halfs(int np, int kp) { return ((int64_t)np * kp + 511) / 512 * 512; }
 
 // ---------------------------------------------------------------------------
+// fp16 query table in x-pair layout: slot e of level l holds the F features of
+// entry e followed by those of entry next(e) = (e+1) mod T within the level.
+// The spatial hash adds x with prime 1, so corner (x0+1, y, z) always lives in
+// next(slot of (x0, y, z)) (dense levels: slot+1): one 2F-half load fetches
+// both x-neighbours, halving the gather instructions of the encoder.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ int64_t pair_next(int64_t e, int64_t T) { return (e & ~(T - 1)) | ((e + 1) & (T - 1)); }
+__host__ __device__ __forceinline__ int64_t pair_prev(int64_t e, int64_t T) { return (e & ~(T - 1)) | ((e - 1) & (T - 1)); }
+
+// ---------------------------------------------------------------------------
 // scene helpers
 // ---------------------------------------------------------------------------
 // Scene.light_points (scene.py:204-215): id < 0 -> light 0; edges from vertices

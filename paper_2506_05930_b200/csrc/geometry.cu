@@ -436,24 +436,95 @@ __global__ void __launch_bounds__(1024) k_screen_finish(nvc_scene sc, nvc_camera
     if (threadIdx.x == 0) *n_rows = n_world + count;
 }
 
+// Warp-packet any-hit: the 32 lanes walk one shared DFS stack (node, lane
+// mask).  A lane takes part in a node only if its own slab test accepted every
+// ancestor, and visits its nodes in the reference's order (push left then
+// right, pop LIFO), so each lane's answer is exactly its scalar traversal's;
+// the warp just stops diverging over the tree.
+__device__ uint32_t any_hit_packet(const nvc_scene& sc, const double o[3], const double d[3], double t_min,
+                                   double t_max, bool active, int32_t* st_node, uint32_t* st_mask) {
+    const int lane = threadIdx.x & 31;
+    uint32_t hit = 0u;
+    const uint32_t act = __ballot_sync(0xffffffffu, active);
+    if (sc.n_tris == 0 || act == 0u) return 0u;
+    const double inv[3] = {inv_dir(d[0]), inv_dir(d[1]), inv_dir(d[2])};
+    int top = 0;
+    if (lane == 0) {
+        st_node[0] = 0;
+        st_mask[0] = act;
+    }
+    top = 1;
+    __syncwarp();
+    while (top > 0) {
+        --top;
+        const int32_t n = st_node[top];
+        uint32_t m = st_mask[top] & ~hit;
+        __syncwarp();
+        if (m == 0u) continue;
+        const bool mine = (m >> lane) & 1u;
+        const bool box = mine && aabb_hit(o, inv, sc.node_min + 3 * n, sc.node_max + 3 * n, t_max);
+        m = __ballot_sync(0xffffffffu, box);
+        if (m == 0u) continue;
+        const int32_t cnt = __ldg(sc.node_count + n);
+        if (cnt > 0) {
+            bool h = false;
+            if ((m >> lane) & 1u) {
+                const int32_t s0 = __ldg(sc.node_start + n);
+                for (int32_t k = s0; k < s0 + cnt && !h; ++k)
+                    h = ray_tri(o, d, sc.bv0 + 3 * k, sc.bv1 + 3 * k, sc.bv2 + 3 * k, t_min, t_max) >= 0.0;
+            }
+            hit |= __ballot_sync(0xffffffffu, h);
+            if ((act & ~hit) == 0u) break;
+        } else {
+            if (lane == 0) {
+                st_node[top] = __ldg(sc.node_left + n);
+                st_mask[top] = m;
+                st_node[top + 1] = __ldg(sc.node_right + n);
+                st_mask[top + 1] = m;
+            }
+            top += 2;
+            __syncwarp();
+        }
+    }
+    return hit;
+}
+
 // compute_visibility_targets (light mode): row i, light j uses draws j*2b + 2i, +1.
-// One warp per row, lanes over lights: the 32 shadow rays of a warp share an
-// origin and fan out to neighbouring emitters, so the BVH walk stays coherent.
+// One warp per row, lanes over lights (K <= 32 per pass): the warp's shadow rays
+// share an origin and fan out to neighbouring emitters -> packet traversal.
 __global__ void __launch_bounds__(128) k_targets(nvc_scene sc, uint64_t key, const double* __restrict__ pos,
                                                  const int64_t* __restrict__ n_rows, int64_t b_host, int shard,
                                                  int n_shards, int64_t cap, float* __restrict__ tgt) {
-    const int64_t r = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    __shared__ int32_t st_node[4][kStack];
+    __shared__ uint32_t st_mask[4][kStack];
+    const int w = threadIdx.x >> 5;
+    const int64_t r = (int64_t)blockIdx.x * 4 + w;
     const int lane = threadIdx.x & 31;
     const int64_t b = n_rows ? *n_rows : b_host;
     const int64_t lo = b * shard / n_shards, hi = b * (shard + 1) / n_shards;
     const int64_t i = lo + r;
-    if (r >= cap || i >= hi) return;
+    if (r >= cap || i >= hi) return;     // warp-uniform
     const double x[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
-    for (int j = lane; j < sc.n_lights; j += 32) {
-        double u0, u1, y[3];
-        draw2(key, (uint64_t)(2 * b * j + 2 * i), u0, u1);
-        light_point(sc, j, u0, u1, y);
-        tgt[r * sc.n_lights + j] = segment_visible(sc, x, y);
+    const double eps = sc.shadow_eps;
+    for (int j0 = 0; j0 < sc.n_lights; j0 += 32) {
+        const int j = j0 + lane;
+        const bool valid = j < sc.n_lights;
+        double y[3] = {0.0, 0.0, 0.0};
+        if (valid) {
+            double u0, u1;
+            draw2(key, (uint64_t)(2 * b * j + 2 * i), u0, u1);
+            light_point(sc, j, u0, u1, y);
+        }
+        // visibility_batch (geometry.py:233-247), per lane
+        const double dd[3] = {y[0] - x[0], y[1] - x[1], y[2] - x[2]};
+        const double dist = sqrt((dd[0] * dd[0] + dd[1] * dd[1]) + dd[2] * dd[2]);
+        const double safe = fmax(dist, 1e-300);
+        const double dir[3] = {dd[0] / safe, dd[1] / safe, dd[2] / safe};
+        double t_max = dist - eps;
+        const bool degenerate = t_max <= eps;
+        t_max = fmax(t_max, eps + 1e-12);
+        const uint32_t hits = any_hit_packet(sc, x, dir, eps, t_max, valid && !degenerate, st_node[w], st_mask[w]);
+        if (valid) tgt[r * sc.n_lights + j] = (degenerate || !((hits >> lane) & 1u)) ? 1.0f : 0.0f;
     }
 }
 

@@ -111,3 +111,70 @@ extern "C" int nvc_micro(int mode, int iters, int n, int blocks, long long* out_
     nvc::k_micro<<<blocks, 128, 50 * 1024, (cudaStream_t)stream>>>(mode, iters, n, out_dev);
     return nvc::check_launch("k_micro");
 }
+
+// ---- encode-only throughput probe: one thread per (pixel, level), fp16 table -> fp16 features
+namespace nvc {
+namespace {
+__global__ void __launch_bounds__(256) k_encode_probe(GridDev g, const __half2* __restrict__ table,
+                                                      const double* __restrict__ pos, int64_t P,
+                                                      __half2* __restrict__ feats) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t p = t / g.L;
+    const int l = (int)(t - p * g.L);
+    if (p >= P) return;
+    const double pp[3] = {__ldg(pos + 3 * p), __ldg(pos + 3 * p + 1), __ldg(pos + 3 * p + 2)};
+    double q[3];
+    normalize(g, pp, q);
+    const int n = g.res[l];
+    uint32_t c0[3];
+    float f[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double x = __dmul_rn(q[a], (double)n);
+        const double tt = __dadd_rd(x, 0x1p52);
+        uint32_t c = (uint32_t)__double2loint(tt);
+        double fr = __dsub_rn(x, __dsub_rn(tt, 0x1p52));
+        if (c > (uint32_t)(n - 1)) {
+            c = (uint32_t)(n - 1);
+            fr = 1.0;
+        }
+        c0[a] = c;
+        f[a] = (float)fr;
+    }
+    uint32_t sy, sz, mask;
+    if (g.dense[l]) {
+        sy = (uint32_t)n + 1u;
+        sz = sy * sy;
+        mask = 0xffffffffu;
+    } else {
+        sy = 2654435761u;
+        sz = 805459861u;
+        mask = g.tmask;
+    }
+    const uint32_t base = c0[0] + c0[1] * sy + c0[2] * sz;
+    const uint2* tl = reinterpret_cast<const uint2*>(table) + (size_t)l * (size_t)g.T;
+    uint2 v[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = __ldg(tl + ((base + ((c >> 1) & 1) * sy + (c & 1) * sz) & mask));
+    const float wy[2] = {1.0f - f[1], f[1]}, wz[2] = {1.0f - f[2], f[2]};
+    float a = 0.0f, b = 0.0f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const float wyz = wy[(c >> 1) & 1] * wz[c & 1];
+        const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&v[c].x));
+        const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&v[c].y));
+        a = fmaf((1.0f - f[0]) * wyz, f0.x, fmaf(f[0] * wyz, f1.x, a));
+        b = fmaf((1.0f - f[0]) * wyz, f0.y, fmaf(f[0] * wyz, f1.y, b));
+    }
+    feats[p * g.L + l] = __floats2half2_rn(a, b);
+}
+}  // namespace
+}  // namespace nvc
+
+extern "C" int nvc_encode_probe(const nvc_model* m, const double* pos, int64_t P, void* feats, void* stream) {
+    nvc::GridDev g = nvc::grid_of(m);
+    const int64_t n = P * g.L;
+    nvc::k_encode_probe<<<(int)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        g, reinterpret_cast<const __half2*>(m->table_h), pos, P, reinterpret_cast<__half2*>(feats));
+    return nvc::check_launch("k_encode_probe");
+}

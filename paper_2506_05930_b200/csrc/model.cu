@@ -594,14 +594,23 @@ __global__ void __launch_bounds__(256) k_reduce_parts(const float* __restrict__ 
 // ---------------------------------------------------------------------------
 struct AdamK {
     float b1, c1, b2, c2, b1c, b2c, lr, eps;
+    double inv_b1c, inv_b2c;   // RN(1 / (double)b1c), RN(1 / (double)b2c)
 };
 
+// One Adam element update with the reference's float32 rounding
+// (mlp.py:209-217).  Quotients by the per-step constants use
+// (float)(x * RN(1/c)) in binary64: a float/float quotient is never a float
+// midpoint and lies >= 2^-49 (relative) from one, so the <= 2^-52 binary64
+// error cannot change the float rounding; the variable quotient uses a
+// binary64 division (double rounding is innocuous for p' >= 2p + 2).
 __device__ __forceinline__ float adam1(float p, float g, float& m, float& v, const AdamK& a) {
     m = __fadd_rn(__fmul_rn(m, a.b1), __fmul_rn(a.c1, g));
     v = __fadd_rn(__fmul_rn(v, a.b2), __fmul_rn(__fmul_rn(a.c2, g), g));
-    const float num = __fmul_rn(a.lr, __fdiv_rn(m, a.b1c));
-    const float den = __fadd_rn(__fsqrt_rn(__fdiv_rn(v, a.b2c)), a.eps);
-    return __fsub_rn(p, __fdiv_rn(num, den));
+    const float mh = (float)__dmul_rn((double)m, a.inv_b1c);
+    const float vh = (float)__dmul_rn((double)v, a.inv_b2c);
+    const float num = __fmul_rn(a.lr, mh);
+    const float den = __fadd_rn(__fsqrt_rn(vh), a.eps);
+    return __fsub_rn(p, (float)__ddiv_rn((double)num, (double)den));
 }
 
 // wpack offset (halfs) of W_i[n][k] in the tcgen05 swizzled K-major layout
@@ -627,11 +636,17 @@ __device__ __forceinline__ void st_stream(float* p, float4 v) {
                  : "memory");
 }
 
+__device__ __forceinline__ void put_pair(uint16_t* t2, int64_t i, int F, int64_t T, uint16_t h) {
+    const int64_t e = i / F, f = i - e * F;
+    t2[e * 2 * F + f] = h;                               // own slot, low half
+    t2[pair_prev(e, T) * 2 * F + F + f] = h;             // previous slot's x-neighbour half
+}
+
 __global__ void __launch_bounds__(256) k_adam_grid(float* __restrict__ p, float* __restrict__ m,
                                                    float* __restrict__ v, int64_t* __restrict__ fx,
                                                    const uint16_t* __restrict__ touched,
                                                    uint16_t* __restrict__ table_h, int64_t n, int F,
-                                                   uint16_t epoch, int dense, AdamK a) {
+                                                   uint16_t epoch, int dense, AdamK a, int64_t T) {
     const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
     if (i0 >= n) return;
     if (i0 + 8 <= n) {
@@ -682,7 +697,19 @@ __global__ void __launch_bounds__(256) k_adam_grid(float* __restrict__ p, float*
             st_stream(m + i0 + 4 * h, M[h]);
             st_stream(v + i0 + 4 * h, V[h]);
         }
-        *reinterpret_cast<uint4*>(table_h + i0) = *reinterpret_cast<const uint4*>(hv);
+        if (F == 2) {   // 4 entries: own slots (4 x 4 B) + previous slots' neighbour halves
+            const int64_t e0 = i0 / 2;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t w = (uint32_t)__half_as_ushort(hv[2 * j]) | ((uint32_t)__half_as_ushort(hv[2 * j + 1]) << 16);
+                const int64_t e = e0 + j;
+                *reinterpret_cast<uint32_t*>(table_h + e * 4) = w;
+                *reinterpret_cast<uint32_t*>(table_h + pair_prev(e, T) * 4 + 2) = w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) put_pair(table_h, i0 + j, F, T, __half_as_ushort(hv[j]));
+        }
     } else {
         for (int64_t i = i0; i < n; ++i) {
             const bool hot = dense || touched[i / F] == epoch;
@@ -695,7 +722,7 @@ __global__ void __launch_bounds__(256) k_adam_grid(float* __restrict__ p, float*
             p[i] = adam1(p[i], g, mm, vv, a);
             m[i] = mm;
             v[i] = vv;
-            table_h[i] = __half_as_ushort(__float2half_rn(p[i]));
+            put_pair(table_h, i, F, T, __half_as_ushort(__float2half_rn(p[i])));
         }
     }
 }
@@ -721,9 +748,9 @@ __global__ void k_adam_mlp(Net net, float* __restrict__ p, float* __restrict__ m
     }
 }
 
-__global__ void k_shadow_grid(const float* __restrict__ p, uint16_t* __restrict__ h, int64_t n) {
+__global__ void k_shadow_grid(const float* __restrict__ p, uint16_t* __restrict__ h, int64_t n, int F, int64_t T) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) h[i] = __half_as_ushort(__float2half_rn(p[i]));
+    if (i < n) put_pair(h, i, F, T, __half_as_ushort(__float2half_rn(p[i])));
 }
 
 __global__ void k_shadow_wpack(Net net, const float* __restrict__ p, uint16_t* __restrict__ wpack, int64_t total) {
@@ -793,7 +820,8 @@ int nvc_refresh_shadow(const nvc_model* m, void* stream) {
     NVC_REQUIRE(m->table_h && m->wpack, "nvc_refresh_shadow: shadow buffers not bound");
     Net net = net_of(m);
     cudaStream_t s = (cudaStream_t)stream;
-    k_shadow_grid<<<grid1(net.grid_count, 256), 256, 0, s>>>(m->params, m->table_h, net.grid_count);
+    k_shadow_grid<<<grid1(net.grid_count, 256), 256, 0, s>>>(m->params, m->table_h, net.grid_count, m->features,
+                                                             m->table_size);
     const int64_t wc = wpack_count_of(m);
     k_shadow_wpack<<<grid1(wc, 256), 256, 0, s>>>(net, m->params, m->wpack, wc);
     return check_launch("refresh_shadow");
@@ -863,10 +891,12 @@ int nvc_adam_step(const nvc_model* m, int64_t t, double lr, uint16_t epoch, int3
     a.b2c = (float)(1.0 - pow(0.999, (double)t));
     a.lr = (float)lr;
     a.eps = (float)1e-8;
+    a.inv_b1c = 1.0 / (double)a.b1c;
+    a.inv_b2c = 1.0 / (double)a.b2c;
     cudaStream_t s = (cudaStream_t)stream;
     k_adam_grid<<<grid1((net.grid_count + 7) / 8, 256), 256, 0, s>>>(m->params, m->adam_m, m->adam_v, m->grad_fx,
                                                                      m->touched, m->table_h, net.grid_count,
-                                                                     m->features, epoch, dense, a);
+                                                                     m->features, epoch, dense, a, m->table_size);
     rc = check_launch("k_adam_grid");
     if (rc) return rc;
     k_adam_mlp<<<grid1(net.mlp_count, 256), 256, 0, s>>>(net, m->params, m->adam_m, m->adam_v, m->grad_fx,

@@ -252,13 +252,15 @@ __device__ __forceinline__ LevelAddr level_addr(const GridDev& g, int l, const u
     return a;
 }
 
-// F == 2: gather four levels at once (32 half2 loads in flight), FP32 blend,
-// one 16-byte store of the 4 levels' 8 features into the core-matrix row
+// F == 2: four levels per batch; each level needs 4 x-pair loads (8 B: both
+// x-neighbours' 2 features) from the pair table, 16 loads in flight per batch;
+// FP32 blend; one 16-byte store of the 4 levels' 8 features
 __device__ __forceinline__ void encode_row2(const GridDev& g, const __half2* __restrict__ table, const double q[3],
                                             uint8_t* a0, int row, int kp0) {
     constexpr int LB = 4;
+    const uint2* t2 = reinterpret_cast<const uint2*>(table);
     for (int l = 0; l < g.L; l += LB) {
-        __half2 v[LB][8];
+        uint2 v[LB][4];
         float w[LB][3];
 #pragma unroll
         for (int j = 0; j < LB; ++j) {
@@ -266,12 +268,10 @@ __device__ __forceinline__ void encode_row2(const GridDev& g, const __half2* __r
                 uint32_t c0[3];
                 cell_fast(g.res[l + j], q, c0, w[j]);
                 const LevelAddr ad = level_addr(g, l + j, c0);
-                const __half2* tl = table + (size_t)(l + j) * (size_t)g.T;
+                const uint2* tl = t2 + (size_t)(l + j) * (size_t)g.T;
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const uint32_t idx = (ad.base + ((c >> 2) & 1) + ((c >> 1) & 1) * ad.sy + (c & 1) * ad.sz) & ad.mask;
-                    v[j][c] = __ldg(tl + idx);
-                }
+                for (int c = 0; c < 4; ++c)    // (y, z) corner pair: slots of (x0,y,z) and (x0+1,y,z)
+                    v[j][c] = __ldg(tl + ((ad.base + ((c >> 1) & 1) * ad.sy + (c & 1) * ad.sz) & ad.mask));
             }
         }
         __align__(16) __half2 out[LB];
@@ -280,13 +280,17 @@ __device__ __forceinline__ void encode_row2(const GridDev& g, const __half2* __r
             float a = 0.0f, b = 0.0f;
             if (l + j < g.L) {
                 const float fx = w[j][0], fy = w[j][1], fz = w[j][2];
-                const float wx[2] = {1.0f - fx, fx}, wy[2] = {1.0f - fy, fy}, wz[2] = {1.0f - fz, fz};
+                const float wy[2] = {1.0f - fy, fy}, wz[2] = {1.0f - fz, fz};
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const float wc = (wx[(c >> 2) & 1] * wy[(c >> 1) & 1]) * wz[c & 1];
-                    const float2 fv = __half22float2(v[j][c]);
-                    a = fmaf(wc, fv.x, a);
-                    b = fmaf(wc, fv.y, b);
+                for (int c = 0; c < 4; ++c) {
+                    const float wyz = wy[(c >> 1) & 1] * wz[c & 1];
+                    const float w0 = (1.0f - fx) * wyz, w1 = fx * wyz;
+                    const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&v[j][c].x));
+                    const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&v[j][c].y));
+                    a = fmaf(w0, f0.x, a);
+                    b = fmaf(w0, f0.y, b);
+                    a = fmaf(w1, f1.x, a);
+                    b = fmaf(w1, f1.y, b);
                 }
             }
             out[j] = __floats2half2_rn(a, b);
@@ -309,14 +313,17 @@ __device__ __forceinline__ void encode_rowF(const GridDev& g, const __half* __re
         float f[3];
         cell_fast(g.res[l], q, c0, f);
         const LevelAddr ad = level_addr(g, l, c0);
-        const float wx[2] = {1.0f - f[0], f[0]}, wy[2] = {1.0f - f[1], f[1]}, wz[2] = {1.0f - f[2], f[2]};
-        const __half* tl = table + (size_t)l * (size_t)g.T * g.F;
+        const float wy[2] = {1.0f - f[1], f[1]}, wz[2] = {1.0f - f[2], f[2]};
+        const __half* tl = table + (size_t)l * (size_t)g.T * 2 * g.F;
         float acc[8];
         for (int k = 0; k < g.F; ++k) acc[k] = 0.0f;
-        for (int c = 0; c < 8; ++c) {
-            const uint32_t idx = (ad.base + ((c >> 2) & 1) + ((c >> 1) & 1) * ad.sy + (c & 1) * ad.sz) & ad.mask;
-            const float wc = (wx[(c >> 2) & 1] * wy[(c >> 1) & 1]) * wz[c & 1];
-            for (int k = 0; k < g.F; ++k) acc[k] = fmaf(wc, __half2float(__ldg(tl + (size_t)idx * g.F + k)), acc[k]);
+        for (int c = 0; c < 4; ++c) {
+            const uint32_t slot = (ad.base + ((c >> 1) & 1) * ad.sy + (c & 1) * ad.sz) & ad.mask;
+            const float wyz = wy[(c >> 1) & 1] * wz[c & 1];
+            const float w0 = (1.0f - f[0]) * wyz, w1 = f[0] * wyz;
+            const __half* s2 = tl + (size_t)slot * 2 * g.F;
+            for (int k = 0; k < g.F; ++k)
+                acc[k] = fmaf(w1, __half2float(__ldg(s2 + g.F + k)), fmaf(w0, __half2float(__ldg(s2 + k)), acc[k]));
         }
         for (int k = 0; k < g.F; ++k)
             *reinterpret_cast<__half*>(a0 + a_off(row, l * g.F + k, kp0)) = __float2half_rn(acc[k]);

@@ -319,7 +319,11 @@ class TestTraining:
         np.testing.assert_array_equal(c.adam_m.cpu().numpy(), st.m)
         np.testing.assert_array_equal(c.adam_v.cpu().numpy(), st.v)
         assert not c.grad_fx.any()
-        np.testing.assert_array_equal(c.table_h.cpu().numpy(), p[:c.grid_cfg.param_count].astype(np.float16))
+        gcfg = c.grid_cfg
+        t2 = c.table_h.cpu().numpy().reshape(gcfg.levels, gcfg.table_size, 2, gcfg.features_per_level)
+        tab = p[:gcfg.param_count].astype(np.float16).reshape(gcfg.levels, gcfg.table_size, gcfg.features_per_level)
+        np.testing.assert_array_equal(t2[:, :, 0], tab)                       # own slot
+        np.testing.assert_array_equal(t2[:, :, 1], np.roll(tab, -1, axis=1))  # x-neighbour (mod T)
 
     def test_touched_map_adam_equals_dense(self, pbox8, g_train):
         a, b = self._c1(pbox8), self._c1(pbox8)
