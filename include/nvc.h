@@ -124,7 +124,11 @@ int nvc_encode(const nvc_model *m, const double *pos, int64_t n, float *feats,
 /* precision 0: f32 SIMT (parity: f32 table + f32 weights);
  * precision 1: fused fp16 table + tcgen05/TMEM MLP (fp32 accumulate). */
 int nvc_infer(const nvc_model *m, const double *pos, int64_t n, int32_t precision,
-              float *out, void *stream);
+              float *out, void *workspace, void *stream);
+/* Scratch for the decoupled fp16 query pipeline (encode tiles -> tcgen05 MLP
+ * -> selection) over p pixels.  Passing workspace = NULL to nvc_infer /
+ * nvc_nls_sample / nvc_neural_di selects the single fused kernel instead. */
+int64_t nvc_query_workspace_bytes(const nvc_model *m, int64_t p);
 
 /* ---- training: cache.py:60-73 (train_step) split at the allreduce point --- */
 /* Accumulates the gradient of the loss into grad_fx and marks touched table
@@ -165,12 +169,14 @@ int nvc_nls_from_vis(const nvc_scene *sc, const float *vis, const void *lum, int
 int nvc_nls_sample(const nvc_model *m, const nvc_scene *sc, const double *pos,
                    const void *lum, int32_t lum_f64, const uint32_t *nz_mask, int64_t p_stride,
                    int64_t p, int64_t p_first, int64_t p_total, uint64_t key, uint64_t offset,
-                   double floor, int64_t *ids, double *pts, double *big_w, void *stream);
+                   double floor, int64_t *ids, double *pts, double *big_w, void *workspace,
+                   void *stream);
 /* Fused Neural DI (sampling.py:215-218): rgb (p,3) f64 = sum_k v_k f_k L_k * albedo/pi,
  * factor in light-major layout (f32 or f64). */
 int nvc_neural_di(const nvc_model *m, const nvc_scene *sc, const double *pos,
                   const double *albedo, const void *factor, int32_t factor_f64,
-                  const uint32_t *nz_mask, int64_t p_stride, int64_t p, double *rgb, void *stream);
+                  const uint32_t *nz_mask, int64_t p_stride, int64_t p, double *rgb, void *workspace,
+                  void *stream);
 /* Nonzero mask of a light-major table (K <= 32 uses one word per pixel):
  * bit j of mask[w*p_stride + r] is set iff table[(32w+j)*p_stride + r] != 0.
  * Passed as nz_mask above, it lets the fused kernels skip zero-weight lights

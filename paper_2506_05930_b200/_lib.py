@@ -67,7 +67,8 @@ _SIGS = {
     "nvc_l2_persist": (c_i32, [c_vp, c_i64, c_vp]),
     "nvc_debug_trace": (c_i32, [c_vp, c_i32, c_i32]),
     "nvc_encode": (c_i32, [P(NvcModel), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
-    "nvc_infer": (c_i32, [P(NvcModel), c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "nvc_infer": (c_i32, [P(NvcModel), c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    "nvc_query_workspace_bytes": (c_i64, [P(NvcModel), c_i64]),
     "nvc_train_grads": (c_i32, [P(NvcModel), c_vp, c_vp, c_vp, c_i64, c_vp, c_i32, c_i32,
                                 ctypes.c_uint16, c_vp, c_vp, c_vp]),
     "nvc_adam_step": (c_i32, [P(NvcModel), c_i64, c_f64, ctypes.c_uint16, c_i32, c_vp]),
@@ -75,9 +76,9 @@ _SIGS = {
     "nvc_nls_from_vis": (c_i32, [P(NvcScene), c_vp, c_vp, c_i32, c_i64, c_i64, c_i32, c_i64, c_i64,
                                  c_u64, c_u64, c_f64, c_vp, c_vp, c_vp, c_vp]),
     "nvc_nls_sample": (c_i32, [P(NvcModel), P(NvcScene), c_vp, c_vp, c_i32, c_vp, c_i64, c_i64, c_i64,
-                               c_i64, c_u64, c_u64, c_f64, c_vp, c_vp, c_vp, c_vp]),
+                               c_i64, c_u64, c_u64, c_f64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "nvc_neural_di": (c_i32, [P(NvcModel), P(NvcScene), c_vp, c_vp, c_vp, c_i32, c_vp, c_i64, c_i64,
-                              c_vp, c_vp]),
+                              c_vp, c_vp, c_vp]),
     "nvc_table_mask": (c_i32, [c_vp, c_i32, c_i64, c_i64, c_i32, c_vp, c_vp]),
     "nvc_gbuffer": (c_i32, [P(NvcScene), P(NvcCamera), c_u64, c_i64, c_i64, c_vp, c_vp, c_vp,
                             c_vp, c_vp, c_vp]),

@@ -19,7 +19,7 @@ OUT = os.path.join(HERE, "libnvc.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
                  "-I", os.path.join(HERE, "..", "include")]
-UNITS = {"geometry.cu": ["-fmad=false"], "model.cu": [], "query.cu": [], "micro.cu": []}
+UNITS = {"geometry.cu": ["-fmad=false"], "model.cu": [], "query.cu": [], "pipeline.cu": [], "micro.cu": []}
 
 
 def nvcc() -> str:

@@ -113,6 +113,10 @@ class VisibilityCache:
         m.table_h, m.wpack = self.table_h.data_ptr(), self.wpack.data_ptr()
         self.model = m
         self._ws = None
+        self._qws = None
+        # "pipeline": decoupled encode -> tcgen05 MLP -> selection (default);
+        # "fused": the single fused kernel
+        self.query_impl = "pipeline"
 
     def _upload(self, table: np.ndarray, net: MLPParams) -> None:
         import torch
@@ -194,19 +198,31 @@ class VisibilityCache:
         out = feats.cpu().numpy()
         return (out, idx.cpu().numpy(), w.cpu().numpy()) if with_ctx else out
 
+    def query_workspace(self, p: int):
+        """Scratch of the decoupled query pipeline (None selects the fused kernel)."""
+        import torch
+        if self.query_impl != "pipeline" or p <= 0:
+            return None
+        need = _lib.load().nvc_query_workspace_bytes(self.model, p)
+        if self._qws is None or self._qws.numel() < need:
+            self._qws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self._qws
+
     def infer_device(self, pos, precision: int | None = None, out=None):
         import torch
         n = pos.shape[0]
         if out is None:
             out = torch.empty((n, self.output_dim), dtype=torch.float32, device=self.device)
         prec = self.precision if precision is None else precision
+        ws = self.query_workspace(n) if prec == PRECISION_FP16 else None
         try:
-            _lib.call("nvc_infer", self.model, pos.data_ptr(), n, prec, out.data_ptr(), _lib.stream_ptr())
+            _lib.call("nvc_infer", self.model, pos.data_ptr(), n, prec, out.data_ptr(), _lib.ptr(ws),
+                      _lib.stream_ptr())
         except _lib.NvcUnsupported:
             if prec != PRECISION_FP16:
                 raise
-            # topology the tcgen05 kernel does not cover (smem/width limits): fp32 CUDA path
-            _lib.call("nvc_infer", self.model, pos.data_ptr(), n, PRECISION_FP32, out.data_ptr(),
+            # topology the tcgen05 kernels do not cover (smem/width limits): fp32 CUDA path
+            _lib.call("nvc_infer", self.model, pos.data_ptr(), n, PRECISION_FP32, out.data_ptr(), None,
                       _lib.stream_ptr())
         return out
 

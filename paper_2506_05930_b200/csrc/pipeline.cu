@@ -1,0 +1,640 @@
+// pipeline.cu -- the decoupled query pipeline (default hot path):
+//
+//   k_enc_tiles   hash-grid encode, one thread per pixel, writes each 128-pixel
+//                 tile's fp16 features as the exact shared-memory image the
+//                 tensor core reads (swizzled K-major, common.cuh umma_off)
+//   k_mlp_tiles   persistent tcgen05 MLP: one bulk copy per feature tile into a
+//                 4-stage ring, four tiles in flight per CTA (TMEM holds four
+//                 accumulators), two epilogue warpgroups ping-ponging their
+//                 tiles; writes fp16 visibilities light-major
+//   k_wrs_tiles   per-pixel FP64 reservoir over the nonzero lights with
+//                 numpy-Philox uniforms (or the Neural-DI sum)
+//
+// Each stage runs at its own occupancy sweet spot (gather-bound encoder with
+// 32+ warps/SM, tensor-pipe-fed MLP, ALU-bound selection), which the single
+// fused kernel (query.cu) cannot: its per-tile chain of gathers, MMA round
+// trips and dependent FP64 work left most issue slots idle.  The price is two
+// HBM round trips of fp16 intermediates (features and visibilities,
+// 2 x 64 B/pixel at K=32).
+//
+// Reference routines: encode_batch hashgrid.py:117-131, forward mlp.py:110-140,
+// clamp_visibility sampling.py:27-30, wrs_select_batch :74-85,
+// nls_sample_batch :194-205, neural_di_batch :215-218.
+#include <cstdlib>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace nvc {
+namespace {
+
+constexpr int kT = 128;   // pixels per tile = UMMA M
+
+__device__ __forceinline__ uint32_t s32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n\t}" ::"r"(s32(bar)),
+        "r"(phase), "r"(1000000u)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     s32(dst)),
+                 "l"(src), "r"(bytes), "r"(s32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ uint64_t desc_of(uint32_t base, int rows, int kp, int kk) {
+    const int lg = umma_sw_log2(kp);
+    const uint32_t kb = (uint32_t)kk * 32u;
+    const uint32_t addr = base + ((kb >> lg) * (uint32_t)rows << lg) + (kb & ((1u << lg) - 1u));
+    const uint64_t layout = lg == 7 ? 2ull : (lg == 6 ? 4ull : 6ull);
+    return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)((8u << lg) >> 4) << 32) |
+           ((uint64_t)1 << 46) | (layout << 61);
+}
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tld16(uint32_t taddr, float v[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---------------------------------------------------------------------------
+// stage 1: encoder -> feature tile images
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cell3(int n, const double q[3], uint32_t c0[3], float f[3]) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {   // floor via round-down add of 2^52 (bit-identical to min(int(x), n-1))
+        const double x = __dmul_rn(q[a], (double)n);
+        const double t = __dadd_rd(x, 0x1p52);
+        uint32_t c = (uint32_t)__double2loint(t);
+        double fr = __dsub_rn(x, __dsub_rn(t, 0x1p52));
+        if (c > (uint32_t)(n - 1)) {
+            c = (uint32_t)(n - 1);
+            fr = 1.0;
+        }
+        c0[a] = c;
+        f[a] = (float)fr;
+    }
+}
+
+template <bool kF2>
+__global__ void __launch_bounds__(kT, 6) k_enc_tiles(GridDev g, const uint16_t* __restrict__ table2,
+                                                     const double* __restrict__ pos, int64_t P, int kp0,
+                                                     uint8_t* __restrict__ tiles) {
+    const int row = threadIdx.x;
+    const int64_t tile = blockIdx.x;
+    const int64_t p = tile * kT + row;
+    uint8_t* img = tiles + tile * (int64_t)(kT * kp0 * 2);
+    if (p >= P) {
+        for (int k = 0; k < kp0; k += 8) *reinterpret_cast<uint4*>(img + umma_off(row, k, kT, kp0)) = make_uint4(0, 0, 0, 0);
+        return;
+    }
+    const double pp[3] = {__ldg(pos + 3 * p), __ldg(pos + 3 * p + 1), __ldg(pos + 3 * p + 2)};
+    double q[3];
+    normalize(g, pp, q);
+    if constexpr (kF2) {
+        const uint2* t2 = reinterpret_cast<const uint2*>(table2);
+        constexpr int LB = 4;
+        for (int l = 0; l < g.L; l += LB) {
+            uint2 v[LB][4];
+            float w[LB][3];
+#pragma unroll
+            for (int j = 0; j < LB; ++j) {
+                if (l + j < g.L) {
+                    uint32_t c0[3];
+                    cell3(g.res[l + j], q, c0, w[j]);
+                    uint32_t sy, sz, mask;
+                    if (g.dense[l + j]) {
+                        sy = (uint32_t)g.res[l + j] + 1u;
+                        sz = sy * sy;
+                        mask = 0xffffffffu;
+                    } else {
+                        sy = 2654435761u;
+                        sz = 805459861u;
+                        mask = g.tmask;
+                    }
+                    const uint32_t base = c0[0] + c0[1] * sy + c0[2] * sz;
+                    const uint2* tl = t2 + (size_t)(l + j) * (size_t)g.T;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) v[j][c] = __ldg(tl + ((base + ((c >> 1) & 1) * sy + (c & 1) * sz) & mask));
+                }
+            }
+            __align__(16) __half2 out[LB];
+#pragma unroll
+            for (int j = 0; j < LB; ++j) {
+                float a = 0.0f, b = 0.0f;
+                if (l + j < g.L) {
+                    const float fx = w[j][0], wy[2] = {1.0f - w[j][1], w[j][1]}, wz[2] = {1.0f - w[j][2], w[j][2]};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const float wyz = wy[(c >> 1) & 1] * wz[c & 1];
+                        const float w0 = (1.0f - fx) * wyz, w1 = fx * wyz;
+                        const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&v[j][c].x));
+                        const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&v[j][c].y));
+                        a = fmaf(w1, f1.x, fmaf(w0, f0.x, a));
+                        b = fmaf(w1, f1.y, fmaf(w0, f0.y, b));
+                    }
+                }
+                out[j] = __floats2half2_rn(a, b);
+            }
+            *reinterpret_cast<uint4*>(img + umma_off(row, 2 * l, kT, kp0)) = *reinterpret_cast<const uint4*>(out);
+        }
+        for (int k = 2 * ((g.L + 3) / 4 * 4); k < kp0; k += 8)
+            *reinterpret_cast<uint4*>(img + umma_off(row, k, kT, kp0)) = make_uint4(0, 0, 0, 0);
+    } else {
+        const __half* t2 = reinterpret_cast<const __half*>(table2);
+        for (int k = 0; k < kp0; ++k) *reinterpret_cast<__half*>(img + umma_off(row, k, kT, kp0)) = __float2half_rn(0.0f);
+        for (int l = 0; l < g.L; ++l) {
+            uint32_t c0[3];
+            float f[3];
+            cell3(g.res[l], q, c0, f);
+            uint32_t sy, sz, mask;
+            if (g.dense[l]) {
+                sy = (uint32_t)g.res[l] + 1u;
+                sz = sy * sy;
+                mask = 0xffffffffu;
+            } else {
+                sy = 2654435761u;
+                sz = 805459861u;
+                mask = g.tmask;
+            }
+            const uint32_t base = c0[0] + c0[1] * sy + c0[2] * sz;
+            const __half* tl = t2 + (size_t)l * (size_t)g.T * 2 * g.F;
+            const float wy[2] = {1.0f - f[1], f[1]}, wz[2] = {1.0f - f[2], f[2]};
+            float acc[8];
+            for (int k = 0; k < g.F; ++k) acc[k] = 0.0f;
+            for (int c = 0; c < 4; ++c) {
+                const uint32_t slot = (base + ((c >> 1) & 1) * sy + (c & 1) * sz) & mask;
+                const float wyz = wy[(c >> 1) & 1] * wz[c & 1];
+                const __half* s2 = tl + (size_t)slot * 2 * g.F;
+                for (int k = 0; k < g.F; ++k)
+                    acc[k] = fmaf(f[0] * wyz, __half2float(__ldg(s2 + g.F + k)),
+                                  fmaf((1.0f - f[0]) * wyz, __half2float(__ldg(s2 + k)), acc[k]));
+            }
+            for (int k = 0; k < g.F; ++k)
+                *reinterpret_cast<__half*>(img + umma_off(row, l * g.F + k, kT, kp0)) = __float2half_rn(acc[k]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// stage 2: persistent tcgen05 MLP over feature tiles
+// ---------------------------------------------------------------------------
+struct MNet {
+    int n_layers;
+    int dims[NVC_MAX_LAYERS + 1];
+    int np[NVC_MAX_LAYERS], kp[NVC_MAX_LAYERS];
+    int wofs[NVC_MAX_LAYERS];     // halfs
+    int64_t boff[NVC_MAX_LAYERS];
+    int wpack_halfs, act_kp, tmem_cols, acc_cols;
+    float alpha;
+    int out_sigmoid;
+    int sm_w, sm_a0, sm_a1, sm_bias, sm_total;
+};
+
+constexpr int kStages = 4, kSlots = 4;
+constexpr int kMlpThreads = 32 * 10;   // warps 0-7 epilogue (2 warpgroups), 8 producer, 9 MMA
+
+struct MBars {
+    uint64_t a0_full[kStages], a0_empty[kStages], acc_full[kSlots], acc_empty[kSlots], a1_full[kSlots];
+};
+
+__global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_tiles(MNet net, const float* __restrict__ params,
+                                                              const uint16_t* __restrict__ wpack,
+                                                              const uint8_t* __restrict__ tiles, int64_t ntiles,
+                                                              int64_t P, __half* __restrict__ vis16, int64_t vstride) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    __shared__ MBars bars;
+    __shared__ uint32_t tbase;
+    uint8_t* smem = smem_raw + ((1024u - (s32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* s_w = smem + net.sm_w;
+    uint8_t* s_a0 = smem + net.sm_a0;
+    uint8_t* s_a1 = smem + net.sm_a1;
+    float* s_bias = reinterpret_cast<float*>(smem + net.sm_bias);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int a0_bytes = kT * net.kp[0] * 2;
+    const int a1_bytes = kT * net.act_kp * 2;
+    const int K = net.dims[net.n_layers];
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(wpack);
+        uint4* dst = reinterpret_cast<uint4*>(s_w);
+        for (int i = tid; i < net.wpack_halfs / 8; i += kMlpThreads) dst[i] = __ldg(src + i);
+        int bo = 0;
+        for (int l = 0; l < net.n_layers; ++l) {
+            for (int n = tid; n < net.np[l]; n += kMlpThreads)
+                s_bias[bo + n] = n < net.dims[l + 1] ? __ldg(params + net.boff[l] + n) : 0.0f;
+            bo += net.np[l];
+        }
+    }
+    if (warp == 9) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(&tbase)),
+                     "r"(net.tmem_cols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&bars.a0_full[s], 1);
+            mbar_init(&bars.a0_empty[s], 1);
+        }
+        for (int j = 0; j < kSlots; ++j) {
+            mbar_init(&bars.acc_full[j], 1);
+            mbar_init(&bars.acc_empty[j], 128);
+            mbar_init(&bars.a1_full[j], 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    fence_async();
+    tc_before();
+    __syncthreads();
+    tc_after();
+    const uint32_t tmem = tbase;
+    const int n_local = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+
+    if (warp == 8) {
+        // ---------------- producer: one bulk copy per feature tile ----------------
+        if (lane == 0) {
+            for (int i = 0; i < n_local; ++i) {
+                const int s = i % kStages;
+                if (i >= kStages) mbar_wait(&bars.a0_empty[s], ((i / kStages) - 1) & 1);
+                mbar_expect_tx(&bars.a0_full[s], (uint32_t)a0_bytes);
+                const int64_t tile = blockIdx.x + (int64_t)i * gridDim.x;
+                bulk_g2s(s_a0 + s * a0_bytes, tiles + tile * a0_bytes, (uint32_t)a0_bytes, &bars.a0_full[s]);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 9) {
+        // ---------------- MMA issuer: quads of 4 tiles, layers interleaved ----------------
+        if (lane == 0) {
+            const uint32_t w_addr = s32(s_w), a0_addr = s32(s_a0), a1_addr = s32(s_a1);
+            uint32_t a1_cnt[kSlots] = {0, 0, 0, 0};
+            auto issue = [&](int l, int j, uint32_t a_addr) {
+                tc_after();
+                const uint32_t idesc = (1u << 4) | ((uint32_t)(net.np[l] >> 3) << 17) | ((uint32_t)(kT >> 4) << 24);
+                const uint32_t b = w_addr + 2u * (uint32_t)net.wofs[l];
+                const uint32_t d = tmem + (uint32_t)(j * net.acc_cols);
+                for (int kk = 0; kk < net.kp[l] / 16; ++kk)
+                    mma(d, desc_of(a_addr, kT, net.kp[l], kk), desc_of(b, net.np[l], net.kp[l], kk), idesc,
+                        kk > 0 ? 1u : 0u);
+            };
+            for (int q0 = 0; q0 < n_local; q0 += kSlots) {
+                const int nq = min(kSlots, n_local - q0);
+                for (int j = 0; j < nq; ++j) {
+                    const int i = q0 + j, s = i % kStages;
+                    mbar_wait(&bars.a0_full[s], (i / kStages) & 1);
+                    if (q0 >= kSlots) mbar_wait(&bars.acc_empty[j], ((q0 / kSlots) - 1) & 1);
+                    issue(0, j, a0_addr + (uint32_t)(s * a0_bytes));
+                    commit(&bars.a0_empty[s]);
+                    commit(&bars.acc_full[j]);
+                }
+                for (int l = 1; l < net.n_layers; ++l)
+                    for (int j = 0; j < nq; ++j) {
+                        mbar_wait(&bars.a1_full[j], a1_cnt[j] & 1);
+                        ++a1_cnt[j];
+                        issue(l, j, a1_addr + (uint32_t)(j * a1_bytes));
+                        commit(&bars.acc_full[j]);
+                    }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- epilogue: warpgroup eg serves slots eg and eg+2 ----------------
+        const int eg = warp >> 2, row = tid & 127;
+        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        uint32_t acc_cnt[2] = {0, 0};
+        for (int q0 = 0; q0 < n_local; q0 += kSlots) {
+            const int nq = min(kSlots, n_local - q0);
+            int bias_off = 0;
+            for (int l = 0; l < net.n_layers; ++l) {
+                for (int jj = 0; jj < 2; ++jj) {
+                    const int j = eg + 2 * jj;
+                    if (j >= nq) continue;
+                    const uint32_t t_acc = tmem + lane_base + (uint32_t)(j * net.acc_cols);
+                    mbar_wait(&bars.acc_full[j], acc_cnt[jj] & 1);
+                    ++acc_cnt[jj];
+                    tc_after();
+                    if (l < net.n_layers - 1) {
+                        uint8_t* a1 = s_a1 + j * a1_bytes;
+                        for (int c = 0; c < net.np[l] / 16; ++c) {
+                            float v[16];
+                            tld16(t_acc + (uint32_t)(c * 16), v);
+                            __align__(16) __half2 h[8];
+                            const float2* bb = reinterpret_cast<const float2*>(s_bias + bias_off + c * 16);
+                            const __half2 al = __float2half2_rn(net.alpha);
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) {
+                                const float2 bj = bb[e];
+                                const __half2 z = __floats2half2_rn(v[2 * e] + bj.x, v[2 * e + 1] + bj.y);
+                                h[e] = __hmax2(z, __hmul2(z, al));
+                            }
+                            *reinterpret_cast<uint4*>(a1 + umma_off(row, c * 16, kT, net.np[l])) =
+                                *reinterpret_cast<const uint4*>(h);
+                            *reinterpret_cast<uint4*>(a1 + umma_off(row, c * 16 + 8, kT, net.np[l])) =
+                                *reinterpret_cast<const uint4*>(h + 4);
+                        }
+                        fence_async();
+                        tc_before();
+                        mbar_arrive(&bars.a1_full[j]);
+                    } else {
+                        const int64_t tile = blockIdx.x + (int64_t)(q0 + j) * gridDim.x;
+                        const int64_t p = tile * kT + row;
+                        for (int c = 0; c < net.np[l] / 16; ++c) {
+                            float v[16];
+                            tld16(t_acc + (uint32_t)(c * 16), v);
+                            if (p >= P) continue;
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) {
+                                const int k = c * 16 + e;
+                                if (k >= K) break;
+                                const float z = v[e] + s_bias[bias_off + k];
+                                float a;
+                                if (net.out_sigmoid) {
+                                    const float ez = __expf(-fabsf(z));
+                                    const float r = __fdividef(1.0f, 1.0f + ez);
+                                    a = z >= 0.0f ? r : ez * r;
+                                    a = fminf(fmaxf(a, 1e-6f), 0.999999f);
+                                } else {
+                                    a = z >= 0.0f ? z : net.alpha * z;
+                                }
+                                vis16[(int64_t)k * vstride + p] = __float2half_rn(a);
+                            }
+                        }
+                        tc_before();
+                        mbar_arrive(&bars.acc_empty[j]);
+                    }
+                }
+                bias_off += net.np[l];
+            }
+        }
+    }
+    tc_before();
+    __syncthreads();
+    tc_after();
+    if (warp == 9)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(net.tmem_cols) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// stage 3: WRS / Neural DI from fp16 visibilities
+// ---------------------------------------------------------------------------
+__device__ __noinline__ U4 philox_fn(uint64_t counter, uint64_t key) { return philox_block(counter, key); }
+
+struct WArgs {
+    const __half* vis16;
+    int64_t vstride;
+    const void* lum;       // light-major f32/f64 (lum for NLS, factor for NDI)
+    int lum_f64;
+    int64_t stride;
+    const uint32_t* nz_mask;
+    int64_t P, p_first, p_total;
+    int K;
+    uint64_t key, offset;
+    double floor;
+    int64_t* ids;
+    double* pts;
+    double* big_w;
+    const double* albedo;
+    double* rgb;
+};
+
+template <bool kNls>
+__global__ void __launch_bounds__(256) k_wrs_tiles(WArgs a, nvc_scene sc) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= a.P) return;
+    const int64_t gp = a.p_first + p;
+    uint32_t m = 0xffffffffu;
+    if (a.nz_mask && a.K <= 32) m = __ldg(a.nz_mask + p);
+    if (a.K < 32) m &= (1u << a.K) - 1u;
+    double s = 0.0, wsel = 0.0, rgb[3] = {0.0, 0.0, 0.0};
+    int sel = -1;
+    uint64_t blk = 0;
+    U4 u;
+    for (int k0 = 0; k0 < a.K; k0 += 32) {
+        uint32_t mm = a.K <= 32 ? m : (a.K - k0 >= 32 ? 0xffffffffu : (1u << (a.K - k0)) - 1u);
+        while (mm) {
+            const int k = k0 + __ffs(mm) - 1;
+            mm &= mm - 1;
+            const float vis = __half2float(__ldg(a.vis16 + (int64_t)k * a.vstride + p));
+            const int64_t li = (int64_t)k * a.stride + p;
+            const double t = a.lum_f64 ? __ldg(reinterpret_cast<const double*>(a.lum) + li)
+                                       : (double)__ldg(reinterpret_cast<const float*>(a.lum) + li);
+            if (kNls) {
+                double vv = (double)vis;
+                vv = a.floor > 0.0 ? fmax(vv, a.floor) : fmax(vv, 0.0);
+                const double w = __dmul_rn(vv, t);
+                s = __dadd_rn(s, w);
+                if (w > 0.0) {   // zero weights never need a uniform (u*s < 0 is impossible)
+                    const uint64_t n = a.offset + (uint64_t)gp * (uint64_t)a.K + (uint64_t)k;
+                    const uint64_t bi = n / 4 + 1;
+                    if (bi != blk) {
+                        u = philox_fn(bi, a.key);
+                        blk = bi;
+                    }
+                    if (__dmul_rn(u01(u.x[n & 3]), s) < w) {
+                        sel = k;
+                        wsel = w;
+                    }
+                }
+            } else {
+                const double wk = __dmul_rn((double)vis, t);
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) rgb[ch] = __dadd_rn(rgb[ch], __dmul_rn(wk, __ldg(sc.lt_radiance + 3 * k + ch)));
+            }
+        }
+    }
+    if (kNls) {
+        const uint64_t n = a.offset + (uint64_t)a.p_total * (uint64_t)a.K + 2ull * (uint64_t)gp;
+        const U4 b0 = philox_fn(n / 4 + 1, a.key);
+        const double u0 = u01(b0.x[n & 3]);
+        double u1;
+        if ((n & 3) != 3) {
+            u1 = u01(b0.x[(n & 3) + 1]);
+        } else {
+            const U4 b1 = philox_fn(n / 4 + 2, a.key);
+            u1 = u01(b1.x[0]);
+        }
+        double y[3];
+        light_point(sc, sel, u0, u1, y);
+        a.ids[p] = sel;
+        a.big_w[p] = sel >= 0 ? __ddiv_rn(s, wsel > 0.0 ? wsel : 1.0) : 0.0;
+        a.pts[3 * p] = y[0];
+        a.pts[3 * p + 1] = y[1];
+        a.pts[3 * p + 2] = y[2];
+    } else {
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) a.rgb[3 * p + ch] = __ddiv_rn(__dmul_rn(rgb[ch], a.albedo[3 * p + ch]), 3.141592653589793);
+    }
+}
+
+// fp16 light-major visibilities -> (P, K) f32 (the infer() output)
+__global__ void k_vis_out(const __half* __restrict__ vis16, int64_t vstride, int64_t P, int K, float* __restrict__ out) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    for (int k = 0; k < K; ++k) out[p * K + k] = __half2float(vis16[(int64_t)k * vstride + p]);
+}
+
+int make_mnet(const nvc_model* m, MNet& q) {
+    NVC_REQUIRE(m && m->params && m->table_h && m->wpack, "pipeline: model state not bound");
+    q.n_layers = m->n_layers;
+    for (int i = 0; i <= m->n_layers; ++i) {
+        q.dims[i] = m->dims[i];
+        if (m->dims[i] > 256) {
+            set_error("pipeline: layer widths must be <= 256");
+            return NVC_ERR_UNSUPPORTED;
+        }
+    }
+    umma_pads(m->dims, m->n_layers, q.np, q.kp);
+    int64_t wo = 0, bo = (int64_t)m->levels * m->table_size * m->features;
+    int hid = 16, maxnp = 16, nb = 0;
+    for (int i = 0; i < m->n_layers; ++i) {
+        if (q.np[i] > 256 || q.kp[i] > 256) {
+            set_error("pipeline: padded widths must be <= 256");
+            return NVC_ERR_UNSUPPORTED;
+        }
+        q.wofs[i] = (int)wo;
+        wo += umma_block_halfs(q.np[i], q.kp[i]);
+        bo += (int64_t)m->dims[i + 1] * m->dims[i];
+        q.boff[i] = bo;
+        bo += m->dims[i + 1];
+        if (i >= 1 && q.kp[i] > hid) hid = q.kp[i];
+        if (q.np[i] > maxnp) maxnp = q.np[i];
+        nb += q.np[i];
+    }
+    q.wpack_halfs = (int)wo;
+    q.act_kp = hid;
+    int col = 32;
+    while (col < maxnp) col <<= 1;
+    q.acc_cols = col;
+    q.tmem_cols = col * kSlots;
+    if (q.tmem_cols > 512) {
+        set_error("pipeline: %d TMEM columns needed", q.tmem_cols);
+        return NVC_ERR_UNSUPPORTED;
+    }
+    q.alpha = m->alpha;
+    q.out_sigmoid = m->out_sigmoid;
+    q.sm_w = 0;
+    q.sm_a0 = (q.wpack_halfs * 2 + 1023) / 1024 * 1024;
+    q.sm_a1 = q.sm_a0 + kStages * ((kT * q.kp[0] * 2 + 1023) / 1024 * 1024);
+    q.sm_bias = q.sm_a1 + kSlots * ((kT * q.act_kp * 2 + 1023) / 1024 * 1024);
+    q.sm_total = q.sm_bias + (nb * 4 + 127) / 128 * 128 + 1024;
+    if (q.sm_total > 226 * 1024) {
+        set_error("pipeline: %d bytes of shared memory needed", q.sm_total);
+        return NVC_ERR_UNSUPPORTED;
+    }
+    return NVC_OK;
+}
+
+inline int grid1(int64_t n, int bs) { return (int)((n + bs - 1) / bs); }
+
+// encode + MLP: vis16 (K rows of vstride halfs); ws holds the feature tiles
+int run_front(const nvc_model* m, const double* pos, int64_t P, uint8_t* tiles, __half* vis16, int64_t vstride,
+              cudaStream_t s) {
+    MNet q;
+    int rc = make_mnet(m, q);
+    if (rc) return rc;
+    GridDev g = grid_of(m);
+    const int64_t ntiles = (P + kT - 1) / kT;
+    if (g.F == 2)
+        k_enc_tiles<true><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
+    else
+        k_enc_tiles<false><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
+    rc = check_launch("k_enc_tiles");
+    if (rc) return rc;
+    cudaFuncSetAttribute(k_mlp_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, q.sm_total);
+    int dev = 0, sms = kNumSMs;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int grid = (int)(ntiles < sms ? ntiles : sms);
+    if (const char* e = getenv("NVC_QUERY_GRID")) grid = max(1, min(grid, atoi(e)));
+    k_mlp_tiles<<<grid, kMlpThreads, q.sm_total, s>>>(q, m->params, m->wpack, tiles, ntiles, P, vis16, vstride);
+    return check_launch("k_mlp_tiles");
+}
+
+}  // namespace
+
+int64_t pipeline_workspace_bytes(const nvc_model* m, int64_t P) {
+    const int kp0 = umma_kpad(m->levels * m->features);
+    const int64_t ntiles = (P + kT - 1) / kT;
+    const int64_t vstride = (P + 63) / 64 * 64;
+    return ntiles * kT * kp0 * 2 + (int64_t)m->dims[m->n_layers] * vstride * 2 + 1024;
+}
+
+int pipeline_query(const nvc_model* m, const nvc_scene* sc, const double* pos, int64_t P, int mode,
+                   const void* lum, int lum_f64, int64_t stride, const uint32_t* nz_mask, int64_t p_first, int64_t p_total,
+                   uint64_t key, uint64_t offset, double floor, int64_t* ids, double* pts, double* big_w,
+                   const double* albedo, double* rgb, float* vis_out, void* ws, cudaStream_t s) {
+    const int kp0 = umma_kpad(m->levels * m->features);
+    const int64_t ntiles = (P + kT - 1) / kT;
+    const int64_t vstride = (P + 63) / 64 * 64;
+    uint8_t* tiles = reinterpret_cast<uint8_t*>(ws);
+    __half* vis16 = reinterpret_cast<__half*>(tiles + (ntiles * kT * kp0 * 2 + 255) / 256 * 256);
+    int rc = run_front(m, pos, P, tiles, vis16, vstride, s);
+    if (rc) return rc;
+    const int K = m->dims[m->n_layers];
+    if (mode == 0) {
+        k_vis_out<<<grid1(P, 256), 256, 0, s>>>(vis16, vstride, P, K, vis_out);
+        return check_launch("k_vis_out");
+    }
+    WArgs a;
+    memset(&a, 0, sizeof a);
+    a.vis16 = vis16;
+    a.vstride = vstride;
+    a.lum = lum;
+    a.lum_f64 = lum_f64;
+    a.stride = stride;
+    a.nz_mask = nz_mask;
+    a.P = P;
+    a.p_first = p_first;
+    a.p_total = p_total;
+    a.K = K;
+    a.key = key;
+    a.offset = offset;
+    a.floor = floor;
+    a.ids = ids;
+    a.pts = pts;
+    a.big_w = big_w;
+    a.albedo = albedo;
+    a.rgb = rgb;
+    if (mode == 1)
+        k_wrs_tiles<true><<<grid1(P, 256), 256, 0, s>>>(a, *sc);
+    else
+        k_wrs_tiles<false><<<grid1(P, 256), 256, 0, s>>>(a, *sc);
+    return check_launch("k_wrs_tiles");
+}
+
+}  // namespace nvc

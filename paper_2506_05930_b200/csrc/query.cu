@@ -1154,16 +1154,30 @@ int launch_query(const nvc_model* m, const double* pos, int64_t P, const nvc_sce
 
 }  // namespace
 
+int64_t pipeline_workspace_bytes(const nvc_model* m, int64_t P);
+int pipeline_query(const nvc_model* m, const nvc_scene* sc, const double* pos, int64_t P, int mode,
+                   const void* lum, int lum_f64, int64_t stride, const uint32_t* nz_mask, int64_t p_first, int64_t p_total,
+                   uint64_t key, uint64_t offset, double floor, int64_t* ids, double* pts, double* big_w,
+                   const double* albedo, double* rgb, float* vis_out, void* ws, cudaStream_t s);
+
 }  // namespace nvc
 
 using namespace nvc;
 
 extern "C" {
 
-int nvc_infer(const nvc_model* m, const double* pos, int64_t n, int32_t precision, float* out, void* stream) {
+int64_t nvc_query_workspace_bytes(const nvc_model* m, int64_t p) {
+    return (m && p > 0) ? pipeline_workspace_bytes(m, p) : 0;
+}
+
+int nvc_infer(const nvc_model* m, const double* pos, int64_t n, int32_t precision, float* out, void* workspace,
+              void* stream) {
     if (n <= 0) return NVC_OK;
     NVC_REQUIRE(m && pos && out, "nvc_infer: null argument");
     if (precision == 0) return nvc_infer_f32(m, pos, n, out, (cudaStream_t)stream);
+    if (workspace)
+        return pipeline_query(m, nullptr, pos, n, 0, nullptr, 0, 0, nullptr, 0, n, 0, 0, 0.0, nullptr, nullptr, nullptr,
+                              nullptr, nullptr, out, workspace, (cudaStream_t)stream);
     QOut o;
     memset(&o, 0, sizeof o);
     o.mode = kModeVis;
@@ -1174,10 +1188,14 @@ int nvc_infer(const nvc_model* m, const double* pos, int64_t n, int32_t precisio
 int nvc_nls_sample(const nvc_model* m, const nvc_scene* sc, const double* pos, const void* lum, int32_t lum_f64,
                    const uint32_t* nz_mask, int64_t stride, int64_t p, int64_t p_first, int64_t p_total,
                    uint64_t key, uint64_t offset, double floor, int64_t* ids, double* pts, double* big_w,
-                   void* stream) {
+                   void* workspace, void* stream) {
     NVC_REQUIRE(m && sc && pos && lum && ids && pts && big_w, "nvc_nls_sample: null argument");
     NVC_REQUIRE(sc->n_lights == m->dims[m->n_layers], "nvc_nls_sample: output_dim != scene lights");
     NVC_REQUIRE(stride >= p && p_total >= p_first + p, "nvc_nls_sample: bad stride / frame size");
+    if (p <= 0) return NVC_OK;
+    if (workspace)
+        return pipeline_query(m, sc, pos, p, 1, lum, lum_f64, stride, nz_mask, p_first, p_total, key, offset, floor, ids, pts,
+                              big_w, nullptr, nullptr, nullptr, workspace, (cudaStream_t)stream);
     QOut o;
     memset(&o, 0, sizeof o);
     o.mode = kModeNls;
@@ -1198,9 +1216,13 @@ int nvc_nls_sample(const nvc_model* m, const nvc_scene* sc, const double* pos, c
 
 int nvc_neural_di(const nvc_model* m, const nvc_scene* sc, const double* pos, const double* albedo,
                   const void* factor, int32_t factor_f64, const uint32_t* nz_mask, int64_t stride, int64_t p,
-                  double* rgb, void* stream) {
+                  double* rgb, void* workspace, void* stream) {
     NVC_REQUIRE(m && sc && pos && albedo && factor && rgb, "nvc_neural_di: null argument");
     NVC_REQUIRE(sc->n_lights == m->dims[m->n_layers], "nvc_neural_di: output_dim != scene lights");
+    if (p <= 0) return NVC_OK;
+    if (workspace)
+        return pipeline_query(m, sc, pos, p, 2, factor, factor_f64, stride, nz_mask, 0, p, 0, 0, 0.0, nullptr, nullptr, nullptr,
+                              albedo, rgb, nullptr, workspace, (cudaStream_t)stream);
     QOut o;
     memset(&o, 0, sizeof o);
     o.mode = kModeNdi;

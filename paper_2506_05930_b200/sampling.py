@@ -242,7 +242,8 @@ def nls_sample_device(ctx: PixelCtx, cache, key: int, offset: int = 0, clamp_flo
             raise ValueError(f"cache has {cache.output_dim} outputs, scene has {k} lights")
         _lib.call("nvc_nls_sample", cache.model, ctx.dscene.struct, ctx.pos.data_ptr(), lum.data_ptr(), lum64,
                   _lib.ptr(ctx.mask_device("lum")), lum.shape[1], p, p_first, total, key, offset, floor,
-                  ids.data_ptr(), pts.data_ptr(), big_w.data_ptr(), _lib.stream_ptr())
+                  ids.data_ptr(), pts.data_ptr(), big_w.data_ptr(), _lib.ptr(cache.query_workspace(p)),
+                  _lib.stream_ptr())
     else:
         vis = cache.infer(ctx.positions)
         vis = vis if isinstance(vis, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(vis, np.float32))
@@ -276,7 +277,7 @@ def neural_di_device(ctx: PixelCtx, cache, out=None):
         fac = ctx.factor_device()
         _lib.call("nvc_neural_di", cache.model, ctx.dscene.struct, ctx.pos.data_ptr(), ctx.alb.data_ptr(),
                   fac.data_ptr(), int(fac.dtype == torch.float64), _lib.ptr(ctx.mask_device("factor")),
-                  fac.shape[1], p, out.data_ptr(), _lib.stream_ptr())
+                  fac.shape[1], p, out.data_ptr(), _lib.ptr(cache.query_workspace(p)), _lib.stream_ptr())
         return out
     vis = cache.infer(ctx.positions)
     out.copy_(torch.from_numpy(ctx.unshadowed_rgb(np.asarray(vis, np.float64))))
