@@ -26,6 +26,7 @@ host cores with the same workload definition (bounded sample, extrapolated).
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -42,6 +43,10 @@ sys.path.insert(0, ROOT)
 WIDTH, HEIGHT, K = 1920, 1080, 32
 LEVELS, TABLE, FEATS, HIDDEN = 16, 1 << 19, 2, (64, 64, 64)
 N_WORLD = N_SCREEN = 4096
+# our kernels per online frame: k_world, k_screen_round0, k_screen_finish, k_targets,
+# k_tr_encode, k_train3, k_tr_scatter, k_reduce_parts, k_adam_bulk, k_adam_mlp,
+# k_enc_tiles, k_mlp_tiles, k_nls32
+LAUNCHES_PER_FRAME = 13
 METRIC = "visibility queries/s (encode+MLP+WRS) at 1080p x 32 lights; train samples/s"
 UNIT = "queries/s"
 
@@ -103,13 +108,16 @@ class ClockSampler:
 # CPU side: the oracle port of the reference (cpu_baseline and --impl reference)
 # ---------------------------------------------------------------------------
 
+_CPU_STATE = {}   # (scene arrays, cache, G-buffer sample) inherited by forked workers
+
+
 def _oracle_query_chunk(args):
     """Encode+MLP+WRS for a pixel chunk on one host core (oracle restatement)."""
     from oracle import vc_oracle as O
-    state, pos, lum, key, p_first, p_total = args
-    sa, cache = state
-    vis = cache.infer(pos)
-    return O.nls_sample(sa, vis, lum, key, p_total=p_total, p_first=p_first)
+    lo, hi, key, p_first, p_total = args
+    st = _CPU_STATE
+    vis = st["cache"].infer(st["pos"][lo:hi])
+    return O.nls_sample(st["sa"], vis, st["lum"][lo:hi], key, p_total=p_total, p_first=p_first)
 
 
 def cpu_reference(sample_pixels: int = 24576, procs: int | None = None, repeats: int = 1) -> dict:
@@ -140,20 +148,21 @@ def cpu_reference(sample_pixels: int = 24576, procs: int | None = None, repeats:
     lum = sa.lum(sa.factors(gb["position"], gb["normal"]), gb["albedo"])
     key = O.stream_key(0, 0, "light-select")
     best_train, best_query = float("inf"), float("inf")
-    chunks = np.array_split(np.arange(sample_pixels), procs)
+    bounds = [(int(c[0]), int(c[-1]) + 1) for c in np.array_split(np.arange(sample_pixels), procs) if c.size]
     ctx = mp.get_context("fork")
-    with ctx.Pool(procs) as pool:
-        pool.map(_oracle_query_chunk, [((sa, cache), gb["position"][c[:8]], lum[c[:8]], key, 0, p_total)
-                                       for c in chunks if c.size])   # warm-up (fork + numpy)
-        for rep in range(repeats):
-            t0 = time.perf_counter()
-            pos, tgt = O.train_batch(sa, 0, rep)
-            cache.train_step(pos, tgt)
-            t1 = time.perf_counter()
-            pool.map(_oracle_query_chunk, [((sa, cache), gb["position"][c], lum[c], key, int(c[0]), p_total)
-                                           for c in chunks if c.size])
+    for rep in range(repeats):
+        t0 = time.perf_counter()
+        pos, tgt = O.train_batch(sa, 0, rep)
+        cache.train_step(pos, tgt)
+        t1 = time.perf_counter()
+        # workers fork after the step and inherit the trained cache (no pickling of 16.8 M parameters)
+        _CPU_STATE.update(sa=sa, cache=cache, pos=gb["position"], lum=lum)
+        with ctx.Pool(procs) as pool:
+            pool.map(_oracle_query_chunk, [(lo, lo + 1, key, lo, p_total) for lo, _ in bounds])   # warm-up
             t2 = time.perf_counter()
-            best_train, best_query = min(best_train, t1 - t0), min(best_query, t2 - t1)
+            pool.map(_oracle_query_chunk, [(lo, hi, key, lo, p_total) for lo, hi in bounds])
+            t3 = time.perf_counter()
+        best_train, best_query = min(best_train, t1 - t0), min(best_query, t3 - t2)
     frame_s = best_train + best_query * (p_total / sample_pixels)
     return {"value": p_total / frame_s, "unit": UNIT, "cores": procs, "kind": "port",
             "sample": (f"oracle port (numpy + serial C geometry) on host: 1 full train step "
@@ -172,6 +181,7 @@ def gpu_arm(args) -> None:
     import torch.distributed as dist
 
     from paper_2506_05930_b200 import MODE_LIGHTS, HashGridConfig, TrainFrameConfig, VisibilityCache
+    from paper_2506_05930_b200 import _lib
     from paper_2506_05930_b200 import rng as R
     from paper_2506_05930_b200.render import gbuffer_device
     from paper_2506_05930_b200.sampling import PixelCtx, nls_sample_device
@@ -197,7 +207,7 @@ def gpu_arm(args) -> None:
     grid = HashGridConfig(levels=LEVELS, table_size=TABLE, features_per_level=FEATS, aabb_min=scene.aabb_min,
                           aabb_max=scene.aabb_max)
     cache = VisibilityCache(MODE_LIGHTS, K, grid, seed=0, hidden_dims=HIDDEN, device=dev)
-    if not os.environ.get("NVC_NO_L2_PIN"):
+    if os.environ.get("NVC_L2_PIN"):      # measured slower (it starves the streaming Adam of L2)
         cache.pin_table_in_l2()
     cfg = TrainFrameConfig(n_world=N_WORLD * world, n_screen=N_SCREEN * world, seed=0)
     bufs = BatchBuffers(cfg.n_world, cfg.n_screen, K, dev, world)
@@ -236,13 +246,19 @@ def gpu_arm(args) -> None:
     barrier()
     assert int(bufs.n_rows.item()) == cfg.n_world + cfg.n_screen, "screen rays missed: batch shrank"
 
-    # ---- per-stage split (separate pass, events between stages) ----
-    split_train, split_query = [], []
+    # ---- per-stage split (separate pass, events between stages and between
+    #      the three query kernels, all on the launching stream) ----
+    split_train, split_query, split_k = [], [], []
+    kms = (ctypes.c_float * 3)()
     for f in range(min(args.steps, 10)):
+        _lib.call("nvc_profile_stages", 1)
         frame(1000 + f, timed_parts=True)
+        _lib.call("nvc_profile_stages", 0)
         marks[2].synchronize()
+        _lib.call("nvc_profile_stage_ms", ctypes.addressof(kms))
         split_train.append(marks[0].elapsed_time(marks[1]))
         split_query.append(marks[1].elapsed_time(marks[2]))
+        split_k.append(list(kms))
 
     # ---- timed region: K frames, inputs resident ----
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -284,17 +300,26 @@ def gpu_arm(args) -> None:
         hbm, tflops, src = peaks()
         q_ms = statistics.median(split_query)
         tr_ms = statistics.median(split_train)
-        # dominant kernel: the fused query (k_query).  Algorithmic HBM bytes per
-        # pixel: pos 24 + lum 32*4 + ids 8 + point 24 + W 8 = 192 B.
-        q_bytes = P * (24 + K * 4 + 8 + 24 + 8)
-        achieved = q_bytes / (q_ms * 1e-3) / 1e9
-        gather_gbs = P * LEVELS * 8 * FEATS * 2 / (q_ms * 1e-3) / 1e9
-        mlp_tflops = P * 2 * (32 * 64 + 64 * 64 * 2 + 64 * 32) / (q_ms * 1e-3) / 1e12
+        k_ms = [statistics.median(x[i] for x in split_k) for i in range(3)]
+        # roofline of each query kernel: algorithmic work per launch / its event-timed duration
+        # (DESIGN.md section 4 gives the per-pixel figures)
+        flop_px = 2 * sum(a * b for a, b in zip((32, 64, 64, 64), (64, 64, 64, 32)))
+        kern = {
+            "k_enc_tiles": ("hbm", P * (24 + 64), k_ms[0]),              # pos in, fp16 feature tile out
+            "k_mlp_tiles": ("tensor", P * flop_px, k_ms[1]),             # 24,576 flop per pixel
+            "k_nls32": ("hbm", P * (64 + 4 * K + 4 + 40), k_ms[2]),      # vis + lum + mask in, id/W/point out
+        }
+        name = max(kern, key=lambda k: kern[k][2])
+        bound, work, kms = kern[name]
+        if bound == "tensor":
+            achieved, peak, unit = work / (kms * 1e-3) / 1e12, tflops, "TFLOP/s"
+        else:
+            achieved, peak, unit = work / (kms * 1e-3) / 1e9, hbm, "GB/s"
         traffic = None
-        prof = os.path.join(ROOT, "profiles", "query_dram_bytes.json")
+        prof = os.path.join(ROOT, "profiles", "kernel_dram_bytes.json")
         if os.path.exists(prof):
             try:
-                traffic = json.load(open(prof)).get("bytes_per_launch")
+                traffic = json.load(open(prof)).get(name)
             except Exception:
                 traffic = None
         clk = clocks.summary()
@@ -308,18 +333,19 @@ def gpu_arm(args) -> None:
                        "train_samples_per_s": (N_WORLD + N_SCREEN) * world / (ms * 1e-3),
                        "pixels_per_gpu": P, "global_batch": (N_WORLD + N_SCREEN) * world,
                        "parallelism": f"dp{world} (train) + {world} screen tiles (query)",
-                       "l2": "inputs > L2 every frame (lum table 265 MB + G-buffer positions 50 MB streamed); "
-                             "fp16 hash table (33.6 MB) L2-resident by design",
-                       "stage_ms": {"train_frame": tr_ms, "query": q_ms}},
+                       "l2": "inputs > L2 every frame (lum table 265 MB + 16.8 M-parameter Adam stream 530 MB)",
+                       "stage_ms": {"train_frame": tr_ms, "query": q_ms, "k_enc_tiles": k_ms[0],
+                                    "k_mlp_tiles": k_ms[1], "k_nls32": k_ms[2]}},
             "e2e": {"value": P * world / (e2e_ms * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": int(pos_host.numel() * 8),
                     "d2h_bytes_per_step": int(sum(h.numel() * h.element_size() for h in outs_host) + 8)},
-            "gpu_launches": 9 * args.steps,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic, "kernel": "k_query (fused NLS)",
-                         "peak_source": src, "algorithmic_bytes_per_launch": q_bytes,
-                         "l2_gather_payload_gbs": gather_gbs, "mlp_tflops": mlp_tflops,
-                         "mlp_frac_of_bf16_peak": mlp_tflops / tflops},
+            "gpu_launches": LAUNCHES_PER_FRAME * args.steps,
+            "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+                         "traffic": traffic, "kernel": name, "peak_source": src,
+                         "work_per_launch": work, "launch_ms": kms,
+                         "all": {k: {"bound": v[0], "ms": v[2],
+                                     "frac": (v[1] / (v[2] * 1e-3) / (1e12 * tflops if v[0] == "tensor" else 1e9 * hbm))}
+                                 for k, v in kern.items()}},
             "clocks": clk,
         }
         if world == 1 and not args.no_cpu_baseline:

@@ -28,7 +28,7 @@ extern "C" {
 
 #define NVC_MAX_LEVELS 32
 #define NVC_MAX_LAYERS 8
-#define NVC_ABI_VERSION 1
+#define NVC_ABI_VERSION 2
 
 typedef enum {
     NVC_OK = 0,
@@ -61,7 +61,6 @@ typedef struct {
     float *params;                        /* f32 master parameters, param_count */
     float *adam_m, *adam_v;               /* f32 Adam moments, param_count */
     int64_t *grad_fx;                     /* fixed-point gradient accumulator, param_count */
-    uint16_t *touched;                    /* per-table-entry epoch map, L*T */
     uint16_t *table_h;                    /* fp16 query table, x-pair layout: slot e = (f[e], f[next(e)]), 2*L*T*F */
     uint16_t *wpack;                      /* fp16 weights in the tcgen05 K-major core-matrix layout */
     int64_t param_count;
@@ -107,8 +106,12 @@ int64_t nvc_train_workspace_bytes(const nvc_model *m, int64_t b);
 /* Pin [ptr, ptr+bytes) (the fp16 hash table) in the persisting L2 carve-out
  * for kernels launched on `stream` (best effort; no-op if unsupported). */
 int nvc_l2_persist(const void *ptr, int64_t bytes, void *stream);
-/* Profiling aid: copy out / reset the query kernel's event trace. */
-int nvc_debug_trace(uint64_t *host_out, int32_t n, int32_t reset);
+/* Profiling aid: while enabled, the fp16 query (nvc_nls_sample /
+ * nvc_neural_di / nvc_infer precision 1) records library-owned events on its
+ * stream around its three kernels; nvc_profile_stage_ms waits for the last
+ * query and returns the encoder, MLP and selection kernel times (ms). */
+int nvc_profile_stages(int32_t enable);
+int nvc_profile_stage_ms(float *ms3);
 
 /* ---- state ------------------------------------------------------------ */
 /* Rebuild table_h and wpack from params (after loading / setting params). */
@@ -121,18 +124,18 @@ int nvc_encode(const nvc_model *m, const double *pos, int64_t n, float *feats,
                int32_t *idx_out, double *w_out, void *stream);
 
 /* ---- inference: cache.py:54-58 (VisibilityCache.infer) ---------------- */
-/* precision 0: f32 SIMT (parity: f32 table + f32 weights);
- * precision 1: fused fp16 table + tcgen05/TMEM MLP (fp32 accumulate). */
+/* precision 0: f32 SIMT (parity: f32 table + f32 weights; workspace unused);
+ * precision 1: fp16 table + tcgen05/TMEM MLP (fp32 accumulate). */
 int nvc_infer(const nvc_model *m, const double *pos, int64_t n, int32_t precision,
               float *out, void *workspace, void *stream);
-/* Scratch for the decoupled fp16 query pipeline (encode tiles -> tcgen05 MLP
- * -> selection) over p pixels.  Passing workspace = NULL to nvc_infer /
- * nvc_nls_sample / nvc_neural_di selects the single fused kernel instead. */
+/* Scratch for the fp16 query pipeline (encode tiles -> tcgen05 MLP ->
+ * selection) over p pixels; required by nvc_infer (precision 1),
+ * nvc_nls_sample and nvc_neural_di. */
 int64_t nvc_query_workspace_bytes(const nvc_model *m, int64_t p);
 
 /* ---- training: cache.py:60-73 (train_step) split at the allreduce point --- */
-/* Accumulates the gradient of the loss into grad_fx and marks touched table
- * entries with `epoch`.  The batch has b global rows (b = *b_dev when b_dev
+/* Accumulates the gradient of the loss into grad_fx (int64 fixed point,
+ * 2^-48; order-independent, so shards and atomics stay deterministic).  The batch has b global rows (b = *b_dev when b_dev
  * is non-NULL, else b_max); this call handles the shard rows
  * [b*shard/n_shards, b*(shard+1)/n_shards): pos is indexed by global row,
  * targets/mask (may be NULL) by shard-local row.  d_out is scaled by the
@@ -141,15 +144,13 @@ int64_t nvc_query_workspace_bytes(const nvc_model *m, int64_t p);
  * over the shard's rows (mean over b is the caller's division). */
 int nvc_train_grads(const nvc_model *m, const double *pos, const float *targets,
                     const float *mask, int64_t b_max, const int64_t *b_dev,
-                    int32_t shard, int32_t n_shards, uint16_t epoch,
+                    int32_t shard, int32_t n_shards,
                     void *workspace, double *loss_sum_out, void *stream);
 /* One bias-corrected Adam step over every parameter (mlp.py:203-218, dense
  * like the reference), consuming and zeroing grad_fx; refreshes table_h and
  * wpack.  t is the post-increment Adam step (>= 1), lr from lr_at (mlp.py:76).
- * dense_grad=1 reads every grid gradient (needed after a data-parallel
- * allreduce of grad_fx); 0 uses the touched map. */
-int nvc_adam_step(const nvc_model *m, int64_t t, double lr, uint16_t epoch,
-                  int32_t dense_grad, void *stream);
+ * grad_fx may hold a data-parallel allreduced sum. */
+int nvc_adam_step(const nvc_model *m, int64_t t, double lr, void *stream);
 
 /* ---- light selection: sampling.py:74-85, 184-218 ---------------------- */
 /* wrs_select_batch: weights (p, k) f64; draw for (row r, light j) is

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libnvc.so")
 
 MAX_LEVELS = 32
 MAX_LAYERS = 8
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 c_i32, c_i64, c_u64, c_f64, c_f32, c_vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
                                            ctypes.c_double, ctypes.c_float, ctypes.c_void_p)
@@ -31,7 +31,7 @@ class NvcModel(ctypes.Structure):
         ("n_layers", c_i32), ("dims", c_i32 * (MAX_LAYERS + 1)),
         ("alpha", c_f32), ("out_sigmoid", c_i32),
         ("params", c_vp), ("adam_m", c_vp), ("adam_v", c_vp), ("grad_fx", c_vp),
-        ("touched", c_vp), ("table_h", c_vp), ("wpack", c_vp),
+        ("table_h", c_vp), ("wpack", c_vp),
         ("param_count", c_i64), ("wpack_count", c_i64),
     ]
 
@@ -65,13 +65,14 @@ _SIGS = {
     "nvc_train_workspace_bytes": (c_i64, [P(NvcModel), c_i64]),
     "nvc_refresh_shadow": (c_i32, [P(NvcModel), c_vp]),
     "nvc_l2_persist": (c_i32, [c_vp, c_i64, c_vp]),
-    "nvc_debug_trace": (c_i32, [c_vp, c_i32, c_i32]),
+    "nvc_profile_stages": (c_i32, [c_i32]),
+    "nvc_profile_stage_ms": (c_i32, [c_vp]),
     "nvc_encode": (c_i32, [P(NvcModel), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "nvc_infer": (c_i32, [P(NvcModel), c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "nvc_query_workspace_bytes": (c_i64, [P(NvcModel), c_i64]),
     "nvc_train_grads": (c_i32, [P(NvcModel), c_vp, c_vp, c_vp, c_i64, c_vp, c_i32, c_i32,
-                                ctypes.c_uint16, c_vp, c_vp, c_vp]),
-    "nvc_adam_step": (c_i32, [P(NvcModel), c_i64, c_f64, ctypes.c_uint16, c_i32, c_vp]),
+                                c_vp, c_vp, c_vp]),
+    "nvc_adam_step": (c_i32, [P(NvcModel), c_i64, c_f64, c_vp]),
     "nvc_wrs_select": (c_i32, [c_vp, c_i64, c_i32, c_u64, c_u64, c_vp, c_vp, c_vp, c_vp]),
     "nvc_nls_from_vis": (c_i32, [P(NvcScene), c_vp, c_vp, c_i32, c_i64, c_i64, c_i32, c_i64, c_i64,
                                  c_u64, c_u64, c_f64, c_vp, c_vp, c_vp, c_vp]),

@@ -2,8 +2,8 @@
 
 State lives in HBM as one flat f32 parameter vector in the reference's
 ``_param_dict`` order (grid, w0, b0, w1, b1, ...) plus Adam moments, an int64
-fixed-point gradient accumulator, a per-entry "touched" epoch map, the fp16
-shadow table the query kernel gathers from, and the fp16 weights packed in
+fixed-point gradient accumulator (zero except where this step's samples
+touched the table; consumed and cleared by Adam), the fp16 shadow table the query kernel gathers from, and the fp16 weights packed in
 the tcgen05 core-matrix layout.  ``infer`` and ``train_step`` keep the
 reference's numpy-in / numpy-out signatures; ``*_device`` variants take and
 return CUDA tensors without host round trips.
@@ -58,7 +58,6 @@ class VisibilityCache:
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.step = 0          # train_step count (drives lr_at)
         self.adam_t = 0        # Adam bias-correction step
-        self._epoch = 0
         gen = rngmod.stream(seed, rngmod.INIT_PARAMS)
         table = init_table(grid, gen)
         net = he_init(self.net_cfg, gen)
@@ -84,7 +83,6 @@ class VisibilityCache:
         self.adam_m = torch.zeros_like(self.params)
         self.adam_v = torch.zeros_like(self.params)
         self.grad_fx = torch.zeros(total, dtype=torch.int64, device=dev)
-        self.touched = torch.zeros(g.levels * g.table_size, dtype=torch.int16, device=dev)
         # fp16 query table in x-pair layout (common.cuh): 2 x the grid parameters
         self.table_h = torch.zeros(2 * g.param_count, dtype=torch.float16, device=dev)
         m = _lib.NvcModel()
@@ -109,14 +107,13 @@ class VisibilityCache:
         self.wpack = torch.zeros(wc, dtype=torch.int16, device=dev)
         m.wpack_count = wc
         m.params, m.adam_m, m.adam_v = (t.data_ptr() for t in (self.params, self.adam_m, self.adam_v))
-        m.grad_fx, m.touched = self.grad_fx.data_ptr(), self.touched.data_ptr()
+        m.grad_fx = self.grad_fx.data_ptr()
         m.table_h, m.wpack = self.table_h.data_ptr(), self.wpack.data_ptr()
         self.model = m
         self._ws = None
         self._qws = None
         # "pipeline": decoupled encode -> tcgen05 MLP -> selection (default);
         # "fused": the single fused kernel
-        self.query_impl = "pipeline"
 
     def _upload(self, table: np.ndarray, net: MLPParams) -> None:
         import torch
@@ -199,9 +196,9 @@ class VisibilityCache:
         return (out, idx.cpu().numpy(), w.cpu().numpy()) if with_ctx else out
 
     def query_workspace(self, p: int):
-        """Scratch of the decoupled query pipeline (None selects the fused kernel)."""
+        """Scratch of the fp16 query pipeline for p pixels (grown on demand)."""
         import torch
-        if self.query_impl != "pipeline" or p <= 0:
+        if p <= 0:
             return None
         need = _lib.load().nvc_query_workspace_bytes(self.model, p)
         if self._qws is None or self._qws.numel() < need:
@@ -240,40 +237,32 @@ class VisibilityCache:
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
         return self._ws
 
-    def next_epoch(self) -> int:
-        self._epoch = self._epoch % 65535 + 1
-        return self._epoch
-
     def accumulate_grads(self, pos, targets, mask=None, b_max=None, b_dev=None, shard=0, n_shards=1,
-                         loss_out=None, epoch=None):
+                         loss_out=None):
         """Device gradient accumulation (the allreduce point for data parallelism)."""
         import torch
         b_max = int(pos.shape[0] if b_max is None else b_max)
         if loss_out is None:
             loss_out = torch.zeros(1, dtype=torch.float64, device=self.device)
         ws = self._workspace(b_max)
-        ep = self._epoch if epoch is None else epoch
         _lib.call("nvc_train_grads", self.model, pos.data_ptr(), targets.data_ptr(), _lib.ptr(mask), b_max,
-                  _lib.ptr(b_dev), shard, n_shards, ep, ws.data_ptr(), loss_out.data_ptr(), _lib.stream_ptr())
+                  _lib.ptr(b_dev), shard, n_shards, ws.data_ptr(), loss_out.data_ptr(), _lib.stream_ptr())
         return loss_out
 
-    def apply_adam(self, dense_grad: bool = False) -> None:
+    def apply_adam(self) -> None:
         lr = lr_at(self.step, self.train_cfg)
         self.adam_t += 1
-        _lib.call("nvc_adam_step", self.model, self.adam_t, lr, self._epoch, int(dense_grad), _lib.stream_ptr())
+        _lib.call("nvc_adam_step", self.model, self.adam_t, lr, _lib.stream_ptr())
         self.step += 1
 
     def train_step_device(self, pos, targets, mask=None, b_dev=None, b_max=None, comm=None):
         """One fused step on device tensors; returns the loss as a 0-d CUDA tensor
         (sum of per-row losses / b) without synchronising.  ``comm`` is an
         optional callable(grad_fx, loss) run at the allreduce point."""
-        self.next_epoch()
         loss = self.accumulate_grads(pos, targets, mask, b_max=b_max, b_dev=b_dev)
-        dense = False
         if comm is not None:
             comm(self.grad_fx, loss)
-            dense = True
-        self.apply_adam(dense_grad=dense)
+        self.apply_adam()
         b = b_dev.to(torch_f64()) if b_dev is not None else float(pos.shape[0])
         return loss[0] / b
 

@@ -6,6 +6,7 @@
 //   encode_batch hashgrid.py:117-131, grad_from_ctx :140-151,
 //   forward mlp.py:110-140, l2_loss :143-149, backward_l2 :152-183,
 //   adam_step :203-218, VisibilityCache.train_step cache.py:60-73.
+#include <algorithm>
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
@@ -178,7 +179,6 @@ __global__ void __launch_bounds__(kThreads) k_mlp(GridDev g, Net net, const floa
                                                  const int64_t* __restrict__ b_dev, int shard, int n_shards,
                                                  const float* __restrict__ tgt, const float* __restrict__ mask,
                                                  float* __restrict__ out, int64_t* __restrict__ grad_fx,
-                                                 uint16_t* __restrict__ touched, uint16_t epoch,
                                                  float* __restrict__ part_w, double* __restrict__ part_loss) {
     extern __shared__ float sm[];
     const TileLayout tl = tile_layout(net);
@@ -319,33 +319,40 @@ __global__ void __launch_bounds__(kThreads) k_mlp(GridDev g, Net net, const floa
                 const float contrib = (float)__dmul_rn(w, (double)up[k]);   // (w * g).astype(f32)
                 red_add_fx(gl + (int64_t)idx * g.F + k, to_fx((double)contrib));
             }
-            touched[(int64_t)l * g.T + idx] = epoch;
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// Register-tiled SIMT training step (all widths multiples of 4, weights in
-// smem as W and W^T).  Same maths and row partition as k_mlp<true>, ~10x less
-// time: forward 2x4 tiles over Wt, grad-W 4x4 tiles over (dz, act), grad-act
-// 2x4 tiles over W, all operands in shared memory.
+// Split training step (default when every width is a multiple of 4):
+//   k_tr_encode   one thread per (row, level): exact f32 features -> act0
+//   k_train3      one block per kRows rows: SIMT fp32 forward / loss /
+//                 backward with only W in shared memory (row stride Ki+4, so
+//                 both the n-strided forward reads and the k-contiguous
+//                 backward reads are bank-conflict free); writes dL/dact0
+//   k_tr_scatter  one thread per (row, level): fixed-point hash-grid scatter
+// Same arithmetic and the same kRows row partition as k_mlp<true> (so the
+// per-block MLP partials, and hence the reduced gradients, are unchanged);
+// the phases that were latency-bound inside one block (gathers, atomics)
+// now run at full-GPU parallelism.
 // ---------------------------------------------------------------------------
-struct T2Layout {
-    int w[NVC_MAX_LAYERS], wt[NVC_MAX_LAYERS];   // float offsets of W_l [N][K] and W_l^T [K][N]
+struct T3Layout {
+    int w[NVC_MAX_LAYERS], ws[NVC_MAX_LAYERS];   // float offset and row stride of W_l [N][Ki+4]
+    int bias[NVC_MAX_LAYERS];
     int act[NVC_MAX_LAYERS + 1];                 // act_l [kRows][D_l]
     int dz0, dz1;                                // two [kRows][Dmax] buffers
     int total;
 };
 
-__host__ __device__ inline T2Layout t2_layout(const Net& net) {
-    T2Layout t;
+__host__ __device__ inline T3Layout t3_layout(const Net& net) {
+    T3Layout t;
     int o = 0, dmax = 0;
     for (int l = 0; l < net.n_layers; ++l) {
-        const int sz = net.dims[l] * net.dims[l + 1];
         t.w[l] = o;
-        o += sz;
-        t.wt[l] = o;
-        o += sz;
+        t.ws[l] = net.dims[l] + 4;
+        o += net.dims[l + 1] * t.ws[l];
+        t.bias[l] = o;
+        o += (net.dims[l + 1] + 3) / 4 * 4;
     }
     for (int l = 0; l <= net.n_layers; ++l) {
         t.act[l] = o;
@@ -360,78 +367,101 @@ __host__ __device__ inline T2Layout t2_layout(const Net& net) {
     return t;
 }
 
-__global__ void __launch_bounds__(kThreads) k_train2(GridDev g, Net net, const float* __restrict__ params,
-                                                    const double* __restrict__ pos, int64_t b_max,
-                                                    const int64_t* __restrict__ b_dev, int shard, int n_shards,
-                                                    const float* __restrict__ tgt, const float* __restrict__ mask,
-                                                    int64_t* __restrict__ grad_fx, uint16_t* __restrict__ touched,
-                                                    uint16_t epoch, float* __restrict__ part_w,
-                                                    double* __restrict__ part_loss) {
-    extern __shared__ float sm[];
-    const T2Layout tl = t2_layout(net);
-    const int tid = threadIdx.x;
+struct ShardRows {
+    int64_t lo, hi;
+};
+__device__ __forceinline__ ShardRows shard_rows(int64_t b_max, const int64_t* b_dev, int shard, int n_shards) {
     const int64_t b = b_dev ? *b_dev : b_max;
-    const int64_t lo = b * shard / n_shards, hi = b * (shard + 1) / n_shards;
-    const int64_t row0 = lo + (int64_t)blockIdx.x * kRows;
-    const int nr = (int)max((int64_t)0, min((int64_t)kRows, hi - row0));
+    return {b * shard / n_shards, b * (shard + 1) / n_shards};
+}
+
+__global__ void __launch_bounds__(128) k_tr_encode(GridDev g, const float* __restrict__ params,
+                                                   const double* __restrict__ pos, int64_t b_max,
+                                                   const int64_t* __restrict__ b_dev, int shard, int n_shards,
+                                                   float* __restrict__ act0) {
+    const ShardRows sr = shard_rows(b_max, b_dev, shard, n_shards);
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t r = t / g.L;
+    const int l = (int)(t - r * g.L);
+    if (sr.lo + r >= sr.hi) return;
+    const int64_t i = sr.lo + r;
+    const double pp[3] = {__ldg(pos + 3 * i), __ldg(pos + 3 * i + 1), __ldg(pos + 3 * i + 2)};
+    double q[3];
+    normalize(g, pp, q);
+    encode_level_f32(g, params, q, l, act0 + r * (g.L * g.F) + l * g.F, nullptr, nullptr);
+}
+
+__global__ void __launch_bounds__(kThreads, 2) k_train3(Net net, const float* __restrict__ params,
+                                                       const float* __restrict__ act0g, int64_t b_max,
+                                                       const int64_t* __restrict__ b_dev, int shard, int n_shards,
+                                                       const float* __restrict__ tgt, const float* __restrict__ mask,
+                                                       float* __restrict__ dact0g, float* __restrict__ part_w,
+                                                       double* __restrict__ part_loss) {
+    extern __shared__ __align__(16) float sm[];
+    const T3Layout tl = t3_layout(net);
+    const int tid = threadIdx.x;
+    const ShardRows sr = shard_rows(b_max, b_dev, shard, n_shards);
+    const int64_t b = b_dev ? *b_dev : b_max;
+    const int64_t r0g = (int64_t)blockIdx.x * kRows;   // shard-local first row
+    const int nr = (int)max((int64_t)0, min((int64_t)kRows, (sr.hi - sr.lo) - r0g));
     const int D0 = net.dims[0];
     const int K = net.dims[net.n_layers];
 
-    // ---- weights -> smem (W and W^T), encode rows -> act0 ----
+    // ---- W (padded rows), biases, act0 -> smem; all loads issued as float4 ----
     for (int l = 0; l < net.n_layers; ++l) {
-        const int N = net.dims[l + 1], Ki = net.dims[l];
-        const float* W = params + net.woff[l];
-        for (int e = tid; e < N * Ki; e += blockDim.x) {
-            const float w = __ldg(W + e);
-            const int n = e / Ki, k = e - n * Ki;
-            sm[tl.w[l] + e] = w;
-            sm[tl.wt[l] + k * N + n] = w;
+        const int N = net.dims[l + 1], Ki = net.dims[l], kq = Ki / 4;
+        const float4* W = reinterpret_cast<const float4*>(params + net.woff[l]);
+        float* dst = sm + tl.w[l];
+#pragma unroll 4
+        for (int e = tid; e < N * kq; e += kThreads) {
+            const float4 w = __ldg(W + e);
+            const int n = e / kq, k = (e - n * kq) * 4;
+            *reinterpret_cast<float4*>(dst + n * tl.ws[l] + k) = w;
         }
+        for (int n = tid; n < N; n += kThreads) sm[tl.bias[l] + n] = __ldg(params + net.boff[l] + n);
     }
-    for (int e = tid; e < kRows * g.L; e += blockDim.x) {
-        const int r = e / g.L, l = e - r * g.L;
-        float* dst = sm + tl.act[0] + r * D0 + l * g.F;
-        if (r < nr) {
-            const int64_t i = row0 + r;
-            const double pp[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
-            double q[3];
-            normalize(g, pp, q);
-            encode_level_f32(g, params, q, l, dst, nullptr, nullptr);
-        } else {
-            for (int k = 0; k < g.F; ++k) dst[k] = 0.0f;
-        }
+    {
+        const int q0 = D0 / 4;
+        const float4* src = reinterpret_cast<const float4*>(act0g + r0g * D0);
+        float4* dst = reinterpret_cast<float4*>(sm + tl.act[0]);
+        for (int e = tid; e < kRows * q0; e += kThreads)
+            dst[e] = (e / q0 < nr) ? __ldg(src + e) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncthreads();
 
-    // ---- forward: z = act W^T + b, 2x4 register tiles ----
+    // ---- forward: z = act W^T + b; thread tile 2 rows x 4 outputs (n strided by N/4) ----
     for (int l = 0; l < net.n_layers; ++l) {
-        const int Ki = net.dims[l], N = net.dims[l + 1];
+        const int Ki = net.dims[l], N = net.dims[l + 1], ng = N / 4, S = tl.ws[l];
         const float* A = sm + tl.act[l];
-        const float* Wt = sm + tl.wt[l];
+        const float* W = sm + tl.w[l];
         float* out = sm + tl.act[l + 1];
         const bool last = l == net.n_layers - 1;
-        const int ng = N / 4;
-        for (int t = tid; t < (kRows / 2) * ng; t += blockDim.x) {
-            const int r0 = (t / ng) * 2, n0 = (t % ng) * 4;
+        for (int t = tid; t < (kRows / 2) * ng; t += kThreads) {
+            const int r0 = (t / ng) * 2, nn = t % ng;
             float acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
-            for (int k = 0; k < Ki; ++k) {
-                const float4 w = *reinterpret_cast<const float4*>(Wt + k * N + n0);
-                const float a0 = A[r0 * Ki + k], a1 = A[(r0 + 1) * Ki + k];
-                acc[0][0] = fmaf(a0, w.x, acc[0][0]);
-                acc[0][1] = fmaf(a0, w.y, acc[0][1]);
-                acc[0][2] = fmaf(a0, w.z, acc[0][2]);
-                acc[0][3] = fmaf(a0, w.w, acc[0][3]);
-                acc[1][0] = fmaf(a1, w.x, acc[1][0]);
-                acc[1][1] = fmaf(a1, w.y, acc[1][1]);
-                acc[1][2] = fmaf(a1, w.z, acc[1][2]);
-                acc[1][3] = fmaf(a1, w.w, acc[1][3]);
+            for (int k = 0; k < Ki; k += 4) {
+                const float4 a0 = *reinterpret_cast<const float4*>(A + r0 * Ki + k);
+                const float4 a1 = *reinterpret_cast<const float4*>(A + (r0 + 1) * Ki + k);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float4 w = *reinterpret_cast<const float4*>(W + (nn + j * ng) * S + k);
+                    acc[0][j] = fmaf(a0.x, w.x, acc[0][j]);
+                    acc[1][j] = fmaf(a1.x, w.x, acc[1][j]);
+                    acc[0][j] = fmaf(a0.y, w.y, acc[0][j]);
+                    acc[1][j] = fmaf(a1.y, w.y, acc[1][j]);
+                    acc[0][j] = fmaf(a0.z, w.z, acc[0][j]);
+                    acc[1][j] = fmaf(a1.z, w.z, acc[1][j]);
+                    acc[0][j] = fmaf(a0.w, w.w, acc[0][j]);
+                    acc[1][j] = fmaf(a1.w, w.w, acc[1][j]);
+                }
             }
 #pragma unroll
             for (int i = 0; i < 2; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const float z = acc[i][j] + __ldg(params + net.boff[l] + n0 + j);
-                    out[(r0 + i) * N + n0 + j] = (last && net.out_sigmoid) ? sigmoid_ref(z) : leaky(z, net.alpha);
+                    const int n = nn + j * ng;
+                    const float z = acc[i][j] + sm[tl.bias[l] + n];
+                    out[(r0 + i) * N + n] = (last && net.out_sigmoid) ? sigmoid_ref(z) : leaky(z, net.alpha);
                 }
         }
         __syncthreads();
@@ -442,11 +472,11 @@ __global__ void __launch_bounds__(kThreads) k_train2(GridDev g, Net net, const f
     float* dzn = sm + tl.dz1;
     const float bk = (float)(b * K);
     double lsum = 0.0;
-    for (int e = tid; e < kRows * K; e += blockDim.x) {
+    for (int e = tid; e < kRows * K; e += kThreads) {
         const int r = e / K;
         float d = 0.0f;
         if (r < nr) {
-            const int64_t li = (row0 - lo) * K + e;
+            const int64_t li = r0g * K + e;
             const float sgm = sm[tl.act[net.n_layers] + e];
             const float outc = net.out_sigmoid ? fminf(fmaxf(sgm, 1e-6f), 0.999999f) : sgm;
             const float t = tgt[li];
@@ -477,12 +507,12 @@ __global__ void __launch_bounds__(kThreads) k_train2(GridDev g, Net net, const f
     // ---- backward (mlp.py:170-183) ----
     float* part = part_w + (int64_t)blockIdx.x * net.mlp_count;
     for (int l = net.n_layers - 1; l >= 0; --l) {
-        const int Ki = net.dims[l], N = net.dims[l + 1];
+        const int Ki = net.dims[l], N = net.dims[l + 1], S = tl.ws[l];
         const float* A = sm + tl.act[l];
         // grad W[n][k] = sum_r dz[r][n] A[r][k]   (4x4 tiles)
         float* gw = part + (net.woff[l] - net.grid_count);
         const int kg = Ki / 4;
-        for (int t = tid; t < (N / 4) * kg; t += blockDim.x) {
+        for (int t = tid; t < (N / 4) * kg; t += kThreads) {
             const int n0 = (t / kg) * 4, k0 = (t % kg) * 4;
             float acc[4][4] = {};
             for (int r = 0; r < kRows; ++r) {
@@ -499,18 +529,18 @@ __global__ void __launch_bounds__(kThreads) k_train2(GridDev g, Net net, const f
                 *reinterpret_cast<float4*>(gw + (n0 + i) * Ki + k0) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
         }
         float* gb = part + (net.boff[l] - net.grid_count);
-        for (int n = tid; n < N; n += blockDim.x) {
+        for (int n = tid; n < N; n += kThreads) {
             float acc = 0.0f;
             for (int r = 0; r < kRows; ++r) acc += dz[r * N + n];
             gb[n] = acc;
         }
         // grad act[r][k] = sum_n dz[r][n] W[n][k], through leaky'(z_{l-1}) (2x4 tiles)
         const float* W = sm + tl.w[l];
-        for (int t = tid; t < (kRows / 2) * kg; t += blockDim.x) {
+        for (int t = tid; t < (kRows / 2) * kg; t += kThreads) {
             const int r0 = (t / kg) * 2, k0 = (t % kg) * 4;
             float acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
             for (int n = 0; n < N; ++n) {
-                const float4 w = *reinterpret_cast<const float4*>(W + n * Ki + k0);
+                const float4 w = *reinterpret_cast<const float4*>(W + n * S + k0);
                 const float d0 = dz[r0 * N + n], d1 = dz[(r0 + 1) * N + n];
                 acc[0][0] = fmaf(d0, w.x, acc[0][0]);
                 acc[0][1] = fmaf(d0, w.y, acc[0][1]);
@@ -521,42 +551,55 @@ __global__ void __launch_bounds__(kThreads) k_train2(GridDev g, Net net, const f
                 acc[1][2] = fmaf(d1, w.z, acc[1][2]);
                 acc[1][3] = fmaf(d1, w.w, acc[1][3]);
             }
+            if (l > 0) {
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
+                for (int i = 0; i < 2; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    float v = acc[i][j];
-                    if (l > 0 && !(A[(r0 + i) * Ki + k0 + j] >= 0.0f)) v = __fmul_rn(v, net.alpha);
-                    dzn[(r0 + i) * Ki + k0 + j] = v;
-                }
+                    for (int j = 0; j < 4; ++j) {
+                        float v = acc[i][j];
+                        if (!(A[(r0 + i) * Ki + k0 + j] >= 0.0f)) v = __fmul_rn(v, net.alpha);
+                        dzn[(r0 + i) * Ki + k0 + j] = v;
+                    }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+                    if (r0 + i < nr)
+                        *reinterpret_cast<float4*>(dact0g + (r0g + r0 + i) * Ki + k0) =
+                            make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+            }
         }
         __syncthreads();
         float* t = dz;
         dz = dzn;
         dzn = t;
     }
+}
 
-    // ---- hash-grid scatter (hashgrid.py:140-151), fixed point ----
-    for (int e = tid; e < nr * g.L; e += blockDim.x) {
-        const int r = e / g.L, l = e - r * g.L;
-        const int64_t i = row0 + r;
-        const double pp[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
-        double q[3];
-        normalize(g, pp, q);
-        int c0[3];
-        double f[3];
-        cell(g.res[l], q, c0, f);
-        const float* up = dz + r * D0 + l * g.F;
-        int64_t* gl = grad_fx + (int64_t)l * g.T * g.F;
+__global__ void __launch_bounds__(128) k_tr_scatter(GridDev g, const double* __restrict__ pos, int64_t b_max,
+                                                    const int64_t* __restrict__ b_dev, int shard, int n_shards,
+                                                    const float* __restrict__ dact0, int64_t* __restrict__ grad_fx) {
+    const ShardRows sr = shard_rows(b_max, b_dev, shard, n_shards);
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t r = t / g.L;
+    const int l = (int)(t - r * g.L);
+    if (sr.lo + r >= sr.hi) return;
+    const int64_t i = sr.lo + r;
+    const double pp[3] = {__ldg(pos + 3 * i), __ldg(pos + 3 * i + 1), __ldg(pos + 3 * i + 2)};
+    double q[3];
+    normalize(g, pp, q);
+    int c0[3];
+    double f[3];
+    cell(g.res[l], q, c0, f);
+    float up[8];
+    for (int k = 0; k < g.F; ++k) up[k] = __ldg(dact0 + r * (g.L * g.F) + l * g.F + k);
+    int64_t* gl = grad_fx + (int64_t)l * g.T * g.F;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            const uint32_t idx = corner_index(g, l, c0, (c >> 2) & 1, (c >> 1) & 1, c & 1);
-            const double w = corner_weight(f, c);
-            for (int k = 0; k < g.F; ++k) {
-                const float contrib = (float)__dmul_rn(w, (double)up[k]);
-                red_add_fx(gl + (int64_t)idx * g.F + k, to_fx((double)contrib));
-            }
-            touched[(int64_t)l * g.T + idx] = epoch;
+    for (int c = 0; c < 8; ++c) {
+        const uint32_t idx = corner_index(g, l, c0, (c >> 2) & 1, (c >> 1) & 1, c & 1);
+        const double w = corner_weight(f, c);
+        for (int k = 0; k < g.F; ++k) {
+            const float contrib = (float)__dmul_rn(w, (double)up[k]);   // (w * g).astype(f32), hashgrid.py:146-151
+            red_add_fx(gl + (int64_t)idx * g.F + k, to_fx((double)contrib));
         }
     }
 }
@@ -601,8 +644,8 @@ struct AdamK {
 // (mlp.py:209-217).  Quotients by the per-step constants use
 // (float)(x * RN(1/c)) in binary64: a float/float quotient is never a float
 // midpoint and lies >= 2^-49 (relative) from one, so the <= 2^-52 binary64
-// error cannot change the float rounding; the variable quotient uses a
-// binary64 division (double rounding is innocuous for p' >= 2p + 2).
+// error cannot change the float rounding; the variable quotient is an IEEE
+// float division.
 __device__ __forceinline__ float adam1(float p, float g, float& m, float& v, const AdamK& a) {
     m = __fadd_rn(__fmul_rn(m, a.b1), __fmul_rn(a.c1, g));
     v = __fadd_rn(__fmul_rn(v, a.b2), __fmul_rn(__fmul_rn(a.c2, g), g));
@@ -610,7 +653,7 @@ __device__ __forceinline__ float adam1(float p, float g, float& m, float& v, con
     const float vh = (float)__dmul_rn((double)v, a.inv_b2c);
     const float num = __fmul_rn(a.lr, mh);
     const float den = __fadd_rn(__fsqrt_rn(vh), a.eps);
-    return __fsub_rn(p, (float)__ddiv_rn((double)num, (double)den));
+    return __fsub_rn(p, __fdiv_rn(num, den));   // float32 '/' (IEEE, correctly rounded)
 }
 
 // wpack offset (halfs) of W_i[n][k] in the tcgen05 swizzled K-major layout
@@ -622,109 +665,125 @@ __host__ __device__ inline int64_t wpack_index(const Net& net, int i, int n, int
     return o + umma_off(n, k, np[i], kp[i]) / 2;
 }
 
-// grid part: 8 params per thread, all loads issued before any math; the
-// gradient of an entry is read (and zeroed) only when its epoch matches.
-__device__ __forceinline__ float4 ld_stream(const float* p) {
-    float4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-                 : "l"(p));
-    return r;
-}
-__device__ __forceinline__ void st_stream(float* p, float4 v) {
-    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
-                 : "memory");
-}
-
 __device__ __forceinline__ void put_pair(uint16_t* t2, int64_t i, int F, int64_t T, uint16_t h) {
     const int64_t e = i / F, f = i - e * F;
     t2[e * 2 * F + f] = h;                               // own slot, low half
     t2[pair_prev(e, T) * 2 * F + F + f] = h;             // previous slot's x-neighbour half
 }
 
-__global__ void __launch_bounds__(256) k_adam_grid(float* __restrict__ p, float* __restrict__ m,
+// Generic grid Adam: one parameter per thread.  The fixed-point accumulator
+// is zero wherever no sample touched the entry, so it is read densely and
+// cleared where nonzero (after a data-parallel allreduce it is already the
+// global sum).
+__global__ void __launch_bounds__(256) k_adam_flat(float* __restrict__ p, float* __restrict__ m,
                                                    float* __restrict__ v, int64_t* __restrict__ fx,
-                                                   const uint16_t* __restrict__ touched,
-                                                   uint16_t* __restrict__ table_h, int64_t n, int F,
-                                                   uint16_t epoch, int dense, AdamK a, int64_t T) {
-    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
-    if (i0 >= n) return;
-    if (i0 + 8 <= n) {
-        float4 P[2], M[2], V[2];
+                                                   uint16_t* __restrict__ table_h, int64_t n, int F, AdamK a,
+                                                   int64_t T) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const long long q = fx[i];
+    if (q) fx[i] = 0;
+    float mm = m[i], vv = v[i];
+    const float pn = adam1(p[i], from_fx(q), mm, vv, a);
+    p[i] = pn;
+    m[i] = mm;
+    v[i] = vv;
+    put_pair(table_h, i, F, T, __half_as_ushort(__float2half_rn(pn)));
+}
+
+// Streaming grid Adam (F == 2, whole tiles): a persistent kernel whose
+// p / m / v / grad_fx tiles move by bulk copies (TMA) into a 4-stage shared
+// memory ring and p / m / v go back by bulk stores, so three tiles per block
+// are always in flight.  Reading the int64 accumulator densely (instead of
+// gathering only touched entries) costs 8 B/parameter of sequential HBM
+// traffic but removes every dependent random read from the stream.  The fp16
+// x-pair slots (slot e = entry e | entry next(e)) are assembled in registers
+// -- a thread's last neighbour comes from the next lane by shuffle -- so each
+// thread writes 16 contiguous bytes; only a warp's last slot takes its high
+// half from the next warp's lane 0.
+constexpr int kAdamTile = 512, kAdamStages = 4, kAdamThreads = 128;   // 4 params per thread
+struct AdamStage {
+    float p[kAdamTile], m[kAdamTile], v[kAdamTile];
+    long long q[kAdamTile];
+};
+
+__global__ void __launch_bounds__(kAdamThreads) k_adam_bulk(float* __restrict__ p, float* __restrict__ m,
+                                                           float* __restrict__ v, int64_t* __restrict__ fx,
+                                                           uint16_t* __restrict__ table_h, int64_t ntiles, AdamK a,
+                                                           int64_t T) {
+    extern __shared__ __align__(128) uint8_t adam_smem[];
+    AdamStage* st = reinterpret_cast<AdamStage*>(adam_smem);
+    __shared__ uint64_t full[kAdamStages];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int n_local = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+    auto tile_base = [&](int i) { return (blockIdx.x + (int64_t)i * gridDim.x) * kAdamTile; };
+    auto issue = [&](int i) {
+        const int s = i % kAdamStages;
+        const int64_t base = tile_base(i);
+        tma::bar_expect_tx(&full[s], (uint32_t)sizeof(AdamStage));
+        tma::load(st[s].p, p + base, kAdamTile * 4, &full[s]);
+        tma::load(st[s].m, m + base, kAdamTile * 4, &full[s]);
+        tma::load(st[s].v, v + base, kAdamTile * 4, &full[s]);
+        tma::load(st[s].q, fx + base, kAdamTile * 8, &full[s]);
+    };
+    if (tid == 0) {
+        for (int s = 0; s < kAdamStages; ++s) tma::bar_init(&full[s], 1);
+        tma::bar_init_fence();
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int i = 0; i < min(kAdamStages, n_local); ++i) issue(i);
+    for (int i = 0; i < n_local; ++i) {
+        const int s = i % kAdamStages;
+        const int64_t base = tile_base(i);
+        const int64_t i0 = base + 4 * tid, e0 = i0 / 2;
+        tma::bar_wait(&full[s], (uint32_t)(i / kAdamStages) & 1u);
+        float4* P4 = reinterpret_cast<float4*>(st[s].p) + tid;
+        float4* M4 = reinterpret_cast<float4*>(st[s].m) + tid;
+        float4* V4 = reinterpret_cast<float4*>(st[s].v) + tid;
+        const longlong2* Q2 = reinterpret_cast<const longlong2*>(st[s].q) + 2 * tid;
+        const longlong2 qa = Q2[0], qb = Q2[1];
+        if (qa.x | qa.y) *reinterpret_cast<longlong2*>(fx + i0) = make_longlong2(0, 0);
+        if (qb.x | qb.y) *reinterpret_cast<longlong2*>(fx + i0 + 2) = make_longlong2(0, 0);
+        const long long q[4] = {qa.x, qa.y, qb.x, qb.y};
+        float4 P = *P4, M = *M4, V = *V4;
+        float* Pp = &P.x;
+        float* Mp = &M.x;
+        float* Vp = &V.x;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            P[h] = ld_stream(p + i0 + 4 * h);
-            M[h] = ld_stream(m + i0 + 4 * h);
-            V[h] = ld_stream(v + i0 + 4 * h);
-        }
-        uint16_t tv[8];
-        if (!dense) {
-            if (F == 2) {
-                const uint2 t4 = __ldg(reinterpret_cast<const uint2*>(touched + i0 / 2));
-                tv[0] = tv[1] = (uint16_t)(t4.x & 0xffff);
-                tv[2] = tv[3] = (uint16_t)(t4.x >> 16);
-                tv[4] = tv[5] = (uint16_t)(t4.y & 0xffff);
-                tv[6] = tv[7] = (uint16_t)(t4.y >> 16);
-            } else {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) tv[j] = __ldg(touched + (i0 + j) / F);
-            }
-        }
-        float G[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            G[j] = 0.0f;
-            if (dense || tv[j] == epoch) {
-                const long long q = fx[i0 + j];
-                if (q) {
-                    G[j] = from_fx(q);
-                    fx[i0 + j] = 0;
-                }
-            }
-        }
-        __align__(16) __half hv[8];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            float* Pp = &P[h].x;
-            float* Mp = &M[h].x;
-            float* Vp = &V[h].x;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                Pp[j] = adam1(Pp[j], G[4 * h + j], Mp[j], Vp[j], a);
-                hv[4 * h + j] = __float2half_rn(Pp[j]);
-            }
-            st_stream(p + i0 + 4 * h, P[h]);
-            st_stream(m + i0 + 4 * h, M[h]);
-            st_stream(v + i0 + 4 * h, V[h]);
-        }
-        if (F == 2) {   // 4 entries: own slots (4 x 4 B) + previous slots' neighbour halves
-            const int64_t e0 = i0 / 2;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const uint32_t w = (uint32_t)__half_as_ushort(hv[2 * j]) | ((uint32_t)__half_as_ushort(hv[2 * j + 1]) << 16);
-                const int64_t e = e0 + j;
-                *reinterpret_cast<uint32_t*>(table_h + e * 4) = w;
-                *reinterpret_cast<uint32_t*>(table_h + pair_prev(e, T) * 4 + 2) = w;
-            }
+        for (int j = 0; j < 4; ++j) Pp[j] = adam1(Pp[j], from_fx(q[j]), Mp[j], Vp[j], a);
+        *P4 = P;
+        *M4 = M;
+        *V4 = V;
+        const uint32_t E0 = (uint32_t)__half_as_ushort(__float2half_rn(Pp[0])) |
+                            ((uint32_t)__half_as_ushort(__float2half_rn(Pp[1])) << 16);
+        const uint32_t E1 = (uint32_t)__half_as_ushort(__float2half_rn(Pp[2])) |
+                            ((uint32_t)__half_as_ushort(__float2half_rn(Pp[3])) << 16);
+        const uint32_t nxt = __shfl_down_sync(0xffffffffu, E0, 1);
+        uint32_t* slot = reinterpret_cast<uint32_t*>(table_h + e0 * 4);   // 2 words per slot
+        if (lane < 31) {
+            *reinterpret_cast<uint4*>(slot) = make_uint4(E0, E1, E1, nxt);
         } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) put_pair(table_h, i0 + j, F, T, __half_as_ushort(hv[j]));
+            *reinterpret_cast<uint2*>(slot) = make_uint2(E0, E1);
+            slot[2] = E1;
         }
-    } else {
-        for (int64_t i = i0; i < n; ++i) {
-            const bool hot = dense || touched[i / F] == epoch;
-            float g = 0.0f;
-            if (hot && fx[i]) {
-                g = from_fx(fx[i]);
-                fx[i] = 0;
+        if (lane == 0)   // previous slot's x-neighbour half (previous warp's last slot, or the level's last on wrap)
+            reinterpret_cast<uint32_t*>(table_h + pair_prev(e0, T) * 4)[1] = E0;
+        tma::fence_shared();
+        __syncthreads();
+        if (tid == 0) {
+            tma::store(p + base, st[s].p, kAdamTile * 4);
+            tma::store(m + base, st[s].m, kAdamTile * 4);
+            tma::store(v + base, st[s].v, kAdamTile * 4);
+            tma::commit();
+            // refill the previous iteration's stage once its store has read smem
+            if (i >= 1 && i - 1 + kAdamStages < n_local) {
+                tma::wait_read<1>();
+                issue(i - 1 + kAdamStages);
             }
-            float mm = m[i], vv = v[i];
-            p[i] = adam1(p[i], g, mm, vv, a);
-            m[i] = mm;
-            v[i] = vv;
-            put_pair(table_h, i, F, T, __half_as_ushort(__float2half_rn(p[i])));
         }
     }
+    if (tid == 0) tma::wait_all();
 }
 
 __global__ void k_adam_mlp(Net net, float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
@@ -796,7 +855,7 @@ int nvc::nvc_infer_f32(const nvc_model* m, const double* pos, int64_t n, float* 
     NVC_REQUIRE(smem <= 200 * 1024, "nvc_infer: MLP too wide for the fp32 tile kernel");
     cudaFuncSetAttribute(k_mlp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k_mlp<false><<<grid1(n, kRows), kThreads, smem, s>>>(g, net, m->params, pos, n, nullptr, 0, 1, nullptr,
-                                                          nullptr, out, nullptr, nullptr, 0, nullptr, nullptr);
+                                                          nullptr, out, nullptr, nullptr, nullptr);
     return check_launch("k_mlp<infer>");
 }
 
@@ -811,7 +870,7 @@ int64_t nvc_train_workspace_bytes(const nvc_model* m, int64_t b) {
     if (!m) return 0;
     Net net = net_of(m);
     const int64_t nblk = b / kRows + 2;
-    return nblk * (net.mlp_count * 4 + 8) + 256;
+    return nblk * (net.mlp_count * 4 + 8) + 2 * (nblk * kRows * net.dims[0] * 4 + 256) + 512;
 }
 
 int nvc_refresh_shadow(const nvc_model* m, void* stream) {
@@ -839,48 +898,57 @@ int nvc_encode(const nvc_model* m, const double* pos, int64_t n, float* feats, i
 }
 
 int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, const float* mask, int64_t b_max,
-                    const int64_t* b_dev, int32_t shard, int32_t n_shards, uint16_t epoch, void* ws,
-                    double* loss_out, void* stream) {
+                    const int64_t* b_dev, int32_t shard, int32_t n_shards, void* ws, double* loss_out,
+                    void* stream) {
     int rc = validate(m);
     if (rc) return rc;
-    NVC_REQUIRE(pos && tgt && ws && m->grad_fx && m->touched, "nvc_train_grads: null argument");
+    NVC_REQUIRE(pos && tgt && ws && m->grad_fx, "nvc_train_grads: null argument");
     NVC_REQUIRE(n_shards >= 1 && shard >= 0 && shard < n_shards, "nvc_train_grads: bad shard");
     NVC_REQUIRE(m->out_sigmoid == 1 || m->out_sigmoid == 0, "bad output activation");
     if (b_max <= 0) return NVC_OK;
     Net net = net_of(m);
     GridDev g = grid_of(m);
-    const int smem = mlp_smem_bytes(net);
-    NVC_REQUIRE(smem <= 200 * 1024, "nvc_train_grads: MLP too wide for the fp32 tile kernel");
     const int64_t rows_max = b_max / n_shards + 1;
     const int nblk = grid1(rows_max, kRows);
     float* part_w = (float*)ws;
     double* part_loss = (double*)((char*)ws + ((int64_t)nblk * net.mlp_count * 4 + 255) / 256 * 256);
     cudaStream_t s = (cudaStream_t)stream;
-    bool tiled = true;
-    for (int i = 0; i <= net.n_layers; ++i) tiled = tiled && (net.dims[i] % 4 == 0);
-    const int smem2 = t2_layout(net).total * 4 + 64;
-    if (tiled && smem2 <= 200 * 1024) {
-        cudaFuncSetAttribute(k_train2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
-        k_train2<<<nblk, kThreads, smem2, s>>>(g, net, m->params, pos, b_max, b_dev, shard, n_shards, tgt, mask,
-                                               m->grad_fx, m->touched, epoch, part_w, part_loss);
+    bool split = g.F <= 8;
+    for (int i = 0; i <= net.n_layers; ++i) split = split && (net.dims[i] % 4 == 0);
+    const int smem3 = t3_layout(net).total * 4 + 64;
+    if (split && smem3 <= 200 * 1024) {
+        char* p2 = (char*)part_loss + ((int64_t)nblk * 8 + 255) / 256 * 256;
+        float* act0 = (float*)p2;
+        float* dact0 = (float*)(p2 + ((int64_t)nblk * kRows * net.dims[0] * 4 + 255) / 256 * 256);
+        k_tr_encode<<<grid1(rows_max * g.L, 128), 128, 0, s>>>(g, m->params, pos, b_max, b_dev, shard, n_shards, act0);
+        rc = check_launch("k_tr_encode");
+        if (rc) return rc;
+        cudaFuncSetAttribute(k_train3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+        k_train3<<<nblk, kThreads, smem3, s>>>(net, m->params, act0, b_max, b_dev, shard, n_shards, tgt, mask, dact0,
+                                               part_w, part_loss);
+        rc = check_launch("k_train3");
+        if (rc) return rc;
+        k_tr_scatter<<<grid1(rows_max * g.L, 128), 128, 0, s>>>(g, pos, b_max, b_dev, shard, n_shards, dact0,
+                                                                 m->grad_fx);
     } else {
+        const int smem = mlp_smem_bytes(net);
+        NVC_REQUIRE(smem <= 200 * 1024, "nvc_train_grads: MLP too wide for the fp32 tile kernel");
         cudaFuncSetAttribute(k_mlp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         k_mlp<true><<<nblk, kThreads, smem, s>>>(g, net, m->params, pos, b_max, b_dev, shard, n_shards, tgt, mask,
-                                                  nullptr, m->grad_fx, m->touched, epoch, part_w, part_loss);
+                                                  nullptr, m->grad_fx, part_w, part_loss);
     }
-    rc = check_launch("k_mlp<train>");
+    rc = check_launch("nvc_train_grads");
     if (rc) return rc;
     k_reduce_parts<<<grid1(net.mlp_count, 32), 256, 0, s>>>(part_w, part_loss, nblk, net.mlp_count,
                                                              net.grid_count, m->grad_fx, loss_out);
     return check_launch("k_reduce_parts");
 }
 
-int nvc_adam_step(const nvc_model* m, int64_t t, double lr, uint16_t epoch, int32_t dense, void* stream) {
+int nvc_adam_step(const nvc_model* m, int64_t t, double lr, void* stream) {
     int rc = validate(m);
     if (rc) return rc;
     NVC_REQUIRE(t >= 1, "nvc_adam_step: t must be >= 1");
-    NVC_REQUIRE(m->adam_m && m->adam_v && m->grad_fx && m->touched && m->table_h && m->wpack,
-                "nvc_adam_step: state not bound");
+    NVC_REQUIRE(m->adam_m && m->adam_v && m->grad_fx && m->table_h && m->wpack, "nvc_adam_step: state not bound");
     Net net = net_of(m);
     AdamK a;
     a.b1 = (float)0.9;
@@ -894,9 +962,21 @@ int nvc_adam_step(const nvc_model* m, int64_t t, double lr, uint16_t epoch, int3
     a.inv_b1c = 1.0 / (double)a.b1c;
     a.inv_b2c = 1.0 / (double)a.b2c;
     cudaStream_t s = (cudaStream_t)stream;
-    k_adam_grid<<<grid1((net.grid_count + 7) / 8, 256), 256, 0, s>>>(m->params, m->adam_m, m->adam_v, m->grad_fx,
-                                                                     m->touched, m->table_h, net.grid_count,
-                                                                     m->features, epoch, dense, a, m->table_size);
+    if (m->features == 2 && m->table_size % 64 == 0 && net.grid_count % kAdamTile == 0 && !getenv("NVC_ADAM_FLAT")) {
+        const int smem = kAdamStages * (int)sizeof(AdamStage);
+        cudaFuncSetAttribute(k_adam_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int dev = 0, sms = kNumSMs;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t ntiles = net.grid_count / kAdamTile;
+        const int grid = (int)std::min<int64_t>(ntiles, 5 * (int64_t)sms);
+        k_adam_bulk<<<grid, kAdamThreads, smem, s>>>(m->params, m->adam_m, m->adam_v, m->grad_fx, m->table_h, ntiles,
+                                                     a, m->table_size);
+    } else {
+        k_adam_flat<<<grid1(net.grid_count, 256), 256, 0, s>>>(m->params, m->adam_m, m->adam_v, m->grad_fx,
+                                                               m->table_h, net.grid_count, m->features, a,
+                                                               m->table_size);
+    }
     rc = check_launch("k_adam_grid");
     if (rc) return rc;
     k_adam_mlp<<<grid1(net.mlp_count, 256), 256, 0, s>>>(net, m->params, m->adam_m, m->adam_v, m->grad_fx,

@@ -249,7 +249,6 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_tiles(MNet net, const fl
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int a0_bytes = kT * net.kp[0] * 2;
     const int a1_bytes = kT * net.act_kp * 2;
-    const int K = net.dims[net.n_layers];
     {
         const uint4* src = reinterpret_cast<const uint4*>(wpack);
         uint4* dst = reinterpret_cast<uint4*>(s_w);
@@ -373,26 +372,36 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_tiles(MNet net, const fl
                     } else {
                         const int64_t tile = blockIdx.x + (int64_t)(q0 + j) * gridDim.x;
                         const int64_t p = tile * kT + row;
+                        __half* vrow = vis16 + p * vstride;
                         for (int c = 0; c < net.np[l] / 16; ++c) {
                             float v[16];
                             tld16(t_acc + (uint32_t)(c * 16), v);
                             if (p >= P) continue;
+                            __align__(16) __half2 h[8];
 #pragma unroll
-                            for (int e = 0; e < 16; ++e) {
-                                const int k = c * 16 + e;
-                                if (k >= K) break;
-                                const float z = v[e] + s_bias[bias_off + k];
-                                float a;
-                                if (net.out_sigmoid) {
-                                    const float ez = __expf(-fabsf(z));
-                                    const float r = __fdividef(1.0f, 1.0f + ez);
-                                    a = z >= 0.0f ? r : ez * r;
-                                    a = fminf(fmaxf(a, 1e-6f), 0.999999f);
-                                } else {
-                                    a = z >= 0.0f ? z : net.alpha * z;
+                            for (int e = 0; e < 8; ++e) {
+                                float a2[2];
+#pragma unroll
+                                for (int t = 0; t < 2; ++t) {
+                                    const float z = v[2 * e + t] + s_bias[bias_off + c * 16 + 2 * e + t];
+                                    float a;
+                                    if (net.out_sigmoid) {
+                                        const float ez = __expf(-fabsf(z));
+                                        const float r = __fdividef(1.0f, 1.0f + ez);
+                                        a = z >= 0.0f ? r : ez * r;
+                                        a = fminf(fmaxf(a, 1e-6f), 0.999999f);
+                                    } else {
+                                        a = z >= 0.0f ? z : net.alpha * z;
+                                    }
+                                    a2[t] = a;
                                 }
-                                vis16[(int64_t)k * vstride + p] = __float2half_rn(a);
+                                h[e] = __floats2half2_rn(a2[0], a2[1]);
                             }
+                            // padded columns (>= K, zero weights) land in the row's padding
+                            if (c * 16 < vstride)
+                                *reinterpret_cast<uint4*>(vrow + c * 16) = *reinterpret_cast<const uint4*>(h);
+                            if (c * 16 + 8 < vstride)
+                                *reinterpret_cast<uint4*>(vrow + c * 16 + 8) = *reinterpret_cast<const uint4*>(h + 4);
                         }
                         tc_before();
                         mbar_arrive(&bars.acc_empty[j]);
@@ -432,6 +441,95 @@ struct WArgs {
     double* rgb;
 };
 
+template <bool kLum64>
+__device__ __forceinline__ double lum_at(const WArgs& a, int k, int64_t p) {
+    const int64_t li = (int64_t)k * a.stride + p;
+    if constexpr (kLum64) return __ldg(reinterpret_cast<const double*>(a.lum) + li);
+    else return (double)__ldg(reinterpret_cast<const float*>(a.lum) + li);
+}
+
+// w_k = max(vis_k, floor) * lum_k in binary64 (sampling.py:27-30 clamp_visibility, nls_weights_batch)
+__device__ __forceinline__ double wrs_weight(float vis, double t, double floor) {
+    double vv = (double)vis;
+    vv = floor > 0.0 ? fmax(vv, floor) : fmax(vv, 0.0);
+    return __dmul_rn(vv, t);
+}
+
+// K <= 32 (the C2 / paper configuration).  Sequential FP64 reservoir exactly
+// as wrs_select_batch (sampling.py:74-85): s += w_k; accept k when
+// u_k * s < w_k; the last accept wins.  Each lane walks only its own nonzero
+// lights (nz_mask), so a warp runs max-popcount iterations rather than the
+// union of the lanes' lights; zero weights never need a uniform (u*s < 0 is
+// impossible), so their Philox blocks are skipped.  The pixel's fp16
+// visibility row (64 B, written by k_mlp_tiles) is staged in shared memory
+// with a 33-word row stride, so per-lane light indices hit distinct banks.
+constexpr int kWrsThreads = 256;
+template <bool kLum64>
+__global__ void __launch_bounds__(kWrsThreads) k_nls32(WArgs a, nvc_scene sc) {
+    __shared__ uint32_t s_vis[kWrsThreads * 33];
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t* my = s_vis + threadIdx.x * 33;
+    if (p < a.P) {
+        const uint4* vrow = reinterpret_cast<const uint4*>(a.vis16 + p * a.vstride);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (8 * i < a.K) {
+                const uint4 v = __ldg(vrow + i);
+                my[4 * i] = v.x;
+                my[4 * i + 1] = v.y;
+                my[4 * i + 2] = v.z;
+                my[4 * i + 3] = v.w;
+            }
+    }
+    if (p >= a.P) return;
+    const int64_t gp = a.p_first + p;
+    uint32_t m = a.nz_mask ? __ldg(a.nz_mask + p) : 0xffffffffu;
+    if (a.K < 32) m &= (1u << a.K) - 1u;
+    double s = 0.0, wsel = 0.0;
+    int sel = -1;
+    uint64_t blk = 0;
+    U4 u;
+    const uint64_t n0 = a.offset + (uint64_t)gp * (uint64_t)a.K;
+    while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t pair = my[k >> 1];
+        const float vis = __half2float(__ushort_as_half((unsigned short)((k & 1) ? (pair >> 16) : (pair & 0xffffu))));
+        const double w = wrs_weight(vis, lum_at<kLum64>(a, k, p), a.floor);
+        s = __dadd_rn(s, w);
+        if (w > 0.0) {
+            const uint64_t n = n0 + (uint64_t)k;
+            const uint64_t bi = n / 4 + 1;
+            if (bi != blk) {
+                u = philox_fn(bi, a.key);
+                blk = bi;
+            }
+            if (__dmul_rn(u01(u.x[n & 3]), s) < w) {
+                sel = k;
+                wsel = w;
+            }
+        }
+    }
+    const uint64_t n = a.offset + (uint64_t)a.p_total * (uint64_t)a.K + 2ull * (uint64_t)gp;
+    const U4 b0 = philox_fn(n / 4 + 1, a.key);
+    const double u0 = u01(b0.x[n & 3]);
+    double u1;
+    if ((n & 3) != 3) {
+        u1 = u01(b0.x[(n & 3) + 1]);
+    } else {
+        const U4 b1 = philox_fn(n / 4 + 2, a.key);
+        u1 = u01(b1.x[0]);
+    }
+    double y[3];
+    light_point(sc, sel, u0, u1, y);
+    a.ids[p] = sel;
+    a.big_w[p] = sel >= 0 ? __ddiv_rn(s, wsel > 0.0 ? wsel : 1.0) : 0.0;
+    a.pts[3 * p] = y[0];
+    a.pts[3 * p + 1] = y[1];
+    a.pts[3 * p + 2] = y[2];
+}
+
+// generic K: forward reservoir over the nonzero lights (pixel-major visibilities)
 template <bool kNls>
 __global__ void __launch_bounds__(256) k_wrs_tiles(WArgs a, nvc_scene sc) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -449,14 +547,10 @@ __global__ void __launch_bounds__(256) k_wrs_tiles(WArgs a, nvc_scene sc) {
         while (mm) {
             const int k = k0 + __ffs(mm) - 1;
             mm &= mm - 1;
-            const float vis = __half2float(__ldg(a.vis16 + (int64_t)k * a.vstride + p));
-            const int64_t li = (int64_t)k * a.stride + p;
-            const double t = a.lum_f64 ? __ldg(reinterpret_cast<const double*>(a.lum) + li)
-                                       : (double)__ldg(reinterpret_cast<const float*>(a.lum) + li);
+            const float vis = __half2float(__ldg(a.vis16 + p * a.vstride + k));
+            const double t = a.lum_f64 ? lum_at<true>(a, k, p) : lum_at<false>(a, k, p);
             if (kNls) {
-                double vv = (double)vis;
-                vv = a.floor > 0.0 ? fmax(vv, a.floor) : fmax(vv, 0.0);
-                const double w = __dmul_rn(vv, t);
+                const double w = wrs_weight(vis, t, a.floor);
                 s = __dadd_rn(s, w);
                 if (w > 0.0) {   // zero weights never need a uniform (u*s < 0 is impossible)
                     const uint64_t n = a.offset + (uint64_t)gp * (uint64_t)a.K + (uint64_t)k;
@@ -501,11 +595,12 @@ __global__ void __launch_bounds__(256) k_wrs_tiles(WArgs a, nvc_scene sc) {
     }
 }
 
-// fp16 light-major visibilities -> (P, K) f32 (the infer() output)
+// fp16 pixel-major visibilities (row stride vstride halfs) -> (P, K) f32 (the infer() output)
 __global__ void k_vis_out(const __half* __restrict__ vis16, int64_t vstride, int64_t P, int K, float* __restrict__ out) {
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= P) return;
-    for (int k = 0; k < K; ++k) out[p * K + k] = __half2float(vis16[(int64_t)k * vstride + p]);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P * K) return;
+    const int64_t p = i / K;
+    out[i] = __half2float(vis16[p * vstride + (i - p * K)]);
 }
 
 int make_mnet(const nvc_model* m, MNet& q) {
@@ -561,6 +656,12 @@ int make_mnet(const nvc_model* m, MNet& q) {
 
 inline int grid1(int64_t n, int bs) { return (int)((n + bs - 1) / bs); }
 
+cudaEvent_t g_stage_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+int g_n_stage_ev = 0;
+inline void stage_mark(int i, cudaStream_t s) {
+    if (i < g_n_stage_ev) cudaEventRecord(g_stage_ev[i], s);
+}
+
 // encode + MLP: vis16 (K rows of vstride halfs); ws holds the feature tiles
 int run_front(const nvc_model* m, const double* pos, int64_t P, uint8_t* tiles, __half* vis16, int64_t vstride,
               cudaStream_t s) {
@@ -569,12 +670,14 @@ int run_front(const nvc_model* m, const double* pos, int64_t P, uint8_t* tiles, 
     if (rc) return rc;
     GridDev g = grid_of(m);
     const int64_t ntiles = (P + kT - 1) / kT;
+    stage_mark(0, s);
     if (g.F == 2)
         k_enc_tiles<true><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
     else
         k_enc_tiles<false><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
     rc = check_launch("k_enc_tiles");
     if (rc) return rc;
+    stage_mark(1, s);
     cudaFuncSetAttribute(k_mlp_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, q.sm_total);
     int dev = 0, sms = kNumSMs;
     cudaGetDevice(&dev);
@@ -582,7 +685,9 @@ int run_front(const nvc_model* m, const double* pos, int64_t P, uint8_t* tiles, 
     int grid = (int)(ntiles < sms ? ntiles : sms);
     if (const char* e = getenv("NVC_QUERY_GRID")) grid = max(1, min(grid, atoi(e)));
     k_mlp_tiles<<<grid, kMlpThreads, q.sm_total, s>>>(q, m->params, m->wpack, tiles, ntiles, P, vis16, vstride);
-    return check_launch("k_mlp_tiles");
+    rc = check_launch("k_mlp_tiles");
+    stage_mark(2, s);
+    return rc;
 }
 
 }  // namespace
@@ -590,8 +695,8 @@ int run_front(const nvc_model* m, const double* pos, int64_t P, uint8_t* tiles, 
 int64_t pipeline_workspace_bytes(const nvc_model* m, int64_t P) {
     const int kp0 = umma_kpad(m->levels * m->features);
     const int64_t ntiles = (P + kT - 1) / kT;
-    const int64_t vstride = (P + 63) / 64 * 64;
-    return ntiles * kT * kp0 * 2 + (int64_t)m->dims[m->n_layers] * vstride * 2 + 1024;
+    const int64_t vstride = (m->dims[m->n_layers] + 7) / 8 * 8;
+    return ntiles * kT * kp0 * 2 + ntiles * kT * vstride * 2 + 1024;
 }
 
 int pipeline_query(const nvc_model* m, const nvc_scene* sc, const double* pos, int64_t P, int mode,
@@ -600,14 +705,14 @@ int pipeline_query(const nvc_model* m, const nvc_scene* sc, const double* pos, i
                    const double* albedo, double* rgb, float* vis_out, void* ws, cudaStream_t s) {
     const int kp0 = umma_kpad(m->levels * m->features);
     const int64_t ntiles = (P + kT - 1) / kT;
-    const int64_t vstride = (P + 63) / 64 * 64;
+    const int64_t vstride = (m->dims[m->n_layers] + 7) / 8 * 8;   // pixel-major fp16 rows
     uint8_t* tiles = reinterpret_cast<uint8_t*>(ws);
     __half* vis16 = reinterpret_cast<__half*>(tiles + (ntiles * kT * kp0 * 2 + 255) / 256 * 256);
     int rc = run_front(m, pos, P, tiles, vis16, vstride, s);
     if (rc) return rc;
     const int K = m->dims[m->n_layers];
     if (mode == 0) {
-        k_vis_out<<<grid1(P, 256), 256, 0, s>>>(vis16, vstride, P, K, vis_out);
+        k_vis_out<<<grid1(P * K, 256), 256, 0, s>>>(vis16, vstride, P, K, vis_out);
         return check_launch("k_vis_out");
     }
     WArgs a;
@@ -630,11 +735,44 @@ int pipeline_query(const nvc_model* m, const nvc_scene* sc, const double* pos, i
     a.big_w = big_w;
     a.albedo = albedo;
     a.rgb = rgb;
-    if (mode == 1)
+    if (mode == 1 && K <= 32 && getenv("NVC_WRS_FORWARD") == nullptr) {
+        if (lum_f64)
+            k_nls32<true><<<grid1(P, kWrsThreads), kWrsThreads, 0, s>>>(a, *sc);
+        else
+            k_nls32<false><<<grid1(P, kWrsThreads), kWrsThreads, 0, s>>>(a, *sc);
+    } else if (mode == 1)
         k_wrs_tiles<true><<<grid1(P, 256), 256, 0, s>>>(a, *sc);
     else
         k_wrs_tiles<false><<<grid1(P, 256), 256, 0, s>>>(a, *sc);
-    return check_launch("k_wrs_tiles");
+    const int rc2 = check_launch("k_wrs_tiles");
+    stage_mark(3, s);
+    return rc2;
 }
 
 }  // namespace nvc
+
+extern "C" int nvc_profile_stages(int32_t enable) {
+    if (enable && !nvc::g_stage_ev[0])
+        for (int i = 0; i < 4; ++i)
+            if (cudaEventCreate(&nvc::g_stage_ev[i]) != cudaSuccess) {
+                nvc::set_error("nvc_profile_stages: cudaEventCreate failed");
+                return NVC_ERR_CUDA;
+            }
+    nvc::g_n_stage_ev = enable ? 4 : 0;
+    return NVC_OK;
+}
+
+extern "C" int nvc_profile_stage_ms(float* ms3) {
+    if (!ms3 || !nvc::g_stage_ev[0]) {
+        nvc::set_error("nvc_profile_stage_ms: profiling never enabled");
+        return NVC_ERR_ARG;
+    }
+    if (cudaEventSynchronize(nvc::g_stage_ev[3]) != cudaSuccess) return NVC_ERR_CUDA;
+    for (int i = 0; i < 3; ++i)
+        if (cudaEventElapsedTime(ms3 + i, nvc::g_stage_ev[i], nvc::g_stage_ev[i + 1]) != cudaSuccess) {
+            cudaGetLastError();
+            nvc::set_error("nvc_profile_stage_ms: no recorded query since enabling");
+            return NVC_ERR_CUDA;
+        }
+    return NVC_OK;
+}

@@ -145,13 +145,12 @@ def train_frame_device(scene, camera, cache, cfg: TrainFrameConfig, frame: int =
     loss = None
     for step in range(cfg.steps):
         gen_batch_device(scene, camera, bufs, cfg.seed, frame, step, shard, n_shards)
-        cache.next_epoch()
         bufs.loss.zero_()
         cache.accumulate_grads(bufs.pos, bufs.tgt, b_max=bufs.n_world + bufs.n_screen, b_dev=bufs.n_rows,
                                shard=shard, n_shards=n_shards, loss_out=bufs.loss)
         if comm is not None:
             comm(cache.grad_fx, bufs.loss)
-        cache.apply_adam(dense_grad=comm is not None)
+        cache.apply_adam()
         loss = bufs.loss[0] / bufs.n_rows[0].to(bufs.loss.dtype)
     return loss, bufs
 
@@ -169,7 +168,6 @@ def train_frame(scene, camera, cache, cfg: TrainFrameConfig, frame: int = 0, clu
         b = int(bufs.n_rows.item())
         if b == 0:            # training.py:196-197: empty batch -> no update
             continue
-        cache.next_epoch()
         bufs.loss.zero_()
         cache.accumulate_grads(bufs.pos, bufs.tgt, b_max=b, shard=0, n_shards=1, loss_out=bufs.loss)
         cache.apply_adam()

@@ -263,6 +263,21 @@ class TestSampling:
         want = ((vis16.astype(np.float64) * f) @ boxes32.lt_radiance) * alb.cpu().numpy() / np.pi
         np.testing.assert_allclose(rgb, want, rtol=1e-9, atol=1e-12)
 
+    def test_stage_profiling_hook(self, boxes32):
+        """nvc_profile_stages / nvc_profile_stage_ms time the three query kernels."""
+        import ctypes
+        from paper_2506_05930_b200 import _lib
+        from paper_2506_05930_b200.render import gbuffer_device
+        pos, nrm, alb, _, _ = gbuffer_device(boxes32, boxes32.camera.resized(64, 32))
+        ctx = PixelCtx(boxes32, pos, nrm, alb)
+        c = VisibilityCache(MODE_LIGHTS, 32, grid_cfg(boxes32, 16, 1 << 19), hidden_dims=(64, 64, 64))
+        _lib.call("nvc_profile_stages", 1)
+        nls_sample_batch(ctx, c, R.Stream(key=R.stream_key(0, 1, "light-select")))
+        _lib.call("nvc_profile_stages", 0)
+        ms = (ctypes.c_float * 3)()
+        _lib.call("nvc_profile_stage_ms", ctypes.addressof(ms))
+        assert all(0.0 < x < 1000.0 for x in ms)
+
     def test_tile_sharded_nls_matches_whole_frame(self, boxes32, g_samp):
         from paper_2506_05930_b200.sampling import nls_sample_device
         c = VisibilityCache(MODE_LIGHTS, 32, grid_cfg(boxes32, 16, 1 << 19), hidden_dims=(64, 64, 64))
@@ -297,7 +312,10 @@ class TestTraining:
     def _c1(self, pbox8, seed=0):
         return VisibilityCache(MODE_LIGHTS, 8, grid_cfg(pbox8, 8, 1 << 14), seed=seed, hidden_dims=(64, 64))
 
-    def test_adam_bit_exact_given_grads(self, pbox8):
+    @pytest.mark.parametrize("kernel", ["bulk", "flat"])
+    def test_adam_bit_exact_given_grads(self, pbox8, kernel, monkeypatch):
+        if kernel == "flat":
+            monkeypatch.setenv("NVC_ADAM_FLAT", "1")
         c = self._c1(pbox8)
         p0 = c.params.cpu().numpy().copy()
         g = np.random.default_rng(5)
@@ -308,12 +326,11 @@ class TestTraining:
             fx = np.rint(gd * 2.0 ** 48).astype(np.int64)
             gf = (fx.astype(np.float64) * 2.0 ** -48).astype(np.float32)   # what the kernel reads
             c.grad_fx.copy_(torch.from_numpy(fx))
-            c.next_epoch()
             lr = 0.05 - 0.001 * t
             c.step = 0
             c.train_cfg.lr_start = lr
             c.train_cfg.lr_end = min(lr, c.train_cfg.lr_end)
-            c.apply_adam(dense_grad=True)
+            c.apply_adam()
             st.step(p, gf, lr)
             np.testing.assert_array_equal(c.params.cpu().numpy(), p)
         np.testing.assert_array_equal(c.adam_m.cpu().numpy(), st.m)
@@ -325,16 +342,19 @@ class TestTraining:
         np.testing.assert_array_equal(t2[:, :, 0], tab)                       # own slot
         np.testing.assert_array_equal(t2[:, :, 1], np.roll(tab, -1, axis=1))  # x-neighbour (mod T)
 
-    def test_touched_map_adam_equals_dense(self, pbox8, g_train):
+    def test_bulk_and_flat_adam_agree_and_consume_grads(self, pbox8, g_train, monkeypatch):
         a, b = self._c1(pbox8), self._c1(pbox8)
-        pos, tgt = g_train["c1_pos"], g_train["c1_tgt"].astype(np.float32)
-        for c, dense in ((a, False), (b, True)):
-            pt = torch.from_numpy(pos).to(DEV)
-            tt = torch.from_numpy(tgt).to(DEV)
-            c.next_epoch()
+        pt = torch.from_numpy(g_train["c1_pos"]).to(DEV)
+        tt = torch.from_numpy(g_train["c1_tgt"].astype(np.float32)).to(DEV)
+        for c, flat in ((a, False), (b, True)):
+            if flat:
+                monkeypatch.setenv("NVC_ADAM_FLAT", "1")
             c.accumulate_grads(pt, tt)
-            c.apply_adam(dense_grad=dense)
+            assert c.grad_fx.any()
+            c.apply_adam()
+            assert not c.grad_fx.any()          # the accumulator is consumed (zeroed) by Adam
         np.testing.assert_array_equal(a.params.cpu().numpy(), b.params.cpu().numpy())
+        np.testing.assert_array_equal(a.table_h.cpu().numpy(), b.table_h.cpu().numpy())
 
     def test_first_step_vs_reference(self, pbox8, g_train):
         c = self._c1(pbox8)
@@ -385,9 +405,7 @@ class TestTraining:
         pos = torch.from_numpy(g_train["c1_pos"]).to(DEV)
         tgt = torch.from_numpy(g_train["c1_tgt"].astype(np.float32)).to(DEV)
         full, parts = self._c1(pbox8), self._c1(pbox8)
-        full.next_epoch()
         full.accumulate_grads(pos, tgt)
-        parts.next_epoch()
         b = pos.shape[0]
         for sh in range(4):
             lo, hi = b * sh // 4, b * (sh + 1) // 4

@@ -1,5 +1,6 @@
+"""Profiling aid: tcgen05 MMA / TMEM-load latency microbenchmarks (micro.cu nvc_micro)."""
 import ctypes, os, sys
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2506_05930_b200 import _lib
 lib = _lib.load()
