@@ -27,27 +27,33 @@ def nvcc() -> str:
     return cand if os.path.exists(cand) else "nvcc"
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    objdir = os.path.join(HERE, "build")
+def build(verbose: bool = False, force: bool = False, defs: list[str] | None = None, out: str = OUT) -> str:
+    """defs: extra -D flags (profiling builds, e.g. ["-DNVC_TRACE"] -> a separate .so)."""
+    defs = defs or []
+    objdir = os.path.join(HERE, "build" + ("_" + "_".join(d.lstrip("-D").lower() for d in defs) if defs else ""))
     os.makedirs(objdir, exist_ok=True)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(HERE, "..", "include", "nvc.h")]
     newest = max(os.path.getmtime(d) for d in deps)
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= newest:
-        return OUT
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= newest:
+        return out
     objs = []
     for unit, extra in UNITS.items():
         obj = os.path.join(objdir, unit.replace(".cu", ".o"))
-        cmd = [nvcc(), *COMMON, *extra, "-c", os.path.join(CSRC, unit), "-o", obj]
+        cmd = [nvcc(), *COMMON, *extra, *defs, "-c", os.path.join(CSRC, unit), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd))
         subprocess.check_call(cmd)
         objs.append(obj)
-    tmp = OUT + ".tmp"
+    tmp = out + ".tmp"
     subprocess.check_call([nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs])
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force=True))
+    if "--trace" in sys.argv:   # profiling build: event timeline of k_mlp_wg (tools/trace_mlp.py)
+        print(build(verbose="-v" in sys.argv, force=True, defs=["-DNVC_TRACE"],
+                    out=os.path.join(HERE, "libnvc_trace.so")))
+    else:
+        print(build(verbose="-v" in sys.argv, force=True))

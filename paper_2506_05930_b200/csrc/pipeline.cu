@@ -20,6 +20,7 @@
 // Reference routines: encode_batch hashgrid.py:117-131, forward mlp.py:110-140,
 // clamp_visibility sampling.py:27-30, wrs_select_batch :74-85,
 // nls_sample_batch :194-205, neural_di_batch :215-218.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -210,6 +211,70 @@ __global__ void __launch_bounds__(kT, 6) k_enc_tiles(GridDev g, const uint16_t* 
                 *reinterpret_cast<__half*>(img + umma_off(row, l * g.F + k, kT, kp0)) = __float2half_rn(acc[k]);
         }
     }
+}
+
+// Compile-time level count, F == 2: levels unrolled (per-level resolution /
+// dense flag / table offset become constants), FP64 cell + hash exactly as the
+// parity encoder, and the trilinear blend in packed half2 (weights (1-fx, fx)
+// times the yz weight, one HFMA2 per x-neighbour pair).
+template <int L>
+__global__ void __launch_bounds__(kT, 8) k_enc_tiles2(GridDev g, const uint16_t* __restrict__ table2,
+                                                      const double* __restrict__ pos, int64_t P, int kp0,
+                                                      uint8_t* __restrict__ tiles) {
+    const int row = threadIdx.x;
+    const int64_t tile = blockIdx.x;
+    const int64_t p = tile * kT + row;
+    uint8_t* img = tiles + tile * (int64_t)(kT * kp0 * 2);
+    if (p >= P) {
+        for (int k = 0; k < kp0; k += 8) *reinterpret_cast<uint4*>(img + umma_off(row, k, kT, kp0)) = make_uint4(0, 0, 0, 0);
+        return;
+    }
+    const double pp[3] = {__ldg(pos + 3 * p), __ldg(pos + 3 * p + 1), __ldg(pos + 3 * p + 2)};
+    double q[3];
+    normalize(g, pp, q);
+    const uint2* t2 = reinterpret_cast<const uint2*>(table2);
+#pragma unroll
+    for (int l0 = 0; l0 < L; l0 += 4) {
+        uint2 v[4][4];
+        float w[4][3];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int l = l0 + j;
+            if (l < L) {
+                uint32_t c0[3];
+                cell3(g.res[l], q, c0, w[j]);
+                const bool dense = g.dense[l] != 0;
+                const uint32_t sy = dense ? (uint32_t)g.res[l] + 1u : 2654435761u;
+                const uint32_t sz = dense ? sy * sy : 805459861u;
+                const uint32_t mask = dense ? 0xffffffffu : g.tmask;
+                const uint32_t base = c0[0] + c0[1] * sy + c0[2] * sz;
+                const uint2* tl = t2 + (size_t)l * (size_t)g.T;
+                v[j][0] = __ldg(tl + (base & mask));
+                v[j][1] = __ldg(tl + ((base + sz) & mask));
+                v[j][2] = __ldg(tl + ((base + sy) & mask));
+                v[j][3] = __ldg(tl + ((base + sy + sz) & mask));
+            }
+        }
+        __align__(16) __half2 out[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            __half2 acc = __float2half2_rn(0.0f);
+            if (l0 + j < L) {
+                const __half2 fx2 = __floats2half2_rn(1.0f - w[j][0], w[j][0]);
+                const float wy[2] = {1.0f - w[j][1], w[j][1]}, wz[2] = {1.0f - w[j][2], w[j][2]};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const __half2 wc = __hmul2(fx2, __float2half2_rn(wy[(c >> 1) & 1] * wz[c & 1]));
+                    acc = __hfma2(__low2half2(wc), *reinterpret_cast<const __half2*>(&v[j][c].x), acc);
+                    acc = __hfma2(__high2half2(wc), *reinterpret_cast<const __half2*>(&v[j][c].y), acc);
+                }
+            }
+            out[j] = acc;
+        }
+        *reinterpret_cast<uint4*>(img + umma_off(row, 2 * l0, kT, kp0)) = *reinterpret_cast<const uint4*>(out);
+    }
+    for (int k = 2 * ((L + 3) / 4 * 4); k < kp0; k += 8)
+        *reinterpret_cast<uint4*>(img + umma_off(row, k, kT, kp0)) = make_uint4(0, 0, 0, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -416,6 +481,302 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_tiles(MNet net, const fl
     tc_after();
     if (warp == 9)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(net.tmem_cols) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// stage 2 (default for widths <= 64): four self-issuing warpgroups
+//
+// Each warpgroup owns two tiles in flight (two 64-column TMEM accumulators,
+// two A0 and two A1 smem buffers) and ping-pongs between them: while it drains
+// tile A's layer-l accumulator (tcgen05.ld -> +bias -> leaky in half2 -> A1),
+// the tensor core runs tile B's layer.  An elected thread of the warpgroup
+// issues its own MMAs right after a warpgroup-local named barrier, so there is
+// no cross-warpgroup lockstep and no separate MMA/producer warps; A0 tiles of
+// the next-but-one tile are bulk-copied as soon as layer 0 has consumed the
+// buffer.  Output: sigmoid via tanh.approx (0.5 + 0.5 tanh(z/2)), clipped,
+// fp16 pixel-major rows.
+// ---------------------------------------------------------------------------
+constexpr int kWG = 4;
+constexpr int kWgThreads = 160 * kWG;   // 4 epilogue warpgroups + one MMA warp per warpgroup
+
+struct WGBars {
+    uint64_t a0_full[2], acc_full[2];
+};
+
+__device__ __forceinline__ void tld16_nowait(uint32_t taddr, uint32_t r[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// issued by a converged warp: operands stay in uniform registers, one elected lane issues
+__device__ __forceinline__ void mma_elect(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void commit_elect(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(s32(bar))
+        : "memory");
+}
+__device__ __forceinline__ float tanh_fast(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+#ifdef NVC_TRACE
+// profiling build only: (clock64 << 16 | wg << 12 | code << 8 | layer << 4 | slot) of CTA 0, one
+// 4096-entry row per warpgroup, written by its issuer with plain stores (no atomics on the path)
+__device__ unsigned long long g_wg_trace[2 * kWG * 4096];   // rows 0-3 epilogue issuers, 4-7 MMA warps
+__device__ unsigned int g_wg_trace_n;
+#define WG_TRACE(code, l, s)                                                                                  \
+    do {                                                                                                      \
+        if (blockIdx.x == 0 && trace_me && trace_n < 4096)                                                    \
+            g_wg_trace[(g + (mma_warp ? kWG : 0)) * 4096 + trace_n++] = ((unsigned long long)clock64() << 16) | ((unsigned)g << 12) | \
+                                               ((code) << 8) | ((l) << 4) | (s);                             \
+    } while (0)
+#else
+#define WG_TRACE(code, l, s) \
+    do {                     \
+    } while (0)
+#endif
+
+// swizzled K-major offset of 16-byte chunk c in row `row` of a [128 x KP] tile
+// (KP <= 64: one swizzle atom per row; common.cuh umma_off)
+template <int KP>
+struct RowSw {
+    static constexpr int lg = KP >= 64 ? 7 : (KP == 32 ? 6 : 5);
+    uint32_t rb, rx;
+    __device__ __forceinline__ explicit RowSw(int row) : rb((uint32_t)row << lg), rx((uint32_t)(row & 7) >> (7 - lg)) {}
+    __device__ __forceinline__ uint32_t chunk(int c) const { return rb + ((((uint32_t)c) ^ rx) << 4); }
+};
+
+// leaky(x + b) on 8 fp16 pairs
+__device__ __forceinline__ uint4 bias_leaky8(const uint32_t* r, uint4 b, __half2 al2) {
+    const __half2* bb = reinterpret_cast<const __half2*>(&b);
+    __align__(16) __half2 h[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        __half2 z = __floats2half2_rn(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+        z = __hadd2(z, bb[e]);
+        h[e] = __hmax2(z, __hmul2(z, al2));
+    }
+    return *reinterpret_cast<const uint4*>(h);
+}
+
+// HID: padded width of every hidden layer (MMA N and next K); OUT: padded
+// output width; KP0: padded input width.  Weights / biases / descriptors are
+// compile-time shaped; the layer count is a runtime value.
+template <int HID, int OUT, int KP0>
+__global__ void __launch_bounds__(kWgThreads, 1) k_mlp_wg(MNet net, const float* __restrict__ params,
+                                                         const uint16_t* __restrict__ wpack,
+                                                         const uint8_t* __restrict__ tiles, int64_t ntiles, int64_t P,
+                                                         __half* __restrict__ vis16, int64_t vstride) {
+    static_assert(HID <= 64 && OUT <= 64 && KP0 <= 64, "one swizzle atom per row");
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    __shared__ WGBars bars[kWG];
+    __shared__ uint32_t tbase;
+    uint8_t* smem = smem_raw + ((1024u - (s32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* s_w = smem + net.sm_w;
+    uint8_t* s_a0 = smem + net.sm_a0;
+    uint8_t* s_a1 = smem + net.sm_a1;
+    __half* s_bh = reinterpret_cast<__half*>(smem + net.sm_bias);           // hidden biases (fp16)
+    float* s_bo = reinterpret_cast<float*>(smem + net.sm_bias + 1024);       // output bias / 2 (f32)
+    const int tid = threadIdx.x, row = tid & 127;
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // warp-uniform (lets descriptors live in URs)
+    const bool mma_warp = warp >= 4 * kWG;                      // warps 16..19: MMA issuer of warpgroup warp-16
+    const int g = mma_warp ? warp - 4 * kWG : warp >> 2, wq = warp & 3;
+    const int L = net.n_layers;
+    constexpr int a0_bytes = kT * KP0 * 2;
+    constexpr int a1_bytes = kT * HID * 2;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(wpack);
+        uint4* dst = reinterpret_cast<uint4*>(s_w);
+        for (int i = tid; i < net.wpack_halfs / 8; i += kWgThreads) dst[i] = __ldg(src + i);
+        for (int l = 0; l < L - 1; ++l)
+            for (int n = tid; n < HID; n += kWgThreads)
+                s_bh[l * HID + n] = __float2half_rn(n < net.dims[l + 1] ? __ldg(params + net.boff[l] + n) : 0.0f);
+        for (int n = tid; n < OUT; n += kWgThreads)
+            s_bo[n] = n < net.dims[L] ? 0.5f * __ldg(params + net.boff[L - 1] + n) : 0.0f;
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(&tbase)), "r"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int w = 0; w < kWG; ++w)
+            for (int s = 0; s < 2; ++s) {
+                mbar_init(&bars[w].a0_full[s], 1);
+                mbar_init(&bars[w].acc_full[s], 1);
+            }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    fence_async();
+    tc_before();
+    __syncthreads();
+    tc_after();
+    const uint32_t tmem = tbase;
+    WGBars& B = bars[g];
+    const int64_t t0 = (int64_t)blockIdx.x * kWG + g, tstep = (int64_t)gridDim.x * kWG;
+    const int n_wg = ntiles > t0 ? (int)((ntiles - 1 - t0) / tstep + 1) : 0;
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    const bool issuer = !mma_warp && (tid & 127) == 0;
+#ifdef NVC_TRACE
+    unsigned trace_n = 0;
+    const bool trace_me = issuer || (mma_warp && (tid & 31) == 0);
+#endif
+    // per-layer B descriptors (k-step kk adds 2: 32 bytes inside the row's swizzle atom)
+    const uint32_t w_addr = s32(s_w);
+    auto a0_of = [&](int s) { return s_a0 + (2 * g + s) * a0_bytes; };
+    auto a1_of = [&](int s) { return s_a1 + (2 * g + s) * a1_bytes; };
+    auto acc_of = [&](int s) { return tmem + (uint32_t)((2 * g + s) * 64); };
+    auto load_a0 = [&](int k, int s) {
+        mbar_expect_tx(&B.a0_full[s], (uint32_t)a0_bytes);
+        bulk_g2s(a0_of(s), tiles + (t0 + (int64_t)k * tstep) * a0_bytes, (uint32_t)a0_bytes, &B.a0_full[s]);
+    };
+    auto issue = [&](int l, int s) {   // the warpgroup's MMA warp, converged
+        tc_after();
+        const bool first = l == 0, last = l == L - 1;
+        const int kp = first ? KP0 : HID, np = last ? OUT : HID;
+        const uint32_t idesc = (1u << 4) | ((uint32_t)(np >> 3) << 17) | ((uint32_t)(kT >> 4) << 24);
+        const uint64_t da = desc_of(s32(first ? a0_of(s) : a1_of(s)), kT, kp, 0);
+        const uint64_t db = desc_of(w_addr + 2u * (uint32_t)net.wofs[l], np, kp, 0);
+        const uint32_t d = acc_of(s);
+        WG_TRACE(6, l, s);
+        mma_elect(d, da, db, idesc, 0u);
+        WG_TRACE(7, l, s);
+        if (kp > 16) mma_elect(d, da + 2, db + 2, idesc, 1u);
+        if (kp > 32) {
+            mma_elect(d, da + 4, db + 4, idesc, 1u);
+            mma_elect(d, da + 6, db + 6, idesc, 1u);
+        }
+        WG_TRACE(8, l, s);
+        commit_elect(&B.acc_full[s]);
+        WG_TRACE(9, l, s);
+    };
+    // the epilogue warps arrive (and move on); the MMA warp waits for all 160 and issues
+    auto handoff = [&](int s) {
+        const int id = 1 + 2 * g + s;
+        if (mma_warp) asm volatile("bar.sync %0, 160;" ::"r"(id) : "memory");
+        else asm volatile("bar.arrive %0, 160;" ::"r"(id) : "memory");
+    };
+    uint32_t a0_ph[2] = {0, 0}, acc_ph[2] = {0, 0};
+    if (issuer)
+        for (int k = 0; k < 2 && k < n_wg; ++k) load_a0(k, k);
+    if (mma_warp) {
+        for (int k = 0; k < 2 && k < n_wg; ++k) {
+            mbar_wait(&B.a0_full[k], a0_ph[k]);
+            a0_ph[k] ^= 1u;
+            issue(0, k);
+        }
+        for (int k = 0; k < n_wg; k += 2)
+            for (int l = 0; l < L; ++l)
+                for (int s = 0; s < 2; ++s) {
+                    const int kk = k + s;
+                    if (kk >= n_wg) continue;
+                    handoff(s);   // epilogue of (kk, l) finished: A1 written / accumulator drained
+                    WG_TRACE(4, l, s);
+                    if (l < L - 1) {
+                        issue(l + 1, s);
+                    } else if (kk + 2 < n_wg) {
+                        mbar_wait(&B.a0_full[s], a0_ph[s]);
+                        a0_ph[s] ^= 1u;
+                        issue(0, s);
+                    }
+                    WG_TRACE(5, l, s);
+                }
+    } else {
+    const __half2 al2 = __float2half2_rn(net.alpha);
+    const RowSw<HID> sw(row);
+    for (int k = 0; k < n_wg; k += 2) {
+        for (int l = 0; l < L; ++l) {
+            for (int s = 0; s < 2; ++s) {
+                const int kk = k + s;
+                if (kk >= n_wg) continue;
+                WG_TRACE(1, l, s);
+                mbar_wait(&B.acc_full[s], acc_ph[s]);
+                acc_ph[s] ^= 1u;
+                tc_after();
+                WG_TRACE(2, l, s);
+                if (l == 0 && issuer && kk + 2 < n_wg) load_a0(kk + 2, s);   // layer 0 has read this A0
+                const uint32_t t_acc = acc_of(s) + lane_base;
+                if (l < L - 1) {
+                    uint32_t r[HID];
+#pragma unroll
+                    for (int c = 0; c < HID; c += 16) tld16_nowait(t_acc + (uint32_t)c, r + c);
+                    tld_wait();
+                    uint8_t* a1 = a1_of(s);
+                    const uint4* bias = reinterpret_cast<const uint4*>(s_bh + l * HID);
+#pragma unroll
+                    for (int c = 0; c < HID / 8; ++c)
+                        *reinterpret_cast<uint4*>(a1 + sw.chunk(c)) = bias_leaky8(r + 8 * c, bias[c], al2);
+                    fence_async();
+                    tc_before();
+                    WG_TRACE(3, l, s);
+                    handoff(s);
+                } else {
+                    uint32_t r[OUT];
+#pragma unroll
+                    for (int c = 0; c < OUT; c += 16) tld16_nowait(t_acc + (uint32_t)c, r + c);
+                    tld_wait();
+                    tc_before();
+                    WG_TRACE(3, l, s);
+                    handoff(s);   // the accumulator is drained: the next tile may overwrite it
+                    const int64_t p = (t0 + (int64_t)kk * tstep) * kT + row;
+                    if (p < P) {
+                        __half* vrow = vis16 + p * vstride;
+                        const float4* bo = reinterpret_cast<const float4*>(s_bo);
+                        const __half2 lo = __float2half2_rn(1e-6f), hi = __float2half2_rn(0.999999f);
+#pragma unroll
+                        for (int c = 0; c < OUT / 8; ++c) {
+                            __align__(16) __half2 h[4];
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const float4 b4 = bo[2 * c + e];
+                                const float* r4 = reinterpret_cast<const float*>(r + 8 * c + 4 * e);
+                                float o[4];
+                                const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+                                for (int t = 0; t < 4; ++t) {
+                                    if (net.out_sigmoid) {   // sigmoid(z) = 0.5 + 0.5 tanh(z / 2)
+                                        o[t] = fmaf(0.5f, tanh_fast(fmaf(r4[t], 0.5f, bv[t])), 0.5f);
+                                    } else {
+                                        const float zz = fmaf(2.0f, bv[t], r4[t]);
+                                        o[t] = zz >= 0.0f ? zz : net.alpha * zz;
+                                    }
+                                }
+                                h[2 * e] = __floats2half2_rn(o[0], o[1]);
+                                h[2 * e + 1] = __floats2half2_rn(o[2], o[3]);
+                                if (net.out_sigmoid) {   // clip [1e-6, 1-1e-6] (mlp.py:135-136) in fp16
+                                    h[2 * e] = __hmin2(__hmax2(h[2 * e], lo), hi);
+                                    h[2 * e + 1] = __hmin2(__hmax2(h[2 * e + 1], lo), hi);
+                                }
+                            }
+                            // padded columns (>= K, zero weights) land in the row's padding
+                            if (8 * c < vstride) *reinterpret_cast<uint4*>(vrow + 8 * c) = *reinterpret_cast<const uint4*>(h);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    }   // epilogue warps
+#ifdef NVC_TRACE
+    if (blockIdx.x == 0 && trace_me) atomicMax(&g_wg_trace_n, trace_n);
+#endif
+    tc_before();
+    __syncthreads();
+    tc_after();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -656,6 +1017,52 @@ int make_mnet(const nvc_model* m, MNet& q) {
 
 inline int grid1(int64_t n, int bs) { return (int)((n + bs - 1) / bs); }
 
+template <int HID, int OUT, int KP0>
+int launch_wg(const MNet& w, const nvc_model* m, const uint8_t* tiles, int64_t ntiles, int64_t P, __half* vis16,
+              int64_t vstride, int grid, cudaStream_t s) {
+    cudaFuncSetAttribute(k_mlp_wg<HID, OUT, KP0>, cudaFuncAttributeMaxDynamicSharedMemorySize, w.sm_total);
+    k_mlp_wg<HID, OUT, KP0><<<grid, kWgThreads, w.sm_total, s>>>(w, m->params, m->wpack, tiles, ntiles, P, vis16,
+                                                                 vstride);
+    return check_launch("k_mlp_wg");
+}
+
+// instantiated shapes (hidden, output, input padded widths); others use k_mlp_tiles
+bool wg_supported(const MNet& w) {
+    const int h = w.np[0], o = w.np[w.n_layers - 1], k = w.kp[0];
+    return h == 64 && (o == 16 || o == 32 || o == 48 || o == 64) && (k == 16 || k == 32 || k == 64);
+}
+
+int launch_mlp_wg(const MNet& w, const nvc_model* m, const uint8_t* tiles, int64_t ntiles, int64_t P, __half* vis16,
+                  int64_t vstride, int grid, cudaStream_t s) {
+    const int o = w.np[w.n_layers - 1], k = w.kp[0];
+#define NVC_WG(O, K) \
+    if (o == O && k == K) return launch_wg<64, O, K>(w, m, tiles, ntiles, P, vis16, vstride, grid, s);
+    NVC_WG(16, 16) NVC_WG(16, 32) NVC_WG(16, 64) NVC_WG(32, 16) NVC_WG(32, 32) NVC_WG(32, 64)
+    NVC_WG(48, 16) NVC_WG(48, 32) NVC_WG(48, 64) NVC_WG(64, 16) NVC_WG(64, 32) NVC_WG(64, 64)
+#undef NVC_WG
+    set_error("k_mlp_wg: shape not instantiated");
+    return NVC_ERR_UNSUPPORTED;
+}
+
+// smem layout of k_mlp_wg (8 tiles in flight: 2 per warpgroup); false if the
+// net does not fit (accumulators wider than 64 columns or smem)
+bool wg_layout(const nvc_model* m, MNet& q) {
+    if (q.n_layers < 2) return false;
+    for (int l = 0; l < q.n_layers - 1; ++l)
+        if (q.np[l] != q.np[0] || (l > 0 && q.kp[l] != q.np[0])) return false;
+    if (q.np[q.n_layers - 1] > 64 || q.np[0] > 64 || q.kp[0] > 64) return false;
+    q.sm_w = 0;
+    q.sm_a0 = (q.wpack_halfs * 2 + 1023) / 1024 * 1024;
+    q.sm_a1 = q.sm_a0 + 2 * kWG * ((kT * q.kp[0] * 2 + 1023) / 1024 * 1024);
+    q.sm_bias = q.sm_a1 + 2 * kWG * ((kT * q.act_kp * 2 + 1023) / 1024 * 1024);
+    int nb = 0;
+    for (int l = 0; l < q.n_layers - 1; ++l) nb += q.np[l];
+    if (nb * 2 > 1024 || q.np[q.n_layers - 1] * 4 > 1024) return false;
+    q.sm_total = q.sm_bias + 1024 + q.np[q.n_layers - 1] * 4 + 1024;
+    (void)m;
+    return q.sm_total <= 227 * 1024;
+}
+
 cudaEvent_t g_stage_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 int g_n_stage_ev = 0;
 inline void stage_mark(int i, cudaStream_t s) {
@@ -671,21 +1078,33 @@ int run_front(const nvc_model* m, const double* pos, int64_t P, uint8_t* tiles, 
     GridDev g = grid_of(m);
     const int64_t ntiles = (P + kT - 1) / kT;
     stage_mark(0, s);
-    if (g.F == 2)
+    const bool h2 = !getenv("NVC_ENC_F32");
+    if (g.F == 2 && g.L == 16 && h2)
+        k_enc_tiles2<16><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
+    else if (g.F == 2 && g.L == 8 && h2)
+        k_enc_tiles2<8><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
+    else if (g.F == 2)
         k_enc_tiles<true><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
     else
         k_enc_tiles<false><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
     rc = check_launch("k_enc_tiles");
     if (rc) return rc;
     stage_mark(1, s);
-    cudaFuncSetAttribute(k_mlp_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, q.sm_total);
     int dev = 0, sms = kNumSMs;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int grid = (int)(ntiles < sms ? ntiles : sms);
-    if (const char* e = getenv("NVC_QUERY_GRID")) grid = max(1, min(grid, atoi(e)));
-    k_mlp_tiles<<<grid, kMlpThreads, q.sm_total, s>>>(q, m->params, m->wpack, tiles, ntiles, P, vis16, vstride);
-    rc = check_launch("k_mlp_tiles");
+    MNet w = q;
+    if (wg_layout(m, w) && wg_supported(w) && !getenv("NVC_MLP_QUADS")) {
+        int grid = (int)std::min<int64_t>((ntiles + kWG - 1) / kWG, sms);
+        if (const char* e = getenv("NVC_QUERY_GRID")) grid = max(1, min(grid, atoi(e)));
+        rc = launch_mlp_wg(w, m, tiles, ntiles, P, vis16, vstride, grid, s);
+    } else {
+        cudaFuncSetAttribute(k_mlp_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, q.sm_total);
+        int grid = (int)(ntiles < sms ? ntiles : sms);
+        if (const char* e = getenv("NVC_QUERY_GRID")) grid = max(1, min(grid, atoi(e)));
+        k_mlp_tiles<<<grid, kMlpThreads, q.sm_total, s>>>(q, m->params, m->wpack, tiles, ntiles, P, vis16, vstride);
+        rc = check_launch("k_mlp_tiles");
+    }
     stage_mark(2, s);
     return rc;
 }
@@ -750,6 +1169,23 @@ int pipeline_query(const nvc_model* m, const nvc_scene* sc, const double* pos, i
 }
 
 }  // namespace nvc
+
+#ifdef NVC_TRACE
+extern "C" int nvc_wg_trace(unsigned long long* host_out, int n, int reset) {
+    if (reset) {
+        unsigned z = 0;
+        cudaMemcpyToSymbol(nvc::g_wg_trace_n, &z, sizeof z);
+        static unsigned long long zeros[2 * nvc::kWG * 4096];
+        cudaMemcpyToSymbol(nvc::g_wg_trace, zeros, sizeof zeros);
+        return 0;
+    }
+    unsigned cnt = 0;   // entries per warpgroup row
+    cudaMemcpyFromSymbol(&cnt, nvc::g_wg_trace_n, sizeof cnt);
+    if (n < 2 * nvc::kWG * 4096) return 0;
+    cudaMemcpyFromSymbol(host_out, nvc::g_wg_trace, 2 * nvc::kWG * 4096 * sizeof(unsigned long long));
+    return (int)cnt;
+}
+#endif
 
 extern "C" int nvc_profile_stages(int32_t enable) {
     if (enable && !nvc::g_stage_ev[0])
