@@ -187,13 +187,16 @@ def gpu_arm(args) -> None:
     from paper_2506_05930_b200.sampling import PixelCtx, nls_sample_device
     from paper_2506_05930_b200.scene import scene_from_dict
     from paper_2506_05930_b200.scenes import boxes_scene
-    from paper_2506_05930_b200.training import BatchBuffers, train_frame_device
+    from paper_2506_05930_b200.training import BatchPipeline, train_frame_device
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    prio = int(os.environ.get("NVC_MAIN_PRIORITY", "0"))
+    if prio:
+        torch.cuda.set_stream(torch.cuda.Stream(dev, priority=prio))
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
@@ -210,7 +213,9 @@ def gpu_arm(args) -> None:
     if os.environ.get("NVC_L2_PIN"):      # measured slower (it starves the streaming Adam of L2)
         cache.pin_table_in_l2()
     cfg = TrainFrameConfig(n_world=N_WORLD * world, n_screen=N_SCREEN * world, seed=0)
-    bufs = BatchBuffers(cfg.n_world, cfg.n_screen, K, dev, world)
+    # training batches are generated one frame ahead on a side stream (they depend on
+    # the frame index only), overlapping the FP64 ray kernels with training + query
+    pipe = BatchPipeline(scene, cam, cfg, K, dev, rank, world)
     out = (torch.empty(P, dtype=torch.int64, device=dev), torch.empty((P, 3), dtype=torch.float64, device=dev),
            torch.empty(P, dtype=torch.float64, device=dev))
 
@@ -221,18 +226,24 @@ def gpu_arm(args) -> None:
     stream = torch.cuda.current_stream()
     marks = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
 
-    def frame(f, timed_parts=None):
+    last_bufs = [None]
+
+    def frame_into(f, outs, timed_parts=None):
         if timed_parts is not None:
             marks[0].record(stream)
-        loss, _ = train_frame_device(scene, cam, cache, cfg, frame=f, bufs=bufs, shard=rank,
-                                     n_shards=world, comm=comm if world > 1 else None)
+        loss, bufs = train_frame_device(scene, cam, cache, cfg, frame=f, shard=rank, n_shards=world,
+                                        comm=comm if world > 1 else None, pipeline=pipe)
+        last_bufs[0] = bufs
         if timed_parts is not None:
             marks[1].record(stream)
         nls_sample_device(ctx, cache, R.stream_key(0, f, "light-select"), 0, p_first=p_first, p_total=p_total,
-                          out=out)
+                          out=outs)
         if timed_parts is not None:
             marks[2].record(stream)
         return loss
+
+    def frame(f, timed_parts=None):
+        return frame_into(f, out, timed_parts)
 
     def barrier():
         torch.cuda.synchronize()
@@ -244,7 +255,7 @@ def gpu_arm(args) -> None:
     for f in range(args.warmup):
         frame(f)
     barrier()
-    assert int(bufs.n_rows.item()) == cfg.n_world + cfg.n_screen, "screen rays missed: batch shrank"
+    assert int(last_bufs[0].n_rows.item()) == cfg.n_world + cfg.n_screen, "screen rays missed: batch shrank"
 
     # ---- per-stage split (separate pass, events between stages and between
     #      the three query kernels, all on the launching stream) ----
@@ -275,21 +286,46 @@ def gpu_arm(args) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
 
-    # ---- e2e: host G-buffer positions in, (ids, points, W, loss) out ----
+    # ---- e2e: host G-buffer positions in, (ids, points, W, loss) out, every frame ----
+    # Copies run on their own streams (H2D and D2H engines) double-buffered
+    # against the compute stream: frame f+1's positions upload and frame f-1's
+    # results download while frame f computes.
     pos_host = pos.cpu().pin_memory()
     outs_host = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in out]
     loss_host = torch.empty(1, dtype=torch.float64, pin_memory=True)
+    pos_buf = [ctx.pos, torch.empty_like(ctx.pos)]
+    out_buf = [out, tuple(torch.empty_like(o) for o in out)]
+    s_h2d, s_d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    ev_h2d = [torch.cuda.Event() for _ in range(2)]
+    ev_comp = [torch.cuda.Event() for _ in range(2)]
+    ev_d2h = [torch.cuda.Event() for _ in range(2)]
+    for e in ev_comp + ev_d2h:
+        e.record(stream)
     e2e_steps = max(3, min(args.steps, 20))
     barrier()
     start.record(stream)
     for f in range(e2e_steps):
-        ctx.pos.copy_(pos_host, non_blocking=True)
-        loss = frame(5000 + f)
-        for h, d in zip(outs_host, out):
-            h.copy_(d, non_blocking=True)
-        loss_host.copy_(loss.reshape(1), non_blocking=True)
+        b = f % 2
+        with torch.cuda.stream(s_h2d):
+            s_h2d.wait_event(ev_comp[b])              # frame f-2 finished reading this buffer
+            pos_buf[b].copy_(pos_host, non_blocking=True)
+            ev_h2d[b].record(s_h2d)
+        stream.wait_event(ev_h2d[b])
+        stream.wait_event(ev_d2h[b])                  # frame f-2's results are downloaded
+        ctx.pos = pos_buf[b]
+        loss = frame_into(5000 + f, out_buf[b])
+        ev_comp[b].record(stream)
+        with torch.cuda.stream(s_d2h):
+            s_d2h.wait_event(ev_comp[b])
+            for h, d in zip(outs_host, out_buf[b]):
+                h.copy_(d, non_blocking=True)
+            loss_host.copy_(loss.reshape(1), non_blocking=True)
+            ev_d2h[b].record(s_d2h)
+    for e in ev_d2h:
+        stream.wait_event(e)
     end.record(stream)
     barrier()
+    ctx.pos = pos_buf[0]
     e2e_ms = start.elapsed_time(end) / e2e_steps
     t = torch.tensor([e2e_ms], device=dev)
     if world > 1:

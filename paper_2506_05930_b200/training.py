@@ -12,6 +12,7 @@ and the fused dense Adam without a host round trip; only the returned loss
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -123,6 +124,59 @@ def compute_visibility_targets(positions, scene, rng, clusters=None) -> np.ndarr
     return tgt.cpu().numpy()
 
 
+class BatchPipeline:
+    """Training batches generated one frame ahead on a side stream.
+
+    A batch depends only on (seed, frame, step) and the scene -- never on the
+    model -- so batch f+1 (primary rays, FP64 shadow rays: latency- and
+    FP64-bound kernels) can run while frame f trains and queries (mostly
+    FP32/INT/tensor work).  Two buffers alternate; events order the side
+    stream against the consumer.  One optimizer step per frame (cfg.steps == 1).
+    """
+
+    def __init__(self, scene, camera, cfg: TrainFrameConfig, k: int, device, shard: int = 0, n_shards: int = 1):
+        import torch
+        if cfg.steps != 1:
+            raise ValueError("BatchPipeline prefetches one batch per frame (cfg.steps == 1)")
+        self.scene, self.camera, self.cfg, self.shard, self.n_shards = scene, camera, cfg, shard, n_shards
+        self.bufs = [BatchBuffers(cfg.n_world, cfg.n_screen, k, device, n_shards) for _ in range(2)]
+        # the batch chain (screen rays -> compaction -> shadow rays) is latency-bound:
+        # give it priority so it completes within the frame it overlaps
+        self.side = torch.cuda.Stream(device, priority=int(os.environ.get("NVC_BATCH_PRIORITY", "-1")))
+        self.ready = [torch.cuda.Event() for _ in range(2)]
+        self.free = [torch.cuda.Event() for _ in range(2)]
+        cur = torch.cuda.current_stream(device)
+        for e in self.free:
+            e.record(cur)
+        self.pending = [None, None]       # frame whose batch each buffer holds / will hold
+
+    def _launch(self, frame: int) -> None:
+        import torch
+        b = frame % 2
+        with torch.cuda.stream(self.side):
+            self.side.wait_event(self.free[b])          # the previous frame on this buffer has trained
+            gen_batch_device(self.scene, self.camera, self.bufs[b], self.cfg.seed, frame, 0, self.shard,
+                             self.n_shards)
+            self.ready[b].record(self.side)
+        self.pending[b] = frame
+
+    def take(self, frame: int) -> BatchBuffers:
+        """The batch of `frame` (ready on the current stream); starts frame+1's batch."""
+        import torch
+        b = frame % 2
+        if self.pending[b] != frame:
+            self._launch(frame)
+        self.pending[b] = None            # consumed: the buffer is rewritten only after release()
+        torch.cuda.current_stream().wait_event(self.ready[b])
+        if self.pending[(frame + 1) % 2] != frame + 1:
+            self._launch(frame + 1)
+        return self.bufs[b]
+
+    def release(self, bufs: BatchBuffers) -> None:
+        import torch
+        self.free[self.bufs.index(bufs)].record(torch.cuda.current_stream())
+
+
 def _check_cache(cache, cfg):
     if cache.mode == MODE_CLUSTERS:
         raise NotImplementedError("clustered NVC is outside this build's hot path (SURVEY §8(f))")
@@ -133,18 +187,23 @@ def _check_cache(cache, cfg):
 
 
 def train_frame_device(scene, camera, cache, cfg: TrainFrameConfig, frame: int = 0,
-                       bufs: BatchBuffers | None = None, shard: int = 0, n_shards: int = 1, comm=None):
+                       bufs: BatchBuffers | None = None, shard: int = 0, n_shards: int = 1, comm=None,
+                       pipeline: BatchPipeline | None = None):
     """Asynchronous frame training: returns the last step's loss as a CUDA tensor.
 
     With ``n_shards > 1`` every rank builds the same global batch, computes the
     targets/gradients of its row shard and ``comm(grad_fx, loss)`` (an
-    allreduce) runs before the identical Adam update."""
+    allreduce) runs before the identical Adam update.  With ``pipeline`` the
+    batch comes from (and the next one is started on) a BatchPipeline."""
     _check_cache(cache, cfg)
-    if bufs is None:
+    if pipeline is not None:
+        bufs = pipeline.take(frame)
+    elif bufs is None:
         bufs = BatchBuffers(cfg.n_world, cfg.n_screen, cache.output_dim, cache.device, n_shards)
     loss = None
     for step in range(cfg.steps):
-        gen_batch_device(scene, camera, bufs, cfg.seed, frame, step, shard, n_shards)
+        if pipeline is None:
+            gen_batch_device(scene, camera, bufs, cfg.seed, frame, step, shard, n_shards)
         bufs.loss.zero_()
         cache.accumulate_grads(bufs.pos, bufs.tgt, b_max=bufs.n_world + bufs.n_screen, b_dev=bufs.n_rows,
                                shard=shard, n_shards=n_shards, loss_out=bufs.loss)
@@ -152,6 +211,8 @@ def train_frame_device(scene, camera, cache, cfg: TrainFrameConfig, frame: int =
             comm(cache.grad_fx, bufs.loss)
         cache.apply_adam()
         loss = bufs.loss[0] / bufs.n_rows[0].to(bufs.loss.dtype)
+    if pipeline is not None:
+        pipeline.release(bufs)
     return loss, bufs
 
 

@@ -380,6 +380,19 @@ class TestTraining:
         assert la == lb
         np.testing.assert_array_equal(pa, pb)
 
+    def test_batch_pipeline_matches_inline_generation(self, pbox8):
+        """Batches prefetched one frame ahead on a side stream train bit-identically."""
+        from paper_2506_05930_b200.training import BatchPipeline, train_frame_device
+        cfg = TrainFrameConfig(n_world=512, n_screen=512, seed=3)
+        a, b = self._c1(pbox8, seed=3), self._c1(pbox8, seed=3)
+        pipe = BatchPipeline(pbox8, pbox8.camera, cfg, 8, DEV)
+        la, lb = [], []
+        for f in range(4):
+            la.append(float(train_frame_device(pbox8, pbox8.camera, a, cfg, frame=f)[0]))
+            lb.append(float(train_frame_device(pbox8, pbox8.camera, b, cfg, frame=f, pipeline=pipe)[0]))
+        assert la == lb
+        np.testing.assert_array_equal(a.params.cpu().numpy(), b.params.cpu().numpy())
+
     def test_reference_determinism_config_loss(self, g_train):
         """levels=4, T=2^10, 64+64 batch, seed 5 (test_mlp.py:205-224): loss within 1e-4."""
         pen = {
