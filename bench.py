@@ -341,8 +341,8 @@ def gpu_arm(args) -> None:
         # (DESIGN.md section 4 gives the per-pixel figures)
         flop_px = 2 * sum(a * b for a, b in zip((32, 64, 64, 64), (64, 64, 64, 32)))
         kern = {
-            "k_enc_tiles": ("hbm", P * (24 + 64), k_ms[0]),              # pos in, fp16 feature tile out
-            "k_mlp_tiles": ("tensor", P * flop_px, k_ms[1]),             # 24,576 flop per pixel
+            "k_enc_tiles2": ("hbm", P * (24 + 64), k_ms[0]),             # pos in, fp16 feature tile out
+            "k_mlp_wg": ("tensor", P * flop_px, k_ms[1]),                # 24,576 flop per pixel
             "k_nls32": ("hbm", P * (64 + 4 * K + 4 + 40), k_ms[2]),      # vis + lum + mask in, id/W/point out
         }
         name = max(kern, key=lambda k: kern[k][2])
@@ -354,8 +354,8 @@ def gpu_arm(args) -> None:
         traffic = None
         prof = os.path.join(ROOT, "profiles", "kernel_dram_bytes.json")
         if os.path.exists(prof):
-            try:
-                traffic = json.load(open(prof)).get(name)
+            try:   # ncu dram__bytes_read+write per launch of that kernel (profiles/, committed)
+                traffic = next((v for k, v in json.load(open(prof)).items() if k.startswith(name)), None)
             except Exception:
                 traffic = None
         clk = clocks.summary()
@@ -370,8 +370,8 @@ def gpu_arm(args) -> None:
                        "pixels_per_gpu": P, "global_batch": (N_WORLD + N_SCREEN) * world,
                        "parallelism": f"dp{world} (train) + {world} screen tiles (query)",
                        "l2": "inputs > L2 every frame (lum table 265 MB + 16.8 M-parameter Adam stream 530 MB)",
-                       "stage_ms": {"train_frame": tr_ms, "query": q_ms, "k_enc_tiles": k_ms[0],
-                                    "k_mlp_tiles": k_ms[1], "k_nls32": k_ms[2]}},
+                       "stage_ms": {"train_frame": tr_ms, "query": q_ms, "k_enc_tiles2": k_ms[0],
+                                    "k_mlp_wg": k_ms[1], "k_nls32": k_ms[2]}},
             "e2e": {"value": P * world / (e2e_ms * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": int(pos_host.numel() * 8),
                     "d2h_bytes_per_step": int(sum(h.numel() * h.element_size() for h in outs_host) + 8)},

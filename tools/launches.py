@@ -1,13 +1,36 @@
-"""Profiling aid: per-kernel mean duration (us) from an ncu --metrics gpu__time_duration.sum --csv launch list."""
+"""Profiling aid: per-kernel mean duration and DRAM bytes from an
+`ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv` launch list."""
 import collections
 import csv
+import json
 import sys
 
-d = collections.defaultdict(list)
-for r in csv.DictReader(l for l in open(sys.argv[1]) if not l.startswith("==")):
-    if r.get("Metric Name") == "gpu__time_duration.sum":
+
+def load(path):
+    d = collections.defaultdict(lambda: collections.defaultdict(list))
+    for r in csv.DictReader(l for l in open(path) if not l.startswith("==")):
+        name = r["Kernel Name"].split("(")[0].split("::")[-1].strip()
         v = float(r["Metric Value"].replace(",", ""))
-        d[r["Kernel Name"].split("(")[0].split("::")[-1][:40]].append(v / (1000.0 if r["Metric Unit"] == "nsecond" else 1.0))
-tot = 0.0
-for k, v in sorted(d.items(), key=lambda kv: -sum(kv[1]) / len(kv[1])):
-    print(f"{k:42s} n={len(v):3d} mean={sum(v) / len(v):8.1f} us")
+        unit = r.get("Metric Unit", "")
+        if r["Metric Name"] == "gpu__time_duration.sum":
+            v = v / 1000.0 if unit in ("ns", "nsecond") else (v * 1000.0 if unit in ("ms", "msecond") else v)   # -> us
+        d[name][r["Metric Name"]].append(v)
+    return d
+
+
+if __name__ == "__main__":
+    d = load(sys.argv[1])
+    rows = []
+    for k, m in d.items():
+        t = m.get("gpu__time_duration.sum", [])
+        if not t:
+            continue
+        rd, wr = m.get("dram__bytes_read.sum", []), m.get("dram__bytes_write.sum", [])
+        rows.append((sum(t) / len(t), k, len(t), (sum(rd) / len(rd)) if rd else None, (sum(wr) / len(wr)) if wr else None))
+    rows.sort(reverse=True)
+    for us, k, n, rd, wr in rows:
+        dram = f"  dram r {rd / 1e6:8.1f} MB  w {wr / 1e6:8.1f} MB" if rd is not None else ""
+        print(f"{k:32s} n={n:3d} mean={us:9.1f} us{dram}")
+    if len(sys.argv) > 2:   # write {kernel: dram bytes per launch} for bench.py's roofline.traffic
+        out = {k: int(rd + wr) for us, k, n, rd, wr in rows if rd is not None}
+        json.dump(out, open(sys.argv[2], "w"), indent=1, sort_keys=True)
