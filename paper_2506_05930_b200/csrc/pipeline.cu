@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -890,6 +891,81 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32(WArgs a, nvc_scene sc) {
     a.pts[3 * p + 2] = y[2];
 }
 
+// K <= 32, K % 4 == 0 and block-aligned draw counters (offset % 4 == 0,
+// light-point counter even): the reservoir walks 4-light groups, so each
+// group's Philox block is generated once at a single (inlined) call site with
+// static word indices, and the group's luminances are loaded before the
+// Philox rounds so their latency hides behind them.  The light-point draw
+// pair is the last "group".  Same arithmetic and order as k_nls32.
+template <bool kLum64>
+__global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
+    __shared__ uint32_t s_vis[kWrsThreads * 33];
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t* my = s_vis + threadIdx.x * 33;
+    if (p < a.P) {
+        const uint4* vrow = reinterpret_cast<const uint4*>(a.vis16 + p * a.vstride);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (8 * i < a.K) {
+                const uint4 v = __ldg(vrow + i);
+                my[4 * i] = v.x;
+                my[4 * i + 1] = v.y;
+                my[4 * i + 2] = v.z;
+                my[4 * i + 3] = v.w;
+            }
+    }
+    if (p >= a.P) return;
+    const int64_t gp = a.p_first + p;
+    uint32_t m = a.nz_mask ? __ldg(a.nz_mask + p) : 0xffffffffu;
+    if (a.K < 32) m &= (1u << a.K) - 1u;
+    uint32_t jobs = 1u << 8;   // bit 8: the light-point pair
+#pragma unroll
+    for (int g = 0; g < 8; ++g) jobs |= (((m >> (4 * g)) & 15u) != 0u ? 1u : 0u) << g;
+    using LT = typename std::conditional<kLum64, double, float>::type;
+    const LT* lp = reinterpret_cast<const LT*>(a.lum) + p;
+    const uint64_t c_grp = (a.offset + (uint64_t)gp * (uint64_t)a.K) / 4 + 1;
+    const uint64_t n_lp = a.offset + (uint64_t)a.p_total * (uint64_t)a.K + 2ull * (uint64_t)gp;
+    double s = 0.0, wsel = 0.0, u0 = 0.0, u1 = 0.0;
+    int sel = -1;
+    while (jobs) {
+        const int g = __ffs(jobs) - 1;
+        jobs &= jobs - 1;
+        const bool lpj = g == 8;
+        const uint32_t bits = lpj ? 0u : (m >> (4 * g)) & 15u;
+        LT t[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) t[j] = ((bits >> j) & 1u) ? __ldg(lp + (int64_t)(4 * g + j) * a.stride) : LT(0);
+        const U4 u = philox_block(lpj ? n_lp / 4 + 1 : c_grp + (uint64_t)g, a.key);
+        if (lpj) {
+            const bool hi = (n_lp & 2) != 0;
+            u0 = u01(hi ? u.x[2] : u.x[0]);
+            u1 = u01(hi ? u.x[3] : u.x[1]);
+            break;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if ((bits >> j) & 1u) {
+                const int k = 4 * g + j;
+                const uint32_t pair = my[k >> 1];
+                const float vis = __half2float(__ushort_as_half((unsigned short)((j & 1) ? (pair >> 16) : (pair & 0xffffu))));
+                const double w = wrs_weight(vis, (double)t[j], a.floor);
+                s = __dadd_rn(s, w);
+                if (w > 0.0 && __dmul_rn(u01(u.x[j]), s) < w) {
+                    sel = k;
+                    wsel = w;
+                }
+            }
+        }
+    }
+    double y[3];
+    light_point(sc, sel, u0, u1, y);
+    a.ids[p] = sel;
+    a.big_w[p] = sel >= 0 ? __ddiv_rn(s, wsel > 0.0 ? wsel : 1.0) : 0.0;
+    a.pts[3 * p] = y[0];
+    a.pts[3 * p + 1] = y[1];
+    a.pts[3 * p + 2] = y[2];
+}
+
 // generic K: forward reservoir over the nonzero lights (pixel-major visibilities)
 template <bool kNls>
 __global__ void __launch_bounds__(256) k_wrs_tiles(WArgs a, nvc_scene sc) {
@@ -1154,7 +1230,13 @@ int pipeline_query(const nvc_model* m, const nvc_scene* sc, const double* pos, i
     a.big_w = big_w;
     a.albedo = albedo;
     a.rgb = rgb;
-    if (mode == 1 && K <= 32 && getenv("NVC_WRS_FORWARD") == nullptr) {
+    const bool aligned = K % 4 == 0 && offset % 4 == 0 && ((uint64_t)p_total * (uint64_t)K) % 2 == 0;
+    if (mode == 1 && K <= 32 && aligned && getenv("NVC_WRS_FORWARD") == nullptr) {
+        if (lum_f64)
+            k_nls32g<true><<<grid1(P, kWrsThreads), kWrsThreads, 0, s>>>(a, *sc);
+        else
+            k_nls32g<false><<<grid1(P, kWrsThreads), kWrsThreads, 0, s>>>(a, *sc);
+    } else if (mode == 1 && K <= 32 && getenv("NVC_WRS_FORWARD") == nullptr) {
         if (lum_f64)
             k_nls32<true><<<grid1(P, kWrsThreads), kWrsThreads, 0, s>>>(a, *sc);
         else

@@ -232,12 +232,13 @@ class TestSampling:
         lum = ctx.lum_matrix()          # f32 table widened to f64, as the kernel does
         sc = O.SceneArrays.from_golden(g_scenes, "boxes32_")
         key = R.stream_key(0, 9, "light-select")
-        oi, op, ow = O.nls_sample(sc, vis16, lum, key)
-        ids, pts, big_w = nls_sample_batch(ctx, c, R.Stream(key=key))
-        np.testing.assert_array_equal(ids, oi)
-        np.testing.assert_array_equal(pts, op)
-        np.testing.assert_array_equal(big_w, ow)
-        assert (ids >= 0).sum() > 100
+        for offset in (0, 1, 2, 3):   # 0: block-aligned group kernel; others: per-light kernel
+            oi, op, ow = O.nls_sample(sc, vis16, lum, key, offset=offset)
+            ids, pts, big_w = nls_sample_batch(ctx, c, R.Stream(key=key, offset=offset))
+            np.testing.assert_array_equal(ids, oi)
+            np.testing.assert_array_equal(pts, op)
+            np.testing.assert_array_equal(big_w, ow)
+            assert (ids >= 0).sum() > 100
 
     @pytest.mark.parametrize("grid", ["3", "7"])
     def test_fused_pipeline_many_tiles_per_cta(self, boxes32, g_scenes, monkeypatch, grid):
