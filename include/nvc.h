@@ -28,7 +28,7 @@ extern "C" {
 
 #define NVC_MAX_LEVELS 32
 #define NVC_MAX_LAYERS 8
-#define NVC_ABI_VERSION 2
+#define NVC_ABI_VERSION 3
 
 typedef enum {
     NVC_OK = 0,
@@ -212,7 +212,7 @@ int nvc_closest_hit(const nvc_scene *sc, const double *orig, const double *dir,
  * [b*shard/n_shards, b*(shard+1)/n_shards) only (tgt may be NULL: no targets).  pos capacity:
  * n_world+n_screen rows; tgt capacity: same rows x K (shard-local rows);
  * n_rows (device int64) receives b. */
-int64_t nvc_batch_workspace_bytes(int32_t n_screen);
+int64_t nvc_batch_workspace_bytes(int32_t n_world, int32_t n_screen);
 /* compute_visibility_targets (training.py:103-120, light mode) for given
  * positions (b,3): tgt (b,K) f32, light j / row i use draws j*2b+2i, +1. */
 int nvc_targets(const nvc_scene *sc, uint64_t key, const double *pos, int64_t b, float *tgt,

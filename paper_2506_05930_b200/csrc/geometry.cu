@@ -14,6 +14,7 @@
 //   gen_world_samples training.py:44-48, gen_screen_hits :67-94,
 //   compute_visibility_targets :103-120.
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -528,6 +529,114 @@ __global__ void __launch_bounds__(128) k_targets(nvc_scene sc, uint64_t key, con
     }
 }
 
+// Shadow rays grouped for coherence: the shard's rows are bucketed by a
+// 12-bit Morton code of their position (one CTA: shared-memory histogram,
+// scan, scatter) and a warp takes 32 consecutive bucketed rows x one light, so
+// its rays start close together and end on the same emitter -- the packet
+// traversal then visits ~one ray's path instead of the union of 32 fanned-out
+// rays.  Results are per (row, light), so the order within a bucket (atomic
+// arrival order) does not affect them.
+constexpr int kSortMax = 16384;
+constexpr int kBuckets = 4096;
+
+__device__ __forceinline__ uint32_t spread4(uint32_t v) {   // 4 bits -> every third bit
+    v &= 15u;
+    v = (v | (v << 4)) & 0x0C3u;
+    v = (v | (v << 2)) & 0x249u;
+    return v;
+}
+
+__global__ void __launch_bounds__(1024) k_morton_order(nvc_scene sc, const double* __restrict__ pos,
+                                                       const int64_t* __restrict__ n_rows, int64_t b_host, int shard,
+                                                       int n_shards, int32_t* __restrict__ order) {
+    __shared__ int hist[kBuckets];
+    __shared__ int warp_sum[32];
+    extern __shared__ int slot[];   // per row: code << 16 | rank within bucket
+    const int64_t b = n_rows ? *n_rows : b_host;
+    const int64_t lo = b * shard / n_shards, hi = b * (shard + 1) / n_shards;
+    const int n = (int)(hi - lo);
+    for (int c = threadIdx.x; c < kBuckets; c += blockDim.x) hist[c] = 0;
+    float lo3[3], inv3[3];
+    for (int a = 0; a < 3; ++a) {
+        const float span = (float)(sc.aabb_max[a] - sc.aabb_min[a]);
+        lo3[a] = (float)sc.aabb_min[a];
+        inv3[a] = span > 0.0f ? 16.0f / span : 0.0f;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        uint32_t c = 0;
+        for (int a = 0; a < 3; ++a) {
+            const float q = ((float)pos[3 * (lo + t) + a] - lo3[a]) * inv3[a];
+            c |= spread4((uint32_t)fminf(fmaxf(q, 0.0f), 15.0f)) << a;
+        }
+        slot[t] = (int)(c << 16) | atomicAdd(&hist[c], 1);
+    }
+    __syncthreads();
+    // exclusive scan of the 4096 bucket counts: 4 per thread, then across warps
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int v[4], run = 0;
+    for (int e = 0; e < 4; ++e) {
+        v[e] = run;
+        run += hist[4 * threadIdx.x + e];
+    }
+    int incl = run;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_sum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        int x = warp_sum[lane], xi = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += y;
+        }
+        warp_sum[lane] = xi - x;
+    }
+    __syncthreads();
+    const int base = warp_sum[wid] + incl - run;
+    for (int e = 0; e < 4; ++e) hist[4 * threadIdx.x + e] = base + v[e];
+    __syncthreads();
+    for (int t = threadIdx.x; t < n; t += blockDim.x) order[hist[slot[t] >> 16] + (slot[t] & 0xFFFF)] = t;
+}
+
+// compute_visibility_targets over Morton-ordered rows: block = 4 warps x 32
+// sorted rows, blockIdx.y = light.  Same per-(row, light) arithmetic as k_targets.
+__global__ void __launch_bounds__(128) k_targets_sorted(nvc_scene sc, uint64_t key, const double* __restrict__ pos,
+                                                        const int64_t* __restrict__ n_rows, int64_t b_host, int shard,
+                                                        int n_shards, const int32_t* __restrict__ order,
+                                                        float* __restrict__ tgt) {
+    __shared__ int32_t st_node[4][kStack];
+    __shared__ uint32_t st_mask[4][kStack];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j = blockIdx.y;
+    const int64_t b = n_rows ? *n_rows : b_host;
+    const int64_t lo = b * shard / n_shards, hi = b * (shard + 1) / n_shards;
+    const int64_t t = (int64_t)blockIdx.x * 128 + threadIdx.x;
+    if ((int64_t)blockIdx.x * 128 + w * 32 >= hi - lo) return;   // warp-uniform
+    const bool valid = t < hi - lo;
+    const int64_t r = valid ? order[t] : 0;
+    const int64_t i = lo + r;
+    const double x[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+    const double eps = sc.shadow_eps;
+    double y[3] = {0.0, 0.0, 0.0};
+    if (valid) {
+        double u0, u1;
+        draw2(key, (uint64_t)(2 * b * j + 2 * i), u0, u1);
+        light_point(sc, j, u0, u1, y);
+    }
+    const double dd[3] = {y[0] - x[0], y[1] - x[1], y[2] - x[2]};
+    const double dist = sqrt((dd[0] * dd[0] + dd[1] * dd[1]) + dd[2] * dd[2]);
+    const double safe = fmax(dist, 1e-300);
+    const double dir[3] = {dd[0] / safe, dd[1] / safe, dd[2] / safe};
+    double t_max = dist - eps;
+    const bool degenerate = t_max <= eps;
+    t_max = fmax(t_max, eps + 1e-12);
+    const uint32_t hits = any_hit_packet(sc, x, dir, eps, t_max, valid && !degenerate, st_node[w], st_mask[w]);
+    if (valid) tgt[r * sc.n_lights + j] = (degenerate || !((hits >> lane) & 1u)) ? 1.0f : 0.0f;
+}
+
 __global__ void k_set_rows(int64_t* n_rows, int64_t v) { *n_rows = v; }
 
 inline int grid1(int64_t n, int bs) { return (int)((n + bs - 1) / bs); }
@@ -581,7 +690,9 @@ int nvc_closest_hit(const nvc_scene* sc, const double* o, const double* d, const
     return check_launch("k_closest");
 }
 
-int64_t nvc_batch_workspace_bytes(int32_t n_screen) { return 64 + 25 * (int64_t)n_screen + 64; }
+int64_t nvc_batch_workspace_bytes(int32_t n_world, int32_t n_screen) {
+    return 64 + 25 * (int64_t)n_screen + 64 + 256 + 4 * ((int64_t)n_world + n_screen);
+}
 
 int nvc_gen_train_batch(const nvc_scene* sc, const nvc_camera* cam, uint64_t key_world, uint64_t key_screen,
                         uint64_t key_targets, int32_t n_world, int32_t n_screen, int32_t shard,
@@ -602,7 +713,16 @@ int nvc_gen_train_batch(const nvc_scene* sc, const nvc_camera* cam, uint64_t key
     const int64_t total = (int64_t)n_world + n_screen;
     const int64_t cap = total / n_shards + 1;
     if (tgt && total > 0) {
-        k_targets<<<grid1(cap, 4), 128, 0, s>>>(*sc, key_targets, pos, n_rows, 0, shard, n_shards, cap, tgt);
+        if (cap <= kSortMax && sc->n_lights <= 65535 && !getenv("NVC_TARGETS_UNSORTED")) {
+            int32_t* order = reinterpret_cast<int32_t*>((char*)ws + (64 + 25 * (int64_t)n_screen + 64 + 255) / 256 * 256);
+            const int smem = (int)cap * 4;
+            cudaFuncSetAttribute(k_morton_order, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            k_morton_order<<<1, 1024, smem, s>>>(*sc, pos, n_rows, 0, shard, n_shards, order);
+            dim3 g(grid1(cap, 128), sc->n_lights);
+            k_targets_sorted<<<g, 128, 0, s>>>(*sc, key_targets, pos, n_rows, 0, shard, n_shards, order, tgt);
+        } else {
+            k_targets<<<grid1(cap, 4), 128, 0, s>>>(*sc, key_targets, pos, n_rows, 0, shard, n_shards, cap, tgt);
+        }
     }
     return check_launch("k_targets");
 }

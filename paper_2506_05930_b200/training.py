@@ -61,7 +61,7 @@ class BatchBuffers:
         self.pos = torch.zeros((max(total, 1), 3), dtype=torch.float64, device=device)
         self.tgt = torch.zeros((max(total // n_shards + 1, 1), k), dtype=torch.float32, device=device)
         self.n_rows = torch.zeros(1, dtype=torch.int64, device=device)
-        ws = _lib.load().nvc_batch_workspace_bytes(n_screen)
+        ws = _lib.load().nvc_batch_workspace_bytes(n_world, n_screen)
         self.ws = torch.zeros(ws, dtype=torch.uint8, device=device)
         self.loss = torch.zeros(1, dtype=torch.float64, device=device)
 
@@ -88,7 +88,7 @@ def gen_world_samples(scene, n: int, rng) -> np.ndarray:
     ds = device_scene(scene)
     pos = torch.zeros((n, 3), dtype=torch.float64, device=ds.device)
     nr = torch.zeros(1, dtype=torch.int64, device=ds.device)
-    ws = torch.zeros(_lib.load().nvc_batch_workspace_bytes(0), dtype=torch.uint8, device=ds.device)
+    ws = torch.zeros(_lib.load().nvc_batch_workspace_bytes(n, 0), dtype=torch.uint8, device=ds.device)
     _lib.call("nvc_gen_train_batch", ds.struct, camera_struct(scene.camera), _fresh_key(rng), 0, 0, n, 0, 0, 1,
               pos.data_ptr(), None, nr.data_ptr(), ws.data_ptr(), _lib.stream_ptr())
     rngmod.advance(rng, 3 * n)
@@ -149,6 +149,7 @@ class BatchPipeline:
         for e in self.free:
             e.record(cur)
         self.pending = [None, None]       # frame whose batch each buffer holds / will hold
+        self.early = os.environ.get("NVC_BATCH_EARLY", "0") == "1"
 
     def _launch(self, frame: int) -> None:
         import torch
@@ -161,20 +162,26 @@ class BatchPipeline:
         self.pending[b] = frame
 
     def take(self, frame: int) -> BatchBuffers:
-        """The batch of `frame` (ready on the current stream); starts frame+1's batch."""
+        """The batch of `frame` (ready on the current stream)."""
         import torch
         b = frame % 2
         if self.pending[b] != frame:
             self._launch(frame)
         self.pending[b] = None            # consumed: the buffer is rewritten only after release()
         torch.cuda.current_stream().wait_event(self.ready[b])
-        if self.pending[(frame + 1) % 2] != frame + 1:
+        if self.early and self.pending[(frame + 1) % 2] != frame + 1:
             self._launch(frame + 1)
         return self.bufs[b]
 
-    def release(self, bufs: BatchBuffers) -> None:
+    def release(self, bufs: BatchBuffers, frame: int) -> None:
+        """`bufs` is consumed; start frame+1's batch (it overlaps this frame's query)."""
         import torch
         self.free[self.bufs.index(bufs)].record(torch.cuda.current_stream())
+        if not self.early and self.pending[(frame + 1) % 2] != frame + 1:
+            # gate the side stream on the end of this frame's training so the batch
+            # chain runs under the query, not under the train step
+            self.free[(frame + 1) % 2].record(torch.cuda.current_stream())
+            self._launch(frame + 1)
 
 
 def _check_cache(cache, cfg):
@@ -212,7 +219,7 @@ def train_frame_device(scene, camera, cache, cfg: TrainFrameConfig, frame: int =
         cache.apply_adam()
         loss = bufs.loss[0] / bufs.n_rows[0].to(bufs.loss.dtype)
     if pipeline is not None:
-        pipeline.release(bufs)
+        pipeline.release(bufs, frame)
     return loss, bufs
 
 
