@@ -228,6 +228,10 @@ def gpu_arm(args) -> None:
 
     last_bufs = [None]
 
+    # the NLS selection of frame f runs on its own stream, overlapping frame f+1's
+    # train step (it reads only the visibilities, luminances and scene)
+    sel_stream = torch.cuda.Stream(dev) if not os.environ.get("NVC_SELECT_INLINE") else None
+
     def frame_into(f, outs, timed_parts=None):
         if timed_parts is not None:
             marks[0].record(stream)
@@ -237,7 +241,7 @@ def gpu_arm(args) -> None:
         if timed_parts is not None:
             marks[1].record(stream)
         nls_sample_device(ctx, cache, R.stream_key(0, f, "light-select"), 0, p_first=p_first, p_total=p_total,
-                          out=outs)
+                          out=outs, select_stream=None if timed_parts is not None else sel_stream)
         if timed_parts is not None:
             marks[2].record(stream)
         return loss
@@ -278,6 +282,8 @@ def gpu_arm(args) -> None:
         start.record(stream)
         for f in range(args.steps):
             loss = frame(args.warmup + f)
+        if cache.select_done is not None:
+            stream.wait_event(cache.select_done)
         end.record(stream)
         barrier()
     ms = start.elapsed_time(end) / args.steps
@@ -312,17 +318,23 @@ def gpu_arm(args) -> None:
             ev_h2d[b].record(s_h2d)
         stream.wait_event(ev_h2d[b])
         stream.wait_event(ev_d2h[b])                  # frame f-2's results are downloaded
+        if sel_stream is not None:
+            sel_stream.wait_event(ev_d2h[b])
         ctx.pos = pos_buf[b]
         loss = frame_into(5000 + f, out_buf[b])
         ev_comp[b].record(stream)
         with torch.cuda.stream(s_d2h):
             s_d2h.wait_event(ev_comp[b])
+            if cache.select_done is not None:
+                s_d2h.wait_event(cache.select_done)
             for h, d in zip(outs_host, out_buf[b]):
                 h.copy_(d, non_blocking=True)
             loss_host.copy_(loss.reshape(1), non_blocking=True)
             ev_d2h[b].record(s_d2h)
     for e in ev_d2h:
         stream.wait_event(e)
+    if cache.select_done is not None:
+        stream.wait_event(cache.select_done)
     end.record(stream)
     barrier()
     ctx.pos = pos_buf[0]

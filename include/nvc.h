@@ -177,6 +177,16 @@ int nvc_nls_sample(const nvc_model *m, const nvc_scene *sc, const double *pos,
                    void *stream);
 /* Fused Neural DI (sampling.py:215-218): rgb (p,3) f64 = sum_k v_k f_k L_k * albedo/pi,
  * factor in light-major layout (f32 or f64). */
+/* nvc_nls_sample split in two (same results): the encoder + MLP write the fp16
+ * visibilities of p pixels into the workspace, and the selection reads them.
+ * The selection may run on another stream (e.g. overlapping the next frame's
+ * train step) as long as no other nvc_query_front reuses the workspace before
+ * it has finished. */
+int nvc_query_front(const nvc_model *m, const double *pos, int64_t p, void *workspace, void *stream);
+int nvc_nls_select(const nvc_model *m, const nvc_scene *sc, const void *lum, int32_t lum_f64,
+                   const uint32_t *nz_mask, int64_t p_stride, int64_t p, int64_t p_first,
+                   int64_t p_total, uint64_t key, uint64_t offset, double floor, int64_t *ids,
+                   double *pts, double *big_w, void *workspace, void *stream);
 int nvc_neural_di(const nvc_model *m, const nvc_scene *sc, const double *pos,
                   const double *albedo, const void *factor, int32_t factor_f64,
                   const uint32_t *nz_mask, int64_t p_stride, int64_t p, double *rgb, void *workspace,

@@ -78,6 +78,9 @@ _SIGS = {
                                  c_u64, c_u64, c_f64, c_vp, c_vp, c_vp, c_vp]),
     "nvc_nls_sample": (c_i32, [P(NvcModel), P(NvcScene), c_vp, c_vp, c_i32, c_vp, c_i64, c_i64, c_i64,
                                c_i64, c_u64, c_u64, c_f64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "nvc_query_front": (c_i32, [P(NvcModel), c_vp, c_i64, c_vp, c_vp]),
+    "nvc_nls_select": (c_i32, [P(NvcModel), P(NvcScene), c_vp, c_i32, c_vp, c_i64, c_i64, c_i64, c_i64,
+                               c_u64, c_u64, c_f64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "nvc_neural_di": (c_i32, [P(NvcModel), P(NvcScene), c_vp, c_vp, c_vp, c_i32, c_vp, c_i64, c_i64,
                               c_vp, c_vp, c_vp]),
     "nvc_table_mask": (c_i32, [c_vp, c_i32, c_i64, c_i64, c_i32, c_vp, c_vp]),

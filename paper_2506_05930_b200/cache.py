@@ -112,6 +112,7 @@ class VisibilityCache:
         self.model = m
         self._ws = None
         self._qws = None
+        self.select_done = None   # CUDA event: last off-stream NLS selection finished
         # "pipeline": decoupled encode -> tcgen05 MLP -> selection (default);
         # "fused": the single fused kernel
 
@@ -196,10 +197,16 @@ class VisibilityCache:
         return (out, idx.cpu().numpy(), w.cpu().numpy()) if with_ctx else out
 
     def query_workspace(self, p: int):
-        """Scratch of the fp16 query pipeline for p pixels (grown on demand)."""
+        """Scratch of the fp16 query pipeline for p pixels (grown on demand).
+
+        If a selection is still running on another stream (``select_done``),
+        the current stream first waits for it: it reads this workspace."""
         import torch
         if p <= 0:
             return None
+        if self.select_done is not None:
+            torch.cuda.current_stream().wait_event(self.select_done)
+            self.select_done = None
         need = _lib.load().nvc_query_workspace_bytes(self.model, p)
         if self._qws is None or self._qws.numel() < need:
             self._qws = torch.empty(need, dtype=torch.uint8, device=self.device)

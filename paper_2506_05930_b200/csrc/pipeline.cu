@@ -1194,26 +1194,45 @@ int64_t pipeline_workspace_bytes(const nvc_model* m, int64_t P) {
     return ntiles * kT * kp0 * 2 + ntiles * kT * vstride * 2 + 1024;
 }
 
-int pipeline_query(const nvc_model* m, const nvc_scene* sc, const double* pos, int64_t P, int mode,
-                   const void* lum, int lum_f64, int64_t stride, const uint32_t* nz_mask, int64_t p_first, int64_t p_total,
-                   uint64_t key, uint64_t offset, double floor, int64_t* ids, double* pts, double* big_w,
-                   const double* albedo, double* rgb, float* vis_out, void* ws, cudaStream_t s) {
+namespace {
+struct QueryWs {
+    uint8_t* tiles;
+    __half* vis16;
+    int64_t vstride;
+};
+QueryWs query_ws(const nvc_model* m, int64_t P, void* ws) {
     const int kp0 = umma_kpad(m->levels * m->features);
     const int64_t ntiles = (P + kT - 1) / kT;
-    const int64_t vstride = (m->dims[m->n_layers] + 7) / 8 * 8;   // pixel-major fp16 rows
-    uint8_t* tiles = reinterpret_cast<uint8_t*>(ws);
-    __half* vis16 = reinterpret_cast<__half*>(tiles + (ntiles * kT * kp0 * 2 + 255) / 256 * 256);
-    int rc = run_front(m, pos, P, tiles, vis16, vstride, s);
-    if (rc) return rc;
+    QueryWs q;
+    q.tiles = reinterpret_cast<uint8_t*>(ws);
+    q.vis16 = reinterpret_cast<__half*>(q.tiles + (ntiles * kT * kp0 * 2 + 255) / 256 * 256);
+    q.vstride = (m->dims[m->n_layers] + 7) / 8 * 8;   // pixel-major fp16 rows
+    return q;
+}
+}  // namespace
+
+// encoder + MLP: fp16 visibilities of P pixels into the workspace
+int pipeline_front(const nvc_model* m, const double* pos, int64_t P, void* ws, cudaStream_t s) {
+    const QueryWs q = query_ws(m, P, ws);
+    return run_front(m, pos, P, q.tiles, q.vis16, q.vstride, s);
+}
+
+// selection (mode 1: NLS reservoir + light point; 2: Neural DI; 0: f32 visibilities)
+// from the visibilities pipeline_front left in the workspace
+int pipeline_select(const nvc_model* m, const nvc_scene* sc, int64_t P, int mode, const void* lum, int lum_f64,
+                    int64_t stride, const uint32_t* nz_mask, int64_t p_first, int64_t p_total, uint64_t key,
+                    uint64_t offset, double floor, int64_t* ids, double* pts, double* big_w, const double* albedo,
+                    double* rgb, float* vis_out, void* ws, cudaStream_t s) {
+    const QueryWs q = query_ws(m, P, ws);
     const int K = m->dims[m->n_layers];
     if (mode == 0) {
-        k_vis_out<<<grid1(P * K, 256), 256, 0, s>>>(vis16, vstride, P, K, vis_out);
+        k_vis_out<<<grid1(P * K, 256), 256, 0, s>>>(q.vis16, q.vstride, P, K, vis_out);
         return check_launch("k_vis_out");
     }
     WArgs a;
     memset(&a, 0, sizeof a);
-    a.vis16 = vis16;
-    a.vstride = vstride;
+    a.vis16 = q.vis16;
+    a.vstride = q.vstride;
     a.lum = lum;
     a.lum_f64 = lum_f64;
     a.stride = stride;
@@ -1245,9 +1264,19 @@ int pipeline_query(const nvc_model* m, const nvc_scene* sc, const double* pos, i
         k_wrs_tiles<true><<<grid1(P, 256), 256, 0, s>>>(a, *sc);
     else
         k_wrs_tiles<false><<<grid1(P, 256), 256, 0, s>>>(a, *sc);
-    const int rc2 = check_launch("k_wrs_tiles");
+    const int rc = check_launch("k_wrs_tiles");
     stage_mark(3, s);
-    return rc2;
+    return rc;
+}
+
+int pipeline_query(const nvc_model* m, const nvc_scene* sc, const double* pos, int64_t P, int mode,
+                   const void* lum, int lum_f64, int64_t stride, const uint32_t* nz_mask, int64_t p_first, int64_t p_total,
+                   uint64_t key, uint64_t offset, double floor, int64_t* ids, double* pts, double* big_w,
+                   const double* albedo, double* rgb, float* vis_out, void* ws, cudaStream_t s) {
+    int rc = pipeline_front(m, pos, P, ws, s);
+    if (rc) return rc;
+    return pipeline_select(m, sc, P, mode, lum, lum_f64, stride, nz_mask, p_first, p_total, key, offset, floor, ids,
+                           pts, big_w, albedo, rgb, vis_out, ws, s);
 }
 
 }  // namespace nvc

@@ -122,6 +122,11 @@ inline int grid1(int64_t n, int bs) { return (int)((n + bs - 1) / bs); }
 }  // namespace
 
 int64_t pipeline_workspace_bytes(const nvc_model* m, int64_t P);
+int pipeline_front(const nvc_model* m, const double* pos, int64_t P, void* ws, cudaStream_t s);
+int pipeline_select(const nvc_model* m, const nvc_scene* sc, int64_t P, int mode, const void* lum, int lum_f64,
+                    int64_t stride, const uint32_t* nz_mask, int64_t p_first, int64_t p_total, uint64_t key,
+                    uint64_t offset, double floor, int64_t* ids, double* pts, double* big_w, const double* albedo,
+                    double* rgb, float* vis_out, void* ws, cudaStream_t s);
 int pipeline_query(const nvc_model* m, const nvc_scene* sc, const double* pos, int64_t P, int mode,
                    const void* lum, int lum_f64, int64_t stride, const uint32_t* nz_mask, int64_t p_first, int64_t p_total,
                    uint64_t key, uint64_t offset, double floor, int64_t* ids, double* pts, double* big_w,
@@ -158,6 +163,23 @@ int nvc_nls_sample(const nvc_model* m, const nvc_scene* sc, const double* pos, c
     NVC_REQUIRE(workspace, "nvc_nls_sample: needs nvc_query_workspace_bytes() of workspace");
     return pipeline_query(m, sc, pos, p, 1, lum, lum_f64, stride, nz_mask, p_first, p_total, key, offset, floor, ids, pts,
                           big_w, nullptr, nullptr, nullptr, workspace, (cudaStream_t)stream);
+}
+
+int nvc_query_front(const nvc_model* m, const double* pos, int64_t p, void* workspace, void* stream) {
+    NVC_REQUIRE(m && pos && workspace, "nvc_query_front: null argument");
+    if (p <= 0) return NVC_OK;
+    return pipeline_front(m, pos, p, workspace, (cudaStream_t)stream);
+}
+
+int nvc_nls_select(const nvc_model* m, const nvc_scene* sc, const void* lum, int32_t lum_f64, const uint32_t* nz_mask,
+                   int64_t stride, int64_t p, int64_t p_first, int64_t p_total, uint64_t key, uint64_t offset,
+                   double floor, int64_t* ids, double* pts, double* big_w, void* workspace, void* stream) {
+    NVC_REQUIRE(m && sc && lum && ids && pts && big_w && workspace, "nvc_nls_select: null argument");
+    NVC_REQUIRE(sc->n_lights == m->dims[m->n_layers], "nvc_nls_select: output_dim != scene lights");
+    NVC_REQUIRE(stride >= p && p_total >= p_first + p, "nvc_nls_select: bad stride / frame size");
+    if (p <= 0) return NVC_OK;
+    return pipeline_select(m, sc, p, 1, lum, lum_f64, stride, nz_mask, p_first, p_total, key, offset, floor, ids, pts,
+                           big_w, nullptr, nullptr, nullptr, workspace, (cudaStream_t)stream);
 }
 
 int nvc_neural_di(const nvc_model* m, const nvc_scene* sc, const double* pos, const double* albedo,

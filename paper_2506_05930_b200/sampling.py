@@ -221,10 +221,14 @@ def nls_weights_batch(ctx: PixelCtx, cache, clamp_floor: float | None = CLAMP_FL
 
 
 def nls_sample_device(ctx: PixelCtx, cache, key: int, offset: int = 0, clamp_floor=CLAMP_FLOOR,
-                      p_first: int = 0, p_total: int | None = None, out=None):
+                      p_first: int = 0, p_total: int | None = None, out=None, select_stream=None):
     """Device-resident NLS: returns (ids int64, pts (P,3) f64, W f64) CUDA tensors.
 
-    Pixels of ctx are rows p_first.. of a p_total-pixel frame (screen-tile shard)."""
+    Pixels of ctx are rows p_first.. of a p_total-pixel frame (screen-tile shard).
+    With ``select_stream`` the encoder + MLP run on the current stream and the
+    reservoir selection on ``select_stream`` (it can then overlap whatever the
+    caller launches next, e.g. the next frame's train step); the outputs are
+    ready when ``cache.select_done`` (a CUDA event) completes."""
     import torch
     p = ctx.n
     k = ctx.dscene.n_lights
@@ -240,10 +244,24 @@ def nls_sample_device(ctx: PixelCtx, cache, key: int, offset: int = 0, clamp_flo
     if _is_native(cache):
         if cache.output_dim != k:
             raise ValueError(f"cache has {cache.output_dim} outputs, scene has {k} lights")
-        _lib.call("nvc_nls_sample", cache.model, ctx.dscene.struct, ctx.pos.data_ptr(), lum.data_ptr(), lum64,
-                  _lib.ptr(ctx.mask_device("lum")), lum.shape[1], p, p_first, total, key, offset, floor,
-                  ids.data_ptr(), pts.data_ptr(), big_w.data_ptr(), _lib.ptr(cache.query_workspace(p)),
-                  _lib.stream_ptr())
+        ws = cache.query_workspace(p)
+        mask = _lib.ptr(ctx.mask_device("lum"))
+        if select_stream is None:
+            _lib.call("nvc_nls_sample", cache.model, ctx.dscene.struct, ctx.pos.data_ptr(), lum.data_ptr(), lum64,
+                      mask, lum.shape[1], p, p_first, total, key, offset, floor, ids.data_ptr(), pts.data_ptr(),
+                      big_w.data_ptr(), _lib.ptr(ws), _lib.stream_ptr())
+        else:
+            cur = torch.cuda.current_stream()
+            _lib.call("nvc_query_front", cache.model, ctx.pos.data_ptr(), p, _lib.ptr(ws), _lib.stream_ptr())
+            front = torch.cuda.Event()
+            front.record(cur)
+            select_stream.wait_event(front)
+            _lib.call("nvc_nls_select", cache.model, ctx.dscene.struct, lum.data_ptr(), lum64, mask, lum.shape[1], p,
+                      p_first, total, key, offset, floor, ids.data_ptr(), pts.data_ptr(), big_w.data_ptr(),
+                      _lib.ptr(ws), select_stream.cuda_stream)
+            done = torch.cuda.Event()
+            done.record(select_stream)
+            cache.select_done = done
     else:
         vis = cache.infer(ctx.positions)
         vis = vis if isinstance(vis, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(vis, np.float32))

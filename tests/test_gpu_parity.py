@@ -279,6 +279,21 @@ class TestSampling:
         _lib.call("nvc_profile_stage_ms", ctypes.addressof(ms))
         assert all(0.0 < x < 1000.0 for x in ms)
 
+    def test_select_on_side_stream_matches_inline(self, boxes32):
+        """nvc_query_front + nvc_nls_select on another stream == nvc_nls_sample."""
+        from paper_2506_05930_b200.render import gbuffer_device
+        from paper_2506_05930_b200.sampling import nls_sample_device
+        pos, nrm, alb, _, _ = gbuffer_device(boxes32, boxes32.camera.resized(96, 54))
+        ctx = PixelCtx(boxes32, pos, nrm, alb)
+        c = VisibilityCache(MODE_LIGHTS, 32, grid_cfg(boxes32, 16, 1 << 19), hidden_dims=(64, 64, 64))
+        key = R.stream_key(0, 4, "light-select")
+        want = [t.clone() for t in nls_sample_device(ctx, c, key)]
+        side = torch.cuda.Stream()
+        got = nls_sample_device(ctx, c, key, select_stream=side)
+        torch.cuda.current_stream().wait_event(c.select_done)
+        for a, b in zip(want, got):
+            assert torch.equal(a, b)
+
     def test_tile_sharded_nls_matches_whole_frame(self, boxes32, g_samp):
         from paper_2506_05930_b200.sampling import nls_sample_device
         c = VisibilityCache(MODE_LIGHTS, 32, grid_cfg(boxes32, 16, 1 << 19), hidden_dims=(64, 64, 64))
