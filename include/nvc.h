@@ -146,6 +146,25 @@ int nvc_train_grads(const nvc_model *m, const double *pos, const float *targets,
                     const float *mask, int64_t b_max, const int64_t *b_dev,
                     int32_t shard, int32_t n_shards,
                     void *workspace, double *loss_sum_out, void *stream);
+/* ---- data-parallel gradient exchange ------------------
+ * Every rank builds the same global batch, so the table entries it touches
+ * are the same on every rank.  nvc_exchange_index lists them (sorted, from the
+ * positions of all b global rows); nvc_exchange_pack copies their fixed-point
+ * gradients (zero-padded to max_entries) and the MLP gradients into one int64
+ * buffer of nvc_exchange_buffer_len elements; the caller allreduces (sum) that
+ * buffer instead of the whole grad_fx; nvc_exchange_unpack writes it back.
+ * Entries nobody touched are zero on every rank, so this equals the dense
+ * allreduce bit for bit. */
+int64_t nvc_exchange_max_entries(const nvc_model *m, int64_t b);
+int64_t nvc_exchange_workspace_bytes(const nvc_model *m);
+int64_t nvc_exchange_buffer_len(const nvc_model *m, int64_t max_entries);
+int nvc_exchange_index(const nvc_model *m, const double *pos, int64_t b_max, const int64_t *b_dev,
+                       void *workspace, int32_t *idx, int64_t *count, void *stream);
+int nvc_exchange_pack(const nvc_model *m, const int32_t *idx, const int64_t *count, int64_t max_entries,
+                      int64_t *buf, void *stream);
+int nvc_exchange_unpack(const nvc_model *m, const int32_t *idx, const int64_t *count, int64_t max_entries,
+                        const int64_t *buf, void *stream);
+
 /* One bias-corrected Adam step over every parameter (mlp.py:203-218, dense
  * like the reference), consuming and zeroing grad_fx; refreshes table_h and
  * wpack.  t is the post-increment Adam step (>= 1), lr from lr_at (mlp.py:76).

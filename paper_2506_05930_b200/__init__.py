@@ -10,7 +10,7 @@ package is the host layer that keeps the reference's API.
 
 from . import rng
 from .cache import (MODE_CLUSTERS, MODE_LIGHTS, MODE_RADIANCE, PRECISION_FP16, PRECISION_FP32,
-                    VisibilityCache, make_cache)
+                    GradExchange, VisibilityCache, make_cache)
 from .hashgrid import HashGridConfig, clustered_config
 from .mlp import MLPConfig, MLPParams, TrainStepConfig, lr_at
 from .render import GBuffer, gbuffer_and_ctx, make_gbuffer

@@ -73,6 +73,12 @@ _SIGS = {
     "nvc_train_grads": (c_i32, [P(NvcModel), c_vp, c_vp, c_vp, c_i64, c_vp, c_i32, c_i32,
                                 c_vp, c_vp, c_vp]),
     "nvc_adam_step": (c_i32, [P(NvcModel), c_i64, c_f64, c_vp]),
+    "nvc_exchange_max_entries": (c_i64, [P(NvcModel), c_i64]),
+    "nvc_exchange_workspace_bytes": (c_i64, [P(NvcModel)]),
+    "nvc_exchange_buffer_len": (c_i64, [P(NvcModel), c_i64]),
+    "nvc_exchange_index": (c_i32, [P(NvcModel), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "nvc_exchange_pack": (c_i32, [P(NvcModel), c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "nvc_exchange_unpack": (c_i32, [P(NvcModel), c_vp, c_vp, c_i64, c_vp, c_vp]),
     "nvc_wrs_select": (c_i32, [c_vp, c_i64, c_i32, c_u64, c_u64, c_vp, c_vp, c_vp, c_vp]),
     "nvc_nls_from_vis": (c_i32, [P(NvcScene), c_vp, c_vp, c_i32, c_i64, c_i64, c_i32, c_i64, c_i64,
                                  c_u64, c_u64, c_f64, c_vp, c_vp, c_vp, c_vp]),

@@ -35,6 +35,47 @@ PRECISION_FP32 = 0     # f32 table + f32 SIMT MLP (parity path)
 PRECISION_FP16 = 1     # fp16 shadow table + tcgen05/TMEM MLP (perf path)
 
 
+class GradExchange:
+    """Compact data-parallel gradient exchange (nvc.h, nvc_exchange_*).
+
+    All ranks hold the same global batch, so the hash-table entries it touches
+    are the same everywhere: ``index`` lists them, ``pack`` gathers their
+    fixed-point gradients (+ the MLP gradients) into ``buf``, the caller
+    allreduces ``buf`` (about 1/8 of the dense accumulator at C2), ``unpack``
+    writes the sums back.  Equal to the dense allreduce bit for bit."""
+
+    def __init__(self, cache, b_max: int):
+        import torch
+        lib = _lib.load()
+        self.cache = cache
+        self.b_max = int(b_max)
+        self.max_entries = int(lib.nvc_exchange_max_entries(cache.model, self.b_max))
+        dev = cache.device
+        self.ws = torch.empty(int(lib.nvc_exchange_workspace_bytes(cache.model)), dtype=torch.uint8, device=dev)
+        self.idx = torch.empty(max(self.max_entries, 1), dtype=torch.int32, device=dev)
+        self.count = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.buf = torch.zeros(int(lib.nvc_exchange_buffer_len(cache.model, self.max_entries)), dtype=torch.int64,
+                               device=dev)
+
+    def index(self, pos, b_dev=None) -> None:
+        _lib.call("nvc_exchange_index", self.cache.model, pos.data_ptr(), self.b_max, _lib.ptr(b_dev),
+                  self.ws.data_ptr(), self.idx.data_ptr(), self.count.data_ptr(), _lib.stream_ptr())
+
+    def pack(self) -> None:
+        _lib.call("nvc_exchange_pack", self.cache.model, self.idx.data_ptr(), self.count.data_ptr(),
+                  self.max_entries, self.buf.data_ptr(), _lib.stream_ptr())
+
+    def unpack(self) -> None:
+        _lib.call("nvc_exchange_unpack", self.cache.model, self.idx.data_ptr(), self.count.data_ptr(),
+                  self.max_entries, self.buf.data_ptr(), _lib.stream_ptr())
+
+    def allreduce(self, comm, loss) -> None:
+        """pack -> comm(buf, loss) (sum allreduce) -> unpack."""
+        self.pack()
+        comm(self.buf, loss)
+        self.unpack()
+
+
 class VisibilityCache:
     """Online-trained cache: position -> one sigmoid output per light/cluster."""
 
@@ -113,6 +154,7 @@ class VisibilityCache:
         self._ws = None
         self._qws = None
         self.select_done = None   # CUDA event: last off-stream NLS selection finished
+        self._exchange = None
         # "pipeline": decoupled encode -> tcgen05 MLP -> selection (default);
         # "fused": the single fused kernel
 
@@ -262,13 +304,24 @@ class VisibilityCache:
         _lib.call("nvc_adam_step", self.model, self.adam_t, lr, _lib.stream_ptr())
         self.step += 1
 
+    def exchange(self, b_max: int) -> GradExchange:
+        """The (cached) compact gradient exchange for batches of up to b_max rows."""
+        if self._exchange is None or self._exchange.b_max < b_max:
+            self._exchange = GradExchange(self, b_max)
+        return self._exchange
+
     def train_step_device(self, pos, targets, mask=None, b_dev=None, b_max=None, comm=None):
         """One fused step on device tensors; returns the loss as a 0-d CUDA tensor
         (sum of per-row losses / b) without synchronising.  ``comm`` is an
-        optional callable(grad_fx, loss) run at the allreduce point."""
+        optional callable(buffer, loss) that sum-allreduces both in place; it
+        receives the compact gradient exchange buffer (GradExchange)."""
+        b = int(pos.shape[0] if b_max is None else b_max)
+        if comm is not None:
+            ex = self.exchange(b)
+            ex.index(pos, b_dev)
         loss = self.accumulate_grads(pos, targets, mask, b_max=b_max, b_dev=b_dev)
         if comm is not None:
-            comm(self.grad_fx, loss)
+            ex.allreduce(comm, loss)
         self.apply_adam()
         b = b_dev.to(torch_f64()) if b_dev is not None else float(pos.shape[0])
         return loss[0] / b

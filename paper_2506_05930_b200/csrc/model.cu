@@ -604,6 +604,150 @@ __global__ void __launch_bounds__(128) k_tr_scatter(GridDev g, const double* __r
     }
 }
 
+// ---------------------------------------------------------------------------
+// Compact data-parallel gradient exchange.  Every rank builds the same global
+// batch, so the set of table entries the batch touches is identical on all
+// ranks: mark them in a bitmap (one bit per L*T entry), compact to a sorted
+// entry list, and allreduce only those entries' fixed-point gradients (plus
+// the MLP part) instead of the whole 8 B x param_count accumulator.  Untouched
+// entries hold zero on every rank, so the result equals the dense allreduce.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_touch_mark(GridDev g, const double* __restrict__ pos, int64_t b_max,
+                                                    const int64_t* __restrict__ b_dev, uint32_t* __restrict__ bits) {
+    const int64_t b = b_dev ? *b_dev : b_max;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t r = t / g.L;
+    const int l = (int)(t - r * g.L);
+    if (r >= b) return;
+    const double pp[3] = {__ldg(pos + 3 * r), __ldg(pos + 3 * r + 1), __ldg(pos + 3 * r + 2)};
+    double q[3];
+    normalize(g, pp, q);
+    int c0[3];
+    double f[3];
+    cell(g.res[l], q, c0, f);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const int64_t e = (int64_t)l * g.T + corner_index(g, l, c0, (c >> 2) & 1, (c >> 1) & 1, c & 1);
+        atomicOr(bits + (e >> 5), 1u << (e & 31));
+    }
+}
+
+// per 1024-word chunk: number of set bits
+__global__ void __launch_bounds__(256) k_touch_count(const uint32_t* __restrict__ bits, int64_t n_words,
+                                                     int* __restrict__ chunk_count) {
+    __shared__ int warp_tot[8];
+    const int64_t w0 = (int64_t)blockIdx.x * 1024;
+    int c = 0;
+    for (int i = threadIdx.x; i < 1024; i += 256)
+        if (w0 + i < n_words) c += __popc(bits[w0 + i]);
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) warp_tot[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < 8; ++w) t += warp_tot[w];
+        chunk_count[blockIdx.x] = t;
+    }
+}
+
+// exclusive scan of the chunk counts (one block, sequential chunks of 1024)
+__global__ void __launch_bounds__(1024) k_touch_scan(int* __restrict__ chunk_count, int n_chunks,
+                                                     int64_t* __restrict__ total) {
+    __shared__ int warp_sum[32];
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int base = 0; base < n_chunks; base += 1024) {
+        const int i = base + threadIdx.x;
+        const int v = i < n_chunks ? chunk_count[i] : 0;
+        int incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) warp_sum[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            const int x = warp_sum[lane];
+            int xi = x;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, xi, o);
+                if (lane >= o) xi += y;
+            }
+            warp_sum[lane] = xi - x;
+        }
+        __syncthreads();
+        const int excl = carry + warp_sum[wid] + incl - v;
+        if (i < n_chunks) chunk_count[i] = excl;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = excl + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+
+// write the sorted entry list: chunk offset + prefix of popcounts inside the chunk
+__global__ void __launch_bounds__(1024) k_touch_emit(const uint32_t* __restrict__ bits, int64_t n_words,
+                                                     const int* __restrict__ chunk_off, int32_t* __restrict__ idx) {
+    __shared__ int warp_sum[32];
+    const int64_t wi = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+    const uint32_t word = wi < n_words ? bits[wi] : 0u;
+    const int v = __popc(word);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_sum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const int x = warp_sum[lane];
+        int xi = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += y;
+        }
+        warp_sum[lane] = xi - x;
+    }
+    __syncthreads();
+    int o = chunk_off[blockIdx.x] + warp_sum[wid] + incl - v;
+    uint32_t w = word;
+    while (w) {
+        const int bit = __ffs(w) - 1;
+        w &= w - 1;
+        idx[o++] = (int32_t)(wi * 32 + bit);
+    }
+}
+
+// buf = [grad of listed entries (F each, zero past the count) | MLP gradients]
+__global__ void k_grad_pack(const int64_t* __restrict__ fx, const int32_t* __restrict__ idx,
+                            const int64_t* __restrict__ count, int64_t max_entries, int F, int64_t grid_count,
+                            int64_t mlp_count, int64_t* __restrict__ buf) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t ng = max_entries * F;
+    if (t < ng) {
+        const int64_t i = t / F;
+        buf[t] = i < *count ? fx[(int64_t)idx[i] * F + (t - i * F)] : 0;
+    } else if (t < ng + mlp_count) {
+        buf[t] = fx[grid_count + (t - ng)];
+    }
+}
+
+__global__ void k_grad_unpack(int64_t* __restrict__ fx, const int32_t* __restrict__ idx,
+                              const int64_t* __restrict__ count, int64_t max_entries, int F, int64_t grid_count,
+                              int64_t mlp_count, const int64_t* __restrict__ buf) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t ng = max_entries * F;
+    if (t < ng) {
+        const int64_t i = t / F;
+        if (i < *count) fx[(int64_t)idx[i] * F + (t - i * F)] = buf[t];
+    } else if (t < ng + mlp_count) {
+        fx[grid_count + (t - ng)] = buf[t];
+    }
+}
+
 // fixed-order reduction of the per-block MLP partials and loss partials:
 // block = 32 parameters x 8 warps; warp w sums partial blocks w, w+8, ...
 // in order, then the 8 warp sums are combined in warp order (deterministic).
@@ -942,6 +1086,72 @@ int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, con
     k_reduce_parts<<<grid1(net.mlp_count, 32), 256, 0, s>>>(part_w, part_loss, nblk, net.mlp_count,
                                                              net.grid_count, m->grad_fx, loss_out);
     return check_launch("k_reduce_parts");
+}
+
+// ---- compact data-parallel gradient exchange ----
+static int64_t touch_words(const nvc_model* m) { return ((int64_t)m->levels * m->table_size + 31) / 32; }
+
+int64_t nvc_exchange_max_entries(const nvc_model* m, int64_t b) {
+    if (!m) return 0;
+    const int64_t e = (int64_t)m->levels * m->table_size;
+    const int64_t bound = b * m->levels * 8;
+    return bound < e ? bound : e;
+}
+
+int64_t nvc_exchange_workspace_bytes(const nvc_model* m) {
+    if (!m) return 0;
+    const int64_t words = touch_words(m);
+    return (words * 4 + 255) / 256 * 256 + ((words + 1023) / 1024 * 4 + 255) / 256 * 256;
+}
+
+int64_t nvc_exchange_buffer_len(const nvc_model* m, int64_t max_entries) {
+    if (!m) return 0;
+    Net net = net_of(m);
+    return max_entries * m->features + net.mlp_count;
+}
+
+int nvc_exchange_index(const nvc_model* m, const double* pos, int64_t b_max, const int64_t* b_dev, void* ws,
+                       int32_t* idx, int64_t* count, void* stream) {
+    int rc = validate(m);
+    if (rc) return rc;
+    NVC_REQUIRE(pos && ws && idx && count, "nvc_exchange_index: null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    GridDev g = grid_of(m);
+    const int64_t words = touch_words(m);
+    const int n_chunks = (int)((words + 1023) / 1024);
+    uint32_t* bits = (uint32_t*)ws;
+    int* chunk = (int*)((char*)ws + (words * 4 + 255) / 256 * 256);
+    cudaMemsetAsync(bits, 0, words * 4, s);
+    if (b_max > 0)
+        k_touch_mark<<<grid1(b_max * g.L, 128), 128, 0, s>>>(g, pos, b_max, b_dev, bits);
+    k_touch_count<<<n_chunks, 256, 0, s>>>(bits, words, chunk);
+    k_touch_scan<<<1, 1024, 0, s>>>(chunk, n_chunks, count);
+    k_touch_emit<<<n_chunks, 1024, 0, s>>>(bits, words, chunk, idx);
+    return check_launch("nvc_exchange_index");
+}
+
+int nvc_exchange_pack(const nvc_model* m, const int32_t* idx, const int64_t* count, int64_t max_entries,
+                      int64_t* buf, void* stream) {
+    int rc = validate(m);
+    if (rc) return rc;
+    NVC_REQUIRE(idx && count && buf && m->grad_fx, "nvc_exchange_pack: null argument");
+    Net net = net_of(m);
+    const int64_t n = max_entries * m->features + net.mlp_count;
+    k_grad_pack<<<grid1(n, 256), 256, 0, (cudaStream_t)stream>>>(m->grad_fx, idx, count, max_entries, m->features,
+                                                                 net.grid_count, net.mlp_count, buf);
+    return check_launch("k_grad_pack");
+}
+
+int nvc_exchange_unpack(const nvc_model* m, const int32_t* idx, const int64_t* count, int64_t max_entries,
+                        const int64_t* buf, void* stream) {
+    int rc = validate(m);
+    if (rc) return rc;
+    NVC_REQUIRE(idx && count && buf && m->grad_fx, "nvc_exchange_unpack: null argument");
+    Net net = net_of(m);
+    const int64_t n = max_entries * m->features + net.mlp_count;
+    k_grad_unpack<<<grid1(n, 256), 256, 0, (cudaStream_t)stream>>>(m->grad_fx, idx, count, max_entries, m->features,
+                                                                   net.grid_count, net.mlp_count, buf);
+    return check_launch("k_grad_unpack");
 }
 
 int nvc_adam_step(const nvc_model* m, int64_t t, double lr, void* stream) {

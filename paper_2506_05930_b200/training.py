@@ -199,8 +199,9 @@ def train_frame_device(scene, camera, cache, cfg: TrainFrameConfig, frame: int =
     """Asynchronous frame training: returns the last step's loss as a CUDA tensor.
 
     With ``n_shards > 1`` every rank builds the same global batch, computes the
-    targets/gradients of its row shard and ``comm(grad_fx, loss)`` (an
-    allreduce) runs before the identical Adam update.  With ``pipeline`` the
+    targets/gradients of its row shard and ``comm(buffer, loss)`` (a sum
+    allreduce of the compact GradExchange buffer and the loss) runs before the
+    identical Adam update.  With ``pipeline`` the
     batch comes from (and the next one is started on) a BatchPipeline."""
     _check_cache(cache, cfg)
     if pipeline is not None:
@@ -208,14 +209,18 @@ def train_frame_device(scene, camera, cache, cfg: TrainFrameConfig, frame: int =
     elif bufs is None:
         bufs = BatchBuffers(cfg.n_world, cfg.n_screen, cache.output_dim, cache.device, n_shards)
     loss = None
+    b_max = bufs.n_world + bufs.n_screen
     for step in range(cfg.steps):
         if pipeline is None:
             gen_batch_device(scene, camera, bufs, cfg.seed, frame, step, shard, n_shards)
+        if comm is not None:   # entries touched by the GLOBAL batch: identical on every rank
+            ex = cache.exchange(b_max)
+            ex.index(bufs.pos, bufs.n_rows)
         bufs.loss.zero_()
-        cache.accumulate_grads(bufs.pos, bufs.tgt, b_max=bufs.n_world + bufs.n_screen, b_dev=bufs.n_rows,
+        cache.accumulate_grads(bufs.pos, bufs.tgt, b_max=b_max, b_dev=bufs.n_rows,
                                shard=shard, n_shards=n_shards, loss_out=bufs.loss)
         if comm is not None:
-            comm(cache.grad_fx, bufs.loss)
+            ex.allreduce(comm, bufs.loss)
         cache.apply_adam()
         loss = bufs.loss[0] / bufs.n_rows[0].to(bufs.loss.dtype)
     if pipeline is not None:

@@ -60,17 +60,37 @@ def _grad_fx_rows(cache, pos, tgt, lo, hi, b):
     return gfx, loss_sum
 
 
-def _worker(rank, world, port, q):
+def touched_entries(cache, pos):
+    """Sorted table entries the whole (global) batch touches -- identical on every rank
+    (restates nvc_exchange_index: 8 corners per (row, level), level-major entry ids)."""
+    _, ctx = O.encode(cache.grid, cache.table, pos)
+    ent = [level * cache.grid.T + idx.reshape(-1) for level, (idx, _) in enumerate(ctx)]
+    return np.unique(np.concatenate(ent))
+
+
+def _worker(rank, world, port, q, compact):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     cache, pos, tgt = _setup()
     b = pos.shape[0]
     lo, hi = shard_rows(b, rank, world)
     gfx, ls = _grad_fx_rows(cache, pos, tgt, lo, hi, b)
-    grad = torch.from_numpy(gfx)
     loss = torch.tensor([ls], dtype=torch.float64)
-    dist.all_reduce(grad)         # the bench's comm(): sum of int64 fixed point
-    dist.all_reduce(loss)
+    if compact:   # GradExchange: allreduce only the entries the global batch touched
+        ent = touched_entries(cache, pos)
+        f = cache.grid.F
+        cols = (ent[:, None] * f + np.arange(f)).reshape(-1)
+        buf = torch.from_numpy(gfx[cols].copy())
+        dist.all_reduce(buf)
+        dist.all_reduce(loss)
+        assert not np.delete(gfx, cols).any()        # untouched entries are zero on every rank
+        gfx = np.zeros_like(gfx)
+        gfx[cols] = buf.numpy()
+        grad = torch.from_numpy(gfx)
+    else:
+        grad = torch.from_numpy(gfx)
+        dist.all_reduce(grad)         # dense: sum of int64 fixed point
+        dist.all_reduce(loss)
     g32 = (grad.numpy().astype(np.float64) / FX).astype(np.float32)
     p = cache.flat()
     st = O.Adam(p.size)
@@ -81,12 +101,12 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_dp_allreduce_matches_full_batch(world):
+@pytest.mark.parametrize("world,compact", [(2, False), (2, True)])
+def test_dp_allreduce_matches_full_batch(world, compact):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, compact)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = sorted(q.get(timeout=120) for _ in range(world))

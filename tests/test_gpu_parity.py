@@ -396,6 +396,30 @@ class TestTraining:
         assert la == lb
         np.testing.assert_array_equal(pa, pb)
 
+    def test_compact_exchange_equals_dense_allreduce(self, pbox8, g_train):
+        """GradExchange: pack -> sum over shards -> unpack == full-batch grad_fx, bit for bit."""
+        pos = torch.from_numpy(g_train["c1_pos"]).to(DEV)
+        tgt = torch.from_numpy(g_train["c1_tgt"].astype(np.float32)).to(DEV)
+        b = pos.shape[0]
+        full = self._c1(pbox8)
+        full.accumulate_grads(pos, tgt)
+        shards = [self._c1(pbox8) for _ in range(3)]
+        for sh, c in enumerate(shards):
+            lo, hi = b * sh // 3, b * (sh + 1) // 3
+            c.accumulate_grads(pos, tgt[lo:hi].contiguous(), b_max=b, shard=sh, n_shards=3)
+            ex = c.exchange(b)
+            ex.index(pos)
+            ex.pack()
+        total = sum(c.exchange(b).buf for c in shards)
+        assert 0 < int(shards[0].exchange(b).count.item()) <= shards[0].exchange(b).max_entries
+        ex0 = shards[0].exchange(b)
+        ex0.buf.copy_(total)
+        ex0.unpack()
+        gc = full.grid_cfg.param_count
+        np.testing.assert_array_equal(full.grad_fx[:gc].cpu().numpy(), shards[0].grad_fx[:gc].cpu().numpy())
+        np.testing.assert_allclose(full.grad_fx[gc:].double().cpu().numpy(),
+                                   shards[0].grad_fx[gc:].double().cpu().numpy(), rtol=1e-5, atol=2.0 ** 48 * 1e-9)
+
     def test_batch_pipeline_matches_inline_generation(self, pbox8):
         """Batches prefetched one frame ahead on a side stream train bit-identically."""
         from paper_2506_05930_b200.training import BatchPipeline, train_frame_device
