@@ -140,8 +140,9 @@ int64_t nvc_query_workspace_bytes(const nvc_model *m, int64_t p);
  * [b*shard/n_shards, b*(shard+1)/n_shards): pos is indexed by global row,
  * targets/mask (may be NULL) by shard-local row.  d_out is scaled by the
  * global b*K (mlp.py:162) so data-parallel shards sum to the full-batch
- * gradient.  loss_sum_out (device double) receives sum_rows(sum_k d^2)/K
- * over the shard's rows (mean over b is the caller's division). */
+ * gradient.  loss_sum_out (device double[2]) receives [0] = sum_rows(sum_k d^2)/K
+ * over the shard's rows and [1] = that sum / b (summing [1] over shards gives
+ * the reference's batch loss, l2_loss mlp.py:143-149). */
 int nvc_train_grads(const nvc_model *m, const double *pos, const float *targets,
                     const float *mask, int64_t b_max, const int64_t *b_dev,
                     int32_t shard, int32_t n_shards,

@@ -292,7 +292,7 @@ class VisibilityCache:
         import torch
         b_max = int(pos.shape[0] if b_max is None else b_max)
         if loss_out is None:
-            loss_out = torch.zeros(1, dtype=torch.float64, device=self.device)
+            loss_out = torch.zeros(2, dtype=torch.float64, device=self.device)   # [sum, mean]
         ws = self._workspace(b_max)
         _lib.call("nvc_train_grads", self.model, pos.data_ptr(), targets.data_ptr(), _lib.ptr(mask), b_max,
                   _lib.ptr(b_dev), shard, n_shards, ws.data_ptr(), loss_out.data_ptr(), _lib.stream_ptr())
@@ -323,8 +323,7 @@ class VisibilityCache:
         if comm is not None:
             ex.allreduce(comm, loss)
         self.apply_adam()
-        b = b_dev.to(torch_f64()) if b_dev is not None else float(pos.shape[0])
-        return loss[0] / b
+        return loss[1]
 
     def train_step(self, positions, targets, mask=None) -> float:
         """One fused encode/forward/backward/Adam update. Returns batch loss."""
@@ -382,11 +381,6 @@ class VisibilityCache:
         bs = [arrays[f"b{i}"] for i in range(len(obj.net_cfg.layer_dims))]
         obj._upload(arrays["grid"], MLPParams(ws, bs))
         return obj
-
-
-def torch_f64():
-    import torch
-    return torch.float64
 
 
 def make_cache(scene, mode: str, seed: int = 0, clusters: int | None = None,

@@ -754,7 +754,8 @@ __global__ void k_grad_unpack(int64_t* __restrict__ fx, const int32_t* __restric
 __global__ void __launch_bounds__(256) k_reduce_parts(const float* __restrict__ part_w,
                                                       const double* __restrict__ part_loss, int nblk,
                                                       int64_t mlp_count, int64_t grid_count,
-                                                      int64_t* __restrict__ grad_fx, double* __restrict__ loss_out) {
+                                                      int64_t* __restrict__ grad_fx, double* __restrict__ loss_out,
+                                                      int64_t b_max, const int64_t* __restrict__ b_dev) {
     __shared__ double s_acc[8][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t j = (int64_t)blockIdx.x * 32 + lane;
@@ -772,7 +773,11 @@ __global__ void __launch_bounds__(256) k_reduce_parts(const float* __restrict__ 
         double t = 0.0;
         for (int b = lane; b < nblk; b += 32) t += part_loss[b];
         for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-        if (lane == 0) *loss_out = t;
+        if (lane == 0) {
+            const int64_t b = b_dev ? *b_dev : b_max;
+            loss_out[0] = t;                                  // sum over the shard's rows
+            loss_out[1] = b > 0 ? t / (double)b : 0.0;         // its share of the global-batch mean
+        }
     }
 }
 
@@ -1084,7 +1089,7 @@ int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, con
     rc = check_launch("nvc_train_grads");
     if (rc) return rc;
     k_reduce_parts<<<grid1(net.mlp_count, 32), 256, 0, s>>>(part_w, part_loss, nblk, net.mlp_count,
-                                                             net.grid_count, m->grad_fx, loss_out);
+                                                             net.grid_count, m->grad_fx, loss_out, b_max, b_dev);
     return check_launch("k_reduce_parts");
 }
 

@@ -63,7 +63,7 @@ class BatchBuffers:
         self.n_rows = torch.zeros(1, dtype=torch.int64, device=device)
         ws = _lib.load().nvc_batch_workspace_bytes(n_world, n_screen)
         self.ws = torch.zeros(ws, dtype=torch.uint8, device=device)
-        self.loss = torch.zeros(1, dtype=torch.float64, device=device)
+        self.loss = torch.zeros(2, dtype=torch.float64, device=device)   # [sum, mean] (nvc_train_grads)
 
 
 def gen_batch_device(scene, camera, bufs: BatchBuffers, seed: int, frame: int, step: int = 0,
@@ -216,13 +216,12 @@ def train_frame_device(scene, camera, cache, cfg: TrainFrameConfig, frame: int =
         if comm is not None:   # entries touched by the GLOBAL batch: identical on every rank
             ex = cache.exchange(b_max)
             ex.index(bufs.pos, bufs.n_rows)
-        bufs.loss.zero_()
         cache.accumulate_grads(bufs.pos, bufs.tgt, b_max=b_max, b_dev=bufs.n_rows,
                                shard=shard, n_shards=n_shards, loss_out=bufs.loss)
         if comm is not None:
             ex.allreduce(comm, bufs.loss)
         cache.apply_adam()
-        loss = bufs.loss[0] / bufs.n_rows[0].to(bufs.loss.dtype)
+        loss = bufs.loss[1]
     if pipeline is not None:
         pipeline.release(bufs, frame)
     return loss, bufs
@@ -241,10 +240,9 @@ def train_frame(scene, camera, cache, cfg: TrainFrameConfig, frame: int = 0, clu
         b = int(bufs.n_rows.item())
         if b == 0:            # training.py:196-197: empty batch -> no update
             continue
-        bufs.loss.zero_()
         cache.accumulate_grads(bufs.pos, bufs.tgt, b_max=b, shard=0, n_shards=1, loss_out=bufs.loss)
         cache.apply_adam()
-        loss = float(bufs.loss.item()) / b
+        loss = float(bufs.loss[1].item())
     return loss
 
 
