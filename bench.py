@@ -354,7 +354,7 @@ def gpu_arm(args) -> None:
         flop_px = 2 * sum(a * b for a, b in zip((32, 64, 64, 64), (64, 64, 64, 32)))
         kern = {
             "k_enc_tiles2": ("hbm", P * (24 + 64), k_ms[0]),             # pos in, fp16 feature tile out
-            "k_mlp_wg": ("tensor", P * flop_px, k_ms[1]),                # 24,576 flop per pixel
+            "k_mlp_ts": ("tensor", P * flop_px, k_ms[1]),                # 24,576 flop per pixel
             "k_nls32": ("hbm", P * (64 + 4 * K + 4 + 40), k_ms[2]),      # vis + lum + mask in, id/W/point out
         }
         name = max(kern, key=lambda k: kern[k][2])
@@ -383,7 +383,7 @@ def gpu_arm(args) -> None:
                        "parallelism": f"dp{world} (train) + {world} screen tiles (query)",
                        "l2": "inputs > L2 every frame (lum table 265 MB + 16.8 M-parameter Adam stream 530 MB)",
                        "stage_ms": {"train_frame": tr_ms, "query": q_ms, "k_enc_tiles2": k_ms[0],
-                                    "k_mlp_wg": k_ms[1], "k_nls32": k_ms[2]}},
+                                    "k_mlp_ts": k_ms[1], "k_nls32": k_ms[2]}},
             "e2e": {"value": P * world / (e2e_ms * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": int(pos_host.numel() * 8),
                     "d2h_bytes_per_step": int(sum(h.numel() * h.element_size() for h in outs_host) + 8)},

@@ -781,6 +781,216 @@ __global__ void __launch_bounds__(kWgThreads, 1) k_mlp_wg(MNet net, const float*
 }
 
 // ---------------------------------------------------------------------------
+// stage 2 (default for widths <= 64): activations stay in tensor memory
+//
+// The SS-mode kernel above re-reads every hidden activation tile from shared
+// memory for each MMA and writes it there in each epilogue; with K = 64 layers
+// that smem traffic (A 4 KB + B 2 KB per 128x64x16 MMA, plus the epilogue
+// stores) saturates the shared-memory pipe.  Here each warpgroup keeps its
+// tile's activations in TMEM: the epilogue drains the fp32 accumulator
+// (tcgen05.ld), applies leaky-ReLU in packed half2 and writes the fp16 result
+// back with tcgen05.st into a 32-column A region, and the next layer's MMA
+// reads A from TMEM (kind::f16 "TS" form); only the weights come from smem.
+// Biases are folded into the accumulation by one extra K=16 step per layer
+// (A = a constant tile whose column 0 is 1.0, B = the layer's bias column), so
+// the epilogue does pack + leaky only.  Four warpgroups (one tile in flight
+// each: 64 accumulator + 32 activation columns) and one MMA warp per group.
+// ---------------------------------------------------------------------------
+constexpr int kTsWG = 4;
+constexpr int kTsThreads = 160 * kTsWG;
+constexpr int kTsCols = 96;   // per warpgroup: 64 accumulator + 32 fp16-pair activation columns
+
+struct TSBars {
+    uint64_t a0_full[2], acc_full;
+};
+
+__device__ __forceinline__ void mma_ts_elect(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void tst16(uint32_t taddr, const uint32_t r[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+__device__ __forceinline__ void tst_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+template <int HID, int OUT, int KP0>
+__global__ void __launch_bounds__(kTsThreads, 1) k_mlp_ts(MNet net, const float* __restrict__ params,
+                                                         const uint16_t* __restrict__ wpack,
+                                                         const uint8_t* __restrict__ tiles, int64_t ntiles, int64_t P,
+                                                         __half* __restrict__ vis16, int64_t vstride) {
+    static_assert(HID == 64 && OUT <= 64 && KP0 <= 64, "TMEM layout sized for 64-wide hidden layers");
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    __shared__ TSBars bars[kTsWG];
+    __shared__ uint32_t tbase;
+    uint8_t* smem = smem_raw + ((1024u - (s32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* s_w = smem + net.sm_w;
+    uint8_t* s_a0 = smem + net.sm_a0;
+    uint8_t* s_ones = smem + net.sm_a1;                   // [128 x 16] K-major SW32, column 0 = 1
+    uint8_t* s_bias = smem + net.sm_bias;                 // per layer [np x 16] K-major SW32, column 0 = bias
+    const int tid = threadIdx.x, row = tid & 127;
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+    const bool mma_warp = warp >= 4 * kTsWG;
+    const int g = mma_warp ? warp - 4 * kTsWG : warp >> 2, wq = warp & 3;
+    const int L = net.n_layers;
+    constexpr int a0_bytes = kT * KP0 * 2;
+    const int bias_block = 64 * 32;                       // bytes per layer block (np <= 64 rows x 32 B)
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(wpack);
+        uint4* dst = reinterpret_cast<uint4*>(s_w);
+        for (int i = tid; i < net.wpack_halfs / 8; i += kTsThreads) dst[i] = __ldg(src + i);
+        for (int i = tid; i < kT * 16; i += kTsThreads) {   // ones tile
+            const int r = i >> 4, k = i & 15;
+            *reinterpret_cast<__half*>(s_ones + umma_off(r, k, kT, 16)) = __float2half_rn(k == 0 ? 1.0f : 0.0f);
+        }
+        for (int l = 0; l < L; ++l) {
+            const int np = l == L - 1 ? OUT : HID;
+            for (int i = tid; i < np * 16; i += kTsThreads) {
+                const int n = i >> 4, k = i & 15;
+                const float b = (k == 0 && n < net.dims[l + 1]) ? __ldg(params + net.boff[l] + n) : 0.0f;
+                *reinterpret_cast<__half*>(s_bias + l * bias_block + umma_off(n, k, np, 16)) = __float2half_rn(b);
+            }
+        }
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(&tbase)), "r"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int w = 0; w < kTsWG; ++w) {
+            mbar_init(&bars[w].a0_full[0], 1);
+            mbar_init(&bars[w].a0_full[1], 1);
+            mbar_init(&bars[w].acc_full, 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    fence_async();
+    tc_before();
+    __syncthreads();
+    tc_after();
+    const uint32_t tmem = tbase;
+    TSBars& B = bars[g];
+    const int64_t t0 = (int64_t)blockIdx.x * kTsWG + g, tstep = (int64_t)gridDim.x * kTsWG;
+    const int n_wg = ntiles > t0 ? (int)((ntiles - 1 - t0) / tstep + 1) : 0;
+    const uint32_t acc = tmem + (uint32_t)(g * kTsCols);      // columns [0, 64): fp32 accumulator
+    const uint32_t act = acc + 64u;                            // columns [64, 96): fp16-pair activations
+    const int id = 1 + g;
+    if (mma_warp) {
+        // ---------------- MMA warp of warpgroup g ----------------
+        const uint32_t w_addr = s32(s_w), ones = s32(s_ones), bias = s32(s_bias);
+        const uint64_t d_ones = desc_of(ones, kT, 16, 0);
+        auto load_a0 = [&](int k) {
+            if ((tid & 31) == 0) {
+                const int b = k & 1;
+                mbar_expect_tx(&B.a0_full[b], (uint32_t)a0_bytes);
+                bulk_g2s(s_a0 + (2 * g + b) * a0_bytes, tiles + (t0 + (int64_t)k * tstep) * a0_bytes,
+                         (uint32_t)a0_bytes, &B.a0_full[b]);
+            }
+            __syncwarp();
+        };
+        uint32_t a0_ph[2] = {0, 0};
+        if (n_wg > 0) load_a0(0);
+        for (int k = 0; k < n_wg; ++k) {
+            if (k + 1 < n_wg) load_a0(k + 1);                     // the other buffer: tile k-1 is done with it
+            const int b = k & 1;
+            mbar_wait(&B.a0_full[b], a0_ph[b]);
+            a0_ph[b] ^= 1u;
+            for (int l = 0; l < L; ++l) {
+                if (k > 0 || l > 0) asm volatile("bar.sync %0, 160;" ::"r"(id) : "memory");   // epilogue done
+                tc_after();
+                const int np = l == L - 1 ? OUT : HID;
+                const uint32_t idesc = (1u << 4) | ((uint32_t)(np >> 3) << 17) | ((uint32_t)(kT >> 4) << 24);
+                const uint64_t db = desc_of(w_addr + 2u * (uint32_t)net.wofs[l], np, l == 0 ? KP0 : HID, 0);
+                if (l == 0) {
+                    const uint64_t da = desc_of(s32(s_a0 + (2 * g + b) * a0_bytes), kT, KP0, 0);
+#pragma unroll
+                    for (int kk = 0; kk < KP0 / 16; ++kk) mma_elect(acc, da + 2 * kk, db + 2 * kk, idesc, kk > 0);
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < HID / 16; ++kk) mma_ts_elect(acc, act + 8u * kk, db + 2 * kk, idesc, kk > 0);
+                }
+                // bias: + ones[128 x 16] x bias_l[np x 16]^T
+                mma_elect(acc, d_ones, desc_of(bias + l * bias_block, np, 16, 0), idesc, 1u);
+                commit_elect(&B.acc_full);
+            }
+        }
+        if (n_wg > 0) asm volatile("bar.sync %0, 160;" ::"r"(id) : "memory");   // the last tile's final arrive
+    } else {
+        // ---------------- epilogue warpgroup g ----------------
+        const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+        const __half2 al2 = __float2half2_rn(net.alpha);
+        const __half2 lo = __float2half2_rn(1e-6f), hi = __float2half2_rn(0.999999f);
+        uint32_t ph = 0;
+        for (int k = 0; k < n_wg; ++k) {
+            for (int l = 0; l < L; ++l) {
+                mbar_wait(&B.acc_full, ph);
+                ph ^= 1u;
+                tc_after();
+                if (l < L - 1) {
+                    uint32_t r[HID];
+#pragma unroll
+                    for (int c = 0; c < HID; c += 16) tld16_nowait(acc + lane_base + (uint32_t)c, r + c);
+                    tld_wait();
+                    uint32_t h[HID / 2];
+#pragma unroll
+                    for (int j = 0; j < HID / 2; ++j) {
+                        const __half2 z = __floats2half2_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+                        const __half2 y = __hmax2(z, __hmul2(z, al2));
+                        h[j] = *reinterpret_cast<const uint32_t*>(&y);
+                    }
+#pragma unroll
+                    for (int c = 0; c < HID / 2; c += 16) tst16(act + lane_base + (uint32_t)c, h + c);
+                    tst_wait();
+                    tc_before();
+                    asm volatile("bar.arrive %0, 160;" ::"r"(id) : "memory");
+                } else {
+                    uint32_t r[OUT];
+#pragma unroll
+                    for (int c = 0; c < OUT; c += 16) tld16_nowait(acc + lane_base + (uint32_t)c, r + c);
+                    tld_wait();
+                    tc_before();
+                    asm volatile("bar.arrive %0, 160;" ::"r"(id) : "memory");   // accumulator drained
+                    const int64_t p = (t0 + (int64_t)k * tstep) * kT + row;
+                    if (p < P) {
+                        __half* vrow = vis16 + p * vstride;
+#pragma unroll
+                        for (int c = 0; c < OUT / 8; ++c) {
+                            __align__(16) __half2 hh[4];
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                float o[2];
+#pragma unroll
+                                for (int t = 0; t < 2; ++t) {
+                                    const float z = __uint_as_float(r[8 * c + 2 * e + t]);
+                                    o[t] = net.out_sigmoid ? fmaf(0.5f, tanh_fast(0.5f * z), 0.5f)
+                                                           : (z >= 0.0f ? z : net.alpha * z);
+                                }
+                                hh[e] = __floats2half2_rn(o[0], o[1]);
+                                if (net.out_sigmoid) hh[e] = __hmin2(__hmax2(hh[e], lo), hi);   // mlp.py:135-136
+                            }
+                            if (8 * c < vstride) *reinterpret_cast<uint4*>(vrow + 8 * c) = *reinterpret_cast<const uint4*>(hh);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    tc_before();
+    __syncthreads();
+    tc_after();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+}
+
+// ---------------------------------------------------------------------------
 // stage 3: WRS / Neural DI from fp16 visibilities
 // ---------------------------------------------------------------------------
 __device__ __noinline__ U4 philox_fn(uint64_t counter, uint64_t key) { return philox_block(counter, key); }
@@ -1102,6 +1312,38 @@ int launch_wg(const MNet& w, const nvc_model* m, const uint8_t* tiles, int64_t n
     return check_launch("k_mlp_wg");
 }
 
+// smem layout of k_mlp_ts: weights | 2 A0 tiles per warpgroup | ones tile | bias blocks
+bool ts_layout(MNet& q) {
+    if (q.n_layers < 2 || q.n_layers > 8) return false;
+    q.sm_w = 0;
+    q.sm_a0 = (q.wpack_halfs * 2 + 1023) / 1024 * 1024;
+    q.sm_a1 = q.sm_a0 + 2 * kTsWG * ((kT * q.kp[0] * 2 + 1023) / 1024 * 1024);   // ones tile
+    q.sm_bias = q.sm_a1 + kT * 16 * 2;
+    q.sm_total = q.sm_bias + q.n_layers * 64 * 32 + 1024;
+    return q.sm_total <= 227 * 1024;
+}
+
+template <int HID, int OUT, int KP0>
+int launch_ts(const MNet& w, const nvc_model* m, const uint8_t* tiles, int64_t ntiles, int64_t P, __half* vis16,
+              int64_t vstride, int grid, cudaStream_t s) {
+    cudaFuncSetAttribute(k_mlp_ts<HID, OUT, KP0>, cudaFuncAttributeMaxDynamicSharedMemorySize, w.sm_total);
+    k_mlp_ts<HID, OUT, KP0><<<grid, kTsThreads, w.sm_total, s>>>(w, m->params, m->wpack, tiles, ntiles, P, vis16,
+                                                                 vstride);
+    return check_launch("k_mlp_ts");
+}
+
+int launch_mlp_ts(const MNet& w, const nvc_model* m, const uint8_t* tiles, int64_t ntiles, int64_t P, __half* vis16,
+                  int64_t vstride, int grid, cudaStream_t s) {
+    const int o = w.np[w.n_layers - 1], k = w.kp[0];
+#define NVC_TS(O, K) \
+    if (o == O && k == K) return launch_ts<64, O, K>(w, m, tiles, ntiles, P, vis16, vstride, grid, s);
+    NVC_TS(16, 16) NVC_TS(16, 32) NVC_TS(16, 64) NVC_TS(32, 16) NVC_TS(32, 32) NVC_TS(32, 64)
+    NVC_TS(48, 16) NVC_TS(48, 32) NVC_TS(48, 64) NVC_TS(64, 16) NVC_TS(64, 32) NVC_TS(64, 64)
+#undef NVC_TS
+    set_error("k_mlp_ts: shape not instantiated");
+    return NVC_ERR_UNSUPPORTED;
+}
+
 // instantiated shapes (hidden, output, input padded widths); others use k_mlp_tiles
 bool wg_supported(const MNet& w) {
     const int h = w.np[0], o = w.np[w.n_layers - 1], k = w.kp[0];
@@ -1170,7 +1412,12 @@ int run_front(const nvc_model* m, const double* pos, int64_t P, uint8_t* tiles, 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     MNet w = q;
-    if (wg_layout(m, w) && wg_supported(w) && !getenv("NVC_MLP_QUADS")) {
+    MNet t = q;
+    if (wg_layout(m, w) && wg_supported(w) && ts_layout(t) && !getenv("NVC_MLP_WG") && !getenv("NVC_MLP_QUADS")) {
+        int grid = (int)std::min<int64_t>((ntiles + kTsWG - 1) / kTsWG, sms);
+        if (const char* e = getenv("NVC_QUERY_GRID")) grid = max(1, min(grid, atoi(e)));
+        rc = launch_mlp_ts(t, m, tiles, ntiles, P, vis16, vstride, grid, s);
+    } else if (wg_layout(m, w) && wg_supported(w) && !getenv("NVC_MLP_QUADS")) {
         int grid = (int)std::min<int64_t>((ntiles + kWG - 1) / kWG, sms);
         if (const char* e = getenv("NVC_QUERY_GRID")) grid = max(1, min(grid, atoi(e)));
         rc = launch_mlp_wg(w, m, tiles, ntiles, P, vis16, vstride, grid, s);
