@@ -2,12 +2,14 @@
 
 A step = one online frame, in the reference's order (render.py:297-324):
   1. training batch on the GPU: 4096 world + 4096 screen samples, 8192 x 32
-     FP64 shadow-ray labels (training.py:166-199);
+     FP64 shadow-ray labels (training.py:166-199) -- generated one frame ahead
+     on a side stream (it depends only on the frame index);
   2. one train step: encode -> MLP fwd/bwd -> fixed-point hash-grid scatter
-     -> fused dense Adam over all 16.8 M parameters (cache.py:60-73);
-  3. full-screen NLS query on the 1920x1080 G-buffer: fused hash-grid encode
-     -> tcgen05 MLP 32-64-64-64-32 -> clamp * lum -> FP64 WRS with numpy
-     Philox -> light point (sampling.py:184-205).
+     -> dense Adam over all 16.8 M parameters (cache.py:60-73);
+  3. full-screen NLS query on the 1920x1080 G-buffer: hash-grid encode ->
+     tcgen05 MLP 32-64-64-64-32 -> clamp * lum -> FP64 WRS with numpy Philox
+     -> light point (sampling.py:184-205); the selection kernel runs on its
+     own stream so it overlaps the next frame's train step.
 Inputs (G-buffer, per-camera light-major lum table) are built once before
 timing, as the reference memoizes them per camera (render.py:128-142).
 
@@ -43,10 +45,11 @@ sys.path.insert(0, ROOT)
 WIDTH, HEIGHT, K = 1920, 1080, 32
 LEVELS, TABLE, FEATS, HIDDEN = 16, 1 << 19, 2, (64, 64, 64)
 N_WORLD = N_SCREEN = 4096
-# our kernels per online frame: k_world, k_screen_round0, k_screen_finish, k_targets,
-# k_tr_encode, k_train3, k_tr_scatter, k_reduce_parts, k_adam_bulk, k_adam_mlp,
-# k_enc_tiles, k_mlp_tiles, k_nls32
-LAUNCHES_PER_FRAME = 13
+# our kernels per online frame: batch (side stream) k_world, k_screen_round0,
+# k_screen_finish, k_morton_order, k_targets_sorted; train k_tr_encode, k_train3,
+# k_tr_scatter, k_reduce_parts, k_adam_bulk, k_adam_mlp; query k_enc_tiles2,
+# k_mlp_ts, k_nls32g
+LAUNCHES_PER_FRAME = 14
 METRIC = "visibility queries/s (encode+MLP+WRS) at 1080p x 32 lights; train samples/s"
 UNIT = "queries/s"
 
