@@ -28,7 +28,7 @@ extern "C" {
 
 #define NVC_MAX_LEVELS 32
 #define NVC_MAX_LAYERS 8
-#define NVC_ABI_VERSION 3
+#define NVC_ABI_VERSION 4
 
 typedef enum {
     NVC_OK = 0,
@@ -60,7 +60,19 @@ typedef struct {
     /* device state, caller-allocated */
     float *params;                        /* f32 master parameters, param_count */
     float *adam_m, *adam_v;               /* f32 Adam moments, param_count */
-    int64_t *grad_fx;                     /* fixed-point gradient accumulator, param_count */
+    int64_t *grad_fx;                     /* fixed-point gradient accumulator, param_count (dense mode) */
+    /* Compact gradient mode (grad_c != NULL; grad_fx is then unused).
+     * nvc_train_index marks the batch's table entries in touch_bits (L*T bits)
+     * and writes touch_off (per 32-entry word: rank of its first marked entry;
+     * nvc_touch_off_len(m) int32 including scratch).  The scatter and Adam
+     * address entry e's gradient as grad_c[rank(e)*F + f] and the MLP
+     * gradients as grad_c[grad_c_entries*F + j]: a few MB that stay in L2,
+     * and exactly the data-parallel allreduce buffer
+     * (nvc_exchange_buffer_len(m, grad_c_entries) int64). */
+    uint32_t *touch_bits;
+    int32_t *touch_off;
+    int64_t *grad_c;
+    int64_t grad_c_entries;
     uint16_t *table_h;                    /* fp16 query table, x-pair layout: slot e = (f[e], f[next(e)]), 2*L*T*F */
     uint16_t *wpack;                      /* fp16 weights in the tcgen05 K-major core-matrix layout */
     int64_t param_count;
@@ -157,6 +169,13 @@ int nvc_train_grads(const nvc_model *m, const double *pos, const float *targets,
  * Entries nobody touched are zero on every rank, so this equals the dense
  * allreduce bit for bit. */
 int64_t nvc_exchange_max_entries(const nvc_model *m, int64_t b);
+/* Compact gradient mode: sizes of touch_bits (uint32 words) and touch_off
+ * (int32), and the per-batch index build (before nvc_train_grads; b rows of
+ * the GLOBAL batch, identical on every data-parallel rank). */
+int64_t nvc_touch_words(const nvc_model *m);
+int64_t nvc_touch_off_len(const nvc_model *m);
+int nvc_train_index(const nvc_model *m, const double *pos, int64_t b_max, const int64_t *b_dev,
+                    void *stream);
 int64_t nvc_exchange_workspace_bytes(const nvc_model *m);
 int64_t nvc_exchange_buffer_len(const nvc_model *m, int64_t max_entries);
 int nvc_exchange_index(const nvc_model *m, const double *pos, int64_t b_max, const int64_t *b_dev,

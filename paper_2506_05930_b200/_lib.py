@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libnvc.so")
 
 MAX_LEVELS = 32
 MAX_LAYERS = 8
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 c_i32, c_i64, c_u64, c_f64, c_f32, c_vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
                                            ctypes.c_double, ctypes.c_float, ctypes.c_void_p)
@@ -31,6 +31,7 @@ class NvcModel(ctypes.Structure):
         ("n_layers", c_i32), ("dims", c_i32 * (MAX_LAYERS + 1)),
         ("alpha", c_f32), ("out_sigmoid", c_i32),
         ("params", c_vp), ("adam_m", c_vp), ("adam_v", c_vp), ("grad_fx", c_vp),
+        ("touch_bits", c_vp), ("touch_off", c_vp), ("grad_c", c_vp), ("grad_c_entries", c_i64),
         ("table_h", c_vp), ("wpack", c_vp),
         ("param_count", c_i64), ("wpack_count", c_i64),
     ]
@@ -74,6 +75,9 @@ _SIGS = {
                                 c_vp, c_vp, c_vp]),
     "nvc_adam_step": (c_i32, [P(NvcModel), c_i64, c_f64, c_vp]),
     "nvc_exchange_max_entries": (c_i64, [P(NvcModel), c_i64]),
+    "nvc_touch_words": (c_i64, [P(NvcModel)]),
+    "nvc_touch_off_len": (c_i64, [P(NvcModel)]),
+    "nvc_train_index": (c_i32, [P(NvcModel), c_vp, c_i64, c_vp, c_vp]),
     "nvc_exchange_workspace_bytes": (c_i64, [P(NvcModel)]),
     "nvc_exchange_buffer_len": (c_i64, [P(NvcModel), c_i64]),
     "nvc_exchange_index": (c_i32, [P(NvcModel), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),

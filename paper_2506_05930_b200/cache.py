@@ -51,6 +51,9 @@ class GradExchange:
         self.b_max = int(b_max)
         self.max_entries = int(lib.nvc_exchange_max_entries(cache.model, self.b_max))
         dev = cache.device
+        if cache.compact:   # the compact gradient slots are exchanged in place
+            self.ws = self.idx = self.count = self.buf = None
+            return
         self.ws = torch.empty(int(lib.nvc_exchange_workspace_bytes(cache.model)), dtype=torch.uint8, device=dev)
         self.idx = torch.empty(max(self.max_entries, 1), dtype=torch.int32, device=dev)
         self.count = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -70,7 +73,11 @@ class GradExchange:
                   self.max_entries, self.buf.data_ptr(), _lib.stream_ptr())
 
     def allreduce(self, comm, loss) -> None:
-        """pack -> comm(buf, loss) (sum allreduce) -> unpack."""
+        """Compact mode: comm(grad_c, loss) -- the compact slots ARE the exchange
+        buffer.  Dense mode: pack -> comm(buf, loss) -> unpack."""
+        if self.cache.grad_c is not None:
+            comm(self.cache.grad_c, loss)
+            return
         self.pack()
         comm(self.buf, loss)
         self.unpack()
@@ -123,7 +130,14 @@ class VisibilityCache:
         self.params = torch.zeros(total, dtype=torch.float32, device=dev)
         self.adam_m = torch.zeros_like(self.params)
         self.adam_v = torch.zeros_like(self.params)
+        # dense int64 gradient accumulator: used only when compact gradients are off
         self.grad_fx = torch.zeros(total, dtype=torch.int64, device=dev)
+        self.grad_c = None          # compact mode buffers (allocated on the first train step)
+        # compact gradients (nvc.h): ~17 MB of slots instead of the 134 MB dense
+        # accumulator at C2 and an in-place data-parallel exchange buffer; measured
+        # slower per step on one B200 (the entry bitmap costs more than the dense
+        # stream saves), so off by default
+        self.compact = False
         # fp16 query table in x-pair layout (common.cuh): 2 x the grid parameters
         self.table_h = torch.zeros(2 * g.param_count, dtype=torch.float16, device=dev)
         m = _lib.NvcModel()
@@ -294,6 +308,9 @@ class VisibilityCache:
         if loss_out is None:
             loss_out = torch.zeros(2, dtype=torch.float64, device=self.device)   # [sum, mean]
         ws = self._workspace(b_max)
+        if self.compact:
+            self._bind_compact(b_max)
+            _lib.call("nvc_train_index", self.model, pos.data_ptr(), b_max, _lib.ptr(b_dev), _lib.stream_ptr())
         _lib.call("nvc_train_grads", self.model, pos.data_ptr(), targets.data_ptr(), _lib.ptr(mask), b_max,
                   _lib.ptr(b_dev), shard, n_shards, ws.data_ptr(), loss_out.data_ptr(), _lib.stream_ptr())
         return loss_out
@@ -303,6 +320,29 @@ class VisibilityCache:
         self.adam_t += 1
         _lib.call("nvc_adam_step", self.model, self.adam_t, lr, _lib.stream_ptr())
         self.step += 1
+
+    def _bind_compact(self, b_max: int) -> None:
+        """(Re)allocate the compact-gradient buffers for batches of up to b_max rows."""
+        import torch
+        lib = _lib.load()
+        need = int(lib.nvc_exchange_max_entries(self.model, b_max))
+        if self.grad_c is not None and self.model.grad_c_entries >= need:
+            return
+        dev = self.device
+        self.touch_bits = torch.zeros(int(lib.nvc_touch_words(self.model)), dtype=torch.int32, device=dev)
+        self.touch_off = torch.zeros(int(lib.nvc_touch_off_len(self.model)), dtype=torch.int32, device=dev)
+        self.grad_c = torch.zeros(int(lib.nvc_exchange_buffer_len(self.model, need)), dtype=torch.int64, device=dev)
+        self.model.touch_bits = self.touch_bits.data_ptr()
+        self.model.touch_off = self.touch_off.data_ptr()
+        self.model.grad_c = self.grad_c.data_ptr()
+        self.model.grad_c_entries = need
+
+    def set_compact(self, on: bool) -> None:
+        """Compact (default) or dense gradient accumulation; switch only between steps."""
+        self.compact = bool(on)
+        if not on:
+            self.model.grad_c = None
+            self.grad_c = None
 
     def exchange(self, b_max: int) -> GradExchange:
         """The (cached) compact gradient exchange for batches of up to b_max rows."""
@@ -316,10 +356,12 @@ class VisibilityCache:
         optional callable(buffer, loss) that sum-allreduces both in place; it
         receives the compact gradient exchange buffer (GradExchange)."""
         b = int(pos.shape[0] if b_max is None else b_max)
-        if comm is not None:
+        if comm is not None and not self.compact:
             ex = self.exchange(b)
             ex.index(pos, b_dev)
         loss = self.accumulate_grads(pos, targets, mask, b_max=b_max, b_dev=b_dev)
+        if comm is not None and self.compact:
+            ex = self.exchange(b)
         if comm is not None:
             ex.allreduce(comm, loss)
         self.apply_adam()

@@ -68,6 +68,44 @@ Net net_of(const nvc_model* m) {
     return n;
 }
 
+// Where gradients accumulate: the dense int64 grad_fx (param order), or the
+// compact mode (nvc.h): entry e -> slot rank(e) of the batch's sorted entry set.
+struct GradSink {
+    int64_t* dense;
+    const uint32_t* bits;
+    const int32_t* off;
+    int64_t* comp;
+    int64_t comp_entries;
+    int F;
+    int64_t grid_count;
+};
+
+GradSink sink_of(const nvc_model* m) {
+    GradSink gs;
+    gs.dense = m->grad_c ? nullptr : m->grad_fx;
+    gs.bits = m->touch_bits;
+    gs.off = m->touch_off;
+    gs.comp = m->grad_c;
+    gs.comp_entries = m->grad_c_entries;
+    gs.F = m->features;
+    gs.grid_count = (int64_t)m->levels * m->table_size * m->features;
+    return gs;
+}
+
+__device__ __forceinline__ bool grid_touched(const GradSink& gs, int64_t e) { return (gs.bits[e >> 5] >> (e & 31)) & 1u; }
+// gradient slot (feature 0) of table entry e; in compact mode e must be marked
+__device__ __forceinline__ int64_t* grid_grad(const GradSink& gs, int64_t e) {
+    if (gs.comp) {
+        const uint32_t w = gs.bits[e >> 5];
+        const int32_t r = gs.off[e >> 5] + __popc(w & ((1u << (e & 31)) - 1u));
+        return gs.comp + (int64_t)r * gs.F;
+    }
+    return gs.dense + e * gs.F;
+}
+__device__ __forceinline__ int64_t* mlp_grad(const GradSink& gs, int64_t j) {
+    return gs.comp ? gs.comp + gs.comp_entries * gs.F + j : gs.dense + gs.grid_count + j;
+}
+
 int validate(const nvc_model* m) {
     NVC_REQUIRE(m, "null model");
     NVC_REQUIRE(m->levels >= 1 && m->levels <= NVC_MAX_LEVELS, "levels out of range");
@@ -178,7 +216,7 @@ __global__ void __launch_bounds__(kThreads) k_mlp(GridDev g, Net net, const floa
                                                  const double* __restrict__ pos, int64_t b_max,
                                                  const int64_t* __restrict__ b_dev, int shard, int n_shards,
                                                  const float* __restrict__ tgt, const float* __restrict__ mask,
-                                                 float* __restrict__ out, int64_t* __restrict__ grad_fx,
+                                                 float* __restrict__ out, GradSink gs,
                                                  float* __restrict__ part_w, double* __restrict__ part_loss) {
     extern __shared__ float sm[];
     const TileLayout tl = tile_layout(net);
@@ -310,14 +348,14 @@ __global__ void __launch_bounds__(kThreads) k_mlp(GridDev g, Net net, const floa
         double f[3];
         cell(g.res[l], q, c0, f);
         const float* up = dz_cur + r * D0 + l * g.F;
-        int64_t* gl = grad_fx + (int64_t)l * g.T * g.F;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
             const uint32_t idx = corner_index(g, l, c0, (c >> 2) & 1, (c >> 1) & 1, c & 1);
             const double w = corner_weight(f, c);
+            int64_t* gp = grid_grad(gs, (int64_t)l * g.T + idx);
             for (int k = 0; k < g.F; ++k) {
                 const float contrib = (float)__dmul_rn(w, (double)up[k]);   // (w * g).astype(f32)
-                red_add_fx(gl + (int64_t)idx * g.F + k, to_fx((double)contrib));
+                red_add_fx(gp + k, to_fx((double)contrib));
             }
         }
     }
@@ -577,7 +615,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_train3(Net net, const float* __
 
 __global__ void __launch_bounds__(128) k_tr_scatter(GridDev g, const double* __restrict__ pos, int64_t b_max,
                                                     const int64_t* __restrict__ b_dev, int shard, int n_shards,
-                                                    const float* __restrict__ dact0, int64_t* __restrict__ grad_fx) {
+                                                    const float* __restrict__ dact0, GradSink gs) {
     const ShardRows sr = shard_rows(b_max, b_dev, shard, n_shards);
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t r = t / g.L;
@@ -592,14 +630,14 @@ __global__ void __launch_bounds__(128) k_tr_scatter(GridDev g, const double* __r
     cell(g.res[l], q, c0, f);
     float up[8];
     for (int k = 0; k < g.F; ++k) up[k] = __ldg(dact0 + r * (g.L * g.F) + l * g.F + k);
-    int64_t* gl = grad_fx + (int64_t)l * g.T * g.F;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
         const uint32_t idx = corner_index(g, l, c0, (c >> 2) & 1, (c >> 1) & 1, c & 1);
         const double w = corner_weight(f, c);
+        int64_t* gp = grid_grad(gs, (int64_t)l * g.T + idx);
         for (int k = 0; k < g.F; ++k) {
             const float contrib = (float)__dmul_rn(w, (double)up[k]);   // (w * g).astype(f32), hashgrid.py:146-151
-            red_add_fx(gl + (int64_t)idx * g.F + k, to_fx((double)contrib));
+            red_add_fx(gp + k, to_fx((double)contrib));
         }
     }
 }
@@ -684,7 +722,7 @@ __global__ void __launch_bounds__(1024) k_touch_scan(int* __restrict__ chunk_cou
         if (threadIdx.x == 1023) carry = excl + v;
         __syncthreads();
     }
-    if (threadIdx.x == 0) *total = carry;
+    if (threadIdx.x == 0 && total) *total = carry;
 }
 
 // write the sorted entry list: chunk offset + prefix of popcounts inside the chunk
@@ -721,6 +759,33 @@ __global__ void __launch_bounds__(1024) k_touch_emit(const uint32_t* __restrict_
     }
 }
 
+// per-word rank of the word's first marked entry (compact gradient mode)
+__global__ void __launch_bounds__(1024) k_touch_offsets(const uint32_t* __restrict__ bits, int64_t n_words,
+                                                        const int* __restrict__ chunk_off, int32_t* __restrict__ off) {
+    __shared__ int warp_sum[32];
+    const int64_t wi = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+    const int v = wi < n_words ? __popc(bits[wi]) : 0;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_sum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const int x = warp_sum[lane];
+        int xi = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += y;
+        }
+        warp_sum[lane] = xi - x;
+    }
+    __syncthreads();
+    if (wi < n_words) off[wi] = chunk_off[blockIdx.x] + warp_sum[wid] + incl - v;
+}
+
 // buf = [grad of listed entries (F each, zero past the count) | MLP gradients]
 __global__ void k_grad_pack(const int64_t* __restrict__ fx, const int32_t* __restrict__ idx,
                             const int64_t* __restrict__ count, int64_t max_entries, int F, int64_t grid_count,
@@ -754,7 +819,7 @@ __global__ void k_grad_unpack(int64_t* __restrict__ fx, const int32_t* __restric
 __global__ void __launch_bounds__(256) k_reduce_parts(const float* __restrict__ part_w,
                                                       const double* __restrict__ part_loss, int nblk,
                                                       int64_t mlp_count, int64_t grid_count,
-                                                      int64_t* __restrict__ grad_fx, double* __restrict__ loss_out,
+                                                      GradSink gs, double* __restrict__ loss_out,
                                                       int64_t b_max, const int64_t* __restrict__ b_dev) {
     __shared__ double s_acc[8][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -767,7 +832,7 @@ __global__ void __launch_bounds__(256) k_reduce_parts(const float* __restrict__ 
     if (w == 0 && j < mlp_count) {
         double t = 0.0;
         for (int i = 0; i < 8; ++i) t += s_acc[i][lane];
-        grad_fx[grid_count + j] += to_fx(t);
+        *mlp_grad(gs, j) += to_fx(t);
     }
     if (blockIdx.x == 0 && w == 1 && loss_out) {
         double t = 0.0;
@@ -825,13 +890,18 @@ __device__ __forceinline__ void put_pair(uint16_t* t2, int64_t i, int F, int64_t
 // cleared where nonzero (after a data-parallel allreduce it is already the
 // global sum).
 __global__ void __launch_bounds__(256) k_adam_flat(float* __restrict__ p, float* __restrict__ m,
-                                                   float* __restrict__ v, int64_t* __restrict__ fx,
+                                                   float* __restrict__ v, GradSink gs,
                                                    uint16_t* __restrict__ table_h, int64_t n, int F, AdamK a,
                                                    int64_t T) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const long long q = fx[i];
-    if (q) fx[i] = 0;
+    const int64_t e = i / F;
+    long long q = 0;
+    if (!gs.comp || grid_touched(gs, e)) {
+        int64_t* gq = grid_grad(gs, e) + (i - e * F);
+        q = *gq;
+        if (q) *gq = 0;
+    }
     float mm = m[i], vv = v[i];
     const float pn = adam1(p[i], from_fx(q), mm, vv, a);
     p[i] = pn;
@@ -856,10 +926,14 @@ struct AdamStage {
     long long q[kAdamTile];
 };
 
+// kCompact: the grid gradients come from the compact slots (GradSink) of the
+// batch's marked entries instead of a dense int64 tile stream.
+template <bool kCompact>
 __global__ void __launch_bounds__(kAdamThreads) k_adam_bulk(float* __restrict__ p, float* __restrict__ m,
-                                                           float* __restrict__ v, int64_t* __restrict__ fx,
+                                                           float* __restrict__ v, GradSink gs,
                                                            uint16_t* __restrict__ table_h, int64_t ntiles, AdamK a,
                                                            int64_t T) {
+    int64_t* __restrict__ fx = gs.dense;
     extern __shared__ __align__(128) uint8_t adam_smem[];
     AdamStage* st = reinterpret_cast<AdamStage*>(adam_smem);
     __shared__ uint64_t full[kAdamStages];
@@ -869,11 +943,11 @@ __global__ void __launch_bounds__(kAdamThreads) k_adam_bulk(float* __restrict__ 
     auto issue = [&](int i) {
         const int s = i % kAdamStages;
         const int64_t base = tile_base(i);
-        tma::bar_expect_tx(&full[s], (uint32_t)sizeof(AdamStage));
+        tma::bar_expect_tx(&full[s], kCompact ? 3u * kAdamTile * 4u : (uint32_t)sizeof(AdamStage));
         tma::load(st[s].p, p + base, kAdamTile * 4, &full[s]);
         tma::load(st[s].m, m + base, kAdamTile * 4, &full[s]);
         tma::load(st[s].v, v + base, kAdamTile * 4, &full[s]);
-        tma::load(st[s].q, fx + base, kAdamTile * 8, &full[s]);
+        if (!kCompact) tma::load(st[s].q, fx + base, kAdamTile * 8, &full[s]);
     };
     if (tid == 0) {
         for (int s = 0; s < kAdamStages; ++s) tma::bar_init(&full[s], 1);
@@ -890,10 +964,30 @@ __global__ void __launch_bounds__(kAdamThreads) k_adam_bulk(float* __restrict__ 
         float4* P4 = reinterpret_cast<float4*>(st[s].p) + tid;
         float4* M4 = reinterpret_cast<float4*>(st[s].m) + tid;
         float4* V4 = reinterpret_cast<float4*>(st[s].v) + tid;
-        const longlong2* Q2 = reinterpret_cast<const longlong2*>(st[s].q) + 2 * tid;
-        const longlong2 qa = Q2[0], qb = Q2[1];
-        if (qa.x | qa.y) *reinterpret_cast<longlong2*>(fx + i0) = make_longlong2(0, 0);
-        if (qb.x | qb.y) *reinterpret_cast<longlong2*>(fx + i0 + 2) = make_longlong2(0, 0);
+        longlong2 qa = make_longlong2(0, 0), qb = make_longlong2(0, 0);
+        if constexpr (kCompact) {   // entries e0, e0+1 share a bitmap word (e0 even)
+            const uint32_t w = __ldg(gs.bits + (e0 >> 5));
+            const int b = (int)(e0 & 31);
+            if ((w >> b) & 3u) {
+                const int32_t r = __ldg(gs.off + (e0 >> 5)) + __popc(w & ((1u << b) - 1u));
+                longlong2* g2 = reinterpret_cast<longlong2*>(gs.comp) + r;   // F == 2: one slot = 16 B
+                if ((w >> b) & 1u) {
+                    qa = *g2;
+                    *g2 = make_longlong2(0, 0);
+                    ++g2;
+                }
+                if ((w >> (b + 1)) & 1u) {
+                    qb = *g2;
+                    *g2 = make_longlong2(0, 0);
+                }
+            }
+        } else {
+            const longlong2* Q2 = reinterpret_cast<const longlong2*>(st[s].q) + 2 * tid;
+            qa = Q2[0];
+            qb = Q2[1];
+            if (qa.x | qa.y) *reinterpret_cast<longlong2*>(fx + i0) = make_longlong2(0, 0);
+            if (qb.x | qb.y) *reinterpret_cast<longlong2*>(fx + i0 + 2) = make_longlong2(0, 0);
+        }
         const long long q[4] = {qa.x, qa.y, qb.x, qb.y};
         float4 P = *P4, M = *M4, V = *V4;
         float* Pp = &P.x;
@@ -936,12 +1030,13 @@ __global__ void __launch_bounds__(kAdamThreads) k_adam_bulk(float* __restrict__ 
 }
 
 __global__ void k_adam_mlp(Net net, float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
-                           int64_t* __restrict__ fx, uint16_t* __restrict__ wpack, AdamK a) {
+                           GradSink gs, uint16_t* __restrict__ wpack, AdamK a) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= net.mlp_count) return;
     const int64_t i = net.grid_count + j;
-    const long long q = fx[i];
-    fx[i] = 0;
+    int64_t* gq = mlp_grad(gs, j);
+    const long long q = *gq;
+    *gq = 0;
     float mm = m[i], vv = v[i];
     const float pn = adam1(p[i], from_fx(q), mm, vv, a);
     p[i] = pn;
@@ -1004,7 +1099,7 @@ int nvc::nvc_infer_f32(const nvc_model* m, const double* pos, int64_t n, float* 
     NVC_REQUIRE(smem <= 200 * 1024, "nvc_infer: MLP too wide for the fp32 tile kernel");
     cudaFuncSetAttribute(k_mlp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k_mlp<false><<<grid1(n, kRows), kThreads, smem, s>>>(g, net, m->params, pos, n, nullptr, 0, 1, nullptr,
-                                                          nullptr, out, nullptr, nullptr, nullptr);
+                                                          nullptr, out, GradSink{}, nullptr, nullptr);
     return check_launch("k_mlp<infer>");
 }
 
@@ -1051,7 +1146,11 @@ int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, con
                     void* stream) {
     int rc = validate(m);
     if (rc) return rc;
-    NVC_REQUIRE(pos && tgt && ws && m->grad_fx, "nvc_train_grads: null argument");
+    NVC_REQUIRE(pos && tgt && ws && (m->grad_fx || m->grad_c), "nvc_train_grads: null argument");
+    NVC_REQUIRE(!m->grad_c || (m->touch_bits && m->touch_off), "nvc_train_grads: compact mode needs the touch index");
+    NVC_REQUIRE(!m->grad_c || m->grad_c_entries >= std::min<int64_t>(b_max * m->levels * 8,
+                                                                     (int64_t)m->levels * m->table_size),
+                "nvc_train_grads: grad_c_entries below nvc_exchange_max_entries(b_max)");
     NVC_REQUIRE(n_shards >= 1 && shard >= 0 && shard < n_shards, "nvc_train_grads: bad shard");
     NVC_REQUIRE(m->out_sigmoid == 1 || m->out_sigmoid == 0, "bad output activation");
     if (b_max <= 0) return NVC_OK;
@@ -1078,18 +1177,18 @@ int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, con
         rc = check_launch("k_train3");
         if (rc) return rc;
         k_tr_scatter<<<grid1(rows_max * g.L, 128), 128, 0, s>>>(g, pos, b_max, b_dev, shard, n_shards, dact0,
-                                                                 m->grad_fx);
+                                                                 sink_of(m));
     } else {
         const int smem = mlp_smem_bytes(net);
         NVC_REQUIRE(smem <= 200 * 1024, "nvc_train_grads: MLP too wide for the fp32 tile kernel");
         cudaFuncSetAttribute(k_mlp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         k_mlp<true><<<nblk, kThreads, smem, s>>>(g, net, m->params, pos, b_max, b_dev, shard, n_shards, tgt, mask,
-                                                  nullptr, m->grad_fx, part_w, part_loss);
+                                                  nullptr, sink_of(m), part_w, part_loss);
     }
     rc = check_launch("nvc_train_grads");
     if (rc) return rc;
     k_reduce_parts<<<grid1(net.mlp_count, 32), 256, 0, s>>>(part_w, part_loss, nblk, net.mlp_count,
-                                                             net.grid_count, m->grad_fx, loss_out, b_max, b_dev);
+                                                             net.grid_count, sink_of(m), loss_out, b_max, b_dev);
     return check_launch("k_reduce_parts");
 }
 
@@ -1113,6 +1212,27 @@ int64_t nvc_exchange_buffer_len(const nvc_model* m, int64_t max_entries) {
     if (!m) return 0;
     Net net = net_of(m);
     return max_entries * m->features + net.mlp_count;
+}
+
+int64_t nvc_touch_words(const nvc_model* m) { return m ? touch_words(m) : 0; }
+int64_t nvc_touch_off_len(const nvc_model* m) { return m ? touch_words(m) + (touch_words(m) + 1023) / 1024 : 0; }
+
+int nvc_train_index(const nvc_model* m, const double* pos, int64_t b_max, const int64_t* b_dev, void* stream) {
+    int rc = validate(m);
+    if (rc) return rc;
+    NVC_REQUIRE(pos && m->touch_bits && m->touch_off, "nvc_train_index: null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    GridDev g = grid_of(m);
+    const int64_t words = touch_words(m);
+    const int n_chunks = (int)((words + 1023) / 1024);
+    int* chunk = m->touch_off + words;
+    cudaMemsetAsync(m->touch_bits, 0, words * 4, s);
+    if (b_max > 0)
+        k_touch_mark<<<grid1(b_max * g.L, 128), 128, 0, s>>>(g, pos, b_max, b_dev, m->touch_bits);
+    k_touch_count<<<n_chunks, 256, 0, s>>>(m->touch_bits, words, chunk);
+    k_touch_scan<<<1, 1024, 0, s>>>(chunk, n_chunks, nullptr);
+    k_touch_offsets<<<n_chunks, 1024, 0, s>>>(m->touch_bits, words, chunk, m->touch_off);
+    return check_launch("nvc_train_index");
 }
 
 int nvc_exchange_index(const nvc_model* m, const double* pos, int64_t b_max, const int64_t* b_dev, void* ws,
@@ -1163,7 +1283,8 @@ int nvc_adam_step(const nvc_model* m, int64_t t, double lr, void* stream) {
     int rc = validate(m);
     if (rc) return rc;
     NVC_REQUIRE(t >= 1, "nvc_adam_step: t must be >= 1");
-    NVC_REQUIRE(m->adam_m && m->adam_v && m->grad_fx && m->table_h && m->wpack, "nvc_adam_step: state not bound");
+    NVC_REQUIRE(m->adam_m && m->adam_v && (m->grad_fx || m->grad_c) && m->table_h && m->wpack,
+                "nvc_adam_step: state not bound");
     Net net = net_of(m);
     AdamK a;
     a.b1 = (float)0.9;
@@ -1179,22 +1300,27 @@ int nvc_adam_step(const nvc_model* m, int64_t t, double lr, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (m->features == 2 && m->table_size % 64 == 0 && net.grid_count % kAdamTile == 0 && !getenv("NVC_ADAM_FLAT")) {
         const int smem = kAdamStages * (int)sizeof(AdamStage);
-        cudaFuncSetAttribute(k_adam_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_adam_bulk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_adam_bulk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int dev = 0, sms = kNumSMs;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int64_t ntiles = net.grid_count / kAdamTile;
         const int grid = (int)std::min<int64_t>(ntiles, 5 * (int64_t)sms);
-        k_adam_bulk<<<grid, kAdamThreads, smem, s>>>(m->params, m->adam_m, m->adam_v, m->grad_fx, m->table_h, ntiles,
-                                                     a, m->table_size);
+        if (m->grad_c)
+            k_adam_bulk<true><<<grid, kAdamThreads, smem, s>>>(m->params, m->adam_m, m->adam_v, sink_of(m), m->table_h,
+                                                               ntiles, a, m->table_size);
+        else
+            k_adam_bulk<false><<<grid, kAdamThreads, smem, s>>>(m->params, m->adam_m, m->adam_v, sink_of(m),
+                                                                m->table_h, ntiles, a, m->table_size);
     } else {
-        k_adam_flat<<<grid1(net.grid_count, 256), 256, 0, s>>>(m->params, m->adam_m, m->adam_v, m->grad_fx,
+        k_adam_flat<<<grid1(net.grid_count, 256), 256, 0, s>>>(m->params, m->adam_m, m->adam_v, sink_of(m),
                                                                m->table_h, net.grid_count, m->features, a,
                                                                m->table_size);
     }
     rc = check_launch("k_adam_grid");
     if (rc) return rc;
-    k_adam_mlp<<<grid1(net.mlp_count, 256), 256, 0, s>>>(net, m->params, m->adam_m, m->adam_v, m->grad_fx,
+    k_adam_mlp<<<grid1(net.mlp_count, 256), 256, 0, s>>>(net, m->params, m->adam_m, m->adam_v, sink_of(m),
                                                          m->wpack, a);
     return check_launch("k_adam_mlp");
 }

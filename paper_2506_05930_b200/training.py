@@ -213,13 +213,13 @@ def train_frame_device(scene, camera, cache, cfg: TrainFrameConfig, frame: int =
     for step in range(cfg.steps):
         if pipeline is None:
             gen_batch_device(scene, camera, bufs, cfg.seed, frame, step, shard, n_shards)
-        if comm is not None:   # entries touched by the GLOBAL batch: identical on every rank
+        if comm is not None and not cache.compact:   # dense mode: list the global batch's entries
             ex = cache.exchange(b_max)
             ex.index(bufs.pos, bufs.n_rows)
         cache.accumulate_grads(bufs.pos, bufs.tgt, b_max=b_max, b_dev=bufs.n_rows,
                                shard=shard, n_shards=n_shards, loss_out=bufs.loss)
         if comm is not None:
-            ex.allreduce(comm, bufs.loss)
+            cache.exchange(b_max).allreduce(comm, bufs.loss)
         cache.apply_adam()
         loss = bufs.loss[1]
     if pipeline is not None:

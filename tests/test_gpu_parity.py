@@ -333,6 +333,7 @@ class TestTraining:
         if kernel == "flat":
             monkeypatch.setenv("NVC_ADAM_FLAT", "1")
         c = self._c1(pbox8)
+        c.set_compact(False)          # feed arbitrary dense gradients
         p0 = c.params.cpu().numpy().copy()
         g = np.random.default_rng(5)
         st = O.Adam(p0.size)
@@ -358,17 +359,20 @@ class TestTraining:
         np.testing.assert_array_equal(t2[:, :, 0], tab)                       # own slot
         np.testing.assert_array_equal(t2[:, :, 1], np.roll(tab, -1, axis=1))  # x-neighbour (mod T)
 
-    def test_bulk_and_flat_adam_agree_and_consume_grads(self, pbox8, g_train, monkeypatch):
+    @pytest.mark.parametrize("compact", [True, False])
+    def test_bulk_and_flat_adam_agree_and_consume_grads(self, pbox8, g_train, monkeypatch, compact):
         a, b = self._c1(pbox8), self._c1(pbox8)
         pt = torch.from_numpy(g_train["c1_pos"]).to(DEV)
         tt = torch.from_numpy(g_train["c1_tgt"].astype(np.float32)).to(DEV)
         for c, flat in ((a, False), (b, True)):
+            c.set_compact(compact)
             if flat:
                 monkeypatch.setenv("NVC_ADAM_FLAT", "1")
             c.accumulate_grads(pt, tt)
-            assert c.grad_fx.any()
+            acc = c.grad_c if compact else c.grad_fx
+            assert acc.any()
             c.apply_adam()
-            assert not c.grad_fx.any()          # the accumulator is consumed (zeroed) by Adam
+            assert not acc.any()                # the accumulator is consumed (zeroed) by Adam
         np.testing.assert_array_equal(a.params.cpu().numpy(), b.params.cpu().numpy())
         np.testing.assert_array_equal(a.table_h.cpu().numpy(), b.table_h.cpu().numpy())
 
@@ -402,9 +406,11 @@ class TestTraining:
         tgt = torch.from_numpy(g_train["c1_tgt"].astype(np.float32)).to(DEV)
         b = pos.shape[0]
         full = self._c1(pbox8)
+        full.set_compact(False)
         full.accumulate_grads(pos, tgt)
         shards = [self._c1(pbox8) for _ in range(3)]
         for sh, c in enumerate(shards):
+            c.set_compact(False)
             lo, hi = b * sh // 3, b * (sh + 1) // 3
             c.accumulate_grads(pos, tgt[lo:hi].contiguous(), b_max=b, shard=sh, n_shards=3)
             ex = c.exchange(b)
@@ -419,6 +425,33 @@ class TestTraining:
         np.testing.assert_array_equal(full.grad_fx[:gc].cpu().numpy(), shards[0].grad_fx[:gc].cpu().numpy())
         np.testing.assert_allclose(full.grad_fx[gc:].double().cpu().numpy(),
                                    shards[0].grad_fx[gc:].double().cpu().numpy(), rtol=1e-5, atol=2.0 ** 48 * 1e-9)
+
+    def test_compact_gradients_match_dense(self, pbox8, g_train):
+        """Compact gradient slots train exactly like the dense accumulator (same arithmetic,
+        same integer sums): identical parameters after three steps, whole-batch and with two
+        row shards whose compact buffers are summed as the allreduce would."""
+        pos = torch.from_numpy(g_train["c1_pos"]).to(DEV)
+        tgt = torch.from_numpy(g_train["c1_tgt"].astype(np.float32)).to(DEV)
+        b = pos.shape[0]
+
+        def run(compact, shards):
+            ranks = [self._c1(pbox8) for _ in range(shards)]
+            for c in ranks:
+                c.set_compact(compact)
+            for step in range(3):
+                for r, c in enumerate(ranks):
+                    lo, hi = b * r // shards, b * (r + 1) // shards
+                    c.accumulate_grads(pos, tgt[lo:hi].contiguous(), b_max=b, shard=r, n_shards=shards)
+                acc = [c.grad_c if compact else c.grad_fx for c in ranks]
+                total = sum(acc)
+                for t in acc:
+                    t.copy_(total)
+                for c in ranks:
+                    c.apply_adam()
+            return ranks[0].params.cpu().numpy()
+
+        for shards in (1, 2):
+            np.testing.assert_array_equal(run(False, shards), run(True, shards))
 
     def test_batch_pipeline_matches_inline_generation(self, pbox8):
         """Batches prefetched one frame ahead on a side stream train bit-identically."""
@@ -458,6 +491,8 @@ class TestTraining:
         pos = torch.from_numpy(g_train["c1_pos"]).to(DEV)
         tgt = torch.from_numpy(g_train["c1_tgt"].astype(np.float32)).to(DEV)
         full, parts = self._c1(pbox8), self._c1(pbox8)
+        full.set_compact(False)
+        parts.set_compact(False)
         full.accumulate_grads(pos, tgt)
         b = pos.shape[0]
         for sh in range(4):
