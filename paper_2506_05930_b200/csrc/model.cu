@@ -825,8 +825,18 @@ __global__ void __launch_bounds__(256) k_reduce_parts(const float* __restrict__ 
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t j = (int64_t)blockIdx.x * 32 + lane;
     double acc = 0.0;
-    if (j < mlp_count)
-        for (int b = w; b < nblk; b += 8) acc += (double)__ldg(part_w + (int64_t)b * mlp_count + j);
+    if (j < mlp_count) {
+        // same sequential order; loads batched so eight are in flight per thread
+        int b = w;
+        for (; b + 56 < nblk; b += 64) {
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldg(part_w + (int64_t)(b + 8 * u) * mlp_count + j);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc += (double)v[u];
+        }
+        for (; b < nblk; b += 8) acc += (double)__ldg(part_w + (int64_t)b * mlp_count + j);
+    }
     s_acc[w][lane] = acc;
     __syncthreads();
     if (w == 0 && j < mlp_count) {
