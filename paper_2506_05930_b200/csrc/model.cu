@@ -429,14 +429,14 @@ __global__ void __launch_bounds__(128) k_tr_encode(GridDev g, const float* __res
     encode_level_f32(g, params, q, l, act0 + r * (g.L * g.F) + l * g.F, nullptr, nullptr);
 }
 
-__global__ void __launch_bounds__(kThreads, 2) k_train3(Net net, const float* __restrict__ params,
+__global__ void __launch_bounds__(kThreads, 2) k_train3(Net net, T3Layout tl, const float* __restrict__ params,
                                                        const float* __restrict__ act0g, int64_t b_max,
                                                        const int64_t* __restrict__ b_dev, int shard, int n_shards,
                                                        const float* __restrict__ tgt, const float* __restrict__ mask,
                                                        float* __restrict__ dact0g, float* __restrict__ part_w,
                                                        double* __restrict__ part_loss) {
     extern __shared__ __align__(16) float sm[];
-    const T3Layout tl = t3_layout(net);
+    // tl arrives in the parameter bank (indexed per layer without a local-memory copy)
     const int tid = threadIdx.x;
     const ShardRows sr = shard_rows(b_max, b_dev, shard, n_shards);
     const int64_t b = b_dev ? *b_dev : b_max;
@@ -1182,8 +1182,8 @@ int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, con
         rc = check_launch("k_tr_encode");
         if (rc) return rc;
         cudaFuncSetAttribute(k_train3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
-        k_train3<<<nblk, kThreads, smem3, s>>>(net, m->params, act0, b_max, b_dev, shard, n_shards, tgt, mask, dact0,
-                                               part_w, part_loss);
+        k_train3<<<nblk, kThreads, smem3, s>>>(net, t3_layout(net), m->params, act0, b_max, b_dev, shard, n_shards,
+                                               tgt, mask, dact0, part_w, part_loss);
         rc = check_launch("k_train3");
         if (rc) return rc;
         k_tr_scatter<<<grid1(rows_max * g.L, 128), 128, 0, s>>>(g, pos, b_max, b_dev, shard, n_shards, dact0,
