@@ -52,8 +52,4 @@ def build(verbose: bool = False, force: bool = False, defs: list[str] | None = N
 
 
 if __name__ == "__main__":
-    if "--trace" in sys.argv:   # profiling build: event timeline of k_mlp_wg (tools/trace_mlp.py)
-        print(build(verbose="-v" in sys.argv, force=True, defs=["-DNVC_TRACE"],
-                    out=os.path.join(HERE, "libnvc_trace.so")))
-    else:
-        print(build(verbose="-v" in sys.argv, force=True))
+    print(build(verbose="-v" in sys.argv, force=True))

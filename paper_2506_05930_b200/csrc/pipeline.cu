@@ -485,25 +485,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_tiles(MNet net, const fl
 }
 
 // ---------------------------------------------------------------------------
-// stage 2 (default for widths <= 64): four self-issuing warpgroups
-//
-// Each warpgroup owns two tiles in flight (two 64-column TMEM accumulators,
-// two A0 and two A1 smem buffers) and ping-pongs between them: while it drains
-// tile A's layer-l accumulator (tcgen05.ld -> +bias -> leaky in half2 -> A1),
-// the tensor core runs tile B's layer.  An elected thread of the warpgroup
-// issues its own MMAs right after a warpgroup-local named barrier, so there is
-// no cross-warpgroup lockstep and no separate MMA/producer warps; A0 tiles of
-// the next-but-one tile are bulk-copied as soon as layer 0 has consumed the
-// buffer.  Output: sigmoid via tanh.approx (0.5 + 0.5 tanh(z/2)), clipped,
-// fp16 pixel-major rows.
+// tcgen05 helpers for the MLP kernels below
 // ---------------------------------------------------------------------------
-constexpr int kWG = 4;
-constexpr int kWgThreads = 160 * kWG;   // 4 epilogue warpgroups + one MMA warp per warpgroup
-
-struct WGBars {
-    uint64_t a0_full[2], acc_full[2];
-};
-
 __device__ __forceinline__ void tld16_nowait(uint32_t taddr, uint32_t r[16]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -532,261 +515,14 @@ __device__ __forceinline__ float tanh_fast(float x) {
     return y;
 }
 
-#ifdef NVC_TRACE
-// profiling build only: (clock64 << 16 | wg << 12 | code << 8 | layer << 4 | slot) of CTA 0, one
-// 4096-entry row per warpgroup, written by its issuer with plain stores (no atomics on the path)
-__device__ unsigned long long g_wg_trace[2 * kWG * 4096];   // rows 0-3 epilogue issuers, 4-7 MMA warps
-__device__ unsigned int g_wg_trace_n;
-#define WG_TRACE(code, l, s)                                                                                  \
-    do {                                                                                                      \
-        if (blockIdx.x == 0 && trace_me && trace_n < 4096)                                                    \
-            g_wg_trace[(g + (mma_warp ? kWG : 0)) * 4096 + trace_n++] = ((unsigned long long)clock64() << 16) | ((unsigned)g << 12) | \
-                                               ((code) << 8) | ((l) << 4) | (s);                             \
-    } while (0)
-#else
-#define WG_TRACE(code, l, s) \
-    do {                     \
-    } while (0)
-#endif
-
-// swizzled K-major offset of 16-byte chunk c in row `row` of a [128 x KP] tile
-// (KP <= 64: one swizzle atom per row; common.cuh umma_off)
-template <int KP>
-struct RowSw {
-    static constexpr int lg = KP >= 64 ? 7 : (KP == 32 ? 6 : 5);
-    uint32_t rb, rx;
-    __device__ __forceinline__ explicit RowSw(int row) : rb((uint32_t)row << lg), rx((uint32_t)(row & 7) >> (7 - lg)) {}
-    __device__ __forceinline__ uint32_t chunk(int c) const { return rb + ((((uint32_t)c) ^ rx) << 4); }
-};
-
-// leaky(x + b) on 8 fp16 pairs
-__device__ __forceinline__ uint4 bias_leaky8(const uint32_t* r, uint4 b, __half2 al2) {
-    const __half2* bb = reinterpret_cast<const __half2*>(&b);
-    __align__(16) __half2 h[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        __half2 z = __floats2half2_rn(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
-        z = __hadd2(z, bb[e]);
-        h[e] = __hmax2(z, __hmul2(z, al2));
-    }
-    return *reinterpret_cast<const uint4*>(h);
-}
-
-// HID: padded width of every hidden layer (MMA N and next K); OUT: padded
-// output width; KP0: padded input width.  Weights / biases / descriptors are
-// compile-time shaped; the layer count is a runtime value.
-template <int HID, int OUT, int KP0>
-__global__ void __launch_bounds__(kWgThreads, 1) k_mlp_wg(MNet net, const float* __restrict__ params,
-                                                         const uint16_t* __restrict__ wpack,
-                                                         const uint8_t* __restrict__ tiles, int64_t ntiles, int64_t P,
-                                                         __half* __restrict__ vis16, int64_t vstride) {
-    static_assert(HID <= 64 && OUT <= 64 && KP0 <= 64, "one swizzle atom per row");
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    __shared__ WGBars bars[kWG];
-    __shared__ uint32_t tbase;
-    uint8_t* smem = smem_raw + ((1024u - (s32(smem_raw) & 1023u)) & 1023u);
-    uint8_t* s_w = smem + net.sm_w;
-    uint8_t* s_a0 = smem + net.sm_a0;
-    uint8_t* s_a1 = smem + net.sm_a1;
-    __half* s_bh = reinterpret_cast<__half*>(smem + net.sm_bias);           // hidden biases (fp16)
-    float* s_bo = reinterpret_cast<float*>(smem + net.sm_bias + 1024);       // output bias / 2 (f32)
-    const int tid = threadIdx.x, row = tid & 127;
-    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // warp-uniform (lets descriptors live in URs)
-    const bool mma_warp = warp >= 4 * kWG;                      // warps 16..19: MMA issuer of warpgroup warp-16
-    const int g = mma_warp ? warp - 4 * kWG : warp >> 2, wq = warp & 3;
-    const int L = net.n_layers;
-    constexpr int a0_bytes = kT * KP0 * 2;
-    constexpr int a1_bytes = kT * HID * 2;
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(wpack);
-        uint4* dst = reinterpret_cast<uint4*>(s_w);
-        for (int i = tid; i < net.wpack_halfs / 8; i += kWgThreads) dst[i] = __ldg(src + i);
-        for (int l = 0; l < L - 1; ++l)
-            for (int n = tid; n < HID; n += kWgThreads)
-                s_bh[l * HID + n] = __float2half_rn(n < net.dims[l + 1] ? __ldg(params + net.boff[l] + n) : 0.0f);
-        for (int n = tid; n < OUT; n += kWgThreads)
-            s_bo[n] = n < net.dims[L] ? 0.5f * __ldg(params + net.boff[L - 1] + n) : 0.0f;
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(&tbase)), "r"(512)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    if (tid == 0) {
-        for (int w = 0; w < kWG; ++w)
-            for (int s = 0; s < 2; ++s) {
-                mbar_init(&bars[w].a0_full[s], 1);
-                mbar_init(&bars[w].acc_full[s], 1);
-            }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    fence_async();
-    tc_before();
-    __syncthreads();
-    tc_after();
-    const uint32_t tmem = tbase;
-    WGBars& B = bars[g];
-    const int64_t t0 = (int64_t)blockIdx.x * kWG + g, tstep = (int64_t)gridDim.x * kWG;
-    const int n_wg = ntiles > t0 ? (int)((ntiles - 1 - t0) / tstep + 1) : 0;
-    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-    const bool issuer = !mma_warp && (tid & 127) == 0;
-#ifdef NVC_TRACE
-    unsigned trace_n = 0;
-    const bool trace_me = issuer || (mma_warp && (tid & 31) == 0);
-#endif
-    // per-layer B descriptors (k-step kk adds 2: 32 bytes inside the row's swizzle atom)
-    const uint32_t w_addr = s32(s_w);
-    auto a0_of = [&](int s) { return s_a0 + (2 * g + s) * a0_bytes; };
-    auto a1_of = [&](int s) { return s_a1 + (2 * g + s) * a1_bytes; };
-    auto acc_of = [&](int s) { return tmem + (uint32_t)((2 * g + s) * 64); };
-    auto load_a0 = [&](int k, int s) {
-        mbar_expect_tx(&B.a0_full[s], (uint32_t)a0_bytes);
-        bulk_g2s(a0_of(s), tiles + (t0 + (int64_t)k * tstep) * a0_bytes, (uint32_t)a0_bytes, &B.a0_full[s]);
-    };
-    auto issue = [&](int l, int s) {   // the warpgroup's MMA warp, converged
-        tc_after();
-        const bool first = l == 0, last = l == L - 1;
-        const int kp = first ? KP0 : HID, np = last ? OUT : HID;
-        const uint32_t idesc = (1u << 4) | ((uint32_t)(np >> 3) << 17) | ((uint32_t)(kT >> 4) << 24);
-        const uint64_t da = desc_of(s32(first ? a0_of(s) : a1_of(s)), kT, kp, 0);
-        const uint64_t db = desc_of(w_addr + 2u * (uint32_t)net.wofs[l], np, kp, 0);
-        const uint32_t d = acc_of(s);
-        WG_TRACE(6, l, s);
-        mma_elect(d, da, db, idesc, 0u);
-        WG_TRACE(7, l, s);
-        if (kp > 16) mma_elect(d, da + 2, db + 2, idesc, 1u);
-        if (kp > 32) {
-            mma_elect(d, da + 4, db + 4, idesc, 1u);
-            mma_elect(d, da + 6, db + 6, idesc, 1u);
-        }
-        WG_TRACE(8, l, s);
-        commit_elect(&B.acc_full[s]);
-        WG_TRACE(9, l, s);
-    };
-    // the epilogue warps arrive (and move on); the MMA warp waits for all 160 and issues
-    auto handoff = [&](int s) {
-        const int id = 1 + 2 * g + s;
-        if (mma_warp) asm volatile("bar.sync %0, 160;" ::"r"(id) : "memory");
-        else asm volatile("bar.arrive %0, 160;" ::"r"(id) : "memory");
-    };
-    uint32_t a0_ph[2] = {0, 0}, acc_ph[2] = {0, 0};
-    if (issuer)
-        for (int k = 0; k < 2 && k < n_wg; ++k) load_a0(k, k);
-    if (mma_warp) {
-        for (int k = 0; k < 2 && k < n_wg; ++k) {
-            mbar_wait(&B.a0_full[k], a0_ph[k]);
-            a0_ph[k] ^= 1u;
-            issue(0, k);
-        }
-        for (int k = 0; k < n_wg; k += 2)
-            for (int l = 0; l < L; ++l)
-                for (int s = 0; s < 2; ++s) {
-                    const int kk = k + s;
-                    if (kk >= n_wg) continue;
-                    handoff(s);   // epilogue of (kk, l) finished: A1 written / accumulator drained
-                    WG_TRACE(4, l, s);
-                    if (l < L - 1) {
-                        issue(l + 1, s);
-                    } else if (kk + 2 < n_wg) {
-                        mbar_wait(&B.a0_full[s], a0_ph[s]);
-                        a0_ph[s] ^= 1u;
-                        issue(0, s);
-                    }
-                    WG_TRACE(5, l, s);
-                }
-    } else {
-    const __half2 al2 = __float2half2_rn(net.alpha);
-    const RowSw<HID> sw(row);
-    for (int k = 0; k < n_wg; k += 2) {
-        for (int l = 0; l < L; ++l) {
-            for (int s = 0; s < 2; ++s) {
-                const int kk = k + s;
-                if (kk >= n_wg) continue;
-                WG_TRACE(1, l, s);
-                mbar_wait(&B.acc_full[s], acc_ph[s]);
-                acc_ph[s] ^= 1u;
-                tc_after();
-                WG_TRACE(2, l, s);
-                if (l == 0 && issuer && kk + 2 < n_wg) load_a0(kk + 2, s);   // layer 0 has read this A0
-                const uint32_t t_acc = acc_of(s) + lane_base;
-                if (l < L - 1) {
-                    uint32_t r[HID];
-#pragma unroll
-                    for (int c = 0; c < HID; c += 16) tld16_nowait(t_acc + (uint32_t)c, r + c);
-                    tld_wait();
-                    uint8_t* a1 = a1_of(s);
-                    const uint4* bias = reinterpret_cast<const uint4*>(s_bh + l * HID);
-#pragma unroll
-                    for (int c = 0; c < HID / 8; ++c)
-                        *reinterpret_cast<uint4*>(a1 + sw.chunk(c)) = bias_leaky8(r + 8 * c, bias[c], al2);
-                    fence_async();
-                    tc_before();
-                    WG_TRACE(3, l, s);
-                    handoff(s);
-                } else {
-                    uint32_t r[OUT];
-#pragma unroll
-                    for (int c = 0; c < OUT; c += 16) tld16_nowait(t_acc + (uint32_t)c, r + c);
-                    tld_wait();
-                    tc_before();
-                    WG_TRACE(3, l, s);
-                    handoff(s);   // the accumulator is drained: the next tile may overwrite it
-                    const int64_t p = (t0 + (int64_t)kk * tstep) * kT + row;
-                    if (p < P) {
-                        __half* vrow = vis16 + p * vstride;
-                        const float4* bo = reinterpret_cast<const float4*>(s_bo);
-                        const __half2 lo = __float2half2_rn(1e-6f), hi = __float2half2_rn(0.999999f);
-#pragma unroll
-                        for (int c = 0; c < OUT / 8; ++c) {
-                            __align__(16) __half2 h[4];
-#pragma unroll
-                            for (int e = 0; e < 2; ++e) {
-                                const float4 b4 = bo[2 * c + e];
-                                const float* r4 = reinterpret_cast<const float*>(r + 8 * c + 4 * e);
-                                float o[4];
-                                const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-                                for (int t = 0; t < 4; ++t) {
-                                    if (net.out_sigmoid) {   // sigmoid(z) = 0.5 + 0.5 tanh(z / 2)
-                                        o[t] = fmaf(0.5f, tanh_fast(fmaf(r4[t], 0.5f, bv[t])), 0.5f);
-                                    } else {
-                                        const float zz = fmaf(2.0f, bv[t], r4[t]);
-                                        o[t] = zz >= 0.0f ? zz : net.alpha * zz;
-                                    }
-                                }
-                                h[2 * e] = __floats2half2_rn(o[0], o[1]);
-                                h[2 * e + 1] = __floats2half2_rn(o[2], o[3]);
-                                if (net.out_sigmoid) {   // clip [1e-6, 1-1e-6] (mlp.py:135-136) in fp16
-                                    h[2 * e] = __hmin2(__hmax2(h[2 * e], lo), hi);
-                                    h[2 * e + 1] = __hmin2(__hmax2(h[2 * e + 1], lo), hi);
-                                }
-                            }
-                            // padded columns (>= K, zero weights) land in the row's padding
-                            if (8 * c < vstride) *reinterpret_cast<uint4*>(vrow + 8 * c) = *reinterpret_cast<const uint4*>(h);
-                        }
-                    }
-                }
-            }
-        }
-    }
-    }   // epilogue warps
-#ifdef NVC_TRACE
-    if (blockIdx.x == 0 && trace_me) atomicMax(&g_wg_trace_n, trace_n);
-#endif
-    tc_before();
-    __syncthreads();
-    tc_after();
-    if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
-}
-
 // ---------------------------------------------------------------------------
 // stage 2 (default for widths <= 64): activations stay in tensor memory
 //
-// The SS-mode kernel above re-reads every hidden activation tile from shared
-// memory for each MMA and writes it there in each epilogue; with K = 64 layers
-// that smem traffic (A 4 KB + B 2 KB per 128x64x16 MMA, plus the epilogue
-// stores) saturates the shared-memory pipe.  Here each warpgroup keeps its
+// An SS-mode MLP (both operands in shared memory; k_mlp_tiles below for wide
+// nets) re-reads every hidden activation tile from shared memory for each MMA
+// and writes it there in each epilogue; with K = 64 layers that smem traffic
+// (A 4 KB + B 2 KB per 128x64x16 MMA, plus the epilogue stores) saturates the
+// shared-memory pipe.  Here each warpgroup keeps its
 // tile's activations in TMEM: the epilogue drains the fp32 accumulator
 // (tcgen05.ld), applies leaky-ReLU in packed half2 and writes the fp16 result
 // back with tcgen05.st into a 32-column A region, and the next layer's MMA
@@ -1303,18 +1039,13 @@ int make_mnet(const nvc_model* m, MNet& q) {
 
 inline int grid1(int64_t n, int bs) { return (int)((n + bs - 1) / bs); }
 
-template <int HID, int OUT, int KP0>
-int launch_wg(const MNet& w, const nvc_model* m, const uint8_t* tiles, int64_t ntiles, int64_t P, __half* vis16,
-              int64_t vstride, int grid, cudaStream_t s) {
-    cudaFuncSetAttribute(k_mlp_wg<HID, OUT, KP0>, cudaFuncAttributeMaxDynamicSharedMemorySize, w.sm_total);
-    k_mlp_wg<HID, OUT, KP0><<<grid, kWgThreads, w.sm_total, s>>>(w, m->params, m->wpack, tiles, ntiles, P, vis16,
-                                                                 vstride);
-    return check_launch("k_mlp_wg");
-}
-
 // smem layout of k_mlp_ts: weights | 2 A0 tiles per warpgroup | ones tile | bias blocks
 bool ts_layout(MNet& q) {
     if (q.n_layers < 2 || q.n_layers > 8) return false;
+    for (int l = 0; l < q.n_layers - 1; ++l)   // uniform 64-wide hidden layers (TMEM sized for them)
+        if (q.np[l] != 64 || (l > 0 && q.kp[l] != 64)) return false;
+    const int o = q.np[q.n_layers - 1], k = q.kp[0];
+    if (!(o == 16 || o == 32 || o == 48 || o == 64) || !(k == 16 || k == 32 || k == 64)) return false;
     q.sm_w = 0;
     q.sm_a0 = (q.wpack_halfs * 2 + 1023) / 1024 * 1024;
     q.sm_a1 = q.sm_a0 + 2 * kTsWG * ((kT * q.kp[0] * 2 + 1023) / 1024 * 1024);   // ones tile
@@ -1342,43 +1073,6 @@ int launch_mlp_ts(const MNet& w, const nvc_model* m, const uint8_t* tiles, int64
 #undef NVC_TS
     set_error("k_mlp_ts: shape not instantiated");
     return NVC_ERR_UNSUPPORTED;
-}
-
-// instantiated shapes (hidden, output, input padded widths); others use k_mlp_tiles
-bool wg_supported(const MNet& w) {
-    const int h = w.np[0], o = w.np[w.n_layers - 1], k = w.kp[0];
-    return h == 64 && (o == 16 || o == 32 || o == 48 || o == 64) && (k == 16 || k == 32 || k == 64);
-}
-
-int launch_mlp_wg(const MNet& w, const nvc_model* m, const uint8_t* tiles, int64_t ntiles, int64_t P, __half* vis16,
-                  int64_t vstride, int grid, cudaStream_t s) {
-    const int o = w.np[w.n_layers - 1], k = w.kp[0];
-#define NVC_WG(O, K) \
-    if (o == O && k == K) return launch_wg<64, O, K>(w, m, tiles, ntiles, P, vis16, vstride, grid, s);
-    NVC_WG(16, 16) NVC_WG(16, 32) NVC_WG(16, 64) NVC_WG(32, 16) NVC_WG(32, 32) NVC_WG(32, 64)
-    NVC_WG(48, 16) NVC_WG(48, 32) NVC_WG(48, 64) NVC_WG(64, 16) NVC_WG(64, 32) NVC_WG(64, 64)
-#undef NVC_WG
-    set_error("k_mlp_wg: shape not instantiated");
-    return NVC_ERR_UNSUPPORTED;
-}
-
-// smem layout of k_mlp_wg (8 tiles in flight: 2 per warpgroup); false if the
-// net does not fit (accumulators wider than 64 columns or smem)
-bool wg_layout(const nvc_model* m, MNet& q) {
-    if (q.n_layers < 2) return false;
-    for (int l = 0; l < q.n_layers - 1; ++l)
-        if (q.np[l] != q.np[0] || (l > 0 && q.kp[l] != q.np[0])) return false;
-    if (q.np[q.n_layers - 1] > 64 || q.np[0] > 64 || q.kp[0] > 64) return false;
-    q.sm_w = 0;
-    q.sm_a0 = (q.wpack_halfs * 2 + 1023) / 1024 * 1024;
-    q.sm_a1 = q.sm_a0 + 2 * kWG * ((kT * q.kp[0] * 2 + 1023) / 1024 * 1024);
-    q.sm_bias = q.sm_a1 + 2 * kWG * ((kT * q.act_kp * 2 + 1023) / 1024 * 1024);
-    int nb = 0;
-    for (int l = 0; l < q.n_layers - 1; ++l) nb += q.np[l];
-    if (nb * 2 > 1024 || q.np[q.n_layers - 1] * 4 > 1024) return false;
-    q.sm_total = q.sm_bias + 1024 + q.np[q.n_layers - 1] * 4 + 1024;
-    (void)m;
-    return q.sm_total <= 227 * 1024;
 }
 
 cudaEvent_t g_stage_ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -1411,16 +1105,11 @@ int run_front(const nvc_model* m, const double* pos, int64_t P, uint8_t* tiles, 
     int dev = 0, sms = kNumSMs;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    MNet w = q;
     MNet t = q;
-    if (wg_layout(m, w) && wg_supported(w) && ts_layout(t) && !getenv("NVC_MLP_WG") && !getenv("NVC_MLP_QUADS")) {
+    if (ts_layout(t) && !getenv("NVC_MLP_QUADS")) {
         int grid = (int)std::min<int64_t>((ntiles + kTsWG - 1) / kTsWG, sms);
         if (const char* e = getenv("NVC_QUERY_GRID")) grid = max(1, min(grid, atoi(e)));
         rc = launch_mlp_ts(t, m, tiles, ntiles, P, vis16, vstride, grid, s);
-    } else if (wg_layout(m, w) && wg_supported(w) && !getenv("NVC_MLP_QUADS")) {
-        int grid = (int)std::min<int64_t>((ntiles + kWG - 1) / kWG, sms);
-        if (const char* e = getenv("NVC_QUERY_GRID")) grid = max(1, min(grid, atoi(e)));
-        rc = launch_mlp_wg(w, m, tiles, ntiles, P, vis16, vstride, grid, s);
     } else {
         cudaFuncSetAttribute(k_mlp_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, q.sm_total);
         int grid = (int)(ntiles < sms ? ntiles : sms);
@@ -1528,22 +1217,6 @@ int pipeline_query(const nvc_model* m, const nvc_scene* sc, const double* pos, i
 
 }  // namespace nvc
 
-#ifdef NVC_TRACE
-extern "C" int nvc_wg_trace(unsigned long long* host_out, int n, int reset) {
-    if (reset) {
-        unsigned z = 0;
-        cudaMemcpyToSymbol(nvc::g_wg_trace_n, &z, sizeof z);
-        static unsigned long long zeros[2 * nvc::kWG * 4096];
-        cudaMemcpyToSymbol(nvc::g_wg_trace, zeros, sizeof zeros);
-        return 0;
-    }
-    unsigned cnt = 0;   // entries per warpgroup row
-    cudaMemcpyFromSymbol(&cnt, nvc::g_wg_trace_n, sizeof cnt);
-    if (n < 2 * nvc::kWG * 4096) return 0;
-    cudaMemcpyFromSymbol(host_out, nvc::g_wg_trace, 2 * nvc::kWG * 4096 * sizeof(unsigned long long));
-    return (int)cnt;
-}
-#endif
 
 extern "C" int nvc_profile_stages(int32_t enable) {
     if (enable && !nvc::g_stage_ev[0])
