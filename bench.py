@@ -360,6 +360,15 @@ def gpu_arm(args) -> None:
             "k_mlp_ts": ("tensor", P * flop_px, k_ms[1]),                # 24,576 flop per pixel
             "k_nls32": ("hbm", P * (64 + 4 * K + 4 + 40), k_ms[2]),      # vis + lum + mask in, id/W/point out
         }
+        # encoder gathers vs the measured random-gather L2 rate over the same 67 MB table
+        # (profiles/r1_l2_gather_probe.txt, tools/l2_probe.py)
+        enc_gathers = P * LEVELS * 4 / (k_ms[0] * 1e-3) / 1e9
+        probe = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "r1_l2_gather_probe.txt")) as fh:
+                probe = max(float(l.split(":")[1].split("G")[0]) for l in fh if "G gathers/s" in l)
+        except Exception:
+            probe = None
         name = max(kern, key=lambda k: kern[k][2])
         bound, work, kms = kern[name]
         if bound == "tensor":
@@ -396,7 +405,10 @@ def gpu_arm(args) -> None:
                          "work_per_launch": work, "launch_ms": kms,
                          "all": {k: {"bound": v[0], "ms": v[2],
                                      "frac": (v[1] / (v[2] * 1e-3) / (1e12 * tflops if v[0] == "tensor" else 1e9 * hbm))}
-                                 for k, v in kern.items()}},
+                                 for k, v in kern.items()},
+                         "encoder_l2": {"gathers_G_per_s": enc_gathers, "payload_GBps": enc_gathers * 8,
+                                        "random_gather_probe_G_per_s": probe,
+                                        "vs_random_probe": (enc_gathers / probe) if probe else None}},
             "clocks": clk,
         }
         if world == 1 and not args.no_cpu_baseline:

@@ -178,3 +178,38 @@ extern "C" int nvc_encode_probe(const nvc_model* m, const double* pos, int64_t P
         g, reinterpret_cast<const __half2*>(m->table_h), pos, P, reinterpret_cast<__half2*>(feats));
     return nvc::check_launch("k_encode_probe");
 }
+
+// ---- achievable L2 gather bandwidth for the encoder's footprint: every lane
+// issues independent 8-byte loads at hashed positions of an L2-resident table
+// (the fp16 x-pair table, 67 MB at C2), 16 in flight per thread.  Payload and
+// sector bytes are reported by the caller from the load count.
+namespace nvc {
+namespace {
+__global__ void __launch_bounds__(256) k_l2_gather_probe(const uint2* __restrict__ table, uint32_t mask, int iters,
+                                                         unsigned long long* __restrict__ sink) {
+    uint32_t x = (blockIdx.x * blockDim.x + threadIdx.x) * 2654435761u + 12345u;
+    uint32_t acc = 0;
+    for (int i = 0; i < iters; ++i) {
+        uint2 v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            x = x * 1664525u + 1013904223u;
+            v[j] = __ldg(table + ((x >> 3) & mask));
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc ^= v[j].x ^ v[j].y;
+    }
+    if (acc == 0x9e3779b9u) sink[0] = acc;
+}
+}  // namespace
+}  // namespace nvc
+
+// loads = grid * 256 * iters * 16, each 8 bytes of payload and one 32-byte sector
+extern "C" int nvc_l2_gather_probe(const void* table, int64_t entries, int32_t grid, int32_t iters, void* sink,
+                                   void* stream) {
+    uint32_t mask = 1;
+    while ((int64_t)mask * 2 <= entries) mask *= 2;
+    nvc::k_l2_gather_probe<<<grid, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const uint2*>(table), mask - 1,
+                                                                   iters, (unsigned long long*)sink);
+    return nvc::check_launch("k_l2_gather_probe");
+}
