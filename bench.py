@@ -218,7 +218,7 @@ def gpu_arm(args) -> None:
     cfg = TrainFrameConfig(n_world=N_WORLD * world, n_screen=N_SCREEN * world, seed=0)
     # training batches are generated one frame ahead on a side stream (they depend on
     # the frame index only), overlapping the FP64 ray kernels with training + query
-    pipe = BatchPipeline(scene, cam, cfg, K, dev, rank, world)
+    pipe = BatchPipeline(scene, cam, cfg, K, dev, rank, world, cache=cache)
     out = (torch.empty(P, dtype=torch.int64, device=dev), torch.empty((P, 3), dtype=torch.float64, device=dev),
            torch.empty(P, dtype=torch.float64, device=dev))
 

@@ -134,12 +134,20 @@ class BatchPipeline:
     stream against the consumer.  One optimizer step per frame (cfg.steps == 1).
     """
 
-    def __init__(self, scene, camera, cfg: TrainFrameConfig, k: int, device, shard: int = 0, n_shards: int = 1):
+    def __init__(self, scene, camera, cfg: TrainFrameConfig, k: int, device, shard: int = 0, n_shards: int = 1,
+                 cache=None):
         import torch
+
+        from .cache import GradExchange
         if cfg.steps != 1:
             raise ValueError("BatchPipeline prefetches one batch per frame (cfg.steps == 1)")
         self.scene, self.camera, self.cfg, self.shard, self.n_shards = scene, camera, cfg, shard, n_shards
         self.bufs = [BatchBuffers(cfg.n_world, cfg.n_screen, k, device, n_shards) for _ in range(2)]
+        # data parallel: the entry list of the gradient exchange depends only on the
+        # batch positions, so it is built here too, off the critical path (one per buffer)
+        self.ex = None
+        if cache is not None and n_shards > 1 and not cache.compact:
+            self.ex = [GradExchange(cache, cfg.n_world + cfg.n_screen) for _ in range(2)]
         # the batch chain (screen rays -> compaction -> shadow rays) is latency-bound:
         # give it priority so it completes within the frame it overlaps
         self.side = torch.cuda.Stream(device, priority=int(os.environ.get("NVC_BATCH_PRIORITY", "-1")))
@@ -158,6 +166,8 @@ class BatchPipeline:
             self.side.wait_event(self.free[b])          # the previous frame on this buffer has trained
             gen_batch_device(self.scene, self.camera, self.bufs[b], self.cfg.seed, frame, 0, self.shard,
                              self.n_shards)
+            if self.ex is not None:
+                self.ex[b].index(self.bufs[b].pos, self.bufs[b].n_rows)
             self.ready[b].record(self.side)
         self.pending[b] = frame
 
@@ -172,6 +182,10 @@ class BatchPipeline:
         if self.early and self.pending[(frame + 1) % 2] != frame + 1:
             self._launch(frame + 1)
         return self.bufs[b]
+
+    def exchange_for(self, bufs: BatchBuffers):
+        """The GradExchange indexed for `bufs` (None if the pipeline does not build one)."""
+        return None if self.ex is None else self.ex[self.bufs.index(bufs)]
 
     def release(self, bufs: BatchBuffers, frame: int) -> None:
         """`bufs` is consumed; start frame+1's batch (it overlaps this frame's query)."""
@@ -213,13 +227,17 @@ def train_frame_device(scene, camera, cache, cfg: TrainFrameConfig, frame: int =
     for step in range(cfg.steps):
         if pipeline is None:
             gen_batch_device(scene, camera, bufs, cfg.seed, frame, step, shard, n_shards)
-        if comm is not None and not cache.compact:   # dense mode: list the global batch's entries
-            ex = cache.exchange(b_max)
-            ex.index(bufs.pos, bufs.n_rows)
+        ex = None
+        if comm is not None:
+            ex = pipeline.exchange_for(bufs) if pipeline is not None else None
+            if ex is None:
+                ex = cache.exchange(b_max)
+                if not cache.compact:    # dense mode: list the global batch's entries
+                    ex.index(bufs.pos, bufs.n_rows)
         cache.accumulate_grads(bufs.pos, bufs.tgt, b_max=b_max, b_dev=bufs.n_rows,
                                shard=shard, n_shards=n_shards, loss_out=bufs.loss)
-        if comm is not None:
-            cache.exchange(b_max).allreduce(comm, bufs.loss)
+        if ex is not None:
+            ex.allreduce(comm, bufs.loss)
         cache.apply_adam()
         loss = bufs.loss[1]
     if pipeline is not None:

@@ -466,6 +466,24 @@ class TestTraining:
         assert la == lb
         np.testing.assert_array_equal(a.params.cpu().numpy(), b.params.cpu().numpy())
 
+    def test_batch_pipeline_builds_the_exchange_index(self, pbox8):
+        """With data parallelism the pipeline lists the batch's table entries on its side stream:
+        identical to building the list inline from the same positions."""
+        from paper_2506_05930_b200 import GradExchange
+        from paper_2506_05930_b200.training import BatchPipeline
+        cfg = TrainFrameConfig(n_world=512, n_screen=512, seed=3)
+        c = self._c1(pbox8, seed=3)
+        pipe = BatchPipeline(pbox8, pbox8.camera, cfg, 8, DEV, shard=1, n_shards=2, cache=c)
+        for f in range(3):
+            bufs = pipe.take(f)
+            ex = pipe.exchange_for(bufs)
+            ref = GradExchange(c, cfg.n_world + cfg.n_screen)
+            ref.index(bufs.pos, bufs.n_rows)
+            n = int(ref.count.item())
+            assert n > 0 and int(ex.count.item()) == n
+            assert torch.equal(ex.idx[:n], ref.idx[:n])
+            pipe.release(bufs, f)
+
     def test_reference_determinism_config_loss(self, g_train):
         """levels=4, T=2^10, 64+64 batch, seed 5 (test_mlp.py:205-224): loss within 1e-4."""
         pen = {
