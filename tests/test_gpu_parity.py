@@ -181,9 +181,13 @@ class TestGeometry:
         tgt = compute_visibility_targets(pos, pbox8, R.stream(*key, R.TARGETS))
         np.testing.assert_array_equal(tgt.astype(np.uint8), g_train["c1_tgt"])
 
-    @pytest.mark.parametrize("shards", [1, 2, 3])
-    def test_boxes32_device_batch_bit_exact(self, boxes32, g_train, shards):
+    @pytest.mark.parametrize("shards,unsorted", [(1, False), (2, False), (3, False), (1, True), (2, True)])
+    def test_boxes32_device_batch_bit_exact(self, boxes32, g_train, shards, unsorted, monkeypatch):
+        """Batch positions and shadow-ray targets (Morton-bucketed warps, and the plain
+        row-per-warp kernel) are bit-identical to the reference, also per shard."""
         from paper_2506_05930_b200.training import BatchBuffers, gen_batch_device
+        if unsorted:
+            monkeypatch.setenv("NVC_TARGETS_UNSORTED", "1")
         pos_all, tgt_all = [], []
         for sh in range(shards):
             bufs = BatchBuffers(2048, 2048, 32, DEV, shards)
@@ -223,8 +227,12 @@ class TestSampling:
         np.testing.assert_array_equal(ids, g_samp["nls_ids_biased"])
         np.testing.assert_array_equal(big_w, g_samp["nls_W_biased"])
 
-    def test_fused_nls_equals_oracle_on_same_visibility(self, boxes32, g_samp, g_scenes):
-        """The fused kernel's WRS is bit-exact given its own (fp16-MLP) visibilities."""
+    @pytest.mark.parametrize("variant", ["default", "NVC_WRS_FORWARD", "NVC_ENC_F32", "NVC_MLP_QUADS"])
+    def test_fused_nls_equals_oracle_on_same_visibility(self, boxes32, g_samp, g_scenes, variant, monkeypatch):
+        """The query's WRS is bit-exact given its own (fp16-MLP) visibilities -- for the default
+        kernels and each alternative (generic reservoir, scalar encoder, SS-mode MLP)."""
+        if variant != "default":
+            monkeypatch.setenv(variant, "1")
         c = VisibilityCache(MODE_LIGHTS, 32, grid_cfg(boxes32, 16, 1 << 19), hidden_dims=(64, 64, 64))
         c.grid_params = (np.random.default_rng(0).standard_normal(c.grid_params.shape) * 0.5).astype(np.float32)
         ctx = PixelCtx(boxes32, g_samp["gb_position"], g_samp["gb_normal"], g_samp["gb_albedo"])
