@@ -419,6 +419,69 @@ def gpu_arm(args) -> None:
         dist.destroy_process_group()
 
 
+def ndi4k_arm(args) -> None:
+    """C3 (BASELINE.json configs[2]): Neural DI at 3840x2160 x 32 lights, screen-tile
+    sharded (rank r renders rows [r*H/N, (r+1)*H/N) of the frame, no communication).
+    One step = encoder + tcgen05 MLP + the FP64 Neural-DI sum over all of the
+    rank's pixels with the G-buffer and per-camera factor table resident."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_05930_b200 import MODE_LIGHTS, HashGridConfig, VisibilityCache
+    from paper_2506_05930_b200.render import gbuffer_device
+    from paper_2506_05930_b200.sampling import PixelCtx, neural_di_device
+    from paper_2506_05930_b200.scene import scene_from_dict
+    from paper_2506_05930_b200.scenes import boxes_scene
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    W4, H4 = 3840, 2160
+    scene = scene_from_dict(boxes_scene(32))
+    cam = scene.camera.resized(W4, H4)
+    rows = H4 // world
+    P = W4 * rows
+    pos, nrm, alb, _, _ = gbuffer_device(scene, cam, rank * P, P)
+    ctx = PixelCtx(scene, pos, nrm, alb)
+    ctx.factor_device()
+    ctx.mask_device("factor")
+    grid = HashGridConfig(levels=LEVELS, table_size=TABLE, features_per_level=FEATS, aabb_min=scene.aabb_min,
+                          aabb_max=scene.aabb_max)
+    cache = VisibilityCache(MODE_LIGHTS, K, grid, seed=0, hidden_dims=HIDDEN, device=dev)
+    out = torch.empty((P, 3), dtype=torch.float64, device=dev)
+    for _ in range(args.warmup):
+        neural_di_device(ctx, cache, out=out)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(args.steps):
+        neural_di_device(ctx, cache, out=out)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / args.steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms = float(t.item())
+    if rank == 0:
+        print(json.dumps({"metric": "neural DI queries/s at 3840x2160 x 32 lights (encode+MLP+NDI)",
+                          "value": P * world / (ms * 1e-3), "unit": "queries/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                          "scaling": "strong", "vs_baseline": None, "dtype": "fp16 MLP / fp64 NDI sum",
+                          "data": "synthetic (boxes_scene(32) fixture, random-init weights, seed 0)",
+                          "config": {"workload": f"C3: {W4}x{H4} boxes32 (K=32) Neural DI, {world} screen tiles",
+                                     "pixels_per_gpu": P}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def reference_arm(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -451,11 +514,15 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-sample", type=int, default=24576)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", choices=["c2", "ndi4k"], default="c2",
+                    help="c2: the headline online frame (default); ndi4k: C3 Neural DI at 4K")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         reference_arm(args)
+    elif args.workload == "ndi4k":
+        ndi4k_arm(args)
     else:
         gpu_arm(args)
 

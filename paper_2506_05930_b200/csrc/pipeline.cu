@@ -912,6 +912,67 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
     a.pts[3 * p + 2] = y[2];
 }
 
+// Neural DI for K <= 32 (sampling.py:215-218): rgb = (sum_k v_k * factor_k *
+// L_e[k]) * albedo / pi over the pixel's nonzero-factor lights, FP64 in
+// ascending light order.  Memory-bound on the light-major factor table, so a
+// warp loads it as 32 x 32 tiles -- one coalesced 128-byte row per light any of
+// its pixels needs -- into shared memory (odd row stride), next to the pixel's
+// fp16 visibility row.  f32 tables only; the f64 parity tables use k_wrs_tiles.
+constexpr int kNdiThreads = 128;
+__global__ void __launch_bounds__(kNdiThreads) k_ndi32(WArgs a, nvc_scene sc) {
+    __shared__ uint32_t s_vis[kNdiThreads * 17];
+    __shared__ float s_fac[kNdiThreads * 33];
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = p < a.P;
+    uint32_t* my = s_vis + threadIdx.x * 17;
+    float* mf = s_fac + threadIdx.x * 33;
+    uint32_t m = 0;
+    if (live) {
+        const uint4* vrow = reinterpret_cast<const uint4*>(a.vis16 + p * a.vstride);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (8 * i < a.K) {
+                const uint4 v = __ldg(vrow + i);
+                my[4 * i] = v.x;
+                my[4 * i + 1] = v.y;
+                my[4 * i + 2] = v.z;
+                my[4 * i + 3] = v.w;
+            }
+        m = a.nz_mask ? __ldg(a.nz_mask + p) : 0xffffffffu;
+        if (a.K < 32) m &= (1u << a.K) - 1u;
+    }
+    // the warp's factor tile: row k for every light any lane needs, 16 loads in flight
+    uint32_t wm = __reduce_or_sync(0xffffffffu, m);
+    const float* fp = reinterpret_cast<const float*>(a.lum) + p;
+    while (wm) {
+        int ks[16];
+        float t[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            ks[j] = wm ? __ffs(wm) - 1 : -1;
+            wm &= wm - 1;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) t[j] = (ks[j] >= 0 && live) ? __ldg(fp + (int64_t)ks[j] * a.stride) : 0.0f;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (ks[j] >= 0) mf[ks[j]] = t[j];
+    }
+    if (!live) return;
+    double rgb[3] = {0.0, 0.0, 0.0};
+    while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t pair = my[k >> 1];
+        const double vis = (double)__half2float(__ushort_as_half((unsigned short)((k & 1) ? (pair >> 16) : (pair & 0xffffu))));
+        const double wk = __dmul_rn(vis, (double)mf[k]);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) rgb[ch] = __dadd_rn(rgb[ch], __dmul_rn(wk, __ldg(sc.lt_radiance + 3 * k + ch)));
+    }
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) a.rgb[3 * p + ch] = __ddiv_rn(__dmul_rn(rgb[ch], a.albedo[3 * p + ch]), 3.141592653589793);
+}
+
 // generic K: forward reservoir over the nonzero lights (pixel-major visibilities)
 template <bool kNls>
 __global__ void __launch_bounds__(256) k_wrs_tiles(WArgs a, nvc_scene sc) {
@@ -1196,10 +1257,13 @@ int pipeline_select(const nvc_model* m, const nvc_scene* sc, int64_t P, int mode
             k_nls32<true><<<grid1(P, kWrsThreads), kWrsThreads, 0, s>>>(a, *sc);
         else
             k_nls32<false><<<grid1(P, kWrsThreads), kWrsThreads, 0, s>>>(a, *sc);
-    } else if (mode == 1)
+    } else if (mode == 1) {
         k_wrs_tiles<true><<<grid1(P, 256), 256, 0, s>>>(a, *sc);
-    else
+    } else if (K <= 32 && !lum_f64 && getenv("NVC_WRS_FORWARD") == nullptr) {
+        k_ndi32<<<grid1(P, kNdiThreads), kNdiThreads, 0, s>>>(a, *sc);
+    } else {
         k_wrs_tiles<false><<<grid1(P, 256), 256, 0, s>>>(a, *sc);
+    }
     const int rc = check_launch("k_wrs_tiles");
     stage_mark(3, s);
     return rc;

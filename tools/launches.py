@@ -29,8 +29,8 @@ if __name__ == "__main__":
         rows.append((sum(t) / len(t), k, len(t), (sum(rd) / len(rd)) if rd else None, (sum(wr) / len(wr)) if wr else None))
     rows.sort(reverse=True)
     for us, k, n, rd, wr in rows:
-        dram = f"  dram r {rd / 1e6:8.1f} MB  w {wr / 1e6:8.1f} MB" if rd is not None else ""
+        dram = (f"  dram r {rd / 1e6:8.1f} MB" + (f"  w {wr / 1e6:8.1f} MB" if wr is not None else "")) if rd is not None else ""
         print(f"{k:32s} n={n:3d} mean={us:9.1f} us{dram}")
     if len(sys.argv) > 2:   # write {kernel: dram bytes per launch} for bench.py's roofline.traffic
-        out = {k: int(rd + wr) for us, k, n, rd, wr in rows if rd is not None}
+        out = {k: int(rd + (wr or 0)) for us, k, n, rd, wr in rows if rd is not None}
         json.dump(out, open(sys.argv[2], "w"), indent=1, sort_keys=True)
