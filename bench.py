@@ -233,7 +233,8 @@ def gpu_arm(args) -> None:
 
     # the NLS selection of frame f runs on its own stream, overlapping frame f+1's
     # train step (it reads only the visibilities, luminances and scene)
-    sel_stream = torch.cuda.Stream(dev) if not os.environ.get("NVC_SELECT_INLINE") else None
+    sel_stream = (torch.cuda.Stream(dev, priority=int(os.environ.get("NVC_SELECT_PRIORITY", "0")))
+                  if not os.environ.get("NVC_SELECT_INLINE") else None)
 
     def frame_into(f, outs, timed_parts=None):
         if timed_parts is not None:

@@ -28,7 +28,7 @@ extern "C" {
 
 #define NVC_MAX_LEVELS 32
 #define NVC_MAX_LAYERS 8
-#define NVC_ABI_VERSION 4
+#define NVC_ABI_VERSION 5
 
 typedef enum {
     NVC_OK = 0,
@@ -94,6 +94,23 @@ typedef struct {
     const double *lt_normal;              /* (K, 3) */
     const double *lt_radiance;            /* (K, 3) */
     const double *lt_lumaw;               /* (K, 3) LUMA * radiance, precomputed by the host */
+    const double *lt_area;                /* (K) scene.py:189 (shade_batch's area term) */
+    /* Shadow-ray acceleration data, precomputed by the host (scene.py
+     * DeviceScene).  tri_plane (n_tris, 4) f32 in BVH order: unit normal and
+     * offset of each triangle's plane, or all zeros for a triangle that must
+     * never be culled (zero area or a sliver); tri_leaf (n_tris) the BVH leaf
+     * holding triangle k; node_parent (n_nodes) the parent node (-1 at the
+     * root).  With anyhit_bf set, any-hit queries test every triangle whose
+     * plane the segment reaches (f32 plane test with margin plane_margin *
+     * (R + |p0|inf + |p1|inf), R = plane_r) exactly, and accept a hit only if
+     * every BVH ancestor of its leaf passes the FP64 slab test -- the same
+     * answer as the reference's pruned BVH traversal. */
+    const float *tri_plane;
+    const int32_t *tri_leaf;
+    const int32_t *node_parent;
+    float plane_margin, plane_r;
+    int32_t anyhit_bf;
+    int32_t pad0;
     int64_t n_nodes, n_tris;
     int32_t n_lights, n_materials;
     double shadow_eps;                    /* geometry.py:221-223 */
@@ -250,6 +267,13 @@ int nvc_light_factors(const nvc_scene *sc, const double *pos, const double *nrm,
 /* visibility_batch (geometry.py:233-247): vis (n) f32 in {0,1}. */
 int nvc_visibility(const nvc_scene *sc, const double *x, const double *y, int64_t n,
                    float *vis, void *stream);
+/* shade_batch (render.py:220-246): one-shadow-ray estimate per row,
+ * rgb (n,3) f64 = albedo/pi * L_e[id] * G * V * (area) * W; rows with id < 0,
+ * id >= K or W <= 0 (and rows with G <= 0) are 0.  Bit-identical to the
+ * reference.  pos/nrm/alb/pts (n,3) f64, ids (n) i64, big_w (n) f64. */
+int nvc_shade(const nvc_scene *sc, const double *pos, const double *nrm, const double *alb,
+              const int64_t *ids, const double *pts, const double *big_w, int64_t n, double *rgb,
+              void *stream);
 /* intersect_scene_batch (geometry.py:191-207): t, original tri index (-1 miss). */
 int nvc_closest_hit(const nvc_scene *sc, const double *orig, const double *dir,
                     const double *t_min, const double *t_max, int64_t n,

@@ -451,8 +451,9 @@ class SceneArrays:
     """The packed scene the reference's Scene carries (scene.py:158-215)."""
 
     def __init__(self, v0, v1, v2, tri_material, tri_light, lt_kind, lt_verts, lt_normal,
-                 lt_radiance, mat_albedo, cam):
+                 lt_radiance, mat_albedo, cam, lt_area=None):
         self.v0, self.v1, self.v2 = v0, v1, v2
+        self.lt_area = None if lt_area is None else np.asarray(lt_area, np.float64)
         self.tri_material, self.tri_light = tri_material, tri_light
         self.lt_kind, self.lt_verts = lt_kind.astype(np.uint8), np.ascontiguousarray(lt_verts)
         self.lt_normal, self.lt_radiance = np.ascontiguousarray(lt_normal), lt_radiance
@@ -471,7 +472,8 @@ class SceneArrays:
     def from_golden(cls, z, prefix):
         g = lambda k: z[prefix + k]  # noqa: E731
         return cls(g("v0"), g("v1"), g("v2"), g("tri_material"), g("tri_light"), g("lt_kind"),
-                   g("lt_verts"), g("lt_normal"), g("lt_radiance"), g("mat_albedo"), g("cam"))
+                   g("lt_verts"), g("lt_normal"), g("lt_radiance"), g("mat_albedo"), g("cam"),
+                   lt_area=g("lt_area") if prefix + "lt_area" in z else None)
 
     def light_points(self, ids, u):                                   # scene.py:204-215
         safe = np.maximum(np.asarray(ids), 0)
@@ -634,3 +636,39 @@ def nls_sample(s: SceneArrays, vis: np.ndarray, lum: np.ndarray, key: int, offse
 
 def neural_di(s: SceneArrays, vis: np.ndarray, factor: np.ndarray, albedo: np.ndarray):
     return ((np.asarray(vis, np.float64) * factor) @ s.lt_radiance) * albedo / np.pi
+
+
+# ---------------------------------------------------------------------------
+# Shading pass 5: render.py:220-246
+# ---------------------------------------------------------------------------
+
+def _dot3(a, b):
+    """np.einsum("pc,pc->p") as numpy 2.3 evaluates it for c = 3: (a0 b0 + a2 b2) + a1 b1
+    (pinned by tests/golden/shade.npz, which the reference's own einsum produced)."""
+    return (a[:, 0] * b[:, 0] + a[:, 2] * b[:, 2]) + a[:, 1] * b[:, 1]
+
+
+def shade(s: SceneArrays, pos, nrm, alb, ids, pts, big_w):              # render.py:220-246
+    """One-shadow-ray estimate per row: albedo/pi * L_e * G * V * area * W."""
+    pos, nrm, alb, pts = (np.asarray(a, np.float64) for a in (pos, nrm, alb, pts))
+    ids, big_w = np.asarray(ids), np.asarray(big_w, np.float64)
+    n = pos.shape[0]
+    out = np.zeros((n, 3))
+    live = (ids >= 0) & (big_w > 0)
+    if not np.any(live):
+        return out
+    safe = np.maximum(ids, 0)
+    w = pts - pos
+    d2 = np.maximum(_dot3(w, w), 1e-24)
+    w = w / np.sqrt(d2)[:, None]
+    cos_x = np.maximum(0.0, _dot3(nrm, w))
+    cos_y = np.maximum(0.0, -_dot3(w, s.lt_normal[safe]))
+    geom = np.where(s.lt_kind[safe] == 0, cos_x * cos_y / d2 * s.lt_area[safe], cos_x / d2)
+    live &= geom > 0
+    if not np.any(live):
+        return out
+    vis = np.zeros(n)
+    vis[live] = s.visibility(pos[live], pts[live])
+    amp = geom * big_w * vis
+    out[live] = (alb[live] / np.pi) * s.lt_radiance[safe[live]] * amp[live, None]
+    return out

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libnvc.so")
 
 MAX_LEVELS = 32
 MAX_LAYERS = 8
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 c_i32, c_i64, c_u64, c_f64, c_f32, c_vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
                                            ctypes.c_double, ctypes.c_float, ctypes.c_void_p)
@@ -45,7 +45,9 @@ class NvcScene(ctypes.Structure):
         ("tv0", c_vp), ("tv1", c_vp), ("tv2", c_vp),
         ("tri_material", c_vp), ("tri_light", c_vp), ("mat_albedo", c_vp),
         ("lt_kind", c_vp), ("lt_verts", c_vp), ("lt_normal", c_vp), ("lt_radiance", c_vp),
-        ("lt_lumaw", c_vp),
+        ("lt_lumaw", c_vp), ("lt_area", c_vp),
+        ("tri_plane", c_vp), ("tri_leaf", c_vp), ("node_parent", c_vp),
+        ("plane_margin", ctypes.c_float), ("plane_r", ctypes.c_float), ("anyhit_bf", c_i32), ("pad0", c_i32),
         ("n_nodes", c_i64), ("n_tris", c_i64), ("n_lights", c_i32), ("n_materials", c_i32),
         ("shadow_eps", c_f64), ("aabb_min", c_f64 * 3), ("aabb_max", c_f64 * 3),
     ]
@@ -99,6 +101,7 @@ _SIGS = {
     "nvc_light_factors": (c_i32, [P(NvcScene), c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_vp,
                                   c_vp, c_vp]),
     "nvc_visibility": (c_i32, [P(NvcScene), c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "nvc_shade": (c_i32, [P(NvcScene), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "nvc_closest_hit": (c_i32, [P(NvcScene), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "nvc_batch_workspace_bytes": (c_i64, [c_i32, c_i32]),
     "nvc_targets": (c_i32, [P(NvcScene), c_u64, c_vp, c_i64, c_vp, c_vp]),

@@ -125,9 +125,57 @@ __device__ int64_t closest_hit(const nvc_scene& sc, const double o[3], const dou
     return best;
 }
 
+// Any-hit by plane culling (scenes with <= BF_MAX_TRIS triangles, nvc.h).
+// The reference's answer is "some triangle k passes ray_tri AND every BVH
+// ancestor of k's leaf passes the FP64 slab test" (its traversal tests exactly
+// those triangles, and any-hit does not depend on the order).  This evaluates
+// the same predicate triangle by triangle:
+//  1. f32 plane test: the segment [o + t_min d, o + t_max d] cannot meet k if
+//     both ends are farther than m on the same side of k's plane.  ray_tri can
+//     only accept a t in [t_min, t_max] whose point lies within
+//     ~1e-15 * sliver * (t + |o - a|) of the plane (sliver <= 2^20 on the
+//     host, else the plane is zero and never culls), and the f32 evaluation
+//     errs by < 2^-20 (R + |p|): m = 2^-15 (R + |p0| + |p1|) covers both 32x;
+//  2. exact FP64 ray_tri (the same function the traversal calls);
+//  3. on a hit only: the FP64 slab test of the leaf and each ancestor.
+// So the result is bit-identical to the traversal's, at ~12 f32 instructions
+// per culled triangle instead of a stack walk of FP64 slab tests.
+__device__ __forceinline__ bool chain_ok(const nvc_scene& sc, int32_t k, const double o[3],
+                                         const double inv[3], double t_max) {
+    for (int32_t n = __ldg(sc.tri_leaf + k); n >= 0; n = __ldg(sc.node_parent + n))
+        if (!aabb_hit(o, inv, sc.node_min + 3 * n, sc.node_max + 3 * n, t_max)) return false;
+    return true;
+}
+
+__device__ __forceinline__ float max_abs3(float a, float b, float c) {
+    return fmaxf(fabsf(a), fmaxf(fabsf(b), fabsf(c)));
+}
+
+__device__ bool any_hit_bf(const nvc_scene& sc, const double o[3], const double d[3], double t_min,
+                           double t_max) {
+    const float a0 = (float)(o[0] + t_min * d[0]), a1 = (float)(o[1] + t_min * d[1]),
+                a2 = (float)(o[2] + t_min * d[2]);
+    const float b0 = (float)(o[0] + t_max * d[0]), b1 = (float)(o[1] + t_max * d[1]),
+                b2 = (float)(o[2] + t_max * d[2]);
+    const float m = sc.plane_margin * ((sc.plane_r + max_abs3(a0, a1, a2)) + max_abs3(b0, b1, b2)) + 1e-30f;
+    const float4* pl = reinterpret_cast<const float4*>(sc.tri_plane);
+    for (int32_t k = 0; k < (int32_t)sc.n_tris; ++k) {
+        const float4 q = __ldg(pl + k);
+        const float s0 = fmaf(q.x, a0, fmaf(q.y, a1, fmaf(q.z, a2, -q.w)));
+        const float s1 = fmaf(q.x, b0, fmaf(q.y, b1, fmaf(q.z, b2, -q.w)));
+        if (fminf(s0, s1) > m || fmaxf(s0, s1) < -m) continue;
+        if (ray_tri(o, d, sc.bv0 + 3 * k, sc.bv1 + 3 * k, sc.bv2 + 3 * k, t_min, t_max) >= 0.0) {
+            const double inv[3] = {inv_dir(d[0]), inv_dir(d[1]), inv_dir(d[2])};
+            if (chain_ok(sc, k, o, inv, t_max)) return true;
+        }
+    }
+    return false;
+}
+
 __device__ bool any_hit(const nvc_scene& sc, const double o[3], const double d[3], double t_min,
                         double t_max) {
     if (sc.n_tris == 0) return false;
+    if (sc.anyhit_bf) return any_hit_bf(sc, o, d, t_min, t_max);
     const double inv[3] = {inv_dir(d[0]), inv_dir(d[1]), inv_dir(d[2])};
     int32_t stack[kStack];
     int top = 0;
@@ -320,6 +368,52 @@ __global__ void k_visibility(nvc_scene sc, const double* __restrict__ x, const d
     vis[i] = segment_visible(sc, a, b);
 }
 
+// ---- shading pass 5: shade_batch (render.py:220-246) --------------------------
+// np.einsum("pc,pc->p") over c = 3 sums (a0 b0 + a2 b2) + a1 b1 (pinned by
+// tests/golden/shade.npz); np.maximum(0, x) keeps NaN and maps -0 to +0.
+__device__ __forceinline__ double dot3e(const double a[3], const double b[3]) {
+    return (a[0] * b[0] + a[2] * b[2]) + a[1] * b[1];
+}
+__device__ __forceinline__ double max0(double x) { return 0.0 >= x ? 0.0 : x; }
+
+__global__ void __launch_bounds__(128) k_shade(nvc_scene sc, const double* __restrict__ pos,
+                                               const double* __restrict__ nrm, const double* __restrict__ alb,
+                                               const int64_t* __restrict__ ids, const double* __restrict__ pts,
+                                               const double* __restrict__ big_w, int64_t n,
+                                               double* __restrict__ rgb) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t id = ids[i];
+    const double W = big_w[i];
+    double out[3] = {0.0, 0.0, 0.0};
+    if (id >= 0 && id < sc.n_lights && W > 0.0) {
+        const double x[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+        const double y[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+        const double nx[3] = {nrm[3 * i], nrm[3 * i + 1], nrm[3 * i + 2]};
+        double w[3] = {y[0] - x[0], y[1] - x[1], y[2] - x[2]};
+        double d2 = dot3e(w, w);
+        d2 = d2 < 1e-24 ? 1e-24 : d2;
+        const double r = sqrt(d2);
+        w[0] = w[0] / r;
+        w[1] = w[1] / r;
+        w[2] = w[2] / r;
+        const double ln[3] = {__ldg(sc.lt_normal + 3 * id), __ldg(sc.lt_normal + 3 * id + 1),
+                              __ldg(sc.lt_normal + 3 * id + 2)};
+        const double cos_x = max0(dot3e(nx, w));
+        const double cos_y = max0(-dot3e(w, ln));
+        const double geom = __ldg(sc.lt_kind + id) == 0 ? cos_x * cos_y / d2 * __ldg(sc.lt_area + id) : cos_x / d2;
+        if (geom > 0.0) {
+            const double amp = geom * W * (double)segment_visible(sc, x, y);
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                out[c] = alb[3 * i + c] / 3.141592653589793 * __ldg(sc.lt_radiance + 3 * id + c) * amp;
+        }
+    }
+    rgb[3 * i] = out[0];
+    rgb[3 * i + 1] = out[1];
+    rgb[3 * i + 2] = out[2];
+}
+
 __global__ void k_closest(nvc_scene sc, const double* __restrict__ o, const double* __restrict__ d,
                           const double* __restrict__ t_min, const double* __restrict__ t_max, int64_t n,
                           double* __restrict__ t_out, int64_t* __restrict__ tri_out) {
@@ -448,6 +542,7 @@ __device__ uint32_t any_hit_packet(const nvc_scene& sc, const double o[3], const
     uint32_t hit = 0u;
     const uint32_t act = __ballot_sync(0xffffffffu, active);
     if (sc.n_tris == 0 || act == 0u) return 0u;
+    if (sc.anyhit_bf) return __ballot_sync(0xffffffffu, active && any_hit_bf(sc, o, d, t_min, t_max));
     const double inv[3] = {inv_dir(d[0]), inv_dir(d[1]), inv_dir(d[2])};
     int top = 0;
     if (lane == 0) {
@@ -680,6 +775,15 @@ int nvc_visibility(const nvc_scene* sc, const double* x, const double* y, int64_
     if (n <= 0) return NVC_OK;
     k_visibility<<<grid1(n, 128), 128, 0, (cudaStream_t)stream>>>(*sc, x, y, n, vis);
     return check_launch("k_visibility");
+}
+
+int nvc_shade(const nvc_scene* sc, const double* pos, const double* nrm, const double* alb, const int64_t* ids,
+              const double* pts, const double* big_w, int64_t n, double* rgb, void* stream) {
+    NVC_REQUIRE(sc && pos && nrm && alb && ids && pts && big_w && rgb, "nvc_shade: null argument");
+    NVC_REQUIRE(sc->lt_area, "nvc_shade: scene without lt_area");
+    if (n <= 0) return NVC_OK;
+    k_shade<<<grid1(n, 128), 128, 0, (cudaStream_t)stream>>>(*sc, pos, nrm, alb, ids, pts, big_w, n, rgb);
+    return check_launch("k_shade");
 }
 
 int nvc_closest_hit(const nvc_scene* sc, const double* o, const double* d, const double* t_min,

@@ -80,3 +80,49 @@ def gbuffer_and_ctx(scene, camera=None, table_dtype=np.float32):
         ctx.hit, ctx.light_id = hit, lid
         memo[key] = ctx
     return memo[key]
+
+
+# ---------------------------------------------------------------------------
+# Shading pass 5 (render.py:220-246): one shadow ray per pixel
+# ---------------------------------------------------------------------------
+
+def shade_device(scene, positions, normals, albedos, ids, points, big_w, out=None):
+    """``shade_batch`` on CUDA tensors (pos/nrm/alb/points (n,3) f64, ids (n) i64,
+    big_w (n) f64, all on the scene's device): rgb (n,3) f64, bit-identical to the
+    reference.  Launches ``k_shade`` on the current stream, no host sync."""
+    import torch
+    ds = device_scene(scene, positions.device)
+    n = positions.shape[0]
+    if out is None:
+        out = torch.empty((n, 3), dtype=torch.float64, device=positions.device)
+    args = [t.contiguous() for t in (positions, normals, albedos, ids, points, big_w)]
+    if args[3].dtype != torch.int64 or any(a.dtype != torch.float64 for i, a in enumerate(args) if i != 3):
+        raise TypeError("shade_device: f64 positions/normals/albedos/points/big_w and int64 ids expected")
+    _lib.call("nvc_shade", ds.struct, *(a.data_ptr() for a in args), n, out.data_ptr(), _lib.stream_ptr())
+    return out
+
+
+def shade_batch(scene, positions, normals, albedos, ids, points, big_w):
+    """One-shadow-ray area-measure estimate per row:
+    albedo/pi * L_e * G * V * area * W (point lights drop the area term).
+
+    Same signature and result as the reference's ``shade_batch``; numpy in ->
+    numpy out (via the device), CUDA tensors in -> CUDA tensor out."""
+    torch = _lib.require_cuda()
+    if isinstance(positions, torch.Tensor) and positions.is_cuda:
+        return shade_device(scene, positions, normals, albedos, ids, points, big_w)
+    dev = device_scene(scene).device
+    f64 = lambda a: torch.from_numpy(np.ascontiguousarray(np.atleast_2d(a), np.float64)).to(dev)  # noqa: E731
+    ids_t = torch.from_numpy(np.ascontiguousarray(np.atleast_1d(ids), np.int64)).to(dev)
+    w_t = torch.from_numpy(np.ascontiguousarray(np.atleast_1d(big_w), np.float64)).to(dev)
+    out = shade_device(scene, f64(positions), f64(normals), f64(albedos), ids_t, f64(points), w_t)
+    return out.cpu().numpy()
+
+
+def shade_pixel(sp, light_sample, scene) -> np.ndarray:
+    """Scalar shading of one (light id, point, W) sample (render.py:249-256)."""
+    lid, point, big_w = light_sample
+    if big_w < 0:
+        raise ValueError("contribution weight must be nonnegative")
+    return shade_batch(scene, np.asarray(sp.position)[None], np.asarray(sp.normal)[None],
+                       np.asarray(sp.albedo)[None], np.array([lid]), np.atleast_2d(point), np.array([big_w]))[0]

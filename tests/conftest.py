@@ -46,3 +46,8 @@ def g_samp():
 @pytest.fixture(scope="session")
 def g_train():
     return golden("training")
+
+
+@pytest.fixture(scope="session")
+def g_shade():
+    return golden("shade")

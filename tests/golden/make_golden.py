@@ -30,7 +30,7 @@ from viscache.hashgrid import (HashGridConfig, _level_lookup, _normalize,  # noq
                                encode_batch, grad_from_ctx, init_params)
 from viscache.mlp import (AdamState, MLPConfig, adam_step, backward_l2,  # noqa: E402
                           forward, he_init, l2_loss)
-from viscache.render import make_gbuffer  # noqa: E402
+from viscache.render import make_gbuffer, shade_batch  # noqa: E402
 from viscache.sampling import (PixelCtx, neural_di_batch, nls_sample_batch,  # noqa: E402
                                wrs_select_batch)
 from viscache.scene import Camera, scene_from_dict  # noqa: E402
@@ -234,6 +234,39 @@ def gen_sampling(out: dict) -> None:
     out["pgb_factor"] = ctxp.factor_matrix()
 
 
+def gen_shade(out: dict) -> None:
+    """render.py:220-246 (shade_batch) on a boxes32 G-buffer with random
+    (id, point, W) samples -- ids include -1, W includes 0 -- on the C1
+    point-light G-buffer, and on the NLS samples of gen_sampling's fixture."""
+    g = R.stream(3, "golden-shade")
+    s = scene_from_dict(boxes_scene(32))
+    cam = Camera(position=s.camera.position, look_at=s.camera.look_at, up=s.camera.up,
+                 fov_deg=s.camera.fov_deg, width=64, height=40)
+    gb = make_gbuffer(s, cam)
+    pos, nrm, alb = gb.flat("position"), gb.flat("normal"), gb.flat("albedo")
+    n = pos.shape[0]
+    ids = g.integers(-1, s.n_lights, size=n)
+    pts = s.light_points(np.maximum(ids, 0), g.random((n, 2)))
+    big_w = g.random(n) * 40.0 * (g.random(n) < 0.9)
+    out["b32_position"], out["b32_normal"], out["b32_albedo"] = pos, nrm, alb
+    out["b32_ids"], out["b32_pts"], out["b32_W"] = ids, pts, big_w
+    out["b32_rgb"] = shade_batch(s, pos, nrm, alb, ids, pts, big_w)
+
+    sp = scene_from_dict(point_light_dict(8))
+    gbp = make_gbuffer(sp)
+    pos, nrm, alb = gbp.flat("position"), gbp.flat("normal"), gbp.flat("albedo")
+    n = pos.shape[0]
+    ids = g.integers(-1, sp.n_lights, size=n)
+    pts = sp.light_points(np.maximum(ids, 0), g.random((n, 2)))
+    big_w = g.random(n) * 8.0
+    out["p8_ids"], out["p8_pts"], out["p8_W"] = ids, pts, big_w
+    out["p8_rgb"] = shade_batch(sp, pos, nrm, alb, ids, pts, big_w)
+
+    smp = np.load(os.path.join(HERE, "sampling.npz"))
+    out["nls_rgb"] = shade_batch(s, smp["gb_position"], smp["gb_normal"], smp["gb_albedo"], smp["nls_ids"],
+                                 smp["nls_pts"], smp["nls_W"])
+
+
 def gen_training(out: dict) -> None:
     s8 = scene_from_dict(boxes_scene(8))
     pts = gen_screen_samples(s8, s8.camera, 256, R.stream(6))
@@ -336,8 +369,16 @@ def main() -> None:
     quick = "--quick" in sys.argv
     groups = {
         "rng": gen_rng, "scenes": gen_scenes, "mlp": gen_mlp,
-        "sampling": gen_sampling, "training": gen_training,
+        "sampling": gen_sampling, "training": gen_training, "shade": gen_shade,
     }
+    only = [a for a in sys.argv[1:] if not a.startswith("-")]
+    if only:   # regenerate just the named groups, e.g. `make_golden.py shade`
+        for name in only:
+            out = {}
+            groups[name](out)
+            np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
+            print("wrote", name)
+        return
     for name, fn in groups.items():
         out: dict = {}
         fn(out)

@@ -181,13 +181,18 @@ class TestGeometry:
         tgt = compute_visibility_targets(pos, pbox8, R.stream(*key, R.TARGETS))
         np.testing.assert_array_equal(tgt.astype(np.uint8), g_train["c1_tgt"])
 
-    @pytest.mark.parametrize("shards,unsorted", [(1, False), (2, False), (3, False), (1, True), (2, True)])
-    def test_boxes32_device_batch_bit_exact(self, boxes32, g_train, shards, unsorted, monkeypatch):
+    @pytest.mark.parametrize("shards,unsorted,anyhit", [(1, False, "auto"), (2, False, "auto"), (3, False, "auto"),
+                                                        (1, True, "auto"), (2, True, "auto"), (1, False, "bvh"),
+                                                        (1, True, "bvh")])
+    def test_boxes32_device_batch_bit_exact(self, g_train, shards, unsorted, anyhit, monkeypatch):
         """Batch positions and shadow-ray targets (Morton-bucketed warps, and the plain
-        row-per-warp kernel) are bit-identical to the reference, also per shard."""
+        row-per-warp kernel; plane-culled any-hit and the packet BVH traversal) are
+        bit-identical to the reference, also per shard."""
         from paper_2506_05930_b200.training import BatchBuffers, gen_batch_device
         if unsorted:
             monkeypatch.setenv("NVC_TARGETS_UNSORTED", "1")
+        monkeypatch.setenv("NVC_ANYHIT", anyhit)
+        boxes32 = scene_from_dict(boxes_scene(32))       # fresh DeviceScene picks up NVC_ANYHIT
         pos_all, tgt_all = [], []
         for sh in range(shards):
             bufs = BatchBuffers(2048, 2048, 32, DEV, shards)
@@ -198,6 +203,89 @@ class TestGeometry:
             tgt_all.append(bufs.tgt[:hi - lo].cpu().numpy())
         np.testing.assert_array_equal(pos_all[0], g_train["b32_pos"])
         np.testing.assert_array_equal(np.concatenate(tgt_all).astype(np.uint8), g_train["b32_tgt"])
+
+
+# ---------------------------------------------------------------------------
+# any-hit strategies + shading pass 5 (render.py:220-246)
+# ---------------------------------------------------------------------------
+def _scene_with(name_fn, anyhit, monkeypatch):
+    monkeypatch.setenv("NVC_ANYHIT", anyhit)
+    return scene_from_dict(name_fn())
+
+
+def _visibility(scene, x, y):
+    from paper_2506_05930_b200.scene import device_scene
+    ds = device_scene(scene, DEV)
+    xt, yt = (torch.from_numpy(np.ascontiguousarray(a)).to(DEV) for a in (x, y))
+    vis = torch.empty(x.shape[0], dtype=torch.float32, device=DEV)
+    _lib.call("nvc_visibility", ds.struct, xt.data_ptr(), yt.data_ptr(), x.shape[0], vis.data_ptr(),
+              _lib.stream_ptr())
+    return vis.cpu().numpy()
+
+
+class TestShade:
+    @pytest.mark.parametrize("anyhit", ["bf", "bvh"])
+    def test_golden_boxes32(self, g_shade, anyhit, monkeypatch):
+        from paper_2506_05930_b200.render import shade_batch
+        s = _scene_with(lambda: boxes_scene(32), anyhit, monkeypatch)
+        z = g_shade
+        rgb = shade_batch(s, z["b32_position"], z["b32_normal"], z["b32_albedo"], z["b32_ids"], z["b32_pts"],
+                          z["b32_W"])
+        np.testing.assert_array_equal(rgb, z["b32_rgb"])
+
+    def test_golden_point_lights_and_nls_chain(self, pbox8, boxes32, g_samp, g_shade):
+        from paper_2506_05930_b200.render import shade_batch, shade_pixel
+        from paper_2506_05930_b200.sampling import ShadingPoint
+        z = g_shade
+        rgb = shade_batch(pbox8, g_samp["pgb_position"], g_samp["pgb_normal"], g_samp["pgb_albedo"], z["p8_ids"],
+                          z["p8_pts"], z["p8_W"])
+        np.testing.assert_array_equal(rgb, z["p8_rgb"])
+        rgb = shade_batch(boxes32, g_samp["gb_position"], g_samp["gb_normal"], g_samp["gb_albedo"],
+                          g_samp["nls_ids"], g_samp["nls_pts"], g_samp["nls_W"])
+        np.testing.assert_array_equal(rgb, z["nls_rgb"])
+        i = int(np.argmax(np.abs(z["nls_rgb"]).sum(axis=1)))
+        sp = ShadingPoint(g_samp["gb_position"][i], g_samp["gb_normal"][i], g_samp["gb_albedo"][i])
+        one = shade_pixel(sp, (int(g_samp["nls_ids"][i]), g_samp["nls_pts"][i], float(g_samp["nls_W"][i])), boxes32)
+        np.testing.assert_array_equal(one, z["nls_rgb"][i])
+        with pytest.raises(ValueError):
+            shade_pixel(sp, (0, g_samp["nls_pts"][i], -1.0), boxes32)
+
+    @pytest.mark.parametrize("anyhit", ["bf", "bvh"])
+    def test_large_random_vs_oracle(self, g_scenes, anyhit, monkeypatch):
+        """200k G-buffer rows (320x...) with random (id, point, W), ids in [-1, K]."""
+        from paper_2506_05930_b200.render import gbuffer_device, shade_device
+        s = _scene_with(lambda: boxes_scene(32), anyhit, monkeypatch)
+        cam = s.camera.resized(480, 416)
+        pos, nrm, alb, _, _ = gbuffer_device(s, cam, device=DEV)
+        n = pos.shape[0]
+        g = np.random.default_rng(7)
+        ids = g.integers(-1, 33, size=n)                 # K = 32 -> id 32 is out of range: row is 0
+        u = g.random((n, 2))
+        o = O.SceneArrays.from_golden(g_scenes, "boxes32_")
+        pts = o.light_points(np.minimum(np.maximum(ids, 0), 31), u)
+        big_w = g.random(n) * 30.0 * (g.random(n) < 0.95)
+        rgb = shade_device(s, pos, nrm, alb, torch.from_numpy(ids).to(DEV), torch.from_numpy(pts).to(DEV),
+                           torch.from_numpy(big_w).to(DEV)).cpu().numpy()
+        ids_o = np.where(ids >= 32, -1, ids)
+        want = O.shade(o, pos.cpu().numpy(), nrm.cpu().numpy(), alb.cpu().numpy(), ids_o, pts, big_w)
+        np.testing.assert_array_equal(rgb, want)
+        assert (rgb != 0).any(axis=1).sum() > n // 10
+
+    @pytest.mark.parametrize("scene_fn", [lambda: boxes_scene(32), lambda: boxes_point_scene(8)])
+    def test_plane_culling_equals_bvh_traversal(self, scene_fn, monkeypatch):
+        """1M random segments inside (and beyond) the scene box, plus segments between
+        surface points: the plane-culled any-hit and the BVH traversal agree bitwise."""
+        bf = _scene_with(scene_fn, "bf", monkeypatch)
+        bvh = _scene_with(scene_fn, "bvh", monkeypatch)
+        g = np.random.default_rng(3)
+        lo, hi = bf.aabb_min - 0.5, bf.aabb_max + 0.5
+        x = g.uniform(lo, hi, (1 << 20, 3))
+        y = g.uniform(lo, hi, (1 << 20, 3))
+        y[::7] = x[::7] + 1e-5 * g.standard_normal((y[::7].shape[0], 3))     # short / degenerate segments
+        a = _visibility(bf, x, y)
+        b = _visibility(bvh, x, y)
+        np.testing.assert_array_equal(a, b)
+        assert 0.05 < a.mean() < 0.95
 
 
 # ---------------------------------------------------------------------------

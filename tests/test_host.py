@@ -127,15 +127,41 @@ def test_library_exports_every_symbol():
 def test_struct_layouts_match_c(tmp_path):
     src = tmp_path / "sz.c"
     src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "nvc.h"\nint main(void){'
-                   'printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(nvc_model), sizeof(nvc_scene),'
+                   'printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(nvc_model), sizeof(nvc_scene),'
                    ' sizeof(nvc_camera), offsetof(nvc_model, params), offsetof(nvc_scene, shadow_eps),'
-                   ' offsetof(nvc_camera, width)); return 0; }\n')
+                   ' offsetof(nvc_camera, width), offsetof(nvc_scene, anyhit_bf)); return 0; }\n')
     exe = tmp_path / "sz"
     subprocess.check_call(["gcc", "-I", os.path.dirname(HEADER), str(src), "-o", str(exe)])
     got = list(map(int, subprocess.check_output([str(exe)]).split()))
     want = [ctypes.sizeof(_lib.NvcModel), ctypes.sizeof(_lib.NvcScene), ctypes.sizeof(_lib.NvcCamera),
-            _lib.NvcModel.params.offset, _lib.NvcScene.shadow_eps.offset, _lib.NvcCamera.width.offset]
+            _lib.NvcModel.params.offset, _lib.NvcScene.shadow_eps.offset, _lib.NvcCamera.width.offset,
+            _lib.NvcScene.anyhit_bf.offset]
     assert got == want
+
+
+@pytest.mark.parametrize("name", sorted(SCENES))
+def test_shadow_accel_tables(name):
+    """Per-triangle planes contain their triangle's vertices (to f32 rounding), every
+    triangle's leaf holds it, and parent links walk from every leaf to the root."""
+    from paper_2506_05930_b200.scene import shadow_accel
+    b = scene_from_dict(SCENES[name]()).bvh
+    plane, leaf, parent, r = shadow_accel(b)
+    assert plane.dtype == np.float32 and plane.shape == (b.v0.shape[0], 4)
+    live = np.abs(plane[:, :3]).sum(axis=1) > 0
+    assert live.mean() > 0.9
+    for v in (b.v0, b.v1, b.v2):
+        resid = (plane[live, :3].astype(np.float64) * v[live]).sum(axis=1) - plane[live, 3]
+        assert np.abs(resid).max() < 1e-5 * (1.0 + r)
+    np.testing.assert_allclose(np.linalg.norm(plane[live, :3], axis=1), 1.0, rtol=1e-6)
+    for k in range(b.v0.shape[0]):
+        n = leaf[k]
+        assert b.node_count[n] > 0 and b.node_start[n] <= k < b.node_start[n] + b.node_count[n]
+        depth = 0
+        while parent[n] >= 0:
+            assert n in (b.node_left[parent[n]], b.node_right[parent[n]])
+            n, depth = parent[n], depth + 1
+        assert n == 0 and depth < 64
+    assert r == max(np.abs(b.v0).max(), np.abs(b.v1).max(), np.abs(b.v2).max())
 
 
 def test_no_device_means_loud_failure():

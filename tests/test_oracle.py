@@ -221,6 +221,30 @@ class TestSampling:
         np.testing.assert_allclose(rgb, g_samp["ndi_rgb"], rtol=1e-12, atol=1e-300)
 
 
+class TestShade:
+    """Shading pass 5 (render.py:220-246) against the reference's shade_batch."""
+
+    def test_boxes32_random_samples(self, g_scenes, g_shade):
+        s = scene(g_scenes, "boxes32")
+        z = g_shade
+        rgb = O.shade(s, z["b32_position"], z["b32_normal"], z["b32_albedo"], z["b32_ids"], z["b32_pts"], z["b32_W"])
+        np.testing.assert_array_equal(rgb, z["b32_rgb"])
+        assert (rgb != 0).any(axis=1).sum() > 100
+
+    def test_point_lights(self, g_scenes, g_samp, g_shade):
+        s = scene(g_scenes, "pbox8")
+        z = g_shade
+        rgb = O.shade(s, g_samp["pgb_position"], g_samp["pgb_normal"], g_samp["pgb_albedo"], z["p8_ids"],
+                      z["p8_pts"], z["p8_W"])
+        np.testing.assert_array_equal(rgb, z["p8_rgb"])
+
+    def test_nls_samples(self, g_scenes, g_samp, g_shade):
+        s = scene(g_scenes, "boxes32")
+        rgb = O.shade(s, g_samp["gb_position"], g_samp["gb_normal"], g_samp["gb_albedo"], g_samp["nls_ids"],
+                      g_samp["nls_pts"], g_samp["nls_W"])
+        np.testing.assert_array_equal(rgb, g_shade["nls_rgb"])
+
+
 class TestTrainingCurve:
     def test_first_step_matches_reference(self, g_scenes, g_train):
         s = scene(g_scenes, "pbox8")
