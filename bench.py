@@ -52,6 +52,7 @@ N_WORLD = N_SCREEN = 4096
 LAUNCHES_PER_FRAME = 14
 METRIC = "visibility queries/s (encode+MLP+WRS) at 1080p x 32 lights; train samples/s"
 UNIT = "queries/s"
+RENDER_METRIC = "rendered pixels/s (online frame: train + NLS + one shadow ray per pixel) at 1080p x 32 lights"
 
 
 def peaks():
@@ -186,7 +187,7 @@ def gpu_arm(args) -> None:
     from paper_2506_05930_b200 import MODE_LIGHTS, HashGridConfig, TrainFrameConfig, VisibilityCache
     from paper_2506_05930_b200 import _lib
     from paper_2506_05930_b200 import rng as R
-    from paper_2506_05930_b200.render import gbuffer_device
+    from paper_2506_05930_b200.render import gbuffer_device, shade_device
     from paper_2506_05930_b200.sampling import PixelCtx, nls_sample_device
     from paper_2506_05930_b200.scene import scene_from_dict
     from paper_2506_05930_b200.scenes import boxes_scene
@@ -236,7 +237,10 @@ def gpu_arm(args) -> None:
     sel_stream = (torch.cuda.Stream(dev, priority=int(os.environ.get("NVC_SELECT_PRIORITY", "0")))
                   if not os.environ.get("NVC_SELECT_INLINE") else None)
 
-    def frame_into(f, outs, timed_parts=None):
+    shade = args.workload == "render"
+    rgb_buf = [torch.empty((P, 3), dtype=torch.float64, device=dev) for _ in range(2)] if shade else [None, None]
+
+    def frame_into(f, outs, timed_parts=None, rgb=None):
         if timed_parts is not None:
             marks[0].record(stream)
         loss, bufs = train_frame_device(scene, cam, cache, cfg, frame=f, shard=rank, n_shards=world,
@@ -248,10 +252,21 @@ def gpu_arm(args) -> None:
                           out=outs, select_stream=None if timed_parts is not None else sel_stream)
         if timed_parts is not None:
             marks[2].record(stream)
+        if shade:   # pass 5: one shadow ray per pixel to its NLS-selected light point
+            if timed_parts is None and sel_stream is not None:
+                with torch.cuda.stream(sel_stream):
+                    shade_device(scene, ctx.pos, ctx.nrm, ctx.alb, *outs, out=rgb)
+                    done = torch.cuda.Event()
+                    done.record(sel_stream)
+                    cache.select_done = done
+            else:
+                shade_device(scene, ctx.pos, ctx.nrm, ctx.alb, *outs, out=rgb)
+            if timed_parts is not None:
+                marks[3].record(stream)
         return loss
 
     def frame(f, timed_parts=None):
-        return frame_into(f, out, timed_parts)
+        return frame_into(f, out, timed_parts, rgb_buf[0])
 
     def barrier():
         torch.cuda.synchronize()
@@ -267,14 +282,16 @@ def gpu_arm(args) -> None:
 
     # ---- per-stage split (separate pass, events between stages and between
     #      the three query kernels, all on the launching stream) ----
-    split_train, split_query, split_k = [], [], []
+    split_train, split_query, split_k, split_shade = [], [], [], []
     kms = (ctypes.c_float * 3)()
     for f in range(min(args.steps, 10)):
         _lib.call("nvc_profile_stages", 1)
         frame(1000 + f, timed_parts=True)
         _lib.call("nvc_profile_stages", 0)
-        marks[2].synchronize()
+        marks[3 if shade else 2].synchronize()
         _lib.call("nvc_profile_stage_ms", ctypes.addressof(kms))
+        if shade:
+            split_shade.append(marks[2].elapsed_time(marks[3]))
         split_train.append(marks[0].elapsed_time(marks[1]))
         split_query.append(marks[1].elapsed_time(marks[2]))
         split_k.append(list(kms))
@@ -301,7 +318,7 @@ def gpu_arm(args) -> None:
     # against the compute stream: frame f+1's positions upload and frame f-1's
     # results download while frame f computes.
     pos_host = pos.cpu().pin_memory()
-    outs_host = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in out]
+    outs_host = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in ((rgb_buf[0],) if shade else out)]
     loss_host = torch.empty(1, dtype=torch.float64, pin_memory=True)
     pos_buf = [ctx.pos, torch.empty_like(ctx.pos)]
     out_buf = [out, tuple(torch.empty_like(o) for o in out)]
@@ -325,13 +342,13 @@ def gpu_arm(args) -> None:
         if sel_stream is not None:
             sel_stream.wait_event(ev_d2h[b])
         ctx.pos = pos_buf[b]
-        loss = frame_into(5000 + f, out_buf[b])
+        loss = frame_into(5000 + f, out_buf[b], rgb=rgb_buf[b])
         ev_comp[b].record(stream)
         with torch.cuda.stream(s_d2h):
             s_d2h.wait_event(ev_comp[b])
             if cache.select_done is not None:
                 s_d2h.wait_event(cache.select_done)
-            for h, d in zip(outs_host, out_buf[b]):
+            for h, d in zip(outs_host, (rgb_buf[b],) if shade else out_buf[b]):
                 h.copy_(d, non_blocking=True)
             loss_host.copy_(loss.reshape(1), non_blocking=True)
             ev_d2h[b].record(s_d2h)
@@ -384,23 +401,26 @@ def gpu_arm(args) -> None:
             except Exception:
                 traffic = None
         clk = clocks.summary()
+        metric, unit = (RENDER_METRIC, "pixels/s") if shade else (METRIC, UNIT)
         line = {
-            "metric": METRIC, "value": P * world / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "metric": metric, "value": P * world / (ms * 1e-3), "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "fp16 MLP / fp64 index+WRS / fp32 train",
             "data": "synthetic (boxes_scene(32) fixture, random-init weights, seed 0)",
             "config": {"workload": f"C2: {WIDTH}x{HEIGHT * world} boxes32 (K=32), L=16 T=2^19 F=2, MLP 3x64, "
-                                   f"1 online frame = train batch {(N_WORLD + N_SCREEN) * world} + NLS over all pixels",
+                                   f"1 online frame = train batch {(N_WORLD + N_SCREEN) * world} + NLS over all pixels"
+                                   + (" + one shadow ray per pixel (shade_batch)" if shade else ""),
                        "train_samples_per_s": (N_WORLD + N_SCREEN) * world / (ms * 1e-3),
                        "pixels_per_gpu": P, "global_batch": (N_WORLD + N_SCREEN) * world,
                        "parallelism": f"dp{world} (train) + {world} screen tiles (query)",
                        "l2": "inputs > L2 every frame (lum table 265 MB + 16.8 M-parameter Adam stream 530 MB)",
                        "stage_ms": {"train_frame": tr_ms, "query": q_ms, "k_enc_tiles2": k_ms[0],
-                                    "k_mlp_ts": k_ms[1], "k_nls32": k_ms[2]}},
-            "e2e": {"value": P * world / (e2e_ms * 1e-3), "unit": UNIT,
+                                    "k_mlp_ts": k_ms[1], "k_nls32": k_ms[2],
+                                    **({"k_shade": statistics.median(split_shade)} if shade else {})}},
+            "e2e": {"value": P * world / (e2e_ms * 1e-3), "unit": unit,
                     "h2d_bytes_per_step": int(pos_host.numel() * 8),
                     "d2h_bytes_per_step": int(sum(h.numel() * h.element_size() for h in outs_host) + 8)},
-            "gpu_launches": LAUNCHES_PER_FRAME * args.steps,
+            "gpu_launches": (LAUNCHES_PER_FRAME + int(shade)) * args.steps,
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
                          "traffic": traffic, "kernel": name, "peak_source": src,
                          "work_per_launch": work, "launch_ms": kms,
@@ -412,7 +432,7 @@ def gpu_arm(args) -> None:
                                         "vs_random_probe": (enc_gathers / probe) if probe else None}},
             "clocks": clk,
         }
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and not shade:
             line["cpu_baseline"] = cpu_reference(sample_pixels=args.cpu_sample)
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -515,8 +535,9 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-sample", type=int, default=24576)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["c2", "ndi4k"], default="c2",
-                    help="c2: the headline online frame (default); ndi4k: C3 Neural DI at 4K")
+    ap.add_argument("--workload", choices=["c2", "ndi4k", "render"], default="c2",
+                    help="c2: the headline online frame (default); ndi4k: C3 Neural DI at 4K; "
+                         "render: the c2 frame plus shading pass 5 (one shadow ray per pixel)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -96,16 +96,18 @@ typedef struct {
     const double *lt_lumaw;               /* (K, 3) LUMA * radiance, precomputed by the host */
     const double *lt_area;                /* (K) scene.py:189 (shade_batch's area term) */
     /* Shadow-ray acceleration data, precomputed by the host (scene.py
-     * DeviceScene).  tri_plane (n_tris, 4) f32 in BVH order: unit normal and
-     * offset of each triangle's plane, or all zeros for a triangle that must
-     * never be culled (zero area or a sliver); tri_leaf (n_tris) the BVH leaf
-     * holding triangle k; node_parent (n_nodes) the parent node (-1 at the
-     * root).  With anyhit_bf set, any-hit queries test every triangle whose
-     * plane the segment reaches (f32 plane test with margin plane_margin *
-     * (R + |p0|inf + |p1|inf), R = plane_r) exactly, and accept a hit only if
+     * shadow_accel).  In BVH triangle order: tri_plane (n_tris, 4) f32 unit
+     * normal and offset of each triangle's plane (all zeros: never culled --
+     * zero area or a sliver); tri_box (n_tris, 8) f32 AABB for the
+     * crossing-box filter; tri_leaf (n_tris) the BVH leaf holding the
+     * triangle.  node_parent (n_nodes): parent node, -1 at the root.  With
+     * anyhit_bf set, any-hit queries cull triangles with f32 tests whose
+     * margin (plane_margin * (plane_r + |p0|inf + |p1|inf)) bounds their error
+     * 32x, test the rest with the exact FP64 ray_tri, and accept a hit only if
      * every BVH ancestor of its leaf passes the FP64 slab test -- the same
-     * answer as the reference's pruned BVH traversal. */
+     * answer as the reference's pruned BVH traversal (geometry.cu). */
     const float *tri_plane;
+    const float *tri_box;                 /* (n_tris, 8) f32: min xyz, flag, max xyz, 0; flag 1 = no box test */
     const int32_t *tri_leaf;
     const int32_t *node_parent;
     float plane_margin, plane_r;

@@ -46,7 +46,7 @@ class NvcScene(ctypes.Structure):
         ("tri_material", c_vp), ("tri_light", c_vp), ("mat_albedo", c_vp),
         ("lt_kind", c_vp), ("lt_verts", c_vp), ("lt_normal", c_vp), ("lt_radiance", c_vp),
         ("lt_lumaw", c_vp), ("lt_area", c_vp),
-        ("tri_plane", c_vp), ("tri_leaf", c_vp), ("node_parent", c_vp),
+        ("tri_plane", c_vp), ("tri_box", c_vp), ("tri_leaf", c_vp), ("node_parent", c_vp),
         ("plane_margin", ctypes.c_float), ("plane_r", ctypes.c_float), ("anyhit_bf", c_i32), ("pad0", c_i32),
         ("n_nodes", c_i64), ("n_tris", c_i64), ("n_lights", c_i32), ("n_materials", c_i32),
         ("shadow_eps", c_f64), ("aabb_min", c_f64 * 3), ("aabb_max", c_f64 * 3),

@@ -125,21 +125,28 @@ __device__ int64_t closest_hit(const nvc_scene& sc, const double o[3], const dou
     return best;
 }
 
-// Any-hit by plane culling (scenes with <= BF_MAX_TRIS triangles, nvc.h).
+// Any-hit by culling (scenes with <= BF_MAX_TRIS triangles, nvc.h).
 // The reference's answer is "some triangle k passes ray_tri AND every BVH
 // ancestor of k's leaf passes the FP64 slab test" (its traversal tests exactly
 // those triangles, and any-hit does not depend on the order).  This evaluates
-// the same predicate triangle by triangle:
-//  1. f32 plane test: the segment [o + t_min d, o + t_max d] cannot meet k if
-//     both ends are farther than m on the same side of k's plane.  ray_tri can
-//     only accept a t in [t_min, t_max] whose point lies within
-//     ~1e-15 * sliver * (t + |o - a|) of the plane (sliver <= 2^20 on the
-//     host, else the plane is zero and never culls), and the f32 evaluation
-//     errs by < 2^-20 (R + |p|): m = 2^-15 (R + |p0| + |p1|) covers both 32x;
-//  2. exact FP64 ray_tri (the same function the traversal calls);
-//  3. on a hit only: the FP64 slab test of the leaf and each ancestor.
-// So the result is bit-identical to the traversal's, at ~12 f32 instructions
-// per culled triangle instead of a stack walk of FP64 slab tests.
+// the same predicate triangle by triangle, with two conservative f32 filters
+// in front of the exact test:
+//  1. plane test: the segment [p0, p1] = [o + t_min d, o + t_max d] cannot
+//     meet k if both ends are farther than m on the same side of k's plane.
+//     ray_tri can only accept a t in [t_min, t_max] whose point lies within
+//     ~1e-15 * sliver * (t + |o - a|) of the plane (sliver = |e1||e2|/|e1 x e2|
+//     <= 2^20 on the host, else the plane is zero and never culls), and the
+//     f32 evaluation errs by < 2^-20 (R + |p|): m = 2^-15 (R + |p0| + |p1|)
+//     covers both 32x;
+//  2. crossing-box test (when |s1 - s0| > 4m and the triangle has a box,
+//     sliver <= 2^8): the part of the segment within m of the plane,
+//     f in [(-m - s0), (m - s0)] / (s1 - s0), widened by m, must overlap k's
+//     AABB.  There ray_tri's barycentrics err by < ~1e-9 |p0 - p1| (the ray is
+//     at least 4m/L away from parallel), far inside the widening;
+//  3. exact FP64 ray_tri (the same function the traversal calls);
+//  4. on a hit only: the FP64 slab test of the leaf and each ancestor.
+// The result is bit-identical to the traversal's; per triangle it costs ~12
+// f32 instructions when culled by the plane, ~30 when culled by the box.
 __device__ __forceinline__ bool chain_ok(const nvc_scene& sc, int32_t k, const double o[3],
                                          const double inv[3], double t_max) {
     for (int32_t n = __ldg(sc.tri_leaf + k); n >= 0; n = __ldg(sc.node_parent + n))
@@ -151,25 +158,141 @@ __device__ __forceinline__ float max_abs3(float a, float b, float c) {
     return fmaxf(fabsf(a), fmaxf(fabsf(b), fabsf(c)));
 }
 
+// per-ray f32 data of the culling filters: segment ends p0, p1, p1 - p0, margin
+struct CullRay {
+    float a[3], b[3], g[3], m;
+};
+
+__device__ __forceinline__ CullRay cull_ray(const nvc_scene& sc, const double o[3], const double d[3], double t_min,
+                                            double t_max) {
+    CullRay r;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        r.a[c] = (float)(o[c] + t_min * d[c]);
+        r.b[c] = (float)(o[c] + t_max * d[c]);
+        r.g[c] = r.b[c] - r.a[c];
+    }
+    r.m = sc.plane_margin * ((sc.plane_r + max_abs3(r.a[0], r.a[1], r.a[2])) + max_abs3(r.b[0], r.b[1], r.b[2])) +
+          1e-30f;
+    return r;
+}
+
+// filters 1 + 2 for triangle k: false = the exact test cannot accept it
+__device__ __forceinline__ bool cull_keep(const nvc_scene& sc, const CullRay& r, int32_t k) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(sc.tri_plane) + k);
+    const float s0 = fmaf(q.x, r.a[0], fmaf(q.y, r.a[1], fmaf(q.z, r.a[2], -q.w)));
+    const float s1 = fmaf(q.x, r.b[0], fmaf(q.y, r.b[1], fmaf(q.z, r.b[2], -q.w)));
+    const float m = r.m;
+    bool keep = !(fminf(s0, s1) > m || fmaxf(s0, s1) < -m);
+    const float ds = s1 - s0;
+    if (keep && fabsf(ds) > 4.0f * m) {
+        const float4* bx = reinterpret_cast<const float4*>(sc.tri_box) + 2 * k;
+        const float4 lo = __ldg(bx), hi = __ldg(bx + 1);
+        if (lo.w == 0.0f) {      // the triangle has a box (w = 1: never box-culled)
+            const float rd = 1.0f / ds;
+            const float fa = (-m - s0) * rd, fb = (m - s0) * rd;
+            const float f_lo = fmaxf(fminf(fa, fb) - 0x1p-12f, 0.0f);
+            const float f_hi = fminf(fmaxf(fa, fb) + 0x1p-12f, 1.0f);
+            const float u0 = fmaf(f_lo, r.g[0], r.a[0]), v0 = fmaf(f_hi, r.g[0], r.a[0]);
+            const float u1 = fmaf(f_lo, r.g[1], r.a[1]), v1 = fmaf(f_hi, r.g[1], r.a[1]);
+            const float u2 = fmaf(f_lo, r.g[2], r.a[2]), v2 = fmaf(f_hi, r.g[2], r.a[2]);
+            keep = f_lo <= f_hi && fminf(u0, v0) - m <= hi.x && fmaxf(u0, v0) + m >= lo.x &&
+                   fminf(u1, v1) - m <= hi.y && fmaxf(u1, v1) + m >= lo.y && fminf(u2, v2) - m <= hi.z &&
+                   fmaxf(u2, v2) + m >= lo.z;
+        }
+    }
+    return keep;
+}
+
+// filters 3 + 4: the reference's own test of triangle k and its leaf's ancestry
+__device__ __forceinline__ bool exact_hit(const nvc_scene& sc, int32_t k, const double o[3], const double d[3],
+                                          double t_min, double t_max) {
+    if (ray_tri(o, d, sc.bv0 + 3 * k, sc.bv1 + 3 * k, sc.bv2 + 3 * k, t_min, t_max) < 0.0) return false;
+    const double inv[3] = {inv_dir(d[0]), inv_dir(d[1]), inv_dir(d[2])};
+    return chain_ok(sc, k, o, inv, t_max);
+}
+
 __device__ bool any_hit_bf(const nvc_scene& sc, const double o[3], const double d[3], double t_min,
                            double t_max) {
-    const float a0 = (float)(o[0] + t_min * d[0]), a1 = (float)(o[1] + t_min * d[1]),
-                a2 = (float)(o[2] + t_min * d[2]);
-    const float b0 = (float)(o[0] + t_max * d[0]), b1 = (float)(o[1] + t_max * d[1]),
-                b2 = (float)(o[2] + t_max * d[2]);
-    const float m = sc.plane_margin * ((sc.plane_r + max_abs3(a0, a1, a2)) + max_abs3(b0, b1, b2)) + 1e-30f;
-    const float4* pl = reinterpret_cast<const float4*>(sc.tri_plane);
-    for (int32_t k = 0; k < (int32_t)sc.n_tris; ++k) {
-        const float4 q = __ldg(pl + k);
-        const float s0 = fmaf(q.x, a0, fmaf(q.y, a1, fmaf(q.z, a2, -q.w)));
-        const float s1 = fmaf(q.x, b0, fmaf(q.y, b1, fmaf(q.z, b2, -q.w)));
-        if (fminf(s0, s1) > m || fmaxf(s0, s1) < -m) continue;
-        if (ray_tri(o, d, sc.bv0 + 3 * k, sc.bv1 + 3 * k, sc.bv2 + 3 * k, t_min, t_max) >= 0.0) {
-            const double inv[3] = {inv_dir(d[0]), inv_dir(d[1]), inv_dir(d[2])};
-            if (chain_ok(sc, k, o, inv, t_max)) return true;
+    const CullRay r = cull_ray(sc, o, d, t_min, t_max);
+    const int32_t n = (int32_t)sc.n_tris;
+    for (int32_t k0 = 0; k0 < n; k0 += 32) {
+        const int32_t cnt = min(32, n - k0);
+        uint32_t cand = 0u;
+#pragma unroll 4
+        for (int32_t j = 0; j < cnt; ++j) cand |= (cull_keep(sc, r, k0 + j) ? 1u : 0u) << j;
+        while (cand) {
+            const int32_t k = k0 + __ffs(cand) - 1;
+            cand &= cand - 1u;
+            if (exact_hit(sc, k, o, d, t_min, t_max)) return true;
         }
     }
     return false;
+}
+
+// order-preserving float <-> int maps for redux.sync min/max
+__device__ __forceinline__ int f2key(float f) {
+    const int b = __float_as_int(f);
+    return b ^ ((b >> 31) & 0x7fffffff);
+}
+__device__ __forceinline__ float key2f(int k) { return __int_as_float(k ^ ((k >> 31) & 0x7fffffff)); }
+
+// Warp-cooperative form (all 32 lanes call it; returns the lane's answer).
+// Filter 0: a triangle can only count if the FP64 slab test of its leaf passes
+// (step 4), i.e. if the segment [o, o + t_max d] reaches the leaf's box (to
+// FP64 rounding).  So a triangle whose leaf box misses the union of the warp's
+// segment boxes, each widened by its margin m, counts for no lane.  Lane j
+// tests triangle k0 + j's leaf box against the union, and the per-lane filters
+// then run only over the warp's candidates -- a short list when the warp's
+// rays are coherent (Morton-sorted targets, light-sorted shading rows).
+__device__ bool any_hit_bf_warp(const nvc_scene& sc, const double o[3], const double d[3], double t_min,
+                                double t_max, bool active) {
+    const int lane = threadIdx.x & 31;
+    const CullRay r = cull_ray(sc, o, d, t_min, t_max);
+    int klo[3], khi[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const float oc = (float)o[c];
+        float lo = fminf(oc, r.b[c]) - r.m, hi = fmaxf(oc, r.b[c]) + r.m;
+        if (!(lo == lo) || !(hi == hi)) {   // NaN: this lane needs every triangle
+            lo = -INFINITY;
+            hi = INFINITY;
+        }
+        klo[c] = __reduce_min_sync(0xffffffffu, active ? f2key(lo) : 0x7fffffff);
+        khi[c] = __reduce_max_sync(0xffffffffu, active ? f2key(hi) : (int)0x80000000);
+    }
+    const float wl0 = key2f(klo[0]), wl1 = key2f(klo[1]), wl2 = key2f(klo[2]);
+    const float wh0 = key2f(khi[0]), wh1 = key2f(khi[1]), wh2 = key2f(khi[2]);
+    bool hit = false, live = active;
+    const int32_t n = (int32_t)sc.n_tris;
+    for (int32_t k0 = 0; k0 < n; k0 += 32) {
+        if (!__any_sync(0xffffffffu, live)) break;
+        bool ov = false;
+        if (k0 + lane < n) {
+            const int32_t leaf = __ldg(sc.tri_leaf + k0 + lane);
+            const double* lo = sc.node_min + 3 * leaf;
+            const double* hi = sc.node_max + 3 * leaf;
+            ov = (float)__ldg(lo) <= wh0 && (float)__ldg(hi) >= wl0 && (float)__ldg(lo + 1) <= wh1 &&
+                 (float)__ldg(hi + 1) >= wl1 && (float)__ldg(lo + 2) <= wh2 && (float)__ldg(hi + 2) >= wl2;
+        }
+        uint32_t wm = __ballot_sync(0xffffffffu, ov);
+        uint32_t cand = 0u;
+        while (wm) {                                   // warp-uniform loop over the warp's candidates
+            const int j = __ffs(wm) - 1;
+            wm &= wm - 1u;
+            cand |= (live && cull_keep(sc, r, k0 + j) ? 1u : 0u) << j;
+        }
+        while (cand) {
+            const int32_t k = k0 + __ffs(cand) - 1;
+            cand &= cand - 1u;
+            if (exact_hit(sc, k, o, d, t_min, t_max)) {
+                hit = true;
+                live = false;
+                break;
+            }
+        }
+    }
+    return hit;
 }
 
 __device__ bool any_hit(const nvc_scene& sc, const double o[3], const double d[3], double t_min,
@@ -542,6 +665,7 @@ __device__ uint32_t any_hit_packet(const nvc_scene& sc, const double o[3], const
     uint32_t hit = 0u;
     const uint32_t act = __ballot_sync(0xffffffffu, active);
     if (sc.n_tris == 0 || act == 0u) return 0u;
+    if (sc.anyhit_bf == 2) return __ballot_sync(0xffffffffu, any_hit_bf_warp(sc, o, d, t_min, t_max, active));
     if (sc.anyhit_bf) return __ballot_sync(0xffffffffu, active && any_hit_bf(sc, o, d, t_min, t_max));
     const double inv[3] = {inv_dir(d[0]), inv_dir(d[1]), inv_dir(d[2])};
     int top = 0;

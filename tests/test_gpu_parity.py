@@ -183,7 +183,7 @@ class TestGeometry:
 
     @pytest.mark.parametrize("shards,unsorted,anyhit", [(1, False, "auto"), (2, False, "auto"), (3, False, "auto"),
                                                         (1, True, "auto"), (2, True, "auto"), (1, False, "bvh"),
-                                                        (1, True, "bvh")])
+                                                        (1, True, "bvh"), (1, False, "bf")])
     def test_boxes32_device_batch_bit_exact(self, g_train, shards, unsorted, anyhit, monkeypatch):
         """Batch positions and shadow-ray targets (Morton-bucketed warps, and the plain
         row-per-warp kernel; plane-culled any-hit and the packet BVH traversal) are
@@ -270,6 +270,23 @@ class TestShade:
         want = O.shade(o, pos.cpu().numpy(), nrm.cpu().numpy(), alb.cpu().numpy(), ids_o, pts, big_w)
         np.testing.assert_array_equal(rgb, want)
         assert (rgb != 0).any(axis=1).sum() > n // 10
+
+    def test_warp_culled_targets_equal_bvh_over_frames(self, monkeypatch):
+        """Shadow-ray targets of 8 full C2 batches (2 M rays): warp-level + per-lane
+        culling (default), per-lane only, and the packet BVH traversal agree bitwise."""
+        from paper_2506_05930_b200.training import BatchBuffers, gen_batch_device
+        got = {}
+        for mode in ("auto", "bf", "bvh"):
+            s = _scene_with(lambda: boxes_scene(32), mode, monkeypatch)
+            outs = []
+            for f in range(8):
+                bufs = BatchBuffers(4096, 4096, 32, DEV, 1)
+                gen_batch_device(s, s.camera.resized(1920, 1080), bufs, 0, f, 0, 0, 1)
+                outs.append(bufs.tgt.cpu().numpy().copy())
+            got[mode] = np.stack(outs)
+        np.testing.assert_array_equal(got["auto"], got["bvh"])
+        np.testing.assert_array_equal(got["bf"], got["bvh"])
+        assert 0.05 < got["bvh"].mean() < 0.95
 
     @pytest.mark.parametrize("scene_fn", [lambda: boxes_scene(32), lambda: boxes_point_scene(8)])
     def test_plane_culling_equals_bvh_traversal(self, scene_fn, monkeypatch):

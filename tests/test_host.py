@@ -145,7 +145,7 @@ def test_shadow_accel_tables(name):
     triangle's leaf holds it, and parent links walk from every leaf to the root."""
     from paper_2506_05930_b200.scene import shadow_accel
     b = scene_from_dict(SCENES[name]()).bvh
-    plane, leaf, parent, r = shadow_accel(b)
+    plane, box, leaf, parent, r = shadow_accel(b)
     assert plane.dtype == np.float32 and plane.shape == (b.v0.shape[0], 4)
     live = np.abs(plane[:, :3]).sum(axis=1) > 0
     assert live.mean() > 0.9
@@ -153,6 +153,9 @@ def test_shadow_accel_tables(name):
         resid = (plane[live, :3].astype(np.float64) * v[live]).sum(axis=1) - plane[live, 3]
         assert np.abs(resid).max() < 1e-5 * (1.0 + r)
     np.testing.assert_allclose(np.linalg.norm(plane[live, :3], axis=1), 1.0, rtol=1e-6)
+    for v in (b.v0, b.v1, b.v2):
+        assert (box[:, 0:3] <= v.astype(np.float32)).all() and (box[:, 4:7] >= v.astype(np.float32)).all()
+    assert set(np.unique(box[:, 3])) <= {0.0, 1.0} and (box[:, 3] == 0).mean() > 0.9
     for k in range(b.v0.shape[0]):
         n = leaf[k]
         assert b.node_count[n] > 0 and b.node_start[n] <= k < b.node_start[n] + b.node_count[n]
