@@ -2,7 +2,8 @@
 
 A drop-in for the hot path of the reference ``viscache`` package: the cache
 object (``VisibilityCache``/``make_cache`` with ``infer``/``train_step``),
-the training-frame driver and WRS light sampling / Neural DI.  All compute
+the training-frame driver, WRS light sampling / Neural DI and the
+one-shadow-ray shading pass.  All compute
 runs in ``libnvc.so`` (hand-written sm_100a CUDA: FP64 geometry, hash-grid
 encoder, tcgen05/TMEM fused MLP, WRS with numpy-compatible Philox); this
 package is the host layer that keeps the reference's API.
@@ -13,7 +14,8 @@ from .cache import (MODE_CLUSTERS, MODE_LIGHTS, MODE_RADIANCE, PRECISION_FP16, P
                     GradExchange, VisibilityCache, make_cache)
 from .hashgrid import HashGridConfig, clustered_config
 from .mlp import MLPConfig, MLPParams, TrainStepConfig, lr_at
-from .render import GBuffer, gbuffer_and_ctx, make_gbuffer
+from . import render
+from .render import GBuffer, gbuffer_and_ctx, make_gbuffer, shade_batch, shade_pixel
 from .sampling import (CLAMP_FLOOR, PixelCtx, Reservoir, ShadingPoint, clamp_visibility,
                        neural_di_batch, neural_di_shade, nls_sample, nls_sample_batch,
                        nls_weights_batch, wrs_select, wrs_select_batch)
@@ -27,7 +29,8 @@ __version__ = "0.1.0"
 __all__ = [
     "rng", "VisibilityCache", "make_cache", "MODE_LIGHTS", "MODE_CLUSTERS", "MODE_RADIANCE",
     "PRECISION_FP16", "PRECISION_FP32", "HashGridConfig", "clustered_config", "MLPConfig",
-    "MLPParams", "TrainStepConfig", "lr_at", "GBuffer", "gbuffer_and_ctx", "make_gbuffer",
+    "MLPParams", "TrainStepConfig", "lr_at", "GBuffer", "gbuffer_and_ctx", "make_gbuffer", "render",
+    "shade_batch", "shade_pixel",
     "CLAMP_FLOOR", "PixelCtx", "Reservoir", "ShadingPoint", "clamp_visibility", "neural_di_batch",
     "neural_di_shade", "nls_sample", "nls_sample_batch", "nls_weights_batch", "wrs_select",
     "wrs_select_batch", "Camera", "Light", "Material", "Scene", "SceneError", "load_scene",
