@@ -52,6 +52,7 @@ N_WORLD = N_SCREEN = 4096
 LAUNCHES_PER_FRAME = 14
 METRIC = "visibility queries/s (encode+MLP+WRS) at 1080p x 32 lights; train samples/s"
 UNIT = "queries/s"
+C4_METRIC = "visibility queries/s (encode+MLP+WRS) at 1080p x 128 lights (C4); train samples/s"
 RENDER_METRIC = "rendered pixels/s (online frame: train + NLS + one shadow ray per pixel) at 1080p x 32 lights"
 
 
@@ -190,7 +191,7 @@ def gpu_arm(args) -> None:
     from paper_2506_05930_b200.render import gbuffer_device, shade_device
     from paper_2506_05930_b200.sampling import PixelCtx, nls_sample_device
     from paper_2506_05930_b200.scene import scene_from_dict
-    from paper_2506_05930_b200.scenes import boxes_scene
+    from paper_2506_05930_b200.scenes import boxes_scene, rooms_scene
     from paper_2506_05930_b200.training import BatchPipeline, train_frame_device
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -204,7 +205,9 @@ def gpu_arm(args) -> None:
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    scene = scene_from_dict(boxes_scene(32))
+    c4 = args.workload == "c4"
+    kk, hid = (128, (128, 128, 128)) if c4 else (K, HIDDEN)
+    scene = scene_from_dict(rooms_scene(128) if c4 else boxes_scene(32))
     cam = scene.camera.resized(WIDTH, HEIGHT * world)      # N tiles of 1080 rows
     P = WIDTH * HEIGHT
     p_first, p_total = rank * P, P * world
@@ -213,13 +216,13 @@ def gpu_arm(args) -> None:
     ctx.lum_device()
     grid = HashGridConfig(levels=LEVELS, table_size=TABLE, features_per_level=FEATS, aabb_min=scene.aabb_min,
                           aabb_max=scene.aabb_max)
-    cache = VisibilityCache(MODE_LIGHTS, K, grid, seed=0, hidden_dims=HIDDEN, device=dev)
+    cache = VisibilityCache(MODE_LIGHTS, kk, grid, seed=0, hidden_dims=hid, device=dev)
     if os.environ.get("NVC_L2_PIN"):      # measured slower (it starves the streaming Adam of L2)
         cache.pin_table_in_l2()
     cfg = TrainFrameConfig(n_world=N_WORLD * world, n_screen=N_SCREEN * world, seed=0)
     # training batches are generated one frame ahead on a side stream (they depend on
     # the frame index only), overlapping the FP64 ray kernels with training + query
-    pipe = BatchPipeline(scene, cam, cfg, K, dev, rank, world, cache=cache)
+    pipe = BatchPipeline(scene, cam, cfg, kk, dev, rank, world, cache=cache)
     out = (torch.empty(P, dtype=torch.int64, device=dev), torch.empty((P, 3), dtype=torch.float64, device=dev),
            torch.empty(P, dtype=torch.float64, device=dev))
 
@@ -372,11 +375,12 @@ def gpu_arm(args) -> None:
         k_ms = [statistics.median(x[i] for x in split_k) for i in range(3)]
         # roofline of each query kernel: algorithmic work per launch / its event-timed duration
         # (DESIGN.md section 4 gives the per-pixel figures)
-        flop_px = 2 * sum(a * b for a, b in zip((32, 64, 64, 64), (64, 64, 64, 32)))
+        dims = (LEVELS * FEATS,) + tuple(hid) + (kk,)
+        flop_px = 2 * sum(a * b for a, b in zip(dims[:-1], dims[1:]))
         kern = {
             "k_enc_tiles2": ("hbm", P * (24 + 64), k_ms[0]),             # pos in, fp16 feature tile out
             "k_mlp_ts": ("tensor", P * flop_px, k_ms[1]),                # 24,576 flop per pixel
-            "k_nls32": ("hbm", P * (64 + 4 * K + 4 + 40), k_ms[2]),      # vis + lum + mask in, id/W/point out
+            "k_nls32": ("hbm", P * (2 * kk + 4 * kk + 4 * ((kk + 31) // 32) + 40), k_ms[2]),   # vis + lum + mask in, id/W/point out
         }
         # encoder gathers vs the measured random-gather L2 rate over the same 67 MB table
         # (profiles/r1_l2_gather_probe.txt, tools/l2_probe.py)
@@ -401,14 +405,16 @@ def gpu_arm(args) -> None:
             except Exception:
                 traffic = None
         clk = clocks.summary()
-        metric, unit = (RENDER_METRIC, "pixels/s") if shade else (METRIC, UNIT)
+        metric, unit = (RENDER_METRIC, "pixels/s") if shade else ((C4_METRIC, UNIT) if c4 else (METRIC, UNIT))
         line = {
             "metric": metric, "value": P * world / (ms * 1e-3), "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "fp16 MLP / fp64 index+WRS / fp32 train",
-            "data": "synthetic (boxes_scene(32) fixture, random-init weights, seed 0)",
-            "config": {"workload": f"C2: {WIDTH}x{HEIGHT * world} boxes32 (K=32), L=16 T=2^19 F=2, MLP 3x64, "
-                                   f"1 online frame = train batch {(N_WORLD + N_SCREEN) * world} + NLS over all pixels"
+            "data": f"synthetic ({'rooms_scene(128)' if c4 else 'boxes_scene(32)'} fixture, random-init weights, seed 0)",
+            "config": {"workload": (f"C4: {WIDTH}x{HEIGHT * world} rooms128 (K=128), L=16 T=2^19 F=2, MLP 3x128, "
+                                    if c4 else
+                                    f"C2: {WIDTH}x{HEIGHT * world} boxes32 (K=32), L=16 T=2^19 F=2, MLP 3x64, ")
+                                   + f"1 online frame = train batch {(N_WORLD + N_SCREEN) * world} + NLS over all pixels"
                                    + (" + one shadow ray per pixel (shade_batch)" if shade else ""),
                        "train_samples_per_s": (N_WORLD + N_SCREEN) * world / (ms * 1e-3),
                        "pixels_per_gpu": P, "global_batch": (N_WORLD + N_SCREEN) * world,
@@ -432,7 +438,7 @@ def gpu_arm(args) -> None:
                                         "vs_random_probe": (enc_gathers / probe) if probe else None}},
             "clocks": clk,
         }
-        if world == 1 and not args.no_cpu_baseline and not shade:
+        if world == 1 and not args.no_cpu_baseline and not shade and not c4:
             line["cpu_baseline"] = cpu_reference(sample_pixels=args.cpu_sample)
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -535,9 +541,10 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-sample", type=int, default=24576)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["c2", "ndi4k", "render"], default="c2",
+    ap.add_argument("--workload", choices=["c2", "ndi4k", "render", "c4"], default="c2",
                     help="c2: the headline online frame (default); ndi4k: C3 Neural DI at 4K; "
-                         "render: the c2 frame plus shading pass 5 (one shadow ray per pixel)")
+                         "render: the c2 frame plus shading pass 5 (one shadow ray per pixel); "
+                         "c4: the online frame on rooms128 with K=128 and a 3x128 MLP")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -225,8 +225,9 @@ int nvc_nls_from_vis(const nvc_scene *sc, const float *vis, const void *lum, int
                      int64_t *ids, double *pts, double *big_w, void *stream);
 /* The hot path: encode -> tcgen05 MLP -> clamp * lum -> WRS -> light point
  * (three kernels: encoder tiles, persistent MLP, per-pixel reservoir) over
- * p pixels.  pos (p, 3) f64; lum light-major (k, p_stride); nz_mask (p) bit k
- * set iff lum[k][p] != 0 (may be NULL); workspace from
+ * p pixels.  pos (p, 3) f64; lum light-major (k, p_stride); nz_mask
+ * ceil(k/32) words per pixel, word w of pixel r at w*p_stride + r, bit j set
+ * iff lum[32w+j][r] != 0 (nvc_table_mask; may be NULL); workspace from
  * nvc_query_workspace_bytes. */
 int nvc_nls_sample(const nvc_model *m, const nvc_scene *sc, const double *pos,
                    const void *lum, int32_t lum_f64, const uint32_t *nz_mask, int64_t p_stride,

@@ -382,13 +382,15 @@ struct T3Layout {
     int total;
 };
 
-__host__ __device__ inline T3Layout t3_layout(const Net& net) {
+// with_w = false: W stays in global memory (L2/L1-resident, row stride Ki) --
+// the layout for MLPs too wide for W + activations in shared memory (C4: 3x128)
+__host__ __device__ inline T3Layout t3_layout(const Net& net, bool with_w = true) {
     T3Layout t;
     int o = 0, dmax = 0;
     for (int l = 0; l < net.n_layers; ++l) {
         t.w[l] = o;
-        t.ws[l] = net.dims[l] + 4;
-        o += net.dims[l + 1] * t.ws[l];
+        t.ws[l] = with_w ? net.dims[l] + 4 : net.dims[l];
+        if (with_w) o += net.dims[l + 1] * t.ws[l];
         t.bias[l] = o;
         o += (net.dims[l + 1] + 3) / 4 * 4;
     }
@@ -429,6 +431,7 @@ __global__ void __launch_bounds__(128) k_tr_encode(GridDev g, const float* __res
     encode_level_f32(g, params, q, l, act0 + r * (g.L * g.F) + l * g.F, nullptr, nullptr);
 }
 
+template <bool kWG>
 __global__ void __launch_bounds__(kThreads, 2) k_train3(Net net, T3Layout tl, const float* __restrict__ params,
                                                        const float* __restrict__ act0g, int64_t b_max,
                                                        const int64_t* __restrict__ b_dev, int shard, int n_shards,
@@ -451,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_train3(Net net, T3Layout tl, co
         const float4* W = reinterpret_cast<const float4*>(params + net.woff[l]);
         float* dst = sm + tl.w[l];
 #pragma unroll 4
-        for (int e = tid; e < N * kq; e += kThreads) {
+        for (int e = tid; e < (kWG ? 0 : N * kq); e += kThreads) {
             const float4 w = __ldg(W + e);
             const int n = e / kq, k = (e - n * kq) * 4;
             *reinterpret_cast<float4*>(dst + n * tl.ws[l] + k) = w;
@@ -471,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_train3(Net net, T3Layout tl, co
     for (int l = 0; l < net.n_layers; ++l) {
         const int Ki = net.dims[l], N = net.dims[l + 1], ng = N / 4, S = tl.ws[l];
         const float* A = sm + tl.act[l];
-        const float* W = sm + tl.w[l];
+        const float* W = kWG ? params + net.woff[l] : sm + tl.w[l];
         float* out = sm + tl.act[l + 1];
         const bool last = l == net.n_layers - 1;
         for (int t = tid; t < (kRows / 2) * ng; t += kThreads) {
@@ -573,7 +576,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_train3(Net net, T3Layout tl, co
             gb[n] = acc;
         }
         // grad act[r][k] = sum_n dz[r][n] W[n][k], through leaky'(z_{l-1}) (2x4 tiles)
-        const float* W = sm + tl.w[l];
+        const float* W = kWG ? params + net.woff[l] : sm + tl.w[l];
         for (int t = tid; t < (kRows / 2) * kg; t += kThreads) {
             const int r0 = (t / kg) * 2, k0 = (t % kg) * 4;
             float acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
@@ -1171,9 +1174,11 @@ int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, con
     float* part_w = (float*)ws;
     double* part_loss = (double*)((char*)ws + ((int64_t)nblk * net.mlp_count * 4 + 255) / 256 * 256);
     cudaStream_t s = (cudaStream_t)stream;
-    bool split = g.F <= 8;
+    bool split = g.F <= 8 && getenv("NVC_TRAIN_FUSED") == nullptr;
     for (int i = 0; i <= net.n_layers; ++i) split = split && (net.dims[i] % 4 == 0);
-    const int smem3 = t3_layout(net).total * 4 + 64;
+    const bool wg = t3_layout(net).total * 4 + 64 > 200 * 1024;   // too wide for W in smem (C4): W from L1/L2
+    const T3Layout tl3 = t3_layout(net, !wg);
+    const int smem3 = tl3.total * 4 + 64;
     if (split && smem3 <= 200 * 1024) {
         char* p2 = (char*)part_loss + ((int64_t)nblk * 8 + 255) / 256 * 256;
         float* act0 = (float*)p2;
@@ -1181,9 +1186,15 @@ int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, con
         k_tr_encode<<<grid1(rows_max * g.L, 128), 128, 0, s>>>(g, m->params, pos, b_max, b_dev, shard, n_shards, act0);
         rc = check_launch("k_tr_encode");
         if (rc) return rc;
-        cudaFuncSetAttribute(k_train3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
-        k_train3<<<nblk, kThreads, smem3, s>>>(net, t3_layout(net), m->params, act0, b_max, b_dev, shard, n_shards,
-                                               tgt, mask, dact0, part_w, part_loss);
+        if (wg) {
+            cudaFuncSetAttribute(k_train3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+            k_train3<true><<<nblk, kThreads, smem3, s>>>(net, tl3, m->params, act0, b_max, b_dev, shard, n_shards,
+                                                         tgt, mask, dact0, part_w, part_loss);
+        } else {
+            cudaFuncSetAttribute(k_train3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+            k_train3<false><<<nblk, kThreads, smem3, s>>>(net, tl3, m->params, act0, b_max, b_dev, shard, n_shards,
+                                                          tgt, mask, dact0, part_w, part_loss);
+        }
         rc = check_launch("k_train3");
         if (rc) return rc;
         k_tr_scatter<<<grid1(rows_max * g.L, 128), 128, 0, s>>>(g, pos, b_max, b_dev, shard, n_shards, dact0,

@@ -287,7 +287,7 @@ struct MNet {
     int np[NVC_MAX_LAYERS], kp[NVC_MAX_LAYERS];
     int wofs[NVC_MAX_LAYERS];     // halfs
     int64_t boff[NVC_MAX_LAYERS];
-    int wpack_halfs, act_kp, tmem_cols, acc_cols;
+    int wpack_halfs, act_kp, tmem_cols, acc_cols, slots;
     float alpha;
     int out_sigmoid;
     int sm_w, sm_a0, sm_a1, sm_bias, sm_total;
@@ -349,6 +349,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_tiles(MNet net, const fl
     __syncthreads();
     tc_after();
     const uint32_t tmem = tbase;
+    const int slots = net.slots;   // tiles in flight: kSlots, or fewer when wide layers fill smem
     const int n_local = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
 
     if (warp == 8) {
@@ -377,12 +378,12 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_tiles(MNet net, const fl
                     mma(d, desc_of(a_addr, kT, net.kp[l], kk), desc_of(b, net.np[l], net.kp[l], kk), idesc,
                         kk > 0 ? 1u : 0u);
             };
-            for (int q0 = 0; q0 < n_local; q0 += kSlots) {
-                const int nq = min(kSlots, n_local - q0);
+            for (int q0 = 0; q0 < n_local; q0 += slots) {
+                const int nq = min(slots, n_local - q0);
                 for (int j = 0; j < nq; ++j) {
                     const int i = q0 + j, s = i % kStages;
                     mbar_wait(&bars.a0_full[s], (i / kStages) & 1);
-                    if (q0 >= kSlots) mbar_wait(&bars.acc_empty[j], ((q0 / kSlots) - 1) & 1);
+                    if (q0 >= slots) mbar_wait(&bars.acc_empty[j], ((q0 / slots) - 1) & 1);
                     issue(0, j, a0_addr + (uint32_t)(s * a0_bytes));
                     commit(&bars.a0_empty[s]);
                     commit(&bars.acc_full[j]);
@@ -402,8 +403,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1) k_mlp_tiles(MNet net, const fl
         const int eg = warp >> 2, row = tid & 127;
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
         uint32_t acc_cnt[2] = {0, 0};
-        for (int q0 = 0; q0 < n_local; q0 += kSlots) {
-            const int nq = min(kSlots, n_local - q0);
+        for (int q0 = 0; q0 < n_local; q0 += slots) {
+            const int nq = min(slots, n_local - q0);
             int bias_off = 0;
             for (int l = 0; l < net.n_layers; ++l) {
                 for (int jj = 0; jj < 2; ++jj) {
@@ -843,15 +844,22 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32(WArgs a, nvc_scene sc) {
 // static word indices, and the group's luminances are loaded before the
 // Philox rounds so their latency hides behind them.  The light-point draw
 // pair is the last "group".  Same arithmetic and order as k_nls32.
-template <bool kLum64>
+template <bool kLum64, int KW>
 __global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
-    __shared__ uint32_t s_vis[kWrsThreads * 33];
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t* my = s_vis + threadIdx.x * 33;
-    if (p < a.P) {
+    // KW 32-light words (K <= 32 KW).  K <= 32: the pixel's fp16 visibility row is
+    // staged in shared memory with one coalesced pass; wider rows (128-512 B) are
+    // read per 4-light group (8 B) next to the group's luminances instead, which
+    // keeps occupancy register-bound.
+    constexpr bool kStage = KW == 1;
+    constexpr int kRow = 16 * KW + 1;
+    using JobT = typename std::conditional<(KW > 2), uint64_t, uint32_t>::type;
+    __shared__ uint32_t s_vis[kStage ? kWrsThreads * kRow : 1];
+    const int64_t p = (int64_t)blockIdx.x * kWrsThreads + threadIdx.x;
+    uint32_t* my = s_vis + (kStage ? threadIdx.x * kRow : 0);
+    if (kStage && p < a.P) {
         const uint4* vrow = reinterpret_cast<const uint4*>(a.vis16 + p * a.vstride);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4 * KW; ++i)
             if (8 * i < a.K) {
                 const uint4 v = __ldg(vrow + i);
                 my[4 * i] = v.x;
@@ -862,11 +870,21 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
     }
     if (p >= a.P) return;
     const int64_t gp = a.p_first + p;
-    uint32_t m = a.nz_mask ? __ldg(a.nz_mask + p) : 0xffffffffu;
-    if (a.K < 32) m &= (1u << a.K) - 1u;
-    uint32_t jobs = 1u << 8;   // bit 8: the light-point pair
+    uint32_t m[KW];
 #pragma unroll
-    for (int g = 0; g < 8; ++g) jobs |= (((m >> (4 * g)) & 15u) != 0u ? 1u : 0u) << g;
+    for (int w = 0; w < KW; ++w) {
+        m[w] = a.nz_mask ? __ldg(a.nz_mask + (int64_t)w * a.stride + p) : 0xffffffffu;
+        const int left = a.K - 32 * w;
+        if (left <= 0)
+            m[w] = 0u;
+        else if (left < 32)
+            m[w] &= (1u << left) - 1u;
+    }
+    JobT jobs = (JobT)1 << (8 * KW);   // the last bit: the light-point pair
+#pragma unroll
+    for (int w = 0; w < KW; ++w)
+#pragma unroll
+        for (int g = 0; g < 8; ++g) jobs |= (JobT)(((m[w] >> (4 * g)) & 15u) != 0u ? 1u : 0u) << (8 * w + g);
     using LT = typename std::conditional<kLum64, double, float>::type;
     const LT* lp = reinterpret_cast<const LT*>(a.lum) + p;
     const uint64_t c_grp = (a.offset + (uint64_t)gp * (uint64_t)a.K) / 4 + 1;
@@ -874,13 +892,19 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
     double s = 0.0, wsel = 0.0, u0 = 0.0, u1 = 0.0;
     int sel = -1;
     while (jobs) {
-        const int g = __ffs(jobs) - 1;
+        const int g = (KW > 2) ? __ffsll((long long)jobs) - 1 : __ffs((uint32_t)jobs) - 1;
         jobs &= jobs - 1;
-        const bool lpj = g == 8;
-        const uint32_t bits = lpj ? 0u : (m >> (4 * g)) & 15u;
+        const bool lpj = g == 8 * KW;
+        uint32_t mw = 0u;
+#pragma unroll
+        for (int w = 0; w < KW; ++w)
+            if ((g >> 3) == w) mw = m[w];
+        const uint32_t bits = lpj ? 0u : (mw >> (4 * (g & 7))) & 15u;
         LT t[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) t[j] = ((bits >> j) & 1u) ? __ldg(lp + (int64_t)(4 * g + j) * a.stride) : LT(0);
+        uint2 vg = make_uint2(0u, 0u);
+        if (!kStage && !lpj) vg = __ldg(reinterpret_cast<const uint2*>(a.vis16 + p * a.vstride) + g);
         const U4 u = philox_block(lpj ? n_lp / 4 + 1 : c_grp + (uint64_t)g, a.key);
         if (lpj) {
             const bool hi = (n_lp & 2) != 0;
@@ -892,7 +916,7 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
         for (int j = 0; j < 4; ++j) {
             if ((bits >> j) & 1u) {
                 const int k = 4 * g + j;
-                const uint32_t pair = my[k >> 1];
+                const uint32_t pair = kStage ? my[k >> 1] : (j < 2 ? vg.x : vg.y);
                 const float vis = __half2float(__ushort_as_half((unsigned short)((j & 1) ? (pair >> 16) : (pair & 0xffffu))));
                 const double w = wrs_weight(vis, (double)t[j], a.floor);
                 s = __dadd_rn(s, w);
@@ -910,6 +934,15 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
     a.pts[3 * p] = y[0];
     a.pts[3 * p + 1] = y[1];
     a.pts[3 * p + 2] = y[2];
+}
+
+template <int KW>
+void launch_nlsg(const WArgs& a, const nvc_scene& sc, int64_t P, cudaStream_t s) {
+    const int thr = kWrsThreads;
+    if (a.lum_f64)
+        k_nls32g<true, KW><<<(int)((P + thr - 1) / thr), thr, 0, s>>>(a, sc);
+    else
+        k_nls32g<false, KW><<<(int)((P + thr - 1) / thr), thr, 0, s>>>(a, sc);
 }
 
 // Neural DI for K <= 32 (sampling.py:215-218): rgb = (sum_k v_k * factor_k *
@@ -1079,18 +1112,22 @@ int make_mnet(const nvc_model* m, MNet& q) {
     int col = 32;
     while (col < maxnp) col <<= 1;
     q.acc_cols = col;
-    q.tmem_cols = col * kSlots;
-    if (q.tmem_cols > 512) {
-        set_error("pipeline: %d TMEM columns needed", q.tmem_cols);
-        return NVC_ERR_UNSUPPORTED;
-    }
     q.alpha = m->alpha;
     q.out_sigmoid = m->out_sigmoid;
     q.sm_w = 0;
     q.sm_a0 = (q.wpack_halfs * 2 + 1023) / 1024 * 1024;
     q.sm_a1 = q.sm_a0 + kStages * ((kT * q.kp[0] * 2 + 1023) / 1024 * 1024);
-    q.sm_bias = q.sm_a1 + kSlots * ((kT * q.act_kp * 2 + 1023) / 1024 * 1024);
-    q.sm_total = q.sm_bias + (nb * 4 + 127) / 128 * 128 + 1024;
+    // as many tiles in flight (4, 2 or 1) as smem holds activation tiles for (C4's 3x128 MLP: 2)
+    for (q.slots = kSlots;; q.slots /= 2) {
+        q.sm_bias = q.sm_a1 + q.slots * ((kT * q.act_kp * 2 + 1023) / 1024 * 1024);
+        q.sm_total = q.sm_bias + (nb * 4 + 127) / 128 * 128 + 1024;
+        if (q.sm_total <= 226 * 1024 || q.slots == 1) break;
+    }
+    q.tmem_cols = col * q.slots;
+    if (q.tmem_cols > 512) {
+        set_error("pipeline: %d TMEM columns needed", q.tmem_cols);
+        return NVC_ERR_UNSUPPORTED;
+    }
     if (q.sm_total > 226 * 1024) {
         set_error("pipeline: %d bytes of shared memory needed", q.sm_total);
         return NVC_ERR_UNSUPPORTED;
@@ -1247,11 +1284,13 @@ int pipeline_select(const nvc_model* m, const nvc_scene* sc, int64_t P, int mode
     a.albedo = albedo;
     a.rgb = rgb;
     const bool aligned = K % 4 == 0 && offset % 4 == 0 && ((uint64_t)p_total * (uint64_t)K) % 2 == 0;
-    if (mode == 1 && K <= 32 && aligned && getenv("NVC_WRS_FORWARD") == nullptr) {
-        if (lum_f64)
-            k_nls32g<true><<<grid1(P, kWrsThreads), kWrsThreads, 0, s>>>(a, *sc);
+    if (mode == 1 && K <= 128 && aligned && getenv("NVC_WRS_FORWARD") == nullptr) {
+        if (K <= 32)
+            launch_nlsg<1>(a, *sc, P, s);
+        else if (K <= 64)
+            launch_nlsg<2>(a, *sc, P, s);
         else
-            k_nls32g<false><<<grid1(P, kWrsThreads), kWrsThreads, 0, s>>>(a, *sc);
+            launch_nlsg<4>(a, *sc, P, s);
     } else if (mode == 1 && K <= 32 && getenv("NVC_WRS_FORWARD") == nullptr) {
         if (lum_f64)
             k_nls32<true><<<grid1(P, kWrsThreads), kWrsThreads, 0, s>>>(a, *sc);

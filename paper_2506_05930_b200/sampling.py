@@ -164,13 +164,13 @@ class PixelCtx:
         return self._lum
 
     def mask_device(self, which: str = "lum"):
-        """Per-pixel nonzero bitmask of the lum/factor table (None when K > 32)."""
+        """Per-pixel nonzero bitmask of the lum/factor table: ceil(K/32) words per
+        pixel, word-major (word w of pixel p at w * stride + p)."""
         import torch
-        if self.dscene.n_lights > 32:
-            return None
         if which not in self._masks:
             t = self.lum_device() if which == "lum" else self.factor_device()
-            m = torch.empty(t.shape[1], dtype=torch.int32, device=self.device)
+            words = (self.dscene.n_lights + 31) // 32
+            m = torch.empty(words * t.shape[1], dtype=torch.int32, device=self.device)
             _lib.call("nvc_table_mask", t.data_ptr(), int(t.dtype == torch.float64), t.shape[1], self.n,
                       self.dscene.n_lights, m.data_ptr(), _lib.stream_ptr())
             self._masks[which] = m

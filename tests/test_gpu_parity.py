@@ -106,6 +106,21 @@ def test_infer_vs_oracle(boxes32, levels, tsize, hidden, k, f):
     assert np.abs(got16 - want).max() < FP16_VIS_TOL
 
 
+def test_c4_mlp_takes_the_tcgen05_path(boxes32):
+    """C4's 3x128 MLP with 128 outputs runs on the tcgen05 kernel (two tiles in
+    flight so the activation tiles fit in smem), not the fp32 fallback."""
+    cfg = grid_cfg(boxes32, 16, 1 << 19)
+    c = VisibilityCache(MODE_LIGHTS, 128, cfg, seed=3, hidden_dims=(128, 128, 128))
+    oc = O.Cache(O.Grid(levels=16, features_per_level=2, table_size=1 << 19, aabb_min=boxes32.aabb_min,
+                        aabb_max=boxes32.aabb_max), 128, hidden=(128, 128, 128), seed=3)
+    pos = np.random.default_rng(4).uniform(boxes32.aabb_min, boxes32.aabb_max, (70001, 3))
+    pt = torch.from_numpy(pos).to(DEV)
+    out = torch.empty((pos.shape[0], 128), dtype=torch.float32, device=DEV)
+    _lib.call("nvc_infer", c.model, pt.data_ptr(), pos.shape[0], PRECISION_FP16, out.data_ptr(),
+              _lib.ptr(c.query_workspace(pos.shape[0])), _lib.stream_ptr())      # raises if unsupported
+    assert np.abs(out.cpu().numpy() - oc.infer(pos)).max() < FP16_VIS_TOL
+
+
 def test_infer_trained_weights_fp16(boxes32):
     """fp16 tolerance also holds away from init (trained-scale weights)."""
     cfg = grid_cfg(boxes32, 16, 1 << 19)
@@ -353,6 +368,32 @@ class TestSampling:
             np.testing.assert_array_equal(big_w, ow)
             assert (ids >= 0).sum() > 100
 
+    @pytest.mark.parametrize("k,hidden", [(64, (64, 64, 64)), (128, (128, 128, 128))])
+    def test_wide_k_nls_equals_oracle(self, k, hidden, monkeypatch):
+        """K = 64 / 128 (rooms scenes, C4's 3x128 MLP): the grouped reservoir over 2 / 4
+        mask words (block-aligned offset) and the generic one (offset 1) are bit-exact."""
+        from paper_2506_05930_b200.render import gbuffer_device
+        from paper_2506_05930_b200.scenes import rooms_scene
+        s = scene_from_dict(rooms_scene(k))
+        cam = s.camera.resized(64, 40)
+        pos, nrm, alb, _, _ = gbuffer_device(s, cam)
+        ctx = PixelCtx(s, pos, nrm, alb)
+        c = VisibilityCache(MODE_LIGHTS, k, grid_cfg(s, 16, 1 << 19), hidden_dims=hidden)
+        c.grid_params = (np.random.default_rng(2).standard_normal(c.grid_params.shape) * 0.5).astype(np.float32)
+        vis16 = c.infer(pos.cpu().numpy(), precision=PRECISION_FP16)
+        sc = O.SceneArrays(s.triangles_v0, s.triangles_v1, s.triangles_v2, s.tri_material, s.tri_light, s.lt_kind,
+                           s.lt_verts, s.lt_normal, s.lt_radiance, s.mat_albedo, np.zeros(12))
+        lum = ctx.lum_matrix()
+        assert (lum != 0).any(axis=1).sum() > 100 and (lum == 0).any()
+        key = R.stream_key(0, 3, "light-select")
+        for offset in (0, 1):
+            oi, op, ow = O.nls_sample(sc, vis16, lum, key, offset=offset)
+            ids, pts, big_w = nls_sample_batch(ctx, c, R.Stream(key=key, offset=offset))
+            np.testing.assert_array_equal(ids, oi)
+            np.testing.assert_array_equal(pts, op)
+            np.testing.assert_array_equal(big_w, ow)
+            assert (ids >= 32).any()
+
     @pytest.mark.parametrize("grid", ["3", "7"])
     def test_fused_pipeline_many_tiles_per_cta(self, boxes32, g_scenes, monkeypatch, grid):
         """Few CTAs -> every CTA cycles its A0 / TMEM / lum stages many times."""
@@ -538,6 +579,28 @@ class TestTraining:
         np.testing.assert_array_equal(full.grad_fx[:gc].cpu().numpy(), shards[0].grad_fx[:gc].cpu().numpy())
         np.testing.assert_allclose(full.grad_fx[gc:].double().cpu().numpy(),
                                    shards[0].grad_fx[gc:].double().cpu().numpy(), rtol=1e-5, atol=2.0 ** 48 * 1e-9)
+
+    def test_wide_split_train_equals_fused_kernel(self, boxes32, monkeypatch):
+        """C4 widths (3x128 hidden, 128 outputs): the split step with W read from L1/L2
+        (k_train3<true>) and the single fused fp32 kernel (k_mlp<true>) produce
+        bit-identical parameters after three steps (same arithmetic and row partition)."""
+        g = np.random.default_rng(5)
+        pos = torch.from_numpy(g.uniform(boxes32.aabb_min, boxes32.aabb_max, (3000, 3))).to(DEV)
+        tgt = torch.from_numpy((g.random((3000, 128)) < 0.5).astype(np.float32)).to(DEV)
+
+        def run(fused):
+            if fused:
+                monkeypatch.setenv("NVC_TRAIN_FUSED", "1")
+            else:
+                monkeypatch.delenv("NVC_TRAIN_FUSED", raising=False)
+            c = VisibilityCache(MODE_LIGHTS, 128, grid_cfg(boxes32, 16, 1 << 19), seed=1,
+                                hidden_dims=(128, 128, 128))
+            losses = [c.train_step(pos, tgt) for _ in range(3)]
+            return c.params.cpu().numpy(), losses
+
+        (pa, la), (pb, lb) = run(False), run(True)
+        np.testing.assert_array_equal(pa, pb)
+        assert la == lb
 
     def test_compact_gradients_match_dense(self, pbox8, g_train):
         """Compact gradient slots train exactly like the dense accumulator (same arithmetic,
