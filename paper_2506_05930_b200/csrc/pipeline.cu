@@ -287,7 +287,7 @@ struct MNet {
     int np[NVC_MAX_LAYERS], kp[NVC_MAX_LAYERS];
     int wofs[NVC_MAX_LAYERS];     // halfs
     int64_t boff[NVC_MAX_LAYERS];
-    int wpack_halfs, act_kp, tmem_cols, acc_cols, slots;
+    int wpack_halfs, act_kp, tmem_cols, acc_cols, slots, ts_hid;
     float alpha;
     int out_sigmoid;
     int sm_w, sm_a0, sm_a1, sm_bias, sm_total;
@@ -533,9 +533,14 @@ __device__ __forceinline__ float tanh_fast(float x) {
 // the epilogue does pack + leaky only.  Four warpgroups (one tile in flight
 // each: 64 accumulator + 32 activation columns) and one MMA warp per group.
 // ---------------------------------------------------------------------------
-constexpr int kTsWG = 4;
-constexpr int kTsThreads = 160 * kTsWG;
-constexpr int kTsCols = 96;   // per warpgroup: 64 accumulator + 32 fp16-pair activation columns
+// HID = 64: four warpgroups x (64 accumulator + 32 fp16-pair activation columns);
+// HID = 128 (C4): two warpgroups x (128 + 64) -- TMEM holds 512 columns.
+template <int HID>
+struct TsCfg {
+    static constexpr int WG = HID == 64 ? 4 : 2;
+    static constexpr int kThreads = 160 * WG;
+    static constexpr int kCols = HID + HID / 2;
+};
 
 struct TSBars {
     uint64_t a0_full[2], acc_full;
@@ -559,11 +564,13 @@ __device__ __forceinline__ void tst16(uint32_t taddr, const uint32_t r[16]) {
 __device__ __forceinline__ void tst_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 template <int HID, int OUT, int KP0>
-__global__ void __launch_bounds__(kTsThreads, 1) k_mlp_ts(MNet net, const float* __restrict__ params,
-                                                         const uint16_t* __restrict__ wpack,
-                                                         const uint8_t* __restrict__ tiles, int64_t ntiles, int64_t P,
-                                                         __half* __restrict__ vis16, int64_t vstride) {
-    static_assert(HID == 64 && OUT <= 64 && KP0 <= 64, "TMEM layout sized for 64-wide hidden layers");
+__global__ void __launch_bounds__(TsCfg<HID>::kThreads, 1) k_mlp_ts(MNet net, const float* __restrict__ params,
+                                                                   const uint16_t* __restrict__ wpack,
+                                                                   const uint8_t* __restrict__ tiles, int64_t ntiles,
+                                                                   int64_t P, __half* __restrict__ vis16,
+                                                                   int64_t vstride) {
+    static_assert((HID == 64 || HID == 128) && OUT <= HID && KP0 <= 64, "TMEM layout: 64/128-wide hidden layers");
+    constexpr int kTsWG = TsCfg<HID>::WG, kTsThreads = TsCfg<HID>::kThreads, kTsCols = TsCfg<HID>::kCols;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ TSBars bars[kTsWG];
     __shared__ uint32_t tbase;
@@ -578,7 +585,7 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_mlp_ts(MNet net, const float*
     const int g = mma_warp ? warp - 4 * kTsWG : warp >> 2, wq = warp & 3;
     const int L = net.n_layers;
     constexpr int a0_bytes = kT * KP0 * 2;
-    const int bias_block = 64 * 32;                       // bytes per layer block (np <= 64 rows x 32 B)
+    const int bias_block = HID * 32;                      // bytes per layer block (np <= HID rows x 32 B)
     {
         const uint4* src = reinterpret_cast<const uint4*>(wpack);
         uint4* dst = reinterpret_cast<uint4*>(s_w);
@@ -617,8 +624,8 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_mlp_ts(MNet net, const float*
     TSBars& B = bars[g];
     const int64_t t0 = (int64_t)blockIdx.x * kTsWG + g, tstep = (int64_t)gridDim.x * kTsWG;
     const int n_wg = ntiles > t0 ? (int)((ntiles - 1 - t0) / tstep + 1) : 0;
-    const uint32_t acc = tmem + (uint32_t)(g * kTsCols);      // columns [0, 64): fp32 accumulator
-    const uint32_t act = acc + 64u;                            // columns [64, 96): fp16-pair activations
+    const uint32_t acc = tmem + (uint32_t)(g * kTsCols);      // columns [0, HID): fp32 accumulator
+    const uint32_t act = acc + (uint32_t)HID;                  // HID/2 columns: fp16-pair activations
     const int id = 1 + g;
     if (mma_warp) {
         // ---------------- MMA warp of warpgroup g ----------------
@@ -650,9 +657,14 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_mlp_ts(MNet net, const float*
                     const uint64_t da = desc_of(s32(s_a0 + (2 * g + b) * a0_bytes), kT, KP0, 0);
 #pragma unroll
                     for (int kk = 0; kk < KP0 / 16; ++kk) mma_elect(acc, da + 2 * kk, db + 2 * kk, idesc, kk > 0);
-                } else {
+                } else if (HID <= 64) {
 #pragma unroll
                     for (int kk = 0; kk < HID / 16; ++kk) mma_ts_elect(acc, act + 8u * kk, db + 2 * kk, idesc, kk > 0);
+                } else {   // K = 128 spans two swizzle blocks of the weight tile
+                    const uint32_t wl = w_addr + 2u * (uint32_t)net.wofs[l];
+#pragma unroll
+                    for (int kk = 0; kk < HID / 16; ++kk)
+                        mma_ts_elect(acc, act + 8u * kk, desc_of(wl, np, HID, kk), idesc, kk > 0);
                 }
                 // bias: + ones[128 x 16] x bias_l[np x 16]^T
                 mma_elect(acc, d_ones, desc_of(bias + l * bias_block, np, 16, 0), idesc, 1u);
@@ -672,19 +684,23 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_mlp_ts(MNet net, const float*
                 ph ^= 1u;
                 tc_after();
                 if (l < L - 1) {
-                    uint32_t r[HID];
 #pragma unroll
-                    for (int c = 0; c < HID; c += 16) tld16_nowait(acc + lane_base + (uint32_t)c, r + c);
-                    tld_wait();
-                    uint32_t h[HID / 2];
+                    for (int cb = 0; cb < HID; cb += 64) {   // 64 accumulator columns at a time
+                        uint32_t r[64];
 #pragma unroll
-                    for (int j = 0; j < HID / 2; ++j) {
-                        const __half2 z = __floats2half2_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-                        const __half2 y = __hmax2(z, __hmul2(z, al2));
-                        h[j] = *reinterpret_cast<const uint32_t*>(&y);
+                        for (int c = 0; c < 64; c += 16) tld16_nowait(acc + lane_base + (uint32_t)(cb + c), r + c);
+                        tld_wait();
+                        uint32_t h[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const __half2 z =
+                                __floats2half2_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+                            const __half2 y = __hmax2(z, __hmul2(z, al2));
+                            h[j] = *reinterpret_cast<const uint32_t*>(&y);
+                        }
+#pragma unroll
+                        for (int c = 0; c < 32; c += 16) tst16(act + lane_base + (uint32_t)(cb / 2 + c), h + c);
                     }
-#pragma unroll
-                    for (int c = 0; c < HID / 2; c += 16) tst16(act + lane_base + (uint32_t)c, h + c);
                     tst_wait();
                     tc_before();
                     asm volatile("bar.arrive %0, 160;" ::"r"(id) : "memory");
@@ -1140,34 +1156,44 @@ inline int grid1(int64_t n, int bs) { return (int)((n + bs - 1) / bs); }
 // smem layout of k_mlp_ts: weights | 2 A0 tiles per warpgroup | ones tile | bias blocks
 bool ts_layout(MNet& q) {
     if (q.n_layers < 2 || q.n_layers > 8) return false;
-    for (int l = 0; l < q.n_layers - 1; ++l)   // uniform 64-wide hidden layers (TMEM sized for them)
-        if (q.np[l] != 64 || (l > 0 && q.kp[l] != 64)) return false;
+    const int hid = q.np[0];
+    if (hid != 64 && hid != 128) return false;
+    for (int l = 0; l < q.n_layers - 1; ++l)   // uniform hidden layers (TMEM sized for them)
+        if (q.np[l] != hid || (l > 0 && q.kp[l] != hid)) return false;
     const int o = q.np[q.n_layers - 1], k = q.kp[0];
-    if (!(o == 16 || o == 32 || o == 48 || o == 64) || !(k == 16 || k == 32 || k == 64)) return false;
+    if (o % 16 != 0 || o > hid || (hid == 64 && o == 0) || !(k == 16 || k == 32 || k == 64)) return false;
+    if (hid == 128 && !(o == 32 || o == 64 || o == 128)) return false;
+    if (hid == 64 && !(o == 16 || o == 32 || o == 48 || o == 64)) return false;
+    const int wg = hid == 64 ? TsCfg<64>::WG : TsCfg<128>::WG;
+    q.ts_hid = hid;
     q.sm_w = 0;
     q.sm_a0 = (q.wpack_halfs * 2 + 1023) / 1024 * 1024;
-    q.sm_a1 = q.sm_a0 + 2 * kTsWG * ((kT * q.kp[0] * 2 + 1023) / 1024 * 1024);   // ones tile
+    q.sm_a1 = q.sm_a0 + 2 * wg * ((kT * q.kp[0] * 2 + 1023) / 1024 * 1024);   // ones tile
     q.sm_bias = q.sm_a1 + kT * 16 * 2;
-    q.sm_total = q.sm_bias + q.n_layers * 64 * 32 + 1024;
+    q.sm_total = q.sm_bias + q.n_layers * hid * 32 + 1024;
     return q.sm_total <= 227 * 1024;
 }
 
 template <int HID, int OUT, int KP0>
 int launch_ts(const MNet& w, const nvc_model* m, const uint8_t* tiles, int64_t ntiles, int64_t P, __half* vis16,
-              int64_t vstride, int grid, cudaStream_t s) {
+              int64_t vstride, int sms, cudaStream_t s) {
+    constexpr int wg = TsCfg<HID>::WG;
+    int grid = (int)std::min<int64_t>((ntiles + wg - 1) / wg, sms);
+    if (const char* e = getenv("NVC_QUERY_GRID")) grid = max(1, min(grid, atoi(e)));
     cudaFuncSetAttribute(k_mlp_ts<HID, OUT, KP0>, cudaFuncAttributeMaxDynamicSharedMemorySize, w.sm_total);
-    k_mlp_ts<HID, OUT, KP0><<<grid, kTsThreads, w.sm_total, s>>>(w, m->params, m->wpack, tiles, ntiles, P, vis16,
-                                                                 vstride);
+    k_mlp_ts<HID, OUT, KP0><<<grid, TsCfg<HID>::kThreads, w.sm_total, s>>>(w, m->params, m->wpack, tiles, ntiles, P,
+                                                                           vis16, vstride);
     return check_launch("k_mlp_ts");
 }
 
 int launch_mlp_ts(const MNet& w, const nvc_model* m, const uint8_t* tiles, int64_t ntiles, int64_t P, __half* vis16,
-                  int64_t vstride, int grid, cudaStream_t s) {
+                  int64_t vstride, int sms, cudaStream_t s) {
     const int o = w.np[w.n_layers - 1], k = w.kp[0];
-#define NVC_TS(O, K) \
-    if (o == O && k == K) return launch_ts<64, O, K>(w, m, tiles, ntiles, P, vis16, vstride, grid, s);
-    NVC_TS(16, 16) NVC_TS(16, 32) NVC_TS(16, 64) NVC_TS(32, 16) NVC_TS(32, 32) NVC_TS(32, 64)
-    NVC_TS(48, 16) NVC_TS(48, 32) NVC_TS(48, 64) NVC_TS(64, 16) NVC_TS(64, 32) NVC_TS(64, 64)
+#define NVC_TS(H, O, K) \
+    if (w.ts_hid == H && o == O && k == K) return launch_ts<H, O, K>(w, m, tiles, ntiles, P, vis16, vstride, sms, s);
+    NVC_TS(64, 16, 16) NVC_TS(64, 16, 32) NVC_TS(64, 16, 64) NVC_TS(64, 32, 16) NVC_TS(64, 32, 32) NVC_TS(64, 32, 64)
+    NVC_TS(64, 48, 16) NVC_TS(64, 48, 32) NVC_TS(64, 48, 64) NVC_TS(64, 64, 16) NVC_TS(64, 64, 32) NVC_TS(64, 64, 64)
+    NVC_TS(128, 32, 32) NVC_TS(128, 64, 32) NVC_TS(128, 128, 16) NVC_TS(128, 128, 32) NVC_TS(128, 128, 64)
 #undef NVC_TS
     set_error("k_mlp_ts: shape not instantiated");
     return NVC_ERR_UNSUPPORTED;
@@ -1205,9 +1231,7 @@ int run_front(const nvc_model* m, const double* pos, int64_t P, uint8_t* tiles, 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     MNet t = q;
     if (ts_layout(t) && !getenv("NVC_MLP_QUADS")) {
-        int grid = (int)std::min<int64_t>((ntiles + kTsWG - 1) / kTsWG, sms);
-        if (const char* e = getenv("NVC_QUERY_GRID")) grid = max(1, min(grid, atoi(e)));
-        rc = launch_mlp_ts(t, m, tiles, ntiles, P, vis16, vstride, grid, s);
+        rc = launch_mlp_ts(t, m, tiles, ntiles, P, vis16, vstride, sms, s);
     } else {
         cudaFuncSetAttribute(k_mlp_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, q.sm_total);
         int grid = (int)(ntiles < sms ? ntiles : sms);

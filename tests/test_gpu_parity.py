@@ -106,9 +106,13 @@ def test_infer_vs_oracle(boxes32, levels, tsize, hidden, k, f):
     assert np.abs(got16 - want).max() < FP16_VIS_TOL
 
 
-def test_c4_mlp_takes_the_tcgen05_path(boxes32):
-    """C4's 3x128 MLP with 128 outputs runs on the tcgen05 kernel (two tiles in
-    flight so the activation tiles fit in smem), not the fp32 fallback."""
+@pytest.mark.parametrize("variant", ["ts", "NVC_MLP_QUADS"])
+def test_c4_mlp_takes_the_tcgen05_path(boxes32, variant, monkeypatch):
+    """C4's 3x128 MLP with 128 outputs runs on the tcgen05 kernels -- TS mode (two
+    warpgroups x 192 TMEM columns) and SS mode (two tiles in flight so the
+    activation tiles fit in smem) -- not the fp32 fallback."""
+    if variant != "ts":
+        monkeypatch.setenv(variant, "1")
     cfg = grid_cfg(boxes32, 16, 1 << 19)
     c = VisibilityCache(MODE_LIGHTS, 128, cfg, seed=3, hidden_dims=(128, 128, 128))
     oc = O.Cache(O.Grid(levels=16, features_per_level=2, table_size=1 << 19, aabb_min=boxes32.aabb_min,
