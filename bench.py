@@ -509,6 +509,69 @@ def ndi4k_arm(args) -> None:
         dist.destroy_process_group()
 
 
+def sweep_arm(args) -> None:
+    """C5: query throughput sweep, N = 2^16 .. 2^26 shading points x
+    K in {8, 32, 128} (boxes8 / boxes32 / rooms128).  Points ~ U(scene AABB) from
+    the reference stream ("sweep"), normals +y, albedo 0.73; one step = encoder +
+    tcgen05 MLP + FP64 WRS + light point over all N points (inputs resident).
+    Grid L=16 T=2^19 F=2; MLP 3x64 for K <= 32, 3x128 for K = 128 (C4)."""
+    import torch
+
+    from paper_2506_05930_b200 import MODE_LIGHTS, HashGridConfig, VisibilityCache
+    from paper_2506_05930_b200 import rng as R
+    from paper_2506_05930_b200.sampling import PixelCtx, nls_sample_device
+    from paper_2506_05930_b200.scene import scene_from_dict
+    from paper_2506_05930_b200.scenes import boxes_scene, rooms_scene
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(dev)
+    max_log2 = int(os.environ.get("NVC_SWEEP_MAX_LOG2", "26"))
+    rows = []
+    for k, mk, hid in ((8, lambda: boxes_scene(8), (64, 64, 64)), (32, lambda: boxes_scene(32), (64, 64, 64)),
+                       (128, lambda: rooms_scene(128), (128, 128, 128))):
+        scene = scene_from_dict(mk())
+        n_max = 1 << max_log2
+        g = R.stream(0, "sweep")
+        pos_all = torch.from_numpy(g.uniform(scene.aabb_min, scene.aabb_max, (n_max, 3))).to(dev)
+        grid = HashGridConfig(levels=LEVELS, table_size=TABLE, features_per_level=FEATS, aabb_min=scene.aabb_min,
+                              aabb_max=scene.aabb_max)
+        cache = VisibilityCache(MODE_LIGHTS, k, grid, seed=0, hidden_dims=hid, device=dev)
+        for lg in range(16, max_log2 + 1, 2):
+            n = 1 << lg
+            pos = pos_all[:n]
+            nrm = torch.zeros_like(pos)
+            nrm[:, 1] = 1.0
+            alb = torch.full_like(pos, 0.73)
+            ctx = PixelCtx(scene, pos, nrm, alb)
+            ctx.lum_device()
+            ctx.mask_device("lum")
+            key = R.stream_key(0, lg, "light-select")
+            for _ in range(args.warmup):
+                nls_sample_device(ctx, cache, key)
+            reps = max(2, min(args.steps, int(2e8 // (n * max(k, 32)))))
+            st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            st.record()
+            for _ in range(reps):
+                nls_sample_device(ctx, cache, key)
+            en.record()
+            torch.cuda.synchronize()
+            ms = st.elapsed_time(en) / reps
+            rows.append({"n": n, "k": k, "ms": ms, "queries_per_s": n / (ms * 1e-3), "reps": reps})
+            del ctx, nrm, alb
+            torch.cuda.empty_cache()
+        del cache, pos_all
+        torch.cuda.empty_cache()
+    head = max((r for r in rows if r["k"] == 32), key=lambda r: r["n"])
+    print(json.dumps({"metric": "visibility queries/s (encode+MLP+WRS), C5 sweep; value at the largest N, K=32",
+                      "value": head["queries_per_s"], "unit": "queries/s", "n_gpus": 1, "steps": head["reps"],
+                      "warmup": args.warmup, "ms_per_step": head["ms"], "higher_is_better": True, "scaling": "weak",
+                      "vs_baseline": None, "dtype": "fp16 MLP / fp64 index+WRS",
+                      "data": "synthetic (points U(AABB) from stream (0, 'sweep'), normals +y, albedo 0.73)",
+                      "config": {"workload": "C5: N = 2^16..2^%d x K in {8 (boxes8), 32 (boxes32), 128 (rooms128)}"
+                                             % max_log2, "sweep": rows}}), flush=True)
+
+
 def reference_arm(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -541,10 +604,11 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-sample", type=int, default=24576)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["c2", "ndi4k", "render", "c4"], default="c2",
+    ap.add_argument("--workload", choices=["c2", "ndi4k", "render", "c4", "sweep"], default="c2",
                     help="c2: the headline online frame (default); ndi4k: C3 Neural DI at 4K; "
                          "render: the c2 frame plus shading pass 5 (one shadow ray per pixel); "
-                         "c4: the online frame on rooms128 with K=128 and a 3x128 MLP")
+                         "c4: the online frame on rooms128 with K=128 and a 3x128 MLP; "
+                         "sweep: C5 query throughput over N = 2^16..2^26 and K = 8/32/128")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -552,6 +616,8 @@ def main() -> None:
         reference_arm(args)
     elif args.workload == "ndi4k":
         ndi4k_arm(args)
+    elif args.workload == "sweep":
+        sweep_arm(args)
     else:
         gpu_arm(args)
 
