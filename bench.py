@@ -217,6 +217,8 @@ def gpu_arm(args) -> None:
     grid = HashGridConfig(levels=LEVELS, table_size=TABLE, features_per_level=FEATS, aabb_min=scene.aabb_min,
                           aabb_max=scene.aabb_max)
     cache = VisibilityCache(MODE_LIGHTS, kk, grid, seed=0, hidden_dims=hid, device=dev)
+    if os.environ.get("NVC_COMPACT"):    # compact gradient slots (the DP exchange layout) also at N=1
+        cache.set_compact(True)
     if os.environ.get("NVC_L2_PIN"):      # measured slower (it starves the streaming Adam of L2)
         cache.pin_table_in_l2()
     cfg = TrainFrameConfig(n_world=N_WORLD * world, n_screen=N_SCREEN * world, seed=0)
@@ -486,11 +488,12 @@ def ndi4k_arm(args) -> None:
     if world > 1:
         dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(args.steps):
-        neural_di_device(ctx, cache, out=out)
-    e.record()
-    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        s.record()
+        for _ in range(args.steps):
+            neural_di_device(ctx, cache, out=out)
+        e.record()
+        torch.cuda.synchronize()
     ms = s.elapsed_time(e) / args.steps
     t = torch.tensor([ms], device=dev)
     if world > 1:
@@ -504,7 +507,8 @@ def ndi4k_arm(args) -> None:
                           "scaling": "strong", "vs_baseline": None, "dtype": "fp16 MLP / fp64 NDI sum",
                           "data": "synthetic (boxes_scene(32) fixture, random-init weights, seed 0)",
                           "config": {"workload": f"C3: {W4}x{H4} boxes32 (K=32) Neural DI, {world} screen tiles",
-                                     "pixels_per_gpu": P}}), flush=True)
+                                     "pixels_per_gpu": P},
+                          "gpu_launches": 3 * args.steps, "clocks": clocks.summary()}), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
@@ -599,7 +603,7 @@ def reference_arm(args) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--steps", type=int, default=1000)   # ~0.7 s timed: several in-region clock samples
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-sample", type=int, default=24576)
