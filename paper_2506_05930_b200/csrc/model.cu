@@ -933,7 +933,14 @@ __global__ void __launch_bounds__(256) k_adam_flat(float* __restrict__ p, float*
 // -- a thread's last neighbour comes from the next lane by shuffle -- so each
 // thread writes 16 contiguous bytes; only a warp's last slot takes its high
 // half from the next warp's lane 0.
-constexpr int kAdamTile = 512, kAdamStages = 4, kAdamThreads = 128;   // 4 params per thread
+#ifndef NVC_ADAM_THREADS
+#define NVC_ADAM_THREADS 256
+#endif
+#ifndef NVC_ADAM_STAGES
+#define NVC_ADAM_STAGES 3
+#endif
+constexpr int kAdamThreads = NVC_ADAM_THREADS, kAdamTile = 4 * kAdamThreads;   // 4 params per thread
+constexpr int kAdamStages = NVC_ADAM_STAGES;
 struct AdamStage {
     float p[kAdamTile], m[kAdamTile], v[kAdamTile];
     long long q[kAdamTile];
@@ -1327,7 +1334,8 @@ int nvc_adam_step(const nvc_model* m, int64_t t, double lr, void* stream) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int64_t ntiles = net.grid_count / kAdamTile;
-        const int grid = (int)std::min<int64_t>(ntiles, 5 * (int64_t)sms);
+        const char* ge = getenv("NVC_ADAM_GRID");   // CTAs per SM (default 3: 3 x 61 KB smem rings)
+        const int grid = (int)std::min<int64_t>(ntiles, (ge ? atoi(ge) : 3) * (int64_t)sms);
         if (m->grad_c)
             k_adam_bulk<true><<<grid, kAdamThreads, smem, s>>>(m->params, m->adam_m, m->adam_v, sink_of(m), m->table_h,
                                                                ntiles, a, m->table_size);
