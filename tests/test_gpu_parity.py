@@ -703,6 +703,50 @@ class TestTraining:
         np.testing.assert_allclose(a, bb, rtol=1e-5, atol=2.0 ** 48 * 1e-9)
 
 
+def test_odd_light_count_mixed_emitters():
+    """K = 5 (three rect + two point lights): the per-light reservoir paths (K % 4 != 0),
+    shading, the training batch and its shadow-ray targets against the oracle."""
+    from paper_2506_05930_b200.render import gbuffer_device, shade_batch
+    from paper_2506_05930_b200.training import BatchBuffers, gen_batch_device
+    d = boxes_scene(8)
+    lights = d["lights"][:5]
+    for i in (1, 3):
+        lt = lights[i]
+        c, u, v = (np.array(lt[k], float) for k in ("corner", "edge_u", "edge_v"))
+        area = float(np.linalg.norm(np.cross(u, v)))
+        lights[i] = {"type": "point", "position": list(c + 0.5 * u + 0.5 * v),
+                     "intensity": [area * r for r in lt["radiance"]]}
+    d["lights"] = lights
+    s = scene_from_dict(d)
+    cam = s.camera.resized(48, 32)
+    sa = O.SceneArrays(s.triangles_v0, s.triangles_v1, s.triangles_v2, s.tri_material, s.tri_light, s.lt_kind,
+                       s.lt_verts, s.lt_normal, s.lt_radiance, s.mat_albedo,
+                       np.array([*cam.position, *cam.look_at, *cam.up, cam.fov_deg, cam.width, cam.height], float),
+                       lt_area=s.lt_area)
+    pos, nrm, alb, _, _ = gbuffer_device(s, cam)
+    ctx = PixelCtx(s, pos, nrm, alb)
+    c = VisibilityCache(MODE_LIGHTS, 5, grid_cfg(s, 8, 1 << 14), seed=2, hidden_dims=(64, 64))
+    c.grid_params = (np.random.default_rng(6).standard_normal(c.grid_params.shape) * 0.5).astype(np.float32)
+    vis16 = c.infer(pos.cpu().numpy(), precision=PRECISION_FP16)
+    key = R.stream_key(0, 4, "light-select")
+    for offset in (0, 2):
+        oi, op, ow = O.nls_sample(sa, vis16, ctx.lum_matrix(), key, offset=offset)
+        ids, pts, big_w = nls_sample_batch(ctx, c, R.Stream(key=key, offset=offset))
+        np.testing.assert_array_equal(ids, oi)
+        np.testing.assert_array_equal(pts, op)
+        np.testing.assert_array_equal(big_w, ow)
+    assert set(np.unique(ids)) >= {1, 3} and (ids >= 0).sum() > 100
+    p_h, n_h, a_h = (t.cpu().numpy() for t in (pos, nrm, alb))
+    np.testing.assert_array_equal(shade_batch(s, p_h, n_h, a_h, ids, pts, big_w),
+                                  O.shade(sa, p_h, n_h, a_h, ids, pts, big_w))
+    bufs = BatchBuffers(256, 256, 5, DEV, 1)
+    gen_batch_device(s, cam, bufs, 3, 1, 0, 0, 1)
+    opos, otgt = O.train_batch(sa, 3, 1, 0, n_world=256, n_screen=256)
+    b = int(bufs.n_rows.item())
+    np.testing.assert_array_equal(bufs.pos[:b].cpu().numpy(), opos)
+    np.testing.assert_array_equal(bufs.tgt[:b].cpu().numpy(), otgt)
+
+
 def test_snapshot_roundtrip(tmp_path, boxes32):
     c = VisibilityCache(MODE_LIGHTS, 32, grid_cfg(boxes32, 8, 1 << 14), hidden_dims=(64, 64))
     c.step = 7
