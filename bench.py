@@ -407,9 +407,9 @@ def gpu_arm(args) -> None:
             except Exception:
                 traffic = None
         clk = clocks.summary()
-        metric, unit = (RENDER_METRIC, "pixels/s") if shade else ((C4_METRIC, UNIT) if c4 else (METRIC, UNIT))
+        metric, munit = (RENDER_METRIC, "pixels/s") if shade else ((C4_METRIC, UNIT) if c4 else (METRIC, UNIT))
         line = {
-            "metric": metric, "value": P * world / (ms * 1e-3), "unit": unit, "n_gpus": world,
+            "metric": metric, "value": P * world / (ms * 1e-3), "unit": munit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "fp16 MLP / fp64 index+WRS / fp32 train",
             "data": f"synthetic ({'rooms_scene(128)' if c4 else 'boxes_scene(32)'} fixture, random-init weights, seed 0)",
@@ -425,7 +425,7 @@ def gpu_arm(args) -> None:
                        "stage_ms": {"train_frame": tr_ms, "query": q_ms, "k_enc_tiles2": k_ms[0],
                                     "k_mlp_ts": k_ms[1], "k_nls32": k_ms[2],
                                     **({"k_shade": statistics.median(split_shade)} if shade else {})}},
-            "e2e": {"value": P * world / (e2e_ms * 1e-3), "unit": unit,
+            "e2e": {"value": P * world / (e2e_ms * 1e-3), "unit": munit,
                     "h2d_bytes_per_step": int(pos_host.numel() * 8),
                     "d2h_bytes_per_step": int(sum(h.numel() * h.element_size() for h in outs_host) + 8)},
             "gpu_launches": (LAUNCHES_PER_FRAME + int(shade)) * args.steps,
@@ -440,6 +440,7 @@ def gpu_arm(args) -> None:
                                         "vs_random_probe": (enc_gathers / probe) if probe else None}},
             "clocks": clk,
         }
+        assert line["roofline"]["unit"] in ("GB/s", "TFLOP/s") and line["roofline"]["bound"] in ("hbm", "tensor")
         if world == 1 and not args.no_cpu_baseline and not shade and not c4:
             line["cpu_baseline"] = cpu_reference(sample_pixels=args.cpu_sample)
         print(json.dumps(line), flush=True)
