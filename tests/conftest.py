@@ -51,3 +51,24 @@ def g_train():
 @pytest.fixture(scope="session")
 def g_shade():
     return golden("shade")
+
+
+@pytest.fixture(scope="session")
+def g_snap():
+    return golden("snapshot")
+
+
+def read_vcsnap(path):
+    """The reference's VCSNAP1 reader (cache.py:99-117) restated: (header, {name: array})."""
+    import json
+    import struct
+    with open(path, "rb") as fh:
+        assert fh.read(8) == b"VCSNAP1\n"
+        (hlen,) = struct.unpack("<I", fh.read(4))
+        header = json.loads(fh.read(hlen).decode("utf-8"))
+        arrays = {}
+        for spec in header["arrays"]:
+            shape = tuple(spec["shape"])
+            arrays[spec["name"]] = np.frombuffer(fh.read(4 * int(np.prod(shape))), dtype="<f4").reshape(shape)
+        assert fh.read() == b""
+    return header, arrays

@@ -267,6 +267,25 @@ def gen_shade(out: dict) -> None:
                                  smp["nls_pts"], smp["nls_W"])
 
 
+def gen_snapshot(out: dict) -> None:
+    """A VCSNAP1 file written by the reference cache after two train steps (cache.py:77-117),
+    plus its infer() output on fixed positions -- pins on-disk interop both ways."""
+    s = scene_from_dict(boxes_scene(8))
+    cfg = HashGridConfig(levels=4, table_size=1 << 10, features_per_level=2, aabb_min=s.aabb_min,
+                         aabb_max=s.aabb_max)
+    c = VisibilityCache(MODE_LIGHTS, 8, cfg, seed=4)
+    g = R.stream(9, "golden-snapshot")
+    pos = g.uniform(s.aabb_min, s.aabb_max, (64, 3))
+    for _ in range(2):
+        c.train_step(pos, (g.random((64, 8)) < 0.5).astype(np.float32))
+    path = os.path.join(HERE, "ref_snapshot.vcsnap")
+    c.save(path)
+    q = g.uniform(s.aabb_min, s.aabb_max, (257, 3))
+    out["snap_pos"] = q
+    out["snap_infer"] = c.infer(q)
+    out["snap_step"] = np.array(c.step)
+
+
 def gen_training(out: dict) -> None:
     s8 = scene_from_dict(boxes_scene(8))
     pts = gen_screen_samples(s8, s8.camera, 256, R.stream(6))
@@ -369,7 +388,7 @@ def main() -> None:
     quick = "--quick" in sys.argv
     groups = {
         "rng": gen_rng, "scenes": gen_scenes, "mlp": gen_mlp,
-        "sampling": gen_sampling, "training": gen_training, "shade": gen_shade,
+        "sampling": gen_sampling, "training": gen_training, "shade": gen_shade, "snapshot": gen_snapshot,
     }
     only = [a for a in sys.argv[1:] if not a.startswith("-")]
     if only:   # regenerate just the named groups, e.g. `make_golden.py shade`

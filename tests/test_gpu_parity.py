@@ -758,6 +758,26 @@ def test_snapshot_roundtrip(tmp_path, boxes32):
     np.testing.assert_array_equal(c.infer(pos), d.infer(pos))
 
 
+def test_reference_snapshot_interop(tmp_path, g_snap):
+    """VCSNAP1 both ways: a snapshot the reference wrote loads here and infers its
+    values; our re-save carries byte-identical arrays and every header field the
+    reference's loader reads (cache.py:77-117)."""
+    import os
+    from conftest import read_vcsnap
+    ref = os.path.join(os.path.dirname(__file__), "golden", "ref_snapshot.vcsnap")
+    c = VisibilityCache.load(ref)
+    assert c.step == int(g_snap["snap_step"]) and c.net_cfg.hidden_dims == (32, 32)
+    np.testing.assert_allclose(c.infer(g_snap["snap_pos"], precision=PRECISION_FP32), g_snap["snap_infer"],
+                               rtol=0, atol=1e-6)
+    c.save(tmp_path / "again.vcsnap")
+    h0, a0 = read_vcsnap(ref)
+    h1, a1 = read_vcsnap(tmp_path / "again.vcsnap")
+    for k in ("mode", "output_dim", "step", "grid", "train", "arrays"):
+        assert h1[k] == h0[k], k
+    for k in a0:
+        np.testing.assert_array_equal(a1[k], a0[k])
+
+
 def test_native_library_is_loaded():
     import ctypes  # noqa: F401
     lib = _lib.load()

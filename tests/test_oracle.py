@@ -245,6 +245,24 @@ class TestShade:
         np.testing.assert_array_equal(rgb, g_shade["nls_rgb"])
 
 
+class TestSnapshot:
+    def test_reference_snapshot_reads_and_infers(self, g_snap):
+        """The reference's VCSNAP1 file, parsed by the restated reader and evaluated by
+        the oracle, reproduces the reference cache's infer() (cache.py:54-58, 99-117)."""
+        import os
+        from conftest import read_vcsnap
+        header, arrays = read_vcsnap(os.path.join(os.path.dirname(__file__), "golden", "ref_snapshot.vcsnap"))
+        assert header["mode"] == "lights" and header["step"] == int(g_snap["snap_step"])
+        gc = header["grid"]
+        g = O.Grid(levels=gc["levels"], base_resolution=gc["base_resolution"],
+                   per_level_scale=gc["per_level_scale"], features_per_level=gc["features_per_level"],
+                   table_size=gc["table_size"], aabb_min=gc["aabb_min"], aabb_max=gc["aabb_max"])
+        n = sum(1 for k in arrays if k.startswith("w"))
+        feats, _ = O.encode(g, arrays["grid"], g_snap["snap_pos"])
+        out, _, _ = O.mlp_forward([arrays[f"w{i}"] for i in range(n)], [arrays[f"b{i}"] for i in range(n)], feats)
+        np.testing.assert_allclose(out, g_snap["snap_infer"], rtol=0, atol=1e-6)
+
+
 class TestTrainingCurve:
     def test_first_step_matches_reference(self, g_scenes, g_train):
         s = scene(g_scenes, "pbox8")
