@@ -72,3 +72,8 @@ def read_vcsnap(path):
             arrays[spec["name"]] = np.frombuffer(fh.read(4 * int(np.prod(shape))), dtype="<f4").reshape(shape)
         assert fh.read() == b""
     return header, arrays
+
+
+@pytest.fixture(scope="session")
+def g_clusters():
+    return golden("clusters")

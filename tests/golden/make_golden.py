@@ -286,6 +286,47 @@ def gen_snapshot(out: dict) -> None:
     out["snap_step"] = np.array(c.step)
 
 
+def gen_clusters(out: dict) -> None:
+    """Clustered NVC (sampling.py:252-359, training.py:121-128): k-means on the
+    rooms scenes' lights, cluster shadow-ray targets, and the two-step sampler
+    with a fixed cluster-visibility cache."""
+    from viscache.sampling import clustered_sample_batch, kmeans_cluster
+    for tag, n_lights, k in (("r128k16", 128, 16), ("r1024k32", 1024, 32), ("b32k8", 32, 8), ("b8k8", 8, 8)):
+        s = scene_from_dict(rooms_scene(n_lights) if tag.startswith("r") else boxes_scene(n_lights))
+        cs = kmeans_cluster(s.lights, k, R.stream(0, R.CLUSTERING))
+        out[f"km_{tag}_centroids"] = cs.centroids
+        out[f"km_{tag}_sizes"] = np.array([mem.size for mem in cs.members])
+        out[f"km_{tag}_members"] = np.concatenate(cs.members)
+        out[f"km_{tag}_history"] = np.array(cs.inertia_history)
+    # targets: rooms128 with 16 clusters, a few hundred rows
+    s = scene_from_dict(rooms_scene(128))
+    cs = kmeans_cluster(s.lights, 16, R.stream(0, R.CLUSTERING))
+    g = R.stream(5, "golden-cluster-pos")
+    pos = g.uniform(s.aabb_min, s.aabb_max, (777, 3))
+    out["ct_pos"] = pos
+    out["ct_tgt"] = compute_visibility_targets(pos, s, R.stream(0, 2, 0, R.TARGETS), clusters=cs)
+    # two-step sampler on a 48x32 rooms128 G-buffer with fixed cluster visibilities
+    cam = Camera(position=s.camera.position, look_at=s.camera.look_at, up=s.camera.up,
+                 fov_deg=s.camera.fov_deg, width=48, height=32)
+    gb = make_gbuffer(s, cam)
+    ctx = PixelCtx(s, gb.flat("position"), gb.flat("normal"), gb.flat("albedo"))
+    vis = g.random((ctx.n, 16)).astype(np.float32)
+    vis[::7] = 0.25
+
+    class Fixed:
+        mode = "clusters"
+        output_dim = 16
+
+        def infer(self, positions):
+            return vis[: positions.shape[0]]
+
+    ids, pts, big_w = clustered_sample_batch(ctx, Fixed(), cs, R.stream(0, 3, R.LIGHT_SELECT))
+    out["cs_vis"] = vis
+    out["cs_ids"], out["cs_pts"], out["cs_W"] = ids, pts, big_w
+    for k in ("position", "normal", "albedo"):
+        out["cs_gb_" + k] = gb.flat(k)
+
+
 def gen_training(out: dict) -> None:
     s8 = scene_from_dict(boxes_scene(8))
     pts = gen_screen_samples(s8, s8.camera, 256, R.stream(6))
@@ -389,6 +430,7 @@ def main() -> None:
     groups = {
         "rng": gen_rng, "scenes": gen_scenes, "mlp": gen_mlp,
         "sampling": gen_sampling, "training": gen_training, "shade": gen_shade, "snapshot": gen_snapshot,
+        "clusters": gen_clusters,
     }
     only = [a for a in sys.argv[1:] if not a.startswith("-")]
     if only:   # regenerate just the named groups, e.g. `make_golden.py shade`

@@ -167,6 +167,24 @@ def test_shadow_accel_tables(name):
     assert r == max(np.abs(b.v0).max(), np.abs(b.v1).max(), np.abs(b.v2).max())
 
 
+@pytest.mark.parametrize("tag,fn,k", [("r128k16", lambda: rooms_scene(128), 16), ("r1024k32", lambda: rooms_scene(1024), 32),
+                                      ("b32k8", lambda: boxes_scene(32), 8), ("b8k8", lambda: boxes_scene(8), 8)])
+def test_kmeans_matches_reference(g_clusters, tag, fn, k):
+    """Light clustering (sampling.py:252-295): members, centroids and inertia history
+    equal the reference's for the same "clustering" stream."""
+    from paper_2506_05930_b200.clusters import kmeans_cluster
+    cs = kmeans_cluster(scene_from_dict(fn()).lights, k, R.stream(0, R.CLUSTERING))
+    np.testing.assert_array_equal(cs.centroids, g_clusters[f"km_{tag}_centroids"])
+    np.testing.assert_array_equal([m.size for m in cs.members], g_clusters[f"km_{tag}_sizes"])
+    np.testing.assert_array_equal(np.concatenate(cs.members), g_clusters[f"km_{tag}_members"])
+    np.testing.assert_array_equal(cs.inertia_history, g_clusters[f"km_{tag}_history"])
+    off, flat = cs.packed()
+    assert off[-1] == flat.size == sum(m.size for m in cs.members)
+    assert (cs.assignment[flat[off[3]:off[4]]] == 3).all()
+    with pytest.raises(ValueError):
+        kmeans_cluster(scene_from_dict(fn()).lights, 0, R.stream(0, R.CLUSTERING))
+
+
 def test_no_device_means_loud_failure():
     import torch
     if torch.cuda.is_available():
