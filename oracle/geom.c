@@ -231,3 +231,14 @@ void orc_light_factors(int64_t n, const double *pos, const double *nrm, int64_t 
                 ? rect_factor(pos + 3 * i, nrm + 3 * i, verts + 12 * j, lnormal + 3 * j)
                 : point_factor(pos + 3 * i, nrm + 3 * i, verts + 12 * j);
 }
+
+/* numpy/OpenBLAS float64 (r,3)@(3,c) as it rounds here (pinned by
+ * tests/golden/clusters.npz): gemm shapes fma(a2,b2, fma(a1,b1, a0*b0)),
+ * gemv shapes (r == 1 or c == 1) fma(a2,b2, fma(a0,b0, a1*b1)). */
+void orc_dot3_fma(int64_t n, const double *a, const double *b, int32_t gemv, double *out) {
+    for (int64_t i = 0; i < n; ++i) {
+        const double *x = a + 3 * i, *y = b + 3 * i;
+        out[i] = gemv ? fma(x[2], y[2], fma(x[0], y[0], x[1] * y[1]))
+                      : fma(x[2], y[2], fma(x[1], y[1], x[0] * y[0]));
+    }
+}

@@ -672,3 +672,105 @@ def shade(s: SceneArrays, pos, nrm, alb, ids, pts, big_w):              # render
     amp = geom * big_w * vis
     out[live] = (alb[live] / np.pi) * s.lt_radiance[safe[live]] * amp[live, None]
     return out
+
+
+# ---------------------------------------------------------------------------
+# Clustered NVC: training.py:121-128, sampling.py:302-352
+# ---------------------------------------------------------------------------
+
+def bounded_ints(key: int, start: int, count: int, n: int, pending=None):
+    """numpy Generator.integers(0, n, size=count) with the stream at 64-bit output
+    `start`: Lemire's bounded draw (with its rare rejection loop) on 32-bit draws.
+    A 32-bit draw is the low half of a fresh output, whose high half the bit
+    generator keeps for the next 32-bit draw -- also across calls (`pending`, the
+    kept half or None); 64-bit draws (random()) skip it.  Returns
+    (values, 64-bit outputs consumed, pending half after the call)."""
+    if n == 1:
+        return np.zeros(count, np.int64), 0, pending
+    out = np.empty(count, np.int64)
+    thresh = ((1 << 32) - n) % n
+    words = raw_at(key, np.arange(start, start + (count + 1) // 2 + 8, dtype=np.uint64))
+    used = 0
+
+    def next32():
+        nonlocal used, words, pending
+        if pending is not None:
+            v, pending = pending, None
+            return v
+        if used >= words.size:
+            words = np.concatenate([words, raw_at(key, np.arange(start + words.size, start + words.size + 64,
+                                                                 dtype=np.uint64))])
+        w = int(words[used])
+        used += 1
+        pending = w >> 32
+        return w & 0xFFFFFFFF
+
+    for i in range(count):
+        m = next32() * n
+        while (m & 0xFFFFFFFF) < thresh:
+            m = next32() * n
+        out[i] = m >> 32
+    return out, used, pending
+
+
+def cluster_targets(s: SceneArrays, pos: np.ndarray, sizes, members, key: int) -> np.ndarray:
+    """compute_visibility_targets(clusters=...) (training.py:121-128): per cluster a
+    uniform member (integers) then its light point (random((b,2)))."""
+    b = pos.shape[0]
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    out = np.empty((b, len(sizes)), np.float32)
+    st, pending = 0, None
+    for j, size in enumerate(sizes):
+        mem = np.asarray(members[off[j]:off[j + 1]])
+        pick, used, pending = bounded_ints(key, st, b, int(size), pending)
+        st += used
+        u = uniform_at(key, st + np.arange(2 * b)).reshape(b, 2)
+        st += 2 * b
+        out[:, j] = s.visibility(pos, s.light_points(mem[pick], u))
+    return out
+
+
+def matmul3(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """(r,3)@(3,c) in float64 with the reference's BLAS rounding (orc_dot3_fma)."""
+    r, c = a.shape[0], b.shape[1]
+    aa = np.ascontiguousarray(np.repeat(a, c, axis=0))
+    bb = np.ascontiguousarray(np.tile(b.T, (r, 1)))
+    out = np.empty(r * c)
+    lib().orc_dot3_fma(ctypes.c_int64(r * c), _p(aa), _p(bb), ctypes.c_int32(int(r == 1 or c == 1)), _p(out))
+    return out.reshape(r, c)
+
+
+def clustered_sample(s: SceneArrays, vis: np.ndarray, factor: np.ndarray, albedo: np.ndarray, sizes, members,
+                     key: int, offset: int = 0, floor: float | None = 0.001):
+    """clustered_sample_batch (sampling.py:302-352): WRS over the clamped cluster
+    visibilities, then per cluster (ascending) a WRS over its member lights with
+    weights phat / p_src on the continuing stream, then the light points.
+    factor: (P, K) unshadowed factors."""
+    luma = np.array([0.2126, 0.7152, 0.0722])
+    vis = np.asarray(vis, np.float64)
+    p, m = vis.shape
+    cw = np.maximum(vis, floor) if floor and floor > 0.0 else np.maximum(vis, 0.0)
+    c_idx, c_w, c_sum = wrs_select(cw, key, offset)
+    pos_draw = offset + p * m
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    ids = np.full(p, -1, np.int64)
+    big_w = np.zeros(p)
+    for j in range(m):
+        rows = np.flatnonzero(c_idx == j)
+        if rows.size == 0:
+            continue
+        mem = np.asarray(members[off[j]:off[j + 1]])
+        my = mem.size
+        f = factor[np.ix_(rows, mem)]
+        scale = matmul3(albedo[rows], luma[:, None] * s.lt_radiance[mem].T) / np.pi
+        phat = f * scale
+        p_src = m * (c_w[rows] / c_sum[rows]) / my
+        w2 = phat / p_src[:, None]
+        sel, _, w2_sum = wrs_select(w2, key, pos_draw)
+        pos_draw += rows.size * my
+        ok = sel >= 0
+        rr = rows[ok]
+        ids[rr] = mem[sel[ok]]
+        big_w[rr] = m * w2_sum[ok] / (my * phat[ok, sel[ok]])
+    u = uniform_at(key, pos_draw + np.arange(2 * p)).reshape(p, 2)
+    return ids, s.light_points(ids, u), big_w

@@ -245,6 +245,41 @@ class TestShade:
         np.testing.assert_array_equal(rgb, g_shade["nls_rgb"])
 
 
+class TestClusters:
+    """Clustered NVC (training.py:121-128, sampling.py:302-352) against the reference."""
+
+    def test_bounded_integers_match_numpy(self):
+        key = O.stream_key(3, "x")
+        for n, cnt, start in ((37, 1001, 0), (2, 7, 5), (1, 10, 3), (1000003, 999, 11)):
+            want = np.random.Generator(np.random.Philox(key=key))
+            want.random(start) if start else None
+            vals, used, pend = O.bounded_ints(key, start, cnt, n)
+            np.testing.assert_array_equal(vals, want.integers(0, n, size=cnt))
+            np.testing.assert_array_equal(O.uniform_at(key, np.arange(start + used, start + used + 2)), want.random(2))
+            more, _, _ = O.bounded_ints(key, start + used + 2, 5, n, pend)   # the kept half carries over
+            np.testing.assert_array_equal(more, want.integers(0, n, size=5))
+
+    def test_cluster_targets_bit_exact(self, g_scenes, g_clusters):
+        s = scene(g_scenes, "rooms128")
+        tgt = O.cluster_targets(s, g_clusters["ct_pos"], g_clusters["km_r128k16_sizes"],
+                                g_clusters["km_r128k16_members"], O.stream_key(0, 2, 0, "targets"))
+        np.testing.assert_array_equal(tgt, g_clusters["ct_tgt"])
+        assert 0.05 < tgt.mean() < 0.95
+
+    def test_clustered_sample(self, g_scenes, g_clusters):
+        """ids and points exact; W to 1e-9 (the unshadowed factors restate numba's
+        acos/sqrt chain to ~1e-12)."""
+        z = g_clusters
+        s = scene(g_scenes, "rooms128")
+        f = s.factors(z["cs_gb_position"], z["cs_gb_normal"])
+        ids, pts, big_w = O.clustered_sample(s, z["cs_vis"], f, z["cs_gb_albedo"], z["km_r128k16_sizes"],
+                                             z["km_r128k16_members"], O.stream_key(0, 3, "light-select"))
+        np.testing.assert_array_equal(ids, z["cs_ids"])
+        np.testing.assert_array_equal(pts, z["cs_pts"])
+        np.testing.assert_allclose(big_w, z["cs_W"], rtol=1e-9, atol=0)
+        assert (ids >= 0).sum() > 1000
+
+
 class TestSnapshot:
     def test_reference_snapshot_reads_and_infers(self, g_snap):
         """The reference's VCSNAP1 file, parsed by the restated reader and evaluated by
