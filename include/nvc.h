@@ -270,6 +270,20 @@ int nvc_light_factors(const nvc_scene *sc, const double *pos, const double *nrm,
 /* visibility_batch (geometry.py:233-247): vis (n) f32 in {0,1}. */
 int nvc_visibility(const nvc_scene *sc, const double *x, const double *y, int64_t n,
                    float *vis, void *stream);
+/* Cluster-mode shadow-ray targets (training.py:121-128) for a batch already in
+ * pos / n_rows (nvc_gen_train_batch with tgt = NULL): per cluster j (ascending)
+ * a uniform member -- numpy Generator.integers, exact including its rejection
+ * loop and the bit generator's kept 32-bit half -- then the member's light point
+ * from the same stream; tgt (rows of this shard, m) f32.  Clusters as device
+ * int32 arrays c_off (m+1) and c_mem (c_off[m]) (clusters.ClusterSet.packed);
+ * ws: nvc_cluster_workspace_bytes(b_max, m); at nvc_cluster_state_offset the
+ * call leaves int64 [m+2]: per cluster the first output of its random() draws,
+ * then the stream's next 64-bit output and its kept 32-bit half (-1: none). */
+int64_t nvc_cluster_workspace_bytes(int64_t b_max, int32_t m);
+int64_t nvc_cluster_state_offset(int64_t b_max, int32_t m);
+int nvc_cluster_targets(const nvc_scene *sc, uint64_t key, const double *pos, const int64_t *n_rows,
+                        int64_t b_max, int32_t shard, int32_t n_shards, int32_t m, const int32_t *c_off,
+                        const int32_t *c_mem, float *tgt, void *ws, void *stream);
 /* shade_batch (render.py:220-246): one-shadow-ray estimate per row,
  * rgb (n,3) f64 = albedo/pi * L_e[id] * G * V * (area) * W; rows with id < 0,
  * id >= K or W <= 0 (and rows with G <= 0) are 0.  Bit-identical to the

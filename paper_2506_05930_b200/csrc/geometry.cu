@@ -858,6 +858,146 @@ __global__ void __launch_bounds__(128) k_targets_sorted(nvc_scene sc, uint64_t k
 
 __global__ void k_set_rows(int64_t* n_rows, int64_t v) { *n_rows = v; }
 
+// ---- cluster-mode targets (training.py:121-128) -------------------------------
+// Per cluster j (ascending) the reference draws ids = mem[rng.integers(0, |mem|,
+// size=b)] and then rng.random((b, 2)) on one stream.  integers() is Lemire's
+// bounded draw on 32-bit draws with a rejection loop; a 32-bit draw is the low
+// half of a fresh 64-bit output and the bit generator keeps the high half for
+// the next 32-bit draw, across calls (random() skips it).  One CTA walks the
+// clusters in order; per cluster all threads evaluate a window of 32-bit draws,
+// a block scan ranks the accepted ones (row i takes the i-th), and the index of
+// the b-th acceptance fixes the outputs consumed and the kept half -- the exact
+// stream positions, rejections included.  |mem| = 1 draws nothing.
+__device__ __forceinline__ uint64_t philox_out(uint64_t key, uint64_t n) {
+    return philox_block(n / 4 + 1, key).x[n & 3];
+}
+
+constexpr int kPickThreads = 1024;
+
+__global__ void __launch_bounds__(kPickThreads) k_cluster_picks(uint64_t key, const int64_t* __restrict__ n_rows,
+                                                                 int32_t m, const int32_t* __restrict__ c_off,
+                                                                 const int32_t* __restrict__ c_mem,
+                                                                 int32_t* __restrict__ picks,
+                                                                 int64_t* __restrict__ uni_start) {
+    __shared__ uint64_t s_next;        // next fresh 64-bit output
+    __shared__ uint32_t s_kept;        // kept high half (valid if s_has)
+    __shared__ int s_has;
+    __shared__ int s_warp[kPickThreads / 32];
+    __shared__ int64_t s_tb;           // draw index of the b-th acceptance (-1: not in window)
+    __shared__ int s_acc;              // acceptances in the window
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int64_t b = *n_rows;
+    if (tid == 0) {
+        s_next = 0;
+        s_has = 0;
+        s_kept = 0;
+    }
+    __syncthreads();
+    for (int j = 0; j < m; ++j) {
+        const int32_t lo = c_off[j], n = c_off[j + 1] - lo;
+        if (n == 1) {
+            for (int64_t i = tid; i < b; i += kPickThreads) picks[i * m + j] = c_mem[lo];
+            __syncthreads();
+            if (tid == 0) {
+                uni_start[j] = (int64_t)s_next;
+                s_next += 2 * (uint64_t)b;
+            }
+            __syncthreads();
+            continue;
+        }
+        const uint32_t nn = (uint32_t)n, thresh = (0u - nn) % nn;
+        const uint64_t base = s_next;
+        const int has = s_has;
+        const uint32_t kept = s_kept;
+        int64_t t0 = 0, done = 0;      // window start (draw index), acceptances before it
+        for (;;) {
+            const int64_t D = b - done + 64;                                // window length
+            const int64_t per = (D + kPickThreads - 1) / kPickThreads;
+            const int64_t my0 = t0 + (int64_t)tid * per, my1 = min(t0 + D, my0 + per);
+            auto draw32 = [&](int64_t t) -> uint32_t {   // t-th 32-bit draw of this call
+                if (has && t == 0) return kept;
+                const int64_t k = t - has;
+                const uint64_t w = philox_out(key, base + (uint64_t)(k >> 1));
+                return (k & 1) ? (uint32_t)(w >> 32) : (uint32_t)w;
+            };
+            int cnt = 0;
+            for (int64_t t = my0; t < my1; ++t) {
+                const uint64_t mm = (uint64_t)draw32(t) * nn;
+                cnt += (uint32_t)mm >= thresh;
+            }
+            int incl = cnt;   // block exclusive scan of the per-thread counts
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) s_warp[wid] = incl;
+            if (tid == 0) s_tb = -1;
+            __syncthreads();
+            if (wid == 0) {
+                int v = s_warp[lane], vi = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, vi, o);
+                    if (lane >= o) vi += y;
+                }
+                s_warp[lane] = vi - v;
+                if (lane == 31) s_acc = vi;
+            }
+            __syncthreads();
+            int64_t r = done + s_warp[wid] + (incl - cnt);
+            for (int64_t t = my0; t < my1 && r < b; ++t) {
+                const uint64_t mm = (uint64_t)draw32(t) * nn;
+                if ((uint32_t)mm >= thresh) {
+                    picks[r * m + j] = c_mem[lo + (int32_t)(mm >> 32)];
+                    if (r == b - 1) s_tb = t;
+                    ++r;
+                }
+            }
+            __syncthreads();
+            if (s_tb >= 0 || b == 0) break;
+            done += s_acc;          // >= 65 rejections in the window: continue after it
+            t0 += D;
+            __syncthreads();
+        }
+        if (tid == 0) {
+            const int64_t used = b == 0 ? 0 : s_tb + 1;                     // 32-bit draws consumed
+            const int64_t fresh = used - (has && used > 0 ? 1 : 0);         // ... from new outputs
+            const uint64_t outs = (uint64_t)((fresh + 1) / 2);
+            if (used > 0) {
+                s_has = (int)(fresh & 1);
+                if (fresh & 1) s_kept = (uint32_t)(philox_out(key, base + outs - 1) >> 32);
+            }
+            uni_start[j] = (int64_t)(base + outs);
+            s_next = base + outs + 2 * (uint64_t)b;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {   // the stream's state after the call: next output, kept half (-1: none)
+        uni_start[m] = (int64_t)s_next;
+        uni_start[m + 1] = s_has ? (int64_t)s_kept : -1;
+    }
+}
+
+// shadow rays toward each row's picked member: draws uni_start[j] + 2i, +1
+__global__ void __launch_bounds__(128) k_cluster_tgt(nvc_scene sc, uint64_t key, const double* __restrict__ pos,
+                                                     const int64_t* __restrict__ n_rows, int shard, int n_shards,
+                                                     int32_t m, const int32_t* __restrict__ picks,
+                                                     const int64_t* __restrict__ uni_start, float* __restrict__ tgt) {
+    const int64_t b = *n_rows;
+    const int64_t lo = b * shard / n_shards, hi = b * (shard + 1) / n_shards;
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y;
+    if (lo + r >= hi) return;
+    const int64_t i = lo + r;
+    const uint64_t n0 = (uint64_t)uni_start[j] + 2 * (uint64_t)i;
+    const double u0 = draw(key, n0), u1 = draw(key, n0 + 1);
+    const double x[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+    double y[3];
+    light_point(sc, picks[i * m + j], u0, u1, y);
+    tgt[r * m + j] = segment_visible(sc, x, y);
+}
+
 inline int grid1(int64_t n, int bs) { return (int)((n + bs - 1) / bs); }
 
 }  // namespace
@@ -953,6 +1093,32 @@ int nvc_gen_train_batch(const nvc_scene* sc, const nvc_camera* cam, uint64_t key
         }
     }
     return check_launch("k_targets");
+}
+
+int64_t nvc_cluster_workspace_bytes(int64_t b_max, int32_t m) {
+    return ((b_max * m * 4 + 255) / 256) * 256 + 8 * ((int64_t)m + 2) + 256;
+}
+
+int64_t nvc_cluster_state_offset(int64_t b_max, int32_t m) {   // int64 [m+2]: uni starts, next, kept
+    return ((b_max * m * 4 + 255) / 256) * 256;
+}
+
+int nvc_cluster_targets(const nvc_scene* sc, uint64_t key, const double* pos, const int64_t* n_rows, int64_t b_max,
+                        int32_t shard, int32_t n_shards, int32_t m, const int32_t* c_off, const int32_t* c_mem,
+                        float* tgt, void* ws, void* stream) {
+    NVC_REQUIRE(sc && pos && n_rows && c_off && c_mem && tgt && ws, "nvc_cluster_targets: null argument");
+    NVC_REQUIRE(m >= 1 && n_shards >= 1 && shard >= 0 && shard < n_shards, "nvc_cluster_targets: bad m/shard");
+    if (b_max <= 0) return NVC_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    int32_t* picks = (int32_t*)ws;
+    int64_t* uni = (int64_t*)((char*)ws + nvc_cluster_state_offset(b_max, m));
+    k_cluster_picks<<<1, kPickThreads, 0, s>>>(key, n_rows, m, c_off, c_mem, picks, uni);
+    int rc = check_launch("k_cluster_picks");
+    if (rc) return rc;
+    const int64_t cap = b_max / n_shards + 1;
+    dim3 g(grid1(cap, 128), m);
+    k_cluster_tgt<<<g, 128, 0, s>>>(*sc, key, pos, n_rows, shard, n_shards, m, picks, uni, tgt);
+    return check_launch("k_cluster_tgt");
 }
 
 int nvc_targets(const nvc_scene* sc, uint64_t key, const double* pos, int64_t b, float* tgt, void* stream) {

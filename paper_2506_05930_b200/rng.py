@@ -108,6 +108,15 @@ def set_position(g: np.random.Generator, n: int) -> None:
     g.bit_generator.state = bg.state
 
 
+def set_kept32(g: np.random.Generator, half) -> None:
+    """Set the bit generator's kept 32-bit half (None: none) -- what numpy's
+    32-bit draws (Generator.integers) leave behind for the next one."""
+    st = g.bit_generator.state
+    st["has_uint32"] = 0 if half is None else 1
+    st["uinteger"] = 0 if half is None else int(half)
+    g.bit_generator.state = st
+
+
 def advance(g, n: int) -> None:
     """Account for n draws made on the device."""
     if isinstance(g, Stream):

@@ -66,16 +66,45 @@ class BatchBuffers:
         self.loss = torch.zeros(2, dtype=torch.float64, device=device)   # [sum, mean] (nvc_train_grads)
 
 
+def _cluster_tables(clusters, device):
+    """(c_off, c_mem) int32 device tensors of a ClusterSet, cached on it per device."""
+    import torch
+    cache = clusters.__dict__.setdefault("_nvc_dev", {})
+    if device not in cache:
+        off, flat = clusters.packed()
+        cache[device] = (torch.from_numpy(off).to(device), torch.from_numpy(flat).to(device))
+    return cache[device]
+
+
+def _cluster_targets(ds, key, pos, n_rows, b_max, shard, n_shards, clusters, tgt, ws=None):
+    """nvc_cluster_targets; returns the workspace (its state block: stream position after the call)."""
+    import torch
+    c_off, c_mem = _cluster_tables(clusters, pos.device)
+    need = _lib.load().nvc_cluster_workspace_bytes(b_max, clusters.m)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=pos.device)
+    _lib.call("nvc_cluster_targets", ds.struct, key, pos.data_ptr(), n_rows.data_ptr(), b_max, shard, n_shards,
+              clusters.m, c_off.data_ptr(), c_mem.data_ptr(), tgt.data_ptr(), ws.data_ptr(), _lib.stream_ptr())
+    return ws
+
+
 def gen_batch_device(scene, camera, bufs: BatchBuffers, seed: int, frame: int, step: int = 0,
-                     shard: int = 0, n_shards: int = 1, targets: bool = True) -> BatchBuffers:
+                     shard: int = 0, n_shards: int = 1, targets: bool = True, clusters=None) -> BatchBuffers:
+    """One training batch on the device (training.py:176-195); with ``clusters`` the
+    targets are cluster visibilities (training.py:121-128)."""
     ds = device_scene(scene, bufs.pos.device)
     cam = camera_struct(camera)
     key = (seed, frame, step)
+    light_tgt = targets and clusters is None
     _lib.call("nvc_gen_train_batch", ds.struct, cam, rngmod.stream_key(*key, rngmod.WORLD_SAMPLES),
               rngmod.stream_key(*key, rngmod.SCREEN_SAMPLES), rngmod.stream_key(*key, rngmod.TARGETS),
               bufs.n_world, bufs.n_screen, shard, n_shards, bufs.pos.data_ptr(),
-              bufs.tgt.data_ptr() if targets else None, bufs.n_rows.data_ptr(), bufs.ws.data_ptr(),
+              bufs.tgt.data_ptr() if light_tgt else None, bufs.n_rows.data_ptr(), bufs.ws.data_ptr(),
               _lib.stream_ptr())
+    if targets and clusters is not None:
+        bufs.cws = _cluster_targets(ds, rngmod.stream_key(*key, rngmod.TARGETS), bufs.pos, bufs.n_rows,
+                                    bufs.n_world + bufs.n_screen, shard, n_shards, clusters, bufs.tgt,
+                                    getattr(bufs, "cws", None))
     return bufs
 
 
@@ -110,14 +139,25 @@ def gen_screen_samples(scene, camera, n: int, rng) -> np.ndarray:
 
 
 def compute_visibility_targets(positions, scene, rng, clusters=None) -> np.ndarray:
-    """Binary shadow-ray targets, one column per light (training.py:103-120)."""
+    """Binary shadow-ray targets, one column per light -- or per cluster, toward a
+    uniform member (training.py:103-128)."""
     import torch
-    if clusters is not None:
-        raise NotImplementedError("cluster targets are outside this build's hot path (SURVEY §8(f))")
     _lib.require_cuda()
     ds = device_scene(scene)
     pos = torch.from_numpy(np.ascontiguousarray(positions, dtype=np.float64)).to(ds.device)
     b = pos.shape[0]
+    if clusters is not None:
+        if isinstance(rng, np.random.Generator) and rng.bit_generator.state.get("has_uint32"):
+            raise ValueError("training-batch streams must be fresh (as train_frame creates them)")
+        tgt = torch.zeros((max(b, 1), clusters.m), dtype=torch.float32, device=ds.device)
+        n_rows = torch.tensor([b], dtype=torch.int64, device=ds.device)
+        ws = _cluster_targets(ds, _fresh_key(rng), pos, n_rows, max(b, 1), 0, 1, clusters, tgt)
+        off = _lib.load().nvc_cluster_state_offset(max(b, 1), clusters.m) // 8
+        state = ws.view(torch.int64)[off + clusters.m: off + clusters.m + 2].cpu().numpy()
+        rngmod.advance(rng, int(state[0]))
+        if isinstance(rng, np.random.Generator):
+            rngmod.set_kept32(rng, None if state[1] < 0 else int(state[1]))
+        return tgt[:b].cpu().numpy()
     tgt = torch.empty((b, ds.n_lights), dtype=torch.float32, device=ds.device)
     _lib.call("nvc_targets", ds.struct, _fresh_key(rng), pos.data_ptr(), b, tgt.data_ptr(), _lib.stream_ptr())
     rngmod.advance(rng, 2 * b * ds.n_lights)
@@ -135,13 +175,14 @@ class BatchPipeline:
     """
 
     def __init__(self, scene, camera, cfg: TrainFrameConfig, k: int, device, shard: int = 0, n_shards: int = 1,
-                 cache=None):
+                 cache=None, clusters=None):
         import torch
 
         from .cache import GradExchange
         if cfg.steps != 1:
             raise ValueError("BatchPipeline prefetches one batch per frame (cfg.steps == 1)")
         self.scene, self.camera, self.cfg, self.shard, self.n_shards = scene, camera, cfg, shard, n_shards
+        self.clusters = clusters
         self.bufs = [BatchBuffers(cfg.n_world, cfg.n_screen, k, device, n_shards) for _ in range(2)]
         # data parallel: the entry list of the gradient exchange depends only on the
         # batch positions, so it is built here too, off the critical path (one per buffer)
@@ -165,7 +206,7 @@ class BatchPipeline:
         with torch.cuda.stream(self.side):
             self.side.wait_event(self.free[b])          # the previous frame on this buffer has trained
             gen_batch_device(self.scene, self.camera, self.bufs[b], self.cfg.seed, frame, 0, self.shard,
-                             self.n_shards)
+                             self.n_shards, clusters=self.clusters)
             if self.ex is not None:
                 self.ex[b].index(self.bufs[b].pos, self.bufs[b].n_rows)
             self.ready[b].record(self.side)
@@ -198,9 +239,11 @@ class BatchPipeline:
             self._launch(frame + 1)
 
 
-def _check_cache(cache, cfg):
-    if cache.mode == MODE_CLUSTERS:
-        raise NotImplementedError("clustered NVC is outside this build's hot path (SURVEY §8(f))")
+def _check_cache(cache, cfg, clusters=None):
+    if cache.mode == MODE_CLUSTERS and clusters is None:
+        raise ValueError("cluster-mode cache needs a ClusterSet")
+    if cache.mode == MODE_CLUSTERS and cache.output_dim != clusters.m:
+        raise ValueError(f"cache has {cache.output_dim} outputs, the ClusterSet {clusters.m} clusters")
     if cache.mode == MODE_RADIANCE:
         raise NotImplementedError("the NRC radiance baseline is out of scope (SURVEY §2)")
     if cfg.surface_samples:
@@ -209,7 +252,7 @@ def _check_cache(cache, cfg):
 
 def train_frame_device(scene, camera, cache, cfg: TrainFrameConfig, frame: int = 0,
                        bufs: BatchBuffers | None = None, shard: int = 0, n_shards: int = 1, comm=None,
-                       pipeline: BatchPipeline | None = None):
+                       pipeline: BatchPipeline | None = None, clusters=None):
     """Asynchronous frame training: returns the last step's loss as a CUDA tensor.
 
     With ``n_shards > 1`` every rank builds the same global batch, computes the
@@ -217,8 +260,11 @@ def train_frame_device(scene, camera, cache, cfg: TrainFrameConfig, frame: int =
     allreduce of the compact GradExchange buffer and the loss) runs before the
     identical Adam update.  With ``pipeline`` the
     batch comes from (and the next one is started on) a BatchPipeline."""
-    _check_cache(cache, cfg)
+    clusters = clusters if cache.mode == MODE_CLUSTERS else None
+    _check_cache(cache, cfg, clusters)
     if pipeline is not None:
+        if (pipeline.clusters is None) != (clusters is None):
+            raise ValueError("the BatchPipeline and the cache disagree on cluster mode")
         bufs = pipeline.take(frame)
     elif bufs is None:
         bufs = BatchBuffers(cfg.n_world, cfg.n_screen, cache.output_dim, cache.device, n_shards)
@@ -226,7 +272,7 @@ def train_frame_device(scene, camera, cache, cfg: TrainFrameConfig, frame: int =
     b_max = bufs.n_world + bufs.n_screen
     for step in range(cfg.steps):
         if pipeline is None:
-            gen_batch_device(scene, camera, bufs, cfg.seed, frame, step, shard, n_shards)
+            gen_batch_device(scene, camera, bufs, cfg.seed, frame, step, shard, n_shards, clusters=clusters)
         ex = None
         if comm is not None:
             ex = pipeline.exchange_for(bufs) if pipeline is not None else None
@@ -248,13 +294,12 @@ def train_frame_device(scene, camera, cache, cfg: TrainFrameConfig, frame: int =
 def train_frame(scene, camera, cache, cfg: TrainFrameConfig, frame: int = 0, clusters=None) -> float:
     """Generate a fresh batch and run the configured optimizer steps; returns
     the last step's batch loss (training.py:166-199)."""
-    if cache.mode == MODE_CLUSTERS and clusters is None:
-        raise ValueError("cluster-mode cache needs a ClusterSet")
-    _check_cache(cache, cfg)
+    clusters = clusters if cache.mode == MODE_CLUSTERS else None
+    _check_cache(cache, cfg, clusters)
     bufs = BatchBuffers(cfg.n_world, cfg.n_screen, cache.output_dim, cache.device)
     loss = 0.0
     for step in range(cfg.steps):
-        gen_batch_device(scene, camera, bufs, cfg.seed, frame, step)
+        gen_batch_device(scene, camera, bufs, cfg.seed, frame, step, clusters=clusters)
         b = int(bufs.n_rows.item())
         if b == 0:            # training.py:196-197: empty batch -> no update
             continue

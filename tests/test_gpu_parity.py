@@ -747,6 +747,94 @@ def test_odd_light_count_mixed_emitters():
     np.testing.assert_array_equal(bufs.tgt[:b].cpu().numpy(), otgt)
 
 
+@pytest.fixture(scope="module")
+def rooms():
+    """rooms128 and its 16 k-means light clusters (the reference's clustering stream)."""
+    from paper_2506_05930_b200.clusters import kmeans_cluster
+    from paper_2506_05930_b200.scenes import rooms_scene
+    s = scene_from_dict(rooms_scene(128))
+    return s, kmeans_cluster(s.lights, 16, R.stream(0, R.CLUSTERING))
+
+
+class TestClusters:
+    """Clustered NVC on the device (training.py:121-128, sampling.py:302-352)."""
+
+    def test_cluster_targets_bit_exact_and_stream_state(self, rooms, g_clusters):
+        s, cs = rooms
+        g = R.stream(0, 2, 0, R.TARGETS)
+        tgt = compute_visibility_targets(g_clusters["ct_pos"], s, g, clusters=cs)
+        np.testing.assert_array_equal(tgt, g_clusters["ct_tgt"])
+        # the generator continues exactly where the reference's would (incl. the kept half)
+        h = R.stream(0, 2, 0, R.TARGETS)
+        b = g_clusters["ct_pos"].shape[0]
+        for mem in cs.members:
+            h.integers(0, mem.size, size=b)
+            h.random((b, 2))
+        np.testing.assert_array_equal(g.integers(0, 7, size=9), h.integers(0, 7, size=9))
+        np.testing.assert_array_equal(g.random(5), h.random(5))
+
+    def test_rejection_loop_and_kept_half(self, rooms, g_scenes):
+        """A 1,431,655,766-member cluster (2^32 mod n = n - 2) rejects a third of its
+        32-bit draws, running the multi-window path; a 3-member cluster follows."""
+        s, _ = rooms
+        from paper_2506_05930_b200.scene import device_scene
+        ds = device_scene(s, DEV)
+        n_big, b, k = 1431655766, 2001, s.lt_kind.shape[0]
+        c_mem = torch.cat([torch.arange(n_big, device=DEV, dtype=torch.int64).remainder_(k).to(torch.int32),
+                           torch.tensor([5, 77, 101], dtype=torch.int32, device=DEV)])
+        c_off = torch.tensor([0, n_big, n_big + 3], dtype=torch.int32, device=DEV)
+        pos_h = np.random.default_rng(1).uniform(s.aabb_min, s.aabb_max, (b, 3))
+        pos = torch.from_numpy(pos_h).to(DEV)
+        n_rows = torch.tensor([b], dtype=torch.int64, device=DEV)
+        tgt = torch.zeros((b + 1, 2), dtype=torch.float32, device=DEV)
+        ws = torch.zeros(_lib.load().nvc_cluster_workspace_bytes(b, 2), dtype=torch.uint8, device=DEV)
+        key = R.stream_key(4, "reject")
+        _lib.call("nvc_cluster_targets", ds.struct, key, pos.data_ptr(), n_rows.data_ptr(), b, 0, 1, 2,
+                  c_off.data_ptr(), c_mem.data_ptr(), tgt.data_ptr(), ws.data_ptr(), _lib.stream_ptr())
+        del c_mem
+        got = tgt[:b].cpu().numpy()
+        st = ws.view(torch.int64)[_lib.load().nvc_cluster_state_offset(b, 2) // 8:][:4].cpu().numpy()
+        sa = O.SceneArrays.from_golden(g_scenes, "rooms128_")
+        pick, used, pend = O.bounded_ints(key, 0, b, n_big)
+        assert used > (b + 1) // 2 + 200                         # many rejections
+        u = O.uniform_at(key, used + np.arange(2 * b)).reshape(b, 2)
+        want0 = sa.visibility(pos_h, sa.light_points(pick % k, u))
+        pick2, used2, pend2 = O.bounded_ints(key, used + 2 * b, b, 3, pend)
+        u2 = O.uniform_at(key, used + 2 * b + used2 + np.arange(2 * b)).reshape(b, 2)
+        want1 = sa.visibility(pos_h, sa.light_points(np.array([5, 77, 101])[pick2], u2))
+        np.testing.assert_array_equal(got[:, 0], want0)
+        np.testing.assert_array_equal(got[:, 1], want1)
+        assert st[0] == used and st[1] == used + 2 * b + used2
+        assert st[2] == used + 2 * b + used2 + 2 * b and st[3] == (-1 if pend2 is None else pend2)
+
+    def test_cluster_train_frame_first_step(self, rooms):
+        """A cluster-mode cache trains on cluster targets: first-step loss equals the
+        oracle's on the oracle's batch (C-config batch scaled down)."""
+        from paper_2506_05930_b200 import make_cache
+        from paper_2506_05930_b200.hashgrid import clustered_config
+        s, cs = rooms
+        cfg = TrainFrameConfig.clustered(n_world=1024, n_screen=1024)
+        c = make_cache(s, "clusters", seed=0, clusters=cs.m)
+        loss = train_frame(s, s.camera, c, cfg, frame=0, clusters=cs)
+        g = clustered_config(aabb_min=s.aabb_min, aabb_max=s.aabb_max)
+        oc = O.Cache(O.Grid(levels=g.levels, base_resolution=g.base_resolution, per_level_scale=g.per_level_scale,
+                            features_per_level=g.features_per_level, table_size=g.table_size,
+                            aabb_min=s.aabb_min, aabb_max=s.aabb_max), cs.m, hidden=c.net_cfg.hidden_dims, seed=0)
+        cam = s.camera
+        sa = O.SceneArrays(s.triangles_v0, s.triangles_v1, s.triangles_v2, s.tri_material, s.tri_light, s.lt_kind,
+                           s.lt_verts, s.lt_normal, s.lt_radiance, s.mat_albedo,
+                           np.array([*cam.position, *cam.look_at, *cam.up, cam.fov_deg, cam.width, cam.height], float))
+        world = O.world_samples(sa, 1024, O.Stream(0, 0, 0, "world-samples"))
+        screen = O.screen_samples(sa, 1024, O.Stream(0, 0, 0, "screen-samples"))
+        pos = np.concatenate([world, screen])
+        off, flat = cs.packed()
+        tgt = O.cluster_targets(sa, pos, np.diff(off), flat, O.stream_key(0, 0, 0, "targets"))
+        oloss = oc.train_step(pos, tgt)
+        assert abs(loss - oloss) <= 1e-5 * abs(oloss), (loss, oloss)
+        with pytest.raises(ValueError):
+            train_frame(s, s.camera, c, cfg, frame=1)
+
+
 def test_snapshot_roundtrip(tmp_path, boxes32):
     c = VisibilityCache(MODE_LIGHTS, 32, grid_cfg(boxes32, 8, 1 << 14), hidden_dims=(64, 64))
     c.step = 7
