@@ -16,7 +16,9 @@ from .hashgrid import HashGridConfig, clustered_config
 from .mlp import MLPConfig, MLPParams, TrainStepConfig, lr_at
 from . import render
 from .render import GBuffer, gbuffer_and_ctx, make_gbuffer, shade_batch, shade_pixel
-from .sampling import (CLAMP_FLOOR, PixelCtx, Reservoir, ShadingPoint, clamp_visibility,
+from .clusters import ClusterSet, kmeans_cluster
+from .sampling import (CLAMP_FLOOR, PixelCtx, Reservoir, ShadingPoint, clamp_visibility, clustered_sample,
+                       clustered_sample_batch,
                        neural_di_batch, neural_di_shade, nls_sample, nls_sample_batch,
                        nls_weights_batch, wrs_select, wrs_select_batch)
 from .scene import Camera, Light, Material, Scene, SceneError, load_scene, scene_from_dict
@@ -36,4 +38,5 @@ __all__ = [
     "wrs_select_batch", "Camera", "Light", "Material", "Scene", "SceneError", "load_scene",
     "scene_from_dict", "boxes_scene", "boxes_point_scene", "rooms_scene", "TrainFrameConfig",
     "compute_visibility_targets", "gen_screen_samples", "gen_world_samples", "train_frame",
+    "ClusterSet", "kmeans_cluster", "clustered_sample", "clustered_sample_batch",
 ]

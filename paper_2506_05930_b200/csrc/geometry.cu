@@ -482,6 +482,174 @@ __global__ void k_factors(nvc_scene sc, const double* __restrict__ pos, const do
     }
 }
 
+// ---- clustered two-step sampling (sampling.py:302-352) -------------------------
+// Step 1: WRS over the m clamped cluster visibilities (draws offset + p*m + k).
+// Step 2, cluster by cluster in ascending order on the continuing stream: the
+// pixels that chose cluster j, in ascending pixel order, draw a (rows x |mem|)
+// row-major block for a WRS over the members with weights phat / p_src.  So a
+// pixel's step-2 draws start at t_j + rank * |mem| with rank its position among
+// cluster j's pixels and t_j the draws of the clusters before j: a stable
+// counting pass (block-local ranks, then a scan over blocks) supplies both.
+// Light points follow all step-2 draws.
+constexpr int kCsThreads = 256;
+
+struct CsWs {
+    int32_t *c_idx, *rank, *blk;   // blk: [nblk][m] counts, then exclusive offsets
+    double *c_w, *c_sum;
+    int64_t *cl_n, *cl_t, *total;  // per-cluster pixel counts, draw bases; [0]: light-point base
+};
+
+// workspace layout: byte offsets of each array (the last entry: total size)
+inline void cs_layout(int64_t p, int m, int64_t off[9]) {
+    const int64_t nblk = (p + kCsThreads - 1) / kCsThreads;
+    const int64_t sz[8] = {4 * p, 4 * p, 4 * nblk * m, 8 * p, 8 * p, 8 * (int64_t)m, 8 * (int64_t)m, 8};
+    off[0] = 0;
+    for (int i = 0; i < 8; ++i) off[i + 1] = off[i] + (sz[i] + 255) / 256 * 256;
+}
+
+inline CsWs cs_ws(void* ws, int64_t p, int m) {
+    int64_t o[9];
+    cs_layout(p, m, o);
+    char* c = (char*)ws;
+    CsWs w;
+    w.c_idx = (int32_t*)(c + o[0]);
+    w.rank = (int32_t*)(c + o[1]);
+    w.blk = (int32_t*)(c + o[2]);
+    w.c_w = (double*)(c + o[3]);
+    w.c_sum = (double*)(c + o[4]);
+    w.cl_n = (int64_t*)(c + o[5]);
+    w.cl_t = (int64_t*)(c + o[6]);
+    w.total = (int64_t*)(c + o[7]);
+    return w;
+}
+
+__global__ void __launch_bounds__(kCsThreads) k_cs_step1(const float* __restrict__ vis, int64_t vstride, int64_t P,
+                                                        int m, uint64_t key, uint64_t offset, double floor, CsWs w) {
+    const int64_t p = (int64_t)blockIdx.x * kCsThreads + threadIdx.x;
+    if (p >= P) return;
+    double s = 0.0, wsel = 0.0;
+    int sel = -1;
+    const uint64_t n0 = offset + (uint64_t)p * (uint64_t)m;
+    U4 u = philox_block(n0 / 4 + 1, key);
+    for (int k = 0; k < m; ++k) {
+        const double v = (double)vis[p * vstride + k];
+        const double cw = floor > 0.0 ? (v > floor ? v : floor) : (v > 0.0 ? v : 0.0);   // np.maximum
+        s = __dadd_rn(s, cw);
+        const uint64_t n = n0 + (uint64_t)k;
+        if (k > 0 && (n & 3) == 0) u = philox_block(n / 4 + 1, key);
+        if (cw > 0.0 && __dmul_rn(u01(u.x[n & 3]), s) < cw) {
+            sel = k;
+            wsel = cw;
+        }
+    }
+    w.c_idx[p] = sel;
+    w.c_w[p] = wsel;
+    w.c_sum[p] = s;
+}
+
+// block-local stable ranks: the block's warps take turns, lanes of one cluster
+// grouped with match.any, so rank order = pixel order
+__global__ void __launch_bounds__(kCsThreads) k_cs_rank(int64_t P, int m, CsWs w) {
+    extern __shared__ int cnt[];
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    for (int j = t; j < m; j += kCsThreads) cnt[j] = 0;
+    __syncthreads();
+    const int64_t p = (int64_t)blockIdx.x * kCsThreads + t;
+    const int j = p < P ? w.c_idx[p] : -1;
+    for (int ww = 0; ww < kCsThreads / 32; ++ww) {
+        if (wid == ww) {
+            const uint32_t grp = __match_any_sync(0xffffffffu, j);
+            const int r = __popc(grp & ((1u << lane) - 1u));
+            const int base = j >= 0 ? cnt[j] : 0;
+            __syncwarp();
+            if (j >= 0 && r == 0) cnt[j] = base + __popc(grp);
+            if (p < P) w.rank[p] = base + r;
+        }
+        __syncthreads();
+    }
+    for (int q = t; q < m; q += kCsThreads) w.blk[(int64_t)blockIdx.x * m + q] = cnt[q];
+}
+
+// per cluster: exclusive scan over blocks, pixel count, draw base t_j
+__global__ void k_cs_scan(int64_t nblk, int m, const int32_t* __restrict__ c_off, int64_t P, uint64_t offset, CsWs w) {
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+        int64_t run = 0;
+        for (int64_t b = 0; b < nblk; ++b) {
+            const int c = w.blk[b * m + j];
+            w.blk[b * m + j] = (int32_t)run;
+            run += c;
+        }
+        w.cl_n[j] = run;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t t = offset + (uint64_t)P * (uint64_t)m;
+        for (int j = 0; j < m; ++j) {
+            w.cl_t[j] = (int64_t)t;
+            t += (uint64_t)w.cl_n[j] * (uint64_t)(c_off[j + 1] - c_off[j]);
+        }
+        w.total[0] = (int64_t)t;
+    }
+}
+
+// numpy/OpenBLAS float64 (r,3)@(3,c): gemm shapes fma(a2,b2, fma(a1,b1, a0 b0)),
+// gemv shapes (r == 1 or c == 1) fma(a2,b2, fma(a0,b0, a1 b1)) (tests/golden/clusters.npz)
+__device__ __forceinline__ double dot3_blas(const double a[3], const double b[3], bool gemv) {
+    return gemv ? fma(a[2], b[2], fma(a[0], b[0], a[1] * b[1])) : fma(a[2], b[2], fma(a[1], b[1], a[0] * b[0]));
+}
+
+__global__ void __launch_bounds__(kCsThreads) k_cs_step2(nvc_scene sc, const double* __restrict__ pos,
+                                                        const double* __restrict__ nrm, const double* __restrict__ alb,
+                                                        int64_t P, int m, const int32_t* __restrict__ c_off,
+                                                        const int32_t* __restrict__ c_mem, uint64_t key, CsWs w,
+                                                        int64_t* __restrict__ ids, double* __restrict__ pts,
+                                                        double* __restrict__ big_w) {
+    const int64_t p = (int64_t)blockIdx.x * kCsThreads + threadIdx.x;
+    if (p >= P) return;
+    const int j = w.c_idx[p];
+    int64_t out_id = -1;
+    double out_w = 0.0;
+    if (j >= 0) {
+        const int lo = c_off[j], my = c_off[j + 1] - lo;
+        const int64_t rank = (int64_t)w.blk[(int64_t)blockIdx.x * m + j] + w.rank[p];
+        const bool gemv = w.cl_n[j] == 1 || my == 1;
+        const double x[3] = {pos[3 * p], pos[3 * p + 1], pos[3 * p + 2]};
+        const double nx[3] = {nrm[3 * p], nrm[3 * p + 1], nrm[3 * p + 2]};
+        const double a[3] = {alb[3 * p], alb[3 * p + 1], alb[3 * p + 2]};
+        const double p_src = (double)m * (w.c_w[p] / w.c_sum[p]) / (double)my;
+        const uint64_t n0 = (uint64_t)w.cl_t[j] + (uint64_t)rank * (uint64_t)my;
+        double s = 0.0, phat_sel = 0.0;
+        int sel = -1;
+        for (int k = 0; k < my; ++k) {
+            const int l = c_mem[lo + k];
+            const double f = sc.lt_kind[l] == 0 ? rect_factor(x, nx, sc.lt_verts + 12 * l, sc.lt_normal + 3 * l)
+                                                : point_factor(x, nx, sc.lt_verts + 12 * l);
+            const double lw[3] = {0.2126 * sc.lt_radiance[3 * l], 0.7152 * sc.lt_radiance[3 * l + 1],
+                                  0.0722 * sc.lt_radiance[3 * l + 2]};
+            const double phat = f * (dot3_blas(a, lw, gemv) / 3.141592653589793);
+            const double w2 = phat / p_src;
+            s = __dadd_rn(s, w2);
+            if (w2 > 0.0 && __dmul_rn(draw(key, n0 + (uint64_t)k), s) < w2) {
+                sel = k;
+                phat_sel = phat;
+            }
+        }
+        if (sel >= 0) {
+            out_id = c_mem[lo + sel];
+            out_w = (double)m * s / ((double)my * phat_sel);
+        }
+    }
+    const uint64_t nl = (uint64_t)w.total[0] + 2ull * (uint64_t)p;
+    const double u0 = draw(key, nl), u1 = draw(key, nl + 1);
+    double y[3];
+    light_point(sc, out_id, u0, u1, y);
+    ids[p] = out_id;
+    big_w[p] = out_w;
+    pts[3 * p] = y[0];
+    pts[3 * p + 1] = y[1];
+    pts[3 * p + 2] = y[2];
+}
+
 __global__ void k_visibility(nvc_scene sc, const double* __restrict__ x, const double* __restrict__ y,
                              int64_t n, float* __restrict__ vis) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1031,6 +1199,36 @@ int nvc_light_factors(const nvc_scene* sc, const double* pos, const double* nrm,
         k_factors<float><<<g, 128, 0, (cudaStream_t)stream>>>(*sc, pos, nrm, alb, p, stride, (float*)factor,
                                                               (float*)lum);
     return check_launch("k_factors");
+}
+
+int64_t nvc_clustered_workspace_bytes(int64_t p, int32_t m) {
+    int64_t o[9];
+    cs_layout(p, m, o);
+    return o[8];
+}
+
+int nvc_clustered_select(const nvc_scene* sc, const float* vis, int64_t vis_stride, const double* pos,
+                         const double* nrm, const double* alb, int64_t p, int32_t m, const int32_t* c_off,
+                         const int32_t* c_mem, uint64_t key, uint64_t offset, double floor, int64_t* ids,
+                         double* pts, double* big_w, void* ws, void* stream) {
+    NVC_REQUIRE(sc && vis && pos && nrm && alb && c_off && c_mem && ids && pts && big_w && ws,
+                "nvc_clustered_select: null argument");
+    NVC_REQUIRE(m >= 1 && vis_stride >= m, "nvc_clustered_select: bad m / stride");
+    if (p <= 0) return NVC_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const CsWs w = cs_ws(ws, p, m);
+    const int nblk = grid1(p, kCsThreads);
+    k_cs_step1<<<nblk, kCsThreads, 0, s>>>(vis, vis_stride, p, m, key, offset, floor, w);
+    k_cs_rank<<<nblk, kCsThreads, (size_t)m * 4, s>>>(p, m, w);
+    k_cs_scan<<<1, 1024, 0, s>>>(nblk, m, c_off, p, offset, w);
+    k_cs_step2<<<nblk, kCsThreads, 0, s>>>(*sc, pos, nrm, alb, p, m, c_off, c_mem, key, w, ids, pts, big_w);
+    return check_launch("nvc_clustered_select");
+}
+
+int64_t nvc_clustered_state_offset(int64_t p, int32_t m) {   // int64: first light-point draw
+    int64_t o[9];
+    cs_layout(p, m, o);
+    return o[7];
 }
 
 int nvc_visibility(const nvc_scene* sc, const double* x, const double* y, int64_t n, float* vis,

@@ -122,5 +122,9 @@ def advance(g, n: int) -> None:
     if isinstance(g, Stream):
         g.offset += int(n)
         return
+    st = g.bit_generator.state
+    kept = st["uinteger"] if st.get("has_uint32") else None   # 64-bit draws leave the kept half alone
     _, pos = position(g)
     set_position(g, pos + int(n))
+    if kept is not None:
+        set_kept32(g, kept)

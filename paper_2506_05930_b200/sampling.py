@@ -309,3 +309,51 @@ def neural_di_batch(ctx: PixelCtx, cache) -> np.ndarray:
 
 def neural_di_shade(sp: ShadingPoint, cache, scene) -> np.ndarray:
     return neural_di_batch(_ctx_for(sp, scene), cache)[0]
+
+
+# ---------------------------------------------------------------------------
+# clustered NVC: two-step sampling (sampling.py:302-359)
+# ---------------------------------------------------------------------------
+
+def clustered_sample_device(ctx: PixelCtx, cache, clusters, key: int, offset: int = 0,
+                            clamp_floor=CLAMP_FLOOR):
+    """Device tensors (ids, pts, W) and the number of draws consumed."""
+    import torch
+    from .training import _cluster_tables
+    m = clusters.m
+    if _is_native(cache):
+        vis = cache.infer_device(ctx.pos)
+    else:
+        vis = cache.infer(ctx.positions)
+        vis = vis if isinstance(vis, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(vis, np.float32))
+        vis = vis.to(ctx.device, torch.float32).contiguous()
+    if vis.shape[1] < m:
+        raise ValueError(f"cache has {vis.shape[1]} outputs, the ClusterSet {m} clusters")
+    p = ctx.n
+    ids = torch.empty(p, dtype=torch.int64, device=ctx.device)
+    pts = torch.empty((p, 3), dtype=torch.float64, device=ctx.device)
+    big_w = torch.empty(p, dtype=torch.float64, device=ctx.device)
+    lib = _lib.load()
+    ws = torch.empty(lib.nvc_clustered_workspace_bytes(p, m), dtype=torch.uint8, device=ctx.device)
+    c_off, c_mem = _cluster_tables(clusters, ctx.device)
+    floor = float(clamp_floor) if clamp_floor and clamp_floor > 0.0 else 0.0
+    _lib.call("nvc_clustered_select", ctx.dscene.struct, vis.data_ptr(), vis.shape[1], ctx.pos.data_ptr(),
+              ctx.nrm.data_ptr(), ctx.alb.data_ptr(), p, m, c_off.data_ptr(), c_mem.data_ptr(), key, offset, floor,
+              ids.data_ptr(), pts.data_ptr(), big_w.data_ptr(), ws.data_ptr(), _lib.stream_ptr())
+    lp = ws.view(torch.int64)[lib.nvc_clustered_state_offset(p, m) // 8]
+    return ids, pts, big_w, lp + 2 * p - offset
+
+
+def clustered_sample_batch(ctx: PixelCtx, cache, clusters, rng, clamp_floor: float | None = CLAMP_FLOOR):
+    """Cluster WRS on predicted cluster visibility, then streaming RIS over the
+    chosen cluster's members; W_total = m * w_sum2 / (m_y * phat(x)).
+    Returns (light ids, emitter points, W_total)."""
+    key, off = rngmod.position(rng)
+    ids, pts, big_w, used = clustered_sample_device(ctx, cache, clusters, key, off, clamp_floor)
+    rngmod.advance(rng, int(used.item()))
+    return ids.cpu().numpy(), pts.cpu().numpy(), big_w.cpu().numpy()
+
+
+def clustered_sample(sp: ShadingPoint, cache, clusters, scene, rng, clamp_floor: float | None = CLAMP_FLOOR):
+    ids, pts, ws = clustered_sample_batch(_ctx_for(sp, scene), cache, clusters, rng, clamp_floor)
+    return int(ids[0]), pts[0], float(ws[0])

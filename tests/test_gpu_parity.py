@@ -835,6 +835,48 @@ class TestClusters:
             train_frame(s, s.camera, c, cfg, frame=1)
 
 
+class TestClusteredSampling:
+    """Two-step clustered light sampling (sampling.py:302-352) on the device."""
+
+    def test_vs_reference_golden(self, rooms, g_clusters):
+        from paper_2506_05930_b200 import clustered_sample_batch
+        s, cs = rooms
+        z = g_clusters
+        ctx = PixelCtx(s, z["cs_gb_position"], z["cs_gb_normal"], z["cs_gb_albedo"])
+        g = R.stream(0, 3, R.LIGHT_SELECT)
+        ids, pts, big_w = clustered_sample_batch(ctx, FixedCache(z["cs_vis"]), cs, g)
+        np.testing.assert_array_equal(ids, z["cs_ids"])
+        np.testing.assert_array_equal(pts, z["cs_pts"])
+        np.testing.assert_allclose(big_w, z["cs_W"], rtol=1e-9, atol=0)   # factors: numba vs FP64 CUDA ~1e-12
+        # the stream advanced past step 1 (P*m), step 2 (sum_j n_j |mem_j|) and the points (2P)
+        key = R.stream_key(0, 3, R.LIGHT_SELECT)
+        c_idx, _, _ = O.wrs_select(np.maximum(z["cs_vis"].astype(np.float64), 0.001), key)
+        n_j = np.bincount(c_idx[c_idx >= 0], minlength=cs.m)
+        want = ctx.n * cs.m + int(sum(n_j[j] * cs.members[j].size for j in range(cs.m))) + 2 * ctx.n
+        assert R.position(g)[1] == want
+
+    def test_native_cluster_cache_vs_oracle(self, rooms, g_scenes):
+        from paper_2506_05930_b200 import clustered_sample_batch, make_cache
+        from paper_2506_05930_b200.render import gbuffer_device
+        s, cs = rooms
+        pos, nrm, alb, _, _ = gbuffer_device(s, s.camera.resized(80, 45))
+        ctx = PixelCtx(s, pos, nrm, alb)
+        c = make_cache(s, "clusters", seed=1, clusters=cs.m)
+        c.grid_params = (np.random.default_rng(3).standard_normal(c.grid_params.shape) * 0.5).astype(np.float32)
+        vis = c.infer(pos.cpu().numpy())
+        sa = O.SceneArrays.from_golden(g_scenes, "rooms128_")
+        off, flat = cs.packed()
+        p_h, n_h, a_h = (t.cpu().numpy() for t in (pos, nrm, alb))
+        key = R.stream_key(0, 9, R.LIGHT_SELECT)
+        for floor in (0.001, 0.0):
+            oi, op, ow = O.clustered_sample(sa, vis, sa.factors(p_h, n_h), a_h, np.diff(off), flat, key, floor=floor)
+            ids, pts, big_w = clustered_sample_batch(ctx, c, cs, R.Stream(key=key), clamp_floor=floor)
+            np.testing.assert_array_equal(ids, oi)
+            np.testing.assert_array_equal(pts, op)
+            np.testing.assert_allclose(big_w, ow, rtol=1e-9, atol=0)
+            assert (ids >= 0).sum() > 1000
+
+
 def test_snapshot_roundtrip(tmp_path, boxes32):
     c = VisibilityCache(MODE_LIGHTS, 32, grid_cfg(boxes32, 8, 1 << 14), hidden_dims=(64, 64))
     c.step = 7
