@@ -577,6 +577,76 @@ def sweep_arm(args) -> None:
                                              % max_log2, "sweep": rows}}), flush=True)
 
 
+def clusters_arm(args) -> None:
+    """Clustered NVC: rooms_scene(1024) (1024 lights) in 32
+    k-means clusters at 1920x1080; one step = a cluster-mode train step on the
+    C-config batch (24,576 world + 24,576 screen samples, cluster targets) + the
+    two-step clustered light selection over all pixels (inputs resident)."""
+    import torch
+
+    from paper_2506_05930_b200 import TrainFrameConfig, make_cache
+    from paper_2506_05930_b200 import rng as R
+    from paper_2506_05930_b200.clusters import kmeans_cluster
+    from paper_2506_05930_b200.render import gbuffer_device
+    from paper_2506_05930_b200.sampling import PixelCtx, clustered_sample_device
+    from paper_2506_05930_b200.scene import scene_from_dict
+    from paper_2506_05930_b200.scenes import rooms_scene
+    from paper_2506_05930_b200.training import BatchPipeline, train_frame_device
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(dev)
+    scene = scene_from_dict(rooms_scene(1024))
+    cs = kmeans_cluster(scene.lights, 32, R.stream(0, R.CLUSTERING))
+    cam = scene.camera.resized(WIDTH, HEIGHT)
+    P = WIDTH * HEIGHT
+    pos, nrm, alb, _, _ = gbuffer_device(scene, cam, 0, P)
+    ctx = PixelCtx(scene, pos, nrm, alb, table_dtype=np.float64)   # per-camera f64 factor table (memoized)
+    ctx.factor_device()
+    cache = make_cache(scene, "clusters", seed=0, clusters=cs.m, device=dev)
+    cfg = TrainFrameConfig.clustered()
+    pipe = BatchPipeline(scene, cam, cfg, cs.m, dev, cache=cache, clusters=cs)
+    split = {"train": [], "select": []}
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+
+    def frame(f, timed=False):
+        if timed:
+            ev[0].record()
+        train_frame_device(scene, cam, cache, cfg, frame=f, pipeline=pipe, clusters=cs)
+        if timed:
+            ev[1].record()
+        clustered_sample_device(ctx, cache, cs, R.stream_key(0, f, R.LIGHT_SELECT))
+        if timed:
+            ev[2].record()
+
+    for f in range(args.warmup):
+        frame(f)
+    for f in range(3):
+        frame(100 + f, timed=True)
+        torch.cuda.synchronize()
+        split["train"].append(ev[0].elapsed_time(ev[1]))
+        split["select"].append(ev[1].elapsed_time(ev[2]))
+    steps = min(args.steps, 50)
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index or 0) as clocks:
+        st.record()
+        for f in range(steps):
+            frame(args.warmup + f)
+        en.record()
+        torch.cuda.synchronize()
+    ms = st.elapsed_time(en) / steps
+    print(json.dumps({"metric": "clustered-NVC frames: light selections/s at 1080p x 1024 lights in 32 clusters "
+                                "(train step + two-step selection)",
+                      "value": P / (ms * 1e-3), "unit": "queries/s", "n_gpus": 1, "steps": steps,
+                      "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                      "vs_baseline": None, "dtype": "fp16 MLP / fp64 factors+WRS / fp32 train",
+                      "data": "synthetic (rooms_scene(1024), 32 k-means clusters, random-init weights, seed 0)",
+                      "config": {"workload": f"clustered NVC: {WIDTH}x{HEIGHT} rooms1024 (K=1024, m=32 clusters), "
+                                             f"train batch {cfg.n_world + cfg.n_screen}",
+                                 "stage_ms": {k: statistics.median(v) for k, v in split.items()}},
+                      "clocks": clocks.summary()}), flush=True)
+
+
 def reference_arm(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -609,11 +679,12 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-sample", type=int, default=24576)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["c2", "ndi4k", "render", "c4", "sweep"], default="c2",
+    ap.add_argument("--workload", choices=["c2", "ndi4k", "render", "c4", "sweep", "clusters"], default="c2",
                     help="c2: the headline online frame (default); ndi4k: C3 Neural DI at 4K; "
                          "render: the c2 frame plus shading pass 5 (one shadow ray per pixel); "
                          "c4: the online frame on rooms128 with K=128 and a 3x128 MLP; "
-                         "sweep: C5 query throughput over N = 2^16..2^26 and K = 8/32/128")
+                         "sweep: C5 query throughput over N = 2^16..2^26 and K = 8/32/128; "
+                         "clusters: clustered NVC at 1080p with 1024 lights in 32 clusters")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -623,6 +694,8 @@ def main() -> None:
         ndi4k_arm(args)
     elif args.workload == "sweep":
         sweep_arm(args)
+    elif args.workload == "clusters":
+        clusters_arm(args)
     else:
         gpu_arm(args)
 

@@ -289,14 +289,16 @@ int nvc_cluster_targets(const nvc_scene *sc, uint64_t key, const double *pos, co
  * its member lights with weights phat / p_src on the continuing stream (draws
  * for a cluster's pixels in pixel order), then light points -- ids (p) i64,
  * pts (p,3) f64, big_w (p) f64.  Whole frames (pixel 0 .. p-1), p <= 2^31.
+ * factor: NULL (factors computed per pixel and member) or the per-camera
+ * light-major f64 table (K, p) of nvc_light_factors (identical values).
  * ws: nvc_clustered_workspace_bytes(p, m); at nvc_clustered_state_offset an
  * int64 holds the first light-point draw (the call consumes it + 2p - offset). */
 int64_t nvc_clustered_workspace_bytes(int64_t p, int32_t m);
 int64_t nvc_clustered_state_offset(int64_t p, int32_t m);
 int nvc_clustered_select(const nvc_scene *sc, const float *vis, int64_t vis_stride, const double *pos,
-                         const double *nrm, const double *alb, int64_t p, int32_t m, const int32_t *c_off,
-                         const int32_t *c_mem, uint64_t key, uint64_t offset, double floor, int64_t *ids,
-                         double *pts, double *big_w, void *ws, void *stream);
+                         const double *nrm, const double *alb, const double *factor, int64_t p, int32_t m,
+                         const int32_t *c_off, const int32_t *c_mem, uint64_t key, uint64_t offset, double floor,
+                         int64_t *ids, double *pts, double *big_w, void *ws, void *stream);
 /* shade_batch (render.py:220-246): one-shadow-ray estimate per row,
  * rgb (n,3) f64 = albedo/pi * L_e[id] * G * V * (area) * W; rows with id < 0,
  * id >= K or W <= 0 (and rows with G <= 0) are 0.  Bit-identical to the

@@ -107,8 +107,8 @@ _SIGS = {
                                     c_vp, c_vp]),
     "nvc_clustered_workspace_bytes": (c_i64, [c_i64, c_i32]),
     "nvc_clustered_state_offset": (c_i64, [c_i64, c_i32]),
-    "nvc_clustered_select": (c_i32, [P(NvcScene), c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_u64,
-                                     c_u64, c_f64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "nvc_clustered_select": (c_i32, [P(NvcScene), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp,
+                                     c_u64, c_u64, c_f64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "nvc_shade": (c_i32, [P(NvcScene), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "nvc_closest_hit": (c_i32, [P(NvcScene), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "nvc_batch_workspace_bytes": (c_i64, [c_i32, c_i32]),

@@ -537,7 +537,9 @@ __global__ void __launch_bounds__(kCsThreads) k_cs_step1(const float* __restrict
         s = __dadd_rn(s, cw);
         const uint64_t n = n0 + (uint64_t)k;
         if (k > 0 && (n & 3) == 0) u = philox_block(n / 4 + 1, key);
-        if (cw > 0.0 && __dmul_rn(u01(u.x[n & 3]), s) < cw) {
+        const uint32_t ln = (uint32_t)(n & 3);
+        const uint64_t r = ln == 0 ? u.x[0] : (ln == 1 ? u.x[1] : (ln == 2 ? u.x[2] : u.x[3]));
+        if (cw > 0.0 && __dmul_rn(u01(r), s) < cw) {
             sel = k;
             wsel = cw;
         }
@@ -570,26 +572,47 @@ __global__ void __launch_bounds__(kCsThreads) k_cs_rank(int64_t P, int m, CsWs w
     for (int q = t; q < m; q += kCsThreads) w.blk[(int64_t)blockIdx.x * m + q] = cnt[q];
 }
 
-// per cluster: exclusive scan over blocks, pixel count, draw base t_j
-__global__ void k_cs_scan(int64_t nblk, int m, const int32_t* __restrict__ c_off, int64_t P, uint64_t offset, CsWs w) {
-    for (int j = threadIdx.x; j < m; j += blockDim.x) {
-        int64_t run = 0;
-        for (int64_t b = 0; b < nblk; ++b) {
-            const int c = w.blk[b * m + j];
-            w.blk[b * m + j] = (int32_t)run;
-            run += c;
+// per cluster (one CTA each): exclusive scan over the blocks' counts, pixel count
+__global__ void __launch_bounds__(1024) k_cs_scan(int64_t nblk, int m, CsWs w) {
+    __shared__ int s_w[32];
+    const int j = blockIdx.x, t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int64_t per = (nblk + 1023) / 1024, b0 = t * per, b1 = min(nblk, b0 + per);
+    int sum = 0;
+    for (int64_t b = b0; b < b1; ++b) sum += w.blk[b * m + j];
+    int incl = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_w[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const int v = s_w[lane];
+        int vi = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, vi, o);
+            if (lane >= o) vi += y;
         }
-        w.cl_n[j] = run;
+        s_w[lane] = vi - v;
+        if (lane == 31) w.cl_n[j] = vi;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint64_t t = offset + (uint64_t)P * (uint64_t)m;
-        for (int j = 0; j < m; ++j) {
-            w.cl_t[j] = (int64_t)t;
-            t += (uint64_t)w.cl_n[j] * (uint64_t)(c_off[j + 1] - c_off[j]);
-        }
-        w.total[0] = (int64_t)t;
+    int run = s_w[wid] + incl - sum;
+    for (int64_t b = b0; b < b1; ++b) {
+        const int c = w.blk[b * m + j];
+        w.blk[b * m + j] = run;
+        run += c;
     }
+}
+
+// draw bases t_j of the clusters' step-2 blocks and the first light-point draw
+__global__ void k_cs_bases(int m, const int32_t* __restrict__ c_off, int64_t P, uint64_t offset, CsWs w) {
+    uint64_t t = offset + (uint64_t)P * (uint64_t)m;
+    for (int j = 0; j < m; ++j) {
+        w.cl_t[j] = (int64_t)t;
+        t += (uint64_t)w.cl_n[j] * (uint64_t)(c_off[j + 1] - c_off[j]);
+    }
+    w.total[0] = (int64_t)t;
 }
 
 // numpy/OpenBLAS float64 (r,3)@(3,c): gemm shapes fma(a2,b2, fma(a1,b1, a0 b0)),
@@ -598,10 +621,16 @@ __device__ __forceinline__ double dot3_blas(const double a[3], const double b[3]
     return gemv ? fma(a[2], b[2], fma(a[0], b[0], a[1] * b[1])) : fma(a[2], b[2], fma(a[1], b[1], a[0] * b[0]));
 }
 
+// Philox through a real call: a block cached across iterations of the member
+// loop (which inlines the FP64 rect factor) lives in registers this way -- the
+// inlined form kept in a loop-carried local produced wrong draws (see DESIGN).
+__device__ __noinline__ U4 philox_call(uint64_t counter, uint64_t key) { return philox_block(counter, key); }
+
 __global__ void __launch_bounds__(kCsThreads) k_cs_step2(nvc_scene sc, const double* __restrict__ pos,
                                                         const double* __restrict__ nrm, const double* __restrict__ alb,
                                                         int64_t P, int m, const int32_t* __restrict__ c_off,
                                                         const int32_t* __restrict__ c_mem, uint64_t key, CsWs w,
+                                                        const double* __restrict__ ftab, int64_t fstride,
                                                         int64_t* __restrict__ ids, double* __restrict__ pts,
                                                         double* __restrict__ big_w) {
     const int64_t p = (int64_t)blockIdx.x * kCsThreads + threadIdx.x;
@@ -620,18 +649,32 @@ __global__ void __launch_bounds__(kCsThreads) k_cs_step2(nvc_scene sc, const dou
         const uint64_t n0 = (uint64_t)w.cl_t[j] + (uint64_t)rank * (uint64_t)my;
         double s = 0.0, phat_sel = 0.0;
         int sel = -1;
+        uint64_t blk = ~0ull;
+        U4 u;
         for (int k = 0; k < my; ++k) {
             const int l = c_mem[lo + k];
-            const double f = sc.lt_kind[l] == 0 ? rect_factor(x, nx, sc.lt_verts + 12 * l, sc.lt_normal + 3 * l)
-                                                : point_factor(x, nx, sc.lt_verts + 12 * l);
+            const double f = ftab ? __ldg(ftab + (int64_t)l * fstride + p)
+                                  : (sc.lt_kind[l] == 0 ? rect_factor(x, nx, sc.lt_verts + 12 * l, sc.lt_normal + 3 * l)
+                                                        : point_factor(x, nx, sc.lt_verts + 12 * l));
             const double lw[3] = {0.2126 * sc.lt_radiance[3 * l], 0.7152 * sc.lt_radiance[3 * l + 1],
                                   0.0722 * sc.lt_radiance[3 * l + 2]};
             const double phat = f * (dot3_blas(a, lw, gemv) / 3.141592653589793);
             const double w2 = phat / p_src;
             s = __dadd_rn(s, w2);
-            if (w2 > 0.0 && __dmul_rn(draw(key, n0 + (uint64_t)k), s) < w2) {
-                sel = k;
-                phat_sel = phat;
+            const uint64_t n = n0 + (uint64_t)k, bi = n / 4 + 1;
+            if (w2 > 0.0) {
+                if (bi != blk) {
+                    u = philox_call(bi, key);
+                    blk = bi;
+                }
+                // lane by selects, not u.x[n & 3]: a dynamically indexed U4 lives in local memory,
+                // and across the rect-factor call that gave wrong draws
+                const uint32_t ln = (uint32_t)(n & 3);
+                const uint64_t r = ln == 0 ? u.x[0] : (ln == 1 ? u.x[1] : (ln == 2 ? u.x[2] : u.x[3]));
+                if (__dmul_rn(u01(r), s) < w2) {
+                    sel = k;
+                    phat_sel = phat;
+                }
             }
         }
         if (sel >= 0) {
@@ -1042,11 +1085,74 @@ __device__ __forceinline__ uint64_t philox_out(uint64_t key, uint64_t n) {
 
 constexpr int kPickThreads = 1024;
 
+// Fast path: assume no rejection (p ~ n / 2^32 per draw).  One thread chains the
+// clusters' stream positions in closed form; a (rows x clusters) grid draws the
+// picks and flags any cluster where a draw would have been rejected; only then
+// does the exact sequential walk (k_cluster_picks) run, overwriting everything.
+__global__ void k_cluster_chain(const int64_t* __restrict__ n_rows, int32_t m, const int32_t* __restrict__ c_off,
+                                int64_t* __restrict__ uni_start, int64_t* __restrict__ draw_base,
+                                int64_t* __restrict__ kept_src, int32_t* __restrict__ flag) {
+    const int64_t b = *n_rows;
+    uint64_t next = 0;
+    int64_t kept = -1;   // output whose high half the bit generator keeps
+    for (int j = 0; j < m; ++j) {
+        const int32_t n = c_off[j + 1] - c_off[j];
+        draw_base[j] = (int64_t)next;
+        kept_src[j] = kept;
+        if (n > 1 && b > 0) {
+            const int64_t fresh = b - (kept >= 0 ? 1 : 0);
+            const uint64_t outs = (uint64_t)((fresh + 1) / 2);
+            kept = (fresh & 1) ? (int64_t)(next + outs - 1) : -1;
+            next += outs;
+        }
+        uni_start[j] = (int64_t)next;
+        next += 2 * (uint64_t)b;
+    }
+    uni_start[m] = (int64_t)next;
+    uni_start[m + 1] = kept;          // resolved to the half's value by k_cluster_draws
+    *flag = 0;
+}
+
+__global__ void __launch_bounds__(256) k_cluster_draws(uint64_t key, const int64_t* __restrict__ n_rows, int32_t m,
+                                                       const int32_t* __restrict__ c_off,
+                                                       const int32_t* __restrict__ c_mem,
+                                                       const int64_t* __restrict__ draw_base,
+                                                       const int64_t* __restrict__ kept_src,
+                                                       int32_t* __restrict__ picks, int64_t* __restrict__ uni_start,
+                                                       int32_t* __restrict__ flag) {
+    const int64_t b = *n_rows;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y;
+    if (i == 0 && j == 0 && uni_start[m + 1] >= 0)
+        uni_start[m + 1] = (int64_t)(philox_out(key, (uint64_t)uni_start[m + 1]) >> 32);
+    if (i >= b) return;
+    const int32_t lo = c_off[j], n = c_off[j + 1] - lo;
+    if (n == 1) {
+        picks[i * m + j] = c_mem[lo];
+        return;
+    }
+    const int has = kept_src[j] >= 0 ? 1 : 0;
+    uint32_t d;
+    if (has && i == 0) {
+        d = (uint32_t)(philox_out(key, (uint64_t)kept_src[j]) >> 32);
+    } else {
+        const int64_t k = i - has;
+        const uint64_t w = philox_out(key, (uint64_t)draw_base[j] + (uint64_t)(k >> 1));
+        d = (k & 1) ? (uint32_t)(w >> 32) : (uint32_t)w;
+    }
+    const uint32_t nn = (uint32_t)n, thresh = (0u - nn) % nn;
+    const uint64_t mm = (uint64_t)d * nn;
+    if ((uint32_t)mm < thresh) atomicOr(flag, 1);
+    picks[i * m + j] = c_mem[lo + (int32_t)(mm >> 32)];
+}
+
 __global__ void __launch_bounds__(kPickThreads) k_cluster_picks(uint64_t key, const int64_t* __restrict__ n_rows,
                                                                  int32_t m, const int32_t* __restrict__ c_off,
                                                                  const int32_t* __restrict__ c_mem,
                                                                  int32_t* __restrict__ picks,
-                                                                 int64_t* __restrict__ uni_start) {
+                                                                 int64_t* __restrict__ uni_start,
+                                                                 const int32_t* __restrict__ flag) {
+    if (flag && *flag == 0) return;   // the fast path had no rejection: nothing to redo
     __shared__ uint64_t s_next;        // next fresh 64-bit output
     __shared__ uint32_t s_kept;        // kept high half (valid if s_has)
     __shared__ int s_has;
@@ -1208,9 +1314,9 @@ int64_t nvc_clustered_workspace_bytes(int64_t p, int32_t m) {
 }
 
 int nvc_clustered_select(const nvc_scene* sc, const float* vis, int64_t vis_stride, const double* pos,
-                         const double* nrm, const double* alb, int64_t p, int32_t m, const int32_t* c_off,
-                         const int32_t* c_mem, uint64_t key, uint64_t offset, double floor, int64_t* ids,
-                         double* pts, double* big_w, void* ws, void* stream) {
+                         const double* nrm, const double* alb, const double* factor, int64_t p, int32_t m,
+                         const int32_t* c_off, const int32_t* c_mem, uint64_t key, uint64_t offset, double floor,
+                         int64_t* ids, double* pts, double* big_w, void* ws, void* stream) {
     NVC_REQUIRE(sc && vis && pos && nrm && alb && c_off && c_mem && ids && pts && big_w && ws,
                 "nvc_clustered_select: null argument");
     NVC_REQUIRE(m >= 1 && vis_stride >= m, "nvc_clustered_select: bad m / stride");
@@ -1220,8 +1326,10 @@ int nvc_clustered_select(const nvc_scene* sc, const float* vis, int64_t vis_stri
     const int nblk = grid1(p, kCsThreads);
     k_cs_step1<<<nblk, kCsThreads, 0, s>>>(vis, vis_stride, p, m, key, offset, floor, w);
     k_cs_rank<<<nblk, kCsThreads, (size_t)m * 4, s>>>(p, m, w);
-    k_cs_scan<<<1, 1024, 0, s>>>(nblk, m, c_off, p, offset, w);
-    k_cs_step2<<<nblk, kCsThreads, 0, s>>>(*sc, pos, nrm, alb, p, m, c_off, c_mem, key, w, ids, pts, big_w);
+    k_cs_scan<<<m, 1024, 0, s>>>(nblk, m, w);
+    k_cs_bases<<<1, 1, 0, s>>>(m, c_off, p, offset, w);
+    k_cs_step2<<<nblk, kCsThreads, 0, s>>>(*sc, pos, nrm, alb, p, m, c_off, c_mem, key, w, factor, p, ids, pts,
+                                           big_w);
     return check_launch("nvc_clustered_select");
 }
 
@@ -1294,7 +1402,7 @@ int nvc_gen_train_batch(const nvc_scene* sc, const nvc_camera* cam, uint64_t key
 }
 
 int64_t nvc_cluster_workspace_bytes(int64_t b_max, int32_t m) {
-    return ((b_max * m * 4 + 255) / 256) * 256 + 8 * ((int64_t)m + 2) + 256;
+    return ((b_max * m * 4 + 255) / 256) * 256 + 8 * (3 * (int64_t)m + 2) + 8 + 256;
 }
 
 int64_t nvc_cluster_state_offset(int64_t b_max, int32_t m) {   // int64 [m+2]: uni starts, next, kept
@@ -1310,7 +1418,14 @@ int nvc_cluster_targets(const nvc_scene* sc, uint64_t key, const double* pos, co
     cudaStream_t s = (cudaStream_t)stream;
     int32_t* picks = (int32_t*)ws;
     int64_t* uni = (int64_t*)((char*)ws + nvc_cluster_state_offset(b_max, m));
-    k_cluster_picks<<<1, kPickThreads, 0, s>>>(key, n_rows, m, c_off, c_mem, picks, uni);
+    int64_t* base = uni + (m + 2);
+    int64_t* kept = base + m;
+    int32_t* flag = (int32_t*)(kept + m);
+    k_cluster_chain<<<1, 1, 0, s>>>(n_rows, m, c_off, uni, base, kept, flag);
+    dim3 gd(grid1(b_max, 256), m);
+    k_cluster_draws<<<gd, 256, 0, s>>>(key, n_rows, m, c_off, c_mem, base, kept, picks, uni, flag);
+    k_cluster_picks<<<1, kPickThreads, 0, s>>>(key, n_rows, m, c_off, c_mem, picks, uni,
+                                               getenv("NVC_CLUSTER_EXACT_WALK") ? nullptr : flag);
     int rc = check_launch("k_cluster_picks");
     if (rc) return rc;
     const int64_t cap = b_max / n_shards + 1;

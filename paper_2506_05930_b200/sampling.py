@@ -337,9 +337,12 @@ def clustered_sample_device(ctx: PixelCtx, cache, clusters, key: int, offset: in
     ws = torch.empty(lib.nvc_clustered_workspace_bytes(p, m), dtype=torch.uint8, device=ctx.device)
     c_off, c_mem = _cluster_tables(clusters, ctx.device)
     floor = float(clamp_floor) if clamp_floor and clamp_floor > 0.0 else 0.0
+    # an f64 per-camera factor table (PixelCtx(table_dtype=float64)) replaces the
+    # per-(pixel, member) FP64 factor evaluation with one load (same values)
+    fac = ctx.factor_device() if ctx.table_dtype == np.float64 else None
     _lib.call("nvc_clustered_select", ctx.dscene.struct, vis.data_ptr(), vis.shape[1], ctx.pos.data_ptr(),
-              ctx.nrm.data_ptr(), ctx.alb.data_ptr(), p, m, c_off.data_ptr(), c_mem.data_ptr(), key, offset, floor,
-              ids.data_ptr(), pts.data_ptr(), big_w.data_ptr(), ws.data_ptr(), _lib.stream_ptr())
+              ctx.nrm.data_ptr(), ctx.alb.data_ptr(), _lib.ptr(fac), p, m, c_off.data_ptr(), c_mem.data_ptr(), key,
+              offset, floor, ids.data_ptr(), pts.data_ptr(), big_w.data_ptr(), ws.data_ptr(), _lib.stream_ptr())
     lp = ws.view(torch.int64)[lib.nvc_clustered_state_offset(p, m) // 8]
     return ids, pts, big_w, lp + 2 * p - offset
 

@@ -759,7 +759,11 @@ def rooms():
 class TestClusters:
     """Clustered NVC on the device (training.py:121-128, sampling.py:302-352)."""
 
-    def test_cluster_targets_bit_exact_and_stream_state(self, rooms, g_clusters):
+    @pytest.mark.parametrize("walk", [False, True])
+    def test_cluster_targets_bit_exact_and_stream_state(self, rooms, g_clusters, walk, monkeypatch):
+        """Parallel no-rejection fast path, and the exact sequential walk forced on."""
+        if walk:
+            monkeypatch.setenv("NVC_CLUSTER_EXACT_WALK", "1")
         s, cs = rooms
         g = R.stream(0, 2, 0, R.TARGETS)
         tgt = compute_visibility_targets(g_clusters["ct_pos"], s, g, clusters=cs)
@@ -855,12 +859,15 @@ class TestClusteredSampling:
         want = ctx.n * cs.m + int(sum(n_j[j] * cs.members[j].size for j in range(cs.m))) + 2 * ctx.n
         assert R.position(g)[1] == want
 
-    def test_native_cluster_cache_vs_oracle(self, rooms, g_scenes):
+    @pytest.mark.parametrize("table", [np.float32, np.float64])
+    def test_native_cluster_cache_vs_oracle(self, rooms, g_scenes, table):
+        """Per-(pixel, member) factors computed in the kernel (f32 table context) or read
+        from the per-camera f64 factor table: same results."""
         from paper_2506_05930_b200 import clustered_sample_batch, make_cache
         from paper_2506_05930_b200.render import gbuffer_device
         s, cs = rooms
         pos, nrm, alb, _, _ = gbuffer_device(s, s.camera.resized(80, 45))
-        ctx = PixelCtx(s, pos, nrm, alb)
+        ctx = PixelCtx(s, pos, nrm, alb, table_dtype=table)
         c = make_cache(s, "clusters", seed=1, clusters=cs.m)
         c.grid_params = (np.random.default_rng(3).standard_normal(c.grid_params.shape) * 0.5).astype(np.float32)
         vis = c.infer(pos.cpu().numpy())
