@@ -306,11 +306,13 @@ def gpu_arm(args) -> None:
     barrier()
     with ClockSampler(local) as clocks:
         start.record(stream)
+        t_issue = time.perf_counter()
         for f in range(args.steps):
             loss = frame(args.warmup + f)
         if cache.select_done is not None:
             stream.wait_event(cache.select_done)
         end.record(stream)
+        issue_ms = (time.perf_counter() - t_issue) * 1e3 / args.steps   # host time to enqueue a frame
         barrier()
     ms = start.elapsed_time(end) / args.steps
     t = torch.tensor([ms], device=dev)
@@ -422,6 +424,7 @@ def gpu_arm(args) -> None:
                        "pixels_per_gpu": P, "global_batch": (N_WORLD + N_SCREEN) * world,
                        "parallelism": f"dp{world} (train) + {world} screen tiles (query)",
                        "l2": "inputs > L2 every frame (lum table 265 MB + 16.8 M-parameter Adam stream 530 MB)",
+                       "host_issue_ms_per_frame": issue_ms,
                        "stage_ms": {"train_frame": tr_ms, "query": q_ms, "k_enc_tiles2": k_ms[0],
                                     "k_mlp_ts": k_ms[1], "k_nls32": k_ms[2],
                                     **({"k_shade": statistics.median(split_shade)} if shade else {})}},
