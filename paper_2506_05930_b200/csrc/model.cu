@@ -892,6 +892,24 @@ __host__ __device__ inline int64_t wpack_index(const Net& net, int i, int n, int
     return o + umma_off(n, k, np[i], kp[i]) / 2;
 }
 
+// transposed packs (the backward dA = dZ . W operand of the tensor-core training
+// step) follow the forward blocks: block l is W_l^T, [kp x np] K-major
+__host__ __device__ inline bool wpack_has_t(const Net& net) {
+    int np[NVC_MAX_LAYERS], kp[NVC_MAX_LAYERS];
+    umma_pads(net.dims, net.n_layers, np, kp);
+    for (int j = 0; j < net.n_layers; ++j)
+        if (np[j] != 16 && np[j] != 32 && np[j] % 64 != 0) return false;
+    return true;
+}
+__host__ __device__ inline int64_t wpack_t_index(const Net& net, int i, int n, int k) {
+    int np[NVC_MAX_LAYERS], kp[NVC_MAX_LAYERS];
+    umma_pads(net.dims, net.n_layers, np, kp);
+    int64_t o = 0;
+    for (int j = 0; j < net.n_layers; ++j) o += umma_block_halfs(np[j], kp[j]);
+    for (int j = 0; j < i; ++j) o += umma_block_halfs(kp[j], np[j]);
+    return o + umma_off(k, n, kp[i], np[i]) / 2;
+}
+
 __device__ __forceinline__ void put_pair(uint16_t* t2, int64_t i, int F, int64_t T, uint16_t h) {
     const int64_t e = i / F, f = i - e * F;
     t2[e * 2 * F + f] = h;                               // own slot, low half
@@ -1066,7 +1084,9 @@ __global__ void k_adam_mlp(Net net, float* __restrict__ p, float* __restrict__ m
         if (i >= net.woff[l] && i < net.boff[l]) {
             const int64_t e = i - net.woff[l];
             const int K = net.dims[l];
-            wpack[wpack_index(net, l, (int)(e / K), (int)(e % K))] = __half_as_ushort(__float2half_rn(pn));
+            const uint16_t hv = __half_as_ushort(__float2half_rn(pn));
+            wpack[wpack_index(net, l, (int)(e / K), (int)(e % K))] = hv;
+            if (wpack_has_t(net)) wpack[wpack_t_index(net, l, (int)(e / K), (int)(e % K))] = hv;
         }
     }
 }
@@ -1090,6 +1110,7 @@ __global__ void k_shadow_wpack(Net net, const float* __restrict__ p, uint16_t* _
             float w = 0.0f;
             if (n < net.dims[l + 1] && k < net.dims[l]) w = p[net.woff[l] + (int64_t)n * net.dims[l] + k];
             wpack[wpack_index(net, l, n, k)] = __half_as_ushort(__float2half_rn(w));
+            if (wpack_has_t(net)) wpack[wpack_t_index(net, l, n, k)] = __half_as_ushort(__float2half_rn(w));
             return;
         }
         o -= sz;
@@ -1103,8 +1124,14 @@ int64_t wpack_count_of(const nvc_model* m) {
     umma_pads(m->dims, m->n_layers, np, kp);
     int64_t c = 0;
     for (int i = 0; i < m->n_layers; ++i) c += umma_block_halfs(np[i], kp[i]);
+    if (wpack_has_t(net_of(m)))
+        for (int i = 0; i < m->n_layers; ++i) c += umma_block_halfs(kp[i], np[i]);
     return c;
 }
+
+int train_tc(const nvc_model* m, int64_t grid_count, const int64_t* woff, const int64_t* boff, int64_t mlp_count,
+             const float* act0, int64_t b_max, const int64_t* b_dev, int shard, int n_shards, const float* tgt,
+             const float* mask, float* dact0, float* part_w, double* part_loss, int nblk, cudaStream_t s);
 
 }  // namespace nvc
 
@@ -1186,6 +1213,7 @@ int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, con
     const bool wg = t3_layout(net).total * 4 + 64 > 200 * 1024;   // too wide for W in smem (C4): W from L1/L2
     const T3Layout tl3 = t3_layout(net, !wg);
     const int smem3 = tl3.total * 4 + 64;
+    int nblk_red = nblk;   // partial sets k_reduce_parts sums (one per training block)
     if (split && smem3 <= 200 * 1024) {
         char* p2 = (char*)part_loss + ((int64_t)nblk * 8 + 255) / 256 * 256;
         float* act0 = (float*)p2;
@@ -1193,7 +1221,12 @@ int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, con
         k_tr_encode<<<grid1(rows_max * g.L, 128), 128, 0, s>>>(g, m->params, pos, b_max, b_dev, shard, n_shards, act0);
         rc = check_launch("k_tr_encode");
         if (rc) return rc;
-        if (wg) {
+        const bool tc = getenv("NVC_TRAIN_TC") != nullptr &&
+                        train_tc(m, net.grid_count, net.woff, net.boff, net.mlp_count, act0, b_max, b_dev, shard,
+                                 n_shards, tgt, mask, dact0, part_w, part_loss, grid1(rows_max, 128), s) == 0;
+        if (tc) {
+            nblk_red = grid1(rows_max, 128);
+        } else if (wg) {
             cudaFuncSetAttribute(k_train3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
             k_train3<true><<<nblk, kThreads, smem3, s>>>(net, tl3, m->params, act0, b_max, b_dev, shard, n_shards,
                                                          tgt, mask, dact0, part_w, part_loss);
@@ -1215,7 +1248,7 @@ int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, con
     }
     rc = check_launch("nvc_train_grads");
     if (rc) return rc;
-    k_reduce_parts<<<grid1(net.mlp_count, 32), 256, 0, s>>>(part_w, part_loss, nblk, net.mlp_count,
+    k_reduce_parts<<<grid1(net.mlp_count, 32), 256, 0, s>>>(part_w, part_loss, nblk_red, net.mlp_count,
                                                              net.grid_count, sink_of(m), loss_out, b_max, b_dev);
     return check_launch("k_reduce_parts");
 }

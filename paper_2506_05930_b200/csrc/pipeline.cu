@@ -1342,6 +1342,289 @@ int pipeline_query(const nvc_model* m, const nvc_scene* sc, const double* pos, i
                            pts, big_w, albedo, rgb, vis_out, ws, s);
 }
 
+
+// ---------------------------------------------------------------------------
+// Training MLP on the tensor cores (opt-in: NVC_TRAIN_TC=1; measured 65 us vs
+// 49 us for the fp32 SIMT k_train3 at the C2 batch -- one 128-row tile per CTA
+// leaves the step latency-bound -- and a loss curve within ~2 % of the
+// reference instead of bit-faithful fp32, so it is not the default): one CTA per
+// 128-row tile runs the forward pass and the backward pass as tcgen05 MMAs
+// (fp16 operands, fp32 accumulators in TMEM):
+//   forward   Z_l   = A_l . W_l^T            (A_l [128 x K] K-major, packed W_l)
+//   backward  dW_l  = dZ_l^T . A_l           (dZ^T [n x 128] and A_l^T [k x 128], K = rows)
+//             db_l  = dZ_l^T . 1             (a ones column)
+//             dA_l  = dZ_l . W_l             (W_l^T packed after the forward blocks)
+// dZ is carried in fp16 scaled by 2^18 (it starts at 2(out-t)/(bK) ~ 1e-6)
+// and unscaled on read-out.  Per-CTA dW/db partials go to the same part_w
+// layout k_reduce_parts sums in fixed order; dA_0 feeds the hash-grid scatter.
+// Parity is by tolerance (loss curve), not bitwise like the fp32 SIMT step.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr float kGradScale = 262144.0f;   // 2^18
+
+struct TrainTC {
+    int L, D0, K;
+    int dims[NVC_MAX_LAYERS + 1], np[NVC_MAX_LAYERS], kp[NVC_MAX_LAYERS];
+    int wofs[NVC_MAX_LAYERS], wofsT[NVC_MAX_LAYERS];   // halfs into the packed weights
+    int64_t woff_rel[NVC_MAX_LAYERS], boff_rel[NVC_MAX_LAYERS], boff_abs[NVC_MAX_LAYERS];
+    int w_halfs;                                        // forward + transposed blocks
+    float alpha;
+    int out_sigmoid;
+    int sm_w, sm_a[NVC_MAX_LAYERS], sm_at[NVC_MAX_LAYERS], sm_g, sm_gt, sm_ones, sm_bias, sm_total;
+};
+
+__device__ __forceinline__ float sigmoid_exact(float z) {   // mlp.py:101-107
+    if (z >= 0.0f) return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-z)));
+    const float e = expf(z);
+    return __fdiv_rn(e, __fadd_rn(1.0f, e));
+}
+
+__device__ __forceinline__ void put_h(uint8_t* base, uint32_t off, float v) {
+    *reinterpret_cast<__half*>(base + off) = __float2half_rn(v);
+}
+
+__global__ void __launch_bounds__(128, 1) k_train_tc(TrainTC t, const float* __restrict__ params,
+                                                    const uint16_t* __restrict__ wpack,
+                                                    const float* __restrict__ act0g, int64_t b_max,
+                                                    const int64_t* __restrict__ b_dev, int shard, int n_shards,
+                                                    const float* __restrict__ tgt, const float* __restrict__ mask,
+                                                    float* __restrict__ dact0g, float* __restrict__ part_w,
+                                                    double* __restrict__ part_loss) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    __shared__ double s_loss[4];
+    uint8_t* sm = smem_raw + ((1024u - (s32(smem_raw) & 1023u)) & 1023u);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t b = b_dev ? *b_dev : b_max;
+    const int64_t lo = b * shard / n_shards, hi = b * (shard + 1) / n_shards;
+    const int64_t r0g = (int64_t)blockIdx.x * kT;
+    const int nr = (int)max((int64_t)0, min((int64_t)kT, (hi - lo) - r0g));
+    const int L = t.L, r = tid;
+    float* bias = reinterpret_cast<float*>(sm + t.sm_bias);
+    {   // weights (forward + transposed packs), biases, ones column, input tile
+        const uint4* src = reinterpret_cast<const uint4*>(wpack);
+        uint4* dst = reinterpret_cast<uint4*>(sm + t.sm_w);
+        for (int i = tid; i < t.w_halfs / 8; i += 128) dst[i] = __ldg(src + i);
+        int bo = 0;
+        for (int l = 0; l < L; ++l) {
+            for (int n = tid; n < t.np[l]; n += 128) bias[bo + n] = n < t.dims[l + 1] ? __ldg(params + t.boff_abs[l] + n) : 0.0f;
+            bo += t.np[l];
+        }
+        for (int i = tid; i < 16 * kT; i += 128) {
+            const int rr = i / kT, k = i % kT;
+            put_h(sm + t.sm_ones, umma_off(rr, k, 16, kT), rr == 0 ? 1.0f : 0.0f);
+        }
+        for (int k = 0; k < t.kp[0]; ++k) {
+            const float v = (r < nr && k < t.D0) ? __ldg(act0g + (r0g + r) * t.D0 + k) : 0.0f;
+            put_h(sm + t.sm_a[0], umma_off(r, k, kT, t.kp[0]), v);
+            put_h(sm + t.sm_at[0], umma_off(k, r, t.kp[0], kT), v);
+        }
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(&tbase)), "r"(256)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    fence_async();
+    tc_before();
+    __syncthreads();   // TMEM address, barrier and the staged tiles visible to every thread
+    tc_after();
+    uint32_t phase = 0;
+    const uint32_t tmem = tbase;
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    auto sync_issue = [&]() {   // generic smem writes -> async proxy, then one thread issues
+        fence_async();
+        tc_before();
+        __syncthreads();
+        tc_after();
+    };
+    auto wait_mma = [&]() {
+        if (tid == 0) commit(&bar);
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        tc_after();
+    };
+    auto idesc = [](int n) { return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kT >> 4) << 24); };
+    const uint32_t w_addr = s32(sm + t.sm_w);
+
+    // ---- forward ----
+    double lsum = 0.0;
+    const float bk = (float)(b * (int64_t)t.K);
+    int bo = 0;
+    for (int l = 0; l < L; ++l) {
+        sync_issue();
+        if (tid == 0) {
+            const uint32_t a_addr = s32(sm + t.sm_a[l]), wl = w_addr + 2u * (uint32_t)t.wofs[l];
+            for (int kk = 0; kk < t.kp[l] / 16; ++kk)
+                mma(tmem, desc_of(a_addr, kT, t.kp[l], kk), desc_of(wl, t.np[l], t.kp[l], kk), idesc(t.np[l]), kk > 0);
+        }
+        wait_mma();
+        const bool last = l == L - 1;
+        for (int c = 0; c < t.np[l]; c += 16) {
+            float v[16];
+            tld16(tmem + lane_base + (uint32_t)c, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int n = c + i;
+                const float z = v[i] + bias[bo + n];
+                if (!last) {
+                    const float a = z >= 0.0f ? z : t.alpha * z;
+                    put_h(sm + t.sm_a[l + 1], umma_off(r, n, kT, t.kp[l + 1]), a);
+                    put_h(sm + t.sm_at[l + 1], umma_off(n, r, t.kp[l + 1], kT), a);
+                } else {
+                    // loss + output delta (mlp.py:143-149, 160-168), dZ scaled into fp16
+                    float d = 0.0f;
+                    if (r < nr && n < t.K) {
+                        const float sg = t.out_sigmoid ? sigmoid_exact(z) : (z >= 0.0f ? z : t.alpha * z);
+                        const int64_t li = (r0g + r) * t.K + n;
+                        const float outc = t.out_sigmoid ? fminf(fmaxf(sg, 1e-6f), 0.999999f) : sg;
+                        const float tt = tgt[li];
+                        const float mk = mask ? mask[li] : 1.0f;
+                        float dd = __fsub_rn(outc, tt);
+                        if (mask) dd = __fmul_rn(dd, mk);
+                        lsum += (double)__fmul_rn(dd, dd);
+                        float dout = __fdiv_rn(__fmul_rn(2.0f, __fsub_rn(sg, tt)), bk);
+                        if (mask) dout = __fmul_rn(dout, mk);
+                        d = t.out_sigmoid ? __fmul_rn(__fmul_rn(dout, sg), __fsub_rn(1.0f, sg))
+                                          : (z >= 0.0f ? dout : __fmul_rn(dout, t.alpha));
+                    }
+                    put_h(sm + t.sm_g, umma_off(r, n, kT, t.np[l]), d * kGradScale);
+                    put_h(sm + t.sm_gt, umma_off(n, r, kT, kT), d * kGradScale);
+                }
+            }
+        }
+        bo += t.np[l];
+    }
+    for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    if (lane == 0) s_loss[warp] = lsum;
+
+    // ---- backward ----
+    for (int l = L - 1; l >= 0; --l) {
+        const int np = t.np[l], kp = t.kp[l], K_in = t.dims[l], N = t.dims[l + 1];
+        sync_issue();
+        if (tid == 0) {
+            const uint32_t gt = s32(sm + t.sm_gt), at = s32(sm + t.sm_at[l]), ones = s32(sm + t.sm_ones);
+            const uint32_t g = s32(sm + t.sm_g), wt = w_addr + 2u * (uint32_t)t.wofsT[l];
+            for (int kk = 0; kk < kT / 16; ++kk) {
+                mma(tmem, desc_of(gt, kT, kT, kk), desc_of(at, kp, kT, kk), idesc(kp), kk > 0);         // dW
+                mma(tmem + 64u, desc_of(gt, kT, kT, kk), desc_of(ones, 16, kT, kk), idesc(16), kk > 0);  // db
+            }
+            for (int kk = 0; kk < np / 16; ++kk)
+                mma(tmem + 128u, desc_of(g, kT, np, kk), desc_of(wt, kp, np, kk), idesc(kp), kk > 0);    // dA
+        }
+        wait_mma();
+        // dW_l / db_l rows: TMEM lane n
+        {
+            float* gw = part_w + (int64_t)blockIdx.x * t.woff_rel[L] + t.woff_rel[l];   // woff_rel[L] = mlp_count
+            float* gb = part_w + (int64_t)blockIdx.x * t.woff_rel[L] + t.boff_rel[l];
+            for (int c = 0; c < kp; c += 16) {
+                float v[16];
+                tld16(tmem + lane_base + (uint32_t)c, v);
+                if (r < N)
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        if (c + i < K_in) gw[(int64_t)r * K_in + c + i] = v[i] * (1.0f / kGradScale);
+            }
+            float v[16];
+            tld16(tmem + lane_base + 64u, v);
+            if (r < N) gb[r] = v[0] * (1.0f / kGradScale);
+        }
+        // dA_{l} rows (TMEM lane = row): next dZ, or the encoder gradient
+        for (int c = 0; c < kp; c += 16) {
+            float v[16];
+            tld16(tmem + lane_base + 128u + (uint32_t)c, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int k = c + i;
+                if (l > 0) {
+                    const __half a = *reinterpret_cast<const __half*>(sm + t.sm_a[l] + umma_off(r, k, kT, kp));
+                    const bool neg = (__half_as_ushort(a) & 0x8000u) != 0;   // leaky'(z): z >= 0 -> 1, else alpha
+                    const float d = r < nr ? (neg ? v[i] * t.alpha : v[i]) : 0.0f;
+                    put_h(sm + t.sm_g, umma_off(r, k, kT, kp), d);
+                    put_h(sm + t.sm_gt, umma_off(k, r, kT, kT), d);
+                } else if (r < nr && k < t.D0) {
+                    dact0g[(r0g + r) * t.D0 + k] = v[i] * (1.0f / kGradScale);
+                }
+            }
+        }
+    }
+    tc_before();
+    __syncthreads();
+    tc_after();
+    if (tid == 0) part_loss[blockIdx.x] = ((s_loss[0] + s_loss[1]) + (s_loss[2] + s_loss[3])) / (double)t.K;
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
+}
+}  // namespace
+
+// plan: 0 if the tensor-core training step covers this model (fits in smem/TMEM)
+int train_tc_plan(const nvc_model* m, int64_t grid_count, const int64_t* woff, const int64_t* boff, int64_t mlp_count,
+                  TrainTC& t) {
+    if (!m->wpack) return 1;
+    if (m->n_layers < 2 || m->n_layers >= NVC_MAX_LAYERS || m->features * m->levels > 64) return 1;
+    t.L = m->n_layers;
+    t.D0 = m->dims[0];
+    t.K = m->dims[m->n_layers];
+    for (int i = 0; i <= t.L; ++i) t.dims[i] = m->dims[i];
+    umma_pads(m->dims, t.L, t.np, t.kp);
+    int o = 0;
+    for (int l = 0; l < t.L; ++l) {
+        if (t.np[l] > 64 || t.kp[l] > 64 || (t.np[l] != 16 && t.np[l] != 32 && t.np[l] != 64)) return 1;
+        t.wofs[l] = o;
+        o += (int)umma_block_halfs(t.np[l], t.kp[l]);
+    }
+    for (int l = 0; l < t.L; ++l) {
+        t.wofsT[l] = o;
+        o += (int)umma_block_halfs(t.kp[l], t.np[l]);
+    }
+    t.w_halfs = o;
+    for (int l = 0; l < t.L; ++l) {
+        t.woff_rel[l] = woff[l] - grid_count;
+        t.boff_rel[l] = boff[l] - grid_count;
+        t.boff_abs[l] = boff[l];
+    }
+    t.woff_rel[t.L] = mlp_count;
+    t.alpha = m->alpha;
+    t.out_sigmoid = m->out_sigmoid;
+    auto al = [](int x) { return (x + 1023) / 1024 * 1024; };
+    int so = 0;
+    t.sm_w = so;
+    so += al(o * 2);
+    for (int l = 0; l < t.L; ++l) {
+        t.sm_a[l] = so;
+        so += al(kT * t.kp[l] * 2);
+        t.sm_at[l] = so;
+        so += al(kT * t.kp[l] * 2);
+    }
+    t.sm_g = so;
+    so += al(kT * 64 * 2);
+    t.sm_gt = so;
+    so += al(kT * kT * 2);
+    t.sm_ones = so;
+    so += al(16 * kT * 2);
+    t.sm_bias = so;
+    so += al(t.L * 64 * 4);
+    t.sm_total = so + 1024;
+    return t.sm_total <= 227 * 1024 ? 0 : 1;
+}
+
+// the whole step: returns 1 (nothing launched) when the model is not covered
+int train_tc(const nvc_model* m, int64_t grid_count, const int64_t* woff, const int64_t* boff, int64_t mlp_count,
+             const float* act0, int64_t b_max, const int64_t* b_dev, int shard, int n_shards, const float* tgt,
+             const float* mask, float* dact0, float* part_w, double* part_loss, int nblk, cudaStream_t s) {
+    TrainTC t;
+    if (train_tc_plan(m, grid_count, woff, boff, mlp_count, t)) return 1;
+    cudaFuncSetAttribute(k_train_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, t.sm_total);
+    k_train_tc<<<nblk, 128, t.sm_total, s>>>(t, m->params, m->wpack, act0, b_max, b_dev, shard, n_shards, tgt, mask,
+                                             dact0, part_w, part_loss);
+    return check_launch("k_train_tc");
+}
+
 }  // namespace nvc
 
 

@@ -548,6 +548,23 @@ class TestTraining:
         ref64 = g_train["c1_loss_f64"]
         assert np.max(np.abs(np.array(got) - ref64) / ref64) < 1e-2
 
+    def test_tensor_core_training_step(self, pbox8, g_train, monkeypatch):
+        """Opt-in tcgen05 training step (fp16 operands, fp32 TMEM accumulators, 2^18
+        gradient scaling): deterministic, first-step loss exact to 1e-6, and the C1
+        loss curve within 3 % of the reference's (fp32 SIMT path: 1 %)."""
+        monkeypatch.setenv("NVC_TRAIN_TC", "1")
+        c = self._c1(pbox8)
+        loss = c.train_step(g_train["c1_pos"], g_train["c1_tgt"].astype(np.float32))
+        assert loss == pytest.approx(float(g_train["c1_step0_loss"]), rel=1e-6)
+        np.testing.assert_allclose(c.net_params.weights[0], g_train["c1_step0_w0"], atol=0.01)
+        c = self._c1(pbox8)
+        want = g_train["c1_loss_f32"]
+        got = [train_frame(pbox8, pbox8.camera, c, TrainFrameConfig(), frame=f) for f in range(len(want))]
+        np.testing.assert_allclose(got, want, rtol=3e-2)
+        c2 = self._c1(pbox8)
+        again = [train_frame(pbox8, pbox8.camera, c2, TrainFrameConfig(), frame=f) for f in range(len(want))]
+        assert got == again
+
     def test_bitwise_deterministic_trajectory(self, pbox8):
         def run():
             c = self._c1(pbox8, seed=5)
