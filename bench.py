@@ -221,7 +221,10 @@ def gpu_arm(args) -> None:
         cache.set_compact(True)
     if os.environ.get("NVC_L2_PIN"):      # measured slower (it starves the streaming Adam of L2)
         cache.pin_table_in_l2()
-    cfg = TrainFrameConfig(n_world=N_WORLD * world, n_screen=N_SCREEN * world, seed=0)
+    # one training step per frame on the reference's batch (4096 world + 4096 screen
+    # samples of the N-tile frame), its rows sharded over the ranks: the gradient
+    # exchange (the batch's touched entries) stays ~17 MB at any N
+    cfg = TrainFrameConfig(n_world=N_WORLD, n_screen=N_SCREEN, seed=0)
     # training batches are generated one frame ahead on a side stream (they depend on
     # the frame index only), overlapping the FP64 ray kernels with training + query
     pipe = BatchPipeline(scene, cam, cfg, kk, dev, rank, world, cache=cache)
@@ -418,11 +421,12 @@ def gpu_arm(args) -> None:
             "config": {"workload": (f"C4: {WIDTH}x{HEIGHT * world} rooms128 (K=128), L=16 T=2^19 F=2, MLP 3x128, "
                                     if c4 else
                                     f"C2: {WIDTH}x{HEIGHT * world} boxes32 (K=32), L=16 T=2^19 F=2, MLP 3x64, ")
-                                   + f"1 online frame = train batch {(N_WORLD + N_SCREEN) * world} + NLS over all pixels"
+                                   + f"1 online frame = train batch {N_WORLD + N_SCREEN} (rows sharded over {world} ranks) "
+                                   + "+ NLS over all pixels"
                                    + (" + one shadow ray per pixel (shade_batch)" if shade else ""),
-                       "train_samples_per_s": (N_WORLD + N_SCREEN) * world / (ms * 1e-3),
-                       "pixels_per_gpu": P, "global_batch": (N_WORLD + N_SCREEN) * world,
-                       "parallelism": f"dp{world} (train) + {world} screen tiles (query)",
+                       "train_samples_per_s": (N_WORLD + N_SCREEN) / (ms * 1e-3),
+                       "pixels_per_gpu": P, "global_batch": N_WORLD + N_SCREEN,
+                       "parallelism": f"dp{world} (train: batch rows sharded, one allreduce) + {world} screen tiles (query)",
                        "l2": "inputs > L2 every frame (lum table 265 MB + 16.8 M-parameter Adam stream 530 MB)",
                        "host_issue_ms_per_frame": issue_ms,
                        "stage_ms": {"train_frame": tr_ms, "query": q_ms, "k_enc_tiles2": k_ms[0],
