@@ -36,7 +36,11 @@ int check_launch(const char* what) {
 
 namespace {
 
-constexpr int kRows = 32;      // rows per block in the SIMT MLP kernels
+#ifndef NVC_TRAIN_ROWS
+#define NVC_TRAIN_ROWS 32
+#endif
+constexpr int kRows = NVC_TRAIN_ROWS;   // rows per block in the SIMT MLP kernels
+constexpr int kRPT = kRows >= 32 ? 2 : 1;   // rows per thread tile in k_train3 (keeps 256 threads busy)
 constexpr int kThreads = 256;
 
 struct Net {
@@ -477,27 +481,28 @@ __global__ void __launch_bounds__(kThreads, 2) k_train3(Net net, T3Layout tl, co
         const float* W = kWG ? params + net.woff[l] : sm + tl.w[l];
         float* out = sm + tl.act[l + 1];
         const bool last = l == net.n_layers - 1;
-        for (int t = tid; t < (kRows / 2) * ng; t += kThreads) {
-            const int r0 = (t / ng) * 2, nn = t % ng;
-            float acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+        for (int t = tid; t < (kRows / kRPT) * ng; t += kThreads) {
+            const int r0 = (t / ng) * kRPT, nn = t % ng;
+            float acc[kRPT][4] = {};
             for (int k = 0; k < Ki; k += 4) {
-                const float4 a0 = *reinterpret_cast<const float4*>(A + r0 * Ki + k);
-                const float4 a1 = *reinterpret_cast<const float4*>(A + (r0 + 1) * Ki + k);
+                float4 av[kRPT];
+#pragma unroll
+                for (int i = 0; i < kRPT; ++i) av[i] = *reinterpret_cast<const float4*>(A + (r0 + i) * Ki + k);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const float4 w = *reinterpret_cast<const float4*>(W + (nn + j * ng) * S + k);
-                    acc[0][j] = fmaf(a0.x, w.x, acc[0][j]);
-                    acc[1][j] = fmaf(a1.x, w.x, acc[1][j]);
-                    acc[0][j] = fmaf(a0.y, w.y, acc[0][j]);
-                    acc[1][j] = fmaf(a1.y, w.y, acc[1][j]);
-                    acc[0][j] = fmaf(a0.z, w.z, acc[0][j]);
-                    acc[1][j] = fmaf(a1.z, w.z, acc[1][j]);
-                    acc[0][j] = fmaf(a0.w, w.w, acc[0][j]);
-                    acc[1][j] = fmaf(a1.w, w.w, acc[1][j]);
+#pragma unroll
+                    for (int i = 0; i < kRPT; ++i) acc[i][j] = fmaf(av[i].x, w.x, acc[i][j]);
+#pragma unroll
+                    for (int i = 0; i < kRPT; ++i) acc[i][j] = fmaf(av[i].y, w.y, acc[i][j]);
+#pragma unroll
+                    for (int i = 0; i < kRPT; ++i) acc[i][j] = fmaf(av[i].z, w.z, acc[i][j]);
+#pragma unroll
+                    for (int i = 0; i < kRPT; ++i) acc[i][j] = fmaf(av[i].w, w.w, acc[i][j]);
                 }
             }
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
+            for (int i = 0; i < kRPT; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int n = nn + j * ng;
@@ -577,24 +582,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_train3(Net net, T3Layout tl, co
         }
         // grad act[r][k] = sum_n dz[r][n] W[n][k], through leaky'(z_{l-1}) (2x4 tiles)
         const float* W = kWG ? params + net.woff[l] : sm + tl.w[l];
-        for (int t = tid; t < (kRows / 2) * kg; t += kThreads) {
-            const int r0 = (t / kg) * 2, k0 = (t % kg) * 4;
-            float acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+        for (int t = tid; t < (kRows / kRPT) * kg; t += kThreads) {
+            const int r0 = (t / kg) * kRPT, k0 = (t % kg) * 4;
+            float acc[kRPT][4] = {};
             for (int n = 0; n < N; ++n) {
                 const float4 w = *reinterpret_cast<const float4*>(W + n * S + k0);
-                const float d0 = dz[r0 * N + n], d1 = dz[(r0 + 1) * N + n];
-                acc[0][0] = fmaf(d0, w.x, acc[0][0]);
-                acc[0][1] = fmaf(d0, w.y, acc[0][1]);
-                acc[0][2] = fmaf(d0, w.z, acc[0][2]);
-                acc[0][3] = fmaf(d0, w.w, acc[0][3]);
-                acc[1][0] = fmaf(d1, w.x, acc[1][0]);
-                acc[1][1] = fmaf(d1, w.y, acc[1][1]);
-                acc[1][2] = fmaf(d1, w.z, acc[1][2]);
-                acc[1][3] = fmaf(d1, w.w, acc[1][3]);
+#pragma unroll
+                for (int i = 0; i < kRPT; ++i) {
+                    const float d = dz[(r0 + i) * N + n];
+                    acc[i][0] = fmaf(d, w.x, acc[i][0]);
+                    acc[i][1] = fmaf(d, w.y, acc[i][1]);
+                    acc[i][2] = fmaf(d, w.z, acc[i][2]);
+                    acc[i][3] = fmaf(d, w.w, acc[i][3]);
+                }
             }
             if (l > 0) {
 #pragma unroll
-                for (int i = 0; i < 2; ++i)
+                for (int i = 0; i < kRPT; ++i)
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         float v = acc[i][j];
@@ -603,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_train3(Net net, T3Layout tl, co
                     }
             } else {
 #pragma unroll
-                for (int i = 0; i < 2; ++i)
+                for (int i = 0; i < kRPT; ++i)
                     if (r0 + i < nr)
                         *reinterpret_cast<float4*>(dact0g + (r0g + r0 + i) * Ki + k0) =
                             make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
