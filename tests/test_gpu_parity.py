@@ -828,6 +828,22 @@ class TestClusters:
         assert st[0] == used and st[1] == used + 2 * b + used2
         assert st[2] == used + 2 * b + used2 + 2 * b and st[3] == (-1 if pend2 is None else pend2)
 
+    def test_sharded_cluster_targets_equal_whole_batch(self, rooms):
+        """Data-parallel shards of a cluster-mode batch: every rank draws the global
+        picks and keeps its rows -- concatenated, they equal the unsharded targets."""
+        from paper_2506_05930_b200.training import BatchBuffers, gen_batch_device
+        s, cs = rooms
+        whole = BatchBuffers(1024, 1024, cs.m, DEV, 1)
+        gen_batch_device(s, s.camera, whole, 0, 4, 0, 0, 1, clusters=cs)
+        b = int(whole.n_rows.item())
+        parts = []
+        for sh in range(3):
+            bufs = BatchBuffers(1024, 1024, cs.m, DEV, 3)
+            gen_batch_device(s, s.camera, bufs, 0, 4, 0, sh, 3, clusters=cs)
+            lo, hi = b * sh // 3, b * (sh + 1) // 3
+            parts.append(bufs.tgt[:hi - lo].cpu().numpy())
+        np.testing.assert_array_equal(np.concatenate(parts), whole.tgt[:b].cpu().numpy())
+
     def test_cluster_train_frame_first_step(self, rooms):
         """A cluster-mode cache trains on cluster targets: first-step loss equals the
         oracle's on the oracle's batch (C-config batch scaled down)."""
