@@ -971,12 +971,17 @@ constexpr int kNdiThreads = 128;
 __global__ void __launch_bounds__(kNdiThreads) k_ndi32(WArgs a, nvc_scene sc) {
     __shared__ uint32_t s_vis[kNdiThreads * 17];
     __shared__ float s_fac[kNdiThreads * 33];
+    __shared__ double s_le[32 * 3];                    // emitter radiance, staged once per block
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = p < a.P;
     uint32_t* my = s_vis + threadIdx.x * 17;
     float* mf = s_fac + threadIdx.x * 33;
+    for (int i = threadIdx.x; i < 3 * a.K; i += kNdiThreads) s_le[i] = __ldg(sc.lt_radiance + i);
     uint32_t m = 0;
+    double al[3] = {0.0, 0.0, 0.0};
     if (live) {
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) al[ch] = __ldg(a.albedo + 3 * p + ch);   // issued early, used last
         const uint4* vrow = reinterpret_cast<const uint4*>(a.vis16 + p * a.vstride);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -1007,6 +1012,7 @@ __global__ void __launch_bounds__(kNdiThreads) k_ndi32(WArgs a, nvc_scene sc) {
         for (int j = 0; j < 16; ++j)
             if (ks[j] >= 0) mf[ks[j]] = t[j];
     }
+    __syncthreads();   // s_le
     if (!live) return;
     double rgb[3] = {0.0, 0.0, 0.0};
     while (m) {
@@ -1016,10 +1022,10 @@ __global__ void __launch_bounds__(kNdiThreads) k_ndi32(WArgs a, nvc_scene sc) {
         const double vis = (double)__half2float(__ushort_as_half((unsigned short)((k & 1) ? (pair >> 16) : (pair & 0xffffu))));
         const double wk = __dmul_rn(vis, (double)mf[k]);
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) rgb[ch] = __dadd_rn(rgb[ch], __dmul_rn(wk, __ldg(sc.lt_radiance + 3 * k + ch)));
+        for (int ch = 0; ch < 3; ++ch) rgb[ch] = __dadd_rn(rgb[ch], __dmul_rn(wk, s_le[3 * k + ch]));
     }
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) a.rgb[3 * p + ch] = __ddiv_rn(__dmul_rn(rgb[ch], a.albedo[3 * p + ch]), 3.141592653589793);
+    for (int ch = 0; ch < 3; ++ch) a.rgb[3 * p + ch] = __ddiv_rn(__dmul_rn(rgb[ch], al[ch]), 3.141592653589793);
 }
 
 // generic K: forward reservoir over the nonzero lights (pixel-major visibilities)
