@@ -313,19 +313,19 @@ class Cache:
         feats, _ = encode(self.grid, self.table, pos)
         return mlp_forward(self.ws, self.bs, feats)[0]
 
-    def grads(self, pos, tgt, b_scale=None):
+    def grads(self, pos, tgt, b_scale=None, mask=None):
         feats, ctx = encode(self.grid, self.table, pos)
         out, zs, acts = mlp_forward(self.ws, self.bs, feats)
-        loss = l2_loss(out, tgt)
-        gw, gb, d_in = mlp_backward(self.ws, zs, acts, tgt, b_scale=b_scale)
+        loss = l2_loss(out, tgt, mask)
+        gw, gb, d_in = mlp_backward(self.ws, zs, acts, tgt, mask=mask, b_scale=b_scale)
         gg = grid_grad(self.grid, ctx, d_in, self.table.dtype)
         parts = [gg.reshape(-1)]
         for w, b in zip(gw, gb):
             parts += [w.reshape(-1), b]
         return loss, np.concatenate(parts)
 
-    def train_step(self, pos, tgt) -> float:
-        loss, g = self.grads(pos, tgt)
+    def train_step(self, pos, tgt, mask=None) -> float:
+        loss, g = self.grads(pos, tgt, mask=mask)
         p = self.flat()
         self.adam.step(p, g, lr_at(self.step))
         self.unflat(p)

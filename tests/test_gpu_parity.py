@@ -540,6 +540,22 @@ class TestTraining:
         assert loss == pytest.approx(float(g_train["c1_step0_loss"]), rel=1e-6)
         np.testing.assert_allclose(c.net_params.weights[0], g_train["c1_step0_w0"], atol=2e-6)
 
+    @pytest.mark.parametrize("kind", ["binary", "fractional"])
+    def test_masked_train_step_vs_oracle(self, pbox8, g_train, kind):
+        """train_step(positions, targets, mask): masked loss and gradients (mlp.py:143-168)
+        against the oracle on the C1 batch."""
+        pos, tgt = g_train["c1_pos"], g_train["c1_tgt"].astype(np.float32)
+        g = np.random.default_rng(8)
+        mask = (g.random(tgt.shape) < 0.7).astype(np.float32) if kind == "binary" else \
+            g.random(tgt.shape).astype(np.float32)
+        c = self._c1(pbox8)
+        oc = O.Cache(O.Grid(levels=8, features_per_level=2, table_size=1 << 14, aabb_min=pbox8.aabb_min,
+                            aabb_max=pbox8.aabb_max), 8, hidden=(64, 64), seed=0)
+        loss = c.train_step(pos, tgt, mask)
+        oloss = oc.train_step(pos, tgt, mask)
+        assert loss == pytest.approx(oloss, rel=1e-6)
+        np.testing.assert_allclose(c.net_params.weights[0], oc.ws[0], atol=2e-6)
+
     def test_loss_curve_vs_reference(self, pbox8, g_train):
         c = self._c1(pbox8)
         want = g_train["c1_loss_f32"]
