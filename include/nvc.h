@@ -28,7 +28,7 @@ extern "C" {
 
 #define NVC_MAX_LEVELS 32
 #define NVC_MAX_LAYERS 8
-#define NVC_ABI_VERSION 5
+#define NVC_ABI_VERSION 6
 
 typedef enum {
     NVC_OK = 0,
@@ -275,15 +275,18 @@ int nvc_visibility(const nvc_scene *sc, const double *x, const double *y, int64_
  * a uniform member -- numpy Generator.integers, exact including its rejection
  * loop and the bit generator's kept 32-bit half -- then the member's light point
  * from the same stream; tgt (rows of this shard, m) f32.  Clusters as device
- * int32 arrays c_off (m+1) and c_mem (c_off[m]) (clusters.ClusterSet.packed);
+ * int32 arrays c_off (m+1) and c_mem (c_off[m]) (clusters.ClusterSet.packed).
+ * The stream starts at 64-bit output `offset` with the bit generator's kept
+ * 32-bit half `kept_in` (-1: none) -- a used numpy Generator continues exactly;
  * ws: nvc_cluster_workspace_bytes(b_max, m); at nvc_cluster_state_offset the
  * call leaves int64 [m+2]: per cluster the first output of its random() draws,
  * then the stream's next 64-bit output and its kept 32-bit half (-1: none). */
 int64_t nvc_cluster_workspace_bytes(int64_t b_max, int32_t m);
 int64_t nvc_cluster_state_offset(int64_t b_max, int32_t m);
-int nvc_cluster_targets(const nvc_scene *sc, uint64_t key, const double *pos, const int64_t *n_rows,
-                        int64_t b_max, int32_t shard, int32_t n_shards, int32_t m, const int32_t *c_off,
-                        const int32_t *c_mem, float *tgt, void *ws, void *stream);
+int nvc_cluster_targets(const nvc_scene *sc, uint64_t key, uint64_t offset, int64_t kept_in,
+                        const double *pos, const int64_t *n_rows, int64_t b_max, int32_t shard,
+                        int32_t n_shards, int32_t m, const int32_t *c_off, const int32_t *c_mem,
+                        float *tgt, void *ws, void *stream);
 /* clustered_sample_batch (sampling.py:302-352): WRS over the m clamped cluster
  * visibilities vis (p, vis_stride) f32, then per cluster (ascending) a WRS over
  * its member lights with weights phat / p_src on the continuing stream (draws
@@ -319,9 +322,10 @@ int nvc_closest_hit(const nvc_scene *sc, const double *orig, const double *dir,
  * n_rows (device int64) receives b. */
 int64_t nvc_batch_workspace_bytes(int32_t n_world, int32_t n_screen);
 /* compute_visibility_targets (training.py:103-120, light mode) for given
- * positions (b,3): tgt (b,K) f32, light j / row i use draws j*2b+2i, +1. */
-int nvc_targets(const nvc_scene *sc, uint64_t key, const double *pos, int64_t b, float *tgt,
-                void *stream);
+ * positions (b,3): tgt (b,K) f32, light j / row i use draws
+ * offset + j*2b + 2i, +1 (offset: the stream's position when called). */
+int nvc_targets(const nvc_scene *sc, uint64_t key, uint64_t offset, const double *pos, int64_t b,
+                float *tgt, void *stream);
 int nvc_gen_train_batch(const nvc_scene *sc, const nvc_camera *cam, uint64_t key_world,
                         uint64_t key_screen, uint64_t key_targets, int32_t n_world,
                         int32_t n_screen, int32_t shard, int32_t n_shards,

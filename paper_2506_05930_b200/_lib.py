@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libnvc.so")
 
 MAX_LEVELS = 32
 MAX_LAYERS = 8
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 c_i32, c_i64, c_u64, c_f64, c_f32, c_vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
                                            ctypes.c_double, ctypes.c_float, ctypes.c_void_p)
@@ -103,8 +103,8 @@ _SIGS = {
     "nvc_visibility": (c_i32, [P(NvcScene), c_vp, c_vp, c_i64, c_vp, c_vp]),
     "nvc_cluster_workspace_bytes": (c_i64, [c_i64, c_i32]),
     "nvc_cluster_state_offset": (c_i64, [c_i64, c_i32]),
-    "nvc_cluster_targets": (c_i32, [P(NvcScene), c_u64, c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp,
-                                    c_vp, c_vp]),
+    "nvc_cluster_targets": (c_i32, [P(NvcScene), c_u64, c_u64, c_i64, c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp,
+                                    c_vp, c_vp, c_vp, c_vp]),
     "nvc_clustered_workspace_bytes": (c_i64, [c_i64, c_i32]),
     "nvc_clustered_state_offset": (c_i64, [c_i64, c_i32]),
     "nvc_clustered_select": (c_i32, [P(NvcScene), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp,
@@ -112,7 +112,7 @@ _SIGS = {
     "nvc_shade": (c_i32, [P(NvcScene), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "nvc_closest_hit": (c_i32, [P(NvcScene), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "nvc_batch_workspace_bytes": (c_i64, [c_i32, c_i32]),
-    "nvc_targets": (c_i32, [P(NvcScene), c_u64, c_vp, c_i64, c_vp, c_vp]),
+    "nvc_targets": (c_i32, [P(NvcScene), c_u64, c_u64, c_vp, c_i64, c_vp, c_vp]),
     "nvc_gen_train_batch": (c_i32, [P(NvcScene), P(NvcCamera), c_u64, c_u64, c_u64, c_i32, c_i32,
                                     c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
 }

@@ -923,7 +923,7 @@ __device__ uint32_t any_hit_packet(const nvc_scene& sc, const double o[3], const
 // compute_visibility_targets (light mode): row i, light j uses draws j*2b + 2i, +1.
 // One warp per row, lanes over lights (K <= 32 per pass): the warp's shadow rays
 // share an origin and fan out to neighbouring emitters -> packet traversal.
-__global__ void __launch_bounds__(128) k_targets(nvc_scene sc, uint64_t key, const double* __restrict__ pos,
+__global__ void __launch_bounds__(128) k_targets(nvc_scene sc, uint64_t key, uint64_t off, const double* __restrict__ pos,
                                                  const int64_t* __restrict__ n_rows, int64_t b_host, int shard,
                                                  int n_shards, int64_t cap, float* __restrict__ tgt) {
     __shared__ int32_t st_node[4][kStack];
@@ -943,7 +943,13 @@ __global__ void __launch_bounds__(128) k_targets(nvc_scene sc, uint64_t key, con
         double y[3] = {0.0, 0.0, 0.0};
         if (valid) {
             double u0, u1;
-            draw2(key, (uint64_t)(2 * b * j + 2 * i), u0, u1);
+            const uint64_t n = off + (uint64_t)(2 * b * j + 2 * i);   // draws off + 2bj + 2i, +1
+            if (off & 1) {
+                u0 = draw(key, n);
+                u1 = draw(key, n + 1);
+            } else {
+                draw2(key, n, u0, u1);
+            }
             light_point(sc, j, u0, u1, y);
         }
         // visibility_batch (geometry.py:233-247), per lane
@@ -1090,17 +1096,20 @@ constexpr int kPickThreads = 1024;
 // picks and flags any cluster where a draw would have been rejected; only then
 // does the exact sequential walk (k_cluster_picks) run, overwriting everything.
 __global__ void k_cluster_chain(const int64_t* __restrict__ n_rows, int32_t m, const int32_t* __restrict__ c_off,
-                                int64_t* __restrict__ uni_start, int64_t* __restrict__ draw_base,
-                                int64_t* __restrict__ kept_src, int32_t* __restrict__ flag) {
+                                uint64_t start, int64_t kept_in, int64_t* __restrict__ uni_start,
+                                int64_t* __restrict__ draw_base, int64_t* __restrict__ kept_src,
+                                int32_t* __restrict__ flag) {
     const int64_t b = *n_rows;
-    uint64_t next = 0;
-    int64_t kept = -1;   // output whose high half the bit generator keeps
+    uint64_t next = start;
+    // the half the bit generator keeps: -1 none, -2 the caller's value (kept_in),
+    // >= 0 the high half of that 64-bit output
+    int64_t kept = kept_in >= 0 ? -2 : -1;
     for (int j = 0; j < m; ++j) {
         const int32_t n = c_off[j + 1] - c_off[j];
         draw_base[j] = (int64_t)next;
         kept_src[j] = kept;
         if (n > 1 && b > 0) {
-            const int64_t fresh = b - (kept >= 0 ? 1 : 0);
+            const int64_t fresh = b - (kept != -1 ? 1 : 0);
             const uint64_t outs = (uint64_t)((fresh + 1) / 2);
             kept = (fresh & 1) ? (int64_t)(next + outs - 1) : -1;
             next += outs;
@@ -1109,7 +1118,8 @@ __global__ void k_cluster_chain(const int64_t* __restrict__ n_rows, int32_t m, c
         next += 2 * (uint64_t)b;
     }
     uni_start[m] = (int64_t)next;
-    uni_start[m + 1] = kept;          // resolved to the half's value by k_cluster_draws
+    uni_start[m + 1] = kept == -2 ? kept_in : kept;   // an output index is resolved by k_cluster_draws
+    if (kept >= 0) uni_start[m + 1] = -3 - kept;       // (encoded: index i -> -3 - i)
     *flag = 0;
 }
 
@@ -1119,22 +1129,22 @@ __global__ void __launch_bounds__(256) k_cluster_draws(uint64_t key, const int64
                                                        const int64_t* __restrict__ draw_base,
                                                        const int64_t* __restrict__ kept_src,
                                                        int32_t* __restrict__ picks, int64_t* __restrict__ uni_start,
-                                                       int32_t* __restrict__ flag) {
+                                                       int32_t* __restrict__ flag, int64_t kept_in) {
     const int64_t b = *n_rows;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y;
-    if (i == 0 && j == 0 && uni_start[m + 1] >= 0)
-        uni_start[m + 1] = (int64_t)(philox_out(key, (uint64_t)uni_start[m + 1]) >> 32);
+    if (i == 0 && j == 0 && uni_start[m + 1] <= -3)
+        uni_start[m + 1] = (int64_t)(philox_out(key, (uint64_t)(-3 - uni_start[m + 1])) >> 32);
     if (i >= b) return;
     const int32_t lo = c_off[j], n = c_off[j + 1] - lo;
     if (n == 1) {
         picks[i * m + j] = c_mem[lo];
         return;
     }
-    const int has = kept_src[j] >= 0 ? 1 : 0;
+    const int has = kept_src[j] != -1 ? 1 : 0;
     uint32_t d;
     if (has && i == 0) {
-        d = (uint32_t)(philox_out(key, (uint64_t)kept_src[j]) >> 32);
+        d = kept_src[j] == -2 ? (uint32_t)kept_in : (uint32_t)(philox_out(key, (uint64_t)kept_src[j]) >> 32);
     } else {
         const int64_t k = i - has;
         const uint64_t w = philox_out(key, (uint64_t)draw_base[j] + (uint64_t)(k >> 1));
@@ -1151,7 +1161,8 @@ __global__ void __launch_bounds__(kPickThreads) k_cluster_picks(uint64_t key, co
                                                                  const int32_t* __restrict__ c_mem,
                                                                  int32_t* __restrict__ picks,
                                                                  int64_t* __restrict__ uni_start,
-                                                                 const int32_t* __restrict__ flag) {
+                                                                 const int32_t* __restrict__ flag, uint64_t start,
+                                                                 int64_t kept_in) {
     if (flag && *flag == 0) return;   // the fast path had no rejection: nothing to redo
     __shared__ uint64_t s_next;        // next fresh 64-bit output
     __shared__ uint32_t s_kept;        // kept high half (valid if s_has)
@@ -1162,9 +1173,9 @@ __global__ void __launch_bounds__(kPickThreads) k_cluster_picks(uint64_t key, co
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int64_t b = *n_rows;
     if (tid == 0) {
-        s_next = 0;
-        s_has = 0;
-        s_kept = 0;
+        s_next = start;
+        s_has = kept_in >= 0 ? 1 : 0;
+        s_kept = kept_in >= 0 ? (uint32_t)kept_in : 0u;
     }
     __syncthreads();
     for (int j = 0; j < m; ++j) {
@@ -1395,7 +1406,7 @@ int nvc_gen_train_batch(const nvc_scene* sc, const nvc_camera* cam, uint64_t key
             dim3 g(grid1(cap, 128), sc->n_lights);
             k_targets_sorted<<<g, 128, 0, s>>>(*sc, key_targets, pos, n_rows, 0, shard, n_shards, order, tgt);
         } else {
-            k_targets<<<grid1(cap, 4), 128, 0, s>>>(*sc, key_targets, pos, n_rows, 0, shard, n_shards, cap, tgt);
+            k_targets<<<grid1(cap, 4), 128, 0, s>>>(*sc, key_targets, 0, pos, n_rows, 0, shard, n_shards, cap, tgt);
         }
     }
     return check_launch("k_targets");
@@ -1409,9 +1420,9 @@ int64_t nvc_cluster_state_offset(int64_t b_max, int32_t m) {   // int64 [m+2]: u
     return ((b_max * m * 4 + 255) / 256) * 256;
 }
 
-int nvc_cluster_targets(const nvc_scene* sc, uint64_t key, const double* pos, const int64_t* n_rows, int64_t b_max,
-                        int32_t shard, int32_t n_shards, int32_t m, const int32_t* c_off, const int32_t* c_mem,
-                        float* tgt, void* ws, void* stream) {
+int nvc_cluster_targets(const nvc_scene* sc, uint64_t key, uint64_t offset, int64_t kept_in, const double* pos,
+                        const int64_t* n_rows, int64_t b_max, int32_t shard, int32_t n_shards, int32_t m,
+                        const int32_t* c_off, const int32_t* c_mem, float* tgt, void* ws, void* stream) {
     NVC_REQUIRE(sc && pos && n_rows && c_off && c_mem && tgt && ws, "nvc_cluster_targets: null argument");
     NVC_REQUIRE(m >= 1 && n_shards >= 1 && shard >= 0 && shard < n_shards, "nvc_cluster_targets: bad m/shard");
     if (b_max <= 0) return NVC_OK;
@@ -1421,11 +1432,11 @@ int nvc_cluster_targets(const nvc_scene* sc, uint64_t key, const double* pos, co
     int64_t* base = uni + (m + 2);
     int64_t* kept = base + m;
     int32_t* flag = (int32_t*)(kept + m);
-    k_cluster_chain<<<1, 1, 0, s>>>(n_rows, m, c_off, uni, base, kept, flag);
+    k_cluster_chain<<<1, 1, 0, s>>>(n_rows, m, c_off, offset, kept_in, uni, base, kept, flag);
     dim3 gd(grid1(b_max, 256), m);
-    k_cluster_draws<<<gd, 256, 0, s>>>(key, n_rows, m, c_off, c_mem, base, kept, picks, uni, flag);
+    k_cluster_draws<<<gd, 256, 0, s>>>(key, n_rows, m, c_off, c_mem, base, kept, picks, uni, flag, kept_in);
     k_cluster_picks<<<1, kPickThreads, 0, s>>>(key, n_rows, m, c_off, c_mem, picks, uni,
-                                               getenv("NVC_CLUSTER_EXACT_WALK") ? nullptr : flag);
+                                               getenv("NVC_CLUSTER_EXACT_WALK") ? nullptr : flag, offset, kept_in);
     int rc = check_launch("k_cluster_picks");
     if (rc) return rc;
     const int64_t cap = b_max / n_shards + 1;
@@ -1434,10 +1445,11 @@ int nvc_cluster_targets(const nvc_scene* sc, uint64_t key, const double* pos, co
     return check_launch("k_cluster_tgt");
 }
 
-int nvc_targets(const nvc_scene* sc, uint64_t key, const double* pos, int64_t b, float* tgt, void* stream) {
+int nvc_targets(const nvc_scene* sc, uint64_t key, uint64_t offset, const double* pos, int64_t b, float* tgt,
+                void* stream) {
     NVC_REQUIRE(sc && pos && tgt, "nvc_targets: null argument");
     if (b <= 0) return NVC_OK;
-    k_targets<<<grid1(b, 4), 128, 0, (cudaStream_t)stream>>>(*sc, key, pos, nullptr, b, 0, 1, b, tgt);
+    k_targets<<<grid1(b, 4), 128, 0, (cudaStream_t)stream>>>(*sc, key, offset, pos, nullptr, b, 0, 1, b, tgt);
     return check_launch("k_targets");
 }
 

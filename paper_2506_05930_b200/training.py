@@ -76,15 +76,16 @@ def _cluster_tables(clusters, device):
     return cache[device]
 
 
-def _cluster_targets(ds, key, pos, n_rows, b_max, shard, n_shards, clusters, tgt, ws=None):
+def _cluster_targets(ds, key, pos, n_rows, b_max, shard, n_shards, clusters, tgt, ws=None, offset=0, kept=-1):
     """nvc_cluster_targets; returns the workspace (its state block: stream position after the call)."""
     import torch
     c_off, c_mem = _cluster_tables(clusters, pos.device)
     need = _lib.load().nvc_cluster_workspace_bytes(b_max, clusters.m)
     if ws is None or ws.numel() < need:
         ws = torch.empty(need, dtype=torch.uint8, device=pos.device)
-    _lib.call("nvc_cluster_targets", ds.struct, key, pos.data_ptr(), n_rows.data_ptr(), b_max, shard, n_shards,
-              clusters.m, c_off.data_ptr(), c_mem.data_ptr(), tgt.data_ptr(), ws.data_ptr(), _lib.stream_ptr())
+    _lib.call("nvc_cluster_targets", ds.struct, key, offset, kept, pos.data_ptr(), n_rows.data_ptr(), b_max, shard,
+              n_shards, clusters.m, c_off.data_ptr(), c_mem.data_ptr(), tgt.data_ptr(), ws.data_ptr(),
+              _lib.stream_ptr())
     return ws
 
 
@@ -146,20 +147,22 @@ def compute_visibility_targets(positions, scene, rng, clusters=None) -> np.ndarr
     ds = device_scene(scene)
     pos = torch.from_numpy(np.ascontiguousarray(positions, dtype=np.float64)).to(ds.device)
     b = pos.shape[0]
+    key, start = rngmod.position(rng)          # any stream position, like the reference
     if clusters is not None:
+        kept = -1
         if isinstance(rng, np.random.Generator) and rng.bit_generator.state.get("has_uint32"):
-            raise ValueError("training-batch streams must be fresh (as train_frame creates them)")
+            kept = int(rng.bit_generator.state["uinteger"])
         tgt = torch.zeros((max(b, 1), clusters.m), dtype=torch.float32, device=ds.device)
         n_rows = torch.tensor([b], dtype=torch.int64, device=ds.device)
-        ws = _cluster_targets(ds, _fresh_key(rng), pos, n_rows, max(b, 1), 0, 1, clusters, tgt)
+        ws = _cluster_targets(ds, key, pos, n_rows, max(b, 1), 0, 1, clusters, tgt, offset=start, kept=kept)
         off = _lib.load().nvc_cluster_state_offset(max(b, 1), clusters.m) // 8
         state = ws.view(torch.int64)[off + clusters.m: off + clusters.m + 2].cpu().numpy()
-        rngmod.advance(rng, int(state[0]))
+        rngmod.advance(rng, int(state[0]) - start)
         if isinstance(rng, np.random.Generator):
             rngmod.set_kept32(rng, None if state[1] < 0 else int(state[1]))
         return tgt[:b].cpu().numpy()
     tgt = torch.empty((b, ds.n_lights), dtype=torch.float32, device=ds.device)
-    _lib.call("nvc_targets", ds.struct, _fresh_key(rng), pos.data_ptr(), b, tgt.data_ptr(), _lib.stream_ptr())
+    _lib.call("nvc_targets", ds.struct, key, start, pos.data_ptr(), b, tgt.data_ptr(), _lib.stream_ptr())
     rngmod.advance(rng, 2 * b * ds.n_lights)
     return tgt.cpu().numpy()
 

@@ -810,6 +810,35 @@ class TestClusters:
         np.testing.assert_array_equal(g.integers(0, 7, size=9), h.integers(0, 7, size=9))
         np.testing.assert_array_equal(g.random(5), h.random(5))
 
+    def test_targets_continue_a_used_stream(self, rooms, g_scenes):
+        """compute_visibility_targets on a Generator that has already drawn -- at an odd
+        position and holding a kept 32-bit half -- matches the same numpy calls
+        made in the reference's order, and leaves the stream where they do."""
+        s, cs = rooms
+        sa = O.SceneArrays.from_golden(g_scenes, "rooms128_")
+        pos = np.random.default_rng(2).uniform(s.aabb_min, s.aabb_max, (301, 3))
+        g, h = R.stream(7, "used"), R.stream(7, "used")
+        for x in (g, h):
+            x.random(5)
+            x.integers(0, 3, size=1)               # leaves a kept half in the bit generator
+        tg = compute_visibility_targets(pos, s, g, clusters=cs)
+        want = np.empty_like(tg)
+        for j, mem in enumerate(cs.members):       # training.py:121-128 with the same generator
+            ids = mem[h.integers(0, mem.size, size=pos.shape[0])]
+            want[:, j] = sa.visibility(pos, sa.light_points(ids, h.random((pos.shape[0], 2))))
+        np.testing.assert_array_equal(tg, want)
+        np.testing.assert_array_equal(g.integers(0, 11, size=7), h.integers(0, 11, size=7))
+        np.testing.assert_array_equal(g.random(3), h.random(3))
+        # light mode from an odd position
+        g.random(1)
+        h.random(1)
+        tl = compute_visibility_targets(pos, s, g)
+        wl = np.empty_like(tl)
+        for j in range(s.lt_kind.shape[0]):
+            wl[:, j] = sa.visibility(pos, sa.light_points(np.full(pos.shape[0], j), h.random((pos.shape[0], 2))))
+        np.testing.assert_array_equal(tl, wl)
+        np.testing.assert_array_equal(g.random(3), h.random(3))
+
     def test_rejection_loop_and_kept_half(self, rooms, g_scenes):
         """A 1,431,655,766-member cluster (2^32 mod n = n - 2) rejects a third of its
         32-bit draws, running the multi-window path; a 3-member cluster follows."""
@@ -826,7 +855,7 @@ class TestClusters:
         tgt = torch.zeros((b + 1, 2), dtype=torch.float32, device=DEV)
         ws = torch.zeros(_lib.load().nvc_cluster_workspace_bytes(b, 2), dtype=torch.uint8, device=DEV)
         key = R.stream_key(4, "reject")
-        _lib.call("nvc_cluster_targets", ds.struct, key, pos.data_ptr(), n_rows.data_ptr(), b, 0, 1, 2,
+        _lib.call("nvc_cluster_targets", ds.struct, key, 0, -1, pos.data_ptr(), n_rows.data_ptr(), b, 0, 1, 2,
                   c_off.data_ptr(), c_mem.data_ptr(), tgt.data_ptr(), ws.data_ptr(), _lib.stream_ptr())
         del c_mem
         got = tgt[:b].cpu().numpy()

@@ -140,3 +140,90 @@ def test_cluster_weights_ignore_radiance(two_cluster_scene):
     ids, _, _ = clustered_sample_batch(tiled_ctx(s, (0.0, 0.0, 1.0), n), FixedCache([0.5, 0.5], "clusters"), cs,
                                        R.stream(65))
     assert np.isin(ids, cs.members[0]).mean() == pytest.approx(0.5, abs=0.01)
+
+
+# ---------------------------------------------------------------------------
+# behaviour of training targets, training and shading (reference
+# tests/test_training.py, test_render.py, restated on the GPU path)
+# ---------------------------------------------------------------------------
+def penumbra_scene():
+    plate = quad((-0.5, 1, -0.5), (0.5, 1, -0.5), (0.5, 1, 0.5), (-0.5, 1, 0.5))
+    return scene_from_dict({"camera": {"position": [0, 1.6, 3.2], "look_at": [0, 0, 0], "up": [0, 1, 0],
+                                       "fov_deg": 55.0, "width": 96, "height": 54},
+                            "materials": [{"albedo": [0.7, 0.7, 0.7]}, {"albedo": [0.5, 0.3, 0.3]}],
+                            "meshes": [{"material": 0, "triangles": FLOOR}, {"material": 1, "triangles": plate}],
+                            "lights": [down_light(0.0, 0.0, 2.0, 0.8)]})
+
+
+def single_light_scene():
+    return make_scene([down_light(0.0, 0.0, 2.0, 1.0)], [{"material": 0, "triangles": FLOOR}])
+
+
+def test_targets_unoccluded_occluded_binary(two_cluster_scene):
+    from paper_2506_05930_b200.training import compute_visibility_targets, gen_world_samples
+    rng = R.stream(8)
+    pts = np.column_stack([rng.uniform(-3, 3, 200), np.zeros(200), rng.uniform(-3, 3, 200)])
+    np.testing.assert_array_equal(compute_visibility_targets(pts, single_light_scene(), rng), 1.0)
+    under = np.zeros((200, 3))                       # under the plate: umbra
+    np.testing.assert_array_equal(compute_visibility_targets(under, penumbra_scene(), R.stream(9)), 0.0)
+    s8 = scene_from_dict(boxes_scene(8))
+    t = compute_visibility_targets(gen_world_samples(s8, 300, R.stream(10)), s8, R.stream(11))
+    assert set(np.unique(t)) <= {0.0, 1.0} and 0.0 < t.mean() < 1.0
+    cs = kmeans_cluster(two_cluster_scene.lights, 2, R.stream(13))
+    tc = compute_visibility_targets(gen_world_samples(two_cluster_scene, 64, R.stream(14)), two_cluster_scene,
+                                    R.stream(15), clusters=cs)
+    assert tc.shape == (64, 2) and set(np.unique(tc)) <= {0.0, 1.0}
+
+
+def test_loss_decreases_frame_to_frame():
+    from paper_2506_05930_b200 import TrainFrameConfig, make_cache, train_frame
+    s8 = scene_from_dict(boxes_scene(8))
+    wins = 0
+    for seed in range(20):
+        c = make_cache(s8, "lights", seed=seed)
+        cfg = TrainFrameConfig(n_world=256, n_screen=256, seed=seed)
+        l0 = train_frame(s8, s8.camera, c, cfg, frame=0)
+        wins += train_frame(s8, s8.camera, c, cfg, frame=1) <= l0
+    assert wins >= 18
+
+
+def test_converged_prediction_tracks_visibility():
+    """512 online frames on the penumbra scene: the umbra predicts ~0, open floor ~1."""
+    from paper_2506_05930_b200 import TrainFrameConfig, make_cache, train_frame
+    s = penumbra_scene()
+    c = make_cache(s, "lights", seed=7)
+    cfg = TrainFrameConfig(n_world=512, n_screen=512, seed=7)
+    for f in range(512):
+        train_frame(s, s.camera, c, cfg, frame=f)
+    pred = c.infer(np.array([[0.0, 0.0, 0.0], [3.0, 0.0, 3.0], [-3.0, 0.0, 2.5]]))[:, 0]
+    assert pred[0] < 0.15 and pred[1] > 0.85 and pred[2] > 0.85
+
+
+def test_shading_closed_forms():
+    from paper_2506_05930_b200 import ShadingPoint, shade_pixel
+    # occluded sample is black
+    sp = ShadingPoint(np.zeros(3), np.array([0.0, 1.0, 0.0]), np.array([0.7, 0.7, 0.7]))
+    np.testing.assert_array_equal(shade_pixel(sp, (0, np.array([0.0, 2.0, 0.0]), 1.0), penumbra_scene()), 0.0)
+    # point light: albedo/pi * I * cos / d^2
+    s = make_scene([{"type": "point", "position": [0.0, 2.0, 1.0], "intensity": [5.0, 4.0, 3.0]}],
+                   [{"material": 0, "triangles": FLOOR}])
+    rgb = shade_pixel(sp, (0, np.array([0.0, 2.0, 1.0]), 1.0), s)
+    want = sp.albedo / np.pi * np.array([5.0, 4.0, 3.0]) * (2.0 / np.sqrt(5.0)) / 5.0
+    np.testing.assert_allclose(rgb, want, rtol=1e-12)
+
+
+def test_unoccluded_single_light_estimate_matches_unshadowed_integral():
+    """One-light area sampling through shade_batch converges to the analytic
+    unshadowed radiance (the factor's closed-form polygon integral)."""
+    s = single_light_scene()
+    n = 400_000
+    ctx = tiled_ctx(s, (0.5, 0.0, 0.5), n)
+    u = np.random.default_rng(3).random((n, 2))
+    sa = O.SceneArrays(s.triangles_v0, s.triangles_v1, s.triangles_v2, s.tri_material, s.tri_light, s.lt_kind,
+                       s.lt_verts, s.lt_normal, s.lt_radiance, s.mat_albedo, np.zeros(12), lt_area=s.lt_area)
+    pts = sa.light_points(np.zeros(n, np.int64), u)
+    est = shade_batch(s, ctx.positions, np.tile([0.0, 1.0, 0.0], (n, 1)), np.tile([0.7, 0.7, 0.7], (n, 1)),
+                      np.zeros(n, np.int64), pts, np.ones(n)) @ LUMA
+    want = ctx.lum_matrix()[0, 0]                       # factor * albedo.(LUMA*L)/pi
+    se = est.std() / np.sqrt(n)
+    assert abs(est.mean() - want) < 4 * se + 1e-3 * want
