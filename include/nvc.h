@@ -327,10 +327,13 @@ int64_t nvc_batch_workspace_bytes(int32_t n_world, int32_t n_screen);
 int nvc_targets(const nvc_scene *sc, uint64_t key, uint64_t offset, const double *pos, int64_t b,
                 float *tgt, void *stream);
 int nvc_gen_train_batch(const nvc_scene *sc, const nvc_camera *cam, uint64_t key_world,
-                        uint64_t key_screen, uint64_t key_targets, int32_t n_world,
-                        int32_t n_screen, int32_t shard, int32_t n_shards,
-                        double *pos, float *tgt, int64_t *n_rows, void *workspace,
-                        void *stream);
+                        uint64_t key_screen, uint64_t key_targets, uint64_t off_world,
+                        uint64_t off_screen, int32_t n_world, int32_t n_screen, int32_t shard,
+                        int32_t n_shards, double *pos, float *tgt, int64_t *n_rows,
+                        void *workspace, void *stream);
+/* (off_world / off_screen: the world / screen streams' positions -- 0 for the
+ * fresh per-frame streams; the screen stream's position after the call is the
+ * int64 at byte 16 of the workspace) */
 
 #ifdef __cplusplus
 }

@@ -113,7 +113,7 @@ _SIGS = {
     "nvc_closest_hit": (c_i32, [P(NvcScene), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "nvc_batch_workspace_bytes": (c_i64, [c_i32, c_i32]),
     "nvc_targets": (c_i32, [P(NvcScene), c_u64, c_u64, c_vp, c_i64, c_vp, c_vp]),
-    "nvc_gen_train_batch": (c_i32, [P(NvcScene), P(NvcCamera), c_u64, c_u64, c_u64, c_i32, c_i32,
+    "nvc_gen_train_batch": (c_i32, [P(NvcScene), P(NvcCamera), c_u64, c_u64, c_u64, c_u64, c_u64, c_i32, c_i32,
                                     c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
 }
 EXPORTS = tuple(_SIGS)

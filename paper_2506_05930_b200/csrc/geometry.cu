@@ -778,11 +778,11 @@ __device__ __forceinline__ BatchWs batch_ws(void* ws, int n_screen) {
 }
 
 // gen_world_samples: pos[i][c] = lo_c + (hi_c - lo_c) * u(3i + c)
-__global__ void k_world(nvc_scene sc, uint64_t key, int n, double* __restrict__ pos) {
+__global__ void k_world(nvc_scene sc, uint64_t key, uint64_t base, int n, double* __restrict__ pos) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 3 * n) return;
     const int c = i % 3;
-    pos[i] = sc.aabb_min[c] + (sc.aabb_max[c] - sc.aabb_min[c]) * draw(key, (uint64_t)i);
+    pos[i] = sc.aabb_min[c] + (sc.aabb_max[c] - sc.aabb_min[c]) * draw(key, base + (uint64_t)i);
 }
 
 // screen round with `want` rays starting at draw offset `off`
@@ -799,11 +799,11 @@ __device__ __forceinline__ void screen_ray(const nvc_scene& sc, const nvc_camera
         for (int a = 0; a < 3; ++a) hp[3 * i + a] = cam.pos[a] + t * d[a];
 }
 
-__global__ void k_screen_round0(nvc_scene sc, nvc_camera cam, uint64_t key, int n, void* ws) {
+__global__ void k_screen_round0(nvc_scene sc, nvc_camera cam, uint64_t key, uint64_t base, int n, void* ws) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     BatchWs w = batch_ws(ws, n);
-    screen_ray(sc, cam, key, 0, n, i, w.flag, w.hp);
+    screen_ray(sc, cam, key, (int64_t)base, n, i, w.flag, w.hp);
 }
 
 // block-wide exclusive scan of 0/1 flags (1024 threads)
@@ -833,13 +833,14 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int* total) {
 
 // one block: order-preserving compaction of round 0, then rounds 1..8 in-block
 __global__ void __launch_bounds__(1024) k_screen_finish(nvc_scene sc, nvc_camera cam, uint64_t key,
-                                                        int n_world, int n, double* __restrict__ pos,
-                                                        int64_t* __restrict__ n_rows, void* ws) {
+                                                        uint64_t base, int n_world, int n,
+                                                        double* __restrict__ pos, int64_t* __restrict__ n_rows,
+                                                        void* ws) {
     __shared__ int s_warp[32];
     __shared__ int s_total;
     BatchWs w = batch_ws(ws, n);
     double* out = pos + 3 * (int64_t)n_world;
-    int64_t count = 0, want = n, off = 0;
+    int64_t count = 0, want = n, off = (int64_t)base;
     for (int round = 0; round < 9 && want > 0; ++round) {
         if (round > 0) {
             for (int64_t i = threadIdx.x; i < want; i += blockDim.x) screen_ray(sc, cam, key, off, want, i, w.flag, w.hp);
@@ -862,7 +863,10 @@ __global__ void __launch_bounds__(1024) k_screen_finish(nvc_scene sc, nvc_camera
         want -= hits;
         __syncthreads();
     }
-    if (threadIdx.x == 0) *n_rows = n_world + count;
+    if (threadIdx.x == 0) {
+        *n_rows = n_world + count;
+        w.counters[2] = off;   // the screen stream's position after the call
+    }
 }
 
 // Warp-packet any-hit: the 32 lanes walk one shared DFS stack (node, lane
@@ -1380,16 +1384,17 @@ int64_t nvc_batch_workspace_bytes(int32_t n_world, int32_t n_screen) {
 }
 
 int nvc_gen_train_batch(const nvc_scene* sc, const nvc_camera* cam, uint64_t key_world, uint64_t key_screen,
-                        uint64_t key_targets, int32_t n_world, int32_t n_screen, int32_t shard,
-                        int32_t n_shards, double* pos, float* tgt, int64_t* n_rows, void* ws, void* stream) {
+                        uint64_t key_targets, uint64_t off_world, uint64_t off_screen, int32_t n_world,
+                        int32_t n_screen, int32_t shard, int32_t n_shards, double* pos, float* tgt, int64_t* n_rows,
+                        void* ws, void* stream) {
     NVC_REQUIRE(sc && cam && pos && n_rows && ws, "nvc_gen_train_batch: null argument");
     NVC_REQUIRE(n_world >= 0 && n_screen >= 0 && n_shards >= 1 && shard >= 0 && shard < n_shards,
                 "nvc_gen_train_batch: bad counts/shard");
     cudaStream_t s = (cudaStream_t)stream;
-    if (n_world > 0) k_world<<<grid1(3 * (int64_t)n_world, 256), 256, 0, s>>>(*sc, key_world, n_world, pos);
+    if (n_world > 0) k_world<<<grid1(3 * (int64_t)n_world, 256), 256, 0, s>>>(*sc, key_world, off_world, n_world, pos);
     if (n_screen > 0) {
-        k_screen_round0<<<grid1(n_screen, 64), 64, 0, s>>>(*sc, *cam, key_screen, n_screen, ws);
-        k_screen_finish<<<1, 1024, 0, s>>>(*sc, *cam, key_screen, n_world, n_screen, pos, n_rows, ws);
+        k_screen_round0<<<grid1(n_screen, 64), 64, 0, s>>>(*sc, *cam, key_screen, off_screen, n_screen, ws);
+        k_screen_finish<<<1, 1024, 0, s>>>(*sc, *cam, key_screen, off_screen, n_world, n_screen, pos, n_rows, ws);
     } else {
         k_set_rows<<<1, 1, 0, s>>>(n_rows, n_world);
     }

@@ -44,13 +44,6 @@ class TrainFrameConfig:
         return cls(**kw)
 
 
-def _fresh_key(g) -> int:
-    key, off = rngmod.position(g)
-    if off != 0:
-        raise ValueError("training-batch streams must be fresh (as train_frame creates them)")
-    return key
-
-
 class BatchBuffers:
     """Device buffers for one training batch (reused across frames)."""
 
@@ -98,7 +91,7 @@ def gen_batch_device(scene, camera, bufs: BatchBuffers, seed: int, frame: int, s
     key = (seed, frame, step)
     light_tgt = targets and clusters is None
     _lib.call("nvc_gen_train_batch", ds.struct, cam, rngmod.stream_key(*key, rngmod.WORLD_SAMPLES),
-              rngmod.stream_key(*key, rngmod.SCREEN_SAMPLES), rngmod.stream_key(*key, rngmod.TARGETS),
+              rngmod.stream_key(*key, rngmod.SCREEN_SAMPLES), rngmod.stream_key(*key, rngmod.TARGETS), 0, 0,
               bufs.n_world, bufs.n_screen, shard, n_shards, bufs.pos.data_ptr(),
               bufs.tgt.data_ptr() if light_tgt else None, bufs.n_rows.data_ptr(), bufs.ws.data_ptr(),
               _lib.stream_ptr())
@@ -119,7 +112,8 @@ def gen_world_samples(scene, n: int, rng) -> np.ndarray:
     pos = torch.zeros((n, 3), dtype=torch.float64, device=ds.device)
     nr = torch.zeros(1, dtype=torch.int64, device=ds.device)
     ws = torch.zeros(_lib.load().nvc_batch_workspace_bytes(n, 0), dtype=torch.uint8, device=ds.device)
-    _lib.call("nvc_gen_train_batch", ds.struct, camera_struct(scene.camera), _fresh_key(rng), 0, 0, n, 0, 0, 1,
+    key, off = rngmod.position(rng)            # any stream position: uniform((n,3)) draws off + 3i + c
+    _lib.call("nvc_gen_train_batch", ds.struct, camera_struct(scene.camera), key, 0, 0, off, 0, n, 0, 0, 1,
               pos.data_ptr(), None, nr.data_ptr(), ws.data_ptr(), _lib.stream_ptr())
     rngmod.advance(rng, 3 * n)
     return pos.cpu().numpy()
@@ -133,9 +127,12 @@ def gen_screen_samples(scene, camera, n: int, rng) -> np.ndarray:
         return np.zeros((0, 3))
     ds = device_scene(scene)
     bufs = BatchBuffers(0, n, ds.n_lights, ds.device)
-    _lib.call("nvc_gen_train_batch", ds.struct, camera_struct(camera), 0, _fresh_key(rng), 0, 0, n, 0, 1,
+    key, off = rngmod.position(rng)            # any stream position; rounds draw sx then sy from there
+    _lib.call("nvc_gen_train_batch", ds.struct, camera_struct(camera), 0, key, 0, 0, off, 0, n, 0, 1,
               bufs.pos.data_ptr(), None, bufs.n_rows.data_ptr(), bufs.ws.data_ptr(), _lib.stream_ptr())
     b = int(bufs.n_rows.item())
+    end = int(bufs.ws[16:24].view(torch.int64).item())
+    rngmod.advance(rng, end - off)             # leave the stream where the reference's rounds do
     return bufs.pos[:b].cpu().numpy()
 
 

@@ -191,6 +191,22 @@ class TestGeometry:
                  "lights": [{"type": "point", "position": [0, 2, 0], "intensity": [1, 1, 1]}]})
         assert gen_screen_samples(s, s.camera, 64, R.stream(5)).shape == (0, 3)
 
+    def test_world_and_screen_samples_continue_a_used_stream(self, boxes8, g_scenes):
+        """gen_world_samples / gen_screen_samples from a Generator that has already drawn:
+        same points as numpy's own calls from there, and the stream ends where they leave it."""
+        g, h = R.stream(3, "used-ws"), R.stream(3, "used-ws")
+        g.random(7)
+        h.random(7)
+        np.testing.assert_array_equal(gen_world_samples(boxes8, 101, g),
+                                      h.uniform(boxes8.aabb_min, boxes8.aabb_max, (101, 3)))
+        np.testing.assert_array_equal(g.random(2), h.random(2))
+        key, off = R.position(g)
+        sa = O.SceneArrays.from_golden(g_scenes, "boxes8_")
+        st = O.Stream(key=key, offset=off)
+        want = O.screen_samples(sa, 300, st)
+        np.testing.assert_array_equal(gen_screen_samples(boxes8, boxes8.camera, 300, g), want)
+        np.testing.assert_array_equal(g.random(3), O.uniform_at(key, st.offset + np.arange(3)))
+
     def test_c1_train_batch_bit_exact(self, pbox8, g_train):
         key = (0, 0, 0)
         world = gen_world_samples(pbox8, 4096, R.stream(*key, R.WORLD_SAMPLES))
