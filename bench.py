@@ -308,6 +308,8 @@ def gpu_arm(args) -> None:
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     with ClockSampler(local) as clocks:
+        if os.environ.get("NVC_PREQUEUE"):   # diagnostic: let the host run ahead of the GPU
+            torch.cuda._sleep(int(os.environ["NVC_PREQUEUE"]))
         start.record(stream)
         t_issue = time.perf_counter()
         for f in range(args.steps):
