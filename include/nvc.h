@@ -28,7 +28,7 @@ extern "C" {
 
 #define NVC_MAX_LEVELS 32
 #define NVC_MAX_LAYERS 8
-#define NVC_ABI_VERSION 6
+#define NVC_ABI_VERSION 7
 
 typedef enum {
     NVC_OK = 0,
@@ -153,6 +153,14 @@ int nvc_refresh_shadow(const nvc_model *m, void *stream);
  * idx_out (n, L, 8) int32 and w_out (n, L, 8) f64 are optional (may be NULL). */
 int nvc_encode(const nvc_model *m, const double *pos, int64_t n, float *feats,
                int32_t *idx_out, double *w_out, void *stream);
+
+/* grad_from_ctx (hashgrid.py:140-151) on nvc_encode's context: idx (b, L, 8)
+ * int32 and w (b, L, 8) f64, upstream (b, L*F) f32; adds into grad (L, T, F)
+ * f32 (zero it first for the reference's fresh table) every entry's
+ * contributions float(w * g) in (row, corner) order -- bit-identical to
+ * np.add.at. */
+int nvc_grid_scatter(int32_t levels, int32_t features, int64_t table_size, const int32_t *idx,
+                     const double *w, const float *upstream, int64_t b, float *grad, void *stream);
 
 /* ---- inference: cache.py:54-58 (VisibilityCache.infer) ---------------- */
 /* precision 0: f32 SIMT (parity: f32 table + f32 weights; workspace unused);
@@ -309,6 +317,12 @@ int nvc_clustered_select(const nvc_scene *sc, const float *vis, int64_t vis_stri
 int nvc_shade(const nvc_scene *sc, const double *pos, const double *nrm, const double *alb,
               const int64_t *ids, const double *pts, const double *big_w, int64_t n, double *rgb,
               void *stream);
+/* trace_rays (render.py:49-75) for camera rays through screen points
+ * sxy (n, 2) f64 (camera_rays_batch, scene.py:129-139): the hit attributes
+ * gen_screen_hits (training.py:67-94) keeps. */
+int nvc_primary_hits(const nvc_scene *sc, const nvc_camera *cam, const double *sxy, int64_t n,
+                     double *pos, double *nrm, double *alb, uint8_t *hit, int32_t *light_id,
+                     void *stream);
 /* intersect_scene_batch (geometry.py:191-207): t, original tri index (-1 miss). */
 int nvc_closest_hit(const nvc_scene *sc, const double *orig, const double *dir,
                     const double *t_min, const double *t_max, int64_t n,

@@ -23,7 +23,7 @@ from .sampling import (CLAMP_FLOOR, PixelCtx, Reservoir, ShadingPoint, clamp_vis
                        nls_weights_batch, wrs_select, wrs_select_batch)
 from .scene import Camera, Light, Material, Scene, SceneError, load_scene, scene_from_dict
 from .scenes import boxes_point_scene, boxes_scene, rooms_scene
-from .training import (TrainFrameConfig, compute_visibility_targets, gen_screen_samples,
+from .training import (TrainFrameConfig, compute_visibility_targets, gen_screen_hits, gen_screen_samples,
                        gen_world_samples, train_frame)
 
 __version__ = "0.1.0"
@@ -37,6 +37,6 @@ __all__ = [
     "neural_di_shade", "nls_sample", "nls_sample_batch", "nls_weights_batch", "wrs_select",
     "wrs_select_batch", "Camera", "Light", "Material", "Scene", "SceneError", "load_scene",
     "scene_from_dict", "boxes_scene", "boxes_point_scene", "rooms_scene", "TrainFrameConfig",
-    "compute_visibility_targets", "gen_screen_samples", "gen_world_samples", "train_frame",
+    "compute_visibility_targets", "gen_screen_hits", "gen_screen_samples", "gen_world_samples", "train_frame",
     "ClusterSet", "kmeans_cluster", "clustered_sample", "clustered_sample_batch",
 ]

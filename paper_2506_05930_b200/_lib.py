@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libnvc.so")
 
 MAX_LEVELS = 32
 MAX_LAYERS = 8
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 c_i32, c_i64, c_u64, c_f64, c_f32, c_vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
                                            ctypes.c_double, ctypes.c_float, ctypes.c_void_p)
@@ -110,6 +110,8 @@ _SIGS = {
     "nvc_clustered_select": (c_i32, [P(NvcScene), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp,
                                      c_u64, c_u64, c_f64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "nvc_shade": (c_i32, [P(NvcScene), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "nvc_primary_hits": (c_i32, [P(NvcScene), P(NvcCamera), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "nvc_grid_scatter": (c_i32, [c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "nvc_closest_hit": (c_i32, [P(NvcScene), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "nvc_batch_workspace_bytes": (c_i64, [c_i32, c_i32]),
     "nvc_targets": (c_i32, [P(NvcScene), c_u64, c_u64, c_vp, c_i64, c_vp, c_vp]),

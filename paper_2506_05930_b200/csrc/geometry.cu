@@ -416,17 +416,24 @@ __device__ double point_factor(const double p[3], const double n[3], const doubl
 // ---------------------------------------------------------------------------
 
 // trace_rays + make_gbuffer: jitter draws (2p, 2p+1) of the PRIMARY stream
+// sxy == nullptr: pixel p_first + i with numpy-Philox jitter (make_gbuffer);
+// else the ray through screen point (sxy[2i], sxy[2i+1]) (gen_screen_hits).
 __global__ void k_gbuffer(nvc_scene sc, nvc_camera cam, uint64_t key, int64_t p_first, int64_t np,
                           double* __restrict__ pos, double* __restrict__ nrm, double* __restrict__ alb,
-                          uint8_t* __restrict__ hit, int32_t* __restrict__ light_id) {
+                          uint8_t* __restrict__ hit, int32_t* __restrict__ light_id,
+                          const double* __restrict__ sxy = nullptr) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= np) return;
-    const int64_t gp = p_first + i;
-    double j0, j1;
-    draw2(key, 2ull * (uint64_t)gp, j0, j1);
-    const int64_t ys = gp / cam.width, xs = gp - ys * cam.width;
     double d[3];
-    camera_ray(cam, (double)xs + j0, (double)ys + j1, d);
+    if (sxy) {
+        camera_ray(cam, sxy[2 * i], sxy[2 * i + 1], d);
+    } else {
+        const int64_t gp = p_first + i;
+        double j0, j1;
+        draw2(key, 2ull * (uint64_t)gp, j0, j1);
+        const int64_t ys = gp / cam.width, xs = gp - ys * cam.width;
+        camera_ray(cam, (double)xs + j0, (double)ys + j1, d);
+    }
     double t;
     const int64_t bt = closest_hit(sc, cam.pos, d, 0.0, __longlong_as_double(0x7ff0000000000000ll), &t);
     const bool h = bt >= 0;
@@ -1303,6 +1310,15 @@ int nvc_gbuffer(const nvc_scene* sc, const nvc_camera* cam, uint64_t key, int64_
     if (p <= 0) return NVC_OK;
     k_gbuffer<<<grid1(p, 128), 128, 0, (cudaStream_t)stream>>>(*sc, *cam, key, p_first, p, pos, nrm, alb, hit,
                                                                 light_id);
+    return check_launch("k_gbuffer");
+}
+
+int nvc_primary_hits(const nvc_scene* sc, const nvc_camera* cam, const double* sxy, int64_t n, double* pos,
+                     double* nrm, double* alb, uint8_t* hit, int32_t* light_id, void* stream) {
+    NVC_REQUIRE(sc && cam && sxy && pos && nrm && alb && hit, "nvc_primary_hits: null argument");
+    if (n <= 0) return NVC_OK;
+    k_gbuffer<<<grid1(n, 128), 128, 0, (cudaStream_t)stream>>>(*sc, *cam, 0, 0, n, pos, nrm, alb, hit, light_id,
+                                                                sxy);
     return check_launch("k_gbuffer");
 }
 

@@ -1155,6 +1155,66 @@ int nvc::nvc_infer_f32(const nvc_model* m, const double* pos, int64_t n, float* 
 }
 
 
+namespace nvc {
+namespace {
+// grad_from_ctx (hashgrid.py:140-151): per level, np.add.at(grad[l], idx, w * g)
+// in float32, i.e. every table entry is the sequential float sum of its
+// contributions in (row, corner) order.  One CTA per level sorts the chunk's
+// (entry, order) keys in shared memory (bitonic) and one thread per entry
+// adds its run in order onto the entry's current value, so chunks applied in
+// stream order reproduce the sequential sum bit for bit.
+constexpr int kScatterChunk = 2048;            // rows per launch: 16384 keys, 128 KB
+__global__ void __launch_bounds__(1024) k_grid_scatter(const int32_t* __restrict__ idx, const double* __restrict__ w,
+                                                       const float* __restrict__ up, int64_t r0, int nr, int L, int F,
+                                                       int64_t T, float* __restrict__ grad) {
+    extern __shared__ unsigned long long keys[];
+    const int l = blockIdx.x;
+    const int n = nr * 8;
+    int np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+        if (i < n) {
+            const int64_t r = r0 + i / 8;
+            const uint32_t e = (uint32_t)idx[(r * L + l) * 8 + (i & 7)];
+            keys[i] = ((unsigned long long)e << 32) | (unsigned)i;
+        } else {
+            keys[i] = ~0ull;
+        }
+    }
+    __syncthreads();
+    for (int k = 2; k <= np2; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+                const int x = i ^ j;
+                if (x > i) {
+                    const unsigned long long a = keys[i], b = keys[x];
+                    if (((i & k) == 0) == (a > b)) {
+                        keys[i] = b;
+                        keys[x] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t e = (uint32_t)(keys[i] >> 32);
+        if (i > 0 && (uint32_t)(keys[i - 1] >> 32) == e) continue;     // not the head of its run
+        float* g = grad + ((int64_t)l * T + e) * F;
+        for (int f = 0; f < F; ++f) {
+            float acc = g[f];
+            for (int q = i; q < n && (uint32_t)(keys[q] >> 32) == e; ++q) {
+                const int o = (int)(keys[q] & 0xffffffffu);
+                const int64_t r = r0 + o / 8;
+                const double wc = w[(r * L + l) * 8 + (o & 7)];
+                acc = __fadd_rn(acc, (float)(wc * (double)up[r * (int64_t)(L * F) + l * F + f]));
+            }
+            g[f] = acc;
+        }
+    }
+}
+}  // namespace
+}  // namespace nvc
+
 extern "C" {
 
 const char* nvc_last_error(void) { return g_err; }
@@ -1179,6 +1239,27 @@ int nvc_refresh_shadow(const nvc_model* m, void* stream) {
     const int64_t wc = wpack_count_of(m);
     k_shadow_wpack<<<grid1(wc, 256), 256, 0, s>>>(net, m->params, m->wpack, wc);
     return check_launch("refresh_shadow");
+}
+
+int nvc_grid_scatter(int32_t levels, int32_t features, int64_t table_size, const int32_t* idx, const double* w,
+                     const float* upstream, int64_t b, float* grad, void* stream) {
+    NVC_REQUIRE(idx && w && upstream && grad, "nvc_grid_scatter: null argument");
+    NVC_REQUIRE(levels > 0 && features > 0 && table_size > 0 && table_size <= (1ll << 32),
+                "nvc_grid_scatter: bad grid shape");
+    const int smem = kScatterChunk * 8 * 8;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_grid_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    for (int64_t r0 = 0; r0 < b; r0 += kScatterChunk) {
+        const int nr = (int)std::min<int64_t>(kScatterChunk, b - r0);
+        k_grid_scatter<<<levels, 1024, smem, (cudaStream_t)stream>>>(idx, w, upstream, r0, nr, levels, features,
+                                                                     table_size, grad);
+        const int rc = check_launch("k_grid_scatter");
+        if (rc != NVC_OK) return rc;
+    }
+    return NVC_OK;
 }
 
 int nvc_encode(const nvc_model* m, const double* pos, int64_t n, float* feats, int32_t* idx_out, double* w_out,

@@ -86,3 +86,103 @@ def encode_batch(positions, cache, with_ctx: bool = False):
     Returns features (B, L*F) float32 numpy; with ``with_ctx`` also the
     per-level corner indices (B, L, 8) int32 and FP64 weights (B, L, 8)."""
     return cache.encode(positions, with_ctx=with_ctx)
+
+
+# ---------------------------------------------------------------------------
+# The reference's functional encoder API (hashgrid.py:75-164), on the device
+# kernels: nvc_encode (exact FP64 index/weight math, sequential FP32 blend =
+# einsum) and nvc_grid_scatter (np.add.at order).  Table and upstream must be
+# float32 (the device encoder's master precision).
+# ---------------------------------------------------------------------------
+
+def init_params(cfg: HashGridConfig, rng: np.random.Generator, dtype=np.float32) -> np.ndarray:
+    """hashgrid.py:75-79."""
+    return init_table(cfg, rng, dtype)
+
+
+def spatial_hash(coords, table_size: int):
+    """hashgrid.py:82-87: (x*1 + y*2654435761 + z*805459861) & (T-1) -- modular add,
+    the index arithmetic k_encode performs in uint32 (host helper for callers)."""
+    c = np.asarray(coords, dtype=np.int64)
+    h = c[..., 0] * HASH_PRIMES[0] + c[..., 1] * HASH_PRIMES[1] + c[..., 2] * HASH_PRIMES[2]
+    return h & (table_size - 1)
+
+
+_GRID_CACHES: dict = {}
+
+
+def _grid_cache(cfg: HashGridConfig):
+    """A device model holding cfg's table (reused per grid shape/AABB)."""
+    import torch
+    from .cache import MODE_LIGHTS, VisibilityCache
+    key = (cfg.levels, cfg.table_size, cfg.features_per_level, cfg.base_resolution, cfg.per_level_scale,
+           tuple(np.asarray(cfg.aabb_min, np.float64)), tuple(np.asarray(cfg.aabb_max, np.float64)),
+           torch.cuda.current_device())
+    c = _GRID_CACHES.get(key)
+    if c is None:
+        c = _GRID_CACHES[key] = VisibilityCache(MODE_LIGHTS, 8, cfg)
+    return c
+
+
+def _encode_functional(pos, cfg: HashGridConfig, params):
+    import torch
+    _lib.require_cuda()
+    params = np.asarray(params)
+    shape = (cfg.levels, cfg.table_size, cfg.features_per_level)
+    if params.shape != shape:
+        raise ValueError(f"params must be {shape}, got {params.shape}")
+    if params.dtype != np.float32:
+        raise ValueError("the CUDA encoder reads a float32 feature table")
+    c = _grid_cache(cfg)
+    c.params[:cfg.param_count].copy_(torch.from_numpy(np.ascontiguousarray(params).reshape(-1)))
+    feats, idx, w = c.encode(np.atleast_2d(np.asarray(pos, dtype=np.float64)), with_ctx=True)
+    ctx = [(idx[:, lvl, :].astype(np.int64), w[:, lvl, :]) for lvl in range(cfg.levels)]
+    return feats, ctx
+
+
+def encode_batch(pos, cfg, params=None, with_ctx: bool = False):
+    """``encode_batch(pos, cfg, params)`` (hashgrid.py:117-131): features (B, L*F)
+    float32 and ctx = [(idx (B,8) int64, w (B,8) float64)] per level.
+
+    ``encode_batch(positions, cache, with_ctx=False)``: the same encoder on a
+    VisibilityCache's own table (features, or features + (B,L,8) idx / w)."""
+    if isinstance(cfg, HashGridConfig):
+        return _encode_functional(pos, cfg, params)
+    return cfg.encode(pos, with_ctx=with_ctx)
+
+
+def encode(pos, cfg: HashGridConfig, params) -> np.ndarray:
+    """hashgrid.py:134-137: the feature vector of one position."""
+    out, _ = _encode_functional(np.asarray(pos, dtype=np.float64)[None, :], cfg, params)
+    return out[0]
+
+
+def grad_from_ctx(cfg: HashGridConfig, ctx, upstream, dtype=None) -> np.ndarray:
+    """hashgrid.py:140-151: dense (L, T, F) table gradient, every entry the
+    sequential float32 sum of float32(w * g) in (row, corner) order (np.add.at);
+    bit-identical, on nvc_grid_scatter."""
+    import torch
+    _lib.require_cuda()
+    up = np.atleast_2d(np.asarray(upstream))
+    dtype = np.dtype(dtype or up.dtype)
+    if dtype != np.float32 or up.dtype != np.float32:
+        raise ValueError("the CUDA scatter accumulates float32 upstream gradients into a float32 table")
+    b, lv = up.shape[0], len(ctx)
+    if lv != cfg.levels or up.shape[1] != cfg.output_dim:
+        raise ValueError("ctx / upstream do not match the grid config")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    idx = np.stack([np.asarray(i).reshape(b, 8) for i, _ in ctx], 1).astype(np.int32)
+    w = np.stack([np.asarray(x, np.float64).reshape(b, 8) for _, x in ctx], 1)
+    idx_d = torch.from_numpy(np.ascontiguousarray(idx)).to(dev)
+    w_d = torch.from_numpy(np.ascontiguousarray(w)).to(dev)
+    up_d = torch.from_numpy(np.ascontiguousarray(up)).to(dev)
+    grad = torch.zeros((cfg.levels, cfg.table_size, cfg.features_per_level), dtype=torch.float32, device=dev)
+    _lib.call("nvc_grid_scatter", cfg.levels, cfg.features_per_level, cfg.table_size, idx_d.data_ptr(),
+              w_d.data_ptr(), up_d.data_ptr(), b, grad.data_ptr(), _lib.stream_ptr())
+    return grad.cpu().numpy()
+
+
+def encode_backward(pos, cfg: HashGridConfig, params, upstream) -> np.ndarray:
+    """hashgrid.py:154-164: gradient of upstream . encode(pos) w.r.t. the table."""
+    _, ctx = _encode_functional(np.atleast_2d(np.asarray(pos, dtype=np.float64)), cfg, params)
+    return grad_from_ctx(cfg, ctx, np.atleast_2d(upstream), dtype=np.asarray(params).dtype)

@@ -119,6 +119,38 @@ def gen_world_samples(scene, n: int, rng) -> np.ndarray:
     return pos.cpu().numpy()
 
 
+def gen_screen_hits(scene, camera, n: int, rng):
+    """training.py:67-94: primary-ray hits through uniformly random screen points,
+    misses redrawn for up to SCREEN_RETRY_ROUNDS rounds (the batch may come back
+    short).  Returns (positions, normals, albedos, is_light).  Each round draws sx
+    then sy from ``rng`` exactly as the reference does; the rays are traced by
+    nvc_primary_hits (k_gbuffer's screen-point mode)."""
+    torch = _lib.require_cuda()
+    ds = device_scene(scene)
+    dev = ds.device
+    cam = camera_struct(camera)
+    parts = ([], [], [], [])
+    want = int(n)
+    for _ in range(SCREEN_RETRY_ROUNDS + 1):
+        if want == 0:
+            break
+        sx = rng.random(want) * camera.width
+        sy = rng.random(want) * camera.height
+        sxy = torch.from_numpy(np.ascontiguousarray(np.stack([sx, sy], 1))).to(dev)
+        pos, nrm, alb = (torch.empty((want, 3), dtype=torch.float64, device=dev) for _ in range(3))
+        hit = torch.empty(want, dtype=torch.uint8, device=dev)
+        lid = torch.empty(want, dtype=torch.int32, device=dev)
+        _lib.call("nvc_primary_hits", ds.struct, cam, sxy.data_ptr(), want, pos.data_ptr(), nrm.data_ptr(),
+                  alb.data_ptr(), hit.data_ptr(), lid.data_ptr(), _lib.stream_ptr())
+        h = hit.bool()
+        for lst, t in zip(parts, (pos[h], nrm[h], alb[h], lid[h] >= 0)):
+            lst.append(t)
+        want -= int(h.sum().item())
+    if not parts[0]:
+        return np.zeros((0, 3)), np.zeros((0, 3)), np.zeros((0, 3)), np.zeros(0, dtype=bool)
+    return tuple(torch.cat(lst).cpu().numpy() for lst in parts)
+
+
 def gen_screen_samples(scene, camera, n: int, rng) -> np.ndarray:
     """Primary-ray hit points, <= 9 rounds of redraws (training.py:67-100)."""
     import torch

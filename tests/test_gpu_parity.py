@@ -1013,3 +1013,106 @@ def test_native_library_is_loaded():
     import ctypes  # noqa: F401
     lib = _lib.load()
     assert lib.nvc_abi_version() == _lib.ABI_VERSION
+
+
+# ---------------------------------------------------------------------------
+# The reference's functional API (hashgrid.py:75-164, mlp.py:110-218,
+# training.py:67-94) on the device kernels
+# ---------------------------------------------------------------------------
+class TestFunctionalApi:
+    def _grid(self, scene, levels=8, tsize=1 << 12):
+        from paper_2506_05930_b200 import hashgrid as H
+        cfg = grid_cfg(scene, levels, tsize)
+        og = O.Grid(levels=levels, features_per_level=2, table_size=tsize, aabb_min=scene.aabb_min,
+                    aabb_max=scene.aabb_max)
+        table = H.init_params(cfg, R.stream(2, "init-params"))
+        return H, cfg, og, table
+
+    def test_encode_batch_and_ctx_bit_exact(self, boxes32):
+        H, cfg, og, table = self._grid(boxes32)
+        pos = R.stream(3, "fn-enc").uniform(boxes32.aabb_min - 0.1, boxes32.aabb_max + 0.1, (3000, 3))
+        feats, ctx = H.encode_batch(pos, cfg, table)
+        want, wctx = O.encode(og, table, pos)
+        np.testing.assert_array_equal(feats, want)
+        assert len(ctx) == cfg.levels
+        for (i, w), (wi, ww) in zip(ctx, wctx):
+            assert i.dtype == np.int64 and i.shape == (3000, 8)
+            np.testing.assert_array_equal(i, wi)
+            np.testing.assert_array_equal(w, ww)
+        np.testing.assert_array_equal(H.encode(pos[5], cfg, table), want[5])
+        np.testing.assert_array_equal(H.spatial_hash(np.array([[3, 5, 7]]), 1 << 12),
+                                      (3 + 5 * 2654435761 + 7 * 805459861) & 4095)
+        with pytest.raises(ValueError):
+            H.encode_batch(pos, cfg, table.astype(np.float64))
+
+    @pytest.mark.parametrize("b", [1, 777, 5000])
+    def test_grad_from_ctx_bit_exact(self, boxes32, b):
+        """np.add.at order (sequential float32 per entry), incl. chunked batches and
+        heavy collisions on the coarse dense levels."""
+        H, cfg, og, table = self._grid(boxes32)
+        pos = R.stream(4, "fn-grad").uniform(boxes32.aabb_min, boxes32.aabb_max, (b, 3))
+        up = R.stream(5, "fn-up").normal(0.0, 1.0, (b, cfg.output_dim)).astype(np.float32)
+        _, ctx = H.encode_batch(pos, cfg, table)
+        got = H.grad_from_ctx(cfg, ctx, up)
+        _, wctx = O.encode(og, table, pos)
+        np.testing.assert_array_equal(got, O.grid_grad(og, wctx, up))
+        np.testing.assert_array_equal(H.encode_backward(pos, cfg, table, up), got)
+
+    def test_mlp_forward_backward_adam(self):
+        from paper_2506_05930_b200 import mlp as M
+        cfg = M.MLPConfig(input_dim=16, output_dim=8, hidden_dims=(64, 64))
+        p = M.he_init(cfg, R.stream(0, "init-params"))
+        x = R.stream(6, "fn-x").normal(0.0, 0.5, (513, 16)).astype(np.float32)
+        t = (R.stream(7, "fn-t").random((513, 8)) > 0.5).astype(np.float32)
+        mask = (R.stream(8, "fn-m").random((513, 8)) > 0.2).astype(np.float32)
+        out, cache = M.forward(p, cfg, x)
+        wout, zs, acts = O.mlp_forward(p.weights, p.biases, x)
+        np.testing.assert_allclose(out, wout, rtol=0, atol=1e-6)        # test_mlp.py:70 tolerance
+        assert set(cache) == {"zs", "acts", "out_raw"} and len(cache["zs"]) == 3
+        assert M.l2_loss(out, t, mask) == pytest.approx(O.l2_loss(wout, t, mask), rel=1e-5)
+        g, d_in = M.backward_l2(p, cfg, cache, t, mask)
+        gw, gb, wd = O.mlp_backward(p.weights, zs, acts, t, mask)
+        for a, b_ in zip(g.weights + g.biases, gw + gb):
+            np.testing.assert_allclose(a, b_, rtol=1e-4, atol=1e-7)
+        np.testing.assert_allclose(d_in, wd, rtol=1e-4, atol=1e-7)
+        with pytest.raises(ValueError):
+            M.forward(p, cfg, np.full((2, 16), np.nan, np.float32))
+        with pytest.raises(ValueError):
+            M.forward(p, cfg, np.zeros((2, 15), np.float32))
+        # Adam: reference op order in float32, bit-exact against the oracle's numpy steps
+        params = {k: v.copy() for k, v in p.as_dict().items()}
+        st = M.AdamState.for_params(params)
+        flat = np.concatenate([v.reshape(-1) for v in params.values()])
+        oa = O.Adam(flat.size)
+        for step in range(3):
+            grads = {k: R.stream(9, step, k).normal(0.0, 1e-2, v.shape).astype(np.float32) for k, v in params.items()}
+            M.adam_step(params, grads, st, 0.05)
+            oa.step(flat, np.concatenate([grads[k].reshape(-1) for k in params]), 0.05)
+        np.testing.assert_array_equal(np.concatenate([v.reshape(-1) for v in params.values()]), flat)
+        assert st.t == 3
+
+    def test_gen_screen_hits_matches_reference(self, boxes8, g_scenes):
+        from paper_2506_05930_b200.training import gen_screen_hits
+        g = R.stream(11, "hits")
+        pos, nrm, alb, is_light = gen_screen_hits(boxes8, boxes8.camera, 400, g)
+        sa = O.SceneArrays.from_golden(g_scenes, "boxes8_")
+        st = O.Stream(key=R.stream_key(11, "hits"))
+        w, h = boxes8.camera.width, boxes8.camera.height
+        want = {"position": [], "normal": [], "albedo": [], "light": []}
+        left = 400
+        for _ in range(9):
+            if left == 0:
+                break
+            sx = st.random(left) * w
+            sy = st.random(left) * h
+            tr = sa.trace(*sa.camera_rays(sx, sy))
+            for k in ("position", "normal", "albedo"):
+                want[k].append(tr[k][tr["hit"]])
+            want["light"].append(tr["light_id"][tr["hit"]] >= 0)
+            left -= int(tr["hit"].sum())
+        np.testing.assert_array_equal(pos, np.concatenate(want["position"]))
+        np.testing.assert_array_equal(nrm, np.concatenate(want["normal"]))
+        np.testing.assert_array_equal(alb, np.concatenate(want["albedo"]))
+        np.testing.assert_array_equal(is_light, np.concatenate(want["light"]))
+        np.testing.assert_array_equal(g.random(2), O.uniform_at(st.key, st.offset + np.arange(2)))
+        np.testing.assert_array_equal(gen_screen_samples(boxes8, boxes8.camera, 400, R.stream(11, "hits")), pos)
