@@ -192,3 +192,32 @@ def test_no_device_means_loud_failure():
     from paper_2506_05930_b200 import VisibilityCache
     with pytest.raises(RuntimeError, match="CUDA device"):
         VisibilityCache("lights", 8, HashGridConfig(levels=2, table_size=64))
+
+
+def test_functional_api_surface():
+    """The reference's module-level functions exist with its names; the host-only
+    pieces (spatial_hash, init_params) agree with the reference formulas and the
+    device ones fail loudly without a GPU."""
+    import torch
+    from paper_2506_05930_b200 import hashgrid as H
+    from paper_2506_05930_b200 import mlp as M
+    from paper_2506_05930_b200 import training as T
+    for mod, names in ((H, ("init_params", "spatial_hash", "encode_batch", "encode", "grad_from_ctx", "encode_backward")),
+                       (M, ("forward", "l2_loss", "backward_l2", "AdamState", "adam_step")),
+                       (T, ("gen_screen_hits", "gen_screen_samples", "gen_world_samples"))):
+        for n in names:
+            assert callable(getattr(mod, n)), n
+    c = np.array([[0, 0, 0], [1, 2, 3], [2**20, 7, 2**19]])
+    np.testing.assert_array_equal(H.spatial_hash(c, 1 << 19),
+                                  (c[:, 0] + c[:, 1] * 2654435761 + c[:, 2] * 805459861) & ((1 << 19) - 1))
+    cfg = HashGridConfig(levels=2, table_size=64)
+    t = H.init_params(cfg, R.stream(0, "init-params"))
+    assert t.shape == (2, 64, 4) and t.dtype == np.float32 and np.abs(t).max() <= 1e-4
+    np.testing.assert_array_equal(t, R.stream(0, "init-params").uniform(-1e-4, 1e-4, (2, 64, 4)).astype(np.float32))
+    st = M.AdamState.for_params({"w": np.ones(3, np.float32)})
+    assert st.t == 0 and st.beta1 == 0.9 and st.beta2 == 0.999 and st.eps == 1e-8
+    if not torch.cuda.is_available():
+        with pytest.raises(RuntimeError, match="CUDA device"):
+            H.encode_batch(np.zeros((1, 3)), cfg, t)
+        with pytest.raises(RuntimeError, match="CUDA device"):
+            M.forward(M.he_init(M.MLPConfig(4, 2), R.stream(0, "x")), M.MLPConfig(4, 2), np.zeros((1, 4), np.float32))
