@@ -199,7 +199,7 @@ def gpu_arm(args) -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    prio = int(os.environ.get("NVC_MAIN_PRIORITY", "0"))
+    prio = int(os.environ.get("NVC_MAIN_PRIORITY", "-1"))
     if prio:
         torch.cuda.set_stream(torch.cuda.Stream(dev, priority=prio))
     if world > 1:

@@ -223,7 +223,7 @@ class BatchPipeline:
             self.ex = [GradExchange(cache, cfg.n_world + cfg.n_screen) for _ in range(2)]
         # the batch chain (screen rays -> compaction -> shadow rays) is latency-bound:
         # give it priority so it completes within the frame it overlaps
-        self.side = torch.cuda.Stream(device, priority=int(os.environ.get("NVC_BATCH_PRIORITY", "-1")))
+        self.side = torch.cuda.Stream(device, priority=int(os.environ.get("NVC_BATCH_PRIORITY", "-2")))
         self.ready = [torch.cuda.Event() for _ in range(2)]
         self.free = [torch.cuda.Event() for _ in range(2)]
         cur = torch.cuda.current_stream(device)
