@@ -604,6 +604,9 @@ def clusters_arm(args) -> None:
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
     torch.cuda.set_device(dev)
+    prio = int(os.environ.get("NVC_MAIN_PRIORITY", "-1"))   # as gpu_arm: the batch stream (-2) outranks the frame
+    if prio:
+        torch.cuda.set_stream(torch.cuda.Stream(dev, priority=prio))
     scene = scene_from_dict(rooms_scene(1024))
     cs = kmeans_cluster(scene.lights, 32, R.stream(0, R.CLUSTERING))
     cam = scene.camera.resized(WIDTH, HEIGHT)

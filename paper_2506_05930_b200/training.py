@@ -230,7 +230,7 @@ class BatchPipeline:
         for e in self.free:
             e.record(cur)
         self.pending = [None, None]       # frame whose batch each buffer holds / will hold
-        self.early = os.environ.get("NVC_BATCH_EARLY", "0") == "1"
+        self.early = os.environ.get("NVC_BATCH_EARLY", "1") == "1"
 
     def _launch(self, frame: int) -> None:
         import torch
