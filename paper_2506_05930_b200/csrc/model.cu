@@ -1452,8 +1452,10 @@ int nvc_adam_step(const nvc_model* m, int64_t t, double lr, void* stream) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int64_t ntiles = net.grid_count / kAdamTile;
-        const char* ge = getenv("NVC_ADAM_GRID");   // CTAs per SM (default 3: 3 x 61 KB smem rings)
-        const int grid = (int)std::min<int64_t>(ntiles, (ge ? atoi(ge) : 3) * (int64_t)sms);
+        // CTAs per SM (default 2: 2 x 61 KB smem rings still stream at HBM rate and
+        // leave each SM room for the previous frame's NLS blocks running beside it)
+        const char* ge = getenv("NVC_ADAM_GRID");
+        const int grid = (int)std::min<int64_t>(ntiles, (ge ? atoi(ge) : 2) * (int64_t)sms);
         if (m->grad_c)
             k_adam_bulk<true><<<grid, kAdamThreads, smem, s>>>(m->params, m->adam_m, m->adam_v, sink_of(m), m->table_h,
                                                                ntiles, a, m->table_size);
