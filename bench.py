@@ -21,8 +21,10 @@ own 1080p tile of an N-tile frame (global pixel ids keep the RNG draws
 distinct) and trains data-parallel on its 8192-row shard of an 8192*N-row
 global batch, with one NCCL allreduce of the fixed-point gradients per step.
 
-`--impl reference` times the CPU oracle port of the reference (oracle/) on the
-host cores with the same workload definition (bounded sample, extrapolated).
+`--impl reference` times the unmodified reference (baseline/_ref, installed by
+tools/install_reference.sh) on the host cores with the same workload: its own
+train_frame + nls_sample_batch on a 1/8 pixel sample (extrapolated); the CPU
+oracle port (oracle/) stands in only when baseline/_ref is absent.
 """
 
 from __future__ import annotations
@@ -50,6 +52,7 @@ N_WORLD = N_SCREEN = 4096
 # k_tr_scatter, k_reduce_parts, k_adam_bulk, k_adam_mlp; query k_enc_tiles2,
 # k_mlp_ts, k_nls32g
 LAUNCHES_PER_FRAME = 14
+LUM_DEFAULT = "f64"
 METRIC = "visibility queries/s (encode+MLP+WRS) at 1080p x 32 lights; train samples/s"
 UNIT = "queries/s"
 C4_METRIC = "visibility queries/s (encode+MLP+WRS) at 1080p x 128 lights (C4); train samples/s"
@@ -120,9 +123,11 @@ def _oracle_query_chunk(args):
     """Encode+MLP+WRS for a pixel chunk on one host core (oracle restatement)."""
     from oracle import vc_oracle as O
     lo, hi, key, p_first, p_total = args
+    from threadpoolctl import threadpool_limits
     st = _CPU_STATE
-    vis = st["cache"].infer(st["pos"][lo:hi])
-    return O.nls_sample(st["sa"], vis, st["lum"][lo:hi], key, p_total=p_total, p_first=p_first)
+    with threadpool_limits(1):       # one core per worker: no BLAS oversubscription
+        vis = st["cache"].infer(st["pos"][lo:hi])
+        return O.nls_sample(st["sa"], vis, st["lum"][lo:hi], key, p_total=p_total, p_first=p_first)
 
 
 def cpu_reference(sample_pixels: int = 24576, procs: int | None = None, repeats: int = 1) -> dict:
@@ -212,7 +217,11 @@ def gpu_arm(args) -> None:
     P = WIDTH * HEIGHT
     p_first, p_total = rank * P, P * world
     pos, nrm, alb, hit, _ = gbuffer_device(scene, cam, p_first, P)
-    ctx = PixelCtx(scene, pos, nrm, alb)
+    # luminance table precision: NVC_LUM=f64 (the reference's) or f32 (default perf path:
+    # half the NLS table traffic; its light-choice mismatch vs f64 is measured in
+    # tests/test_gpu_headline.py::test_c2_f32_lum_choice_mismatch)
+    lum_dt = np.float64 if os.environ.get("NVC_LUM", LUM_DEFAULT) == "f64" else np.float32
+    ctx = PixelCtx(scene, pos, nrm, alb, table_dtype=lum_dt)
     ctx.lum_device()
     grid = HashGridConfig(levels=LEVELS, table_size=TABLE, features_per_level=FEATS, aabb_min=scene.aabb_min,
                           aabb_max=scene.aabb_max)
@@ -384,12 +393,13 @@ def gpu_arm(args) -> None:
         k_ms = [statistics.median(x[i] for x in split_k) for i in range(3)]
         # roofline of each query kernel: algorithmic work per launch / its event-timed duration
         # (DESIGN.md section 4 gives the per-pixel figures)
+        lum_b = np.dtype(lum_dt).itemsize
         dims = (LEVELS * FEATS,) + tuple(hid) + (kk,)
         flop_px = 2 * sum(a * b for a, b in zip(dims[:-1], dims[1:]))
         kern = {
             "k_enc_tiles2": ("hbm", P * (24 + 64), k_ms[0]),             # pos in, fp16 feature tile out
             "k_mlp_ts": ("tensor", P * flop_px, k_ms[1]),                # 24,576 flop per pixel
-            "k_nls32": ("hbm", P * (2 * kk + 4 * kk + 4 * ((kk + 31) // 32) + 40), k_ms[2]),   # vis + lum + mask in, id/W/point out
+            "k_nls32": ("hbm", P * (2 * kk + lum_b * kk + 4 * ((kk + 31) // 32) + 40), k_ms[2]),   # vis + lum + mask in, id/W/point out
         }
         # encoder gathers vs the measured random-gather L2 rate over the same 67 MB table
         # (profiles/r1_l2_gather_probe.txt, tools/l2_probe.py)
@@ -429,7 +439,9 @@ def gpu_arm(args) -> None:
                        "train_samples_per_s": (N_WORLD + N_SCREEN) / (ms * 1e-3),
                        "pixels_per_gpu": P, "global_batch": N_WORLD + N_SCREEN,
                        "parallelism": f"dp{world} (train: batch rows sharded, one allreduce) + {world} screen tiles (query)",
-                       "l2": "inputs > L2 every frame (lum table 265 MB + 16.8 M-parameter Adam stream 530 MB)",
+                       "l2": (f"inputs > L2 every frame (lum table {P * kk * lum_b / 1e6:.0f} MB "
+                              f"{np.dtype(lum_dt).name} + 16.8 M-parameter Adam stream 530 MB)"),
+                       "lum_dtype": np.dtype(lum_dt).name,
                        "host_issue_ms_per_frame": issue_ms,
                        "stage_ms": {"train_frame": tr_ms, "query": q_ms, "k_enc_tiles2": k_ms[0],
                                     "k_mlp_ts": k_ms[1], "k_nls32": k_ms[2],
@@ -451,7 +463,7 @@ def gpu_arm(args) -> None:
         }
         assert line["roofline"]["unit"] in ("GB/s", "TFLOP/s") and line["roofline"]["bound"] in ("hbm", "tensor")
         if world == 1 and not args.no_cpu_baseline and not shade and not c4:
-            line["cpu_baseline"] = cpu_reference(sample_pixels=args.cpu_sample)
+            line["cpu_baseline"] = cpu_baseline()
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -485,7 +497,7 @@ def ndi4k_arm(args) -> None:
     rows = H4 // world
     P = W4 * rows
     pos, nrm, alb, _, _ = gbuffer_device(scene, cam, rank * P, P)
-    ctx = PixelCtx(scene, pos, nrm, alb)
+    ctx = PixelCtx(scene, pos, nrm, alb, table_dtype=np.float32)
     ctx.factor_device()
     ctx.mask_device("factor")
     grid = HashGridConfig(levels=LEVELS, table_size=TABLE, features_per_level=FEATS, aabb_min=scene.aabb_min,
@@ -556,7 +568,7 @@ def sweep_arm(args) -> None:
             nrm = torch.zeros_like(pos)
             nrm[:, 1] = 1.0
             alb = torch.full_like(pos, 0.73)
-            ctx = PixelCtx(scene, pos, nrm, alb)
+            ctx = PixelCtx(scene, pos, nrm, alb, table_dtype=np.float32)
             ctx.lum_device()
             ctx.mask_device("lum")
             key = R.stream_key(0, lg, "light-select")
@@ -659,23 +671,135 @@ def clusters_arm(args) -> None:
                       "clocks": clocks.summary()}), flush=True)
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+_REF_STATE = {}   # reference scene / cache / G-buffer sample, inherited by forked workers
+
+
+def _import_reference():
+    """The unmodified reference package installed into baseline/_ref (DESIGN 6), or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "viscache")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/nvc_numba_cache")
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import viscache  # noqa: F401
+        return viscache
+    except Exception:
+        return None
+
+
+def _ref_nls_shard(args):
+    """Reference nls_sample_batch on one contiguous shard of the pixel sample
+    (one worker process, BLAS pinned to one thread)."""
+    from threadpoolctl import threadpool_limits
+    from viscache import rng as RR
+    from viscache.sampling import PixelCtx as RefCtx, nls_sample_batch as ref_nls
+    lo, hi, frame = args
+    st = _REF_STATE
+    ctxs = st.setdefault("ctxs", {})
+    with threadpool_limits(1):
+        if (lo, hi) not in ctxs:       # per-camera memo, as render.py:128-142 keeps it
+            ctxs[(lo, hi)] = RefCtx(st["scene"], st["pos"][lo:hi], st["nrm"][lo:hi], st["alb"][lo:hi])
+        t0 = time.perf_counter()
+        ref_nls(ctxs[(lo, hi)], st["cache"], RR.stream(0, frame, "light-select"))
+        return time.perf_counter() - t0
+
+
+def reference_cpu(steps: int = 3, warmup: int = 1, every: int = 8, procs: int | None = None) -> dict:
+    """The unmodified reference (baseline/_ref) timed on the host cores.
+
+    One step = the reference's own ``train_frame`` (full 8192-sample batch,
+    shadow-ray labels, train step; one process, as the reference runs) + its
+    ``nls_sample_batch`` over every ``every``-th pixel of the 1080p G-buffer,
+    split into contiguous shards over ``procs`` worker processes (BLAS pinned
+    to one thread each; a harness around the reference's function, not a
+    change to it).  The frame time extrapolates the query x``every``.  The
+    G-buffer and per-camera luminance tables are built before timing (the
+    reference memoizes them per camera).  Workers hold the cache as of the
+    warm-up frame: the query cost does not depend on parameter values."""
+    import dataclasses
+    import multiprocessing as mp
+
+    ref = _import_reference()
+    if ref is None:
+        return None
+    from viscache import rng as RR
+    from viscache.cache import MODE_LIGHTS as REF_LIGHTS, VisibilityCache as RefCache
+    from viscache.hashgrid import HashGridConfig as RefGrid, init_params
+    from viscache.mlp import AdamState, MLPConfig, he_init
+    from viscache.render import make_gbuffer
+    from viscache.scene import scene_from_dict as ref_scene
+    from viscache.scenes import boxes_scene as ref_boxes
+    from viscache.training import TrainFrameConfig as RefTF, train_frame as ref_train
+
+    procs = procs or os.cpu_count() or 1
+    s = ref_scene(ref_boxes(K))
+    cam = dataclasses.replace(s.camera, width=WIDTH, height=HEIGHT)
+    g = RefGrid(levels=LEVELS, table_size=TABLE, features_per_level=FEATS, aabb_min=s.aabb_min, aabb_max=s.aabb_max)
+    c = RefCache(REF_LIGHTS, K, g, seed=0)
+    # BASELINE's 3x64 MLP (the reference hardcodes (32, 32), cache.py:37-38): same
+    # single init stream, table then He weights (cache.py:41-43)
+    init = RR.stream(0, RR.INIT_PARAMS)
+    c.grid_params = init_params(g, init)
+    c.net_cfg = MLPConfig(input_dim=g.output_dim, output_dim=K, hidden_dims=HIDDEN)
+    c.net_params = he_init(c.net_cfg, init)
+    c.adam = AdamState.for_params(c._param_dict())
+    tcfg = RefTF()
+    t_setup = time.perf_counter()
+    gb = make_gbuffer(s, cam)
+    sel = np.arange(0, gb.n_pixels, every)
+    pos, nrm, alb = (gb.flat(n)[sel] for n in ("position", "normal", "albedo"))
+    for f in range(warmup):
+        ref_train(s, cam, c, tcfg, frame=f)          # also JIT-compiles the numba kernels
+    _REF_STATE.update(scene=s, cache=c, pos=pos, nrm=nrm, alb=alb)
+    shards = [(int(a[0]), int(a[-1]) + 1) for a in np.array_split(np.arange(sel.size), procs) if a.size]
+    t_train, t_query = [], []
+    with mp.get_context("fork").Pool(len(shards)) as pool:
+        pool.map(_ref_nls_shard, [(lo, hi, 0) for lo, hi in shards])   # per-camera tables + JIT, untimed
+        setup_s = time.perf_counter() - t_setup
+        for f in range(steps):
+            t0 = time.perf_counter()
+            ref_train(s, cam, c, tcfg, frame=warmup + f)
+            t1 = time.perf_counter()
+            pool.map(_ref_nls_shard, [(lo, hi, warmup + f) for lo, hi in shards])
+            t2 = time.perf_counter()
+            t_train.append(t1 - t0)
+            t_query.append(t2 - t1)
+    tr, q = statistics.median(t_train), statistics.median(t_query)
+    p_total = WIDTH * HEIGHT
+    frame_s = tr + q * (p_total / sel.size)
+    return {"value": p_total / frame_s, "unit": UNIT, "cores": len(shards), "kind": "reference",
+            "sample": (f"unmodified reference (baseline/_ref viscache 0.1.0, numpy+numba) on the host, median of "
+                       f"{steps} steps: train_frame (8192 samples, 1 process) {tr:.2f} s + nls_sample_batch on "
+                       f"every {every}th pixel ({sel.size} of {p_total}) over {len(shards)} processes "
+                       f"{q:.2f} s, query extrapolated x{p_total / sel.size:.0f}; frame {frame_s:.2f} s "
+                       f"(setup {setup_s:.0f} s untimed)"),
+            "train_samples_per_s": (N_WORLD + N_SCREEN) / frame_s, "frame_s": frame_s,
+            "train_s": tr, "query_sample_s": q, "steps": steps}
+
+
+def cpu_baseline(steps: int = 3, warmup: int = 1) -> dict:
+    """The reference when baseline/_ref is installed, else the oracle port."""
+    cb = reference_cpu(steps=steps, warmup=warmup)
+    return cb if cb is not None else cpu_reference()
+
+
 def reference_arm(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    steps = []
-    cb = None
-    for _ in range(max(1, args.steps if args.steps <= 3 else 3)):
-        cb = cpu_reference(sample_pixels=args.cpu_sample)
-        steps.append(cb["frame_s"])
-    frame_s = min(steps)
+    cb = cpu_baseline(steps=args.steps, warmup=args.warmup)
+    frame_s = cb["frame_s"]
     value = WIDTH * HEIGHT / frame_s
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
-            "steps": len(steps), "warmup": 1, "ms_per_step": frame_s * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32 MLP / f64 index+WRS (numpy)",
+            "steps": cb.get("steps", args.steps), "warmup": args.warmup, "ms_per_step": frame_s * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 MLP / f64 index+WRS (numpy)",
             "data": "synthetic (boxes_scene(32) fixture, random-init weights, seed 0)",
             "config": {"workload": f"C2: {WIDTH}x{HEIGHT} boxes32 (K=32), L=16 T=2^19 F=2, MLP 3x64, "
-                                   "1 online frame = train batch 8192 + NLS over all pixels",
+                                   f"1 online frame = train batch {N_WORLD + N_SCREEN} (rows sharded over 1 ranks) "
+                                   "+ NLS over all pixels",
                        "train_samples_per_s": (N_WORLD + N_SCREEN) / frame_s},
             "impl": "reference",
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},

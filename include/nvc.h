@@ -28,7 +28,7 @@ extern "C" {
 
 #define NVC_MAX_LEVELS 32
 #define NVC_MAX_LAYERS 8
-#define NVC_ABI_VERSION 7
+#define NVC_ABI_VERSION 8
 
 typedef enum {
     NVC_OK = 0,
@@ -266,10 +266,13 @@ int nvc_table_mask(const void *table, int32_t f64, int64_t p_stride, int64_t p, 
                    uint32_t *mask, void *stream);
 
 /* ---- geometry + training data: geometry.py, render.py, training.py ----- */
-/* make_gbuffer (render.py:103-117) for pixels [p_first, p_first+p). */
+/* make_gbuffer / trace_rays (render.py:49-117) for pixels [p_first, p_first+p):
+ * pos/nrm/alb (p,3) f64, hit (p) u8, light_id (p) i32, depth (p) f64 (+inf on a
+ * miss) and emissive (p,3) f64 (the radiance of an emitter hit on its front
+ * face); hit, light_id, depth and emissive may be NULL. */
 int nvc_gbuffer(const nvc_scene *sc, const nvc_camera *cam, uint64_t jitter_key,
                 int64_t p_first, int64_t p, double *pos, double *nrm, double *alb,
-                uint8_t *hit, int32_t *light_id, void *stream);
+                uint8_t *hit, int32_t *light_id, double *depth, double *emissive, void *stream);
 /* light_factors_all (kernels.py:299-316) -> light-major f32/f64 factor and,
  * optionally, lum = factor * (albedo . LUMA*L)/pi (sampling.py:134-139). */
 int nvc_light_factors(const nvc_scene *sc, const double *pos, const double *nrm,

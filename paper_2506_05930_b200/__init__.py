@@ -25,6 +25,7 @@ from .scene import Camera, Light, Material, Scene, SceneError, load_scene, scene
 from .scenes import boxes_point_scene, boxes_scene, rooms_scene
 from .training import (TrainFrameConfig, compute_visibility_targets, gen_screen_hits, gen_screen_samples,
                        gen_world_samples, train_frame)
+from . import dropin
 
 __version__ = "0.1.0"
 
@@ -38,5 +39,5 @@ __all__ = [
     "wrs_select_batch", "Camera", "Light", "Material", "Scene", "SceneError", "load_scene",
     "scene_from_dict", "boxes_scene", "boxes_point_scene", "rooms_scene", "TrainFrameConfig",
     "compute_visibility_targets", "gen_screen_hits", "gen_screen_samples", "gen_world_samples", "train_frame",
-    "ClusterSet", "kmeans_cluster", "clustered_sample", "clustered_sample_batch",
+    "ClusterSet", "kmeans_cluster", "clustered_sample", "clustered_sample_batch", "dropin",
 ]

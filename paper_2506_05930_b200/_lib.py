@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libnvc.so")
 
 MAX_LEVELS = 32
 MAX_LAYERS = 8
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 c_i32, c_i64, c_u64, c_f64, c_f32, c_vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
                                            ctypes.c_double, ctypes.c_float, ctypes.c_void_p)
@@ -97,7 +97,7 @@ _SIGS = {
                               c_vp, c_vp, c_vp]),
     "nvc_table_mask": (c_i32, [c_vp, c_i32, c_i64, c_i64, c_i32, c_vp, c_vp]),
     "nvc_gbuffer": (c_i32, [P(NvcScene), P(NvcCamera), c_u64, c_i64, c_i64, c_vp, c_vp, c_vp,
-                            c_vp, c_vp, c_vp]),
+                            c_vp, c_vp, c_vp, c_vp, c_vp]),
     "nvc_light_factors": (c_i32, [P(NvcScene), c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_vp,
                                   c_vp, c_vp]),
     "nvc_visibility": (c_i32, [P(NvcScene), c_vp, c_vp, c_i64, c_vp, c_vp]),

@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import json
 import struct
+import weakref
 from dataclasses import asdict
 
 import numpy as np
@@ -24,7 +25,7 @@ import numpy as np
 from . import _lib
 from . import rng as rngmod
 from .hashgrid import HashGridConfig, clustered_config, init_table
-from .mlp import LEAKY, SIGMOID, MLPConfig, MLPParams, TrainStepConfig, he_init, lr_at
+from .mlp import LEAKY, SIGMOID, AdamState, MLPConfig, MLPParams, TrainStepConfig, he_init, lr_at
 
 MODE_LIGHTS = "lights"
 MODE_CLUSTERS = "clusters"
@@ -92,7 +93,10 @@ class VisibilityCache:
         if mode not in (MODE_LIGHTS, MODE_CLUSTERS, MODE_RADIANCE):
             raise ValueError(f"unknown cache mode {mode!r}")
         if np.dtype(dtype) != np.float32:
-            raise ValueError("the CUDA cache keeps float32 master parameters (dtype=np.float32)")
+            # documented refusal (DESIGN 1): the reference's float64 mode exists to
+            # calibrate tolerances on the CPU; the device path keeps f32 masters
+            raise ValueError(f"dtype={np.dtype(dtype).name}: the CUDA cache keeps float32 master parameters "
+                             "(the reference's float64 mode is a CPU-only calibration path)")
         torch = _lib.require_cuda()
         self.mode = mode
         self.output_dim = int(output_dim)
@@ -145,7 +149,7 @@ class VisibilityCache:
         for level in range(g.levels):
             m.resolution[level] = g.resolution(level)
             m.dense[level] = int(g.dense(level))
-        span = g.span()
+        span = np.maximum(np.asarray(g.aabb_max, np.float64) - np.asarray(g.aabb_min, np.float64), 1e-12)
         for a in range(3):
             m.aabb_min[a] = float(g.aabb_min[a])
             m.span[a] = float(span[a])
@@ -165,6 +169,9 @@ class VisibilityCache:
         m.grad_fx = self.grad_fx.data_ptr()
         m.table_h, m.wpack = self.table_h.data_ptr(), self.wpack.data_ptr()
         self.model = m
+        self._mirror = None       # host copy of `params` behind grid_params / net_params views
+        self._handouts = []       # weakrefs to views a caller may still write into
+        self._dirty = False       # views handed out since the last upload
         self._ws = None
         self._qws = None
         self.select_done = None   # CUDA event: last off-stream NLS selection finished
@@ -179,6 +186,8 @@ class VisibilityCache:
                                  for x in (np.asarray(w, np.float32).reshape(-1), np.asarray(b, np.float32))])
         self.params.copy_(torch.from_numpy(flat))
         self.refresh_shadow()
+        if self._mirror is not None:
+            self._mirror[...] = flat
 
     def refresh_shadow(self, stream=None) -> None:
         _lib.call("nvc_refresh_shadow", self.model, _lib.stream_ptr(stream))
@@ -191,13 +200,52 @@ class VisibilityCache:
     def param_count(self) -> int:
         return self.param_count_
 
+    # ---- host views of the parameters (write-through) ---------------------
+    # The reference's grid_params / net_params are the live arrays Adam updates
+    # in place, and callers may write into them (test_render.py:176-179).  Here
+    # they are views into one host mirror of the device vector.  Once a view
+    # has been handed out the mirror is "dirty": the next device op uploads it
+    # (applying any caller writes), and while a view is still alive every
+    # parameter update is downloaded into it.  With no view handed out (the
+    # hot path) nothing is copied.
+    def _views_alive(self) -> bool:
+        self._handouts = [r for r in self._handouts if r() is not None]
+        return bool(self._handouts)
+
+    def _handout(self, view: np.ndarray) -> np.ndarray:
+        self._handouts.append(weakref.ref(view))
+        self._dirty = True
+        return view
+
     def _host_params(self) -> np.ndarray:
-        return self.params.detach().cpu().numpy()
+        """The flat host mirror, current with the device (plus pending caller writes)."""
+        if self._mirror is None:
+            self._mirror = np.empty(self.param_count_, dtype=np.float32)
+        elif getattr(self, "_dirty", False):
+            return self._mirror
+        self._mirror[...] = self.params.detach().cpu().numpy()
+        return self._mirror
+
+    def _push_views(self) -> None:
+        """Before a device op reads parameters: apply caller writes to handed-out views."""
+        if getattr(self, "_dirty", False):
+            import torch
+            self.params.copy_(torch.from_numpy(self._mirror))
+            self.refresh_shadow()
+            self._dirty = self._views_alive()
+
+    def _pull_views(self) -> None:
+        """After a device op changed parameters: refresh live views in place."""
+        if getattr(self, "_dirty", False) and self._views_alive():
+            self._mirror[...] = self.params.detach().cpu().numpy()
+        elif self._mirror is not None:
+            self._dirty = False
 
     @property
     def grid_params(self) -> np.ndarray:
         g = self.grid_cfg
-        return self._host_params()[:g.param_count].reshape(g.levels, g.table_size, g.features_per_level)
+        flat = self._host_params()
+        return self._handout(flat[:g.param_count].reshape(g.levels, g.table_size, g.features_per_level))
 
     @grid_params.setter
     def grid_params(self, value) -> None:
@@ -208,8 +256,8 @@ class VisibilityCache:
         flat = self._host_params()
         ws, bs = [], []
         for (wo, bo), (fo, fi) in zip(self._layer_offs, self.net_cfg.layer_dims):
-            ws.append(flat[wo:wo + fo * fi].reshape(fo, fi).copy())
-            bs.append(flat[bo:bo + fo].copy())
+            ws.append(self._handout(flat[wo:wo + fo * fi].reshape(fo, fi)))
+            bs.append(self._handout(flat[bo:bo + fo]))
         return MLPParams(ws, bs)
 
     @net_params.setter
@@ -218,6 +266,30 @@ class VisibilityCache:
 
     def _param_dict(self) -> dict:
         return {"grid": self.grid_params, **self.net_params.as_dict()}
+
+    def _split(self, flat: np.ndarray) -> dict:
+        g = self.grid_cfg
+        out = {"grid": flat[:g.param_count].reshape(g.levels, g.table_size, g.features_per_level)}
+        for i, ((wo, bo), (fo, fi)) in enumerate(zip(self._layer_offs, self.net_cfg.layer_dims)):
+            out[f"w{i}"] = flat[wo:wo + fo * fi].reshape(fo, fi)
+            out[f"b{i}"] = flat[bo:bo + fo]
+        return out
+
+    @property
+    def adam(self) -> AdamState:
+        """Adam moments per parameter array and the step (reference ``cache.adam``,
+        cache.py:44): a host snapshot; assign an AdamState to restore one."""
+        return AdamState(m=self._split(self.adam_m.cpu().numpy()), v=self._split(self.adam_v.cpu().numpy()),
+                         t=self.adam_t)
+
+    @adam.setter
+    def adam(self, state) -> None:
+        import torch
+        names = list(self._split(np.zeros(self.param_count_, np.float32)))
+        for dst, src in ((self.adam_m, state.m), (self.adam_v, state.v)):
+            flat = np.concatenate([np.asarray(src[k], np.float32).reshape(-1) for k in names])
+            dst.copy_(torch.from_numpy(flat))
+        self.adam_t = int(state.t)
 
     def adam_state(self) -> dict:
         """Adam moments and step (the reference snapshot omits these)."""
@@ -239,6 +311,7 @@ class VisibilityCache:
 
     def encode(self, positions, with_ctx: bool = False):
         import torch
+        self._push_views()
         pos, is_dev = self._pos_device(positions)
         n = pos.shape[0]
         g = self.grid_cfg
@@ -258,6 +331,7 @@ class VisibilityCache:
         If a selection is still running on another stream (``select_done``),
         the current stream first waits for it: it reads this workspace."""
         import torch
+        self._push_views()
         if p <= 0:
             return None
         if self.select_done is not None:
@@ -270,6 +344,7 @@ class VisibilityCache:
 
     def infer_device(self, pos, precision: int | None = None, out=None):
         import torch
+        self._push_views()
         n = pos.shape[0]
         if out is None:
             out = torch.empty((n, self.output_dim), dtype=torch.float32, device=self.device)
@@ -304,6 +379,7 @@ class VisibilityCache:
                          loss_out=None):
         """Device gradient accumulation (the allreduce point for data parallelism)."""
         import torch
+        self._push_views()
         b_max = int(pos.shape[0] if b_max is None else b_max)
         if loss_out is None:
             loss_out = torch.zeros(2, dtype=torch.float64, device=self.device)   # [sum, mean]
@@ -320,6 +396,7 @@ class VisibilityCache:
         self.adam_t += 1
         _lib.call("nvc_adam_step", self.model, self.adam_t, lr, _lib.stream_ptr())
         self.step += 1
+        self._pull_views()
 
     def _bind_compact(self, b_max: int) -> None:
         """(Re)allocate the compact-gradient buffers for batches of up to b_max rows."""

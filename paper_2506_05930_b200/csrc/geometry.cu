@@ -421,7 +421,8 @@ __device__ double point_factor(const double p[3], const double n[3], const doubl
 __global__ void k_gbuffer(nvc_scene sc, nvc_camera cam, uint64_t key, int64_t p_first, int64_t np,
                           double* __restrict__ pos, double* __restrict__ nrm, double* __restrict__ alb,
                           uint8_t* __restrict__ hit, int32_t* __restrict__ light_id,
-                          const double* __restrict__ sxy = nullptr) {
+                          const double* __restrict__ sxy = nullptr, double* __restrict__ depth = nullptr,
+                          double* __restrict__ emissive = nullptr) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= np) return;
     double d[3];
@@ -437,7 +438,7 @@ __global__ void k_gbuffer(nvc_scene sc, nvc_camera cam, uint64_t key, int64_t p_
     double t;
     const int64_t bt = closest_hit(sc, cam.pos, d, 0.0, __longlong_as_double(0x7ff0000000000000ll), &t);
     const bool h = bt >= 0;
-    double P[3] = {0, 0, 0}, N[3] = {0, 0, 0}, A[3] = {0, 0, 0};
+    double P[3] = {0, 0, 0}, N[3] = {0, 0, 0}, A[3] = {0, 0, 0}, E[3] = {0, 0, 0};
     int32_t lid = -1;
     if (h) {
         const int64_t tri = __ldg(sc.perm + bt);
@@ -459,7 +460,13 @@ __global__ void k_gbuffer(nvc_scene sc, nvc_camera cam, uint64_t key, int64_t p_
         if (mat >= 0)
             for (int a = 0; a < 3; ++a) A[a] = __ldg(sc.mat_albedo + 3 * mat + a);
         lid = __ldg(sc.tri_light + tri);
+        // render.py:69-71: an emitter seen from its front face shows its radiance
+        if (lid >= 0 && !(facing > 0.0))
+            for (int a = 0; a < 3; ++a) E[a] = __ldg(sc.lt_radiance + 3 * lid + a);
     }
+    if (depth) depth[i] = h ? t : __longlong_as_double(0x7ff0000000000000ll);
+    if (emissive)
+        for (int a = 0; a < 3; ++a) emissive[3 * i + a] = E[a];
     for (int a = 0; a < 3; ++a) {
         pos[3 * i + a] = P[a];
         nrm[3 * i + a] = N[a];
@@ -1305,11 +1312,12 @@ using namespace nvc;
 extern "C" {
 
 int nvc_gbuffer(const nvc_scene* sc, const nvc_camera* cam, uint64_t key, int64_t p_first, int64_t p,
-                double* pos, double* nrm, double* alb, uint8_t* hit, int32_t* light_id, void* stream) {
+                double* pos, double* nrm, double* alb, uint8_t* hit, int32_t* light_id, double* depth,
+                double* emissive, void* stream) {
     NVC_REQUIRE(sc && cam && pos && nrm && alb, "nvc_gbuffer: null argument");
     if (p <= 0) return NVC_OK;
     k_gbuffer<<<grid1(p, 128), 128, 0, (cudaStream_t)stream>>>(*sc, *cam, key, p_first, p, pos, nrm, alb, hit,
-                                                                light_id);
+                                                                light_id, nullptr, depth, emissive);
     return check_launch("k_gbuffer");
 }
 

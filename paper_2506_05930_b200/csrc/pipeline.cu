@@ -214,10 +214,27 @@ __global__ void __launch_bounds__(kT, 6) k_enc_tiles(GridDev g, const uint16_t* 
     }
 }
 
+// Mixed-precision FMA (sm_100: fma.rn.f32.f16 -> SASS FHFMA): f16 x f16 + f32.
+// The half operands are selected from packed half2 registers (lo / hi).
+__device__ __forceinline__ uint32_t h2bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+#define NVC_FHFMA(NAME, SA, SB)                                                                     \
+    __device__ __forceinline__ float NAME(uint32_t a2, uint32_t b2, float c) {                       \
+        asm("{\n\t.reg .f16 xa, xb, ya, yb;\n\tmov.b32 {xa, ya}, %1;\n\tmov.b32 {xb, yb}, %2;\n\t" \
+            "fma.rn.f32.f16 %0, " SA ", " SB ", %0;\n\t}"                                          \
+            : "+f"(c) : "r"(a2), "r"(b2));                                                          \
+        return c;                                                                                   \
+    }
+NVC_FHFMA(fhfma_lo_lo, "xa", "xb")
+NVC_FHFMA(fhfma_lo_hi, "xa", "yb")
+NVC_FHFMA(fhfma_hi_lo, "ya", "xb")
+NVC_FHFMA(fhfma_hi_hi, "ya", "yb")
+#undef NVC_FHFMA
+
 // Compile-time level count, F == 2: levels unrolled (per-level resolution /
 // dense flag / table offset become constants), FP64 cell + hash exactly as the
-// parity encoder, and the trilinear blend in packed half2 (weights (1-fx, fx)
-// times the yz weight, one HFMA2 per x-neighbour pair).
+// parity encoder, and the trilinear blend with fp16 operands (table entries,
+// corner weights rounded once) and an fp32 accumulator -- the same contract as
+// the tensor-core MLP that consumes the tile; fp16 only on the final store.
 template <int L>
 __global__ void __launch_bounds__(kT, 8) k_enc_tiles2(GridDev g, const uint16_t* __restrict__ table2,
                                                       const double* __restrict__ pos, int64_t P, int kp0,
@@ -259,18 +276,23 @@ __global__ void __launch_bounds__(kT, 8) k_enc_tiles2(GridDev g, const uint16_t*
         __align__(16) __half2 out[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            __half2 acc = __float2half2_rn(0.0f);
+            float a = 0.0f, b = 0.0f;
             if (l0 + j < L) {
-                const __half2 fx2 = __floats2half2_rn(1.0f - w[j][0], w[j][0]);
-                const float wy[2] = {1.0f - w[j][1], w[j][1]}, wz[2] = {1.0f - w[j][2], w[j][2]};
+                const float fx = w[j][0], wy[2] = {1.0f - w[j][1], w[j][1]}, wz[2] = {1.0f - w[j][2], w[j][2]};
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    const __half2 wc = __hmul2(fx2, __float2half2_rn(wy[(c >> 1) & 1] * wz[c & 1]));
-                    acc = __hfma2(__low2half2(wc), *reinterpret_cast<const __half2*>(&v[j][c].x), acc);
-                    acc = __hfma2(__high2half2(wc), *reinterpret_cast<const __half2*>(&v[j][c].y), acc);
+                    const float wyz = wy[(c >> 1) & 1] * wz[c & 1];
+                    // corner weights rounded once to fp16 (the table's precision);
+                    // f16 x f16 products are exact in f32 and accumulate in f32
+                    // (FHFMA: one mixed-precision FMA per product, half selectors)
+                    const uint32_t wc = h2bits(__floats2half2_rn((1.0f - fx) * wyz, fx * wyz));
+                    a = fhfma_lo_lo(wc, v[j][c].x, a);
+                    b = fhfma_lo_hi(wc, v[j][c].x, b);
+                    a = fhfma_hi_lo(wc, v[j][c].y, a);
+                    b = fhfma_hi_hi(wc, v[j][c].y, b);
                 }
             }
-            out[j] = acc;
+            out[j] = __floats2half2_rn(a, b);
         }
         *reinterpret_cast<uint4*>(img + umma_off(row, 2 * l0, kT, kp0)) = *reinterpret_cast<const uint4*>(out);
     }

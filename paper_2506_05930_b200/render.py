@@ -22,13 +22,17 @@ from .scene import camera_struct, device_scene
 
 @dataclass
 class GBuffer:
+    """The reference's G-buffer (render.py:79-100): (h, w[, 3]) host arrays."""
+
     width: int
     height: int
     hit: object
     position: object
     normal: object
     albedo: object
+    depth: object
     light_id: object
+    emissive: object
 
     @property
     def shape(self):
@@ -43,8 +47,10 @@ class GBuffer:
         return a.reshape(self.n_pixels, *a.shape[2:])
 
 
-def gbuffer_device(scene, camera=None, p_first: int = 0, p_count: int | None = None, device=None):
-    """(pos, nrm, alb, hit, light_id) CUDA tensors for pixels [p_first, p_first+p_count)."""
+def gbuffer_device(scene, camera=None, p_first: int = 0, p_count: int | None = None, device=None,
+                   full: bool = False):
+    """(pos, nrm, alb, hit, light_id) CUDA tensors for pixels [p_first, p_first+p_count);
+    with ``full`` also (depth, emissive)."""
     import torch
     camera = camera or scene.camera
     ds = device_scene(scene, device)
@@ -55,30 +61,43 @@ def gbuffer_device(scene, camera=None, p_first: int = 0, p_count: int | None = N
     alb = torch.empty((p, 3), dtype=torch.float64, device=dev)
     hit = torch.empty(p, dtype=torch.uint8, device=dev)
     lid = torch.empty(p, dtype=torch.int32, device=dev)
+    depth = torch.empty(p, dtype=torch.float64, device=dev) if full else None
+    emis = torch.empty((p, 3), dtype=torch.float64, device=dev) if full else None
     _lib.call("nvc_gbuffer", ds.struct, camera_struct(camera), rngmod.stream_key(rngmod.PRIMARY), p_first, p,
-              pos.data_ptr(), nrm.data_ptr(), alb.data_ptr(), hit.data_ptr(), lid.data_ptr(), _lib.stream_ptr())
-    return pos, nrm, alb, hit, lid
+              pos.data_ptr(), nrm.data_ptr(), alb.data_ptr(), hit.data_ptr(), lid.data_ptr(), _lib.ptr(depth),
+              _lib.ptr(emis), _lib.stream_ptr())
+    return (pos, nrm, alb, hit, lid, depth, emis) if full else (pos, nrm, alb, hit, lid)
+
+
+def _gbuffer_host(camera, pos, nrm, alb, hit, lid, depth, emis) -> GBuffer:
+    w, h = camera.width, camera.height
+    pos, nrm, alb, hit, lid, depth, emis = (t.cpu().numpy() for t in (pos, nrm, alb, hit, lid, depth, emis))
+    return GBuffer(w, h, hit.astype(bool).reshape(h, w), pos.reshape(h, w, 3), nrm.reshape(h, w, 3),
+                   alb.reshape(h, w, 3), depth.reshape(h, w), lid.astype(np.int64).reshape(h, w),
+                   emis.reshape(h, w, 3))
 
 
 def make_gbuffer(scene, camera=None) -> GBuffer:
+    """Primary-ray G-buffer (render.py:103-117), bit-identical to the reference."""
     camera = camera or scene.camera
-    w, h = camera.width, camera.height
-    pos, nrm, alb, hit, lid = (t.cpu().numpy() for t in gbuffer_device(scene, camera))
-    return GBuffer(w, h, hit.astype(bool).reshape(h, w), pos.reshape(h, w, 3), nrm.reshape(h, w, 3),
-                   alb.reshape(h, w, 3), lid.reshape(h, w))
+    return _gbuffer_host(camera, *gbuffer_device(scene, camera, full=True))
 
 
-def gbuffer_and_ctx(scene, camera=None, table_dtype=np.float32):
-    """Device PixelCtx over all pixels, memoized on the scene per camera."""
+def gbuffer_and_ctx(scene, camera=None, table_dtype=np.float64):
+    """(G-buffer, PixelCtx over all pixels), memoized on the scene per camera
+    (render.py:128-142).  The G-buffer is host-side like the reference's; the
+    PixelCtx keeps its positions / normals / albedos and its light-major
+    factor and luminance tables on the device (``table_dtype`` float64 is the
+    reference's precision; float32 halves the hot loop's table traffic)."""
     camera = camera or scene.camera
     key = ("gbuf", camera.width, camera.height, tuple(camera.position), tuple(camera.look_at),
            camera.fov_deg, np.dtype(table_dtype).str)
     memo = scene.__dict__.setdefault("_nvc_memo", {})
     if key not in memo:
-        pos, nrm, alb, hit, lid = gbuffer_device(scene, camera)
+        pos, nrm, alb, hit, lid, depth, emis = gbuffer_device(scene, camera, full=True)
         ctx = PixelCtx(scene, pos, nrm, alb, table_dtype=table_dtype)
         ctx.hit, ctx.light_id = hit, lid
-        memo[key] = ctx
+        memo[key] = (_gbuffer_host(camera, pos, nrm, alb, hit, lid, depth, emis), ctx)
     return memo[key]
 
 

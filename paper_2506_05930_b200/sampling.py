@@ -97,10 +97,12 @@ class PixelCtx:
     """Per-pixel shading data resident on the GPU, with lazily built
     light-major (K, P) factor / luminance tables (sampling.py:109-160).
 
-    ``table_dtype`` float32 (default, half the HBM traffic of the hot loop)
-    or float64 (bit-faithful to the reference's FP64 tables)."""
+    ``table_dtype`` float64 (default: the reference's FP64 tables, so light
+    choices are bit-exact given the visibilities) or float32 (half the hot
+    loop's table traffic; the perf path requests it explicitly -- its choice
+    mismatch rate against f64 is measured in tests/test_gpu_headline.py)."""
 
-    def __init__(self, scene, positions, normals, albedos, factors=None, table_dtype=np.float32,
+    def __init__(self, scene, positions, normals, albedos, factors=None, table_dtype=np.float64,
                  device=None):
         torch = _lib.require_cuda()
         self.scene = scene
@@ -132,6 +134,18 @@ class PixelCtx:
         if self._host_pos is None:
             self._host_pos = self.pos.cpu().numpy()
         return self._host_pos
+
+    @property
+    def normals(self) -> np.ndarray:
+        if getattr(self, "_host_nrm", None) is None:
+            self._host_nrm = self.nrm.cpu().numpy()
+        return self._host_nrm
+
+    @property
+    def albedos(self) -> np.ndarray:
+        if getattr(self, "_host_alb", None) is None:
+            self._host_alb = self.alb.cpu().numpy()
+        return self._host_alb
 
     def _build(self, want_lum: bool) -> None:
         import torch
@@ -177,15 +191,34 @@ class PixelCtx:
         return self._masks[which]
 
     def factor_matrix(self) -> np.ndarray:
-        return self.factor_device().T.to(dtype=__import__("torch").float64).cpu().numpy()
+        """(P, K) f64 host copy of the factor table (memoized like the reference's)."""
+        if getattr(self, "_host_fac", None) is None:
+            self._host_fac = self.factor_device().T.to(dtype=__import__("torch").float64).cpu().numpy()
+        return self._host_fac
+
+    @property
+    def _factors(self):
+        """The reference PixelCtx's cached factor matrix (sampling.py:117), read by
+        its ReSTIR/RIS code: the host table once built on the device, else None."""
+        return self.factor_matrix() if self._factor is not None else None
 
     def lum_matrix(self) -> np.ndarray:
-        return self.lum_device().T.to(dtype=__import__("torch").float64).cpu().numpy()
+        """(P, K) f64 host copy of the luminance table (memoized)."""
+        if getattr(self, "_host_lum", None) is None:
+            self._host_lum = self.lum_device().T.to(dtype=__import__("torch").float64).cpu().numpy()
+        return self._host_lum
 
     def phat_ids(self, ids) -> np.ndarray:
+        """Luminance target weight of one light per pixel, id < 0 -> 0
+        (sampling.py:141-155): f * (albedo . LUMA*L_e)/pi with the reference's
+        per-row einsum, f from the device factor table (FP64 restatement of
+        the numba factor kernel, within 1e-10 of it)."""
         ids = np.asarray(ids)
-        lum = self.lum_matrix()
-        return np.where(ids >= 0, np.take_along_axis(lum, np.maximum(ids, 0)[:, None], 1)[:, 0], 0.0)
+        safe = np.maximum(ids, 0)
+        f = np.take_along_axis(self.factor_matrix(), safe[:, None], 1)[:, 0]
+        rad = self.scene.lt_radiance[safe]
+        scale = np.einsum("pc,pc->p", self.albedos, LUMA * rad) / np.pi
+        return np.where(ids >= 0, f * scale, 0.0)
 
     def unshadowed_rgb(self, vis) -> np.ndarray:
         import torch
@@ -193,6 +226,25 @@ class PixelCtx:
         f = self.factor_device().to(torch.float64).T
         rgb = ((v * f) @ self.dscene.lt_radiance) * self.alb / np.pi
         return rgb.cpu().numpy()
+
+
+def as_pixel_ctx(ctx) -> PixelCtx:
+    """This package's PixelCtx for ``ctx``.  A foreign context -- the reference's
+    ``viscache.sampling.PixelCtx`` or any object with ``scene``, ``positions``,
+    ``normals``, ``albedos`` (and optionally precomputed ``_factors``) -- is
+    wrapped once on the device (f64 tables, as the reference's) and the
+    wrapper memoized on it, so a caller that keeps its context per camera
+    (render.py:128-142) uploads it once."""
+    if isinstance(ctx, PixelCtx):
+        return ctx
+    memo = getattr(ctx, "__dict__", {}).get("_nvc_ctx")
+    if memo is not None and memo[0] == ctx.positions.ctypes.data:
+        return memo[1]
+    factors = getattr(ctx, "_factors", None)
+    mine = PixelCtx(ctx.scene, ctx.positions, ctx.normals, ctx.albedos, factors=factors, table_dtype=np.float64)
+    if hasattr(ctx, "__dict__"):
+        ctx.__dict__["_nvc_ctx"] = (ctx.positions.ctypes.data, mine)
+    return mine
 
 
 def _ctx_for(sp: ShadingPoint, scene) -> PixelCtx:
@@ -214,7 +266,29 @@ def _is_native(cache) -> bool:
     return isinstance(cache, VisibilityCache)
 
 
+FACTOR_CACHE_LIMIT = 64_000_000     # render.py:46
+
+
+def _fused(cache) -> bool:
+    """This package's cache on its fp16 tcgen05 query path: the fused
+    encode -> MLP -> selection kernels.  A cache set to PRECISION_FP32 (the
+    parity path) or a foreign cache gives its visibilities first."""
+    from .cache import PRECISION_FP16
+    return _is_native(cache) and cache.precision == PRECISION_FP16
+
+
+def _visibility_device(ctx, cache):
+    """(P, K) f32 CUDA visibilities of ctx's pixels from any cache."""
+    import torch
+    if _is_native(cache):
+        return cache.infer_device(ctx.pos)
+    vis = cache.infer(ctx.positions)
+    vis = vis if isinstance(vis, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(vis, np.float32))
+    return vis.to(ctx.device, torch.float32).contiguous()
+
+
 def nls_weights_batch(ctx: PixelCtx, cache, clamp_floor: float | None = CLAMP_FLOOR) -> np.ndarray:
+    ctx = as_pixel_ctx(ctx)
     vis = np.asarray(cache.infer(ctx.positions), dtype=np.float64)
     vis = clamp_visibility(vis, clamp_floor) if clamp_floor and clamp_floor > 0.0 else np.maximum(vis, 0.0)
     return vis * ctx.lum_matrix()
@@ -229,6 +303,7 @@ def nls_sample_device(ctx: PixelCtx, cache, key: int, offset: int = 0, clamp_flo
     reservoir selection on ``select_stream`` (it can then overlap whatever the
     caller launches next, e.g. the next frame's train step); the outputs are
     ready when ``cache.select_done`` (a CUDA event) completes."""
+    ctx = as_pixel_ctx(ctx)
     import torch
     p = ctx.n
     k = ctx.dscene.n_lights
@@ -241,9 +316,9 @@ def nls_sample_device(ctx: PixelCtx, cache, key: int, offset: int = 0, clamp_flo
     floor = float(clamp_floor) if clamp_floor and clamp_floor > 0.0 else 0.0
     lum = ctx.lum_device()
     lum64 = int(lum.dtype == torch.float64)
-    if _is_native(cache):
-        if cache.output_dim != k:
-            raise ValueError(f"cache has {cache.output_dim} outputs, scene has {k} lights")
+    if _is_native(cache) and cache.output_dim != k:
+        raise ValueError(f"cache has {cache.output_dim} outputs, scene has {k} lights")
+    if _fused(cache):
         ws = cache.query_workspace(p)
         mask = _lib.ptr(ctx.mask_device("lum"))
         if select_stream is None:
@@ -262,10 +337,13 @@ def nls_sample_device(ctx: PixelCtx, cache, key: int, offset: int = 0, clamp_flo
             done = torch.cuda.Event()
             done.record(select_stream)
             cache.select_done = done
+            # the selection reads / writes these on select_stream: keep the caching
+            # allocator from recycling them before it finishes, even if the caller
+            # drops the context or the outputs first
+            for t in (lum, ctx.mask_device("lum"), ws, ids, pts, big_w):
+                t.record_stream(select_stream)
     else:
-        vis = cache.infer(ctx.positions)
-        vis = vis if isinstance(vis, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(vis, np.float32))
-        vis = vis.to(ctx.device, torch.float32).contiguous()
+        vis = _visibility_device(ctx, cache)
         _lib.call("nvc_nls_from_vis", ctx.dscene.struct, vis.data_ptr(), lum.data_ptr(), lum64, lum.shape[1], p,
                   k, p_first, total, key, offset, floor, ids.data_ptr(), pts.data_ptr(), big_w.data_ptr(),
                   _lib.stream_ptr())
@@ -274,6 +352,7 @@ def nls_sample_device(ctx: PixelCtx, cache, key: int, offset: int = 0, clamp_flo
 
 def nls_sample_batch(ctx: PixelCtx, cache, rng, clamp_floor: float | None = CLAMP_FLOOR):
     """Exhaustive-stream WRS over all lights: (light ids, emitter points, W = w_sum/w_sel)."""
+    ctx = as_pixel_ctx(ctx)
     key, off = rngmod.position(rng)
     ids, pts, big_w = nls_sample_device(ctx, cache, key, off, clamp_floor)
     k = ctx.dscene.n_lights
@@ -287,18 +366,21 @@ def nls_sample(sp: ShadingPoint, cache, scene, rng, clamp_floor: float | None = 
 
 
 def neural_di_device(ctx: PixelCtx, cache, out=None):
+    ctx = as_pixel_ctx(ctx)
     import torch
     p = ctx.n
     if out is None:
         out = torch.empty((p, 3), dtype=torch.float64, device=ctx.device)
-    if _is_native(cache):
+    if _fused(cache):
         fac = ctx.factor_device()
         _lib.call("nvc_neural_di", cache.model, ctx.dscene.struct, ctx.pos.data_ptr(), ctx.alb.data_ptr(),
                   fac.data_ptr(), int(fac.dtype == torch.float64), _lib.ptr(ctx.mask_device("factor")),
                   fac.shape[1], p, out.data_ptr(), _lib.ptr(cache.query_workspace(p)), _lib.stream_ptr())
         return out
-    vis = cache.infer(ctx.positions)
-    out.copy_(torch.from_numpy(ctx.unshadowed_rgb(np.asarray(vis, np.float64))))
+    # unshadowed_rgb (sampling.py:157-160) on the device: (v * f) @ L_e * albedo / pi
+    vis = _visibility_device(ctx, cache).to(torch.float64)
+    f = ctx.factor_device().to(torch.float64).T
+    out.copy_(((vis * f) @ ctx.dscene.lt_radiance) * ctx.alb / np.pi)
     return out
 
 
@@ -318,15 +400,11 @@ def neural_di_shade(sp: ShadingPoint, cache, scene) -> np.ndarray:
 def clustered_sample_device(ctx: PixelCtx, cache, clusters, key: int, offset: int = 0,
                             clamp_floor=CLAMP_FLOOR):
     """Device tensors (ids, pts, W) and the number of draws consumed."""
+    ctx = as_pixel_ctx(ctx)
     import torch
     from .training import _cluster_tables
     m = clusters.m
-    if _is_native(cache):
-        vis = cache.infer_device(ctx.pos)
-    else:
-        vis = cache.infer(ctx.positions)
-        vis = vis if isinstance(vis, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(vis, np.float32))
-        vis = vis.to(ctx.device, torch.float32).contiguous()
+    vis = _visibility_device(ctx, cache)
     if vis.shape[1] < m:
         raise ValueError(f"cache has {vis.shape[1]} outputs, the ClusterSet {m} clusters")
     p = ctx.n
@@ -337,9 +415,12 @@ def clustered_sample_device(ctx: PixelCtx, cache, clusters, key: int, offset: in
     ws = torch.empty(lib.nvc_clustered_workspace_bytes(p, m), dtype=torch.uint8, device=ctx.device)
     c_off, c_mem = _cluster_tables(clusters, ctx.device)
     floor = float(clamp_floor) if clamp_floor and clamp_floor > 0.0 else 0.0
-    # an f64 per-camera factor table (PixelCtx(table_dtype=float64)) replaces the
-    # per-(pixel, member) FP64 factor evaluation with one load (same values)
-    fac = ctx.factor_device() if ctx.table_dtype == np.float64 else None
+    # an f64 per-camera factor table replaces the per-(pixel, member) FP64 factor
+    # evaluation with one load (same values); like the reference (render.py:138,
+    # FACTOR_CACHE_LIMIT) it is built only up to 64 M (pixel, light) pairs
+    k = ctx.dscene.n_lights
+    use_table = ctx.table_dtype == np.float64 and (ctx._factor is not None or p * k <= FACTOR_CACHE_LIMIT)
+    fac = ctx.factor_device() if use_table else None
     _lib.call("nvc_clustered_select", ctx.dscene.struct, vis.data_ptr(), vis.shape[1], ctx.pos.data_ptr(),
               ctx.nrm.data_ptr(), ctx.alb.data_ptr(), _lib.ptr(fac), p, m, c_off.data_ptr(), c_mem.data_ptr(), key,
               offset, floor, ids.data_ptr(), pts.data_ptr(), big_w.data_ptr(), ws.data_ptr(), _lib.stream_ptr())

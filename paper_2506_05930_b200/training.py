@@ -20,6 +20,7 @@ import numpy as np
 from . import _lib
 from . import rng as rngmod
 from .cache import MODE_CLUSTERS, MODE_LIGHTS, MODE_RADIANCE
+from .clusters import pack_clusters
 from .scene import camera_struct, device_scene
 
 SCREEN_RETRY_ROUNDS = 8
@@ -64,7 +65,7 @@ def _cluster_tables(clusters, device):
     import torch
     cache = clusters.__dict__.setdefault("_nvc_dev", {})
     if device not in cache:
-        off, flat = clusters.packed()
+        off, flat = pack_clusters(clusters)
         cache[device] = (torch.from_numpy(off).to(device), torch.from_numpy(flat).to(device))
     return cache[device]
 
@@ -305,6 +306,8 @@ def train_frame_device(scene, camera, cache, cfg: TrainFrameConfig, frame: int =
     for step in range(cfg.steps):
         if pipeline is None:
             gen_batch_device(scene, camera, bufs, cfg.seed, frame, step, shard, n_shards, clusters=clusters)
+        if bufs.n_world == 0 and int(bufs.n_rows.item()) == 0:
+            continue    # training.py:196-197: an empty batch (all screen rays missed) skips the update
         ex = None
         if comm is not None:
             ex = pipeline.exchange_for(bufs) if pipeline is not None else None

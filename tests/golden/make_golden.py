@@ -425,12 +425,55 @@ def gen_curves(out: dict, quick: bool) -> None:
                                        for f in range(6)])
 
 
+def gen_long_curves(out: dict) -> None:
+    """Headline-config loss curves (north_star: "the loss curve over N online
+    frames stays within tolerance"): C2 = boxes32, L=16 T=2^19 F=2, MLP 3x64,
+    K=32, 60 online frames (BASELINE configs[1]), run by the reference at
+    float32 and float64 (the f32-vs-f64 spread calibrates the tolerance); C4 =
+    rooms128, 3x128 MLP, K=128, 8 frames at both dtypes.  Also the trained C2
+    cache's visibility on fixed probes (mean-abs compare only: SURVEY 8(c))."""
+    cfg = TrainFrameConfig()
+    s32 = scene_from_dict(boxes_scene(32))
+    g2 = HashGridConfig(levels=16, table_size=1 << 19, features_per_level=2,
+                        aabb_min=s32.aabb_min, aabb_max=s32.aabb_max)
+    probes = R.stream(0, "probes").uniform(s32.aabb_min, s32.aabb_max, (4096, 3))
+    out["c2_probe_pos"] = probes
+    for dt, tag in ((np.float32, "f32"), (np.float64, "f64")):
+        c2 = widened_cache(32, g2, (64, 64, 64), dtype=dt)
+        out["c2_loss60_" + tag] = np.array([train_frame(s32, s32.camera, c2, cfg, frame=f) for f in range(60)])
+        out["c2_probe_vis_" + tag] = c2.infer(probes)
+        print("c2", tag, out["c2_loss60_" + tag][[0, 1, 10, 59]], flush=True)
+    # reference-trained C1 cache (20 frames, f32): its parameters and its own
+    # visibility on fixed probes, so the GPU inference paths can be checked
+    # against the reference at trained scale (not only at init)
+    sp = scene_from_dict(point_light_dict(8))
+    c1 = c1_cache(sp)
+    for f in range(20):
+        train_frame(sp, sp.camera, c1, cfg, frame=f)
+    out["c1t_grid"] = c1.grid_params
+    for i, (w, b) in enumerate(zip(c1.net_params.weights, c1.net_params.biases)):
+        out[f"c1t_w{i}"] = w
+        out[f"c1t_b{i}"] = b
+    p1 = R.stream(0, "probes").uniform(sp.aabb_min, sp.aabb_max, (4096, 3))
+    gb = make_gbuffer(sp, sp.camera)
+    p1 = np.concatenate([p1, gb.flat("position")[gb.flat("hit")]])
+    out["c1t_probe_pos"] = p1
+    out["c1t_probe_vis"] = c1.infer(p1)
+    r128 = scene_from_dict(rooms_scene(128))
+    g4 = HashGridConfig(levels=16, table_size=1 << 19, features_per_level=2,
+                        aabb_min=r128.aabb_min, aabb_max=r128.aabb_max)
+    for dt, tag in ((np.float32, "f32"), (np.float64, "f64")):
+        c4 = widened_cache(128, g4, (128, 128, 128), dtype=dt)
+        out["c4_loss_" + tag] = np.array([train_frame(r128, r128.camera, c4, cfg, frame=f) for f in range(8)])
+        print("c4", tag, out["c4_loss_" + tag], flush=True)
+
+
 def main() -> None:
     quick = "--quick" in sys.argv
     groups = {
         "rng": gen_rng, "scenes": gen_scenes, "mlp": gen_mlp,
         "sampling": gen_sampling, "training": gen_training, "shade": gen_shade, "snapshot": gen_snapshot,
-        "clusters": gen_clusters,
+        "clusters": gen_clusters, "curves": gen_long_curves,
     }
     only = [a for a in sys.argv[1:] if not a.startswith("-")]
     if only:   # regenerate just the named groups, e.g. `make_golden.py shade`

@@ -163,6 +163,15 @@ class TestGeometry:
         np.testing.assert_array_equal(gb.flat("normal"), g_samp["gb_normal"])
         np.testing.assert_array_equal(gb.flat("albedo"), g_samp["gb_albedo"])
         np.testing.assert_array_equal(gb.flat("light_id"), g_samp["gb_light_id"])
+        np.testing.assert_array_equal(gb.flat("depth"), g_samp["gb_depth"])
+        np.testing.assert_array_equal(gb.flat("emissive"), g_samp["gb_emissive"])
+        assert np.isinf(gb.flat("depth")[~gb.flat("hit")]).all()
+        from paper_2506_05930_b200 import gbuffer_and_ctx
+        gb2, ctx = gbuffer_and_ctx(boxes32, cam)             # (gb, ctx) as render.py:128-142
+        assert gbuffer_and_ctx(boxes32, cam)[1] is ctx        # memoized per camera
+        np.testing.assert_array_equal(gb2.flat("emissive"), g_samp["gb_emissive"])
+        np.testing.assert_array_equal(ctx.normals, g_samp["gb_normal"])
+        np.testing.assert_array_equal(ctx.albedos, g_samp["gb_albedo"])
 
     def test_point_gbuffer_and_factors(self, pbox8, g_samp):
         gb = make_gbuffer(pbox8)
