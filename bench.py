@@ -244,6 +244,16 @@ def gpu_arm(args) -> None:
         dist.all_reduce(grad_fx)
         dist.all_reduce(loss)
 
+    if world > 1 and os.environ.get("NVC_SHARD_OPT"):
+        # sharded optimizer: Adam on 1/N of the table per rank + an
+        # all-gather of the updated slices (off by default: at C2 the 67 MB
+        # all-gather costs more than the replicated 121 us Adam it replaces)
+        def gather(buf):
+            out = torch.empty((world, buf.numel()), dtype=buf.dtype, device=buf.device)
+            dist.all_gather_into_tensor(out, buf)
+            return out
+        cache.set_optimizer_shard(rank, world, gather)
+
     stream = torch.cuda.current_stream()
     marks = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
 
@@ -394,22 +404,31 @@ def gpu_arm(args) -> None:
         # roofline of each query kernel: algorithmic work per launch / its event-timed duration
         # (DESIGN.md section 4 gives the per-pixel figures)
         lum_b = np.dtype(lum_dt).itemsize
+        lum_nnz = int(torch.count_nonzero(ctx.lum_device()).item())
         dims = (LEVELS * FEATS,) + tuple(hid) + (kk,)
         flop_px = 2 * sum(a * b for a, b in zip(dims[:-1], dims[1:]))
         kern = {
             "k_enc_tiles2": ("hbm", P * (24 + 64), k_ms[0]),             # pos in, fp16 feature tile out
             "k_mlp_ts": ("tensor", P * flop_px, k_ms[1]),                # 24,576 flop per pixel
-            "k_nls32": ("hbm", P * (2 * kk + lum_b * kk + 4 * ((kk + 31) // 32) + 40), k_ms[2]),   # vis + lum + mask in, id/W/point out
+            # vis row + mask in, id/W/point out per pixel, plus the luminances of the
+            # nonzero (pixel, light) pairs only: zero-weight lights are never read
+            "k_nls32": ("hbm", P * (2 * kk + 4 * ((kk + 31) // 32) + 40) + lum_b * lum_nnz, k_ms[2]),
         }
-        # encoder gathers vs the measured random-gather L2 rate over the same 67 MB table
-        # (profiles/r1_l2_gather_probe.txt, tools/l2_probe.py)
-        enc_gathers = P * LEVELS * 4 / (k_ms[0] * 1e-3) / 1e9
-        probe = None
+        # roofline denominators measured on this GPU in this run (tools/rooflines.py,
+        # libnvc_micro.so): Philox block rate, L2 streaming read, random L2 gathers
         try:
-            with open(os.path.join(ROOT, "profiles", "r1_l2_gather_probe.txt")) as fh:
-                probe = max(float(l.split(":")[1].split("G")[0]) for l in fh if "G gathers/s" in l)
-        except Exception:
-            probe = None
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            import rooflines
+            roof = rooflines.measure(quick=True)
+        except Exception as exc:      # microbenchmarks absent: report without them
+            roof = {"error": str(exc)[:200]}
+        enc_gathers = P * LEVELS * 4 / (k_ms[0] * 1e-3) / 1e9
+        probe = roof.get("l2_gather_G_per_s_67MB")
+        l2_peak = max((v for k, v in roof.items() if k.startswith("l2_stream_GBps")), default=None)
+        # NLS Philox work: one block per nonzero 4-light group + the light-point pair
+        m = ctx.mask_device("lum").view(torch.int32)
+        groups = sum(((m >> (4 * g)) & 15).ne(0).sum().item() for g in range(8)) if kk <= 32 else None
+        nls_blocks = (groups + P) if groups is not None else None
         name = max(kern, key=lambda k: kern[k][2])
         bound, work, kms = kern[name]
         if bound == "tensor":
@@ -442,6 +461,7 @@ def gpu_arm(args) -> None:
                        "l2": (f"inputs > L2 every frame (lum table {P * kk * lum_b / 1e6:.0f} MB "
                               f"{np.dtype(lum_dt).name} + 16.8 M-parameter Adam stream 530 MB)"),
                        "lum_dtype": np.dtype(lum_dt).name,
+                       "lum_nonzero_per_pixel": lum_nnz / P,
                        "host_issue_ms_per_frame": issue_ms,
                        "stage_ms": {"train_frame": tr_ms, "query": q_ms, "k_enc_tiles2": k_ms[0],
                                     "k_mlp_ts": k_ms[1], "k_nls32": k_ms[2],
@@ -457,8 +477,16 @@ def gpu_arm(args) -> None:
                                      "frac": (v[1] / (v[2] * 1e-3) / (1e12 * tflops if v[0] == "tensor" else 1e9 * hbm))}
                                  for k, v in kern.items()},
                          "encoder_l2": {"gathers_G_per_s": enc_gathers, "payload_GBps": enc_gathers * 8,
+                                        "l2_stream_peak_GBps": l2_peak,
+                                        "frac_of_l2_stream": (enc_gathers * 8 / l2_peak) if l2_peak else None,
                                         "random_gather_probe_G_per_s": probe,
-                                        "vs_random_probe": (enc_gathers / probe) if probe else None}},
+                                        "vs_random_probe": (enc_gathers / probe) if probe else None},
+                         "nls_issue": ({"bound": "philox", "blocks_per_launch": nls_blocks,
+                                        "achieved_blocks_per_s": nls_blocks / (k_ms[2] * 1e-3),
+                                        "peak_blocks_per_s": roof["philox_blocks_per_s"],
+                                        "frac": nls_blocks / (k_ms[2] * 1e-3) / roof["philox_blocks_per_s"]}
+                                       if nls_blocks and "philox_blocks_per_s" in roof else None),
+                         "microbench": roof},
             "clocks": clk,
         }
         assert line["roofline"]["unit"] in ("GB/s", "TFLOP/s") and line["roofline"]["bound"] in ("hbm", "tensor")

@@ -28,7 +28,7 @@ extern "C" {
 
 #define NVC_MAX_LEVELS 32
 #define NVC_MAX_LAYERS 8
-#define NVC_ABI_VERSION 8
+#define NVC_ABI_VERSION 9
 
 typedef enum {
     NVC_OK = 0,
@@ -217,6 +217,15 @@ int nvc_exchange_unpack(const nvc_model *m, const int32_t *idx, const int64_t *c
  * wpack.  t is the post-increment Adam step (>= 1), lr from lr_at (mlp.py:76).
  * grad_fx may hold a data-parallel allreduced sum. */
 int nvc_adam_step(const nvc_model *m, int64_t t, double lr, void *stream);
+/* Sharded optimizer for data parallelism: the same update on
+ * the hash-table parameters [lo, hi) of shard `shard` of n_shards only (whole
+ * Adam tiles; nvc_adam_shard_range gives the range), the MLP on every shard;
+ * the other shards' gradients are cleared.  The caller then all-gathers the
+ * table parameters and calls nvc_refresh_shadow.  Dense gradients, F == 2.
+ * nvc_adam_step == shard 0 of 1. */
+int nvc_adam_step_shard(const nvc_model *m, int64_t t, double lr, int32_t shard, int32_t n_shards,
+                        void *stream);
+int nvc_adam_shard_range(const nvc_model *m, int32_t shard, int32_t n_shards, int64_t *lo, int64_t *hi);
 
 /* ---- light selection: sampling.py:74-85, 184-218 ---------------------- */
 /* wrs_select_batch: weights (p, k) f64; draw for (row r, light j) is

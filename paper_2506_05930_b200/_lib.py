@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libnvc.so")
 
 MAX_LEVELS = 32
 MAX_LAYERS = 8
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 c_i32, c_i64, c_u64, c_f64, c_f32, c_vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
                                            ctypes.c_double, ctypes.c_float, ctypes.c_void_p)
@@ -76,6 +76,8 @@ _SIGS = {
     "nvc_train_grads": (c_i32, [P(NvcModel), c_vp, c_vp, c_vp, c_i64, c_vp, c_i32, c_i32,
                                 c_vp, c_vp, c_vp]),
     "nvc_adam_step": (c_i32, [P(NvcModel), c_i64, c_f64, c_vp]),
+    "nvc_adam_step_shard": (c_i32, [P(NvcModel), c_i64, c_f64, c_i32, c_i32, c_vp]),
+    "nvc_adam_shard_range": (c_i32, [P(NvcModel), c_i32, c_i32, P(c_i64), P(c_i64)]),
     "nvc_exchange_max_entries": (c_i64, [P(NvcModel), c_i64]),
     "nvc_touch_words": (c_i64, [P(NvcModel)]),
     "nvc_touch_off_len": (c_i64, [P(NvcModel)]),
@@ -129,6 +131,25 @@ class NvcError(RuntimeError):
 
 class NvcUnsupported(NvcError):
     """A valid configuration the requested kernel does not cover (NVC_ERR_UNSUPPORTED)."""
+
+
+def load_micro() -> ctypes.CDLL:
+    """libnvc_micro.so (microbenchmarks; tools and bench rooflines only)."""
+    p = os.path.join(os.path.dirname(LIB_PATH), "libnvc_micro.so")
+    if not os.path.exists(p):
+        raise ImportError(f"{p} is missing: python -m paper_2506_05930_b200.build")
+    lib = ctypes.CDLL(p)
+    c_vp, c_i32, c_i64, c_u32, c_u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64
+    for name, args in {"nvc_micro": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vp, c_vp],
+                       "nvc_encode_probe": [ctypes.POINTER(NvcModel), c_vp, c_i64, c_vp, c_vp],
+                       "nvc_l2_gather_probe": [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp],
+                       "nvc_philox_rate": [c_i32, c_i32, c_i32, c_u64, c_vp, c_vp],
+                       "nvc_philox_check": [c_u64, c_u32, c_u32, c_vp, c_vp],
+                       "nvc_l2_stream": [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp]}.items():
+        fn = getattr(lib, name)
+        fn.restype = c_i32
+        fn.argtypes = args
+    return lib
 
 
 def load(path: str | None = None) -> ctypes.CDLL:

@@ -19,7 +19,8 @@ OUT = os.path.join(HERE, "libnvc.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
                  "-I", os.path.join(HERE, "..", "include")]
-UNITS = {"geometry.cu": ["-fmad=false"], "model.cu": [], "query.cu": [], "pipeline.cu": [], "micro.cu": []}
+UNITS = {"geometry.cu": ["-fmad=false"], "model.cu": [], "query.cu": [], "pipeline.cu": []}
+MICRO_OUT = os.path.join(HERE, "libnvc_micro.so")     # microbenchmarks (tools/, bench rooflines)
 
 
 def nvcc() -> str:
@@ -51,5 +52,18 @@ def build(verbose: bool = False, force: bool = False, defs: list[str] | None = N
     return out
 
 
+def build_micro(force: bool = False, out: str = MICRO_OUT) -> str:
+    """libnvc_micro.so: csrc/micro.cu alone (roofline-denominator microbenchmarks)."""
+    src = os.path.join(CSRC, "micro.cu")
+    deps = [src, os.path.join(CSRC, "common.cuh"), os.path.join(HERE, "..", "include", "nvc.h")]
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(d) for d in deps):
+        return out
+    tmp = out + ".tmp"
+    subprocess.check_call([nvcc(), *COMMON, "-DNVC_MICRO_STANDALONE", "-shared", "-cudart", "static", src, "-o", tmp])
+    os.replace(tmp, out)
+    return out
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv, force=True))
+    print(build_micro(force=True))

@@ -172,6 +172,7 @@ class VisibilityCache:
         self._mirror = None       # host copy of `params` behind grid_params / net_params views
         self._handouts = []       # weakrefs to views a caller may still write into
         self._dirty = False       # views handed out since the last upload
+        self._opt_shard = None    # sharded optimizer (set_optimizer_shard)
         self._ws = None
         self._qws = None
         self.select_done = None   # CUDA event: last off-stream NLS selection finished
@@ -394,9 +395,48 @@ class VisibilityCache:
     def apply_adam(self) -> None:
         lr = lr_at(self.step, self.train_cfg)
         self.adam_t += 1
-        _lib.call("nvc_adam_step", self.model, self.adam_t, lr, _lib.stream_ptr())
+        sh = self._opt_shard
+        if sh is None:
+            _lib.call("nvc_adam_step", self.model, self.adam_t, lr, _lib.stream_ptr())
+        else:
+            # sharded optimizer: this rank updates its slice of the table (+ the MLP),
+            # then the slices are all-gathered and the fp16 query table rebuilt
+            shard, n, gather, lo, hi, buf = sh
+            _lib.call("nvc_adam_step_shard", self.model, self.adam_t, lr, shard, n, _lib.stream_ptr())
+            buf[:hi - lo].copy_(self.params[lo:hi])
+            gathered = gather(buf)                     # (n, span) in rank order
+            for r in range(n):
+                rlo, rhi = self._opt_ranges[r]
+                self.params[rlo:rhi].copy_(gathered[r, :rhi - rlo])
+            self.refresh_shadow()
         self.step += 1
         self._pull_views()
+
+    def _adam_range(self, shard: int, n_shards: int):
+        """[lo, hi) of the table parameters shard `shard` of n_shards updates."""
+        lo, hi = _lib.ctypes.c_int64(), _lib.ctypes.c_int64()
+        _lib.call("nvc_adam_shard_range", self.model, shard, n_shards, _lib.ctypes.byref(lo), _lib.ctypes.byref(hi))
+        return lo.value, hi.value
+
+    def set_optimizer_shard(self, shard: int, n_shards: int, all_gather=None) -> None:
+        """Shard the optimizer over data-parallel ranks: each rank runs
+        Adam on 1/n_shards of the hash-table parameters (its m/v slices are the only
+        ones it keeps current) and ``all_gather(buf) -> (n_shards, len(buf))``
+        collects the updated slices (e.g. torch.distributed.all_gather_into_tensor).
+        The gradients must be the allreduced sum (GradExchange, dense mode).  The
+        result is bit-identical to the replicated update; n_shards == 1 turns it off."""
+        import torch
+        if n_shards <= 1:
+            self._opt_shard = None
+            return
+        if self.compact:
+            raise ValueError("the sharded optimizer needs dense gradients (set_compact(False))")
+        ranges = [self._adam_range(r, n_shards) for r in range(n_shards)]
+        self._opt_ranges = ranges
+        self._opt_span = max(h - l for l, h in ranges)
+        lo, hi = ranges[shard]
+        buf = torch.zeros(self._opt_span, dtype=torch.float32, device=self.device)
+        self._opt_shard = (shard, n_shards, all_gather, lo, hi, buf)
 
     def _bind_compact(self, b_max: int) -> None:
         """(Re)allocate the compact-gradient buffers for batches of up to b_max rows."""

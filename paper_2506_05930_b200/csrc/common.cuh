@@ -66,6 +66,61 @@ __device__ __forceinline__ U4 philox_block(uint64_t counter, uint64_t key) {
     return o;
 }
 
+// The same block when the counter fits in 32 bits (every stream position below
+// 2^34 draws: all per-frame streams here) -- the first two rounds simplify
+// because the counter words c1..c3 start at zero and the key words are known:
+//   round 0: M0*c0 is a 64x32 product and M1*c2 = 0, so the state becomes
+//            (key, 0, hi(M0*c0), lo(M0*c0));
+//   round 1: M0*c0 = M0*key is a per-stream constant (PhiloxKey, once per thread).
+// 1.5 of the 20 64x64->128 multiplies instead of 4 in those rounds.  Measured
+// (tools/rooflines.py): the same block rate as philox_block once the compiler
+// sees a 32-bit counter (it folds the zero words itself), so the kernels keep
+// philox_block; this form is the microbenchmark's cross-check.
+struct PhiloxKey {
+    uint64_t key, mk_hi, mk_lo;   // mk = 0xD2E7470EE14C6C93 * key (128-bit)
+};
+
+__device__ __forceinline__ PhiloxKey philox_key(uint64_t key) {
+    PhiloxKey k;
+    k.key = key;
+    k.mk_hi = __umul64hi(0xD2E7470EE14C6C93ull, key);
+    k.mk_lo = 0xD2E7470EE14C6C93ull * key;
+    return k;
+}
+
+__device__ __forceinline__ U4 philox_block32(uint32_t counter, const PhiloxKey& pk) {
+    // round 0 (k0 = key, k1 = 0)
+    const uint64_t p0 = 0xD2E7470EE14C6C93ull * (uint64_t)counter;            // lo(M0*c0)
+    const uint64_t h0 = __umul64hi(0xD2E7470EE14C6C93ull, (uint64_t)counter);  // hi(M0*c0)
+    // round 1 (k0 = key + W0, k1 = W1): c = (key, 0, h0, p0)
+    const uint64_t hi1 = __umul64hi(0xCA5A826395121157ull, h0);
+    const uint64_t lo1 = 0xCA5A826395121157ull * h0;
+    uint64_t c0 = hi1 ^ (pk.key + 0x9E3779B97F4A7C15ull);
+    uint64_t c1 = lo1;
+    uint64_t c2 = pk.mk_hi ^ p0 ^ 0xBB67AE8584CAA73Bull;
+    uint64_t c3 = pk.mk_lo;
+    uint64_t k0 = pk.key + 0x9E3779B97F4A7C15ull, k1 = 0xBB67AE8584CAA73Bull;
+#pragma unroll
+    for (int r = 2; r < 10; ++r) {
+        k0 += 0x9E3779B97F4A7C15ull;
+        k1 += 0xBB67AE8584CAA73Bull;
+        const uint64_t a_hi = __umul64hi(0xD2E7470EE14C6C93ull, c0);
+        const uint64_t a_lo = 0xD2E7470EE14C6C93ull * c0;
+        const uint64_t b_hi = __umul64hi(0xCA5A826395121157ull, c2);
+        const uint64_t b_lo = 0xCA5A826395121157ull * c2;
+        c0 = b_hi ^ c1 ^ k0;
+        c1 = b_lo;
+        c2 = a_hi ^ c3 ^ k1;
+        c3 = a_lo;
+    }
+    U4 o;
+    o.x[0] = c0;
+    o.x[1] = c1;
+    o.x[2] = c2;
+    o.x[3] = c3;
+    return o;
+}
+
 // numpy Generator.random(): (x >> 11) * 2^-53 (exact in binary64)
 __device__ __forceinline__ double u01(uint64_t x) { return (double)(x >> 11) * 0x1.0p-53; }
 

@@ -1,7 +1,32 @@
-// micro.cu -- tcgen05 microbenchmarks used to calibrate the query kernel
-// (MMA issue/throughput, commit->mbarrier round trip, TMEM load latency).
-// Profiling aid only; not on the product path.
+// micro.cu -- microbenchmarks that calibrate the kernels' roofline denominators:
+// tcgen05 MMA issue / commit round trip / TMEM load latency, the L2 gather and
+// L2 streaming-read rates over the encoder's footprint, and the Philox4x64-10
+// block rate (the NLS kernel's integer-issue ceiling).  Built as its own
+// library, libnvc_micro.so (build.py build_micro); not part of libnvc.so.
 #include "common.cuh"
+
+#ifdef NVC_MICRO_STANDALONE
+#include <cstdarg>
+#include <cstdio>
+namespace nvc {
+static thread_local char g_micro_err[256];
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_micro_err, sizeof g_micro_err, fmt, ap);
+    va_end(ap);
+}
+int check_launch(const char* what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("%s: %s", what, cudaGetErrorString(e));
+        return NVC_ERR_CUDA;
+    }
+    return NVC_OK;
+}
+}  // namespace nvc
+extern "C" const char* nvc_micro_last_error(void) { return nvc::g_micro_err; }
+#endif
 
 namespace nvc {
 namespace {
@@ -212,4 +237,66 @@ extern "C" int nvc_l2_gather_probe(const void* table, int64_t entries, int32_t g
     nvc::k_l2_gather_probe<<<grid, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const uint2*>(table), mask - 1,
                                                                    iters, (unsigned long long*)sink);
     return nvc::check_launch("k_l2_gather_probe");
+}
+
+// ---- Philox4x64-10 block rate: every thread generates `iters` consecutive
+// blocks of one stream (generic 64-bit-counter form, or the 32-bit-counter form
+// the NLS kernel uses) and folds them, so the loop is the block arithmetic alone.
+namespace nvc {
+namespace {
+template <bool kC32>
+__global__ void __launch_bounds__(256) k_philox_rate(uint64_t key, int iters, unsigned long long* __restrict__ sink) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    const PhiloxKey pk = philox_key(key);
+    uint64_t acc = 0;
+    for (int i = 0; i < iters; ++i) {
+        const uint32_t ctr = t * (uint32_t)iters + (uint32_t)i + 1u;
+        const U4 u = kC32 ? philox_block32(ctr, pk) : philox_block((uint64_t)ctr, key);
+        acc += u.x[0] ^ u.x[1] ^ u.x[2] ^ u.x[3];
+    }
+    if (acc == 0x9E3779B97F4A7C15ull) sink[0] = acc;
+}
+
+// both forms on the same counters: count the blocks that differ (must be 0)
+__global__ void k_philox_check(uint64_t key, uint32_t n, uint32_t first, unsigned long long* __restrict__ bad) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t ctr = first + i;
+    const U4 a = philox_block((uint64_t)ctr, key), b = philox_block32(ctr, philox_key(key));
+    if (a.x[0] != b.x[0] || a.x[1] != b.x[1] || a.x[2] != b.x[2] || a.x[3] != b.x[3]) atomicAdd(bad, 1ull);
+}
+
+// L2 streaming read: each thread reads 16-byte words of an L2-resident buffer in
+// a grid-stride sweep, `passes` times over.
+__global__ void __launch_bounds__(256) k_l2_stream(const uint4* __restrict__ buf, int64_t n16, int passes,
+                                                   unsigned long long* __restrict__ sink) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    uint32_t acc = 0;
+    for (int r = 0; r < passes; ++r)
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) {
+            const uint4 v = __ldcg(buf + i);
+            acc ^= v.x ^ v.y ^ v.z ^ v.w;
+        }
+    if (acc == 0x9e3779b9u) sink[0] = acc;
+}
+}  // namespace
+}  // namespace nvc
+
+extern "C" int nvc_philox_rate(int32_t c32, int32_t grid, int32_t iters, uint64_t key, void* sink, void* stream) {
+    if (c32)
+        nvc::k_philox_rate<true><<<grid, 256, 0, (cudaStream_t)stream>>>(key, iters, (unsigned long long*)sink);
+    else
+        nvc::k_philox_rate<false><<<grid, 256, 0, (cudaStream_t)stream>>>(key, iters, (unsigned long long*)sink);
+    return nvc::check_launch("k_philox_rate");
+}
+
+extern "C" int nvc_philox_check(uint64_t key, uint32_t n, uint32_t first, void* bad, void* stream) {
+    nvc::k_philox_check<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(key, n, first, (unsigned long long*)bad);
+    return nvc::check_launch("k_philox_check");
+}
+
+extern "C" int nvc_l2_stream(const void* buf, int64_t bytes, int32_t grid, int32_t passes, void* sink, void* stream) {
+    nvc::k_l2_stream<<<grid, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const uint4*>(buf), bytes / 16, passes,
+                                                             (unsigned long long*)sink);
+    return nvc::check_launch("k_l2_stream");
 }

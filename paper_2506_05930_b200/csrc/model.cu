@@ -828,28 +828,32 @@ __global__ void __launch_bounds__(256) k_reduce_parts(const float* __restrict__ 
                                                       int64_t mlp_count, int64_t grid_count,
                                                       GradSink gs, double* __restrict__ loss_out,
                                                       int64_t b_max, const int64_t* __restrict__ b_dev) {
-    __shared__ double s_acc[8][32];
+    // Each 32-row block's partial is rounded to fixed point on its own and the
+    // blocks are summed as integers: the MLP gradient then depends only on which
+    // rows form each block, not on how blocks are split over data-parallel ranks
+    // (shards aligned to 32 rows reproduce the full batch bit for bit).
+    __shared__ long long s_acc[8][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t j = (int64_t)blockIdx.x * 32 + lane;
-    double acc = 0.0;
+    long long acc = 0;
     if (j < mlp_count) {
-        // same sequential order; loads batched so eight are in flight per thread
+        // loads batched so eight are in flight per thread
         int b = w;
         for (; b + 56 < nblk; b += 64) {
             float v[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) v[u] = __ldg(part_w + (int64_t)(b + 8 * u) * mlp_count + j);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) acc += (double)v[u];
+            for (int u = 0; u < 8; ++u) acc += to_fx((double)v[u]);
         }
-        for (; b < nblk; b += 8) acc += (double)__ldg(part_w + (int64_t)b * mlp_count + j);
+        for (; b < nblk; b += 8) acc += to_fx((double)__ldg(part_w + (int64_t)b * mlp_count + j));
     }
     s_acc[w][lane] = acc;
     __syncthreads();
     if (w == 0 && j < mlp_count) {
-        double t = 0.0;
+        long long t = 0;
         for (int i = 0; i < 8; ++i) t += s_acc[i][lane];
-        *mlp_grad(gs, j) += to_fx(t);
+        *mlp_grad(gs, j) += t;
     }
     if (blockIdx.x == 0 && w == 1 && loss_out) {
         double t = 0.0;
@@ -974,14 +978,14 @@ template <bool kCompact>
 __global__ void __launch_bounds__(kAdamThreads) k_adam_bulk(float* __restrict__ p, float* __restrict__ m,
                                                            float* __restrict__ v, GradSink gs,
                                                            uint16_t* __restrict__ table_h, int64_t ntiles, AdamK a,
-                                                           int64_t T) {
+                                                           int64_t T, int64_t tile0) {
     int64_t* __restrict__ fx = gs.dense;
     extern __shared__ __align__(128) uint8_t adam_smem[];
     AdamStage* st = reinterpret_cast<AdamStage*>(adam_smem);
     __shared__ uint64_t full[kAdamStages];
     const int tid = threadIdx.x, lane = tid & 31;
     const int n_local = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
-    auto tile_base = [&](int i) { return (blockIdx.x + (int64_t)i * gridDim.x) * kAdamTile; };
+    auto tile_base = [&](int i) { return (tile0 + blockIdx.x + (int64_t)i * gridDim.x) * kAdamTile; };
     auto issue = [&](int i) {
         const int s = i % kAdamStages;
         const int64_t base = tile_base(i);
@@ -1426,9 +1430,27 @@ int nvc_exchange_unpack(const nvc_model* m, const int32_t* idx, const int64_t* c
 }
 
 int nvc_adam_step(const nvc_model* m, int64_t t, double lr, void* stream) {
+    return nvc_adam_step_shard(m, t, lr, 0, 1, stream);
+}
+
+int nvc_adam_shard_range(const nvc_model* m, int32_t shard, int32_t n_shards, int64_t* lo, int64_t* hi) {
+    int rc = validate(m);
+    if (rc) return rc;
+    NVC_REQUIRE(lo && hi && n_shards >= 1 && shard >= 0 && shard < n_shards, "nvc_adam_shard_range: bad shard");
+    const Net net = net_of(m);
+    NVC_REQUIRE(m->features == 2 && m->table_size % 64 == 0 && net.grid_count % kAdamTile == 0,
+                "nvc_adam_shard_range: the sharded optimizer needs F == 2 and whole Adam tiles");
+    const int64_t ntiles = net.grid_count / kAdamTile;
+    *lo = ntiles * shard / n_shards * kAdamTile;
+    *hi = ntiles * (shard + 1) / n_shards * kAdamTile;
+    return NVC_OK;
+}
+
+int nvc_adam_step_shard(const nvc_model* m, int64_t t, double lr, int32_t shard, int32_t n_shards, void* stream) {
     int rc = validate(m);
     if (rc) return rc;
     NVC_REQUIRE(t >= 1, "nvc_adam_step: t must be >= 1");
+    NVC_REQUIRE(n_shards >= 1 && shard >= 0 && shard < n_shards, "nvc_adam_step_shard: bad shard");
     NVC_REQUIRE(m->adam_m && m->adam_v && (m->grad_fx || m->grad_c) && m->table_h && m->wpack,
                 "nvc_adam_step: state not bound");
     Net net = net_of(m);
@@ -1444,24 +1466,36 @@ int nvc_adam_step(const nvc_model* m, int64_t t, double lr, void* stream) {
     a.inv_b1c = 1.0 / (double)a.b1c;
     a.inv_b2c = 1.0 / (double)a.b2c;
     cudaStream_t s = (cudaStream_t)stream;
-    if (m->features == 2 && m->table_size % 64 == 0 && net.grid_count % kAdamTile == 0 && !getenv("NVC_ADAM_FLAT")) {
+    const bool bulk = m->features == 2 && m->table_size % 64 == 0 && net.grid_count % kAdamTile == 0;
+    NVC_REQUIRE(n_shards == 1 || (bulk && !m->grad_c),
+                "nvc_adam_step_shard: the sharded optimizer needs F == 2, whole Adam tiles and dense gradients");
+    if (bulk && (n_shards > 1 || !getenv("NVC_ADAM_FLAT"))) {
         const int smem = kAdamStages * (int)sizeof(AdamStage);
         cudaFuncSetAttribute(k_adam_bulk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(k_adam_bulk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int dev = 0, sms = kNumSMs;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int64_t ntiles = net.grid_count / kAdamTile;
+        const int64_t all_tiles = net.grid_count / kAdamTile;
+        const int64_t tile0 = all_tiles * shard / n_shards, ntiles = all_tiles * (shard + 1) / n_shards - tile0;
+        if (n_shards > 1) {   // the other shards' (allreduced) gradients are consumed by their owners
+            if (tile0 > 0) cudaMemsetAsync(m->grad_fx, 0, (size_t)(tile0 * kAdamTile) * 8, s);
+            const int64_t end = (tile0 + ntiles) * kAdamTile;
+            if (end < net.grid_count)
+                cudaMemsetAsync(m->grad_fx + end, 0, (size_t)(net.grid_count - end) * 8, s);
+        }
         // CTAs per SM (default 2: 2 x 61 KB smem rings still stream at HBM rate and
         // leave each SM room for the previous frame's NLS blocks running beside it)
         const char* ge = getenv("NVC_ADAM_GRID");
         const int grid = (int)std::min<int64_t>(ntiles, (ge ? atoi(ge) : 2) * (int64_t)sms);
-        if (m->grad_c)
-            k_adam_bulk<true><<<grid, kAdamThreads, smem, s>>>(m->params, m->adam_m, m->adam_v, sink_of(m), m->table_h,
-                                                               ntiles, a, m->table_size);
-        else
-            k_adam_bulk<false><<<grid, kAdamThreads, smem, s>>>(m->params, m->adam_m, m->adam_v, sink_of(m),
-                                                                m->table_h, ntiles, a, m->table_size);
+        if (ntiles > 0) {
+            if (m->grad_c)
+                k_adam_bulk<true><<<grid, kAdamThreads, smem, s>>>(m->params, m->adam_m, m->adam_v, sink_of(m),
+                                                                   m->table_h, ntiles, a, m->table_size, tile0);
+            else
+                k_adam_bulk<false><<<grid, kAdamThreads, smem, s>>>(m->params, m->adam_m, m->adam_v, sink_of(m),
+                                                                    m->table_h, ntiles, a, m->table_size, tile0);
+        }
     } else {
         k_adam_flat<<<grid1(net.grid_count, 256), 256, 0, s>>>(m->params, m->adam_m, m->adam_v, sink_of(m),
                                                                m->table_h, net.grid_count, m->features, a,

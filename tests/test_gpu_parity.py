@@ -756,9 +756,9 @@ class TestTraining:
             parts.accumulate_grads(pos, tgt[lo:hi].contiguous(), b_max=b, shard=sh, n_shards=4)
         gc = full.grid_cfg.param_count
         np.testing.assert_array_equal(full.grad_fx[:gc].cpu().numpy(), parts.grad_fx[:gc].cpu().numpy())
-        a = full.grad_fx[gc:].double().cpu().numpy()
-        bb = parts.grad_fx[gc:].double().cpu().numpy()
-        np.testing.assert_allclose(a, bb, rtol=1e-5, atol=2.0 ** 48 * 1e-9)
+        # 4 shards of 8192 rows are 32-row aligned: per-block fixed point makes the
+        # MLP gradient shard-exact too
+        np.testing.assert_array_equal(full.grad_fx[gc:].cpu().numpy(), parts.grad_fx[gc:].cpu().numpy())
 
 
 def test_odd_light_count_mixed_emitters():

@@ -9,9 +9,7 @@ import torch  # noqa: E402
 
 from paper_2506_05930_b200 import _lib  # noqa: E402
 
-lib = _lib.load()
-lib.nvc_l2_gather_probe.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
-                                    ctypes.c_void_p]
+lib = _lib.load_micro()
 entries = 16 * (1 << 19) * 2          # x-pair slots of the C2 table (8 B each, 67 MB)
 table = torch.randint(0, 1 << 30, (entries * 2,), dtype=torch.int32, device="cuda")
 sink = torch.zeros(1, dtype=torch.int64, device="cuda")

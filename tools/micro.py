@@ -3,8 +3,7 @@ import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2506_05930_b200 import _lib
-lib = _lib.load()
-lib.nvc_micro.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+lib = _lib.load_micro()
 out = torch.zeros(1024, dtype=torch.int64, device="cuda")
 def run(mode, iters, n, blocks):
     lib.nvc_micro(mode, iters, n, blocks, out.data_ptr(), None); torch.cuda.synchronize()

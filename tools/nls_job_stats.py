@@ -23,6 +23,8 @@ for name, sc in (("boxes32", boxes_scene(32)), ("rooms128", rooms_scene(128))):
     print(name, "mean jobs/pixel", jobs.mean(), "warp max mean", warp.max(1).mean(),
           "balanced ceil", np.ceil(warp.sum(1) / 32).mean(), "ratio", warp.max(1).mean() / np.ceil(warp.sum(1) / 32).mean())
 
+if "--reverse" not in sys.argv:
+    sys.exit(0)
 # Reverse-scan estimate: the WRS selection is the LAST light with u*s_k < w_k, so a
 # scan from the top group down could stop at the selected light's group.  Blocks a
 # reverse scan would need = nonzero groups at or above the selected group (+1 pair).
