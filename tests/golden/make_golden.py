@@ -468,12 +468,68 @@ def gen_long_curves(out: dict) -> None:
         print("c4", tag, out["c4_loss_" + tag], flush=True)
 
 
+class WaveCache:
+    """Deterministic stand-in cache (the reference's FixedCache pattern,
+    test_sampling.py:21-30): visibility = 0.5 + 0.4 sin(a . pos + j)."""
+    mode = MODE_LIGHTS
+
+    def __init__(self, k):
+        self.output_dim = k
+
+    def infer(self, positions):
+        pos = np.atleast_2d(np.asarray(positions, np.float64))
+        ph = pos @ np.array([1.3, 2.1, 0.7])
+        return (0.5 + 0.4 * np.sin(ph[:, None] + np.arange(self.output_dim))).astype(np.float32)
+
+
+def gen_scalar(out: dict) -> None:
+    """Scalar API wrappers (sampling.py:88-101,141-176,208-222): wrs_select,
+    nls_sample, neural_di_shade, unshadowed_weight, unshadowed_rgb_one and
+    PixelCtx.phat_ids on 48 shading points of boxes8 (rect lights) and 16 of
+    the point-light C1 scene."""
+    from viscache.sampling import (ShadingPoint, neural_di_shade, nls_sample, unshadowed_rgb_one,
+                                   unshadowed_weight, wrs_select)
+    g = np.random.default_rng(21)
+    rows = []
+    for tag, sc, n in (("b8", scene_from_dict(boxes_scene(8)), 48), ("p8", scene_from_dict(point_light_dict(8)), 16)):
+        cam = Camera(position=sc.camera.position, look_at=sc.camera.look_at, up=sc.camera.up,
+                     fov_deg=sc.camera.fov_deg, width=40, height=24)
+        gb = make_gbuffer(sc, cam)
+        hit = np.flatnonzero(gb.flat("hit"))
+        pick = hit[g.choice(hit.size, n, replace=False)]
+        pos, nrm, alb = (gb.flat(k)[pick] for k in ("position", "normal", "albedo"))
+        out[f"sc_{tag}_pos"], out[f"sc_{tag}_nrm"], out[f"sc_{tag}_alb"] = pos, nrm, alb
+        k = sc.n_lights
+        cache = WaveCache(k)
+        wts = g.random((n, 6)) * (g.random((n, 6)) < 0.7)
+        out[f"sc_{tag}_wrs_w"] = wts
+        res, nls, ndi, uw, urgb = [], [], [], [], []
+        for i in range(n):
+            sp = ShadingPoint(position=pos[i], normal=nrm[i], albedo=alb[i])
+            r = wrs_select(wts[i], R.stream(0, i, "wrs-scalar"))
+            res.append([r.y, r.w_y, r.w_sum, r.M, r.W])
+            lid, pt, big_w = nls_sample(sp, cache, sc, R.stream(1, i, "light-select"))
+            nls.append([lid, *pt, big_w])
+            ndi.append(neural_di_shade(sp, cache, sc))
+            uw.append([unshadowed_weight(sp, j, sc) for j in range(k)])
+            urgb.append([unshadowed_rgb_one(sp, j, sc) for j in range(k)])
+        out[f"sc_{tag}_wrs"] = np.array(res, float)
+        out[f"sc_{tag}_nls"] = np.array(nls, float)
+        out[f"sc_{tag}_ndi"] = np.array(ndi)
+        out[f"sc_{tag}_uw"] = np.array(uw)
+        out[f"sc_{tag}_urgb"] = np.array(urgb)
+        ctx = PixelCtx(sc, pos, nrm, alb)
+        ids = g.integers(-1, k, n)
+        out[f"sc_{tag}_phat_ids"] = ids
+        out[f"sc_{tag}_phat"] = ctx.phat_ids(ids)
+
+
 def main() -> None:
     quick = "--quick" in sys.argv
     groups = {
         "rng": gen_rng, "scenes": gen_scenes, "mlp": gen_mlp,
         "sampling": gen_sampling, "training": gen_training, "shade": gen_shade, "snapshot": gen_snapshot,
-        "clusters": gen_clusters, "curves": gen_long_curves,
+        "clusters": gen_clusters, "curves": gen_long_curves, "scalar": gen_scalar,
     }
     only = [a for a in sys.argv[1:] if not a.startswith("-")]
     if only:   # regenerate just the named groups, e.g. `make_golden.py shade`
