@@ -28,7 +28,7 @@ extern "C" {
 
 #define NVC_MAX_LEVELS 32
 #define NVC_MAX_LAYERS 8
-#define NVC_ABI_VERSION 9
+#define NVC_ABI_VERSION 10
 
 typedef enum {
     NVC_OK = 0,
@@ -273,6 +273,37 @@ int nvc_neural_di(const nvc_model *m, const nvc_scene *sc, const double *pos,
  * (exact: they add 0 to the reservoir sum and are never selected). */
 int nvc_table_mask(const void *table, int32_t f64, int64_t p_stride, int64_t p, int32_t k,
                    uint32_t *mask, void *stream);
+
+/* ---- RIS / screen-space ReSTIR baselines: sampling.py:369-637 ---------- */
+/* A reservoir grid (ReservoirGrid, sampling.py:369-402), struct of arrays on
+ * the device: y (p) i64, point (p,3) f64, w_y/w_sum/M/W (p) f64, valid (p) u8. */
+typedef struct nvc_rgrid {
+    int64_t *y;
+    double *point, *w_y, *w_sum, *M, *W;
+    uint8_t *valid;
+} nvc_rgrid;
+/* ris_initial_batch (:405-432): m_cand candidates per pixel from
+ * integers(0, K) (Lemire, rejections and the kept 32-bit half exact; kept_in
+ * -1: none), phat from the light-major luminance table, streaming WRS, light
+ * points.  state_dev (2 int64, device): the stream's next 64-bit output and
+ * kept half after the call.  ws: nvc_ris_workspace_bytes. */
+int64_t nvc_ris_workspace_bytes(int64_t p, int32_t m_cand, int32_t k);
+int nvc_ris_initial(const nvc_scene *sc, const void *lum, int32_t lum_f64, int64_t stride, int64_t p,
+                    int32_t m_cand, uint64_t key, uint64_t offset, int64_t kept_in, const nvc_rgrid *out,
+                    void *ws, int64_t *state_dev, void *stream);
+/* restir_temporal_batch (:487-526): clamp_mode 0 "m", 1 "contribution";
+ * phat from the f64 light-major factor table and the pixel albedos. */
+int nvc_restir_temporal(const nvc_scene *sc, const double *factor, int64_t stride, const double *alb,
+                        int64_t p, const nvc_rgrid *cur, const nvc_rgrid *prev, uint64_t key, uint64_t offset,
+                        double clamp, int32_t clamp_mode, const nvc_rgrid *out, void *stream);
+/* restir_spatial_batch (:541-595) over a width x height frame (out must not alias grid). */
+int nvc_restir_spatial(const nvc_scene *sc, const double *factor, int64_t stride, const double *alb,
+                       const double *nrm, const uint8_t *hit, const double *depth, int32_t width,
+                       int32_t height, const nvc_rgrid *grid, uint64_t key, uint64_t offset, int32_t radius,
+                       int32_t neighbors, const nvc_rgrid *out, void *stream);
+/* PixelCtx.phat_ids (:141-155), one id per pixel (id < 0 -> 0). */
+int nvc_phat_ids(const nvc_scene *sc, const double *factor, int64_t stride, const double *alb,
+                 const int64_t *ids, int64_t p, double *out, void *stream);
 
 /* ---- geometry + training data: geometry.py, render.py, training.py ----- */
 /* make_gbuffer / trace_rays (render.py:49-117) for pixels [p_first, p_first+p):

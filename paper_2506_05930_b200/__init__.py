@@ -25,6 +25,9 @@ from .scene import Camera, Light, Material, Scene, SceneError, load_scene, scene
 from .scenes import boxes_point_scene, boxes_scene, rooms_scene
 from .training import (TrainFrameConfig, compute_visibility_targets, gen_screen_hits, gen_screen_samples,
                        gen_world_samples, train_frame)
+from . import restir
+from .restir import (ReservoirGrid, cnvc_initial_batch, restir_spatial_batch, restir_temporal_batch,
+                     ris_initial_batch)
 from . import dropin
 
 __version__ = "0.1.0"
@@ -40,4 +43,6 @@ __all__ = [
     "scene_from_dict", "boxes_scene", "boxes_point_scene", "rooms_scene", "TrainFrameConfig",
     "compute_visibility_targets", "gen_screen_hits", "gen_screen_samples", "gen_world_samples", "train_frame",
     "ClusterSet", "kmeans_cluster", "clustered_sample", "clustered_sample_batch", "dropin",
+    "restir", "ReservoirGrid", "ris_initial_batch", "restir_temporal_batch", "restir_spatial_batch",
+    "cnvc_initial_batch",
 ]

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libnvc.so")
 
 MAX_LEVELS = 32
 MAX_LAYERS = 8
-ABI_VERSION = 9
+ABI_VERSION = 10
 
 c_i32, c_i64, c_u64, c_f64, c_f32, c_vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
                                            ctypes.c_double, ctypes.c_float, ctypes.c_void_p)
@@ -35,6 +35,11 @@ class NvcModel(ctypes.Structure):
         ("table_h", c_vp), ("wpack", c_vp),
         ("param_count", c_i64), ("wpack_count", c_i64),
     ]
+
+
+class NvcRGrid(ctypes.Structure):
+    _fields_ = [("y", c_vp), ("point", c_vp), ("w_y", c_vp), ("w_sum", c_vp), ("M", c_vp), ("W", c_vp),
+                ("valid", c_vp)]
 
 
 class NvcScene(ctypes.Structure):
@@ -112,6 +117,14 @@ _SIGS = {
     "nvc_clustered_select": (c_i32, [P(NvcScene), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp,
                                      c_u64, c_u64, c_f64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "nvc_shade": (c_i32, [P(NvcScene), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "nvc_ris_workspace_bytes": (c_i64, [c_i64, c_i32, c_i32]),
+    "nvc_ris_initial": (c_i32, [P(NvcScene), c_vp, c_i32, c_i64, c_i64, c_i32, c_u64, c_u64, c_i64,
+                                P(NvcRGrid), c_vp, c_vp, c_vp]),
+    "nvc_restir_temporal": (c_i32, [P(NvcScene), c_vp, c_i64, c_vp, c_i64, P(NvcRGrid), P(NvcRGrid), c_u64,
+                                    c_u64, c_f64, c_i32, P(NvcRGrid), c_vp]),
+    "nvc_restir_spatial": (c_i32, [P(NvcScene), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32,
+                                   P(NvcRGrid), c_u64, c_u64, c_i32, c_i32, P(NvcRGrid), c_vp]),
+    "nvc_phat_ids": (c_i32, [P(NvcScene), c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "nvc_primary_hits": (c_i32, [P(NvcScene), P(NvcCamera), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "nvc_grid_scatter": (c_i32, [c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "nvc_closest_hit": (c_i32, [P(NvcScene), c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),

@@ -1303,6 +1303,182 @@ __global__ void __launch_bounds__(128) k_cluster_tgt(nvc_scene sc, uint64_t key,
 
 inline int grid1(int64_t n, int bs) { return (int)((n + bs - 1) / bs); }
 
+
+// ---- RIS / screen-space ReSTIR baselines (sampling.py:369-637) ----------------
+// A reservoir grid is struct-of-arrays on the device: y (p) i64, point (p,3)
+// f64, w_y, w_sum, M, W (p) f64, valid (p) u8.  Target weight of light id at
+// pixel i (PixelCtx.phat_ids, sampling.py:141-155): f(i, id) * (albedo .
+// LUMA*L_e[id]) / pi, the dot in einsum order, f from the f64 light-major
+// factor table; id < 0 -> 0.
+struct RGrid {
+    int64_t* y;
+    double *pt, *w_y, *w_sum, *M, *W;
+    uint8_t* valid;
+};
+struct RGridC {
+    const int64_t* y;
+    const double *pt, *w_y, *w_sum, *M, *W;
+    const uint8_t* valid;
+};
+
+__device__ __forceinline__ double phat_at(const nvc_scene& sc, const double* __restrict__ factor, int64_t stride,
+                                          const double alb[3], int64_t i, int64_t id) {
+    if (id < 0) return 0.0;
+    const double f = __ldg(factor + id * stride + i);
+    const double lw[3] = {__ldg(sc.lt_lumaw + 3 * id), __ldg(sc.lt_lumaw + 3 * id + 1),
+                          __ldg(sc.lt_lumaw + 3 * id + 2)};
+    return f * (dot3e(alb, lw) / 3.141592653589793);
+}
+
+// ris_initial_batch: candidate ids = integers(0, K, (p, M)) (picks), phat from
+// the luminance table, weights phat * K, streaming WRS on draws
+// uni + i*M + j, W = w_sum / (M * phat(y)), points on draws uni + p*M + 2i.
+template <typename LT>
+__global__ void __launch_bounds__(128) k_ris_initial(nvc_scene sc, const LT* __restrict__ lum, int64_t stride,
+                                                     int64_t p, int32_t mc, const int32_t* __restrict__ picks,
+                                                     uint64_t key, const int64_t* __restrict__ uni, RGrid out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p) return;
+    const uint64_t u0 = (uint64_t)uni[0];
+    const double kd = (double)sc.n_lights;
+    double s = 0.0, phs = 0.0;
+    int sel = -1;
+    for (int j = 0; j < mc; ++j) {
+        const int64_t id = picks[i * mc + j];
+        const double ph = (double)__ldg(lum + id * stride + i);
+        const double w = ph * kd;
+        s = s + w;
+        if (u01(philox_out(key, u0 + (uint64_t)(i * mc + j))) * s < w) {
+            sel = j;
+            phs = ph;
+        }
+    }
+    const bool ok = sel >= 0;
+    const int64_t y = ok ? (int64_t)picks[i * mc + sel] : -1;
+    const uint64_t np = u0 + (uint64_t)p * (uint64_t)mc + 2ull * (uint64_t)i;
+    double pt[3];
+    light_point(sc, y, u01(philox_out(key, np)), u01(philox_out(key, np + 1)), pt);
+    out.y[i] = y;
+    out.w_y[i] = ok ? phs : 0.0;
+    out.w_sum[i] = s;
+    out.M[i] = (double)mc;
+    out.W[i] = ok ? s / ((double)mc * phs) : 0.0;
+    for (int a = 0; a < 3; ++a) out.pt[3 * i + a] = pt[a];
+    out.valid[i] = 1;
+}
+
+// restir_temporal_batch (sampling.py:487-526): draw offset + i
+__global__ void __launch_bounds__(128) k_restir_temporal(nvc_scene sc, const double* __restrict__ factor,
+                                                         int64_t stride, const double* __restrict__ alb_all, int64_t p,
+                                                         RGridC cur, RGridC prev, uint64_t key, uint64_t offset,
+                                                         double clamp, int32_t contribution, RGrid out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p) return;
+    const double alb[3] = {alb_all[3 * i], alb_all[3 * i + 1], alb_all[3 * i + 2]};
+    const bool pv = prev.valid[i] != 0;
+    const int64_t yc = cur.y[i], yp = prev.y[i];
+    const double ph_c = phat_at(sc, factor, stride, alb, i, yc);
+    const double ph_p = phat_at(sc, factor, stride, alb, i, pv ? yp : -1);
+    double m_prev, w_prev;
+    if (!contribution) {
+        m_prev = pv ? fmin(prev.M[i], clamp * cur.M[i]) : 0.0;
+        w_prev = ph_p * prev.W[i] * m_prev;
+    } else {
+        m_prev = pv ? prev.M[i] : 0.0;
+        w_prev = ph_p * prev.W[i] * m_prev;
+        w_prev = fmin(w_prev, clamp * ph_c * cur.W[i] * cur.M[i]);
+    }
+    const double w_cur = ph_c * cur.W[i] * cur.M[i];
+    const double w_sum = w_cur + w_prev;
+    const bool take = (draw(key, offset + (uint64_t)i) * w_sum < w_prev) && (w_prev > 0.0);
+    int64_t y = take ? yp : yc;
+    const double M = cur.M[i] + m_prev;
+    const double w_y = take ? ph_p : ph_c;
+    const bool ok = (w_sum > 0.0) && (w_y > 0.0) && (M > 0.0);
+    for (int a = 0; a < 3; ++a) out.pt[3 * i + a] = take ? prev.pt[3 * i + a] : cur.pt[3 * i + a];
+    out.y[i] = ok ? y : -1;
+    out.w_sum[i] = w_sum;
+    out.M[i] = M;
+    out.w_y[i] = w_y;
+    out.W[i] = ok ? w_sum / (M * w_y) : 0.0;
+    out.valid[i] = 1;
+}
+
+// restir_spatial_batch (sampling.py:541-595): per neighbour round r the draws
+// offset + (3r)p + i (angle), (3r+1)p + i (radius), (3r+2)p + i (merge)
+__global__ void __launch_bounds__(128) k_restir_spatial(nvc_scene sc, const double* __restrict__ factor,
+                                                        int64_t stride, const double* __restrict__ alb_all,
+                                                        const double* __restrict__ nrm, const uint8_t* __restrict__ hit,
+                                                        const double* __restrict__ depth, int32_t width, int32_t height,
+                                                        RGridC g, uint64_t key, uint64_t offset, int32_t radius,
+                                                        int32_t neighbors, RGrid out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t p = (int64_t)width * height;
+    if (i >= p) return;
+    const double alb[3] = {alb_all[3 * i], alb_all[3 * i + 1], alb_all[3 * i + 2]};
+    const double ni[3] = {nrm[3 * i], nrm[3 * i + 1], nrm[3 * i + 2]};
+    const int64_t ys = i / width, xs = i - ys * width;
+    int64_t acc_y = g.y[i];
+    double acc_pt[3] = {g.pt[3 * i], g.pt[3 * i + 1], g.pt[3 * i + 2]};
+    double acc_w = phat_at(sc, factor, stride, alb, i, acc_y) * g.W[i] * g.M[i];
+    double acc_m = g.M[i];
+    const bool hit_i = hit[i] != 0;
+    const double di = depth[i];
+    for (int r = 0; r < neighbors; ++r) {
+        const uint64_t base = offset + (uint64_t)(3 * r) * (uint64_t)p + (uint64_t)i;
+        const double ang = draw(key, base) * 2.0 * 3.141592653589793;
+        const double rad = (double)radius * sqrt(draw(key, base + (uint64_t)p));
+        const int64_t dx = (int64_t)rint(rad * cos(ang)), dy = (int64_t)rint(rad * sin(ang));
+        const int64_t nx = xs + dx, ny = ys + dy;
+        const bool inb = nx >= 0 && nx < width && ny >= 0 && ny < height && (dx != 0 || dy != 0);
+        const int64_t j = inb ? ny * width + nx : 0;
+        bool ok = inb && g.valid[j] && hit_i && hit[j];
+        const double nj[3] = {nrm[3 * j], nrm[3 * j + 1], nrm[3 * j + 2]};
+        const double ndot = dot3e(ni, nj);
+        const double ratio = depth[j] / fmax(di, 1e-12);
+        ok = ok && ndot >= 0.9 && ratio >= 0.9 && ratio <= 1.1;
+        const int64_t n_y = ok ? g.y[j] : -1;
+        const double w_n = ok ? phat_at(sc, factor, stride, alb, i, n_y) * g.W[j] * g.M[j] : 0.0;
+        const double w_sum = acc_w + w_n;
+        const bool take = (draw(key, base + 2ull * (uint64_t)p) * w_sum < w_n) && (w_n > 0.0);
+        acc_w = w_sum;
+        if (take) {
+            acc_y = n_y;
+            for (int a = 0; a < 3; ++a) acc_pt[a] = g.pt[3 * j + a];
+        }
+        acc_m = acc_m + (ok ? g.M[j] : 0.0);
+    }
+    const double w_y = phat_at(sc, factor, stride, alb, i, acc_y);
+    const bool ok = (acc_w > 0.0) && (w_y > 0.0) && (acc_m > 0.0);
+    out.y[i] = ok ? acc_y : -1;
+    for (int a = 0; a < 3; ++a) out.pt[3 * i + a] = acc_pt[a];
+    out.w_sum[i] = acc_w;
+    out.M[i] = acc_m;
+    out.w_y[i] = w_y;
+    out.W[i] = ok ? acc_w / (acc_m * w_y) : 0.0;
+    out.valid[i] = 1;
+}
+
+// PixelCtx.phat_ids for one id per pixel
+__global__ void k_phat_ids(nvc_scene sc, const double* __restrict__ factor, int64_t stride,
+                           const double* __restrict__ alb_all, const int64_t* __restrict__ ids, int64_t p,
+                           double* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p) return;
+    const double alb[3] = {alb_all[3 * i], alb_all[3 * i + 1], alb_all[3 * i + 2]};
+    out[i] = phat_at(sc, factor, stride, alb, i, ids[i]);
+}
+
+__global__ void k_ris_setup(int32_t* c_off, int32_t* c_mem, int32_t k, int64_t* n_rows, int64_t b) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < k) c_mem[t] = t;
+    if (t == 0) {
+        c_off[0] = 0;
+        c_off[1] = k;
+        *n_rows = b;
+    }
+}
+
 }  // namespace
 
 }  // namespace nvc
@@ -1480,6 +1656,90 @@ int nvc_targets(const nvc_scene* sc, uint64_t key, uint64_t offset, const double
     if (b <= 0) return NVC_OK;
     k_targets<<<grid1(b, 4), 128, 0, (cudaStream_t)stream>>>(*sc, key, offset, pos, nullptr, b, 0, 1, b, tgt);
     return check_launch("k_targets");
+}
+
+static RGrid rgrid(const nvc_rgrid* g) {
+    return RGrid{g->y, g->point, g->w_y, g->w_sum, g->M, g->W, g->valid};
+}
+static RGridC rgridc(const nvc_rgrid* g) {
+    return RGridC{g->y, g->point, g->w_y, g->w_sum, g->M, g->W, g->valid};
+}
+
+int64_t nvc_ris_workspace_bytes(int64_t p, int32_t m_cand, int32_t k) {
+    return nvc_cluster_workspace_bytes(p * m_cand, 1) + 8 * ((int64_t)k + 2) + 256;
+}
+
+int nvc_ris_initial(const nvc_scene* sc, const void* lum, int32_t lum_f64, int64_t stride, int64_t p, int32_t m_cand,
+                    uint64_t key, uint64_t offset, int64_t kept_in, const nvc_rgrid* out, void* ws,
+                    int64_t* state_dev, void* stream) {
+    NVC_REQUIRE(sc && lum && out && ws && state_dev, "nvc_ris_initial: null argument");
+    NVC_REQUIRE(m_cand >= 1 && stride >= p, "nvc_ris_initial: bad candidate count / stride");
+    if (p <= 0) return NVC_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t b = p * m_cand;
+    const int32_t k = sc->n_lights;
+    int32_t* picks = (int32_t*)ws;
+    int64_t* uni = (int64_t*)((char*)ws + nvc_cluster_state_offset(b, 1));   // [uni0, next, kept]
+    int64_t* base = uni + 3;
+    int64_t* kept = base + 1;
+    int32_t* flag = (int32_t*)(kept + 1);
+    char* tail = (char*)ws + nvc_cluster_workspace_bytes(b, 1);
+    int64_t* n_rows = (int64_t*)tail;
+    int32_t* c_off = (int32_t*)(n_rows + 1);
+    int32_t* c_mem = c_off + 2;
+    k_ris_setup<<<grid1(k, 128), 128, 0, s>>>(c_off, c_mem, k, n_rows, b);
+    // integers(0, K, (p, M)): Lemire on 32-bit halves, rejections and kept half exact
+    k_cluster_chain<<<1, 1, 0, s>>>(n_rows, 1, c_off, offset, kept_in, uni, base, kept, flag);
+    k_cluster_draws<<<dim3(grid1(b, 256), 1), 256, 0, s>>>(key, n_rows, 1, c_off, c_mem, base, kept, picks, uni, flag,
+                                                           kept_in);
+    k_cluster_picks<<<1, kPickThreads, 0, s>>>(key, n_rows, 1, c_off, c_mem, picks, uni,
+                                               getenv("NVC_CLUSTER_EXACT_WALK") ? nullptr : flag, offset, kept_in);
+    int rc = check_launch("k_cluster_picks");
+    if (rc) return rc;
+    if (lum_f64)
+        k_ris_initial<double><<<grid1(p, 128), 128, 0, s>>>(*sc, (const double*)lum, stride, p, m_cand, picks, key, uni,
+                                                            rgrid(out));
+    else
+        k_ris_initial<float><<<grid1(p, 128), 128, 0, s>>>(*sc, (const float*)lum, stride, p, m_cand, picks, key, uni,
+                                                           rgrid(out));
+    // the stream after the call: next output (uni0 + p*M + 2p) and the kept half
+    cudaMemcpyAsync(state_dev, uni, 8, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(state_dev + 1, uni + 2, 8, cudaMemcpyDeviceToDevice, s);
+    return check_launch("k_ris_initial");
+}
+
+int nvc_restir_temporal(const nvc_scene* sc, const double* factor, int64_t stride, const double* alb, int64_t p,
+                        const nvc_rgrid* cur, const nvc_rgrid* prev, uint64_t key, uint64_t offset, double clamp,
+                        int32_t clamp_mode, const nvc_rgrid* out, void* stream) {
+    NVC_REQUIRE(sc && factor && alb && cur && prev && out, "nvc_restir_temporal: null argument");
+    NVC_REQUIRE(clamp_mode == 0 || clamp_mode == 1, "nvc_restir_temporal: clamp_mode 0 (m) or 1 (contribution)");
+    if (p <= 0) return NVC_OK;
+    k_restir_temporal<<<grid1(p, 128), 128, 0, (cudaStream_t)stream>>>(*sc, factor, stride, alb, p, rgridc(cur),
+                                                                        rgridc(prev), key, offset, clamp, clamp_mode,
+                                                                        rgrid(out));
+    return check_launch("k_restir_temporal");
+}
+
+int nvc_restir_spatial(const nvc_scene* sc, const double* factor, int64_t stride, const double* alb,
+                       const double* nrm, const uint8_t* hit, const double* depth, int32_t width, int32_t height,
+                       const nvc_rgrid* grid, uint64_t key, uint64_t offset, int32_t radius, int32_t neighbors,
+                       const nvc_rgrid* out, void* stream) {
+    NVC_REQUIRE(sc && factor && alb && nrm && hit && depth && grid && out, "nvc_restir_spatial: null argument");
+    NVC_REQUIRE(width > 0 && height > 0 && neighbors >= 0, "nvc_restir_spatial: bad frame");
+    NVC_REQUIRE(grid->y != out->y, "nvc_restir_spatial: the output grid must not alias the input");
+    const int64_t p = (int64_t)width * height;
+    k_restir_spatial<<<grid1(p, 128), 128, 0, (cudaStream_t)stream>>>(*sc, factor, stride, alb, nrm, hit, depth, width,
+                                                                       height, rgridc(grid), key, offset, radius,
+                                                                       neighbors, rgrid(out));
+    return check_launch("k_restir_spatial");
+}
+
+int nvc_phat_ids(const nvc_scene* sc, const double* factor, int64_t stride, const double* alb, const int64_t* ids,
+                 int64_t p, double* out, void* stream) {
+    NVC_REQUIRE(sc && factor && alb && ids && out, "nvc_phat_ids: null argument");
+    if (p <= 0) return NVC_OK;
+    k_phat_ids<<<grid1(p, 128), 128, 0, (cudaStream_t)stream>>>(*sc, factor, stride, alb, ids, p, out);
+    return check_launch("k_phat_ids");
 }
 
 }  // extern "C"

@@ -18,6 +18,9 @@ sampling/render.neural_di_batch       sampling.neural_di_batch
 sampling/render.clustered_sample_batch sampling.clustered_sample_batch
 render.gbuffer_and_ctx (:128-142)     render.gbuffer_and_ctx ((gb, ctx))
 render.shade_batch (:220-246)         render.shade_batch (k_shade)
+sampling/render.ris_initial_batch,    restir.* (nvc_ris_initial,
+  cnvc_initial_batch,                   nvc_restir_temporal,
+  restir_temporal/spatial_batch         nvc_restir_spatial)
 ====================================  ========================================
 
 Everything else -- scenes, cameras, configs, ``ClusterSet`` / k-means, the
@@ -44,6 +47,7 @@ import numpy as np
 
 from . import cache as _cache
 from . import render as _render
+from . import restir as _restir
 from . import sampling as _sampling
 from . import training as _training
 
@@ -82,13 +86,22 @@ PATCHES = {
     "viscache.sampling": {"nls_sample_batch": _sampling.nls_sample_batch,
                           "nls_weights_batch": _sampling.nls_weights_batch,
                           "neural_di_batch": _sampling.neural_di_batch,
-                          "clustered_sample_batch": _sampling.clustered_sample_batch},
+                          "clustered_sample_batch": _sampling.clustered_sample_batch,
+                          "ris_initial_batch": _restir.ris_initial_batch,
+                          "cnvc_initial_batch": _restir.cnvc_initial_batch,
+                          "restir_temporal_batch": _restir.restir_temporal_batch,
+                          "restir_spatial_batch": _restir.restir_spatial_batch},
     "viscache.render": {"make_cache": make_cache, "train_frame": train_frame,
                         "nls_sample_batch": _sampling.nls_sample_batch,
                         "neural_di_batch": _sampling.neural_di_batch,
                         "clustered_sample_batch": _sampling.clustered_sample_batch,
                         "gbuffer_and_ctx": _render.gbuffer_and_ctx,
-                        "shade_batch": _render.shade_batch},
+                        "shade_batch": _render.shade_batch,
+                        "ris_initial_batch": _restir.ris_initial_batch,
+                        "cnvc_initial_batch": _restir.cnvc_initial_batch,
+                        "restir_temporal_batch": _restir.restir_temporal_batch,
+                        "restir_spatial_batch": _restir.restir_spatial_batch,
+                        "ReservoirGrid": _restir.ReservoirGrid},
 }
 
 

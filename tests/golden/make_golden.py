@@ -524,12 +524,61 @@ def gen_scalar(out: dict) -> None:
         out[f"sc_{tag}_phat"] = ctx.phat_ids(ids)
 
 
+def gen_restir(out: dict) -> None:
+    """RIS / ReSTIR baselines (sampling.py:369-637) on boxes8 at 48x32: two RIS
+    frames (the first on a stream whose integers() left a kept 32-bit half),
+    temporal merges in both clamp modes (one with a partly invalid history),
+    spatial reuse at radius 32 and 4, clustered initial reservoirs; plus the
+    next draws of each stream (the continuation)."""
+    from viscache.sampling import (ReservoirGrid, cnvc_initial_batch, kmeans_cluster, restir_spatial_batch,
+                                   restir_temporal_batch, ris_initial_batch)
+    s = scene_from_dict(boxes_scene(8))
+    cam = Camera(position=s.camera.position, look_at=s.camera.look_at, up=s.camera.up,
+                 fov_deg=s.camera.fov_deg, width=48, height=32)
+    gb = make_gbuffer(s, cam)
+    ctx = PixelCtx(s, gb.flat("position"), gb.flat("normal"), gb.flat("albedo"))
+
+    def save(tag, g, rng=None):
+        for k in ("y", "point", "w_y", "w_sum", "M", "W", "valid"):
+            out[f"{tag}_{k}"] = np.asarray(getattr(g, k))
+        if rng is not None:
+            out[f"{tag}_next"] = rng.random(3)
+
+    r0 = R.stream(0, 0, "restir-initial")
+    out["pre_ints"] = r0.integers(0, 7, size=3)
+    g0 = ris_initial_batch(ctx, r0, 8)
+    save("ris0", g0, r0)
+    r1 = R.stream(0, 1, "restir-initial")
+    g1 = ris_initial_batch(ctx, r1, 8)
+    save("ris1", g1, r1)
+    rt = R.stream(0, 1, "restir-temporal")
+    t_m = restir_temporal_batch(g1, g0, ctx, rt, 20.0, "m")
+    save("tm", t_m, rt)
+    g0b = ReservoirGrid(g0.n)
+    for k in ("y", "point", "w_y", "w_sum", "M", "W", "valid"):
+        setattr(g0b, k, np.array(getattr(g0, k)))
+    g0b.valid[::3] = False
+    g0b.M[1::5] = 60.0
+    rt2 = R.stream(0, 2, "restir-temporal")
+    t_c = restir_temporal_batch(g1, g0b, ctx, rt2, 2.0, "contribution")
+    save("tc", t_c, rt2)
+    rt3 = R.stream(0, 3, "restir-temporal")
+    save("tm2", restir_temporal_batch(g1, g0b, ctx, rt3, 2.0, "m"), rt3)
+    for rad in (32, 4):
+        rs = R.stream(0, rad, "restir-spatial")
+        sp = restir_spatial_batch(t_m, ctx, gb.shape, gb.flat("hit"), gb.flat("depth"), ctx.normals, rs, rad, 4)
+        save(f"sp{rad}", sp, rs)
+    cl = kmeans_cluster(s.lights, 4, R.stream(0, "clustering"))
+    rc = R.stream(0, 2, "restir-initial")
+    save("cn", cnvc_initial_batch(ctx, WaveCache(4), cl, rc), rc)
+
+
 def main() -> None:
     quick = "--quick" in sys.argv
     groups = {
         "rng": gen_rng, "scenes": gen_scenes, "mlp": gen_mlp,
         "sampling": gen_sampling, "training": gen_training, "shade": gen_shade, "snapshot": gen_snapshot,
-        "clusters": gen_clusters, "curves": gen_long_curves, "scalar": gen_scalar,
+        "clusters": gen_clusters, "curves": gen_long_curves, "scalar": gen_scalar, "restir": gen_restir,
     }
     only = [a for a in sys.argv[1:] if not a.startswith("-")]
     if only:   # regenerate just the named groups, e.g. `make_golden.py shade`
