@@ -77,6 +77,8 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index, self.rows, self.proc = index, [], None
+        self.recording = True     # rows are kept only inside window() once it has been used
+        self.seen = 0
 
     def __enter__(self):
         try:
@@ -89,11 +91,36 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def settle(self, timeout: float = 3.0):
+        """Wait for the first sample: nvidia-smi's start-up (a CPU burst) is over
+        before a timed region begins, so it cannot delay the host's frame issue."""
+        t0 = time.perf_counter()
+        while self.proc is not None and self.seen == 0 and time.perf_counter() - t0 < timeout:
+            time.sleep(0.02)
+        self.recording = False
+        self.rows = []
+
+    class _Window:
+        def __init__(self, s):
+            self.s = s
+
+        def __enter__(self):
+            self.s.recording = True
+
+        def __exit__(self, *exc):
+            time.sleep(0.25)            # the sample covering the region's end
+            self.s.recording = False
+
+    def window(self):
+        return ClockSampler._Window(self)
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 6:
-                self.rows.append(parts)
+                self.seen += 1
+                if self.recording:
+                    self.rows.append(parts)
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -307,13 +334,17 @@ def gpu_arm(args) -> None:
     barrier()
     assert int(last_bufs[0].n_rows.item()) == cfg.n_world + cfg.n_screen, "screen rays missed: batch shrank"
 
+    # the clock sampler starts now (its start-up must not overlap the timed region)
+    sampler = ClockSampler(local).__enter__()
     # ---- per-stage split (separate pass, events between stages and between
-    #      the three query kernels, all on the launching stream) ----
+    #      the three query kernels, all on the launching stream); frame numbers
+    #      continue the sequence so the batch pipeline's prefetch stays valid ----
     split_train, split_query, split_k, split_shade = [], [], [], []
     kms = (ctypes.c_float * 3)()
-    for f in range(min(args.steps, 10)):
+    n_split = min(args.steps, 10)
+    for f in range(n_split):
         _lib.call("nvc_profile_stages", 1)
-        frame(1000 + f, timed_parts=True)
+        frame(args.warmup + f, timed_parts=True)
         _lib.call("nvc_profile_stages", 0)
         marks[3 if shade else 2].synchronize()
         _lib.call("nvc_profile_stage_ms", ctypes.addressof(kms))
@@ -325,14 +356,16 @@ def gpu_arm(args) -> None:
 
     # ---- timed region: K frames, inputs resident ----
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0 = args.warmup + n_split        # its batch was prefetched by the last split frame
+    sampler.settle()
     barrier()
-    with ClockSampler(local) as clocks:
+    with sampler as clocks, clocks.window():
         if os.environ.get("NVC_PREQUEUE"):   # diagnostic: let the host run ahead of the GPU
             torch.cuda._sleep(int(os.environ["NVC_PREQUEUE"]))
         start.record(stream)
         t_issue = time.perf_counter()
         for f in range(args.steps):
-            loss = frame(args.warmup + f)
+            loss = frame(f0 + f)
         if cache.select_done is not None:
             stream.wait_event(cache.select_done)
         end.record(stream)
@@ -373,7 +406,7 @@ def gpu_arm(args) -> None:
         if sel_stream is not None:
             sel_stream.wait_event(ev_d2h[b])
         ctx.pos = pos_buf[b]
-        loss = frame_into(5000 + f, out_buf[b], rgb=rgb_buf[b])
+        loss = frame_into(f0 + args.steps + f, out_buf[b], rgb=rgb_buf[b])
         ev_comp[b].record(stream)
         with torch.cuda.stream(s_d2h):
             s_d2h.wait_event(ev_comp[b])

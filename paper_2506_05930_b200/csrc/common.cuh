@@ -27,7 +27,15 @@ int check_launch(const char* what);
         }                                   \
     } while (0)
 
-constexpr int kNumSMs = 148;
+// SM count of the current device (queried once per device; 148 on B200)
+inline int num_sms() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cached[dev]) cudaDeviceGetAttribute(&cached[dev], cudaDevAttrMultiProcessorCount, dev);
+    return cached[dev] > 0 ? cached[dev] : 1;
+}
 
 // fp32 SIMT inference (model.cu), used by nvc_infer(precision=0)
 int nvc_infer_f32(const nvc_model* m, const double* pos, int64_t n, float* out, cudaStream_t s);

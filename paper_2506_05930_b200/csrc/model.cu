@@ -1473,9 +1473,7 @@ int nvc_adam_step_shard(const nvc_model* m, int64_t t, double lr, int32_t shard,
         const int smem = kAdamStages * (int)sizeof(AdamStage);
         cudaFuncSetAttribute(k_adam_bulk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(k_adam_bulk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        int dev = 0, sms = kNumSMs;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int sms = num_sms();
         const int64_t all_tiles = net.grid_count / kAdamTile;
         const int64_t tile0 = all_tiles * shard / n_shards, ntiles = all_tiles * (shard + 1) / n_shards - tile0;
         if (n_shards > 1) {   // the other shards' (allreduced) gradients are consumed by their owners

@@ -1254,9 +1254,7 @@ int run_front(const nvc_model* m, const double* pos, int64_t P, uint8_t* tiles, 
     rc = check_launch("k_enc_tiles");
     if (rc) return rc;
     stage_mark(1, s);
-    int dev = 0, sms = kNumSMs;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = num_sms();
     MNet t = q;
     if (ts_layout(t) && !getenv("NVC_MLP_QUADS")) {
         rc = launch_mlp_ts(t, m, tiles, ntiles, P, vis16, vstride, sms, s);

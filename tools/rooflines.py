@@ -53,11 +53,11 @@ def measure(quick: bool = False) -> dict:
             ms = _time(lambda: lib.nvc_philox_rate(c32, grid, iters, key, sink.data_ptr(), st))
             best = max(best, grid * 256 * iters / (ms * 1e-3))
         out["philox_blocks_per_s" + ("_c32" if c32 else "")] = best
-    for mb in ((32,) if quick else (16, 32, 64)):
+    for mb in ((32, 64) if quick else (16, 32, 64)):
         buf = torch.randint(0, 1 << 30, (mb * (1 << 20) // 4,), dtype=torch.int32, device="cuda")
         best = 0.0
         for per_sm in (4, 8):
-            grid, passes = sms * per_sm, 8 if quick else 32
+            grid, passes = sms * per_sm, 32     # >= 1 GB per launch: launch overhead is noise
             ms = _time(lambda: lib.nvc_l2_stream(buf.data_ptr(), buf.numel() * 4, grid, passes, sink.data_ptr(), st))
             best = max(best, buf.numel() * 4 * passes / (ms * 1e-3))
         out[f"l2_stream_GBps_{mb}MB"] = best / 1e9
