@@ -398,7 +398,8 @@ def gpu_arm(args) -> None:
     for f in range(e2e_steps):
         b = f % 2
         with torch.cuda.stream(s_h2d):
-            s_h2d.wait_event(ev_comp[b])              # frame f-2 finished reading this buffer
+            s_h2d.wait_event(ev_comp[b])              # frame f-2's main-stream kernels are done with it
+            s_h2d.wait_event(ev_d2h[b])               # ... and its select-stream work (render: shading reads pos)
             pos_buf[b].copy_(pos_host, non_blocking=True)
             ev_h2d[b].record(s_h2d)
         stream.wait_event(ev_h2d[b])

@@ -266,11 +266,15 @@ __global__ void __launch_bounds__(kT, 8) k_enc_tiles2(GridDev g, const uint16_t*
                 const uint32_t sz = dense ? sy * sy : 805459861u;
                 const uint32_t mask = dense ? 0xffffffffu : g.tmask;
                 const uint32_t base = c0[0] + c0[1] * sy + c0[2] * sz;
-                const uint2* tl = t2 + (size_t)l * (size_t)g.T;
-                v[j][0] = __ldg(tl + (base & mask));
-                v[j][1] = __ldg(tl + ((base + sz) & mask));
-                v[j][2] = __ldg(tl + ((base + sy) & mask));
-                v[j][3] = __ldg(tl + ((base + sy + sz) & mask));
+                // 32-bit byte offsets from the table base (the x-pair table is < 4 GB,
+                // checked on the host): one shift-add per gather instead of a 64-bit
+                // index multiply-add per gather
+                const uint32_t lofs = (uint32_t)l * (uint32_t)g.T * 8u;
+                const char* tb = reinterpret_cast<const char*>(t2);
+                v[j][0] = __ldg(reinterpret_cast<const uint2*>(tb + (lofs + ((base & mask) << 3))));
+                v[j][1] = __ldg(reinterpret_cast<const uint2*>(tb + (lofs + (((base + sz) & mask) << 3))));
+                v[j][2] = __ldg(reinterpret_cast<const uint2*>(tb + (lofs + (((base + sy) & mask) << 3))));
+                v[j][3] = __ldg(reinterpret_cast<const uint2*>(tb + (lofs + (((base + sy + sz) & mask) << 3))));
             }
         }
         __align__(16) __half2 out[4];
@@ -1242,7 +1246,8 @@ int run_front(const nvc_model* m, const double* pos, int64_t P, uint8_t* tiles, 
     GridDev g = grid_of(m);
     const int64_t ntiles = (P + kT - 1) / kT;
     stage_mark(0, s);
-    const bool h2 = !getenv("NVC_ENC_F32");
+    // k_enc_tiles2 addresses the x-pair table with 32-bit byte offsets
+    const bool h2 = !getenv("NVC_ENC_F32") && (int64_t)g.L * g.T * 8 <= 0xffffffffll;
     if (g.F == 2 && g.L == 16 && h2)
         k_enc_tiles2<16><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
     else if (g.F == 2 && g.L == 8 && h2)
