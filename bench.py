@@ -228,14 +228,19 @@ def gpu_arm(args) -> None:
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # NVC_RANKS_PER_GPU=n (test only): n ranks share a GPU over gloo -- the N>1
+    # code path on a 1-GPU box (no kernel waits on another rank; NCCL refuses it)
+    local = int(os.environ.get("LOCAL_RANK", "0")) // int(os.environ.get("NVC_RANKS_PER_GPU", "1"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     prio = int(os.environ.get("NVC_MAIN_PRIORITY", "-1"))
     if prio:
         torch.cuda.set_stream(torch.cuda.Stream(dev, priority=prio))
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if os.environ.get("NVC_RANKS_PER_GPU"):
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     c4 = args.workload == "c4"
     kk, hid = (128, (128, 128, 128)) if c4 else (K, HIDDEN)
@@ -276,6 +281,10 @@ def gpu_arm(args) -> None:
         # all-gather of the updated slices (off by default: at C2 the 67 MB
         # all-gather costs more than the replicated 121 us Adam it replaces)
         def gather(buf):
+            if dist.get_backend() == "gloo":    # the NVC_RANKS_PER_GPU test mode
+                parts = [torch.empty_like(buf) for _ in range(world)]
+                dist.all_gather(parts, buf)
+                return torch.stack(parts)
             out = torch.empty((world, buf.numel()), dtype=buf.dtype, device=buf.device)
             dist.all_gather_into_tensor(out, buf)
             return out
@@ -548,11 +557,16 @@ def ndi4k_arm(args) -> None:
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # NVC_RANKS_PER_GPU=n (test only): n ranks share a GPU over gloo -- the N>1
+    # code path on a 1-GPU box (no kernel waits on another rank; NCCL refuses it)
+    local = int(os.environ.get("LOCAL_RANK", "0")) // int(os.environ.get("NVC_RANKS_PER_GPU", "1"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if os.environ.get("NVC_RANKS_PER_GPU"):
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     W4, H4 = 3840, 2160
     scene = scene_from_dict(boxes_scene(32))
     cam = scene.camera.resized(W4, H4)
