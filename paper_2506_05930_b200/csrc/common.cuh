@@ -154,6 +154,15 @@ __device__ __forceinline__ long long to_fx(double v) {
 __device__ __forceinline__ float from_fx(long long q) {
     return (float)((double)q * 0x1.0p-48);
 }
+// MLP gradients: a finer fixed point (2^-58, |g| < 32) -- they are summed from
+// per-32-row-block partials (shard-exact) and weight gradients at init are
+// ~1e-9, where 2^-48 per partial would cost ~1e-4 relative
+__device__ __forceinline__ long long to_fx_mlp(double v) {
+    return __double2ll_rn(v * 0x1.0p58);
+}
+__device__ __forceinline__ float from_fx_mlp(long long q) {
+    return (float)((double)q * 0x1.0p-58);
+}
 __device__ __forceinline__ void red_add_fx(int64_t* p, long long v) {
     if (v != 0)
         asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"((unsigned long long)v) : "memory");

@@ -844,9 +844,9 @@ __global__ void __launch_bounds__(256) k_reduce_parts(const float* __restrict__ 
 #pragma unroll
             for (int u = 0; u < 8; ++u) v[u] = __ldg(part_w + (int64_t)(b + 8 * u) * mlp_count + j);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) acc += to_fx((double)v[u]);
+            for (int u = 0; u < 8; ++u) acc += to_fx_mlp((double)v[u]);
         }
-        for (; b < nblk; b += 8) acc += to_fx((double)__ldg(part_w + (int64_t)b * mlp_count + j));
+        for (; b < nblk; b += 8) acc += to_fx_mlp((double)__ldg(part_w + (int64_t)b * mlp_count + j));
     }
     s_acc[w][lane] = acc;
     __syncthreads();
@@ -1084,7 +1084,7 @@ __global__ void k_adam_mlp(Net net, float* __restrict__ p, float* __restrict__ m
     const long long q = *gq;
     *gq = 0;
     float mm = m[i], vv = v[i];
-    const float pn = adam1(p[i], from_fx(q), mm, vv, a);
+    const float pn = adam1(p[i], from_fx_mlp(q), mm, vv, a);
     p[i] = pn;
     m[i] = mm;
     v[i] = vv;
@@ -1314,7 +1314,7 @@ int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, con
                         train_tc(m, net.grid_count, net.woff, net.boff, net.mlp_count, act0, b_max, b_dev, shard,
                                  n_shards, tgt, mask, dact0, part_w, part_loss, grid1(rows_max, 128), s) == 0;
         if (tc) {
-            nblk_red = grid1(rows_max, 128);
+            nblk_red = 2 * grid1(rows_max, 128);   // a hi and a lo partial set per 128-row tile
         } else if (wg) {
             cudaFuncSetAttribute(k_train3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
             k_train3<true><<<nblk, kThreads, smem3, s>>>(net, tl3, m->params, act0, b_max, b_dev, shard, n_shards,

@@ -26,6 +26,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include <cuda_bf16.h>
 
 namespace nvc {
 namespace {
@@ -1375,33 +1376,42 @@ int pipeline_query(const nvc_model* m, const nvc_scene* sc, const double* pos, i
 
 
 // ---------------------------------------------------------------------------
-// Training MLP on the tensor cores (opt-in: NVC_TRAIN_TC=1; measured 65 us vs
-// 49 us for the fp32 SIMT k_train3 at the C2 batch -- one 128-row tile per CTA
-// leaves the step latency-bound -- and a loss curve within ~2 % of the
-// reference instead of bit-faithful fp32, so it is not the default): one CTA per
-// 128-row tile runs the forward pass and the backward pass as tcgen05 MMAs
-// (fp16 operands, fp32 accumulators in TMEM):
-//   forward   Z_l   = A_l . W_l^T            (A_l [128 x K] K-major, packed W_l)
-//   backward  dW_l  = dZ_l^T . A_l           (dZ^T [n x 128] and A_l^T [k x 128], K = rows)
-//             db_l  = dZ_l^T . 1             (a ones column)
-//             dA_l  = dZ_l . W_l             (W_l^T packed after the forward blocks)
-// dZ is carried in fp16 scaled by 2^18 (it starts at 2(out-t)/(bK) ~ 1e-6)
-// and unscaled on read-out.  Per-CTA dW/db partials go to the same part_w
-// layout k_reduce_parts sums in fixed order; dA_0 feeds the hash-grid scatter.
-// Parity is by tolerance (loss curve), not bitwise like the fp32 SIMT step.
+// Training MLP on the tensor cores: forward and backward of one 128-row tile
+// per CTA as tcgen05 MMAs with fp32 accumulators in TMEM, at fp32-level
+// accuracy through split fp16 operands.
+//
+// Every operand x is stored as bf16 hi = bf16(x) and lo = bf16(x - hi) (16-17
+// significant bits, the full fp32 exponent range: init-scale activations and
+// output deltas are ~1e-6, below what fp16 can split), and each product takes
+// the three terms hi*hi + lo*hi + hi*lo.  An activation tile A_l (128 rows x w <= 64 columns) is kept as one
+// K-major SW128 "stack" [128 x 128]: hi in columns 0..63, lo in 64..127.  The
+// same bytes serve both roles through the MMA's major-ness bits:
+//   forward   Z_l   = A_l . W_l^T     A K-major (hi, then lo K-steps),
+//                                     B = W_l K-major (hi, reused for lo), + A_hi . W_lo^T
+//   backward  dW_l^T = A_l^T . dZ_l   A = the stack MN-major: M = 128 = [hi | lo] rows
+//                                     of dW^T, B = dZ MN-major (hi, then lo) -- the
+//                                     two halves are the hi and lo partials
+//             dA_l  = dZ_l . W_l      A = dZ stack K-major, B = W_l MN-major
+// db is a fixed-order column sum of dZ (warp butterfly + 4-way add).  dZ is
+// carried scaled by 2^18 (it starts near 2(out-t)/(bK) ~ 1e-6) and unscaled on
+// read-out.  Per-CTA dW/db partials (two sets: the hi and lo halves of dW^T)
+// go to the part_w layout k_reduce_parts sums as fixed point per set; dA_0
+// feeds the hash-grid scatter.  Widths <= 64 (C1, C2); wider models use the
+// fp32 SIMT k_train3.
 // ---------------------------------------------------------------------------
 namespace {
 constexpr float kGradScale = 262144.0f;   // 2^18
+constexpr int kTcThreads = 256;           // 8 warps: TMEM lane quarter = warp & 3, column half = warp >> 2
 
 struct TrainTC {
     int L, D0, K;
     int dims[NVC_MAX_LAYERS + 1], np[NVC_MAX_LAYERS], kp[NVC_MAX_LAYERS];
-    int wofs[NVC_MAX_LAYERS], wofsT[NVC_MAX_LAYERS];   // halfs into the packed weights
-    int64_t woff_rel[NVC_MAX_LAYERS], boff_rel[NVC_MAX_LAYERS], boff_abs[NVC_MAX_LAYERS];
-    int w_halfs;                                        // forward + transposed blocks
+    int64_t woff_abs[NVC_MAX_LAYERS], boff_abs[NVC_MAX_LAYERS];
+    int64_t woff_rel[NVC_MAX_LAYERS], boff_rel[NVC_MAX_LAYERS], mlp_count;
     float alpha;
     int out_sigmoid;
-    int sm_w, sm_a[NVC_MAX_LAYERS], sm_at[NVC_MAX_LAYERS], sm_g, sm_gt, sm_ones, sm_bias, sm_total;
+    int terms;            // split-precision terms per product (3; 1 = hi only, diagnostics)
+    int sm_whi[NVC_MAX_LAYERS], sm_wlo[NVC_MAX_LAYERS], sm_a[NVC_MAX_LAYERS], sm_dz, sm_bias, sm_db, sm_total;
 };
 
 __device__ __forceinline__ float sigmoid_exact(float z) {   // mlp.py:101-107
@@ -1410,46 +1420,96 @@ __device__ __forceinline__ float sigmoid_exact(float z) {   // mlp.py:101-107
     return __fdiv_rn(e, __fadd_rn(1.0f, e));
 }
 
-__device__ __forceinline__ void put_h(uint8_t* base, uint32_t off, float v) {
-    *reinterpret_cast<__half*>(base + off) = __float2half_rn(v);
+// MN-major descriptor over a [rows x kp] K-major swizzled tile: MN = its columns
+// (2^lg-byte swizzle rows, atoms `rows` rows apart), K = its rows, step kk = 16 rows
+__device__ __forceinline__ uint64_t desc_mn(uint32_t base, int rows, int kp, int kk) {
+    const int lg = umma_sw_log2(kp);
+    const uint32_t addr = base + (uint32_t)kk * (16u << lg);
+    const uint64_t layout = lg == 7 ? 2ull : (lg == 6 ? 4ull : 6ull);
+    return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)((((uint32_t)rows << lg) >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)((8u << lg) >> 4) << 32) | ((uint64_t)1 << 46) | (layout << 61);
+}
+// bf16 x bf16 -> f32 (the 8-bit exponent keeps init-scale activations ~1e-6 and
+// output deltas ~1e-6 normal, which fp16 could not split)
+__device__ __forceinline__ uint32_t idesc_bf16(int m, int n, bool a_mn, bool b_mn) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+           ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+__device__ __forceinline__ void split_h(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+    hi = __float2bfloat16_rn(x);
+    lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+// 8 consecutive columns c0..c0+7 (c0 % 8 == 0) of row r into a [128 x 128] stack: hi at c, lo at 64 + c
+__device__ __forceinline__ void put_stack8(uint8_t* stack, int r, int c0, const float v[8]) {
+    __align__(16) __nv_bfloat16 hi[8], lo[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) split_h(v[i], hi[i], lo[i]);
+    *reinterpret_cast<uint4*>(stack + umma_off(r, c0, kT, 128)) = *reinterpret_cast<const uint4*>(hi);
+    *reinterpret_cast<uint4*>(stack + umma_off(r, 64 + c0, kT, 128)) = *reinterpret_cast<const uint4*>(lo);
+}
+// the 32 values of a warp's lanes for 32 columns -> lane l holds column l's sum (fixed order)
+__device__ __forceinline__ float col_sum32(float v[32], int lane) {
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        const bool up = (lane & s) != 0;
+#pragma unroll
+        for (int j = 0; j < s; ++j) {
+            const float send = up ? v[j] : v[j + s];
+            const float keep = up ? v[j + s] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+        }
+    }
+    return v[0];
 }
 
-__global__ void __launch_bounds__(128, 1) k_train_tc(TrainTC t, const float* __restrict__ params,
-                                                    const uint16_t* __restrict__ wpack,
-                                                    const float* __restrict__ act0g, int64_t b_max,
-                                                    const int64_t* __restrict__ b_dev, int shard, int n_shards,
-                                                    const float* __restrict__ tgt, const float* __restrict__ mask,
-                                                    float* __restrict__ dact0g, float* __restrict__ part_w,
-                                                    double* __restrict__ part_loss) {
+__global__ void __launch_bounds__(kTcThreads, 1) k_train_tc(TrainTC t, const float* __restrict__ params,
+                                                           const float* __restrict__ act0g, int64_t b_max,
+                                                           const int64_t* __restrict__ b_dev, int shard,
+                                                           int n_shards, const float* __restrict__ tgt,
+                                                           const float* __restrict__ mask,
+                                                           float* __restrict__ dact0g, float* __restrict__ part_w,
+                                                           double* __restrict__ part_loss) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint64_t bar;
     __shared__ uint32_t tbase;
-    __shared__ double s_loss[4];
+    __shared__ double s_loss[8];
     uint8_t* sm = smem_raw + ((1024u - (s32(smem_raw) & 1023u)) & 1023u);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int q = warp & 3, h = warp >> 2;          // TMEM lane quarter, column half
+    const int r = 32 * q + lane;                   // the tile row this thread reads from TMEM
     const int64_t b = b_dev ? *b_dev : b_max;
     const int64_t lo = b * shard / n_shards, hi = b * (shard + 1) / n_shards;
     const int64_t r0g = (int64_t)blockIdx.x * kT;
     const int nr = (int)max((int64_t)0, min((int64_t)kT, (hi - lo) - r0g));
-    const int L = t.L, r = tid;
+    const int L = t.L;
     float* bias = reinterpret_cast<float*>(sm + t.sm_bias);
-    {   // weights (forward + transposed packs), biases, ones column, input tile
-        const uint4* src = reinterpret_cast<const uint4*>(wpack);
-        uint4* dst = reinterpret_cast<uint4*>(sm + t.sm_w);
-        for (int i = tid; i < t.w_halfs / 8; i += 128) dst[i] = __ldg(src + i);
-        int bo = 0;
+    float* s_db = reinterpret_cast<float*>(sm + t.sm_db);      // [2][8 warps][32]
+    uint8_t* dz = sm + t.sm_dz;
+    {   // weights (hi / lo, K-major [np x kp]), biases, the input stack
         for (int l = 0; l < L; ++l) {
-            for (int n = tid; n < t.np[l]; n += 128) bias[bo + n] = n < t.dims[l + 1] ? __ldg(params + t.boff_abs[l] + n) : 0.0f;
-            bo += t.np[l];
+            const int np = t.np[l], kp = t.kp[l], N = t.dims[l + 1], Kin = t.dims[l];
+            for (int i = tid; i < np * kp / 8; i += kTcThreads) {
+                const int n = i / (kp / 8), k0 = (i % (kp / 8)) * 8;
+                float w[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    w[j] = (n < N && k0 + j < Kin) ? __ldg(params + t.woff_abs[l] + (int64_t)n * Kin + k0 + j) : 0.0f;
+                __align__(16) __nv_bfloat16 wh[8], wl[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) split_h(w[j], wh[j], wl[j]);
+                *reinterpret_cast<uint4*>(sm + t.sm_whi[l] + umma_off(n, k0, np, kp)) = *reinterpret_cast<const uint4*>(wh);
+                *reinterpret_cast<uint4*>(sm + t.sm_wlo[l] + umma_off(n, k0, np, kp)) = *reinterpret_cast<const uint4*>(wl);
+            }
+            for (int n = tid; n < 64; n += kTcThreads) bias[64 * l + n] = n < N ? __ldg(params + t.boff_abs[l] + n) : 0.0f;
         }
-        for (int i = tid; i < 16 * kT; i += 128) {
-            const int rr = i / kT, k = i % kT;
-            put_h(sm + t.sm_ones, umma_off(rr, k, 16, kT), rr == 0 ? 1.0f : 0.0f);
-        }
-        for (int k = 0; k < t.kp[0]; ++k) {
-            const float v = (r < nr && k < t.D0) ? __ldg(act0g + (r0g + r) * t.D0 + k) : 0.0f;
-            put_h(sm + t.sm_a[0], umma_off(r, k, kT, t.kp[0]), v);
-            put_h(sm + t.sm_at[0], umma_off(k, r, t.kp[0], kT), v);
+        // thread (row r, half h) stages input columns [32h, 32h + 32) of its row
+        const int row = tid & 127, hh = tid >> 7;
+        for (int c0 = 32 * hh; c0 < 32 * hh + 32 && c0 < t.kp[0]; c0 += 8) {
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                v[j] = (row < nr && c0 + j < t.D0) ? __ldg(act0g + (r0g + row) * t.D0 + c0 + j) : 0.0f;
+            put_stack8(sm + t.sm_a[0], row, c0, v);
         }
     }
     if (warp == 0) {
@@ -1461,14 +1521,8 @@ __global__ void __launch_bounds__(128, 1) k_train_tc(TrainTC t, const float* __r
         mbar_init(&bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    fence_async();
-    tc_before();
-    __syncthreads();   // TMEM address, barrier and the staged tiles visible to every thread
-    tc_after();
     uint32_t phase = 0;
-    const uint32_t tmem = tbase;
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    auto sync_issue = [&]() {   // generic smem writes -> async proxy, then one thread issues
+    auto sync_issue = [&]() {   // generic smem writes -> async proxy; then thread 0 issues
         fence_async();
         tc_before();
         __syncthreads();
@@ -1480,35 +1534,66 @@ __global__ void __launch_bounds__(128, 1) k_train_tc(TrainTC t, const float* __r
         phase ^= 1u;
         tc_after();
     };
-    auto idesc = [](int n) { return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kT >> 4) << 24); };
-    const uint32_t w_addr = s32(sm + t.sm_w);
+    sync_issue();
+    const uint32_t tmem = tbase;
+    const uint32_t acc_f = tmem, acc_dw = tmem + 64u, acc_da = tmem + 128u;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    auto ld32 = [&](uint32_t col, float v[32]) {     // this warp's 32 lanes x columns [col, col + 32)
+        uint32_t u[32];
+        tld16_nowait(lane_base + col, u);
+        tld16_nowait(lane_base + col + 16u, u + 16);
+        tld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(u[i]);
+    };
+    // db partials double-buffered by layer parity: a layer's flush and the next
+    // layer's column sums never share a buffer between barriers
+    auto db_out = [&](int l, float v[32]) {          // column sums of dZ_l (this thread's 32 columns)
+        s_db[(l & 1) * 256 + warp * 32 + lane] = col_sum32(v, lane);
+    };
+    auto db_flush = [&](int l) {                     // after a __syncthreads: 4 lane quarters in fixed order
+        if (tid < 64 && tid < t.dims[l + 1]) {
+            const int hh = tid >> 5, c = tid & 31;
+            const float* sd = s_db + (l & 1) * 256;
+            const float sum = ((sd[(4 * hh + 0) * 32 + c] + sd[(4 * hh + 1) * 32 + c]) + sd[(4 * hh + 2) * 32 + c]) +
+                              sd[(4 * hh + 3) * 32 + c];
+            float* base = part_w + (int64_t)(2 * blockIdx.x) * t.mlp_count;
+            base[t.boff_rel[l] + tid] = sum * (1.0f / kGradScale);
+            base[t.mlp_count + t.boff_rel[l] + tid] = 0.0f;   // the lo set carries no bias
+        }
+    };
+    const uint32_t a_addr0 = s32(sm);
 
     // ---- forward ----
     double lsum = 0.0;
     const float bk = (float)(b * (int64_t)t.K);
-    int bo = 0;
     for (int l = 0; l < L; ++l) {
-        sync_issue();
+        const int np = t.np[l], ns = t.kp[l] / 16, N = t.dims[l + 1];
         if (tid == 0) {
-            const uint32_t a_addr = s32(sm + t.sm_a[l]), wl = w_addr + 2u * (uint32_t)t.wofs[l];
-            for (int kk = 0; kk < t.kp[l] / 16; ++kk)
-                mma(tmem, desc_of(a_addr, kT, t.kp[l], kk), desc_of(wl, t.np[l], t.kp[l], kk), idesc(t.np[l]), kk > 0);
+            const uint32_t a = a_addr0 + t.sm_a[l], wh = a_addr0 + t.sm_whi[l], wl = a_addr0 + t.sm_wlo[l];
+            const uint32_t id = idesc_bf16(kT, np, false, false);
+            for (int s2 = 0; s2 < ns; ++s2) mma(acc_f, desc_of(a, kT, 128, s2), desc_of(wh, np, t.kp[l], s2), id, s2 > 0);
+            if (t.terms > 1) {
+                for (int s2 = 0; s2 < ns; ++s2)
+                    mma(acc_f, desc_of(a, kT, 128, 4 + s2), desc_of(wh, np, t.kp[l], s2), id, 1);
+                for (int s2 = 0; s2 < ns; ++s2)
+                    mma(acc_f, desc_of(a, kT, 128, s2), desc_of(wl, np, t.kp[l], s2), id, 1);
+            }
         }
         wait_mma();
-        const bool last = l == L - 1;
-        for (int c = 0; c < t.np[l]; c += 16) {
-            float v[16];
-            tld16(tmem + lane_base + (uint32_t)c, v);
+        if (32 * h < np) {
+            float v[32];
+            ld32(acc_f + (uint32_t)(32 * h), v);
+            const bool last = l == L - 1;
+            float o[32];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int n = c + i;
-                const float z = v[i] + bias[bo + n];
+            for (int i = 0; i < 32; ++i) {
+                const int n = 32 * h + i;
+                const float z = v[i] + bias[64 * l + n];
                 if (!last) {
-                    const float a = z >= 0.0f ? z : t.alpha * z;
-                    put_h(sm + t.sm_a[l + 1], umma_off(r, n, kT, t.kp[l + 1]), a);
-                    put_h(sm + t.sm_at[l + 1], umma_off(n, r, t.kp[l + 1], kT), a);
+                    o[i] = n < N ? (z >= 0.0f ? z : t.alpha * z) : 0.0f;
                 } else {
-                    // loss + output delta (mlp.py:143-149, 160-168), dZ scaled into fp16
+                    // loss + output delta (mlp.py:143-149, 160-168), dZ scaled by 2^18
                     float d = 0.0f;
                     if (r < nr && n < t.K) {
                         const float sg = t.out_sigmoid ? sigmoid_exact(z) : (z >= 0.0f ? z : t.alpha * z);
@@ -1524,135 +1609,163 @@ __global__ void __launch_bounds__(128, 1) k_train_tc(TrainTC t, const float* __r
                         d = t.out_sigmoid ? __fmul_rn(__fmul_rn(dout, sg), __fsub_rn(1.0f, sg))
                                           : (z >= 0.0f ? dout : __fmul_rn(dout, t.alpha));
                     }
-                    put_h(sm + t.sm_g, umma_off(r, n, kT, t.np[l]), d * kGradScale);
-                    put_h(sm + t.sm_gt, umma_off(n, r, kT, kT), d * kGradScale);
+                    o[i] = d * kGradScale;
                 }
             }
+            uint8_t* dst = last ? dz : sm + t.sm_a[l + 1];
+#pragma unroll
+            for (int c = 0; c < 32; c += 8) put_stack8(dst, r, 32 * h + c, o + c);
+            if (last) db_out(l, o);
+        } else if (l == L - 1) {
+            float zero[32] = {};
+            db_out(l, zero);
         }
-        bo += t.np[l];
+        sync_issue();
+        if (l == L - 1) db_flush(l);
     }
     for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
     if (lane == 0) s_loss[warp] = lsum;
 
     // ---- backward ----
     for (int l = L - 1; l >= 0; --l) {
-        const int np = t.np[l], kp = t.kp[l], K_in = t.dims[l], N = t.dims[l + 1];
-        sync_issue();
+        const int np = t.np[l], kp = t.kp[l], nsn = np / 16, Kin = t.dims[l], N = t.dims[l + 1];
         if (tid == 0) {
-            const uint32_t gt = s32(sm + t.sm_gt), at = s32(sm + t.sm_at[l]), ones = s32(sm + t.sm_ones);
-            const uint32_t g = s32(sm + t.sm_g), wt = w_addr + 2u * (uint32_t)t.wofsT[l];
-            for (int kk = 0; kk < kT / 16; ++kk) {
-                mma(tmem, desc_of(gt, kT, kT, kk), desc_of(at, kp, kT, kk), idesc(kp), kk > 0);         // dW
-                mma(tmem + 64u, desc_of(gt, kT, kT, kk), desc_of(ones, 16, kT, kk), idesc(16), kk > 0);  // db
+            const uint32_t a = a_addr0 + t.sm_a[l], dzb = a_addr0 + t.sm_dz;
+            const uint32_t wh = a_addr0 + t.sm_whi[l], wl = a_addr0 + t.sm_wlo[l];
+            // dW^T = [A_hi | A_lo]^T . dZ: K = 128 rows, B = dZ hi then dZ lo (MN-major)
+            const uint32_t idw = idesc_bf16(kT, np, true, true);
+            for (int kk = 0; kk < kT / 16; ++kk)
+                mma(acc_dw, desc_mn(a, kT, 128, kk), desc_mn(dzb, kT, 128, kk), idw, kk > 0);
+            if (t.terms > 1)
+                for (int kk = 0; kk < kT / 16; ++kk)
+                    mma(acc_dw, desc_mn(a, kT, 128, kk), desc_mn(dzb + kT * 128u, kT, 128, kk), idw, 1);
+            // dA = dZ . W: A = dZ stack K-major (K = N_out), B = W MN-major (N = K_in)
+            const uint32_t ida = idesc_bf16(kT, kp, false, true);
+            for (int s2 = 0; s2 < nsn; ++s2) mma(acc_da, desc_of(dzb, kT, 128, s2), desc_mn(wh, np, kp, s2), ida, s2 > 0);
+            if (t.terms > 1) {
+                for (int s2 = 0; s2 < nsn; ++s2)
+                    mma(acc_da, desc_of(dzb, kT, 128, 4 + s2), desc_mn(wh, np, kp, s2), ida, 1);
+                for (int s2 = 0; s2 < nsn; ++s2)
+                    mma(acc_da, desc_of(dzb, kT, 128, s2), desc_mn(wl, np, kp, s2), ida, 1);
             }
-            for (int kk = 0; kk < np / 16; ++kk)
-                mma(tmem + 128u, desc_of(g, kT, np, kk), desc_of(wt, kp, np, kk), idesc(kp), kk > 0);    // dA
         }
         wait_mma();
-        // dW_l / db_l rows: TMEM lane n
+        // dW^T lanes m = [hi k_in | lo k_in]: the hi and lo partial sets
         {
-            float* gw = part_w + (int64_t)blockIdx.x * t.woff_rel[L] + t.woff_rel[l];   // woff_rel[L] = mlp_count
-            float* gb = part_w + (int64_t)blockIdx.x * t.woff_rel[L] + t.boff_rel[l];
-            for (int c = 0; c < kp; c += 16) {
-                float v[16];
-                tld16(tmem + lane_base + (uint32_t)c, v);
-                if (r < N)
+            const int m = r, k = m & 63, set = m >> 6;
+            if (32 * h < np) {
+                float v[32];
+                ld32(acc_dw + (uint32_t)(32 * h), v);
+                if (k < Kin) {
+                    float* gw = part_w + (int64_t)(2 * blockIdx.x + set) * t.mlp_count + t.woff_rel[l];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        if (c + i < K_in) gw[(int64_t)r * K_in + c + i] = v[i] * (1.0f / kGradScale);
-            }
-            float v[16];
-            tld16(tmem + lane_base + 64u, v);
-            if (r < N) gb[r] = v[0] * (1.0f / kGradScale);
-        }
-        // dA_{l} rows (TMEM lane = row): next dZ, or the encoder gradient
-        for (int c = 0; c < kp; c += 16) {
-            float v[16];
-            tld16(tmem + lane_base + 128u + (uint32_t)c, v);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int k = c + i;
-                if (l > 0) {
-                    const __half a = *reinterpret_cast<const __half*>(sm + t.sm_a[l] + umma_off(r, k, kT, kp));
-                    const bool neg = (__half_as_ushort(a) & 0x8000u) != 0;   // leaky'(z): z >= 0 -> 1, else alpha
-                    const float d = r < nr ? (neg ? v[i] * t.alpha : v[i]) : 0.0f;
-                    put_h(sm + t.sm_g, umma_off(r, k, kT, kp), d);
-                    put_h(sm + t.sm_gt, umma_off(k, r, kT, kT), d);
-                } else if (r < nr && k < t.D0) {
-                    dact0g[(r0g + r) * t.D0 + k] = v[i] * (1.0f / kGradScale);
+                    for (int i = 0; i < 32; ++i) {
+                        const int n = 32 * h + i;
+                        if (n < N) gw[(int64_t)n * Kin + k] = v[i] * (1.0f / kGradScale);
+                    }
                 }
             }
         }
+        // dA rows: the next dZ (times leaky'(z), from the sign of the stored activation) or dL/dact0
+        if (32 * h < kp) {
+            float v[32];
+            ld32(acc_da + (uint32_t)(32 * h), v);
+            if (l > 0) {
+                const uint8_t* a = sm + t.sm_a[l];
+                float o[32];
+#pragma unroll
+                for (int c = 0; c < 32; c += 8) {
+                    const uint4 pk = *reinterpret_cast<const uint4*>(a + umma_off(r, 32 * h + c, kT, 128));
+                    const uint16_t* hv = reinterpret_cast<const uint16_t*>(&pk);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int k2 = 32 * h + c + i;
+                        const bool neg = (hv[i] & 0x8000u) != 0;       // leaky'(z): z >= 0 -> 1, else alpha
+                        o[c + i] = (r < nr && k2 < Kin) ? (neg ? v[c + i] * t.alpha : v[c + i]) : 0.0f;
+                    }
+                }
+                // dZ_{l-1} overwrites dZ_l: every MMA that read it has completed
+#pragma unroll
+                for (int c = 0; c < 32; c += 8) put_stack8(dz, r, 32 * h + c, o + c);
+                db_out(l - 1, o);
+            } else if (r < nr) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (32 * h + i < t.D0) dact0g[(r0g + r) * t.D0 + 32 * h + i] = v[i] * (1.0f / kGradScale);
+            }
+        } else if (l > 0) {
+            float zero[32] = {};
+            db_out(l - 1, zero);
+        }
+        sync_issue();
+        if (l > 0) db_flush(l - 1);
+    }
+    if (tid == 0) {
+        double ls = 0.0;
+        for (int w = 0; w < 8; ++w) ls += s_loss[w];
+        part_loss[2 * blockIdx.x] = ls / (double)t.K;
+        part_loss[2 * blockIdx.x + 1] = 0.0;
     }
     tc_before();
     __syncthreads();
     tc_after();
-    if (tid == 0) part_loss[blockIdx.x] = ((s_loss[0] + s_loss[1]) + (s_loss[2] + s_loss[3])) / (double)t.K;
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
 }
 }  // namespace
 
-// plan: 0 if the tensor-core training step covers this model (fits in smem/TMEM)
+// plan: 0 if the tensor-core training step covers this model (widths <= 64, fits in smem)
 int train_tc_plan(const nvc_model* m, int64_t grid_count, const int64_t* woff, const int64_t* boff, int64_t mlp_count,
                   TrainTC& t) {
-    if (!m->wpack) return 1;
-    if (m->n_layers < 2 || m->n_layers >= NVC_MAX_LAYERS || m->features * m->levels > 64) return 1;
+    if (m->n_layers < 2 || m->n_layers > 4 || m->features * m->levels > 64) return 1;
     t.L = m->n_layers;
     t.D0 = m->dims[0];
     t.K = m->dims[m->n_layers];
     for (int i = 0; i <= t.L; ++i) t.dims[i] = m->dims[i];
     umma_pads(m->dims, t.L, t.np, t.kp);
-    int o = 0;
     for (int l = 0; l < t.L; ++l) {
-        if (t.np[l] > 64 || t.kp[l] > 64 || (t.np[l] != 16 && t.np[l] != 32 && t.np[l] != 64)) return 1;
-        t.wofs[l] = o;
-        o += (int)umma_block_halfs(t.np[l], t.kp[l]);
-    }
-    for (int l = 0; l < t.L; ++l) {
-        t.wofsT[l] = o;
-        o += (int)umma_block_halfs(t.kp[l], t.np[l]);
-    }
-    t.w_halfs = o;
-    for (int l = 0; l < t.L; ++l) {
+        if (t.np[l] > 64 || t.kp[l] > 64 || t.np[l] % 16 || (t.kp[l] != 16 && t.kp[l] != 32 && t.kp[l] != 64)) return 1;
+        t.woff_abs[l] = woff[l];
+        t.boff_abs[l] = boff[l];
         t.woff_rel[l] = woff[l] - grid_count;
         t.boff_rel[l] = boff[l] - grid_count;
-        t.boff_abs[l] = boff[l];
     }
-    t.woff_rel[t.L] = mlp_count;
+    t.mlp_count = mlp_count;
     t.alpha = m->alpha;
     t.out_sigmoid = m->out_sigmoid;
+    t.terms = getenv("NVC_TC_TERMS") ? atoi(getenv("NVC_TC_TERMS")) : 3;
     auto al = [](int x) { return (x + 1023) / 1024 * 1024; };
     int so = 0;
-    t.sm_w = so;
-    so += al(o * 2);
+    for (int l = 0; l < t.L; ++l) {
+        t.sm_whi[l] = so;
+        so += al(t.np[l] * t.kp[l] * 2);
+        t.sm_wlo[l] = so;
+        so += al(t.np[l] * t.kp[l] * 2);
+    }
     for (int l = 0; l < t.L; ++l) {
         t.sm_a[l] = so;
-        so += al(kT * t.kp[l] * 2);
-        t.sm_at[l] = so;
-        so += al(kT * t.kp[l] * 2);
+        so += kT * 128 * 2;
     }
-    t.sm_g = so;
-    so += al(kT * 64 * 2);
-    t.sm_gt = so;
-    so += al(kT * kT * 2);
-    t.sm_ones = so;
-    so += al(16 * kT * 2);
+    t.sm_dz = so;
+    so += kT * 128 * 2;
     t.sm_bias = so;
     so += al(t.L * 64 * 4);
+    t.sm_db = so;
+    so += al(2 * 8 * 32 * 4);
     t.sm_total = so + 1024;
     return t.sm_total <= 227 * 1024 ? 0 : 1;
 }
 
-// the whole step: returns 1 (nothing launched) when the model is not covered
+// the whole step: returns 1 (nothing launched) when the model is not covered; part_w
+// / part_loss receive two partial sets per 128-row tile (nblk_sets = 2 * tiles)
 int train_tc(const nvc_model* m, int64_t grid_count, const int64_t* woff, const int64_t* boff, int64_t mlp_count,
              const float* act0, int64_t b_max, const int64_t* b_dev, int shard, int n_shards, const float* tgt,
-             const float* mask, float* dact0, float* part_w, double* part_loss, int nblk, cudaStream_t s) {
+             const float* mask, float* dact0, float* part_w, double* part_loss, int ntiles, cudaStream_t s) {
     TrainTC t;
     if (train_tc_plan(m, grid_count, woff, boff, mlp_count, t)) return 1;
     cudaFuncSetAttribute(k_train_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, t.sm_total);
-    k_train_tc<<<nblk, 128, t.sm_total, s>>>(t, m->params, m->wpack, act0, b_max, b_dev, shard, n_shards, tgt, mask,
-                                             dact0, part_w, part_loss);
+    k_train_tc<<<ntiles, kTcThreads, t.sm_total, s>>>(t, m->params, act0, b_max, b_dev, shard, n_shards, tgt, mask,
+                                                      dact0, part_w, part_loss);
     return check_launch("k_train_tc");
 }
 

@@ -177,6 +177,26 @@ def test_c2_loss_curve_60_frames(c2_trained, g_curves):
     assert got[-1] < 0.2 * got[0]        # it learned
 
 
+def test_c2_loss_curve_60_frames_tensor_core_training(g_curves, monkeypatch):
+    """The same 60 C2 frames with the training step on the tensor cores
+    (k_train_tc: tcgen05 forward + backward, split bf16 operands ~16 bits, fp32
+    TMEM accumulators).  Its gradients are ~1e-5 from fp32 (vs ~1e-7 for the
+    SIMT step) and Adam's m/sqrt(v) turns sign changes of near-zero hash-grid
+    gradients into full-size steps, so the curve tracks the reference to 1e-3
+    over the first 10 frames and then drifts (measured max ~16 % by frame 60,
+    printed here) -- which is why the fp32 SIMT step stays the default."""
+    monkeypatch.setenv("NVC_TRAIN_TC", "1")
+    scene = scene_from_dict(boxes_scene(32))
+    c = VisibilityCache(MODE_LIGHTS, 32, grid_cfg(scene, 16, 1 << 19), seed=0, hidden_dims=(64, 64, 64))
+    got = np.array([train_frame(scene, scene.camera, c, TrainFrameConfig(), frame=f) for f in range(60)])
+    ref32, ref64 = g_curves["c2_loss60_f32"], g_curves["c2_loss60_f64"]
+    rel32, rel64 = np.abs(got - ref32) / ref32, np.abs(got - ref64) / ref64
+    print(f"C2 60 frames (tensor-core training): max rel vs ref f32 {rel32.max():.2e} (mean {rel32.mean():.2e}), "
+          f"vs f64 {rel64.max():.2e}; loss {got[0]:.5f} -> {got[-1]:.5f}")
+    assert rel32[:10].max() < 1e-3 and rel64[:10].max() < 1e-3
+    assert got[-1] < 0.2 * got[0]        # it learns
+
+
 def test_c2_trained_inference_vs_oracle(c2_trained, g_curves):
     """The GPU-trained C2 cache (60 frames) vs the oracle on the SAME parameters,
     at 4096 random probes and 1080p G-buffer pixels: fp32 path within 1e-5,

@@ -523,8 +523,10 @@ class TestTraining:
         p = p0.copy()
         for t in range(3):
             gd = (g.standard_normal(p0.size) * 10.0 ** g.integers(-7, 0, p0.size))
-            fx = np.rint(gd * 2.0 ** 48).astype(np.int64)
-            gf = (fx.astype(np.float64) * 2.0 ** -48).astype(np.float32)   # what the kernel reads
+            # fixed point: 2^-48 for the hash table, 2^-58 for the MLP (common.cuh)
+            scale = np.where(np.arange(p0.size) < c.grid_cfg.param_count, 2.0 ** 48, 2.0 ** 58)
+            fx = np.rint(gd * scale).astype(np.int64)
+            gf = (fx.astype(np.float64) / scale).astype(np.float32)   # what the kernel reads
             c.grad_fx.copy_(torch.from_numpy(fx))
             lr = 0.05 - 0.001 * t
             c.step = 0
@@ -590,21 +592,45 @@ class TestTraining:
         assert np.max(np.abs(np.array(got) - ref64) / ref64) < 1e-2
 
     def test_tensor_core_training_step(self, pbox8, g_train, monkeypatch):
-        """Opt-in tcgen05 training step (fp16 operands, fp32 TMEM accumulators, 2^18
-        gradient scaling): deterministic, first-step loss exact to 1e-6, and the C1
-        loss curve within 3 % of the reference's (fp32 SIMT path: 1 %)."""
+        """tcgen05 training step (split bf16 operands, fp32 TMEM accumulators):
+        deterministic, first-step loss and weights at the fp32 path's tolerances,
+        the C1 loss curve within the same 1e-2 band as the fp32 SIMT step."""
         monkeypatch.setenv("NVC_TRAIN_TC", "1")
         c = self._c1(pbox8)
         loss = c.train_step(g_train["c1_pos"], g_train["c1_tgt"].astype(np.float32))
         assert loss == pytest.approx(float(g_train["c1_step0_loss"]), rel=1e-6)
-        np.testing.assert_allclose(c.net_params.weights[0], g_train["c1_step0_w0"], atol=0.01)
+        np.testing.assert_allclose(c.net_params.weights[0], g_train["c1_step0_w0"], atol=2e-6)
         c = self._c1(pbox8)
         want = g_train["c1_loss_f32"]
         got = [train_frame(pbox8, pbox8.camera, c, TrainFrameConfig(), frame=f) for f in range(len(want))]
-        np.testing.assert_allclose(got, want, rtol=3e-2)
+        np.testing.assert_allclose(got, want, rtol=1e-2)
         c2 = self._c1(pbox8)
         again = [train_frame(pbox8, pbox8.camera, c2, TrainFrameConfig(), frame=f) for f in range(len(want))]
         assert got == again
+
+    def test_tensor_core_gradients_match_fp32(self, boxes32, g_train, monkeypatch):
+        """The tcgen05 step's gradients against the fp32 SIMT step's on a C2-shaped
+        batch: MLP gradients within 1e-3 of each block's largest (w0 is the worst,
+        ~6e-4: the init-scale features), hash-grid gradients within 1e-4 relative
+        for 99 % of the touched entries (the rest: leaky-ReLU kinks, z ~ 0)."""
+        pos = torch.from_numpy(g_train["b32_pos"]).to(DEV)
+        tgt = torch.from_numpy(g_train["b32_tgt"].astype(np.float32)).to(DEV)
+        out = []
+        for tc in (False, True):
+            if tc:
+                monkeypatch.setenv("NVC_TRAIN_TC", "1")
+            c = VisibilityCache(MODE_LIGHTS, 32, grid_cfg(boxes32, 16, 1 << 19), seed=0, hidden_dims=(64, 64, 64))
+            c.set_compact(False)
+            c.accumulate_grads(pos, tgt)
+            out.append(c.grad_fx.double().cpu().numpy() * 2.0 ** -48)
+        a, b = out
+        n = c.grid_cfg.param_count
+        for (wo, bo), (fo, fi) in zip(c._layer_offs, c.net_cfg.layer_dims):
+            for sl in (slice(wo, wo + fo * fi), slice(bo, bo + fo)):
+                assert np.abs(a[sl] - b[sl]).max() <= 1e-3 * np.abs(a[sl]).max()
+        live = np.abs(a[:n]) > 1e-3 * np.abs(a[:n]).max()
+        rel = np.abs(a[:n][live] - b[:n][live]) / np.abs(a[:n][live])
+        assert np.quantile(rel, 0.99) < 1e-4
 
     def test_bitwise_deterministic_trajectory(self, pbox8):
         def run():
@@ -640,7 +666,7 @@ class TestTraining:
         gc = full.grid_cfg.param_count
         np.testing.assert_array_equal(full.grad_fx[:gc].cpu().numpy(), shards[0].grad_fx[:gc].cpu().numpy())
         np.testing.assert_allclose(full.grad_fx[gc:].double().cpu().numpy(),
-                                   shards[0].grad_fx[gc:].double().cpu().numpy(), rtol=1e-5, atol=2.0 ** 48 * 1e-9)
+                                   shards[0].grad_fx[gc:].double().cpu().numpy(), rtol=1e-5, atol=2.0 ** 58 * 1e-9)
 
     def test_wide_split_train_equals_fused_kernel(self, boxes32, monkeypatch):
         """C4 widths (3x128 hidden, 128 outputs): the split step with W read from L1/L2
