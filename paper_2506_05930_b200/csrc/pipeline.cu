@@ -934,27 +934,20 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
     const uint64_t n_lp = a.offset + (uint64_t)a.p_total * (uint64_t)a.K + 2ull * (uint64_t)gp;
     double s = 0.0, wsel = 0.0, u0 = 0.0, u1 = 0.0;
     int sel = -1;
-    while (jobs) {
-        const int g = (KW > 2) ? __ffsll((long long)jobs) - 1 : __ffs((uint32_t)jobs) - 1;
-        jobs &= jobs - 1;
-        const bool lpj = g == 8 * KW;
+    // one 4-light group: its luminances (nonzero lights only) and visibility pair
+    auto group_in = [&](int g, LT t[4], uint2& vg, uint32_t& bits) {
         uint32_t mw = 0u;
 #pragma unroll
         for (int w = 0; w < KW; ++w)
             if ((g >> 3) == w) mw = m[w];
-        const uint32_t bits = lpj ? 0u : (mw >> (4 * (g & 7))) & 15u;
-        LT t[4];
+        bits = (mw >> (4 * (g & 7))) & 15u;
 #pragma unroll
         for (int j = 0; j < 4; ++j) t[j] = ((bits >> j) & 1u) ? __ldg(lp + (int64_t)(4 * g + j) * a.stride) : LT(0);
-        uint2 vg = make_uint2(0u, 0u);
-        if (!kStage && !lpj) vg = __ldg(reinterpret_cast<const uint2*>(a.vis16 + p * a.vstride) + g);
-        const U4 u = philox_block(lpj ? n_lp / 4 + 1 : c_grp + (uint64_t)g, a.key);
-        if (lpj) {
-            const bool hi = (n_lp & 2) != 0;
-            u0 = u01(hi ? u.x[2] : u.x[0]);
-            u1 = u01(hi ? u.x[3] : u.x[1]);
-            break;
-        }
+        vg = make_uint2(0u, 0u);
+        if (!kStage) vg = __ldg(reinterpret_cast<const uint2*>(a.vis16 + p * a.vstride) + g);
+    };
+    // the group's lights in order into the FP64 reservoir
+    auto group_wrs = [&](int g, const LT t[4], uint2 vg, uint32_t bits, const U4& u) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if ((bits >> j) & 1u) {
@@ -969,6 +962,29 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
                 }
             }
         }
+    };
+    auto light_pair = [&](const U4& u) {
+        const bool hi = (n_lp & 2) != 0;
+        u0 = u01(hi ? u.x[2] : u.x[0]);
+        u1 = u01(hi ? u.x[3] : u.x[1]);
+    };
+    const int lp_job = 8 * KW;
+    {
+        while (jobs) {
+            const int g = (KW > 2) ? __ffsll((long long)jobs) - 1 : __ffs((uint32_t)jobs) - 1;
+            jobs &= jobs - 1;
+            const bool lpj = g == lp_job;
+            LT t[4];
+            uint2 vg;
+            uint32_t bits = 0u;
+            if (!lpj) group_in(g, t, vg, bits);
+            const U4 u = philox_block(lpj ? n_lp / 4 + 1 : c_grp + (uint64_t)g, a.key);
+            if (lpj) {
+                light_pair(u);
+                break;
+            }
+            group_wrs(g, t, vg, bits, u);
+        }
     }
     double y[3];
     light_point(sc, sel, u0, u1, y);
@@ -982,10 +998,11 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
 template <int KW>
 void launch_nlsg(const WArgs& a, const nvc_scene& sc, int64_t P, cudaStream_t s) {
     const int thr = kWrsThreads;
+    const int grid = (int)((P + thr - 1) / thr);
     if (a.lum_f64)
-        k_nls32g<true, KW><<<(int)((P + thr - 1) / thr), thr, 0, s>>>(a, sc);
+        k_nls32g<true, KW><<<grid, thr, 0, s>>>(a, sc);
     else
-        k_nls32g<false, KW><<<(int)((P + thr - 1) / thr), thr, 0, s>>>(a, sc);
+        k_nls32g<false, KW><<<grid, thr, 0, s>>>(a, sc);
 }
 
 // Neural DI for K <= 32 (sampling.py:215-218): rgb = (sum_k v_k * factor_k *
