@@ -303,16 +303,24 @@ def gpu_arm(args) -> None:
     shade = args.workload == "render"
     rgb_buf = [torch.empty((P, 3), dtype=torch.float64, device=dev) for _ in range(2)] if shade else [None, None]
 
+    # NVC_DIAG=no-train / no-query (diagnostics only, never a bench value): drop one
+    # half of the frame to see which work bounds the overlapped frame
+    diag = os.environ.get("NVC_DIAG", "")
+
     def frame_into(f, outs, timed_parts=None, rgb=None):
         if timed_parts is not None:
             marks[0].record(stream)
-        loss, bufs = train_frame_device(scene, cam, cache, cfg, frame=f, shard=rank, n_shards=world,
-                                        comm=comm if world > 1 else None, pipeline=pipe)
-        last_bufs[0] = bufs
+        if diag != "no-train" or f < args.warmup:
+            loss, bufs = train_frame_device(scene, cam, cache, cfg, frame=f, shard=rank, n_shards=world,
+                                            comm=comm if world > 1 else None, pipeline=pipe)
+            last_bufs[0] = bufs
+        else:
+            loss = last_bufs[0].loss[1]
         if timed_parts is not None:
             marks[1].record(stream)
-        nls_sample_device(ctx, cache, R.stream_key(0, f, "light-select"), 0, p_first=p_first, p_total=p_total,
-                          out=outs, select_stream=None if timed_parts is not None else sel_stream)
+        if diag != "no-query":
+            nls_sample_device(ctx, cache, R.stream_key(0, f, "light-select"), 0, p_first=p_first, p_total=p_total,
+                              out=outs, select_stream=None if timed_parts is not None else sel_stream)
         if timed_parts is not None:
             marks[2].record(stream)
         if shade:   # pass 5: one shadow ray per pixel to its NLS-selected light point
@@ -356,7 +364,8 @@ def gpu_arm(args) -> None:
         frame(args.warmup + f, timed_parts=True)
         _lib.call("nvc_profile_stages", 0)
         marks[3 if shade else 2].synchronize()
-        _lib.call("nvc_profile_stage_ms", ctypes.addressof(kms))
+        if diag != "no-query":
+            _lib.call("nvc_profile_stage_ms", ctypes.addressof(kms))
         if shade:
             split_shade.append(marks[2].elapsed_time(marks[3]))
         split_train.append(marks[0].elapsed_time(marks[1]))
@@ -385,6 +394,10 @@ def gpu_arm(args) -> None:
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
+    if diag:                          # diagnostics: the frame time only, never a bench line
+        if rank == 0:
+            print(json.dumps({"diag": diag, "ms_per_step": ms, "steps": args.steps}), flush=True)
+        return
 
     # ---- e2e: host G-buffer positions in, (ids, points, W, loss) out, every frame ----
     # Copies run on their own streams (H2D and D2H engines) double-buffered
