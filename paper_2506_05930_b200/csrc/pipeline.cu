@@ -236,8 +236,8 @@ NVC_FHFMA(fhfma_hi_hi, "ya", "yb")
 // parity encoder, and the trilinear blend with fp16 operands (table entries,
 // corner weights rounded once) and an fp32 accumulator -- the same contract as
 // the tensor-core MLP that consumes the tile; fp16 only on the final store.
-template <int L>
-__global__ void __launch_bounds__(kT, 8) k_enc_tiles2(GridDev g, const uint16_t* __restrict__ table2,
+template <int L, int kMinBlocks = 8>
+__global__ void __launch_bounds__(kT, kMinBlocks) k_enc_tiles2(GridDev g, const uint16_t* __restrict__ table2,
                                                       const double* __restrict__ pos, int64_t P, int kp0,
                                                       uint8_t* __restrict__ tiles) {
     const int row = threadIdx.x;
@@ -1267,9 +1267,20 @@ int run_front(const nvc_model* m, const double* pos, int64_t P, uint8_t* tiles, 
     // k_enc_tiles2 addresses the x-pair table with 32-bit byte offsets
     const bool h2 = !getenv("NVC_ENC_F32") && (int64_t)g.L * g.T * 8 <= 0xffffffffll;
     if (g.F == 2 && g.L == 16 && h2)
-        k_enc_tiles2<16><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
+    {
+        // 10 resident CTAs per SM: the compiler fits the unrolled levels in 48
+        // registers with 4 B of spill, and the extra warps hide more gather
+        // latency (154 vs 162 us at the 64-register / 8-CTA budget, which
+        // spills 32 B; 6, 7, 12 and 16 CTAs measured 160-181 us).
+        // NVC_ENC_BLOCKS=8 selects the 8-CTA build (A/B).
+        const char* eb = getenv("NVC_ENC_BLOCKS");
+        if (eb && atoi(eb) == 8)
+            k_enc_tiles2<16, 8><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
+        else
+            k_enc_tiles2<16, 10><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
+    }
     else if (g.F == 2 && g.L == 8 && h2)
-        k_enc_tiles2<8><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
+        k_enc_tiles2<8, 10><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
     else if (g.F == 2)
         k_enc_tiles<true><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
     else
