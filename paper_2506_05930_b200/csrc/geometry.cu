@@ -1057,7 +1057,8 @@ __global__ void __launch_bounds__(1024) k_morton_order(nvc_scene sc, const doubl
 
 // compute_visibility_targets over Morton-ordered rows: block = 4 warps x 32
 // sorted rows, blockIdx.y = light.  Same per-(row, light) arithmetic as k_targets.
-__global__ void __launch_bounds__(128) k_targets_sorted(nvc_scene sc, uint64_t key, const double* __restrict__ pos,
+template <int kMinBlocks>
+__global__ void __launch_bounds__(128, kMinBlocks) k_targets_sorted(nvc_scene sc, uint64_t key, const double* __restrict__ pos,
                                                         const int64_t* __restrict__ n_rows, int64_t b_host, int shard,
                                                         int n_shards, const int32_t* __restrict__ order,
                                                         float* __restrict__ tgt) {
@@ -1609,7 +1610,8 @@ int nvc_gen_train_batch(const nvc_scene* sc, const nvc_camera* cam, uint64_t key
             cudaFuncSetAttribute(k_morton_order, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             k_morton_order<<<1, 1024, smem, s>>>(*sc, pos, n_rows, 0, shard, n_shards, order);
             dim3 g(grid1(cap, 128), sc->n_lights);
-            k_targets_sorted<<<g, 128, 0, s>>>(*sc, key_targets, pos, n_rows, 0, shard, n_shards, order, tgt);
+            // 8 resident CTAs per SM (64 registers): 0.322 vs 0.326 ms for the train-only frame
+            k_targets_sorted<8><<<g, 128, 0, s>>>(*sc, key_targets, pos, n_rows, 0, shard, n_shards, order, tgt);
         } else {
             k_targets<<<grid1(cap, 4), 128, 0, s>>>(*sc, key_targets, 0, pos, n_rows, 0, shard, n_shards, cap, tgt);
         }
