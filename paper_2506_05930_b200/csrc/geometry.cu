@@ -1610,8 +1610,9 @@ int nvc_gen_train_batch(const nvc_scene* sc, const nvc_camera* cam, uint64_t key
             cudaFuncSetAttribute(k_morton_order, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             k_morton_order<<<1, 1024, smem, s>>>(*sc, pos, n_rows, 0, shard, n_shards, order);
             dim3 g(grid1(cap, 128), sc->n_lights);
-            // 8 resident CTAs per SM (64 registers): 0.322 vs 0.326 ms for the train-only frame
-            k_targets_sorted<8><<<g, 128, 0, s>>>(*sc, key_targets, pos, n_rows, 0, shard, n_shards, order, tgt);
+            // (8 resident CTAs per SM -- 64 registers -- measured 97 vs 90 us standalone and
+            // a frame within noise, so the register budget stays the compiler's)
+            k_targets_sorted<1><<<g, 128, 0, s>>>(*sc, key_targets, pos, n_rows, 0, shard, n_shards, order, tgt);
         } else {
             k_targets<<<grid1(cap, 4), 128, 0, s>>>(*sc, key_targets, 0, pos, n_rows, 0, shard, n_shards, cap, tgt);
         }
