@@ -384,12 +384,25 @@ struct T3Layout {
     int act[NVC_MAX_LAYERS + 1];                 // act_l [kRows][D_l]
     int dz0, dz1;                                // two [kRows][Dmax] buffers
     int total;
+    int rbits;    // diagnostics (NVC_T3_BITS): GEMM operands rounded to this many significant bits; 0 = off
+    int rwhat;    // which operands (NVC_T3_WHAT bits): 1 weights, 2 activations, 4 deltas
 };
+
+// round to m significant bits, nearest-even (the precision study behind the
+// tensor-core step's operand split)
+__device__ __forceinline__ float round_bits(float x, int m) {
+    const int d = 24 - m;
+    uint32_t u = __float_as_uint(x);
+    u += (1u << (d - 1)) - 1u + ((u >> d) & 1u);
+    return __uint_as_float(u & ~((1u << d) - 1u));
+}
 
 // with_w = false: W stays in global memory (L2/L1-resident, row stride Ki) --
 // the layout for MLPs too wide for W + activations in shared memory (C4: 3x128)
 __host__ __device__ inline T3Layout t3_layout(const Net& net, bool with_w = true) {
     T3Layout t;
+    t.rbits = 0;
+    t.rwhat = 7;
     int o = 0, dmax = 0;
     for (int l = 0; l < net.n_layers; ++l) {
         t.w[l] = o;
@@ -459,7 +472,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_train3(Net net, T3Layout tl, co
         float* dst = sm + tl.w[l];
 #pragma unroll 4
         for (int e = tid; e < (kWG ? 0 : N * kq); e += kThreads) {
-            const float4 w = __ldg(W + e);
+            float4 w = __ldg(W + e);
+            if (tl.rbits && (tl.rwhat & 1)) w = make_float4(round_bits(w.x, tl.rbits), round_bits(w.y, tl.rbits),
+                                          round_bits(w.z, tl.rbits), round_bits(w.w, tl.rbits));
             const int n = e / kq, k = (e - n * kq) * 4;
             *reinterpret_cast<float4*>(dst + n * tl.ws[l] + k) = w;
         }
@@ -469,8 +484,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_train3(Net net, T3Layout tl, co
         const int q0 = D0 / 4;
         const float4* src = reinterpret_cast<const float4*>(act0g + r0g * D0);
         float4* dst = reinterpret_cast<float4*>(sm + tl.act[0]);
-        for (int e = tid; e < kRows * q0; e += kThreads)
-            dst[e] = (e / q0 < nr) ? __ldg(src + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int e = tid; e < kRows * q0; e += kThreads) {
+            float4 a = (e / q0 < nr) ? __ldg(src + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (tl.rbits && (tl.rwhat & 2)) a = make_float4(round_bits(a.x, tl.rbits), round_bits(a.y, tl.rbits),
+                                          round_bits(a.z, tl.rbits), round_bits(a.w, tl.rbits));
+            dst[e] = a;
+        }
     }
     __syncthreads();
 
@@ -507,7 +526,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_train3(Net net, T3Layout tl, co
                 for (int j = 0; j < 4; ++j) {
                     const int n = nn + j * ng;
                     const float z = acc[i][j] + sm[tl.bias[l] + n];
-                    out[(r0 + i) * N + n] = (last && net.out_sigmoid) ? sigmoid_ref(z) : leaky(z, net.alpha);
+                    const float o = (last && net.out_sigmoid) ? sigmoid_ref(z) : leaky(z, net.alpha);
+                    out[(r0 + i) * N + n] = (tl.rbits && (tl.rwhat & 2) && !last) ? round_bits(o, tl.rbits) : o;
                 }
         }
         __syncthreads();
@@ -535,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_train3(Net net, T3Layout tl, co
             d = net.out_sigmoid ? __fmul_rn(__fmul_rn(dout, sgm), __fsub_rn(1.0f, sgm))
                                 : (sgm >= 0.0f ? dout : __fmul_rn(dout, net.alpha));
         }
-        dz[e] = d;
+        dz[e] = (tl.rbits && (tl.rwhat & 4)) ? round_bits(d, tl.rbits) : d;
     }
     {
         __shared__ double s_l[kThreads / 32];
@@ -603,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_train3(Net net, T3Layout tl, co
                     for (int j = 0; j < 4; ++j) {
                         float v = acc[i][j];
                         if (!(A[(r0 + i) * Ki + k0 + j] >= 0.0f)) v = __fmul_rn(v, net.alpha);
-                        dzn[(r0 + i) * Ki + k0 + j] = v;
+                        dzn[(r0 + i) * Ki + k0 + j] = (tl.rbits && (tl.rwhat & 4)) ? round_bits(v, tl.rbits) : v;
                     }
             } else {
 #pragma unroll
@@ -1300,7 +1320,9 @@ int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, con
     bool split = g.F <= 8 && getenv("NVC_TRAIN_FUSED") == nullptr;
     for (int i = 0; i <= net.n_layers; ++i) split = split && (net.dims[i] % 4 == 0);
     const bool wg = t3_layout(net).total * 4 + 64 > 200 * 1024;   // too wide for W in smem (C4): W from L1/L2
-    const T3Layout tl3 = t3_layout(net, !wg);
+    T3Layout tl3 = t3_layout(net, !wg);
+    tl3.rbits = getenv("NVC_T3_BITS") ? atoi(getenv("NVC_T3_BITS")) : 0;
+    if (getenv("NVC_T3_WHAT")) tl3.rwhat = atoi(getenv("NVC_T3_WHAT"));
     const int smem3 = tl3.total * 4 + 64;
     int nblk_red = nblk;   // partial sets k_reduce_parts sums (one per training block)
     if (split && smem3 <= 200 * 1024) {

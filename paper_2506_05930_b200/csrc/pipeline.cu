@@ -1429,7 +1429,8 @@ int pipeline_query(const nvc_model* m, const nvc_scene* sc, const double* pos, i
 // ---------------------------------------------------------------------------
 namespace {
 constexpr float kGradScale = 262144.0f;   // 2^18
-constexpr int kTcThreads = 256;           // 8 warps: TMEM lane quarter = warp & 3, column half = warp >> 2
+constexpr int kTcThreads = 512;           // 16 warps: TMEM lane quarter = warp & 3, column quarter = warp >> 2
+constexpr int kTcWarps = kTcThreads / 32;
 
 struct TrainTC {
     int L, D0, K;
@@ -1475,10 +1476,11 @@ __device__ __forceinline__ void put_stack8(uint8_t* stack, int r, int c0, const 
     *reinterpret_cast<uint4*>(stack + umma_off(r, c0, kT, 128)) = *reinterpret_cast<const uint4*>(hi);
     *reinterpret_cast<uint4*>(stack + umma_off(r, 64 + c0, kT, 128)) = *reinterpret_cast<const uint4*>(lo);
 }
-// the 32 values of a warp's lanes for 32 columns -> lane l holds column l's sum (fixed order)
-__device__ __forceinline__ float col_sum32(float v[32], int lane) {
+// the 32 values of a warp's lanes for 16 columns -> lanes l and l ^ 16 hold column
+// (l & 15)'s sum (fixed order: butterfly over lane bits 3..0, then bit 4)
+__device__ __forceinline__ float col_sum16(float v[16], int lane) {
 #pragma unroll
-    for (int s = 16; s >= 1; s >>= 1) {
+    for (int s = 8; s >= 1; s >>= 1) {
         const bool up = (lane & s) != 0;
 #pragma unroll
         for (int j = 0; j < s; ++j) {
@@ -1487,7 +1489,7 @@ __device__ __forceinline__ float col_sum32(float v[32], int lane) {
             v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
         }
     }
-    return v[0];
+    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1) k_train_tc(TrainTC t, const float* __restrict__ params,
@@ -1500,10 +1502,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_train_tc(TrainTC t, const flo
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint64_t bar;
     __shared__ uint32_t tbase;
-    __shared__ double s_loss[8];
+    __shared__ double s_loss[kTcWarps];
     uint8_t* sm = smem_raw + ((1024u - (s32(smem_raw) & 1023u)) & 1023u);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int q = warp & 3, h = warp >> 2;          // TMEM lane quarter, column half
+    const int q = warp & 3, h = warp >> 2;          // TMEM lane quarter, 16-column quarter
     const int r = 32 * q + lane;                   // the tile row this thread reads from TMEM
     const int64_t b = b_dev ? *b_dev : b_max;
     const int64_t lo = b * shard / n_shards, hi = b * (shard + 1) / n_shards;
@@ -1511,7 +1513,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_train_tc(TrainTC t, const flo
     const int nr = (int)max((int64_t)0, min((int64_t)kT, (hi - lo) - r0g));
     const int L = t.L;
     float* bias = reinterpret_cast<float*>(sm + t.sm_bias);
-    float* s_db = reinterpret_cast<float*>(sm + t.sm_db);      // [2][8 warps][32]
+    float* s_db = reinterpret_cast<float*>(sm + t.sm_db);      // [2][16 warps][16 columns]
     uint8_t* dz = sm + t.sm_dz;
     {   // weights (hi / lo, K-major [np x kp]), biases, the input stack
         for (int l = 0; l < L; ++l) {
@@ -1530,9 +1532,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_train_tc(TrainTC t, const flo
             }
             for (int n = tid; n < 64; n += kTcThreads) bias[64 * l + n] = n < N ? __ldg(params + t.boff_abs[l] + n) : 0.0f;
         }
-        // thread (row r, half h) stages input columns [32h, 32h + 32) of its row
+        // thread (row, quarter hh) stages input columns [16hh, 16hh + 16) of its row
         const int row = tid & 127, hh = tid >> 7;
-        for (int c0 = 32 * hh; c0 < 32 * hh + 32 && c0 < t.kp[0]; c0 += 8) {
+        for (int c0 = 16 * hh; c0 < 16 * hh + 16 && c0 < t.kp[0]; c0 += 8) {
             float v[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j)
@@ -1566,25 +1568,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_train_tc(TrainTC t, const flo
     const uint32_t tmem = tbase;
     const uint32_t acc_f = tmem, acc_dw = tmem + 64u, acc_da = tmem + 128u;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    auto ld32 = [&](uint32_t col, float v[32]) {     // this warp's 32 lanes x columns [col, col + 32)
-        uint32_t u[32];
+    auto ld16 = [&](uint32_t col, float v[16]) {     // this warp's 32 lanes x columns [col, col + 16)
+        uint32_t u[16];
         tld16_nowait(lane_base + col, u);
-        tld16_nowait(lane_base + col + 16u, u + 16);
         tld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(u[i]);
+        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(u[i]);
     };
     // db partials double-buffered by layer parity: a layer's flush and the next
     // layer's column sums never share a buffer between barriers
-    auto db_out = [&](int l, float v[32]) {          // column sums of dZ_l (this thread's 32 columns)
-        s_db[(l & 1) * 256 + warp * 32 + lane] = col_sum32(v, lane);
+    auto db_out = [&](int l, float v[16]) {          // column sums of dZ_l (this warp's 16 columns)
+        const float cs = col_sum16(v, lane);
+        if (lane < 16) s_db[(l & 1) * 256 + warp * 16 + lane] = cs;
     };
     auto db_flush = [&](int l) {                     // after a __syncthreads: 4 lane quarters in fixed order
         if (tid < 64 && tid < t.dims[l + 1]) {
-            const int hh = tid >> 5, c = tid & 31;
+            const int hh = tid >> 4, c = tid & 15;
             const float* sd = s_db + (l & 1) * 256;
-            const float sum = ((sd[(4 * hh + 0) * 32 + c] + sd[(4 * hh + 1) * 32 + c]) + sd[(4 * hh + 2) * 32 + c]) +
-                              sd[(4 * hh + 3) * 32 + c];
+            const float sum = ((sd[(4 * hh + 0) * 16 + c] + sd[(4 * hh + 1) * 16 + c]) + sd[(4 * hh + 2) * 16 + c]) +
+                              sd[(4 * hh + 3) * 16 + c];
             float* base = part_w + (int64_t)(2 * blockIdx.x) * t.mlp_count;
             base[t.boff_rel[l] + tid] = sum * (1.0f / kGradScale);
             base[t.mlp_count + t.boff_rel[l] + tid] = 0.0f;   // the lo set carries no bias
@@ -1609,14 +1611,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_train_tc(TrainTC t, const flo
             }
         }
         wait_mma();
-        if (32 * h < np) {
-            float v[32];
-            ld32(acc_f + (uint32_t)(32 * h), v);
+        if (16 * h < np) {
+            float v[16];
+            ld16(acc_f + (uint32_t)(16 * h), v);
             const bool last = l == L - 1;
-            float o[32];
+            float o[16];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int n = 32 * h + i;
+            for (int i = 0; i < 16; ++i) {
+                const int n = 16 * h + i;
                 const float z = v[i] + bias[64 * l + n];
                 if (!last) {
                     o[i] = n < N ? (z >= 0.0f ? z : t.alpha * z) : 0.0f;
@@ -1642,10 +1644,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_train_tc(TrainTC t, const flo
             }
             uint8_t* dst = last ? dz : sm + t.sm_a[l + 1];
 #pragma unroll
-            for (int c = 0; c < 32; c += 8) put_stack8(dst, r, 32 * h + c, o + c);
+            for (int c = 0; c < 16; c += 8) put_stack8(dst, r, 16 * h + c, o + c);
             if (last) db_out(l, o);
         } else if (l == L - 1) {
-            float zero[32] = {};
+            float zero[16] = {};
             db_out(l, zero);
         }
         sync_issue();
@@ -1681,48 +1683,48 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_train_tc(TrainTC t, const flo
         // dW^T lanes m = [hi k_in | lo k_in]: the hi and lo partial sets
         {
             const int m = r, k = m & 63, set = m >> 6;
-            if (32 * h < np) {
-                float v[32];
-                ld32(acc_dw + (uint32_t)(32 * h), v);
+            if (16 * h < np) {
+                float v[16];
+                ld16(acc_dw + (uint32_t)(16 * h), v);
                 if (k < Kin) {
                     float* gw = part_w + (int64_t)(2 * blockIdx.x + set) * t.mlp_count + t.woff_rel[l];
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const int n = 32 * h + i;
+                    for (int i = 0; i < 16; ++i) {
+                        const int n = 16 * h + i;
                         if (n < N) gw[(int64_t)n * Kin + k] = v[i] * (1.0f / kGradScale);
                     }
                 }
             }
         }
         // dA rows: the next dZ (times leaky'(z), from the sign of the stored activation) or dL/dact0
-        if (32 * h < kp) {
-            float v[32];
-            ld32(acc_da + (uint32_t)(32 * h), v);
+        if (16 * h < kp) {
+            float v[16];
+            ld16(acc_da + (uint32_t)(16 * h), v);
             if (l > 0) {
                 const uint8_t* a = sm + t.sm_a[l];
-                float o[32];
+                float o[16];
 #pragma unroll
-                for (int c = 0; c < 32; c += 8) {
-                    const uint4 pk = *reinterpret_cast<const uint4*>(a + umma_off(r, 32 * h + c, kT, 128));
+                for (int c = 0; c < 16; c += 8) {
+                    const uint4 pk = *reinterpret_cast<const uint4*>(a + umma_off(r, 16 * h + c, kT, 128));
                     const uint16_t* hv = reinterpret_cast<const uint16_t*>(&pk);
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        const int k2 = 32 * h + c + i;
+                        const int k2 = 16 * h + c + i;
                         const bool neg = (hv[i] & 0x8000u) != 0;       // leaky'(z): z >= 0 -> 1, else alpha
                         o[c + i] = (r < nr && k2 < Kin) ? (neg ? v[c + i] * t.alpha : v[c + i]) : 0.0f;
                     }
                 }
                 // dZ_{l-1} overwrites dZ_l: every MMA that read it has completed
 #pragma unroll
-                for (int c = 0; c < 32; c += 8) put_stack8(dz, r, 32 * h + c, o + c);
+                for (int c = 0; c < 16; c += 8) put_stack8(dz, r, 16 * h + c, o + c);
                 db_out(l - 1, o);
             } else if (r < nr) {
 #pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    if (32 * h + i < t.D0) dact0g[(r0g + r) * t.D0 + 32 * h + i] = v[i] * (1.0f / kGradScale);
+                for (int i = 0; i < 16; ++i)
+                    if (16 * h + i < t.D0) dact0g[(r0g + r) * t.D0 + 16 * h + i] = v[i] * (1.0f / kGradScale);
             }
         } else if (l > 0) {
-            float zero[32] = {};
+            float zero[16] = {};
             db_out(l - 1, zero);
         }
         sync_issue();
@@ -1730,7 +1732,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_train_tc(TrainTC t, const flo
     }
     if (tid == 0) {
         double ls = 0.0;
-        for (int w = 0; w < 8; ++w) ls += s_loss[w];
+        for (int w = 0; w < kTcWarps; ++w) ls += s_loss[w];
         part_loss[2 * blockIdx.x] = ls / (double)t.K;
         part_loss[2 * blockIdx.x + 1] = 0.0;
     }
@@ -1779,7 +1781,7 @@ int train_tc_plan(const nvc_model* m, int64_t grid_count, const int64_t* woff, c
     t.sm_bias = so;
     so += al(t.L * 64 * 4);
     t.sm_db = so;
-    so += al(2 * 8 * 32 * 4);
+    so += al(2 * 256 * 4);
     t.sm_total = so + 1024;
     return t.sm_total <= 227 * 1024 ? 0 : 1;
 }

@@ -179,12 +179,15 @@ def test_c2_loss_curve_60_frames(c2_trained, g_curves):
 
 def test_c2_loss_curve_60_frames_tensor_core_training(g_curves, monkeypatch):
     """The same 60 C2 frames with the training step on the tensor cores
-    (k_train_tc: tcgen05 forward + backward, split bf16 operands ~16 bits, fp32
-    TMEM accumulators).  Its gradients are ~1e-5 from fp32 (vs ~1e-7 for the
-    SIMT step) and Adam's m/sqrt(v) turns sign changes of near-zero hash-grid
-    gradients into full-size steps, so the curve tracks the reference to 1e-3
-    over the first 10 frames and then drifts (measured max ~16 % by frame 60,
-    printed here) -- which is why the fp32 SIMT step stays the default."""
+    (k_train_tc: tcgen05 forward + backward, split bf16 operands ~17 bits, fp32
+    TMEM accumulators).  The curve tracks the reference to 1e-3 over the first
+    10 frames; from frame 11 (the first loss spike at lr 0.05) any trajectory
+    whose GEMM arithmetic is not bit-faithful fp32 leaves the 1e-2 band --
+    the fp32 step with its weights rounded to 23 bits does too
+    (tools/precision_study.py, profiles/r2_precision_study.txt) -- which is why
+    the fp32 SIMT step stays the default.  What is asserted beyond frame 10 is
+    that it learns as well: the mean loss over frames 40-59 within 8 % of the
+    reference's (perturbed fp32 runs: -1 % to +5 %; this step: ~+5 %)."""
     monkeypatch.setenv("NVC_TRAIN_TC", "1")
     scene = scene_from_dict(boxes_scene(32))
     c = VisibilityCache(MODE_LIGHTS, 32, grid_cfg(scene, 16, 1 << 19), seed=0, hidden_dims=(64, 64, 64))
@@ -194,7 +197,9 @@ def test_c2_loss_curve_60_frames_tensor_core_training(g_curves, monkeypatch):
     print(f"C2 60 frames (tensor-core training): max rel vs ref f32 {rel32.max():.2e} (mean {rel32.mean():.2e}), "
           f"vs f64 {rel64.max():.2e}; loss {got[0]:.5f} -> {got[-1]:.5f}")
     assert rel32[:10].max() < 1e-3 and rel64[:10].max() < 1e-3
-    assert got[-1] < 0.2 * got[0]        # it learns
+    late = got[40:].mean() / ref32[40:].mean() - 1.0
+    print(f"frames 40-59 mean loss {got[40:].mean():.5f} vs ref {ref32[40:].mean():.5f} ({late:+.2%})")
+    assert abs(late) < 0.08 and got[-1] < 0.2 * got[0]
 
 
 def test_c2_trained_inference_vs_oracle(c2_trained, g_curves):
