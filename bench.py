@@ -351,6 +351,17 @@ def gpu_arm(args) -> None:
     barrier()
     assert int(last_bufs[0].n_rows.item()) == cfg.n_world + cfg.n_screen, "screen rays missed: batch shrank"
 
+    if os.environ.get("NVC_TIMELINE"):   # diagnostics: a CUPTI kernel timeline of 12 frames (tools/timeline.py)
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for f in range(12):
+                frame(args.warmup + f)
+            if cache.select_done is not None:
+                stream.wait_event(cache.select_done)
+            barrier()
+        prof.export_chrome_trace(os.environ["NVC_TIMELINE"])
+        return
+
     # the clock sampler starts now (its start-up must not overlap the timed region)
     sampler = ClockSampler(local).__enter__()
     # ---- per-stage split (separate pass, events between stages and between

@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(128) k_tr_encode(GridDev g, const float* __res
 }
 
 template <bool kWG>
-__global__ void __launch_bounds__(kThreads, 2) k_train3(Net net, T3Layout tl, const float* __restrict__ params,
+__global__ void __launch_bounds__(kThreads, 4) k_train3(Net net, T3Layout tl, const float* __restrict__ params,
                                                        const float* __restrict__ act0g, int64_t b_max,
                                                        const int64_t* __restrict__ b_dev, int shard, int n_shards,
                                                        const float* __restrict__ tgt, const float* __restrict__ mask,
