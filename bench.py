@@ -885,11 +885,16 @@ def cpu_baseline(steps: int = 3, warmup: int = 1) -> dict:
     return cb if cb is not None else cpu_reference()
 
 
+REF_MAX_STEPS = 50
+
+
 def reference_arm(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cb = cpu_baseline(steps=args.steps, warmup=args.warmup)
+    # one reference step is ~0.7 s of host work: at most 50 steps keep the run
+    # within a minute (the default --steps 1000 of the GPU arm would take ~12 min)
+    cb = cpu_baseline(steps=min(args.steps, REF_MAX_STEPS), warmup=args.warmup)
     frame_s = cb["frame_s"]
     value = WIDTH * HEIGHT / frame_s
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
@@ -901,7 +906,7 @@ def reference_arm(args) -> None:
                                    f"1 online frame = train batch {N_WORLD + N_SCREEN} (rows sharded over 1 ranks) "
                                    "+ NLS over all pixels",
                        "train_samples_per_s": (N_WORLD + N_SCREEN) / frame_s},
-            "impl": "reference",
+            "impl": "reference", "steps_requested": args.steps,
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
