@@ -128,8 +128,112 @@ __global__ void __launch_bounds__(128, 1) k_micro(int mode, int iters, int n, lo
     if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tm) : "memory");
 }
 
+// back-to-back MMAs issued by `issuers` warps of one CTA at once (lane 0 of
+// warp w into TMEM columns [64w, 64w + 64)), one commit each on a shared barrier
+__global__ void __launch_bounds__(128, 1) k_micro_multi(int issuers, int iters, int n, long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    uint8_t* sm = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+    for (int i = threadIdx.x; i < 48 * 1024 / 16; i += 128) reinterpret_cast<uint4*>(sm)[i] = make_uint4(0, 0, 0, 0);
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tbase)) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&bar)), "r"(issuers) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tm = tbase;
+    const uint32_t idesc = (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const int w = threadIdx.x >> 5;
+    const uint64_t ad = desc_sw128(su32(sm + w * 8192)), bd = desc_sw128(su32(sm + 32768));
+    long long t0 = clock64();
+    if ((threadIdx.x & 31) == 0 && w < issuers) {
+        for (int i = 0; i < iters; ++i)
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tm + (uint32_t)(w * n)),
+                         "l"(ad), "l"(bd), "r"(idesc), "r"(1)
+                         : "memory");
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar))
+                     : "memory");
+    }
+    asm volatile("{\n\t.reg .pred P1;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+                 "@P1 bra D_%=;\n\tbra W_%=;\nD_%=:\n\t}" ::"r"(su32(&bar)), "r"(0)
+                 : "memory");
+    long long t1 = clock64();
+    __syncthreads();
+    if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
+}
+
+// a CTA pair: back-to-back cta_group::2 MMAs (M = 256: 128 rows per SM) issued
+// by the leader CTA, one multicast commit
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_micro_pair(int iters, int n, long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    uint8_t* sm = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+    for (int i = threadIdx.x; i < 48 * 1024 / 16; i += 128) reinterpret_cast<uint4*>(sm)[i] = make_uint4(0, 0, 0, 0);
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&tbase)) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tm = tbase;
+    const uint32_t idesc = (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+    const uint64_t ad = desc_sw128(su32(sm)), bd = desc_sw128(su32(sm + 16384));
+    long long t0 = clock64();
+    if (rank == 0 && threadIdx.x == 0) {
+        for (int i = 0; i < iters; ++i)
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tm),
+                         "l"(ad), "l"(bd), "r"(idesc), "r"(1)
+                         : "memory");
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                     ::"r"(su32(&bar)), "h"((unsigned short)3)
+                     : "memory");
+    }
+    asm volatile("{\n\t.reg .pred P1;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+                 "@P1 bra D_%=;\n\tbra W_%=;\nD_%=:\n\t}" ::"r"(su32(&bar)), "r"(0)
+                 : "memory");
+    long long t1 = clock64();
+    __syncthreads();
+    if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 256;" ::"r"(tm) : "memory");
+}
+
 }  // namespace
 }  // namespace nvc
+
+extern "C" int nvc_micro_multi(int issuers, int iters, int n, int blocks, long long* out_dev, void* stream) {
+    cudaFuncSetAttribute(nvc::k_micro_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, 50 * 1024);
+    nvc::k_micro_multi<<<blocks, 128, 50 * 1024, (cudaStream_t)stream>>>(issuers, iters, n, out_dev);
+    return nvc::check_launch("k_micro_multi");
+}
+
+extern "C" int nvc_micro_pair(int iters, int n, int pairs, long long* out_dev, void* stream) {
+    cudaFuncSetAttribute(nvc::k_micro_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, 50 * 1024);
+    nvc::k_micro_pair<<<2 * pairs, 128, 50 * 1024, (cudaStream_t)stream>>>(iters, n, out_dev);
+    return nvc::check_launch("k_micro_pair");
+}
 
 extern "C" int nvc_micro(int mode, int iters, int n, int blocks, long long* out_dev, void* stream) {
     cudaFuncSetAttribute(nvc::k_micro, cudaFuncAttributeMaxDynamicSharedMemorySize, 50 * 1024);
