@@ -455,7 +455,8 @@ class VisibilityCache:
         self.model.grad_c_entries = need
 
     def set_compact(self, on: bool) -> None:
-        """Compact (default) or dense gradient accumulation; switch only between steps."""
+        """Compact gradient slots (on) or the dense fixed-point accumulator (off, the
+        default: measured faster on one GPU); switch only between steps."""
         self.compact = bool(on)
         if not on:
             self.model.grad_c = None
