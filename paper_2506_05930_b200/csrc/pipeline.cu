@@ -800,11 +800,12 @@ __device__ __forceinline__ double lum_at(const WArgs& a, int k, int64_t p) {
     else return (double)__ldg(reinterpret_cast<const float*>(a.lum) + li);
 }
 
-// w_k = max(vis_k, floor) * lum_k in binary64 (sampling.py:27-30 clamp_visibility, nls_weights_batch)
-__device__ __forceinline__ double wrs_weight(float vis, double t, double floor) {
-    double vv = (double)vis;
-    vv = floor > 0.0 ? fmax(vv, floor) : fmax(vv, 0.0);
-    return __dmul_rn(vv, t);
+// w_k = max(vis_k, floor) * lum_k in binary64 (sampling.py:27-30 clamp_visibility, nls_weights_batch);
+// lo = clamp_lo(floor) is the clamp's lower bound (the floor, or 0 in biased mode)
+__device__ __forceinline__ double clamp_lo(double floor) { return floor > 0.0 ? floor : 0.0; }
+__device__ __forceinline__ double wrs_weight(float vis, double t, double lo) {
+    const double vv = (double)vis;
+    return __dmul_rn(vv < lo ? lo : vv, t);
 }
 
 // K <= 32 (the C2 / paper configuration).  Sequential FP64 reservoir exactly
@@ -847,7 +848,7 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32(WArgs a, nvc_scene sc) {
         m &= m - 1;
         const uint32_t pair = my[k >> 1];
         const float vis = __half2float(__ushort_as_half((unsigned short)((k & 1) ? (pair >> 16) : (pair & 0xffffu))));
-        const double w = wrs_weight(vis, lum_at<kLum64>(a, k, p), a.floor);
+        const double w = wrs_weight(vis, lum_at<kLum64>(a, k, p), clamp_lo(a.floor));
         s = __dadd_rn(s, w);
         if (w > 0.0) {
             const uint64_t n = n0 + (uint64_t)k;
@@ -930,6 +931,8 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
         for (int g = 0; g < 8; ++g) jobs |= (JobT)(((m[w] >> (4 * g)) & 15u) != 0u ? 1u : 0u) << (8 * w + g);
     using LT = typename std::conditional<kLum64, double, float>::type;
     const LT* lp = reinterpret_cast<const LT*>(a.lum) + p;
+    const int64_t st1 = a.stride, st2 = 2 * st1, st3 = 3 * st1;   // light-major rows: hoisted strides
+    const double lo = clamp_lo(a.floor);
     const uint64_t c_grp = (a.offset + (uint64_t)gp * (uint64_t)a.K) / 4 + 1;
     const uint64_t n_lp = a.offset + (uint64_t)a.p_total * (uint64_t)a.K + 2ull * (uint64_t)gp;
     double s = 0.0, wsel = 0.0, u0 = 0.0, u1 = 0.0;
@@ -941,8 +944,11 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
         for (int w = 0; w < KW; ++w)
             if ((g >> 3) == w) mw = m[w];
         bits = (mw >> (4 * (g & 7))) & 15u;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) t[j] = ((bits >> j) & 1u) ? __ldg(lp + (int64_t)(4 * g + j) * a.stride) : LT(0);
+        const LT* lg = lp + (int64_t)(4 * g) * st1;
+        t[0] = (bits & 1u) ? __ldg(lg) : LT(0);
+        t[1] = (bits & 2u) ? __ldg(lg + st1) : LT(0);
+        t[2] = (bits & 4u) ? __ldg(lg + st2) : LT(0);
+        t[3] = (bits & 8u) ? __ldg(lg + st3) : LT(0);
         vg = make_uint2(0u, 0u);
         if (!kStage) vg = __ldg(reinterpret_cast<const uint2*>(a.vis16 + p * a.vstride) + g);
     };
@@ -954,7 +960,7 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
                 const int k = 4 * g + j;
                 const uint32_t pair = kStage ? my[k >> 1] : (j < 2 ? vg.x : vg.y);
                 const float vis = __half2float(__ushort_as_half((unsigned short)((j & 1) ? (pair >> 16) : (pair & 0xffffu))));
-                const double w = wrs_weight(vis, (double)t[j], a.floor);
+                const double w = wrs_weight(vis, (double)t[j], lo);
                 s = __dadd_rn(s, w);
                 if (w > 0.0 && __dmul_rn(u01(u.x[j]), s) < w) {
                     sel = k;
@@ -1093,7 +1099,7 @@ __global__ void __launch_bounds__(256) k_wrs_tiles(WArgs a, nvc_scene sc) {
             const float vis = __half2float(__ldg(a.vis16 + p * a.vstride + k));
             const double t = a.lum_f64 ? lum_at<true>(a, k, p) : lum_at<false>(a, k, p);
             if (kNls) {
-                const double w = wrs_weight(vis, t, a.floor);
+                const double w = wrs_weight(vis, t, clamp_lo(a.floor));
                 s = __dadd_rn(s, w);
                 if (w > 0.0) {   // zero weights never need a uniform (u*s < 0 is impossible)
                     const uint64_t n = a.offset + (uint64_t)gp * (uint64_t)a.K + (uint64_t)k;
