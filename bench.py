@@ -303,8 +303,8 @@ def gpu_arm(args) -> None:
     shade = args.workload == "render"
     rgb_buf = [torch.empty((P, 3), dtype=torch.float64, device=dev) for _ in range(2)] if shade else [None, None]
 
-    # NVC_DIAG=no-train / no-query (diagnostics only, never a bench value): drop one
-    # half of the frame to see which work bounds the overlapped frame
+    # NVC_DIAG=no-train / no-query / no-nls (diagnostics only, never a bench value):
+    # drop part of the frame to see which work bounds the overlapped frame
     diag = os.environ.get("NVC_DIAG", "")
 
     def frame_into(f, outs, timed_parts=None, rgb=None):
@@ -318,7 +318,10 @@ def gpu_arm(args) -> None:
             loss = last_bufs[0].loss[1]
         if timed_parts is not None:
             marks[1].record(stream)
-        if diag != "no-query":
+        if diag == "no-nls":       # encoder + MLP only (what a free NLS would leave)
+            ws = cache.query_workspace(P)
+            _lib.call("nvc_query_front", cache.model, ctx.pos.data_ptr(), P, _lib.ptr(ws), _lib.stream_ptr())
+        elif diag != "no-query":
             nls_sample_device(ctx, cache, R.stream_key(0, f, "light-select"), 0, p_first=p_first, p_total=p_total,
                               out=outs, select_stream=None if timed_parts is not None else sel_stream)
         if timed_parts is not None:
@@ -375,7 +378,7 @@ def gpu_arm(args) -> None:
         frame(args.warmup + f, timed_parts=True)
         _lib.call("nvc_profile_stages", 0)
         marks[3 if shade else 2].synchronize()
-        if diag != "no-query":
+        if diag not in ("no-query", "no-nls"):
             _lib.call("nvc_profile_stage_ms", ctypes.addressof(kms))
         if shade:
             split_shade.append(marks[2].elapsed_time(marks[3]))
