@@ -889,6 +889,10 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32(WArgs a, nvc_scene sc) {
 // Philox rounds so their latency hides behind them.  The light-point draw
 // pair is the last "group".  Same arithmetic and order as k_nls32.
 template <bool kLum64, int KW>
+__device__ __forceinline__ void nls_pixel(const WArgs& a, const nvc_scene& sc, int64_t p, uint32_t* my);
+
+// one thread per pixel (the tile loop also serves grids smaller than the pixel count)
+template <bool kLum64, int KW>
 __global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
     // KW 32-light words (K <= 32 KW).  K <= 32: the pixel's fp16 visibility row is
     // staged in shared memory with one coalesced pass; wider rows (128-512 B) are
@@ -896,10 +900,17 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
     // keeps occupancy register-bound.
     constexpr bool kStage = KW == 1;
     constexpr int kRow = 16 * KW + 1;
-    using JobT = typename std::conditional<(KW > 2), uint64_t, uint32_t>::type;
     __shared__ uint32_t s_vis[kStage ? kWrsThreads * kRow : 1];
-    const int64_t p = (int64_t)blockIdx.x * kWrsThreads + threadIdx.x;
     uint32_t* my = s_vis + (kStage ? threadIdx.x * kRow : 0);
+    const int64_t ntiles = (a.P + kWrsThreads - 1) / kWrsThreads;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+        nls_pixel<kLum64, KW>(a, sc, t * kWrsThreads + threadIdx.x, my);
+}
+
+template <bool kLum64, int KW>
+__device__ __forceinline__ void nls_pixel(const WArgs& a, const nvc_scene& sc, int64_t p, uint32_t* my) {
+    constexpr bool kStage = KW == 1;
+    using JobT = typename std::conditional<(KW > 2), uint64_t, uint32_t>::type;
     if (kStage && p < a.P) {
         const uint4* vrow = reinterpret_cast<const uint4*>(a.vis16 + p * a.vstride);
 #pragma unroll
@@ -1004,7 +1015,7 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
 template <int KW>
 void launch_nlsg(const WArgs& a, const nvc_scene& sc, int64_t P, cudaStream_t s) {
     const int thr = kWrsThreads;
-    const int grid = (int)((P + thr - 1) / thr);
+    const int grid = (int)((P + thr - 1) / thr);   // one tile per CTA (a persistent grid measured slower in the frame)
     if (a.lum_f64)
         k_nls32g<true, KW><<<grid, thr, 0, s>>>(a, sc);
     else
