@@ -791,6 +791,10 @@ struct WArgs {
     double* big_w;
     const double* albedo;
     double* rgb;
+    // k_nls32g only (set by pipeline_select; 32-bit index math, checked on the host):
+    uint64_t grp0;       // offset / 4 + 1: Philox block of the frame's first 4-light group
+    uint64_t lp0;        // offset + p_total * K: draw index of the first light-point pair
+    uint32_t stride32;   // luminance row stride (elements)
 };
 
 template <bool kLum64>
@@ -924,11 +928,11 @@ __device__ __forceinline__ void nls_pixel(const WArgs& a, const nvc_scene& sc, i
             }
     }
     if (p >= a.P) return;
-    const int64_t gp = a.p_first + p;
+    const uint32_t gp = (uint32_t)(a.p_first + p);   // < 2^31 (host check)
     uint32_t m[KW];
 #pragma unroll
     for (int w = 0; w < KW; ++w) {
-        m[w] = a.nz_mask ? __ldg(a.nz_mask + (int64_t)w * a.stride + p) : 0xffffffffu;
+        m[w] = a.nz_mask ? __ldg(a.nz_mask + (uint32_t)w * a.stride32 + p) : 0xffffffffu;
         const int left = a.K - 32 * w;
         if (left <= 0)
             m[w] = 0u;
@@ -942,10 +946,10 @@ __device__ __forceinline__ void nls_pixel(const WArgs& a, const nvc_scene& sc, i
         for (int g = 0; g < 8; ++g) jobs |= (JobT)(((m[w] >> (4 * g)) & 15u) != 0u ? 1u : 0u) << (8 * w + g);
     using LT = typename std::conditional<kLum64, double, float>::type;
     const LT* lp = reinterpret_cast<const LT*>(a.lum) + p;
-    const int64_t st1 = a.stride, st2 = 2 * st1, st3 = 3 * st1;   // light-major rows: hoisted strides
+    const uint32_t st1 = a.stride32;   // light-major rows; K * stride < 2^32 elements (host check)
     const double lo = clamp_lo(a.floor);
-    const uint64_t c_grp = (a.offset + (uint64_t)gp * (uint64_t)a.K) / 4 + 1;
-    const uint64_t n_lp = a.offset + (uint64_t)a.p_total * (uint64_t)a.K + 2ull * (uint64_t)gp;
+    const uint64_t c_grp = a.grp0 + (uint64_t)(gp * (uint32_t)(a.K / 4));   // (offset + gp K) / 4 + 1
+    const uint64_t n_lp = a.lp0 + 2ull * gp;                                // offset + p_total K + 2 gp
     double s = 0.0, wsel = 0.0, u0 = 0.0, u1 = 0.0;
     int sel = -1;
     // one 4-light group: its luminances (nonzero lights only) and visibility pair
@@ -955,11 +959,11 @@ __device__ __forceinline__ void nls_pixel(const WArgs& a, const nvc_scene& sc, i
         for (int w = 0; w < KW; ++w)
             if ((g >> 3) == w) mw = m[w];
         bits = (mw >> (4 * (g & 7))) & 15u;
-        const LT* lg = lp + (int64_t)(4 * g) * st1;
-        t[0] = (bits & 1u) ? __ldg(lg) : LT(0);
-        t[1] = (bits & 2u) ? __ldg(lg + st1) : LT(0);
-        t[2] = (bits & 4u) ? __ldg(lg + st2) : LT(0);
-        t[3] = (bits & 8u) ? __ldg(lg + st3) : LT(0);
+        const uint32_t o = (uint32_t)(4 * g) * st1;
+        t[0] = (bits & 1u) ? __ldg(lp + o) : LT(0);
+        t[1] = (bits & 2u) ? __ldg(lp + (o + st1)) : LT(0);
+        t[2] = (bits & 4u) ? __ldg(lp + (o + 2 * st1)) : LT(0);
+        t[3] = (bits & 8u) ? __ldg(lp + (o + 3 * st1)) : LT(0);
         vg = make_uint2(0u, 0u);
         if (!kStage) vg = __ldg(reinterpret_cast<const uint2*>(a.vis16 + p * a.vstride) + g);
     };
@@ -1384,8 +1388,13 @@ int pipeline_select(const nvc_model* m, const nvc_scene* sc, int64_t P, int mode
     a.big_w = big_w;
     a.albedo = albedo;
     a.rgb = rgb;
+    a.grp0 = offset / 4 + 1;
+    a.lp0 = offset + (uint64_t)p_total * (uint64_t)K;
+    a.stride32 = (uint32_t)stride;
     const bool aligned = K % 4 == 0 && offset % 4 == 0 && ((uint64_t)p_total * (uint64_t)K) % 2 == 0;
-    if (mode == 1 && K <= 128 && aligned && getenv("NVC_WRS_FORWARD") == nullptr) {
+    const bool small = (uint64_t)p_total < (1ull << 31) && (uint64_t)stride * (uint64_t)K < (1ull << 32) &&
+                       (uint64_t)p_total * (uint64_t)(K / 4) < (1ull << 32);   // k_nls32g's 32-bit index math
+    if (mode == 1 && K <= 128 && aligned && small && getenv("NVC_WRS_FORWARD") == nullptr) {
         if (K <= 32)
             launch_nlsg<1>(a, *sc, P, s);
         else if (K <= 64)
