@@ -590,6 +590,17 @@ __device__ __forceinline__ void tst16(uint32_t taddr, const uint32_t r[16]) {
 }
 __device__ __forceinline__ void tst_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+#ifdef NVC_MLP_TRACE
+// profiling build only (tools/mlp_trace.py): clock64 stamps of CTA 0's first 8 tiles per
+// warpgroup, [wg][tile][layer][event]: 0 MMA issue start, 1 commit issued, 2 epilogue
+// wake-up, 3 epilogue done (accumulator released), 4 A0 tile ready, 5 output stores issued
+__device__ long long g_mlp_trace[4][8][4][6];
+#define MLP_STAMP(g, k, l, e) \
+    { if (blockIdx.x == 0 && (k) < 8 && (l) < 4) g_mlp_trace[g][k][l][e] = clock64(); }
+#else
+#define MLP_STAMP(g, k, l, e) {}
+#endif
+
 template <int HID, int OUT, int KP0>
 __global__ void __launch_bounds__(TsCfg<HID>::kThreads, 1) k_mlp_ts(MNet net, const float* __restrict__ params,
                                                                    const uint16_t* __restrict__ wpack,
@@ -673,10 +684,12 @@ __global__ void __launch_bounds__(TsCfg<HID>::kThreads, 1) k_mlp_ts(MNet net, co
             if (k + 1 < n_wg) load_a0(k + 1);                     // the other buffer: tile k-1 is done with it
             const int b = k & 1;
             mbar_wait(&B.a0_full[b], a0_ph[b]);
+            if ((tid & 31) == 0) MLP_STAMP(g, k, 0, 4)
             a0_ph[b] ^= 1u;
             for (int l = 0; l < L; ++l) {
                 if (k > 0 || l > 0) asm volatile("bar.sync %0, 160;" ::"r"(id) : "memory");   // epilogue done
                 tc_after();
+                if ((tid & 31) == 0) MLP_STAMP(g, k, l, 0)
                 const int np = l == L - 1 ? OUT : HID;
                 const uint32_t idesc = (1u << 4) | ((uint32_t)(np >> 3) << 17) | ((uint32_t)(kT >> 4) << 24);
                 const uint64_t db = desc_of(w_addr + 2u * (uint32_t)net.wofs[l], np, l == 0 ? KP0 : HID, 0);
@@ -696,6 +709,7 @@ __global__ void __launch_bounds__(TsCfg<HID>::kThreads, 1) k_mlp_ts(MNet net, co
                 // bias: + ones[128 x 16] x bias_l[np x 16]^T
                 mma_elect(acc, d_ones, desc_of(bias + l * bias_block, np, 16, 0), idesc, 1u);
                 commit_elect(&B.acc_full);
+                if ((tid & 31) == 0) MLP_STAMP(g, k, l, 1)
             }
         }
         if (n_wg > 0) asm volatile("bar.sync %0, 160;" ::"r"(id) : "memory");   // the last tile's final arrive
@@ -710,6 +724,7 @@ __global__ void __launch_bounds__(TsCfg<HID>::kThreads, 1) k_mlp_ts(MNet net, co
                 mbar_wait(&B.acc_full, ph);
                 ph ^= 1u;
                 tc_after();
+                if (wq == 0 && (tid & 31) == 0) MLP_STAMP(g, k, l, 2)
                 if (l < L - 1) {
 #pragma unroll
                     for (int cb = 0; cb < HID; cb += 64) {   // 64 accumulator columns at a time
@@ -730,6 +745,7 @@ __global__ void __launch_bounds__(TsCfg<HID>::kThreads, 1) k_mlp_ts(MNet net, co
                     }
                     tst_wait();
                     tc_before();
+                    if (wq == 0 && (tid & 31) == 0) MLP_STAMP(g, k, l, 3)
                     asm volatile("bar.arrive %0, 160;" ::"r"(id) : "memory");
                 } else {
                     uint32_t r[OUT];
@@ -737,6 +753,7 @@ __global__ void __launch_bounds__(TsCfg<HID>::kThreads, 1) k_mlp_ts(MNet net, co
                     for (int c = 0; c < OUT; c += 16) tld16_nowait(acc + lane_base + (uint32_t)c, r + c);
                     tld_wait();
                     tc_before();
+                    if (wq == 0 && (tid & 31) == 0) MLP_STAMP(g, k, l, 3)
                     asm volatile("bar.arrive %0, 160;" ::"r"(id) : "memory");   // accumulator drained
                     const int64_t p = (t0 + (int64_t)k * tstep) * kT + row;
                     if (p < P) {
@@ -756,9 +773,14 @@ __global__ void __launch_bounds__(TsCfg<HID>::kThreads, 1) k_mlp_ts(MNet net, co
                                 hh[e] = __floats2half2_rn(o[0], o[1]);
                                 if (net.out_sigmoid) hh[e] = __hmin2(__hmax2(hh[e], lo), hi);   // mlp.py:135-136
                             }
+#ifndef NVC_MLP_NOSTORE
                             if (8 * c < vstride) *reinterpret_cast<uint4*>(vrow + 8 * c) = *reinterpret_cast<const uint4*>(hh);
+#else   // experiment: the outputs computed but not stored
+                            if (P < 0) *reinterpret_cast<uint4*>(vrow + 8 * c) = *reinterpret_cast<const uint4*>(hh);
+#endif
                         }
                     }
+                    if (wq == 0 && (tid & 31) == 0) MLP_STAMP(g, k, l, 5)
                 }
             }
         }
@@ -1853,3 +1875,9 @@ extern "C" int nvc_profile_stage_ms(float* ms3) {
         }
     return NVC_OK;
 }
+
+#ifdef NVC_MLP_TRACE
+extern "C" int nvc_mlp_trace_get(long long* host) {
+    return cudaMemcpyFromSymbol(host, nvc::g_mlp_trace, sizeof(nvc::g_mlp_trace)) == cudaSuccess ? 0 : -1;
+}
+#endif
