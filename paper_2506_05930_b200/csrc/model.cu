@@ -1095,6 +1095,79 @@ __global__ void __launch_bounds__(kAdamThreads) k_adam_bulk(float* __restrict__ 
     if (tid == 0) tma::wait_all();
 }
 
+// The dense-gradient grid Adam with two parameters (one x-pair entry) per
+// thread and 512 threads: the same bulk-copy ring and tile as k_adam_bulk, twice
+// the warps to hide the FP32 division / square-root latency of the update, and
+// 8- / 16-byte shared-memory accesses that are bank-conflict free.
+constexpr int kAdam2Threads = kAdamTile / 2;
+__global__ void __launch_bounds__(kAdam2Threads) k_adam_dense2(float* __restrict__ p, float* __restrict__ m,
+                                                               float* __restrict__ v, int64_t* __restrict__ fx,
+                                                               uint16_t* __restrict__ table_h, int64_t ntiles,
+                                                               AdamK a, int64_t T, int64_t tile0) {
+    extern __shared__ __align__(128) uint8_t adam_smem[];
+    AdamStage* st = reinterpret_cast<AdamStage*>(adam_smem);
+    __shared__ uint64_t full[kAdamStages];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int n_local = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+    auto tile_base = [&](int i) { return (tile0 + blockIdx.x + (int64_t)i * gridDim.x) * kAdamTile; };
+    auto issue = [&](int i) {
+        const int s = i % kAdamStages;
+        const int64_t base = tile_base(i);
+        tma::bar_expect_tx(&full[s], (uint32_t)sizeof(AdamStage));
+        tma::load(st[s].p, p + base, kAdamTile * 4, &full[s]);
+        tma::load(st[s].m, m + base, kAdamTile * 4, &full[s]);
+        tma::load(st[s].v, v + base, kAdamTile * 4, &full[s]);
+        tma::load(st[s].q, fx + base, kAdamTile * 8, &full[s]);
+    };
+    if (tid == 0) {
+        for (int s = 0; s < kAdamStages; ++s) tma::bar_init(&full[s], 1);
+        tma::bar_init_fence();
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int i = 0; i < min(kAdamStages, n_local); ++i) issue(i);
+    for (int i = 0; i < n_local; ++i) {
+        const int s = i % kAdamStages;
+        const int64_t base = tile_base(i);
+        const int64_t i0 = base + 2 * tid, e0 = i0 / 2;
+        tma::bar_wait(&full[s], (uint32_t)(i / kAdamStages) & 1u);
+        float2* P2 = reinterpret_cast<float2*>(st[s].p) + tid;
+        float2* M2 = reinterpret_cast<float2*>(st[s].m) + tid;
+        float2* V2 = reinterpret_cast<float2*>(st[s].v) + tid;
+        const longlong2 q = reinterpret_cast<const longlong2*>(st[s].q)[tid];
+        if (q.x | q.y) *reinterpret_cast<longlong2*>(fx + i0) = make_longlong2(0, 0);
+        float2 P = *P2, M = *M2, V = *V2;
+        P.x = adam1(P.x, from_fx(q.x), M.x, V.x, a);
+        P.y = adam1(P.y, from_fx(q.y), M.y, V.y, a);
+        *P2 = P;
+        *M2 = M;
+        *V2 = V;
+        const uint32_t E0 = (uint32_t)__half_as_ushort(__float2half_rn(P.x)) |
+                            ((uint32_t)__half_as_ushort(__float2half_rn(P.y)) << 16);
+        const uint32_t nxt = __shfl_down_sync(0xffffffffu, E0, 1);
+        uint32_t* slot = reinterpret_cast<uint32_t*>(table_h + e0 * 4);   // x-pair slot e0 = (entry e0 | entry e0 + 1)
+        if (lane < 31)
+            *reinterpret_cast<uint2*>(slot) = make_uint2(E0, nxt);
+        else
+            slot[0] = E0;
+        if (lane == 0)   // previous slot's x-neighbour half (previous warp's last slot, or the level's last on wrap)
+            reinterpret_cast<uint32_t*>(table_h + pair_prev(e0, T) * 4)[1] = E0;
+        tma::fence_shared();
+        __syncthreads();
+        if (tid == 0) {
+            tma::store(p + base, st[s].p, kAdamTile * 4);
+            tma::store(m + base, st[s].m, kAdamTile * 4);
+            tma::store(v + base, st[s].v, kAdamTile * 4);
+            tma::commit();
+            if (i >= 1 && i - 1 + kAdamStages < n_local) {
+                tma::wait_read<1>();
+                issue(i - 1 + kAdamStages);
+            }
+        }
+    }
+    if (tid == 0) tma::wait_all();
+}
+
 __global__ void k_adam_mlp(Net net, float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
                            GradSink gs, uint16_t* __restrict__ wpack, AdamK a) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1508,7 +1581,11 @@ int nvc_adam_step_shard(const nvc_model* m, int64_t t, double lr, int32_t shard,
         // leave each SM room for the previous frame's NLS blocks running beside it)
         const char* ge = getenv("NVC_ADAM_GRID");
         const int grid = (int)std::min<int64_t>(ntiles, (ge ? atoi(ge) : 2) * (int64_t)sms);
-        if (ntiles > 0) {
+        if (ntiles > 0 && !m->grad_c && !getenv("NVC_ADAM_BULK4")) {   // default: 512 threads x 2 parameters
+            cudaFuncSetAttribute(k_adam_dense2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            k_adam_dense2<<<grid, kAdam2Threads, smem, s>>>(m->params, m->adam_m, m->adam_v, m->grad_fx, m->table_h,
+                                                            ntiles, a, m->table_size, tile0);
+        } else if (ntiles > 0) {
             if (m->grad_c)
                 k_adam_bulk<true><<<grid, kAdamThreads, smem, s>>>(m->params, m->adam_m, m->adam_v, sink_of(m),
                                                                    m->table_h, ntiles, a, m->table_size, tile0);
