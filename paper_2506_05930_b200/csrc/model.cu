@@ -617,14 +617,21 @@ __global__ void __launch_bounds__(kThreads, 4) k_train3(Net net, T3Layout tl, co
                 }
             }
             if (l > 0) {
+                // 16-byte shared accesses (a thread's 4 columns are contiguous): scalar ones
+                // at a 4-word stride across the warp were 4-way bank conflicts
 #pragma unroll
-                for (int i = 0; i < kRPT; ++i)
+                for (int i = 0; i < kRPT; ++i) {
+                    const float4 a4 = *reinterpret_cast<const float4*>(A + (r0 + i) * Ki + k0);
+                    const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+                    float o[4];
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         float v = acc[i][j];
-                        if (!(A[(r0 + i) * Ki + k0 + j] >= 0.0f)) v = __fmul_rn(v, net.alpha);
-                        dzn[(r0 + i) * Ki + k0 + j] = (tl.rbits && (tl.rwhat & 4)) ? round_bits(v, tl.rbits) : v;
+                        if (!(av[j] >= 0.0f)) v = __fmul_rn(v, net.alpha);
+                        o[j] = (tl.rbits && (tl.rwhat & 4)) ? round_bits(v, tl.rbits) : v;
                     }
+                    *reinterpret_cast<float4*>(dzn + (r0 + i) * Ki + k0) = make_float4(o[0], o[1], o[2], o[3]);
+                }
             } else {
 #pragma unroll
                 for (int i = 0; i < kRPT; ++i)
