@@ -968,6 +968,10 @@ __device__ __forceinline__ void nls_pixel(const WArgs& a, const nvc_scene& sc, i
         for (int g = 0; g < 8; ++g) jobs |= (JobT)(((m[w] >> (4 * g)) & 15u) != 0u ? 1u : 0u) << (8 * w + g);
     using LT = typename std::conditional<kLum64, double, float>::type;
     const LT* lp = reinterpret_cast<const LT*>(a.lum) + p;
+    // keep the pixel's row base in a register: each luminance address is then one
+    // 32 x 32 + 64-bit multiply-add (the compiler otherwise re-derives lum + (p + o) * 8
+    // from the parameter bank for every load)
+    asm volatile("" : "+l"(lp));
     const uint32_t st1 = a.stride32;   // light-major rows; K * stride < 2^32 elements (host check)
     const double lo = clamp_lo(a.floor);
     const uint64_t c_grp = a.grp0 + (uint64_t)(gp * (uint32_t)(a.K / 4));   // (offset + gp K) / 4 + 1
@@ -982,10 +986,11 @@ __device__ __forceinline__ void nls_pixel(const WArgs& a, const nvc_scene& sc, i
             if ((g >> 3) == w) mw = m[w];
         bits = (mw >> (4 * (g & 7))) & 15u;
         const uint32_t o = (uint32_t)(4 * g) * st1;
-        t[0] = (bits & 1u) ? __ldg(lp + o) : LT(0);
-        t[1] = (bits & 2u) ? __ldg(lp + (o + st1)) : LT(0);
-        t[2] = (bits & 4u) ? __ldg(lp + (o + 2 * st1)) : LT(0);
-        t[3] = (bits & 8u) ? __ldg(lp + (o + 3 * st1)) : LT(0);
+        // only the nonzero lights' entries are read (group_wrs reads t[j] only for them)
+        if (bits & 1u) t[0] = __ldg(lp + o);
+        if (bits & 2u) t[1] = __ldg(lp + (o + st1));
+        if (bits & 4u) t[2] = __ldg(lp + (o + 2 * st1));
+        if (bits & 8u) t[3] = __ldg(lp + (o + 3 * st1));
         vg = make_uint2(0u, 0u);
         if (!kStage) vg = __ldg(reinterpret_cast<const uint2*>(a.vis16 + p * a.vstride) + g);
     };
