@@ -925,10 +925,8 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
     // read per 4-light group (8 B) next to the group's luminances instead, which
     // keeps occupancy register-bound.
     constexpr bool kStage = KW == 1;
-    // 34-word rows: 8-B aligned, so a 4-light group's visibilities are one 64-bit
-    // shared load, and lanes' rows 2 banks apart keep half-warps conflict-free
-    constexpr int kRow = 16 * KW + 2;
-    __shared__ __align__(16) uint32_t s_vis[kStage ? kWrsThreads * kRow : 1];
+    constexpr int kRow = 16 * KW + 1;
+    __shared__ uint32_t s_vis[kStage ? kWrsThreads * kRow : 1];
     uint32_t* my = s_vis + (kStage ? threadIdx.x * kRow : 0);
     const int64_t ntiles = (a.P + kWrsThreads - 1) / kWrsThreads;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
@@ -989,27 +987,27 @@ __device__ __forceinline__ void nls_pixel(const WArgs& a, const nvc_scene& sc, i
         bits = (mw >> (4 * (g & 7))) & 15u;
         const uint32_t o = (uint32_t)(4 * g) * st1;
         // only the nonzero lights' entries are read (group_wrs reads t[j] only for them)
-        // only the nonzero lights' entries are read; a zero light's weight is then 0,
-        // which adds +0 to the running sum and is never selected (w > 0 fails)
-        t[0] = (bits & 1u) ? __ldg(lp + o) : LT(0);
-        t[1] = (bits & 2u) ? __ldg(lp + (o + st1)) : LT(0);
-        t[2] = (bits & 4u) ? __ldg(lp + (o + 2 * st1)) : LT(0);
-        t[3] = (bits & 8u) ? __ldg(lp + (o + 3 * st1)) : LT(0);
-        vg = kStage ? *reinterpret_cast<const uint2*>(my + 2 * g)
-                    : __ldg(reinterpret_cast<const uint2*>(a.vis16 + p * a.vstride) + g);
+        if (bits & 1u) t[0] = __ldg(lp + o);
+        if (bits & 2u) t[1] = __ldg(lp + (o + st1));
+        if (bits & 4u) t[2] = __ldg(lp + (o + 2 * st1));
+        if (bits & 8u) t[3] = __ldg(lp + (o + 3 * st1));
+        vg = make_uint2(0u, 0u);
+        if (!kStage) vg = __ldg(reinterpret_cast<const uint2*>(a.vis16 + p * a.vstride) + g);
     };
     // the group's lights in order into the FP64 reservoir
     auto group_wrs = [&](int g, const LT t[4], uint2 vg, uint32_t bits, const U4& u) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {   // branch-free over the group: zero lights have t = 0 (above)
-            const int k = 4 * g + j;
-            const uint32_t pair = j < 2 ? vg.x : vg.y;
-            const float vis = __half2float(__ushort_as_half((unsigned short)((j & 1) ? (pair >> 16) : (pair & 0xffffu))));
-            const double w = wrs_weight(vis, (double)t[j], lo);
-            s = __dadd_rn(s, w);
-            if (w > 0.0 && __dmul_rn(u01(u.x[j]), s) < w) {
-                sel = k;
-                wsel = w;
+        for (int j = 0; j < 4; ++j) {
+            if ((bits >> j) & 1u) {
+                const int k = 4 * g + j;
+                const uint32_t pair = kStage ? my[k >> 1] : (j < 2 ? vg.x : vg.y);
+                const float vis = __half2float(__ushort_as_half((unsigned short)((j & 1) ? (pair >> 16) : (pair & 0xffffu))));
+                const double w = wrs_weight(vis, (double)t[j], lo);
+                s = __dadd_rn(s, w);
+                if (w > 0.0 && __dmul_rn(u01(u.x[j]), s) < w) {
+                    sel = k;
+                    wsel = w;
+                }
             }
         }
     };
