@@ -15,6 +15,35 @@
 #include "common.cuh"
 
 namespace nvc {
+// A per-device side stream (highest priority) and events that let the small
+// MLP-gradient kernels run beside the grid kernels of the same step: the
+// per-block partial reduce beside the hash-grid scatter, the MLP Adam beside
+// the grid Adam.  Both pairs touch disjoint memory; the caller's stream waits
+// for the side stream before each entry point returns, so its ordering
+// contract is unchanged.  NVC_NO_SIDE_STREAM=1 serialises them (A/B).
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+inline SideStream* side_stream() {
+    if (getenv("NVC_NO_SIDE_STREAM")) return nullptr;
+    static SideStream per_dev[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    SideStream& ss = per_dev[dev];
+    if (!ss.s) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (cudaStreamCreateWithPriority(&ss.s, cudaStreamNonBlocking, hi) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            ss.s = nullptr;
+            return nullptr;
+        }
+    }
+    return &ss;
+}
 
 static thread_local char g_err[512];
 
@@ -1405,6 +1434,7 @@ int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, con
     if (getenv("NVC_T3_WHAT")) tl3.rwhat = atoi(getenv("NVC_T3_WHAT"));
     const int smem3 = tl3.total * 4 + 64;
     int nblk_red = nblk;   // partial sets k_reduce_parts sums (one per training block)
+    bool reduced = false;  // launched on the side stream already
     if (split && smem3 <= 200 * 1024) {
         char* p2 = (char*)part_loss + ((int64_t)nblk * 8 + 255) / 256 * 256;
         float* act0 = (float*)p2;
@@ -1428,8 +1458,21 @@ int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, con
         }
         rc = check_launch("k_train3");
         if (rc) return rc;
-        k_tr_scatter<<<grid1(rows_max * g.L, 128), 128, 0, s>>>(g, pos, b_max, b_dev, shard, n_shards, dact0,
-                                                                 sink_of(m));
+        if (SideStream* ss = side_stream()) {   // the MLP partial reduce beside the grid scatter
+            cudaEventRecord(ss->fork, s);
+            cudaStreamWaitEvent(ss->s, ss->fork, 0);
+            k_reduce_parts<<<grid1(net.mlp_count, 32), 256, 0, ss->s>>>(part_w, part_loss, nblk_red, net.mlp_count,
+                                                                        net.grid_count, sink_of(m), loss_out, b_max,
+                                                                        b_dev);
+            cudaEventRecord(ss->join, ss->s);
+            reduced = true;
+            k_tr_scatter<<<grid1(rows_max * g.L, 128), 128, 0, s>>>(g, pos, b_max, b_dev, shard, n_shards, dact0,
+                                                                     sink_of(m));
+            cudaStreamWaitEvent(s, ss->join, 0);
+        } else {
+            k_tr_scatter<<<grid1(rows_max * g.L, 128), 128, 0, s>>>(g, pos, b_max, b_dev, shard, n_shards, dact0,
+                                                                     sink_of(m));
+        }
     } else {
         const int smem = mlp_smem_bytes(net);
         NVC_REQUIRE(smem <= 200 * 1024, "nvc_train_grads: MLP too wide for the fp32 tile kernel");
@@ -1439,8 +1482,9 @@ int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, con
     }
     rc = check_launch("nvc_train_grads");
     if (rc) return rc;
-    k_reduce_parts<<<grid1(net.mlp_count, 32), 256, 0, s>>>(part_w, part_loss, nblk_red, net.mlp_count,
-                                                             net.grid_count, sink_of(m), loss_out, b_max, b_dev);
+    if (!reduced)
+        k_reduce_parts<<<grid1(net.mlp_count, 32), 256, 0, s>>>(part_w, part_loss, nblk_red, net.mlp_count,
+                                                                 net.grid_count, sink_of(m), loss_out, b_max, b_dev);
     return check_launch("k_reduce_parts");
 }
 
@@ -1568,6 +1612,15 @@ int nvc_adam_step_shard(const nvc_model* m, int64_t t, double lr, int32_t shard,
     a.inv_b1c = 1.0 / (double)a.b1c;
     a.inv_b2c = 1.0 / (double)a.b2c;
     cudaStream_t s = (cudaStream_t)stream;
+    // the MLP Adam (disjoint parameters) beside the grid Adam, on the side stream
+    SideStream* ss = side_stream();
+    if (ss) {
+        cudaEventRecord(ss->fork, s);
+        cudaStreamWaitEvent(ss->s, ss->fork, 0);
+        k_adam_mlp<<<grid1(net.mlp_count, 256), 256, 0, ss->s>>>(net, m->params, m->adam_m, m->adam_v, sink_of(m),
+                                                                 m->wpack, a);
+        cudaEventRecord(ss->join, ss->s);
+    }
     const bool bulk = m->features == 2 && m->table_size % 64 == 0 && net.grid_count % kAdamTile == 0;
     NVC_REQUIRE(n_shards == 1 || (bulk && !m->grad_c),
                 "nvc_adam_step_shard: the sharded optimizer needs F == 2, whole Adam tiles and dense gradients");
@@ -1607,8 +1660,12 @@ int nvc_adam_step_shard(const nvc_model* m, int64_t t, double lr, int32_t shard,
     }
     rc = check_launch("k_adam_grid");
     if (rc) return rc;
-    k_adam_mlp<<<grid1(net.mlp_count, 256), 256, 0, s>>>(net, m->params, m->adam_m, m->adam_v, sink_of(m),
-                                                         m->wpack, a);
+    if (ss) {
+        cudaStreamWaitEvent(s, ss->join, 0);
+    } else {
+        k_adam_mlp<<<grid1(net.mlp_count, 256), 256, 0, s>>>(net, m->params, m->adam_m, m->adam_v, sink_of(m),
+                                                             m->wpack, a);
+    }
     return check_launch("k_adam_mlp");
 }
 
