@@ -27,7 +27,7 @@ struct SideStream {
 };
 inline SideStream* side_stream() {
     if (getenv("NVC_NO_SIDE_STREAM")) return nullptr;
-    static SideStream per_dev[64];
+    static thread_local SideStream per_dev[64];   // per host thread: the fork/join events are never shared
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
     SideStream& ss = per_dev[dev];
