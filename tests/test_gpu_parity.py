@@ -511,10 +511,11 @@ class TestTraining:
     def _c1(self, pbox8, seed=0):
         return VisibilityCache(MODE_LIGHTS, 8, grid_cfg(pbox8, 8, 1 << 14), seed=seed, hidden_dims=(64, 64))
 
-    @pytest.mark.parametrize("kernel", ["bulk", "flat"])
+    @pytest.mark.parametrize("kernel", ["dense2", "bulk4", "flat", "no_side_stream"])
     def test_adam_bit_exact_given_grads(self, pbox8, kernel, monkeypatch):
-        if kernel == "flat":
-            monkeypatch.setenv("NVC_ADAM_FLAT", "1")
+        env = {"flat": "NVC_ADAM_FLAT", "bulk4": "NVC_ADAM_BULK4", "no_side_stream": "NVC_NO_SIDE_STREAM"}
+        if kernel in env:
+            monkeypatch.setenv(env[kernel], "1")
         c = self._c1(pbox8)
         c.set_compact(False)          # feed arbitrary dense gradients
         p0 = c.params.cpu().numpy().copy()
