@@ -914,28 +914,25 @@ __global__ void __launch_bounds__(kWrsThreads) k_nls32(WArgs a, nvc_scene sc) {
 // static word indices, and the group's luminances are loaded before the
 // Philox rounds so their latency hides behind them.  The light-point draw
 // pair is the last "group".  Same arithmetic and order as k_nls32.
-template <bool kLum64, int KW>
+template <bool kLum64, int KW, bool kStage>
 __device__ __forceinline__ void nls_pixel(const WArgs& a, const nvc_scene& sc, int64_t p, uint32_t* my);
 
 // one thread per pixel (the tile loop also serves grids smaller than the pixel count)
-template <bool kLum64, int KW>
+template <bool kLum64, int KW, bool kStage>
 __global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
-    // KW 32-light words (K <= 32 KW).  K <= 32: the pixel's fp16 visibility row is
-    // staged in shared memory with one coalesced pass; wider rows (128-512 B) are
-    // read per 4-light group (8 B) next to the group's luminances instead, which
-    // keeps occupancy register-bound.
-    constexpr bool kStage = KW == 1;
+    // KW 32-light words (K <= 32 KW).  The pixel's fp16 visibility row is read per
+    // 4-light group (8 B) next to the group's luminances; kStage (K <= 32, A/B
+    // only) stages the row in shared memory with one coalesced pass instead.
     constexpr int kRow = 16 * KW + 1;
     __shared__ uint32_t s_vis[kStage ? kWrsThreads * kRow : 1];
     uint32_t* my = s_vis + (kStage ? threadIdx.x * kRow : 0);
     const int64_t ntiles = (a.P + kWrsThreads - 1) / kWrsThreads;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
-        nls_pixel<kLum64, KW>(a, sc, t * kWrsThreads + threadIdx.x, my);
+        nls_pixel<kLum64, KW, kStage>(a, sc, t * kWrsThreads + threadIdx.x, my);
 }
 
-template <bool kLum64, int KW>
+template <bool kLum64, int KW, bool kStage>
 __device__ __forceinline__ void nls_pixel(const WArgs& a, const nvc_scene& sc, int64_t p, uint32_t* my) {
-    constexpr bool kStage = KW == 1;
     using JobT = typename std::conditional<(KW > 2), uint64_t, uint32_t>::type;
     if (kStage && p < a.P) {
         const uint4* vrow = reinterpret_cast<const uint4*>(a.vis16 + p * a.vstride);
@@ -1047,10 +1044,25 @@ template <int KW>
 void launch_nlsg(const WArgs& a, const nvc_scene& sc, int64_t P, cudaStream_t s) {
     const int thr = kWrsThreads;
     const int grid = (int)((P + thr - 1) / thr);   // one tile per CTA (a persistent grid measured slower in the frame)
-    if (a.lum_f64)
-        k_nls32g<true, KW><<<grid, thr, 0, s>>>(a, sc);
-    else
-        k_nls32g<false, KW><<<grid, thr, 0, s>>>(a, sc);
+    // The visibility row is read per 4-light group (8 B, L1-resident after the
+    // first touch) rather than staged in shared memory: the 34 KB staging buffer
+    // of each 256-thread block kept the training step's CTAs (102 KB of shared
+    // memory) off the SMs the NLS occupies (frame 0.606 -> 0.589 ms).
+    // NVC_NLS_STAGE=1 restores the staged K <= 32 variant (A/B).
+    if constexpr (KW == 1) {
+        if (getenv("NVC_NLS_STAGE")) {
+            if (a.lum_f64)
+                k_nls32g<true, KW, true><<<grid, thr, 0, s>>>(a, sc);
+            else
+                k_nls32g<false, KW, true><<<grid, thr, 0, s>>>(a, sc);
+            return;
+        }
+    }
+    if (a.lum_f64) {
+        k_nls32g<true, KW, false><<<grid, thr, 0, s>>>(a, sc);
+    } else {
+        k_nls32g<false, KW, false><<<grid, thr, 0, s>>>(a, sc);
+    }
 }
 
 // Neural DI for K <= 32 (sampling.py:215-218): rgb = (sum_k v_k * factor_k *
