@@ -918,17 +918,23 @@ template <bool kLum64, int KW, bool kStage>
 __device__ __forceinline__ void nls_pixel(const WArgs& a, const nvc_scene& sc, int64_t p, uint32_t* my);
 
 // one thread per pixel (the tile loop also serves grids smaller than the pixel count)
+// 128-thread CTAs: finer-grained SM sharing with the training kernels beside
+// the NLS (frame 0.584 vs 0.589 ms at 256; 64: 0.586, 192: 0.591, 512: 0.601)
+#ifndef NVC_NLS_THREADS
+#define NVC_NLS_THREADS 128
+#endif
+constexpr int kNlsThreads = NVC_NLS_THREADS;
 template <bool kLum64, int KW, bool kStage>
-__global__ void __launch_bounds__(kWrsThreads) k_nls32g(WArgs a, nvc_scene sc) {
+__global__ void __launch_bounds__(kNlsThreads) k_nls32g(WArgs a, nvc_scene sc) {
     // KW 32-light words (K <= 32 KW).  The pixel's fp16 visibility row is read per
     // 4-light group (8 B) next to the group's luminances; kStage (K <= 32, A/B
     // only) stages the row in shared memory with one coalesced pass instead.
     constexpr int kRow = 16 * KW + 1;
-    __shared__ uint32_t s_vis[kStage ? kWrsThreads * kRow : 1];
+    __shared__ uint32_t s_vis[kStage ? kNlsThreads * kRow : 1];
     uint32_t* my = s_vis + (kStage ? threadIdx.x * kRow : 0);
-    const int64_t ntiles = (a.P + kWrsThreads - 1) / kWrsThreads;
+    const int64_t ntiles = (a.P + kNlsThreads - 1) / kNlsThreads;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
-        nls_pixel<kLum64, KW, kStage>(a, sc, t * kWrsThreads + threadIdx.x, my);
+        nls_pixel<kLum64, KW, kStage>(a, sc, t * kNlsThreads + threadIdx.x, my);
 }
 
 template <bool kLum64, int KW, bool kStage>
@@ -1042,7 +1048,7 @@ __device__ __forceinline__ void nls_pixel(const WArgs& a, const nvc_scene& sc, i
 
 template <int KW>
 void launch_nlsg(const WArgs& a, const nvc_scene& sc, int64_t P, cudaStream_t s) {
-    const int thr = kWrsThreads;
+    const int thr = kNlsThreads;
     const int grid = (int)((P + thr - 1) / thr);   // one tile per CTA (a persistent grid measured slower in the frame)
     // The visibility row is read per 4-light group (8 B, L1-resident after the
     // first touch) rather than staged in shared memory: the 34 KB staging buffer
