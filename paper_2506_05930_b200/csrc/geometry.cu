@@ -238,42 +238,111 @@ __device__ __forceinline__ int f2key(float f) {
 __device__ __forceinline__ float key2f(int k) { return __int_as_float(k ^ ((k >> 31) & 0x7fffffff)); }
 
 // Warp-cooperative form (all 32 lanes call it; returns the lane's answer).
-// Filter 0: a triangle can only count if the FP64 slab test of its leaf passes
-// (step 4), i.e. if the segment [o, o + t_max d] reaches the leaf's box (to
-// FP64 rounding).  So a triangle whose leaf box misses the union of the warp's
-// segment boxes, each widened by its margin m, counts for no lane.  Lane j
-// tests triangle k0 + j's leaf box against the union, and the per-lane filters
-// then run only over the warp's candidates -- a short list when the warp's
-// rays are coherent (Morton-sorted targets, light-sorted shading rows).
+// The warp's segments all lie in the shaft H = hull(A, B) of the box A of its
+// segment starts {o, p0} and the box B of its ends {p1}, each widened by the
+// lane's margin m: H = { (1-s) a + s b : a in A, b in B, s in [0, 1] }.  Lane j
+// decides for triangle k = k0 + j whether any lane can count it:
+//  0. leaf: k counts only if the FP64 slab test of its leaf passes (step 4),
+//     i.e. the segment [o, o + t_max d] reaches the leaf's box (to FP64
+//     rounding) -- impossible if the leaf box misses H;
+//  1. plane (warp form of filter 1): H's projection onto k's plane normal
+//     lies farther than the largest m on one side of the plane;
+//  2. crossing box (warp form of filter 2): the projections of A and B onto
+//     the normal are more than 4.5 max m apart, so every lane's segment has
+//     |s1 - s0| > 4 m, and k's box misses H (then each lane's crossing part,
+//     widened, misses it too).
+// Test "box T meets H": per axis, H's slice at s spans [lo(s), hi(s)] with
+// lo(s) = Alo + s (Blo - Alo) and hi(s) = Ahi + s (Bhi - Ahi) (linear), so
+// each of lo(s) <= Thi, hi(s) >= Tlo is a half-line in s; T meets H iff the
+// six half-lines and [0, 1] intersect (H's bounding box covers the axes where
+// A and B share a bound).  The f32 errors here are ~2^-22 of the scene scale,
+// far inside the margin m (2^-15 of it) that the per-lane filters rest on.
+// The per-lane filters then run only over the warp's candidates -- a short
+// list when the warp's rays are coherent (Morton-sorted targets, light-sorted
+// shading rows); tools/shaft_sim.py counts them (C2: ~15 of 98 per warp, the
+// leaf-box-vs-segment-union filter alone kept ~55).
+// Shaft parameters, computed once per warp call and kept in the warp's shared
+// scratch (read back as broadcasts) rather than in ~40 registers across the
+// triangle loop.
+struct Shaft {
+    float alo[3], ahi[3], blo[3], bhi[3], dl[3], dh[3], il[3], ih[3], ca[3], ea[3], cb[3], eb[3], mmax;
+};
+static_assert(sizeof(Shaft) <= kStack * sizeof(int32_t), "shaft scratch is a warp's packet-stack row");
+
+__device__ __forceinline__ bool shaft_meets(const Shaft& h, const float tlo[3], const float thi[3]) {
+    float s_lo = 0.0f, s_hi = 1.0f;
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        ok = ok && fminf(h.alo[a], h.blo[a]) <= thi[a] && fmaxf(h.ahi[a], h.bhi[a]) >= tlo[a];
+        const float tl = (thi[a] - h.alo[a]) * h.il[a];   // lo(s) <= thi: s <= tl (dl > 0), s >= tl (dl < 0)
+        const float th = (tlo[a] - h.ahi[a]) * h.ih[a];   // hi(s) >= tlo: s >= th (dh > 0), s <= th (dh < 0)
+        s_hi = fminf(s_hi, h.dl[a] > 0.0f ? tl : INFINITY);
+        s_lo = fmaxf(s_lo, h.dl[a] < 0.0f ? tl : -INFINITY);
+        s_lo = fmaxf(s_lo, h.dh[a] > 0.0f ? th : -INFINITY);
+        s_hi = fminf(s_hi, h.dh[a] < 0.0f ? th : INFINITY);
+    }
+    return ok && s_lo <= s_hi + 0x1p-16f;
+}
+
+// scratch: >= sizeof(Shaft) bytes of shared memory private to the warp
 __device__ bool any_hit_bf_warp(const nvc_scene& sc, const double o[3], const double d[3], double t_min,
-                                double t_max, bool active) {
+                                double t_max, bool active, Shaft* scratch) {
     const int lane = threadIdx.x & 31;
     const CullRay r = cull_ray(sc, o, d, t_min, t_max);
-    int klo[3], khi[3];
+    bool all = false;   // a lane with NaN bounds needs every triangle
+    {
+        Shaft h;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        const float oc = (float)o[c];
-        float lo = fminf(oc, r.b[c]) - r.m, hi = fmaxf(oc, r.b[c]) + r.m;
-        if (!(lo == lo) || !(hi == hi)) {   // NaN: this lane needs every triangle
-            lo = -INFINITY;
-            hi = INFINITY;
+        for (int c = 0; c < 3; ++c) {
+            const float oc = (float)o[c];
+            float v[4] = {fminf(oc, r.a[c]) - r.m, fmaxf(oc, r.a[c]) + r.m, r.b[c] - r.m, r.b[c] + r.m};
+            all = all || !(v[0] == v[0]) || !(v[1] == v[1]) || !(v[2] == v[2]) || !(v[3] == v[3]);
+            h.alo[c] = key2f(__reduce_min_sync(0xffffffffu, active ? f2key(v[0]) : 0x7fffffff));
+            h.ahi[c] = key2f(__reduce_max_sync(0xffffffffu, active ? f2key(v[1]) : (int)0x80000000));
+            h.blo[c] = key2f(__reduce_min_sync(0xffffffffu, active ? f2key(v[2]) : 0x7fffffff));
+            h.bhi[c] = key2f(__reduce_max_sync(0xffffffffu, active ? f2key(v[3]) : (int)0x80000000));
+            h.dl[c] = h.blo[c] - h.alo[c];
+            h.dh[c] = h.bhi[c] - h.ahi[c];
+            h.il[c] = h.dl[c] != 0.0f ? 1.0f / h.dl[c] : 0.0f;
+            h.ih[c] = h.dh[c] != 0.0f ? 1.0f / h.dh[c] : 0.0f;
+            h.ca[c] = 0.5f * (h.alo[c] + h.ahi[c]);
+            h.ea[c] = 0.5f * (h.ahi[c] - h.alo[c]);
+            h.cb[c] = 0.5f * (h.blo[c] + h.bhi[c]);
+            h.eb[c] = 0.5f * (h.bhi[c] - h.blo[c]);
         }
-        klo[c] = __reduce_min_sync(0xffffffffu, active ? f2key(lo) : 0x7fffffff);
-        khi[c] = __reduce_max_sync(0xffffffffu, active ? f2key(hi) : (int)0x80000000);
+        h.mmax = key2f(__reduce_max_sync(0xffffffffu, active ? f2key(r.m) : (int)0x80000000));
+        all = __any_sync(0xffffffffu, active && (all || !(r.m == r.m)));
+        if (lane == 0) *scratch = h;
+        __syncwarp();
     }
-    const float wl0 = key2f(klo[0]), wl1 = key2f(klo[1]), wl2 = key2f(klo[2]);
-    const float wh0 = key2f(khi[0]), wh1 = key2f(khi[1]), wh2 = key2f(khi[2]);
+    const Shaft& h = *scratch;
     bool hit = false, live = active;
     const int32_t n = (int32_t)sc.n_tris;
     for (int32_t k0 = 0; k0 < n; k0 += 32) {
         if (!__any_sync(0xffffffffu, live)) break;
         bool ov = false;
         if (k0 + lane < n) {
-            const int32_t leaf = __ldg(sc.tri_leaf + k0 + lane);
+            const int32_t k = k0 + lane;
+            const int32_t leaf = __ldg(sc.tri_leaf + k);
             const double* lo = sc.node_min + 3 * leaf;
             const double* hi = sc.node_max + 3 * leaf;
-            ov = (float)__ldg(lo) <= wh0 && (float)__ldg(hi) >= wl0 && (float)__ldg(lo + 1) <= wh1 &&
-                 (float)__ldg(hi + 1) >= wl1 && (float)__ldg(lo + 2) <= wh2 && (float)__ldg(hi + 2) >= wl2;
+            float tlo[3] = {(float)__ldg(lo), (float)__ldg(lo + 1), (float)__ldg(lo + 2)};
+            float thi[3] = {(float)__ldg(hi), (float)__ldg(hi + 1), (float)__ldg(hi + 2)};
+            const float4 q = __ldg(reinterpret_cast<const float4*>(sc.tri_plane) + k);
+            const float pa = fmaf(q.x, h.ca[0], fmaf(q.y, h.ca[1], q.z * h.ca[2]));
+            const float pb = fmaf(q.x, h.cb[0], fmaf(q.y, h.cb[1], q.z * h.cb[2]));
+            const float ra = fmaf(fabsf(q.x), h.ea[0], fmaf(fabsf(q.y), h.ea[1], fabsf(q.z) * h.ea[2]));
+            const float rb = fmaf(fabsf(q.x), h.eb[0], fmaf(fabsf(q.y), h.eb[1], fabsf(q.z) * h.eb[2]));
+            // plane: zero for slivers (then both sides are 0 - 0 and nothing is culled)
+            const bool side = fminf(pa - ra, pb - rb) - q.w > h.mmax || fmaxf(pa + ra, pb + rb) - q.w < -h.mmax;
+            const float4* bx = reinterpret_cast<const float4*>(sc.tri_box) + 2 * k;
+            const float4 blo = __ldg(bx), bhi = __ldg(bx + 1);
+            if (blo.w == 0.0f && fabsf(pb - pa) - ra - rb > 4.5f * h.mmax) {
+                tlo[0] = blo.x; tlo[1] = blo.y; tlo[2] = blo.z;   // the triangle's own box
+                thi[0] = bhi.x; thi[1] = bhi.y; thi[2] = bhi.z;
+            }
+            ov = all || (!side && shaft_meets(h, tlo, thi));
         }
         uint32_t wm = __ballot_sync(0xffffffffu, ov);
         uint32_t cand = 0u;
@@ -894,7 +963,9 @@ __device__ uint32_t any_hit_packet(const nvc_scene& sc, const double o[3], const
     uint32_t hit = 0u;
     const uint32_t act = __ballot_sync(0xffffffffu, active);
     if (sc.n_tris == 0 || act == 0u) return 0u;
-    if (sc.anyhit_bf == 2) return __ballot_sync(0xffffffffu, any_hit_bf_warp(sc, o, d, t_min, t_max, active));
+    if (sc.anyhit_bf == 2)
+        return __ballot_sync(0xffffffffu, any_hit_bf_warp(sc, o, d, t_min, t_max, active,
+                                                          reinterpret_cast<Shaft*>(st_node)));
     if (sc.anyhit_bf) return __ballot_sync(0xffffffffu, active && any_hit_bf(sc, o, d, t_min, t_max));
     const double inv[3] = {inv_dir(d[0]), inv_dir(d[1]), inv_dir(d[2])};
     int top = 0;
