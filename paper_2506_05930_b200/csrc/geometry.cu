@@ -189,7 +189,10 @@ __device__ __forceinline__ bool cull_keep(const nvc_scene& sc, const CullRay& r,
         const float4* bx = reinterpret_cast<const float4*>(sc.tri_box) + 2 * k;
         const float4 lo = __ldg(bx), hi = __ldg(bx + 1);
         if (lo.w == 0.0f) {      // the triangle has a box (w = 1: never box-culled)
-            const float rd = 1.0f / ds;
+            // approximate reciprocal (rel. error ~2^-23): |fa|, |fb| err by ~2^-22 of
+            // themselves, far inside the 2^-12 widening wherever they are not clamped
+            float rd;
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rd) : "f"(ds));
             const float fa = (-m - s0) * rd, fb = (m - s0) * rd;
             const float f_lo = fmaxf(fminf(fa, fb) - 0x1p-12f, 0.0f);
             const float f_hi = fminf(fmaxf(fa, fb) + 0x1p-12f, 1.0f);
@@ -1021,7 +1024,8 @@ __global__ void __launch_bounds__(128) k_targets(nvc_scene sc, uint64_t key, uin
     const int64_t r = (int64_t)blockIdx.x * 4 + w;
     const int lane = threadIdx.x & 31;
     const int64_t b = n_rows ? *n_rows : b_host;
-    const int64_t lo = b * shard / n_shards, hi = b * (shard + 1) / n_shards;
+    int64_t lo, hi;
+    shard_range(b, shard, n_shards, lo, hi);
     const int64_t i = lo + r;
     if (r >= cap || i >= hi) return;     // warp-uniform
     const double x[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
@@ -1078,7 +1082,8 @@ __global__ void __launch_bounds__(1024) k_morton_order(nvc_scene sc, const doubl
     __shared__ int warp_sum[32];
     extern __shared__ int slot[];   // per row: code << 16 | rank within bucket
     const int64_t b = n_rows ? *n_rows : b_host;
-    const int64_t lo = b * shard / n_shards, hi = b * (shard + 1) / n_shards;
+    int64_t lo, hi;
+    shard_range(b, shard, n_shards, lo, hi);
     const int n = (int)(hi - lo);
     for (int c = threadIdx.x; c < kBuckets; c += blockDim.x) hist[c] = 0;
     float lo3[3], inv3[3];
@@ -1138,7 +1143,8 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_targets_sorted(nvc_scene sc
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int j = blockIdx.y;
     const int64_t b = n_rows ? *n_rows : b_host;
-    const int64_t lo = b * shard / n_shards, hi = b * (shard + 1) / n_shards;
+    int64_t lo, hi;
+    shard_range(b, shard, n_shards, lo, hi);
     const int64_t t = (int64_t)blockIdx.x * 128 + threadIdx.x;
     if ((int64_t)blockIdx.x * 128 + w * 32 >= hi - lo) return;   // warp-uniform
     const bool valid = t < hi - lo;
@@ -1360,7 +1366,8 @@ __global__ void __launch_bounds__(128) k_cluster_tgt(nvc_scene sc, uint64_t key,
                                                      int32_t m, const int32_t* __restrict__ picks,
                                                      const int64_t* __restrict__ uni_start, float* __restrict__ tgt) {
     const int64_t b = *n_rows;
-    const int64_t lo = b * shard / n_shards, hi = b * (shard + 1) / n_shards;
+    int64_t lo, hi;
+    shard_range(b, shard, n_shards, lo, hi);
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y;
     if (lo + r >= hi) return;

@@ -254,7 +254,8 @@ __global__ void __launch_bounds__(kThreads) k_mlp(GridDev g, Net net, const floa
     extern __shared__ float sm[];
     const TileLayout tl = tile_layout(net);
     const int64_t b = b_dev ? *b_dev : b_max;
-    const int64_t lo = b * shard / n_shards, hi = b * (shard + 1) / n_shards;
+    int64_t lo, hi;
+    shard_range(b, shard, n_shards, lo, hi);
     const int64_t row0 = lo + (int64_t)blockIdx.x * kRows;
     const int nr = (int)max((int64_t)0, min((int64_t)kRows, hi - row0));
     const int D0 = net.dims[0];
@@ -458,7 +459,9 @@ struct ShardRows {
 };
 __device__ __forceinline__ ShardRows shard_rows(int64_t b_max, const int64_t* b_dev, int shard, int n_shards) {
     const int64_t b = b_dev ? *b_dev : b_max;
-    return {b * shard / n_shards, b * (shard + 1) / n_shards};
+    ShardRows r;
+    shard_range(b, shard, n_shards, r.lo, r.hi);
+    return r;
 }
 
 __global__ void __launch_bounds__(128) k_tr_encode(GridDev g, const float* __restrict__ params,

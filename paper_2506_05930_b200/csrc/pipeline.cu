@@ -1579,7 +1579,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_train_tc(TrainTC t, const flo
     const int q = warp & 3, h = warp >> 2;          // TMEM lane quarter, 16-column quarter
     const int r = 32 * q + lane;                   // the tile row this thread reads from TMEM
     const int64_t b = b_dev ? *b_dev : b_max;
-    const int64_t lo = b * shard / n_shards, hi = b * (shard + 1) / n_shards;
+    int64_t lo, hi;
+    shard_range(b, shard, n_shards, lo, hi);
     const int64_t r0g = (int64_t)blockIdx.x * kT;
     const int nr = (int)max((int64_t)0, min((int64_t)kT, (hi - lo) - r0g));
     const int L = t.L;

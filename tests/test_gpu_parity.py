@@ -19,7 +19,7 @@ from paper_2506_05930_b200 import (PRECISION_FP16, PRECISION_FP32, HashGridConfi
                                    TrainFrameConfig, wrs_select_batch)
 from paper_2506_05930_b200 import rng as R  # noqa: E402
 from paper_2506_05930_b200 import _lib  # noqa: E402
-from paper_2506_05930_b200.scenes import boxes_point_scene, boxes_scene  # noqa: E402
+from paper_2506_05930_b200.scenes import boxes_point_scene, boxes_scene, rooms_scene  # noqa: E402
 from paper_2506_05930_b200.training import (compute_visibility_targets, gen_screen_samples,  # noqa: E402
                                             gen_world_samples)
 
@@ -328,6 +328,33 @@ class TestShade:
                 gen_batch_device(s, s.camera.resized(1920, 1080), bufs, 0, f, 0, 0, 1)
                 outs.append(bufs.tgt.cpu().numpy().copy())
             got[mode] = np.stack(outs)
+        np.testing.assert_array_equal(got["auto"], got["bvh"])
+        np.testing.assert_array_equal(got["bf"], got["bvh"])
+        assert 0.05 < got["bvh"].mean() < 0.95
+
+    @pytest.mark.parametrize("scene_fn", [lambda: boxes_scene(32), lambda: rooms_scene(32)])
+    def test_warp_shaft_filter_grazing_rows(self, scene_fn, monkeypatch):
+        """The warp filter's shaft / plane-side / crossing-box culling against rows
+        placed ON scene triangles (and 1e-12 .. 1e-3 off them, on both sides), so many
+        of the 32 shadow rays of a row graze a plane or start inside one: targets
+        agree bitwise with per-lane culling and with the BVH traversal."""
+        from paper_2506_05930_b200.training import compute_visibility_targets
+        s0 = scene_from_dict(scene_fn())
+        g = np.random.default_rng(11)
+        tri = g.integers(0, s0.triangles_v0.shape[0], 6000)
+        u = g.random((6000, 2))
+        flip = u.sum(1) > 1.0
+        u[flip] = 1.0 - u[flip]
+        v0, v1, v2 = s0.triangles_v0[tri], s0.triangles_v1[tri], s0.triangles_v2[tri]
+        p = v0 + u[:, :1] * (v1 - v0) + u[:, 1:] * (v2 - v0)
+        nrm = np.cross(v1 - v0, v2 - v0)
+        nrm /= np.maximum(np.linalg.norm(nrm, axis=1, keepdims=True), 1e-300)
+        off = np.array([0.0, 1e-12, -1e-12, 1e-9, -1e-9, 1e-6, -1e-6, 1e-3, -1e-3, 0.0])[g.integers(0, 10, 6000)]
+        pos = np.concatenate([p + off[:, None] * nrm, g.uniform(s0.aabb_min, s0.aabb_max, (2192, 3))])
+        got = {}
+        for mode in ("auto", "bf", "bvh"):
+            s = _scene_with(scene_fn, mode, monkeypatch)
+            got[mode] = compute_visibility_targets(pos, s, R.Stream(5, 0, 0, "grazing"))
         np.testing.assert_array_equal(got["auto"], got["bvh"])
         np.testing.assert_array_equal(got["bf"], got["bvh"])
         assert 0.05 < got["bvh"].mean() < 0.95
