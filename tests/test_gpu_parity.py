@@ -503,6 +503,15 @@ class TestSampling:
         torch.cuda.current_stream().wait_event(c.select_done)
         for a, b in zip(want, got):
             assert torch.equal(a, b)
+        # back-to-back frames: the query workspaces alternate, so frame f+1's encoder
+        # and MLP run while frame f's selection may still read its workspace
+        keys = [R.stream_key(0, f, "light-select") for f in range(5)]
+        want = [[t.clone() for t in nls_sample_device(ctx, c, k)] for k in keys]
+        got = [nls_sample_device(ctx, c, k, select_stream=side) for k in keys]
+        torch.cuda.current_stream().wait_event(c.select_done)
+        for w, g in zip(want, got):
+            for a, b in zip(w, g):
+                assert torch.equal(a, b)
 
     def test_tile_sharded_nls_matches_whole_frame(self, boxes32, g_samp):
         from paper_2506_05930_b200.sampling import nls_sample_device
