@@ -796,19 +796,26 @@ __device__ __forceinline__ double dot3e(const double a[3], const double b[3]) {
 }
 __device__ __forceinline__ double max0(double x) { return 0.0 >= x ? 0.0 : x; }
 
+// One thread per pixel.  With the warp any-hit (anyhit_bf == 2) all 32 lanes
+// of a warp take part in one shaft-filtered any-hit call for their shadow rays
+// (a warp's pixels are neighbours on the screen), lanes without a ray inactive.
 __global__ void __launch_bounds__(128) k_shade(nvc_scene sc, const double* __restrict__ pos,
                                                const double* __restrict__ nrm, const double* __restrict__ alb,
                                                const int64_t* __restrict__ ids, const double* __restrict__ pts,
                                                const double* __restrict__ big_w, int64_t n,
                                                double* __restrict__ rgb) {
+    __shared__ Shaft s_shaft[4];
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int64_t id = ids[i];
-    const double W = big_w[i];
+    const bool warp_mode = sc.anyhit_bf == 2;
+    if (i >= n && !warp_mode) return;
+    const bool in = i < n;
+    const int64_t id = in ? ids[i] : -1;
+    const double W = in ? big_w[i] : 0.0;
     double out[3] = {0.0, 0.0, 0.0};
+    double x[3] = {0.0, 0.0, 0.0}, y[3] = {0.0, 0.0, 0.0}, geom = 0.0;
     if (id >= 0 && id < sc.n_lights && W > 0.0) {
-        const double x[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
-        const double y[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+        x[0] = pos[3 * i]; x[1] = pos[3 * i + 1]; x[2] = pos[3 * i + 2];
+        y[0] = pts[3 * i]; y[1] = pts[3 * i + 1]; y[2] = pts[3 * i + 2];
         const double nx[3] = {nrm[3 * i], nrm[3 * i + 1], nrm[3 * i + 2]};
         double w[3] = {y[0] - x[0], y[1] - x[1], y[2] - x[2]};
         double d2 = dot3e(w, w);
@@ -821,17 +828,37 @@ __global__ void __launch_bounds__(128) k_shade(nvc_scene sc, const double* __res
                               __ldg(sc.lt_normal + 3 * id + 2)};
         const double cos_x = max0(dot3e(nx, w));
         const double cos_y = max0(-dot3e(w, ln));
-        const double geom = __ldg(sc.lt_kind + id) == 0 ? cos_x * cos_y / d2 * __ldg(sc.lt_area + id) : cos_x / d2;
-        if (geom > 0.0) {
-            const double amp = geom * W * (double)segment_visible(sc, x, y);
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-                out[c] = alb[3 * i + c] / 3.141592653589793 * __ldg(sc.lt_radiance + 3 * id + c) * amp;
-        }
+        geom = __ldg(sc.lt_kind + id) == 0 ? cos_x * cos_y / d2 * __ldg(sc.lt_area + id) : cos_x / d2;
     }
-    rgb[3 * i] = out[0];
-    rgb[3 * i + 1] = out[1];
-    rgb[3 * i + 2] = out[2];
+    const bool need = geom > 0.0;
+    float vis = 1.0f;
+    if (warp_mode) {
+        // segment_visible's arithmetic, then one warp-wide call
+        const double eps = sc.shadow_eps;
+        const double d[3] = {y[0] - x[0], y[1] - x[1], y[2] - x[2]};
+        const double dist = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+        const double safe = fmax(dist, 1e-300);
+        const double dir[3] = {d[0] / safe, d[1] / safe, d[2] / safe};
+        double t_max = dist - eps;
+        const bool active = need && !(t_max <= eps) && sc.n_tris > 0;
+        t_max = fmax(t_max, eps + 1e-12);
+        if (__any_sync(0xffffffffu, active) &&
+            any_hit_bf_warp(sc, x, dir, eps, t_max, active, &s_shaft[threadIdx.x >> 5]) && active)
+            vis = 0.0f;
+    } else if (need) {
+        vis = segment_visible(sc, x, y);
+    }
+    if (need) {
+        const double amp = geom * W * (double)vis;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            out[c] = alb[3 * i + c] / 3.141592653589793 * __ldg(sc.lt_radiance + 3 * id + c) * amp;
+    }
+    if (in) {
+        rgb[3 * i] = out[0];
+        rgb[3 * i + 1] = out[1];
+        rgb[3 * i + 2] = out[2];
+    }
 }
 
 __global__ void k_closest(nvc_scene sc, const double* __restrict__ o, const double* __restrict__ d,

@@ -268,7 +268,7 @@ def _visibility(scene, x, y):
 
 
 class TestShade:
-    @pytest.mark.parametrize("anyhit", ["bf", "bvh"])
+    @pytest.mark.parametrize("anyhit", ["auto", "bf", "bvh"])
     def test_golden_boxes32(self, g_shade, anyhit, monkeypatch):
         from paper_2506_05930_b200.render import shade_batch
         s = _scene_with(lambda: boxes_scene(32), anyhit, monkeypatch)
@@ -294,7 +294,7 @@ class TestShade:
         with pytest.raises(ValueError):
             shade_pixel(sp, (0, g_samp["nls_pts"][i], -1.0), boxes32)
 
-    @pytest.mark.parametrize("anyhit", ["bf", "bvh"])
+    @pytest.mark.parametrize("anyhit", ["auto", "bf", "bvh"])
     def test_large_random_vs_oracle(self, g_scenes, anyhit, monkeypatch):
         """200k G-buffer rows (320x...) with random (id, point, W), ids in [-1, K]."""
         from paper_2506_05930_b200.render import gbuffer_device, shade_device
