@@ -8,7 +8,7 @@ batch's shadow rays, under
               (1-s) A + s B, s in [0, 1]: an exact box-vs-hull test),
 plus the per-lane survivors of the plane + crossing-box filters.
 Warps = 32 Morton-bucketed rows x one light, as k_targets_sorted.
-Usage: shaft_sim.py [n_frames]"""
+Usage: shaft_sim.py [n_frames] [boxes32|rooms128]"""
 import os
 import sys
 
@@ -19,9 +19,9 @@ sys.path.insert(0, ROOT)
 from oracle import vc_oracle as O  # noqa: E402
 from paper_2506_05930_b200 import scene_from_dict  # noqa: E402
 from paper_2506_05930_b200.scene import PLANE_MARGIN, shadow_accel, shadow_epsilon  # noqa: E402
-from paper_2506_05930_b200.scenes import boxes_scene  # noqa: E402
+from paper_2506_05930_b200.scenes import boxes_scene, rooms_scene  # noqa: E402
 
-s = scene_from_dict(boxes_scene(32))
+s = scene_from_dict(rooms_scene(128) if len(sys.argv) > 2 and sys.argv[2] == "rooms128" else boxes_scene(32))
 c = s.camera
 sa = O.SceneArrays(s.triangles_v0, s.triangles_v1, s.triangles_v2, s.tri_material, s.tri_light, s.lt_kind,
                    s.lt_verts, s.lt_normal, s.lt_radiance, s.mat_albedo,
