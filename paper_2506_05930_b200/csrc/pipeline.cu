@@ -1073,19 +1073,23 @@ void launch_nlsg(const WArgs& a, const nvc_scene& sc, int64_t P, cudaStream_t s)
 
 // Neural DI for K <= 32 (sampling.py:215-218): rgb = (sum_k v_k * factor_k *
 // L_e[k]) * albedo / pi over the pixel's nonzero-factor lights, FP64 in
-// ascending light order.  Memory-bound on the light-major factor table, so a
-// warp loads it as 32 x 32 tiles -- one coalesced 128-byte row per light any of
-// its pixels needs -- into shared memory (odd row stride), next to the pixel's
-// fp16 visibility row.  f32 tables only; the f64 parity tables use k_wrs_tiles.
+// ascending light order.  The light-major factor table is read one coalesced
+// 128-byte row per light any of the warp's pixels needs (each lane loads its
+// own pixel's factor only where it is nonzero), a few lights per batch held in
+// registers; the pixel's fp16 visibility row sits in shared memory (odd row
+// stride).  Staging the factor tile in shared memory instead (round 1) cost
+// 367 vs 329 us at C3 (fewer resident warps); batches of 16 lights: slower.
+// f32 tables only; the f64 parity tables use k_wrs_tiles.
 constexpr int kNdiThreads = 128;
+#ifndef NVC_NDI_BATCH
+#define NVC_NDI_BATCH 4
+#endif
 __global__ void __launch_bounds__(kNdiThreads) k_ndi32(WArgs a, nvc_scene sc) {
     __shared__ uint32_t s_vis[kNdiThreads * 17];
-    __shared__ float s_fac[kNdiThreads * 33];
     __shared__ double s_le[32 * 3];                    // emitter radiance, staged once per block
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = p < a.P;
     uint32_t* my = s_vis + threadIdx.x * 17;
-    float* mf = s_fac + threadIdx.x * 33;
     for (int i = threadIdx.x; i < 3 * a.K; i += kNdiThreads) s_le[i] = __ldg(sc.lt_radiance + i);
     uint32_t m = 0;
     double al[3] = {0.0, 0.0, 0.0};
@@ -1105,35 +1109,37 @@ __global__ void __launch_bounds__(kNdiThreads) k_ndi32(WArgs a, nvc_scene sc) {
         m = a.nz_mask ? __ldg(a.nz_mask + p) : 0xffffffffu;
         if (a.K < 32) m &= (1u << a.K) - 1u;
     }
-    // the warp's factor tile: row k for every light any lane needs, 16 loads in flight
+    __syncthreads();   // s_le
+    // the warp walks the union of its pixels' nonzero lights in ascending order,
+    // NVC_NDI_BATCH (4) at a time: each lane loads its own factor of light k (one coalesced row
+    // per light for the warp) only if k is one of its lights, then accumulates
+    // those in order -- the pixel's own ascending sum, factors kept in registers
     uint32_t wm = __reduce_or_sync(0xffffffffu, m);
     const float* fp = reinterpret_cast<const float*>(a.lum) + p;
+    double rgb[3] = {0.0, 0.0, 0.0};
     while (wm) {
-        int ks[16];
-        float t[16];
+        int ks[NVC_NDI_BATCH];
+        float t[NVC_NDI_BATCH];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            ks[j] = wm ? __ffs(wm) - 1 : -1;
+        for (int j = 0; j < NVC_NDI_BATCH; ++j) {
+            ks[j] = wm ? __ffs(wm) - 1 : 32;
             wm &= wm - 1;
         }
 #pragma unroll
-        for (int j = 0; j < 16; ++j) t[j] = (ks[j] >= 0 && live) ? __ldg(fp + (int64_t)ks[j] * a.stride) : 0.0f;
+        for (int j = 0; j < NVC_NDI_BATCH; ++j) t[j] = (ks[j] < 32 && ((m >> ks[j]) & 1u)) ? __ldg(fp + (int64_t)ks[j] * a.stride) : 0.0f;
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-            if (ks[j] >= 0) mf[ks[j]] = t[j];
+        for (int j = 0; j < NVC_NDI_BATCH; ++j) {
+            const int k = ks[j];
+            if (k < 32 && ((m >> k) & 1u)) {
+                const uint32_t pair = my[k >> 1];
+                const double vis = (double)__half2float(__ushort_as_half((unsigned short)((k & 1) ? (pair >> 16) : (pair & 0xffffu))));
+                const double wk = __dmul_rn(vis, (double)t[j]);
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) rgb[ch] = __dadd_rn(rgb[ch], __dmul_rn(wk, s_le[3 * k + ch]));
+            }
+        }
     }
-    __syncthreads();   // s_le
     if (!live) return;
-    double rgb[3] = {0.0, 0.0, 0.0};
-    while (m) {
-        const int k = __ffs(m) - 1;
-        m &= m - 1;
-        const uint32_t pair = my[k >> 1];
-        const double vis = (double)__half2float(__ushort_as_half((unsigned short)((k & 1) ? (pair >> 16) : (pair & 0xffffu))));
-        const double wk = __dmul_rn(vis, (double)mf[k]);
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) rgb[ch] = __dadd_rn(rgb[ch], __dmul_rn(wk, s_le[3 * k + ch]));
-    }
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) a.rgb[3 * p + ch] = __ddiv_rn(__dmul_rn(rgb[ch], al[ch]), 3.141592653589793);
 }

@@ -539,6 +539,27 @@ class TestSampling:
         want = ((vis16.astype(np.float64) * ctx.factor_matrix()) @ boxes32.lt_radiance) * g_samp["gb_albedo"] / np.pi
         np.testing.assert_allclose(neural_di_batch(ctx, c), want, rtol=1e-9, atol=1e-12)
 
+    def test_neural_di_f32_table_kernel(self, boxes32, g_samp):
+        """The f32-factor-table Neural DI kernel (k_ndi32: the warp walks the union of
+        its pixels' nonzero lights, factors in registers) equals the per-pixel
+        ascending-light FP64 sum op for op: sum_k (v_k f_k) L_e[k], then * albedo / pi."""
+        from paper_2506_05930_b200.render import gbuffer_device
+        pos, nrm, alb, _, _ = gbuffer_device(boxes32, boxes32.camera.resized(320, 180))
+        ctx = PixelCtx(boxes32, pos, nrm, alb, table_dtype=np.float32)
+        c = VisibilityCache(MODE_LIGHTS, 32, grid_cfg(boxes32, 16, 1 << 19), hidden_dims=(64, 64, 64))
+        c.grid_params = (np.random.default_rng(4).standard_normal(c.grid_params.shape) * 0.3).astype(np.float32)
+        got = neural_di_batch(ctx, c)
+        vis = c.infer(pos.cpu().numpy()).astype(np.float64)
+        fac = ctx.factor_matrix().astype(np.float64)
+        le = boxes32.lt_radiance
+        rgb = np.zeros((vis.shape[0], 3))
+        for k in range(vis.shape[1]):
+            wk = vis[:, k] * fac[:, k]
+            rgb = rgb + wk[:, None] * le[k][None, :]
+        want = rgb * alb.cpu().numpy() / np.pi
+        np.testing.assert_array_equal(got, want)
+        assert (got != 0).any(axis=1).mean() > 0.5
+
 
 # ---------------------------------------------------------------------------
 # training: Adam, one step, loss curve, determinism, shard equivalence
