@@ -427,19 +427,26 @@ __device__ __forceinline__ float round_bits(float x, int m) {
     return __uint_as_float(u & ~((1u << d) - 1u));
 }
 
-// with_w = false: W stays in global memory (L2/L1-resident, row stride Ki) --
-// the layout for MLPs too wide for W + activations in shared memory (C4: 3x128)
+// with_w = false: the layout for MLPs too wide for every W + the activations in
+// shared memory (C4: 3x128): one W buffer sized for the largest layer, which
+// k_train3<true> refills with the layer it is about to use (forward and the
+// backward's dL/dact); same padded row stride Ki+4
 __host__ __device__ inline T3Layout t3_layout(const Net& net, bool with_w = true) {
     T3Layout t;
     t.rbits = 0;
     t.rwhat = 7;
-    int o = 0, dmax = 0;
+    int o = 0, dmax = 0, wmax = 0;
     for (int l = 0; l < net.n_layers; ++l) {
         t.w[l] = o;
-        t.ws[l] = with_w ? net.dims[l] + 4 : net.dims[l];
+        t.ws[l] = net.dims[l] + 4;
         if (with_w) o += net.dims[l + 1] * t.ws[l];
+        else if (net.dims[l + 1] * t.ws[l] > wmax) wmax = net.dims[l + 1] * t.ws[l];
         t.bias[l] = o;
         o += (net.dims[l + 1] + 3) / 4 * 4;
+    }
+    if (!with_w) {   // the shared W buffer
+        for (int l = 0; l < net.n_layers; ++l) t.w[l] = o;
+        o += wmax;
     }
     for (int l = 0; l <= net.n_layers; ++l) {
         t.act[l] = o;
@@ -498,19 +505,23 @@ __global__ void __launch_bounds__(kThreads, 4) k_train3(Net net, T3Layout tl, co
     const int K = net.dims[net.n_layers];
 
     // ---- W (padded rows), biases, act0 -> smem; all loads issued as float4 ----
-    for (int l = 0; l < net.n_layers; ++l) {
+    // (kWG: only the biases here; each layer's W is staged right before its use)
+    auto stage_w = [&](int l) {
         const int N = net.dims[l + 1], Ki = net.dims[l], kq = Ki / 4;
         const float4* W = reinterpret_cast<const float4*>(params + net.woff[l]);
         float* dst = sm + tl.w[l];
 #pragma unroll 4
-        for (int e = tid; e < (kWG ? 0 : N * kq); e += kThreads) {
+        for (int e = tid; e < N * kq; e += kThreads) {
             float4 w = __ldg(W + e);
             if (tl.rbits && (tl.rwhat & 1)) w = make_float4(round_bits(w.x, tl.rbits), round_bits(w.y, tl.rbits),
                                           round_bits(w.z, tl.rbits), round_bits(w.w, tl.rbits));
             const int n = e / kq, k = (e - n * kq) * 4;
             *reinterpret_cast<float4*>(dst + n * tl.ws[l] + k) = w;
         }
-        for (int n = tid; n < N; n += kThreads) sm[tl.bias[l] + n] = __ldg(params + net.boff[l] + n);
+    };
+    for (int l = 0; l < net.n_layers; ++l) {
+        if (!kWG) stage_w(l);
+        for (int n = tid; n < net.dims[l + 1]; n += kThreads) sm[tl.bias[l] + n] = __ldg(params + net.boff[l] + n);
     }
     {
         const int q0 = D0 / 4;
@@ -529,7 +540,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_train3(Net net, T3Layout tl, co
     for (int l = 0; l < net.n_layers; ++l) {
         const int Ki = net.dims[l], N = net.dims[l + 1], ng = N / 4, S = tl.ws[l];
         const float* A = sm + tl.act[l];
-        const float* W = kWG ? params + net.woff[l] : sm + tl.w[l];
+        if (kWG) {
+            if (l > 0) __syncthreads();   // (l = 0: the barrier after the act0 load follows)
+            stage_w(l);
+            __syncthreads();
+        }
+        const float* W = sm + tl.w[l];
         float* out = sm + tl.act[l + 1];
         const bool last = l == net.n_layers - 1;
         for (int t = tid; t < (kRows / kRPT) * ng; t += kThreads) {
@@ -633,7 +649,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_train3(Net net, T3Layout tl, co
             gb[n] = acc;
         }
         // grad act[r][k] = sum_n dz[r][n] W[n][k], through leaky'(z_{l-1}) (2x4 tiles)
-        const float* W = kWG ? params + net.woff[l] : sm + tl.w[l];
+        if (kWG && l != net.n_layers - 1) {   // (the last layer's W is still staged from the forward pass)
+            __syncthreads();   // the previous layer's dL/dact pass is done with the W buffer
+            stage_w(l);
+            __syncthreads();
+        }
+        const float* W = sm + tl.w[l];
         for (int t = tid; t < (kRows / kRPT) * kg; t += kThreads) {
             const int r0 = (t / kg) * kRPT, k0 = (t % kg) * 4;
             float acc[kRPT][4] = {};
