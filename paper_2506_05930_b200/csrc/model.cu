@@ -1452,7 +1452,7 @@ int nvc_train_grads(const nvc_model* m, const double* pos, const float* tgt, con
     cudaStream_t s = (cudaStream_t)stream;
     bool split = g.F <= 8 && getenv("NVC_TRAIN_FUSED") == nullptr;
     for (int i = 0; i <= net.n_layers; ++i) split = split && (net.dims[i] % 4 == 0);
-    const bool wg = t3_layout(net).total * 4 + 64 > 200 * 1024;   // too wide for W in smem (C4): W from L1/L2
+    const bool wg = t3_layout(net).total * 4 + 64 > 200 * 1024;   // too wide for every W in smem (C4): W staged per layer
     T3Layout tl3 = t3_layout(net, !wg);
     tl3.rbits = getenv("NVC_T3_BITS") ? atoi(getenv("NVC_T3_BITS")) : 0;
     if (getenv("NVC_T3_WHAT")) tl3.rwhat = atoi(getenv("NVC_T3_WHAT"));
