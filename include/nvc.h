@@ -28,7 +28,7 @@ extern "C" {
 
 #define NVC_MAX_LEVELS 32
 #define NVC_MAX_LAYERS 8
-#define NVC_ABI_VERSION 10
+#define NVC_ABI_VERSION 11
 
 typedef enum {
     NVC_OK = 0,
@@ -353,6 +353,20 @@ int nvc_clustered_select(const nvc_scene *sc, const float *vis, int64_t vis_stri
                          const double *nrm, const double *alb, const double *factor, int64_t p, int32_t m,
                          const int32_t *c_off, const int32_t *c_mem, uint64_t key, uint64_t offset, double floor,
                          int64_t *ids, double *pts, double *big_w, void *ws, void *stream);
+/* The clustered selection with the factors read from a cluster-ordered
+ * pixel-major table: nvc_cluster_factor_table writes out (p, k) f64 with
+ * out[q*k + i] = factor[c_mem[i]*p + q] (factor: the light-major (K, p) table
+ * of nvc_light_factors, k = c_off[m] members), so a pixel's candidate members
+ * are one contiguous run; nvc_clustered_select_ct then takes that table
+ * (ct_stride = k) in place of the light-major one.  Identical results to
+ * nvc_clustered_select with the light-major table. */
+int nvc_cluster_factor_table(const double *factor, int64_t p, int32_t k, const int32_t *c_mem, double *out,
+                             void *stream);
+int nvc_clustered_select_ct(const nvc_scene *sc, const float *vis, int64_t vis_stride, const double *pos,
+                            const double *nrm, const double *alb, const double *factor_ct, int64_t ct_stride,
+                            int64_t p, int32_t m, const int32_t *c_off, const int32_t *c_mem, uint64_t key,
+                            uint64_t offset, double floor, int64_t *ids, double *pts, double *big_w, void *ws,
+                            void *stream);
 /* shade_batch (render.py:220-246): one-shadow-ray estimate per row,
  * rgb (n,3) f64 = albedo/pi * L_e[id] * G * V * (area) * W; rows with id < 0,
  * id >= K or W <= 0 (and rows with G <= 0) are 0.  Bit-identical to the

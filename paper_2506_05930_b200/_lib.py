@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libnvc.so")
 
 MAX_LEVELS = 32
 MAX_LAYERS = 8
-ABI_VERSION = 10
+ABI_VERSION = 11
 
 c_i32, c_i64, c_u64, c_f64, c_f32, c_vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
                                            ctypes.c_double, ctypes.c_float, ctypes.c_void_p)
@@ -116,6 +116,9 @@ _SIGS = {
     "nvc_clustered_state_offset": (c_i64, [c_i64, c_i32]),
     "nvc_clustered_select": (c_i32, [P(NvcScene), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp,
                                      c_u64, c_u64, c_f64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "nvc_cluster_factor_table": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    "nvc_clustered_select_ct": (c_i32, [P(NvcScene), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_vp,
+                                        c_vp, c_u64, c_u64, c_f64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "nvc_shade": (c_i32, [P(NvcScene), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "nvc_ris_workspace_bytes": (c_i64, [c_i64, c_i32, c_i32]),
     "nvc_ris_initial": (c_i32, [P(NvcScene), c_vp, c_i32, c_i64, c_i64, c_i32, c_u64, c_u64, c_i64,

@@ -712,6 +712,10 @@ __device__ __forceinline__ double dot3_blas(const double a[3], const double b[3]
 // inlined form kept in a loop-carried local produced wrong draws (see DESIGN).
 __device__ __noinline__ U4 philox_call(uint64_t counter, uint64_t key) { return philox_block(counter, key); }
 
+// kCT: ftab is the cluster-ordered pixel-major table of nvc_cluster_factor_table
+// (row p holds the pixel's factors in c_mem order, so a pixel's members are one
+// contiguous run); otherwise the light-major (K, p) table or NULL
+template <bool kCT>
 __global__ void __launch_bounds__(kCsThreads) k_cs_step2(nvc_scene sc, const double* __restrict__ pos,
                                                         const double* __restrict__ nrm, const double* __restrict__ alb,
                                                         int64_t P, int m, const int32_t* __restrict__ c_off,
@@ -739,7 +743,8 @@ __global__ void __launch_bounds__(kCsThreads) k_cs_step2(nvc_scene sc, const dou
         U4 u;
         for (int k = 0; k < my; ++k) {
             const int l = c_mem[lo + k];
-            const double f = ftab ? __ldg(ftab + (int64_t)l * fstride + p)
+            const double f = kCT   ? __ldg(ftab + p * fstride + (lo + k))
+                           : ftab ? __ldg(ftab + (int64_t)l * fstride + p)
                                   : (sc.lt_kind[l] == 0 ? rect_factor(x, nx, sc.lt_verts + 12 * l, sc.lt_normal + 3 * l)
                                                         : point_factor(x, nx, sc.lt_verts + 12 * l));
             const double lw[3] = {0.2126 * sc.lt_radiance[3 * l], 0.7152 * sc.lt_radiance[3 * l + 1],
@@ -1649,9 +1654,58 @@ int nvc_clustered_select(const nvc_scene* sc, const float* vis, int64_t vis_stri
     k_cs_rank<<<nblk, kCsThreads, (size_t)m * 4, s>>>(p, m, w);
     k_cs_scan<<<m, 1024, 0, s>>>(nblk, m, w);
     k_cs_bases<<<1, 1, 0, s>>>(m, c_off, p, offset, w);
-    k_cs_step2<<<nblk, kCsThreads, 0, s>>>(*sc, pos, nrm, alb, p, m, c_off, c_mem, key, w, factor, p, ids, pts,
-                                           big_w);
+    k_cs_step2<false><<<nblk, kCsThreads, 0, s>>>(*sc, pos, nrm, alb, p, m, c_off, c_mem, key, w, factor, p, ids,
+                                                  pts, big_w);
     return check_launch("nvc_clustered_select");
+}
+
+// (K, p) light-major -> (p, K) pixel-major with the columns in c_mem order:
+// 32 x 32 tiles through shared memory, both sides coalesced
+__global__ void __launch_bounds__(256) k_cluster_ftab(const double* __restrict__ f, int64_t p, int32_t k,
+                                                      const int32_t* __restrict__ c_mem, double* __restrict__ out) {
+    __shared__ double t[32][33];
+    const int64_t p0 = (int64_t)blockIdx.x * 32;
+    const int i0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += 8) {   // r: member column i0 + r
+        const int i = i0 + r;
+        const int64_t q = p0 + threadIdx.x;
+        t[r][threadIdx.x] = (i < k && q < p) ? __ldg(f + (int64_t)__ldg(c_mem + i) * p + q) : 0.0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += 8) {   // r: pixel p0 + r
+        const int64_t q = p0 + r;
+        const int i = i0 + threadIdx.x;
+        if (q < p && i < k) out[q * k + i] = t[threadIdx.x][r];
+    }
+}
+
+int nvc_cluster_factor_table(const double* factor, int64_t p, int32_t k, const int32_t* c_mem, double* out,
+                             void* stream) {
+    NVC_REQUIRE(factor && c_mem && out && k >= 1, "nvc_cluster_factor_table: bad argument");
+    if (p <= 0) return NVC_OK;
+    const dim3 grid((unsigned)((p + 31) / 32), (unsigned)((k + 31) / 32));
+    k_cluster_ftab<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(factor, p, k, c_mem, out);
+    return check_launch("k_cluster_ftab");
+}
+
+int nvc_clustered_select_ct(const nvc_scene* sc, const float* vis, int64_t vis_stride, const double* pos,
+                            const double* nrm, const double* alb, const double* factor_ct, int64_t ct_stride,
+                            int64_t p, int32_t m, const int32_t* c_off, const int32_t* c_mem, uint64_t key, uint64_t offset, double floor,
+                            int64_t* ids, double* pts, double* big_w, void* ws, void* stream) {
+    NVC_REQUIRE(sc && vis && pos && nrm && alb && factor_ct && c_off && c_mem && ids && pts && big_w && ws,
+                "nvc_clustered_select_ct: null argument");
+    NVC_REQUIRE(m >= 1 && vis_stride >= m && ct_stride >= 1, "nvc_clustered_select_ct: bad m / stride");
+    if (p <= 0) return NVC_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const CsWs w = cs_ws(ws, p, m);
+    const int nblk = grid1(p, kCsThreads);
+    k_cs_step1<<<nblk, kCsThreads, 0, s>>>(vis, vis_stride, p, m, key, offset, floor, w);
+    k_cs_rank<<<nblk, kCsThreads, (size_t)m * 4, s>>>(p, m, w);
+    k_cs_scan<<<m, 1024, 0, s>>>(nblk, m, w);
+    k_cs_bases<<<1, 1, 0, s>>>(m, c_off, p, offset, w);
+    k_cs_step2<true><<<nblk, kCsThreads, 0, s>>>(*sc, pos, nrm, alb, p, m, c_off, c_mem, key, w, factor_ct,
+                                                 ct_stride, ids, pts, big_w);
+    return check_launch("nvc_clustered_select_ct");
 }
 
 int64_t nvc_clustered_state_offset(int64_t p, int32_t m) {   // int64: first light-point draw

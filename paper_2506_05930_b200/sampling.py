@@ -13,6 +13,7 @@ and screen-tile shards (``p_first``/``p_total``) reproduce the whole frame.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -397,6 +398,27 @@ def neural_di_shade(sp: ShadingPoint, cache, scene) -> np.ndarray:
 # clustered NVC: two-step sampling (sampling.py:302-359)
 # ---------------------------------------------------------------------------
 
+CLUSTER_TABLE_MAX_BYTES = 32 << 30   # the cluster-ordered copy doubles the factor table's footprint
+
+
+def _cluster_factor_table(ctx, fac, clusters, c_mem):
+    """(p, members) f64 copy of the light-major factor table, columns in the
+    ClusterSet's member order (nvc_cluster_factor_table); cached on the context
+    per ClusterSet.  None when it would not fit CLUSTER_TABLE_MAX_BYTES."""
+    import torch
+    n = int(c_mem.numel())
+    if os.environ.get("NVC_CLUSTER_LIGHT_MAJOR") or ctx.n * n * 8 > CLUSTER_TABLE_MAX_BYTES:
+        return None
+    cached = ctx.__dict__.setdefault("_nvc_cluster_ct", {})
+    key = id(clusters)
+    if key not in cached or cached[key][0] is not clusters:
+        out = torch.empty((ctx.n, n), dtype=torch.float64, device=ctx.device)
+        _lib.call("nvc_cluster_factor_table", fac.data_ptr(), ctx.n, n, c_mem.data_ptr(), out.data_ptr(),
+                  _lib.stream_ptr())
+        cached[key] = (clusters, out)
+    return cached[key][1]
+
+
 def clustered_sample_device(ctx: PixelCtx, cache, clusters, key: int, offset: int = 0,
                             clamp_floor=CLAMP_FLOOR):
     """Device tensors (ids, pts, W) and the number of draws consumed."""
@@ -421,9 +443,20 @@ def clustered_sample_device(ctx: PixelCtx, cache, clusters, key: int, offset: in
     k = ctx.dscene.n_lights
     use_table = ctx.table_dtype == np.float64 and (ctx._factor is not None or p * k <= FACTOR_CACHE_LIMIT)
     fac = ctx.factor_device() if use_table else None
-    _lib.call("nvc_clustered_select", ctx.dscene.struct, vis.data_ptr(), vis.shape[1], ctx.pos.data_ptr(),
-              ctx.nrm.data_ptr(), ctx.alb.data_ptr(), _lib.ptr(fac), p, m, c_off.data_ptr(), c_mem.data_ptr(), key,
-              offset, floor, ids.data_ptr(), pts.data_ptr(), big_w.data_ptr(), ws.data_ptr(), _lib.stream_ptr())
+    # with a table: read it as the cluster-ordered pixel-major copy (a pixel's
+    # candidate members contiguous; built once per (camera, ClusterSet)) -- the
+    # light-major rows are gathered 8 B per (pixel, member) from scattered rows
+    ct = _cluster_factor_table(ctx, fac, clusters, c_mem) if use_table else None
+    if ct is not None:
+        _lib.call("nvc_clustered_select_ct", ctx.dscene.struct, vis.data_ptr(), vis.shape[1], ctx.pos.data_ptr(),
+                  ctx.nrm.data_ptr(), ctx.alb.data_ptr(), ct.data_ptr(), ct.shape[1], p, m, c_off.data_ptr(),
+                  c_mem.data_ptr(), key, offset, floor, ids.data_ptr(), pts.data_ptr(), big_w.data_ptr(),
+                  ws.data_ptr(), _lib.stream_ptr())
+    else:
+        _lib.call("nvc_clustered_select", ctx.dscene.struct, vis.data_ptr(), vis.shape[1], ctx.pos.data_ptr(),
+                  ctx.nrm.data_ptr(), ctx.alb.data_ptr(), _lib.ptr(fac), p, m, c_off.data_ptr(), c_mem.data_ptr(),
+                  key, offset, floor, ids.data_ptr(), pts.data_ptr(), big_w.data_ptr(), ws.data_ptr(),
+                  _lib.stream_ptr())
     lp = ws.view(torch.int64)[lib.nvc_clustered_state_offset(p, m) // 8]
     return ids, pts, big_w, lp + 2 * p - offset
 

@@ -1046,12 +1046,16 @@ class TestClusteredSampling:
         want = ctx.n * cs.m + int(sum(n_j[j] * cs.members[j].size for j in range(cs.m))) + 2 * ctx.n
         assert R.position(g)[1] == want
 
-    @pytest.mark.parametrize("table", [np.float32, np.float64])
-    def test_native_cluster_cache_vs_oracle(self, rooms, g_scenes, table):
-        """Per-(pixel, member) factors computed in the kernel (f32 table context) or read
-        from the per-camera f64 factor table: same results."""
+    @pytest.mark.parametrize("table", ["f32", "f64", "f64_light_major"])
+    def test_native_cluster_cache_vs_oracle(self, rooms, g_scenes, table, monkeypatch):
+        """Per-(pixel, member) factors computed in the kernel (f32 table context), read
+        from the cluster-ordered pixel-major copy of the per-camera f64 factor table
+        (default), or read from the light-major table itself: same results."""
         from paper_2506_05930_b200 import clustered_sample_batch, make_cache
         from paper_2506_05930_b200.render import gbuffer_device
+        if table == "f64_light_major":
+            monkeypatch.setenv("NVC_CLUSTER_LIGHT_MAJOR", "1")
+        table = np.float32 if table == "f32" else np.float64
         s, cs = rooms
         pos, nrm, alb, _, _ = gbuffer_device(s, s.camera.resized(80, 45))
         ctx = PixelCtx(s, pos, nrm, alb, table_dtype=table)
