@@ -215,6 +215,69 @@ __global__ void __launch_bounds__(kT, 6) k_enc_tiles(GridDev g, const uint16_t* 
     }
 }
 
+// F == 4 (the reference's default grid, e.g. the clustered preset L=8,
+// T=2^14): one x-pair slot is 8 halves = one 16-byte load per (level, y/z
+// corner), levels unrolled, two levels per 16-byte tile store.  The blend is
+// the generic path's arithmetic exactly (f32 weights, the same fmaf order per
+// feature, one fp16 rounding at the store), so the tiles are bit-identical to
+// k_enc_tiles<false> -- which issues 2-byte loads, 8 per (level, corner).
+template <int L>
+__global__ void __launch_bounds__(kT, 6) k_enc_tiles4(GridDev g, const uint16_t* __restrict__ table2,
+                                                      const double* __restrict__ pos, int64_t P, int kp0,
+                                                      uint8_t* __restrict__ tiles) {
+    static_assert(L % 2 == 0, "two levels per 16-byte store");
+    const int row = threadIdx.x;
+    const int64_t tile = blockIdx.x;
+    const int64_t p = tile * kT + row;
+    uint8_t* img = tiles + tile * (int64_t)(kT * kp0 * 2);
+    if (p >= P) {
+        for (int k = 0; k < kp0; k += 8) *reinterpret_cast<uint4*>(img + umma_off(row, k, kT, kp0)) = make_uint4(0, 0, 0, 0);
+        return;
+    }
+    const double pp[3] = {__ldg(pos + 3 * p), __ldg(pos + 3 * p + 1), __ldg(pos + 3 * p + 2)};
+    double q[3];
+    normalize(g, pp, q);
+    const uint4* t4 = reinterpret_cast<const uint4*>(table2);
+#pragma unroll
+    for (int l0 = 0; l0 < L; l0 += 2) {
+        uint4 v[2][4];
+        float w[2][3];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int l = l0 + j;
+            uint32_t c0[3];
+            cell3(g.res[l], q, c0, w[j]);
+            const bool dense = g.dense[l] != 0;
+            const uint32_t sy = dense ? (uint32_t)g.res[l] + 1u : 2654435761u;
+            const uint32_t sz = dense ? sy * sy : 805459861u;
+            const uint32_t mask = dense ? 0xffffffffu : g.tmask;
+            const uint32_t base = c0[0] + c0[1] * sy + c0[2] * sz;
+            const uint4* tl = t4 + (size_t)l * (size_t)g.T;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[j][c] = __ldg(tl + ((base + ((c >> 1) & 1) * sy + (c & 1) * sz) & mask));
+        }
+        __align__(16) __half out[8];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const float f0 = w[j][0], wy[2] = {1.0f - w[j][1], w[j][1]}, wz[2] = {1.0f - w[j][2], w[j][2]};
+            float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float wyz = wy[(c >> 1) & 1] * wz[c & 1];
+                const __half* h = reinterpret_cast<const __half*>(&v[j][c]);   // x0 features 0-3 | x1 features 0-3
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    acc[k] = fmaf(f0 * wyz, __half2float(h[4 + k]), fmaf((1.0f - f0) * wyz, __half2float(h[k]), acc[k]));
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) out[4 * j + k] = __float2half_rn(acc[k]);
+        }
+        *reinterpret_cast<uint4*>(img + umma_off(row, 4 * l0, kT, kp0)) = *reinterpret_cast<const uint4*>(out);
+    }
+    for (int k = 4 * L; k < kp0; k += 8)
+        *reinterpret_cast<uint4*>(img + umma_off(row, k, kT, kp0)) = make_uint4(0, 0, 0, 0);
+}
+
 // Mixed-precision FMA (sm_100: fma.rn.f32.f16 -> SASS FHFMA): f16 x f16 + f32.
 // The half operands are selected from packed half2 registers (lo / hi).
 __device__ __forceinline__ uint32_t h2bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
@@ -1353,6 +1416,10 @@ int run_front(const nvc_model* m, const double* pos, int64_t P, uint8_t* tiles, 
     }
     else if (g.F == 2 && g.L == 8 && h2)
         k_enc_tiles2<8, 10><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
+    else if (g.F == 4 && g.L == 8 && h2 && !getenv("NVC_ENC_GENERIC"))
+        k_enc_tiles4<8><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
+    else if (g.F == 4 && g.L == 16 && h2 && !getenv("NVC_ENC_GENERIC"))
+        k_enc_tiles4<16><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
     else if (g.F == 2)
         k_enc_tiles<true><<<(int)ntiles, kT, 0, s>>>(g, m->table_h, pos, P, q.kp[0], tiles);
     else

@@ -125,6 +125,25 @@ def test_c4_mlp_takes_the_tcgen05_path(boxes32, variant, monkeypatch):
     assert np.abs(out.cpu().numpy() - oc.infer(pos)).max() < FP16_VIS_TOL
 
 
+@pytest.mark.parametrize("levels,tsize,hidden", [(8, 1 << 14, (32, 32)), (16, 1 << 19, (64, 64, 64))])
+def test_f4_encoder_equals_generic(boxes32, levels, tsize, hidden, monkeypatch):
+    """F = 4 grids (the reference's default features_per_level; the clustered
+    preset is L=8, T=2^14): the 16-byte-gather encoder k_enc_tiles4 gives the
+    same fp16 query outputs, bit for bit, as the generic per-half encoder, on
+    N(0, 0.3) tables; and both stay within the fp16 tolerance of the oracle."""
+    cfg = HashGridConfig(levels=levels, table_size=tsize, features_per_level=4, aabb_min=boxes32.aabb_min,
+                         aabb_max=boxes32.aabb_max)
+    c = VisibilityCache(MODE_LIGHTS, 32, cfg, seed=2, hidden_dims=hidden)
+    c.grid_params = (np.random.default_rng(6).standard_normal(c.grid_params.shape) * 0.3).astype(np.float32)
+    pos = np.random.default_rng(7).uniform(boxes32.aabb_min, boxes32.aabb_max, (50003, 3))
+    fast = c.infer(pos, precision=PRECISION_FP16)
+    monkeypatch.setenv("NVC_ENC_GENERIC", "1")
+    generic = c.infer(pos, precision=PRECISION_FP16)
+    np.testing.assert_array_equal(fast, generic)
+    ref = c.infer(pos, precision=PRECISION_FP32)
+    assert np.abs(fast.astype(np.float64) - ref).max() < 2e-2
+
+
 def test_infer_trained_weights_fp16(boxes32):
     """fp16 tolerance also holds away from init (trained-scale weights)."""
     cfg = grid_cfg(boxes32, 16, 1 << 19)
