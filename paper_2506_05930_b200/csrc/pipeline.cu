@@ -1141,7 +1141,8 @@ void launch_nlsg(const WArgs& a, const nvc_scene& sc, int64_t P, cudaStream_t s)
 // own pixel's factor only where it is nonzero), a few lights per batch held in
 // registers; the pixel's fp16 visibility row sits in shared memory (odd row
 // stride).  Staging the factor tile in shared memory instead (round 1) cost
-// 367 vs 329 us at C3 (fewer resident warps); batches of 16 lights: slower.
+// 367 vs 329 us at C3 (fewer resident warps); batches of 16 lights: slower;
+// 2 lights, or 64 / 256 threads per block: within noise.
 // f32 tables only; the f64 parity tables use k_wrs_tiles.
 constexpr int kNdiThreads = 128;
 #ifndef NVC_NDI_BATCH
